@@ -1,0 +1,260 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Runs only in the build container (needs /root/reference).  Output:
+``tests/golden/*.npz`` (committed).  The harness extensions SURVEY §0 asks for
+are applied from the outside, without editing the reference:
+
+* closed trimming curves (F3/F5) -- the oracle's harness curve classes wrapped
+  as reference ``TrimmingCurve`` subclasses (the curves are harness
+  definitions; every algorithm applied to them is the reference's);
+* seam routing (F3) -- ``trimming._curve_for_element`` replaced by a router
+  that hands seam-containing cells a seam-shifted copy of the curve;
+* q<=6 cap lift (F4) -- ``cut_cell_quadrature`` re-bound without the cap,
+  otherwise calling the reference's ``decompose_cut_element``.
+
+Usage:  python tests/golden/make_golden.py [--big]
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+import scipy.sparse as sp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import trimquad  # noqa: E402
+from trimquad import assembly as RA  # noqa: E402
+from trimquad import cases as RC  # noqa: E402
+from trimquad import projection as RP  # noqa: E402
+from trimquad import quadrature as RQ  # noqa: E402
+from trimquad import splines as RS  # noqa: E402
+from trimquad import trimming as RT  # noqa: E402
+
+from oracle import configs as OC  # noqa: E402  (harness curve definitions only)
+
+
+class HarnessCurve(RT.TrimmingCurve):
+    """Adapter: a harness (closed) curve seen through the reference interface."""
+
+    straight = False
+
+    def __init__(self, inner):
+        self.inner = inner
+
+    def evaluate(self, t):
+        return self.inner.evaluate(t)
+
+    def derivative(self, t):
+        return self.inner.derivative(t)
+
+    def is_inside(self, points):
+        return self.inner.is_inside(points)
+
+    def signed_distance(self, points):
+        return self.inner.signed_distance(points)
+
+    def intersect_line(self, axis, level):
+        return self.inner.intersect_line(axis, level)
+
+    def shifted(self):
+        return HarnessCurve(self.inner.shifted())
+
+
+_orig_curve_for_element = RT._curve_for_element
+
+
+def _routed_curve_for_element(config, bounds):
+    cv = _orig_curve_for_element(config, bounds)
+    if isinstance(cv, HarnessCurve):
+        x0, x1, y0, y1 = bounds
+        s = np.asarray(cv.evaluate(0.0), float).reshape(2)
+        tol = RT.SNAP_REL_TOL * max(x1 - x0, y1 - y0)
+        if x0 - tol <= s[0] <= x1 + tol and y0 - tol <= s[1] <= y1 + tol:
+            return cv.shifted()
+    return cv
+
+
+def _uncapped_cut_cell_quadrature(config, q):
+    rules, counts = {}, {}
+    for (e1, e2) in config.cut_elements:
+        bounds = config.element_bounds(e1, e2)
+        cells = RT.decompose_cut_element(bounds, RT._curve_for_element(config, bounds), q)
+        if cells:
+            pts = np.vstack([c.points for c in cells])
+            wts = np.concatenate([c.weights for c in cells])
+        else:
+            pts, wts = np.empty((0, 2)), np.empty(0)
+        rules[(e1, e2)] = (pts, wts)
+        counts[(e1, e2)] = len(cells)
+    return RT.CutCellQuadrature(q, rules, counts)
+
+
+RT._curve_for_element = _routed_curve_for_element
+RT.cut_cell_quadrature = _uncapped_cut_cell_quadrature
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def space(nel, p, curves):
+    b = RS.make_uniform_basis(nel, p)
+    b2d = RS.TensorBasis2D(b, RS.make_uniform_basis(nel, p))
+    return b2d, RT.classify_elements(b2d, curves)
+
+
+def pack_rules(rules):
+    k0 = np.full(len(rules.rows), -1, np.int64)
+    lens = np.zeros(len(rules.rows), np.int64)
+    ws = []
+    for i, r in enumerate(rules.rows):
+        if r is None:
+            continue
+        k0[i], lens[i] = r[0], r[1].size
+        ws.append(r[1])
+    return k0, np.concatenate([[0], np.cumsum(lens)]), (np.concatenate(ws) if ws else np.empty(0))
+
+
+def cut_rule_arrays(cfg, q):
+    rule = cfg.cut_cell_rule(q)
+    keys = sorted(rule.rules)
+    el = np.array(keys, np.int64).reshape(-1, 2)
+    cnt = np.array([rule.rules[k][0].shape[0] for k in keys], np.int64)
+    ptr = np.concatenate([[0], np.cumsum(cnt)])
+    P = np.vstack([rule.rules[k][0] for k in keys]) if keys else np.empty((0, 2))
+    W = np.concatenate([rule.rules[k][1] for k in keys]) if keys else np.empty(0)
+    return el, ptr, P, W
+
+
+def dump_case(out, tag, b2d, cfg, strategies, target, coeff=None, full=True, project=True, rows_sample=64):
+    d = {}
+    d["element_class"] = cfg.element_class
+    d["func_class"] = cfg.func_class
+    d["u_disc1"], d["u_disc2"] = cfg.u_disc
+    d["active"] = cfg.active_functions()
+    q = max(b2d.degrees)
+    el, ptr, P, W = cut_rule_arrays(cfg, q)
+    d["cut_el"], d["cut_ptr"], d["cut_pts"], d["cut_w"] = el, ptr, P, W
+    cf = RA.CoefficientField(coeff) if coeff is not None else None
+    mats = {}
+    for s in strategies:
+        t0 = time.perf_counter()
+        M = RA.assemble_mass(b2d, cfg, cf, strategy=s).data
+        mats[s] = M
+        d[f"{s}_hash"] = sha(M.indptr, M.indices)
+        d[f"{s}_nnz"] = M.nnz
+        d[f"{s}_fro"] = float(sp.linalg.norm(M))
+        if full:
+            d[f"{s}_indptr"], d[f"{s}_indices"], d[f"{s}_data"] = M.indptr, M.indices, M.data
+        else:
+            rng = np.random.default_rng(0)
+            rows = np.unique(rng.integers(0, M.shape[0], rows_sample))
+            d[f"{s}_rows"] = rows
+            d[f"{s}_rowsdata"] = np.concatenate([M.data[M.indptr[r]:M.indptr[r + 1]] for r in rows])
+            d[f"{s}_rowsptr"] = np.concatenate([[0], np.cumsum([M.indptr[r + 1] - M.indptr[r] for r in rows])])
+        print(f"  {tag} {s}: nnz={M.nnz} ({time.perf_counter() - t0:.1f}s)", flush=True)
+    if target is not None:
+        prob = RP.ProjectionProblem(target, b2d, cfg, strategy=strategies[-1], coeff=cf)
+        b = RP.assemble_rhs(prob)
+        d["rhs"] = b
+        if project:
+            x = RP.solve_spd(mats[strategies[-1]], b)
+            d["x"] = x
+            d["l2"] = RP.l2_error(x, prob)
+    np.savez_compressed(os.path.join(HERE, f"{tag}.npz"), **d)
+    return mats
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="also configs 3/4 (minutes)")
+    args = ap.parse_args()
+    t_all = time.perf_counter()
+
+    # 1. 1-D weighted-quadrature rules and DWQ rules (weights pinned bit-exact)
+    d = {}
+    for nel, p in ((9, 1), (9, 2), (9, 3), (7, 4), (8, 5), (10, 6), (16, 2), (64, 3), (12, 8)):
+        b = RS.make_uniform_basis(nel, p)
+        r = RQ.compute_wq_rules(b)
+        k0, ptr, w = pack_rules(r)
+        d[f"wq_{nel}_{p}_k0"], d[f"wq_{nel}_{p}_ptr"], d[f"wq_{nel}_{p}_w"] = k0, ptr, w
+        d[f"wq_{nel}_{p}_pts"] = r.layout.points
+        d[f"wq_{nel}_{p}_M"] = RQ.mass_matrix_1d(b)
+        ub = float(b.breakpoints[nel // 2])
+        dq = RQ.build_dwq(b, r.layout, ub)
+        k0, ptr, w = pack_rules(dq)
+        d[f"dwq_{nel}_{p}_k0"], d[f"dwq_{nel}_{p}_ptr"], d[f"dwq_{nel}_{p}_w"] = k0, ptr, w
+        d[f"dwq_{nel}_{p}_pts"] = dq.layout.points
+        d[f"dwq_{nel}_{p}_u"] = ub
+    # non-uniform knots with multiplicities
+    kv = RS.KnotVector([0, 0, 0, 0.1, 0.25, 0.25, 0.5, 0.5, 0.5, 0.8, 1, 1, 1], 2)
+    b = RS.Basis1D(kv)
+    r = RQ.compute_wq_rules(b)
+    k0, ptr, w = pack_rules(r)
+    d["wq_nonuni_k0"], d["wq_nonuni_ptr"], d["wq_nonuni_w"], d["wq_nonuni_pts"] = k0, ptr, w, r.layout.points
+    d["wq_nonuni_knots"] = kv.knots
+    u = np.linspace(0, 1, 37)
+    f, v = b.eval_nonzero_batch(u)
+    d["eval_nonuni_u"], d["eval_nonuni_first"], d["eval_nonuni_vals"] = u, f, v
+    np.savez_compressed(os.path.join(HERE, "rules_1d.npz"), **d)
+    print("rules_1d done", flush=True)
+
+    # 2. the reference's canonical cases (all four strategies, full matrices)
+    for name in ("line", "circle", "corner"):
+        for nel, p in ((5, 1), (8, 2), (10, 3), (6, 4), (5, 6)):
+            b2d, cfg = RC.build_space(RC.make_case(name), nel, p)
+            dump_case(None, f"case_{name}_{nel}_{p}", b2d, cfg, ("reference", "wq", "hybrid", "dwq"),
+                      RP.default_target)
+
+    # 3. BASELINE config 1 (untrimmed 16^2 p=2)
+    c1 = OC.config(1)
+    b2d, cfg = space(16, 2, [])
+    dump_case(None, "config1", b2d, cfg, ("reference", "wq", "hybrid", "dwq"), c1["target"])
+
+    # 4. BASELINE config 2 (closed circle 64^2 p=3, hybrid), and the same
+    #    circle on small meshes through every strategy (seam cells included)
+    circ = HarnessCurve(OC.closed_circle())
+    for nel, p in ((10, 2), (16, 3)):
+        b2d, cfg = space(nel, p, [circ])
+        # cross-check the harness against the reference's own CircleTrim(pi, -pi)
+        _, cfg_ref = space(nel, p, [RT.CircleTrim((0.5, 0.5), 0.3, np.pi, -np.pi)])
+        assert np.array_equal(cfg.element_class, cfg_ref.element_class)
+        dump_case(None, f"ccircle_{nel}_{p}", b2d, cfg, ("reference", "wq", "hybrid", "dwq"), OC.f_config23)
+    b2d, cfg = space(64, 3, [circ])
+    dump_case(None, "config2", b2d, cfg, ("hybrid", "dwq"), OC.f_config23)
+
+    # 5. periodic B-spline trim (configs 4/5 curve) on small meshes, with and
+    #    without the det J coefficient
+    c4 = OC.config(4)
+    bs = HarnessCurve(c4["curves"][0])
+    for nel, p in ((24, 2), (32, 3)):
+        b2d, cfg = space(nel, p, [bs])
+        dump_case(None, f"bspline_{nel}_{p}", b2d, cfg, ("reference", "hybrid", "dwq"), OC.f_config5)
+        dump_case(None, f"bspline_detj_{nel}_{p}", b2d, cfg, ("reference", "hybrid", "dwq"), OC.f_config5,
+                  coeff=c4["coeff"], project=False)
+
+    if args.big:
+        b2d, cfg = space(128, 4, [circ])
+        dump_case(None, "config3", b2d, cfg, ("hybrid", "dwq"), OC.f_config23, full=False)
+        for p in (6, 8):
+            b2d, cfg = space(256, p, [bs])
+            dump_case(None, f"config4_p{p}", b2d, cfg, ("dwq",), None, coeff=c4["coeff"], full=False)
+    print(f"done in {time.perf_counter() - t_all:.1f}s")
+
+
+if __name__ == "__main__":
+    main()
