@@ -1,0 +1,189 @@
+/*
+ * trimquad_b200 -- C ABI of the B200-native formation path of arXiv 2101.08053
+ * (weighted-quadrature row assembly of trimmed bivariate B-spline mass
+ * matrices and the L2-projection right-hand side).
+ *
+ * Conventions
+ *   - every entry point returns 0 on success or a TQ_E* status; the message of
+ *     the last failure on the calling thread is in tq_last_error();
+ *   - every array argument is a caller-owned DEVICE pointer unless its name
+ *     ends in _h (host pointer); sizes are element counts;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *   - no hidden global device state: all buffers belong to the caller.
+ *
+ * Each entry point names the reference interface it replaces
+ * (src/ = /root/reference/pkg/src/trimquad/).
+ */
+#ifndef TRIMQUAD_B200_H
+#define TRIMQUAD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> Python exceptions (paper_2101_08053_b200/_lib.py) */
+#define TQ_OK 0
+#define TQ_EINVAL 1        /* ValueError                    */
+#define TQ_ERULE 2         /* RuleConstructionError          */
+#define TQ_ETRIM 3         /* TrimmingConfigurationError     */
+#define TQ_EPATTERN 4      /* RuntimeError (pattern miss)    */
+#define TQ_ECUDA 5         /* RuntimeError (CUDA failure)    */
+#define TQ_EOVERFLOW 6     /* OverflowError (nnz >= 2^31)    */
+
+/* element / function classes (src/trimming.py:53-56) */
+#define TQ_INTERIOR 0
+#define TQ_CUT 1
+#define TQ_EXTERIOR 2
+
+/* one univariate B-spline space (src/splines.py:32-232); device arrays */
+typedef struct {
+    const double* knots;     /* nknots = n + p + 1 */
+    const double* bp;        /* nel + 1 breakpoints */
+    const int32_t* espan;    /* nel: knot span of each element */
+    const int32_t* el_first; /* n: first support element */
+    const int32_t* el_last;  /* n: last support element */
+    const int32_t* ov_lo;    /* n: first overlapping trial */
+    const int32_t* ov_hi;    /* n: last overlapping trial */
+    int32_t nknots, p, n, nel;
+} tq_space1d;
+
+/* a point layout (src/quadrature.py:74-121); device arrays */
+typedef struct {
+    const double* pts;       /* npts, sorted, strictly interior to elements */
+    const int32_t* offsets;  /* nel + 1 */
+    int32_t npts, nel;
+} tq_layout;
+
+/* a weighted rule set (src/quadrature.py:201-260): row i holds weights
+ * w[wptr[i] .. wptr[i+1]) on layout points k0[i] ..; k0[i] < 0: no rule */
+typedef struct {
+    const int64_t* wptr;     /* n + 1 */
+    const int32_t* k0;       /* n */
+    const double* w;
+} tq_rules;
+
+/* trimming curve descriptor (src/trimming.py:69-351 + harness curves) */
+#define TQ_CURVE_LINE 1           /* data: p0x p0y p1x p1y                    */
+#define TQ_CURVE_ARC 2            /* data: cx cy r theta0 theta1              */
+#define TQ_CURVE_CLOSED_CIRCLE 3  /* data: cx cy r ccw(0/1) seam              */
+#define TQ_CURVE_BEZIER 4         /* data: 4 ctrl (x,y) + 3 anchors (x,y)     */
+#define TQ_CURVE_BSPLINE 5        /* data: shift, ccw(0/1), m ctrl (x,y)      */
+typedef struct {
+    int32_t kind;
+    int32_t m;               /* control points (BSPLINE), else 0 */
+    const double* data;      /* host or device pointer per entry point */
+} tq_curve;
+
+/* coefficient field c(u1,u2) (src/assembly.py:54-85) */
+#define TQ_COEFF_IDENTITY 0
+#define TQ_COEFF_GEOMETRY 1  /* det J of a B-spline map; data below           */
+typedef struct {
+    int32_t kind;
+    int32_t p, n;            /* geometry spline degree and #functions/dir     */
+    const double* knots;     /* device: n + p + 1 (same in both directions)   */
+    const double* X;         /* device: n*n control x, row-major (i1, i2)     */
+    const double* Y;         /* device: n*n control y                         */
+} tq_coeff;
+
+int tq_version(void);
+const char* tq_last_error(void);
+int tq_device_sync(void* stream);
+
+/* ---- subsystem (1): basis, moments, weights ------------------------------ */
+
+/* Cox-de Boor at n points: first function index and p+1 values (and first
+ * derivatives if ders != NULL).  Replaces Basis1D.eval_nonzero_batch
+ * (src/splines.py:245-269). */
+int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* first,
+                  double* vals, double* ders, int32_t* status, void* stream);
+
+/* exact banded 1-D mass matrix mom[i*(2p+1) + (j-i+p)] with (p+1)-point
+ * Gauss per element.  Replaces mass_matrix_1d (src/quadrature.py:160-188). */
+int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng,
+                    double* mom, void* stream);
+
+/* batched moment fits, one pivoted-QR basic solve per listed test row, on
+ * layout `lay` with basis values (first, vals) at its points.  Writes
+ * rules.w (at wptr offsets), rules.k0, and fail[r] = 1 where the residual
+ * exceeds 1e-12 max|b|.  Replaces _solve_rows/_qr_basic_solve
+ * (src/quadrature.py:263-303). */
+int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, const double* vals,
+                const double* mom, const int32_t* rows, int32_t nrows,
+                int32_t tmax, int32_t mmax, int64_t* wptr, int32_t* k0, double* w,
+                int32_t* fail, void* stream);
+
+/* DWQ combination w_j = sum_i S_ij w~_i over augmented points (S in CSC,
+ * device).  Replaces build_dwq step 4 (src/quadrature.py:434-444). */
+int tq_dwq_combine(const int32_t* rows, int32_t nrows, const int32_t* s_colptr,
+                   const int32_t* s_rowidx, const double* s_val,
+                   tq_rules fine, tq_rules out_rules, void* stream);
+
+/* ---- subsystem (2): classification --------------------------------------- */
+
+/* element classes nel1 x nel2 (int8, row-major).  Replaces classify_elements
+ * (src/trimming.py:607-733).  `curves` data pointers are DEVICE pointers. */
+int tq_classify_elements(const tq_curve* curves_h, int32_t ncurves,
+                         tq_space1d s1, tq_space1d s2, int8_t* elem_class,
+                         int32_t* status, void* stream);
+
+/* function classes n1 x n2 and discontinuity-face flags per direction.
+ * Replaces TrimConfiguration.__init__ (src/trimming.py:441-484). */
+int tq_function_classes(tq_space1d s1, tq_space1d s2, const int8_t* elem_class,
+                        int8_t* func_class, int32_t* face1, int32_t* face2, void* stream);
+
+/* active compact index col_of (n1*n2, -1 = exterior), active list and K
+ * (host out).  Replaces active_functions + _Pattern.col_of
+ * (src/trimming.py:514-517, src/assembly.py:148-153). */
+int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* col_of,
+                    int32_t* active, int32_t* K_h, void* stream);
+
+/* DWQ routing of each cut row (src/trimming.py:545-586): route[r*8 + ...] =
+ * {eligible, iu1, iu2, box a1, b1, a2, b2, side flags}; iu = index into
+ * udisc arrays or -1. */
+int tq_dwq_route(tq_space1d s1, tq_space1d s2, const int8_t* elem_class,
+                 const double* udisc1, int32_t nu1, const double* udisc2, int32_t nu2,
+                 const int32_t* cut_rows, int32_t ncut, int32_t* route, void* stream);
+
+/* ---- subsystems (3)+(4): rows ------------------------------------------- */
+
+/* banded WQ product table a[i*(2p+1) + (j-i+p)] = sum_k w_i[k] B_j(x_k) --
+ * the direction-wise contraction of sum_factor_row (src/assembly.py:245-252)
+ * for a coefficient-free direction. */
+int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first, const double* vals,
+                   tq_rules rules, double* a, void* stream);
+
+/* per-row kept-entry counts of the symmetrised pattern and the final CSR
+ * fill (src/assembly.py:400-404 fused with the row assembly
+ * src/assembly.py:409-449).  See DESIGN.md "rows". */
+typedef struct {
+    int32_t n1, n2, p1, p2;
+    const int32_t* ov_lo1; const int32_t* ov_hi1;
+    const int32_t* ov_lo2; const int32_t* ov_hi2;
+    const int32_t* col_of;       /* n1*n2 */
+    const int32_t* active;       /* K: i1*n2 + i2 */
+    const int32_t* slot;         /* n1*n2: raw-block slot or -1 (separable) */
+    const double* a1;            /* n1*(2p1+1) */
+    const double* a2;            /* n2*(2p2+1) */
+    const double* raw;           /* nslots * (2p1+1)*(2p2+1) */
+    const int8_t* deep;          /* n1*n2: 1 = separable row whose window holds
+                                    only separable rows with positive factors */
+    int32_t row_begin, row_end;  /* active rows [begin, end) */
+} tq_rowctx;
+
+/* deep-row flags: deep[i] = separable(i) && no raw row in window(i) &&
+ * positive direction factors (the fill then needs no per-entry gathers) */
+int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows,
+                  int32_t nraw, int8_t* deep, void* stream);
+
+int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
+int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
+                   int64_t* nnz_h, void* stream);
+int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIMQUAD_B200_H */

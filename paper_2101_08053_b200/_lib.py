@@ -1,0 +1,144 @@
+"""ctypes binding of the C ABI in ``include/trimquad_b200.h``.
+
+The library is built in-tree (``paper_2101_08053_b200/libtq_b200.so``).  There
+is no CPU fallback: importing a formation entry point without the library or
+without a CUDA device raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtq_b200.so")
+
+TQ_OK, TQ_EINVAL, TQ_ERULE, TQ_ETRIM, TQ_EPATTERN, TQ_ECUDA, TQ_EOVERFLOW = range(7)
+INTERIOR, CUT, EXTERIOR = 0, 1, 2
+
+
+class RuleConstructionError(RuntimeError):
+    """A weight row cannot satisfy its moment system (src/quadrature.py:46-47)."""
+
+
+class TrimmingConfigurationError(RuntimeError):
+    """Trimming layout outside the supported catalog (src/trimming.py:49-50)."""
+
+
+class NativeError(RuntimeError):
+    """CUDA / native failure."""
+
+
+_EXC = {TQ_EINVAL: ValueError, TQ_ERULE: RuleConstructionError, TQ_ETRIM: TrimmingConfigurationError,
+        TQ_EPATTERN: RuntimeError, TQ_ECUDA: NativeError, TQ_EOVERFLOW: OverflowError}
+
+vp = C.c_void_p
+i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
+
+
+class Space1D(C.Structure):
+    _fields_ = [("knots", vp), ("bp", vp), ("espan", vp), ("el_first", vp), ("el_last", vp),
+                ("ov_lo", vp), ("ov_hi", vp), ("nknots", i32), ("p", i32), ("n", i32), ("nel", i32)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("pts", vp), ("offsets", vp), ("npts", i32), ("nel", i32)]
+
+
+class Rules(C.Structure):
+    _fields_ = [("wptr", vp), ("k0", vp), ("w", vp)]
+
+
+class Curve(C.Structure):
+    _fields_ = [("kind", i32), ("m", i32), ("data", vp)]
+
+
+class Coeff(C.Structure):
+    _fields_ = [("kind", i32), ("p", i32), ("n", i32), ("knots", vp), ("X", vp), ("Y", vp)]
+
+
+class RowCtx(C.Structure):
+    _fields_ = [("n1", i32), ("n2", i32), ("p1", i32), ("p2", i32),
+                ("ov_lo1", vp), ("ov_hi1", vp), ("ov_lo2", vp), ("ov_hi2", vp),
+                ("col_of", vp), ("active", vp), ("slot", vp), ("a1", vp), ("a2", vp), ("raw", vp),
+                ("deep", vp), ("row_begin", i32), ("row_end", i32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the native library (once).  Fails loudly: no fallback exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"native library missing: {LIB_PATH} (run __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "tq_version": ([], i32),
+        "tq_last_error": ([], C.c_char_p),
+        "tq_device_sync": ([vp], i32),
+        "tq_basis_eval": ([Space1D, vp, i64, vp, vp, vp, vp, vp], i32),
+        "tq_moments_1d_g": ([Space1D, vp, vp, i32, vp, vp], i32),
+        "tq_wq_solve": ([Space1D, Layout, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp], i32),
+        "tq_dwq_combine": ([vp, i32, vp, vp, vp, Rules, Rules, vp], i32),
+        "tq_wq_products": ([Space1D, Layout, vp, vp, Rules, vp, vp], i32),
+        "tq_row_counts": ([RowCtx, vp, vp], i32),
+        "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
+        "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),
+        "tq_deep_flags": ([RowCtx, vp, vp, i32, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def optional(name, args, res=i32):
+    """Bind an entry point added after the first release (absent -> None)."""
+    L = lib()
+    fn = getattr(L, name, None)
+    if fn is not None:
+        fn.argtypes = args
+        fn.restype = res
+    return fn
+
+
+def call(name, *args):
+    fn = getattr(lib(), name)
+    rc = fn(*args)
+    if rc != TQ_OK:
+        msg = lib().tq_last_error().decode(errors="replace")
+        raise _EXC.get(rc, RuntimeError)(f"{name}: {msg}")
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("trimquad_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    return vp(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return vp(t.data_ptr()) if t is not None else vp(0)
+
+
+def dev(x, dtype):
+    """Upload a host array (numpy) as a contiguous device tensor."""
+    import numpy as np
+    a = np.ascontiguousarray(x)
+    t = torch.from_numpy(a).to(device=device(), dtype=dtype, non_blocking=False)
+    return t.contiguous()
+
+
+def sync():
+    call("tq_device_sync", stream())

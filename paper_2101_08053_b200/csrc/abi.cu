@@ -1,0 +1,32 @@
+// C-ABI plumbing: error reporting and stream sync.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace tq {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+    set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+    return TQ_ECUDA;
+}
+
+}  // namespace tq
+
+extern "C" int tq_version(void) { return 1; }
+
+extern "C" const char* tq_last_error(void) { return tq::g_err; }
+
+extern "C" int tq_device_sync(void* stream) {
+    TQ_CUDA(cudaStreamSynchronize(tq::S(stream)));
+    TQ_CUDA(cudaGetLastError());
+    return TQ_OK;
+}

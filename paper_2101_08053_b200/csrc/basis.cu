@@ -1,0 +1,97 @@
+// Subsystem (1): univariate basis evaluation and exact 1-D moments.
+//
+//  tq_basis_eval  <- Basis1D.eval_nonzero_batch   src/splines.py:245-269
+//  tq_moments_1d  <- mass_matrix_1d              src/quadrature.py:160-188
+#include "common.cuh"
+
+namespace tq {
+
+template <int P>
+__global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t n,
+                             int32_t* __restrict__ first, double* __restrict__ vals,
+                             double* __restrict__ ders, int32_t* status) {
+    const double lo = s.knots[0], hi = s.knots[s.nknots - 1];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        double x = u[t];
+        if (!(x >= lo && x <= hi)) {
+            atomicOr(status, kStatusDomain);
+            x = x < lo ? lo : hi;
+        }
+        int span = find_span(s.knots, s.nknots, P, s.n, x);
+        double N[P + 1];
+        if (ders) {
+            double D[kMaxP + 1];
+            double Nr[kMaxP + 1];
+            basis_funs_ders_rt(s.knots, P, span, x, Nr, D);
+#pragma unroll
+            for (int k = 0; k <= P; ++k) { N[k] = Nr[k]; ders[t * (P + 1) + k] = D[k]; }
+        } else {
+            basis_funs<P>(s.knots, span, x, N);
+        }
+        first[t] = span - P;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) vals[t * (P + 1) + k] = N[k];
+    }
+}
+
+// Banded exact 1-D mass matrix: thread per (i, o), j = i - p + o; element
+// loop over the shared support in element order (the order np.add.at
+// accumulates element blocks in the reference).
+__global__ void k_moments(tq_space1d s, const double* __restrict__ gx, const double* __restrict__ gw,
+                          int ng, double* __restrict__ mom) {
+    const int p = s.p, W = 2 * p + 1;
+    int64_t total = (int64_t)s.n * W;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int i = (int)(t / W), o = (int)(t % W);
+        int j = i - p + o;
+        double acc = 0.0;
+        if (j >= 0 && j < s.n && j >= s.ov_lo[i] && j <= s.ov_hi[i]) {
+            int ea = max(s.el_first[i], s.el_first[j]);
+            int eb = min(s.el_last[i], s.el_last[j]);
+            for (int e = ea; e <= eb; ++e) {
+                double a = s.bp[e], b = s.bp[e + 1];
+                double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+                int span = s.espan[e];
+                double part = 0.0;
+                for (int g = 0; g < ng; ++g) {
+                    double x = mid + half * gx[g];
+                    double N[kMaxP + 1];
+                    basis_funs_rt(s.knots, p, span, x, N);
+                    double bi = N[i - (span - p)], bj = N[j - (span - p)];
+                    part += bi * bj * (half * gw[g]);
+                }
+                acc += part;
+            }
+        }
+        mom[t] = acc;
+    }
+}
+
+}  // namespace tq
+
+using namespace tq;
+
+extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* first,
+                             double* vals, double* ders, int32_t* status, void* stream) {
+    if (n == 0) return TQ_OK;
+    if (s.p < 0 || s.p > kMaxP) { set_error("degree %d unsupported (max %d)", s.p, kMaxP); return TQ_EINVAL; }
+    int grid = grid_for(n, 256);
+    switch (s.p) {
+#define CASE(P) case P: k_basis_eval<P><<<grid, 256, 0, S(stream)>>>(s, u, n, first, vals, ders, status); break;
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    }
+    TQ_LAUNCH_CHECK("k_basis_eval");
+    return TQ_OK;
+}
+
+extern "C" int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng,
+                               double* mom, void* stream) {
+    if (s.p > kMaxP) { set_error("degree %d unsupported", s.p); return TQ_EINVAL; }
+    int64_t total = (int64_t)s.n * (2 * s.p + 1);
+    k_moments<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, gx, gw, ng, mom);
+    TQ_LAUNCH_CHECK("k_moments");
+    return TQ_OK;
+}

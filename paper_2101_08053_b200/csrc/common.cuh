@@ -1,0 +1,134 @@
+// Shared helpers for the trimquad_b200 native library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/trimquad_b200.h"
+
+namespace tq {
+
+void set_error(const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+
+#define TQ_CUDA(call)                                              \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return ::tq::check_cuda(_e, #call); \
+    } while (0)
+
+#define TQ_LAUNCH_CHECK(name)                                        \
+    do {                                                             \
+        cudaError_t _e = cudaGetLastError();                         \
+        if (_e != cudaSuccess) return ::tq::check_cuda(_e, name);    \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kMaxP = 10;          // largest supported degree
+constexpr int kSms = 148;          // B200 SM count (grid sizing)
+
+// device status word bits (accumulated with atomicOr by kernels)
+constexpr int kStatusDomain = 1;   // coordinate outside the knot domain
+constexpr int kStatusTrim = 2;     // unsupported trimming configuration
+constexpr int kStatusOverflow = 4;
+
+// searchsorted(a, x, side="right") on a sorted device array
+__host__ __device__ inline int upper_bound_d(const double* a, int n, double x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// searchsorted(a, x, side="left")
+__host__ __device__ inline int lower_bound_d(const double* a, int n, double x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// knot span of u (src/splines.py:114-122): searchsorted right - 1, clipped
+__host__ __device__ inline int find_span(const double* knots, int nknots, int p, int n, double u) {
+    int s = upper_bound_d(knots, nknots, u) - 1;
+    if (s < p) s = p;
+    if (s > n - 1) s = n - 1;
+    return s;
+}
+
+// Cox-de Boor triangle (NURBS book A2.2) -- the p+1 non-zero values at u on
+// span `span`; same operation order as src/splines.py:256-268.
+template <int P>
+__host__ __device__ inline void basis_funs(const double* kn, int span, double u, double* N) {
+    double left[P + 1], right[P + 1];
+    N[0] = 1.0;
+#pragma unroll
+    for (int j = 1; j <= P; ++j) {
+        left[j - 1] = u - kn[span + 1 - j];
+        right[j - 1] = kn[span + j] - u;
+        double saved = 0.0;
+#pragma unroll
+        for (int r = 0; r < j; ++r) {
+            double temp = N[r] / (right[r] + left[j - r - 1]);
+            N[r] = saved + right[r] * temp;
+            saved = left[j - r - 1] * temp;
+        }
+        N[j] = saved;
+    }
+}
+
+// runtime-degree version (p <= kMaxP)
+__host__ __device__ inline void basis_funs_rt(const double* kn, int p, int span, double u, double* N) {
+    double left[kMaxP + 1], right[kMaxP + 1];
+    N[0] = 1.0;
+    for (int j = 1; j <= p; ++j) {
+        left[j - 1] = u - kn[span + 1 - j];
+        right[j - 1] = kn[span + j] - u;
+        double saved = 0.0;
+        for (int r = 0; r < j; ++r) {
+            double temp = N[r] / (right[r] + left[j - r - 1]);
+            N[r] = saved + right[r] * temp;
+            saved = left[j - r - 1] * temp;
+        }
+        N[j] = saved;
+    }
+}
+
+// values + first derivatives on span (derivative via degree p-1 values)
+__host__ __device__ inline void basis_funs_ders_rt(const double* kn, int p, int span, double u,
+                                                   double* N, double* D) {
+    basis_funs_rt(kn, p, span, u, N);
+    if (p == 0) { D[0] = 0.0; return; }
+    double Nl[kMaxP + 1];
+    basis_funs_rt(kn, p - 1, span, u, Nl);  // B_{span-p+1 .. span, p-1}
+    for (int k = 0; k <= p; ++k) {
+        int i = span - p + k;
+        double acc = 0.0;
+        if (k >= 1) {
+            double den = kn[i + p] - kn[i];
+            if (den > 0.0) acc += (double)p / den * Nl[k - 1];
+        }
+        if (k <= p - 1) {
+            double den = kn[i + p + 1] - kn[i + 1];
+            if (den > 0.0) acc -= (double)p / den * Nl[k];
+        }
+        D[k] = acc;
+    }
+}
+
+inline int grid_for(int64_t work, int per_block) {
+    int64_t g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > (int64_t)kSms * 64) g = kSms * 64;
+    return (int)g;
+}
+
+}  // namespace tq

@@ -1,0 +1,388 @@
+"""Quadrature rules: Gauss, WQ point layouts, GPU moment fits, DWQ.
+
+Drop-in for ``trimquad.quadrature`` (src/quadrature.py:25-449).  Host side:
+point-layout integer logic (counts, nested augmentation, knot insertion),
+which is O(n) bookkeeping.  Device side: basis tables, exact 1-D moments,
+the batched pivoted-QR moment fits and the DWQ combination
+(``tq_moments_1d_g``, ``tq_wq_solve``, ``tq_dwq_combine``).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib as L
+from ._lib import RuleConstructionError
+from .splines import Basis1D, refine_to_c_minus_1
+
+FIT_TOL = 1e-12       # src/quadrature.py:40
+MAX_RETRIES = 5       # src/quadrature.py:43
+
+
+@dataclass(frozen=True)
+class GaussRule:
+    """src/quadrature.py:50-60."""
+    points: np.ndarray
+    weights: np.ndarray
+
+    def mapped(self, a, b):
+        mid, half = 0.5 * (a + b), 0.5 * (b - a)
+        return mid + half * self.points, half * self.weights
+
+
+@lru_cache(maxsize=None)
+def gauss_legendre(n: int) -> GaussRule:
+    """n-point Gauss-Legendre rule on [-1,1] (src/quadrature.py:63-71)."""
+    if n < 1:
+        raise ValueError(f"point count must be positive, got {n}")
+    x, w = np.polynomial.legendre.leggauss(n)
+    x.setflags(write=False)
+    w.setflags(write=False)
+    return GaussRule(x, w)
+
+
+_gauss_dev = {}
+
+
+def gauss_device(n):
+    if n not in _gauss_dev:
+        g = gauss_legendre(n)
+        _gauss_dev[n] = (L.dev(g.points, torch.float64), L.dev(g.weights, torch.float64))
+    return _gauss_dev[n]
+
+
+class PointLayout:
+    """Points grouped by element, strictly interior (src/quadrature.py:74-121)."""
+
+    def __init__(self, breakpoints, per_element=None, *, points=None, offsets=None, check=True):
+        self.breakpoints = np.asarray(breakpoints, dtype=float)
+        if per_element is not None:
+            counts = np.array([len(g) for g in per_element], dtype=np.int64)
+            self.offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            self.points = np.concatenate(per_element) if self.offsets[-1] else np.empty(0)
+        else:
+            self.points = np.asarray(points, dtype=float)
+            self.offsets = np.asarray(offsets, dtype=np.int64)
+        counts = np.diff(self.offsets)
+        self.element_of_point = np.repeat(np.arange(counts.size), counts)
+        if check and self.points.size:
+            e = self.element_of_point
+            if np.any(self.points <= self.breakpoints[e]) or np.any(self.points >= self.breakpoints[e + 1]):
+                bad = int(e[np.nonzero((self.points <= self.breakpoints[e]) |
+                                       (self.points >= self.breakpoints[e + 1]))[0][0]])
+                raise ValueError(f"points of element {bad} not strictly interior")
+        self._dev = None
+
+    num_points = property(lambda self: int(self.offsets[-1]))
+    num_elements = property(lambda self: self.breakpoints.size - 1)
+
+    def counts(self):
+        return np.diff(self.offsets)
+
+    def element_points(self, e):
+        return self.points[self.offsets[e]: self.offsets[e + 1]]
+
+    def range_for_elements(self, e0, e1):
+        return int(self.offsets[e0]), int(self.offsets[e1 + 1])
+
+    def contains(self, other, tol=1e-12):
+        idx = np.clip(np.searchsorted(self.points, other.points), 0, self.num_points - 1)
+        near = np.abs(self.points[idx] - other.points) <= tol
+        idx2 = np.clip(idx - 1, 0, self.num_points - 1)
+        near |= np.abs(self.points[idx2] - other.points) <= tol
+        return bool(np.all(near))
+
+    def device(self):
+        if self._dev is None:
+            pts = L.dev(self.points, torch.float64)
+            off = L.dev(self.offsets, torch.int32)
+            self._dev = (L.Layout(L.ptr(pts), L.ptr(off), self.num_points, self.num_elements), pts, off)
+        return self._dev[0]
+
+    def device_points(self):
+        self.device()
+        return self._dev[1]
+
+
+def _required_counts(basis: Basis1D) -> np.ndarray:
+    """max over tests of ceil(#trials / #support elements) (src/quadrature.py:130-143)."""
+    t = basis._ov_hi - basis._ov_lo + 1
+    ne = basis._el_last - basis._el_first + 1
+    need = -(-t // ne)
+    req = np.zeros(basis.num_elements, dtype=np.int64)
+    # each function raises its support elements to its need
+    for off in range(int(ne.max()) if ne.size else 0):
+        e = basis._el_first + off
+        ok = e <= basis._el_last
+        np.maximum.at(req, e[ok], need[ok])
+    return req
+
+
+def _layout_from_counts(basis: Basis1D, counts) -> PointLayout:
+    """a + (b-a)*k/(count+1), k = 1..count per element (src/quadrature.py:124-152)."""
+    bp = basis.breakpoints
+    counts = np.asarray(counts, dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(counts)])
+    e = np.repeat(np.arange(counts.size), counts)
+    k = np.arange(offsets[-1]) - offsets[e] + 1
+    a, b = bp[e], bp[e + 1]
+    pts = a + (b - a) * k / (counts[e] + 1)
+    return PointLayout(bp, points=pts, offsets=offsets)
+
+
+def place_wq_points(basis: Basis1D) -> PointLayout:
+    """src/quadrature.py:155-157."""
+    return _layout_from_counts(basis, _required_counts(basis))
+
+
+_mom_cache = {}
+
+
+def moments_device(basis: Basis1D):
+    """Banded exact 1-D mass matrix on the GPU, n x (2p+1) (cached per basis)."""
+    key = id(basis)
+    hit = _mom_cache.get(key)
+    if hit is not None and hit[0] is basis:
+        return hit[1]
+    gx, gw = gauss_device(basis.p + 1)
+    mom = torch.empty((basis.n, 2 * basis.p + 1), dtype=torch.float64, device=L.device())
+    L.call("tq_moments_1d_g", basis.device(), L.ptr(gx), L.ptr(gw), basis.p + 1, L.ptr(mom), L.stream())
+    _mom_cache[key] = (basis, mom)
+    return mom
+
+
+def mass_matrix_1d(basis: Basis1D, trial_basis=None) -> np.ndarray:
+    """Exact 1-D mass matrix (src/quadrature.py:160-188), formed on the GPU."""
+    if trial_basis is not None and trial_basis is not basis:
+        raise NotImplementedError("mixed test/trial bases are not on the formation path")
+    band = moments_device(basis).cpu().numpy()
+    n, p = basis.n, basis.p
+    M = np.zeros((n, n))
+    i = np.repeat(np.arange(n), 2 * p + 1)
+    j = i - p + np.tile(np.arange(2 * p + 1), n)
+    ok = (j >= 0) & (j < n)
+    M[i[ok], j[ok]] = band.ravel()[ok]
+    return M
+
+
+def exact_moments(basis, i):
+    j0, j1 = basis.overlapping(i)
+    return j0, mass_matrix_1d(basis)[i, j0: j1 + 1].copy()
+
+
+class WeightedRuleSet:
+    """Per-test weight rows on one layout, stored on the device
+    (src/quadrature.py:201-232).  ``rows`` materializes host copies lazily."""
+
+    def __init__(self, basis, layout, wptr, k0, w, direction=None):
+        self.basis = basis
+        self.layout = layout
+        self.wptr, self.k0, self.w = wptr, k0, w     # device tensors
+        self.direction = direction
+        self._rows = None
+        self._basis_tab = None
+
+    def device(self):
+        return L.Rules(L.ptr(self.wptr), L.ptr(self.k0), L.ptr(self.w))
+
+    @property
+    def rows(self):
+        if self._rows is None:
+            wptr = self.wptr.cpu().numpy()
+            k0 = self.k0.cpu().numpy()
+            w = self.w.cpu().numpy()
+            self._rows = [None if k0[i] < 0 else (int(k0[i]), w[wptr[i]: wptr[i + 1]].copy())
+                          for i in range(k0.size)]
+        return self._rows
+
+    def row(self, i):
+        return self.rows[i]
+
+    def row_full(self, i):
+        k0, w = self.rows[i]
+        full = np.zeros(self.layout.num_points)
+        full[k0: k0 + w.size] = w
+        return full
+
+    def total_points(self):
+        return self.layout.num_points
+
+    def apply(self, i, values_at_points):
+        k0, w = self.rows[i]
+        return float(np.dot(w, values_at_points[k0: k0 + w.size]))
+
+    def basis_table(self):
+        """(first, vals) of the basis at this layout's points (device)."""
+        if self._basis_tab is None:
+            self._basis_tab = self.basis.eval_device(self.layout.device_points())
+        return self._basis_tab
+
+
+class DiscontinuousRuleSet(WeightedRuleSet):
+    """src/quadrature.py:235-260."""
+
+    def __init__(self, basis, layout, wptr, k0, w, u_disc, subdivision, refined_basis, base_layout,
+                 direction=None, regular_side=None):
+        super().__init__(basis, layout, wptr, k0, w, direction)
+        self.u_disc = float(u_disc)
+        self.subdivision = subdivision
+        self.refined_basis = refined_basis
+        self.base_layout = base_layout
+        self.regular_side = regular_side
+
+    def side_points(self, side):
+        if side == "left":
+            return np.nonzero(self.layout.points < self.u_disc)[0]
+        if side == "right":
+            return np.nonzero(self.layout.points > self.u_disc)[0]
+        raise ValueError(f"side must be 'left' or 'right', got {side!r}")
+
+
+def _row_lengths(basis, layout):
+    e0, e1 = basis._el_first, basis._el_last
+    return layout.offsets[e1 + 1] - layout.offsets[e0]
+
+
+def _solve_rows(basis: Basis1D, layout: PointLayout, which=None):
+    """GPU moment fits of the selected rows (src/quadrature.py:281-303).
+    Returns (wptr, k0, w device tensors, failing rows list)."""
+    dev = L.device()
+    lens = _row_lengths(basis, layout)
+    wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    rows_h = np.arange(basis.n, dtype=np.int32) if which is None else np.asarray(which, dtype=np.int32)
+    wptr = L.dev(wptr_h, torch.int64)
+    k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
+    w = torch.zeros(int(wptr_h[-1]), dtype=torch.float64, device=dev)
+    if rows_h.size == 0:
+        return wptr, k0, w, []
+    first, vals = basis.eval_device(layout.device_points())
+    mom = moments_device(basis)
+    t = basis._ov_hi - basis._ov_lo + 1
+    tmax = int(t[rows_h].max())
+    mmax = int(lens[rows_h].max())
+    fail = torch.zeros(rows_h.size, dtype=torch.int32, device=dev)
+    rows = L.dev(rows_h, torch.int32)
+    L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
+           L.ptr(rows), rows_h.size, tmax, mmax, L.ptr(wptr), L.ptr(k0), L.ptr(w), L.ptr(fail), L.stream())
+    failing = rows_h[fail.cpu().numpy() != 0].tolist()
+    return wptr, k0, w, failing
+
+
+def _least_covered_element(basis, layout, i):
+    """src/quadrature.py:306-309."""
+    e0, e1 = basis.support_elements(i)
+    return int(e0 + np.argmin(layout.counts()[e0: e1 + 1]))
+
+
+def compute_wq_rules(basis: Basis1D, layout: PointLayout | None = None, direction=None) -> WeightedRuleSet:
+    """WQ rules for every test function, GPU fits + enrichment retries
+    (src/quadrature.py:312-337)."""
+    if layout is None:
+        layout = place_wq_points(basis)
+    counts = layout.counts().copy()
+    failing = []
+    for attempt in range(MAX_RETRIES + 1):
+        wptr, k0, w, failing = _solve_rows(basis, layout)
+        if not failing:
+            return WeightedRuleSet(basis, layout, wptr, k0, w, direction)
+        if attempt == MAX_RETRIES:
+            break
+        for i in failing:
+            counts[_least_covered_element(basis, layout, i)] += 1
+        layout = _layout_from_counts(basis, counts)
+    raise RuleConstructionError(f"moment fit residual above {FIT_TOL:g} for test functions {failing} "
+                                f"after {MAX_RETRIES} enrichment retries")
+
+
+def _split_largest_gap(pts, a, b):
+    """Midpoint of the first largest gap of [a, *pts, b] (src/quadrature.py:340-345)."""
+    fence = np.concatenate([[a], pts, [b]])
+    g = int(np.argmax(np.diff(fence)))
+    return 0.5 * (fence[g] + fence[g + 1])
+
+
+def _augment_nested(layout: PointLayout, extra) -> PointLayout:
+    """Nested largest-gap augmentation, only where extra > 0 (src/quadrature.py:348-363)."""
+    extra = np.asarray(extra)
+    if not np.any(extra):
+        return layout
+    groups = []
+    bp = layout.breakpoints
+    for e in range(layout.num_elements):
+        pts = layout.element_points(e)
+        if extra[e]:
+            pts = np.sort(pts)
+            for _ in range(int(extra[e])):
+                pts = np.sort(np.append(pts, _split_largest_gap(pts, bp[e], bp[e + 1])))
+        groups.append(pts)
+    return PointLayout(bp, groups)
+
+
+def dwq_layout(basis: Basis1D, layout: PointLayout, u: float):
+    """Integer/point part of DWQ (src/quadrature.py:382-407):
+    refined basis, subdivision matrix, nested augmented layout."""
+    refined, S = refine_to_c_minus_1(basis, u)
+    need = _required_counts(refined)
+    aug = _augment_nested(layout, np.maximum(need - layout.counts(), 0))
+    lens_needed = refined._ov_hi - refined._ov_lo + 1
+    for i in range(refined.n):
+        e0, e1 = refined.support_elements(i)
+        while aug.offsets[e1 + 1] - aug.offsets[e0] < lens_needed[i]:
+            bump = np.zeros(aug.num_elements, dtype=np.int64)
+            bump[_least_covered_element(refined, aug, i)] = 1
+            aug = _augment_nested(aug, bump)
+    return refined, S, aug
+
+
+def build_dwq(basis: Basis1D, layout: PointLayout, u_disc: float, direction=None,
+              regular_side=None, only_rows=None) -> DiscontinuousRuleSet:
+    """Discontinuous WQ (src/quadrature.py:366-449): host layout, GPU fits of
+    the refined rows, GPU combination w = S^T w~."""
+    bp = basis.breakpoints
+    if not np.any(np.abs(bp - u_disc) <= 1e-12):
+        raise ValueError(f"{u_disc} is not a breakpoint of the basis")
+    u = float(bp[np.argmin(np.abs(bp - u_disc))])
+    refined, S, aug = dwq_layout(basis, layout, u)
+    Sc = S.matrix.tocsc()
+    Sc.sort_indices()
+    wanted = np.arange(basis.n) if only_rows is None else np.array(sorted(set(int(r) for r in only_rows)))
+    fine_needed = None
+    if only_rows is not None:
+        seen = set()
+        for j in wanted:
+            seen.update(Sc.indices[Sc.indptr[j]: Sc.indptr[j + 1]].tolist())
+        fine_needed = sorted(seen)
+    failing = []
+    for attempt in range(MAX_RETRIES + 1):
+        fwptr, fk0, fw, failing = _solve_rows(refined, aug, fine_needed)
+        if not failing:
+            break
+        if attempt == MAX_RETRIES:
+            raise RuleConstructionError(f"discontinuous rule fit failed for refined test functions "
+                                        f"{failing} at u_disc={u}")
+        bump = np.zeros(aug.num_elements, dtype=np.int64)
+        for i in failing:
+            bump[_least_covered_element(refined, aug, i)] += 1
+        aug = _augment_nested(aug, bump)
+    # output rows of the original functions over the augmented layout
+    lens = _row_lengths(basis, aug)
+    sel = np.zeros(basis.n, dtype=bool)
+    sel[wanted] = True
+    lens = np.where(sel, lens, 0)
+    wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    k0_h = np.where(sel, aug.offsets[basis._el_first], -1).astype(np.int32)
+    wptr, k0 = L.dev(wptr_h, torch.int64), L.dev(k0_h, torch.int32)
+    w = torch.zeros(int(wptr_h[-1]), dtype=torch.float64, device=L.device())
+    cp = L.dev(Sc.indptr.astype(np.int32), torch.int32)
+    ri = L.dev(Sc.indices.astype(np.int32), torch.int32)
+    sv = L.dev(Sc.data, torch.float64)
+    rows = L.dev(wanted.astype(np.int32), torch.int32)
+    L.call("tq_dwq_combine", L.ptr(rows), wanted.size, L.ptr(cp), L.ptr(ri), L.ptr(sv),
+           L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(wptr), L.ptr(k0), L.ptr(w)), L.stream())
+    return DiscontinuousRuleSet(basis, aug, wptr, k0, w, u, S, refined, layout, direction, regular_side)

@@ -1,0 +1,296 @@
+"""Univariate and tensor-product B-spline spaces (host metadata + device mirror).
+
+Drop-in for the reference ``trimquad.splines`` types (src/splines.py:17-455):
+same class names, constructor arguments, properties and errors.  The index
+bookkeeping is O(n) host work; evaluation runs on the GPU
+(``Basis1D.eval_nonzero_batch`` -> ``tq_basis_eval``).
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib as L
+
+KNOT_TOL = 1e-12  # src/splines.py:29
+
+
+def _breakpoints(knots, tol=KNOT_TOL):
+    """Unique values merging entries within tol of the running value
+    (src/splines.py:156-166)."""
+    keep = [0]
+    mult = [1]
+    for k in range(1, knots.size):
+        if knots[k] - knots[keep[-1]] <= tol:
+            mult[-1] += 1
+        else:
+            keep.append(k)
+            mult.append(1)
+    return knots[np.asarray(keep)], np.asarray(mult, dtype=np.int64)
+
+
+class KnotVector:
+    """Open knot vector + degree (src/splines.py:32-153)."""
+
+    def __init__(self, knots, degree: int):
+        knots = np.ascontiguousarray(knots, dtype=float)
+        degree = int(degree)
+        if degree < 0:
+            raise ValueError(f"degree must be non-negative, got {degree}")
+        if knots.ndim != 1 or knots.size < 2 * (degree + 1):
+            raise ValueError("knot vector too short for the requested degree")
+        if np.any(np.diff(knots) < 0):
+            raise ValueError("knots must be non-decreasing")
+        bp, mult = _breakpoints(knots)
+        if mult[0] != degree + 1 or mult[-1] != degree + 1:
+            raise ValueError("open knot vector required: boundary knots must have "
+                             f"multiplicity exactly {degree + 1}")
+        if mult.size > 2 and np.any(mult[1:-1] > degree + 1):
+            raise ValueError(f"interior knot multiplicity exceeds {degree + 1}")
+        self.knots = knots
+        self.knots.setflags(write=False)
+        self.degree = degree
+        self.breakpoints = bp
+        self.multiplicities = mult
+        self.element_spans = np.cumsum(mult)[:-1] - 1
+
+    @property
+    def num_elements(self):
+        return self.breakpoints.size - 1
+
+    @property
+    def num_functions(self):
+        return self.knots.size - self.degree - 1
+
+    @property
+    def domain(self):
+        return float(self.knots[0]), float(self.knots[-1])
+
+    def multiplicity_of(self, u):
+        return int(np.sum(np.abs(self.knots - u) <= KNOT_TOL))
+
+    def find_spans(self, u):
+        u = np.asarray(u, dtype=float)
+        lo, hi = self.domain
+        if np.any(u < lo) or np.any(u > hi):
+            bad = u[(u < lo) | (u > hi)][0]
+            raise ValueError(f"coordinate {bad} outside domain [{lo}, {hi}]")
+        s = np.searchsorted(self.knots, u, side="right") - 1
+        return np.clip(s, self.degree, self.num_functions - 1)
+
+    def find_span(self, u):
+        return int(self.find_spans(np.asarray([u]))[0])
+
+    def element_of(self, u):
+        e = np.searchsorted(self.breakpoints, np.asarray(u, dtype=float), side="right") - 1
+        return np.clip(e, 0, self.num_elements - 1)
+
+    def insert(self, ubar):
+        at = int(np.searchsorted(self.knots, ubar, side="right"))
+        return KnotVector(np.insert(self.knots, at, ubar), self.degree)
+
+    def to_json(self):
+        return json.dumps({"degree": self.degree, "knots": self.knots.tolist()})
+
+    @classmethod
+    def from_json(cls, text):
+        d = json.loads(text)
+        return cls(d["knots"], d["degree"])
+
+    def __eq__(self, other):
+        return (isinstance(other, KnotVector) and self.degree == other.degree
+                and self.knots.size == other.knots.size
+                and bool(np.all(np.abs(self.knots - other.knots) <= KNOT_TOL)))
+
+    def __repr__(self):
+        return f"KnotVector(degree={self.degree}, n={self.num_functions})"
+
+
+class Basis1D:
+    """B-spline basis over a KnotVector (src/splines.py:169-300)."""
+
+    def __init__(self, kv: KnotVector):
+        self.kv = kv
+        spans = kv.element_spans
+        i = np.arange(kv.num_functions)
+        # support elements: spans in [i, i+p] (src/splines.py:178-190)
+        self._el_first = np.searchsorted(spans, i, side="left")
+        self._el_last = np.searchsorted(spans, i + kv.degree, side="right") - 1
+        self._ov_lo = spans[self._el_first] - kv.degree
+        self._ov_hi = spans[self._el_last]
+        self._dev = None
+
+    p = property(lambda self: self.kv.degree)
+    n = property(lambda self: self.kv.num_functions)
+    breakpoints = property(lambda self: self.kv.breakpoints)
+    num_elements = property(lambda self: self.kv.num_elements)
+    domain = property(lambda self: self.kv.domain)
+
+    def support_elements(self, i):
+        return int(self._el_first[i]), int(self._el_last[i])
+
+    def support_interval(self, i):
+        kn = self.kv.knots
+        return float(kn[i]), float(kn[i + self.p + 1])
+
+    def functions_on_element(self, e):
+        s = int(self.kv.element_spans[e])
+        return s - self.p, s
+
+    def overlapping(self, i):
+        return int(self._ov_lo[i]), int(self._ov_hi[i])
+
+    # -- device mirror ---------------------------------------------------------
+    def device(self):
+        """tq_space1d view with device arrays (cached)."""
+        if self._dev is None:
+            keep = {
+                "knots": L.dev(self.kv.knots, torch.float64),
+                "bp": L.dev(self.breakpoints, torch.float64),
+                "espan": L.dev(self.kv.element_spans, torch.int32),
+                "el_first": L.dev(self._el_first, torch.int32),
+                "el_last": L.dev(self._el_last, torch.int32),
+                "ov_lo": L.dev(self._ov_lo, torch.int32),
+                "ov_hi": L.dev(self._ov_hi, torch.int32),
+            }
+            st = L.Space1D(*(L.ptr(keep[k]) for k in ("knots", "bp", "espan", "el_first", "el_last",
+                                                     "ov_lo", "ov_hi")),
+                           self.kv.knots.size, self.p, self.n, self.num_elements)
+            self._dev = (st, keep)
+        return self._dev[0]
+
+    def device_arrays(self):
+        self.device()
+        return self._dev[1]
+
+    def eval_device(self, u_dev, ders=False):
+        """GPU Cox-de Boor at device points -> (first int32, vals[, ders])."""
+        n = u_dev.numel()
+        first = torch.empty(n, dtype=torch.int32, device=u_dev.device)
+        vals = torch.empty((n, self.p + 1), dtype=torch.float64, device=u_dev.device)
+        dv = torch.empty_like(vals) if ders else None
+        status = torch.zeros(1, dtype=torch.int32, device=u_dev.device)
+        L.call("tq_basis_eval", self.device(), L.ptr(u_dev), n, L.ptr(first), L.ptr(vals), L.ptr(dv),
+               L.ptr(status), L.stream())
+        if int(status.item()) & 1:
+            raise ValueError("coordinate outside the knot domain")
+        return (first, vals, dv) if ders else (first, vals)
+
+    def eval_nonzero_batch(self, u):
+        """(first, values) like src/splines.py:245-269, computed on the GPU."""
+        u = np.asarray(u, dtype=float).reshape(-1)
+        self.kv.find_spans(u)  # domain check with the reference's message
+        first, vals = self.eval_device(L.dev(u, torch.float64))
+        return first.cpu().numpy().astype(np.int64), vals.cpu().numpy()
+
+    def eval_nonzero(self, u):
+        f, v = self.eval_nonzero_batch(np.asarray([u]))
+        return int(f[0]), v[0]
+
+    def eval_single(self, i, u):
+        a, b = self.support_interval(i)
+        if u < a or u > b:
+            return 0.0
+        f, v = self.eval_nonzero(u)
+        k = i - f
+        return float(v[k]) if 0 <= k <= self.p else 0.0
+
+    def collocation(self, points):
+        points = np.asarray(points, dtype=float)
+        f, v = self.eval_nonzero_batch(points)
+        C = np.zeros((points.size, self.n))
+        rows = np.repeat(np.arange(points.size), self.p + 1)
+        cols = (f[:, None] + np.arange(self.p + 1)[None, :]).ravel()
+        C[rows, cols] = v.ravel()
+        return C
+
+    def spline_value(self, coeffs, u):
+        f, v = self.eval_nonzero_batch(u)
+        idx = f[:, None] + np.arange(self.p + 1)[None, :]
+        return np.einsum("kj,kj->k", np.asarray(coeffs)[idx], v)
+
+    def __repr__(self):
+        return f"Basis1D(p={self.p}, n={self.n}, elements={self.num_elements})"
+
+
+class TensorBasis2D:
+    """src/splines.py:303-330."""
+
+    def __init__(self, basis1: Basis1D, basis2: Basis1D):
+        self.dir = (basis1, basis2)
+
+    shape = property(lambda self: (self.dir[0].n, self.dir[1].n))
+    degrees = property(lambda self: (self.dir[0].p, self.dir[1].p))
+    num_elements = property(lambda self: (self.dir[0].num_elements, self.dir[1].num_elements))
+
+    def value(self, index, u1, u2):
+        return self.dir[0].eval_single(index[0], u1) * self.dir[1].eval_single(index[1], u2)
+
+    def __repr__(self):
+        return f"TensorBasis2D(p={self.degrees}, n={self.shape})"
+
+
+class SubdivisionMatrix:
+    """Sparse coarse->fine coefficient map (src/splines.py:333-366)."""
+
+    def __init__(self, matrix, source, target):
+        self.matrix = sp.csr_matrix(matrix)
+        self.source = source
+        self.target = target
+
+    shape = property(lambda self: self.matrix.shape)
+
+    def apply(self, coeffs):
+        return self.matrix @ np.asarray(coeffs)
+
+    def __matmul__(self, other):
+        return SubdivisionMatrix(self.matrix @ other.matrix, other.source, self.target)
+
+
+def insert_knot(basis: Basis1D, ubar: float):
+    """One knot insertion with its subdivision map (src/splines.py:369-403;
+    PAPER Eq. 9 alpha coefficients)."""
+    kv = basis.kv
+    p, n, kn = kv.degree, kv.num_functions, kv.knots
+    lo, hi = kv.domain
+    if not (lo <= ubar <= hi):
+        raise ValueError(f"insertion point {ubar} outside domain [{lo}, {hi}]")
+    if kv.multiplicity_of(ubar) >= p + 1:
+        raise ValueError(f"multiplicity of {ubar} would exceed {p + 1}")
+    l = kv.find_span(ubar)
+    k = np.arange(n + 1)
+    alpha = np.where(k <= l - p, 1.0, 0.0)
+    mid = np.arange(max(l - p + 1, 0), l + 1)
+    alpha[mid] = (ubar - kn[mid]) / (kn[mid + p] - kn[mid])
+    r = np.concatenate([np.arange(n), np.arange(1, n + 1)])
+    c = np.concatenate([np.arange(n), np.arange(n)])
+    S = sp.coo_matrix((np.concatenate([alpha[:n], 1.0 - alpha[1:]]), (r, c)), shape=(n + 1, n)).tocsr()
+    S.eliminate_zeros()
+    fine = Basis1D(kv.insert(ubar))
+    return fine, SubdivisionMatrix(S, basis, fine)
+
+
+def refine_to_c_minus_1(basis: Basis1D, u: float):
+    """Insert u up to multiplicity p+1 -> (refined basis, SubdivisionMatrix)."""
+    cur = basis
+    S = sp.identity(basis.n, format="csr")
+    for _ in range(basis.p + 1 - basis.kv.multiplicity_of(u)):
+        cur, step = insert_knot(cur, u)
+        S = step.matrix @ S
+    return cur, SubdivisionMatrix(S, basis, cur)
+
+
+def make_uniform_knots(num_elements, degree, a=0.0, b=1.0):
+    """src/splines.py:445-451."""
+    if num_elements < 1:
+        raise ValueError("need at least one element")
+    inner = np.linspace(a, b, num_elements + 1)[1:-1]
+    return KnotVector(np.concatenate([np.full(degree + 1, a), inner, np.full(degree + 1, b)]), degree)
+
+
+def make_uniform_basis(num_elements, degree, a=0.0, b=1.0):
+    return Basis1D(make_uniform_knots(num_elements, degree, a, b))
