@@ -140,8 +140,8 @@ int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* col_of,
                     int32_t* active, int32_t* K_h, void* stream);
 
 /* DWQ routing of each cut row (src/trimming.py:545-586): route[r*8 + ...] =
- * {eligible, iu1, iu2, box a1, b1, a2, b2, side flags}; iu = index into
- * udisc arrays or -1. */
+ * {eligible, iu1, iu2, a1, b1, a2, b2, 0}; iu = index into the udisc arrays
+ * or -1; a1 = -1 when no all-interior box exists. */
 int tq_dwq_route(tq_space1d s1, tq_space1d s2, const int8_t* elem_class,
                  const double* udisc1, int32_t nu1, const double* udisc2, int32_t nu2,
                  const int32_t* cut_rows, int32_t ncut, int32_t* route, void* stream);
@@ -182,6 +182,66 @@ int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                  void* stream);
+
+
+/* ---- raw (non-separable) rows ------------------------------------------ */
+
+/* a rule set with its basis table at the layout points */
+typedef struct {
+    tq_rules rules;
+    tq_layout lay;
+    const int32_t* first;    /* npts */
+    const double* vals;      /* npts x (p+1) */
+} tq_ruleset;
+
+#define TQ_ROW_GAUSS 0   /* element Gauss over the interior support elements */
+#define TQ_ROW_BOX 1     /* sum factorization over a point box + Gauss residual */
+#define TQ_ROW_MASK 2    /* naive WQ: sum factorization masked to interior elements */
+
+/* Everything the raw-row kernels read; all device pointers. */
+typedef struct {
+    int32_t n1, n2, p1, p2, nel1, nel2;
+    const int32_t* el_first1; const int32_t* el_last1;
+    const int32_t* el_first2; const int32_t* el_last2;
+    const int32_t* ov_lo1; const int32_t* ov_hi1;
+    const int32_t* ov_lo2; const int32_t* ov_hi2;
+    const int32_t* espan1; const int32_t* espan2;
+    const int8_t* elem_class;        /* nel1*nel2 */
+    int32_t ng1, ng2;                /* element Gauss points per direction (p+1) */
+    const double* ew1; const double* ev1;   /* nel*ng weights; nel*ng*(p+1) values */
+    const double* ew2; const double* ev2;
+    const double* em1; const double* em2;   /* nel*(p+1)^2 element 1-D masses (c == 1) */
+    const double* cg;                /* c at element Gauss points, (nel1*ng1) x (nel2*ng2); NULL: c == 1 */
+    const tq_ruleset* sets1; const tq_ruleset* sets2;
+    int32_t nsets1, nsets2;
+    const double* const* grids;      /* nsets1*nsets2 coefficient grids; NULL table: c == 1 */
+    const int32_t* cutidx;           /* nel1*nel2 -> cut element id, -1 */
+    const int64_t* cut_ptr;          /* ncut + 1 */
+    const double* cut_cw;            /* c * w per cut point */
+    const int32_t* cfirst1; const double* cvals1;
+    const int32_t* cfirst2; const double* cvals2;
+    const int32_t* desc;             /* nraw x 8: fidx, mode, set1, set2, a1, b1, a2, b2 */
+    int32_t nraw;
+    int32_t nmax1, nmax2;            /* max points of one rule row per direction */
+    double* raw;                     /* nraw x (2p1+1)(2p2+1) */
+} tq_rawctx;
+
+/* regular-support part of raw rows [r0, r1) (overwrites their blocks).
+ * Replaces sum_factor_row / _gauss_rows_by_element / _cut_regular_rows /
+ * the element loop of the reference strategy (src/assembly.py:218-252,
+ * 522-528, 553-648). */
+int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+
+/* cut-element part of raw rows [r0, r1) (accumulates).  Replaces
+ * _Run.add_cut_blocks (src/assembly.py:369-398). */
+int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+
+/* coefficient c = det J of a B-spline geometry map on a tensor grid / at
+ * points (the reference takes a host callable, src/assembly.py:54-85) */
+int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const double* x2, int32_t n2,
+                  double* out, void* stream);
+int tq_coeff_points(tq_coeff g, const double* pts, int64_t n, const double* w, double* out,
+                    void* stream);
 
 #ifdef __cplusplus
 }

@@ -306,11 +306,6 @@ class BezierTrim(Curve):
 
 # -- harness periodic cubic B-spline -----------------------------------------
 
-_UCB = np.array([[-1.0, 3.0, -3.0, 1.0],
-                 [3.0, -6.0, 3.0, 0.0],
-                 [-3.0, 0.0, 3.0, 0.0],
-                 [1.0, 4.0, 1.0, 0.0]]) / 6.0
-
 BISECT_ITERS = 64
 
 
@@ -353,7 +348,13 @@ class PeriodicBSplineTrim(Curve):
         m = self.m
         idx = (np.arange(m)[:, None] + np.arange(4)[None, :]) % m
         G = self.ctrl[idx]                       # (m, 4, 2)
-        self.pw = np.einsum("ij,kjd->kid", _UCB, G)  # (m, 4 coeffs, 2)
+        P0, P1, P2, P3 = G[:, 0], G[:, 1], G[:, 2], G[:, 3]
+        # power form of the uniform cubic B-spline segment, evaluated in this
+        # exact order by the CUDA classifier too (bit-identical coefficients)
+        self.pw = np.stack([(-P0 + 3.0 * P1 - 3.0 * P2 + P3) / 6.0,
+                            (3.0 * P0 - 6.0 * P1 + 3.0 * P2) / 6.0,
+                            (-3.0 * P0 + 3.0 * P2) / 6.0,
+                            (P0 + 4.0 * P1 + P2) / 6.0], axis=1)   # (m, 4 coeffs, 2)
         # shared vertex value at the start of each segment: coefficient d
         self.start = self.pw[:, 3, :].copy()
         # enclosed-area sign: positive = ccw

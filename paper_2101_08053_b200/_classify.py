@@ -1,0 +1,116 @@
+"""Curve descriptors -> tq_curve, GPU classification and host cut-cell rules."""
+
+from __future__ import annotations
+
+import ctypes as C
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+TQ_CURVE_LINE, TQ_CURVE_ARC, TQ_CURVE_CLOSED_CIRCLE, TQ_CURVE_BEZIER, TQ_CURVE_BSPLINE = 1, 2, 3, 4, 5
+
+
+def curve_array(curves):
+    """ctypes array of tq_curve with host data (kept alive by the return)."""
+    keep = []
+    arr = (L.Curve * max(len(curves), 1))()
+    for k, cv in enumerate(curves):
+        kind, m, data = cv.descriptor()
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        keep.append(data)
+        arr[k] = L.Curve(kind, m, data.ctypes.data_as(L.vp))
+    return arr, keep
+
+
+def classify_device(basis2d, curves):
+    b1, b2 = basis2d.dir
+    arr, keep = curve_array(curves)
+    ec = torch.empty((b1.num_elements, b2.num_elements), dtype=torch.int8, device=L.device())
+    status = torch.zeros(1, dtype=torch.int32, device=L.device())
+    fn = L.optional("tq_classify_elements", [C.POINTER(L.Curve), L.i32, L.Space1D, L.Space1D, L.vp, L.vp, L.vp])
+    L.call("tq_classify_elements", arr, len(curves), b1.device(), b2.device(), L.ptr(ec), L.ptr(status),
+           L.stream())
+    return ec
+
+
+@lru_cache(maxsize=None)
+def cell_tables(q):
+    """Lobatto nodes, Gauss rule on [0,1] and Lagrange tables, computed the
+    way the reference does (src/trimming.py:769-798)."""
+    if q == 1:
+        x = np.array([-1.0, 1.0])
+    else:
+        c = np.zeros(q + 1)
+        c[q] = 1.0
+        x = np.concatenate([[-1.0], np.polynomial.legendre.legroots(np.polynomial.legendre.legder(c)), [1.0]])
+    nodes = 0.5 * (x + 1.0)
+    gx, gw = np.polynomial.legendre.leggauss(q + 1)
+    xi, wx = 0.5 * (gx + 1.0), 0.5 * gw
+    V = np.vander(nodes, q + 1, increasing=True)
+    co = np.linalg.solve(V, np.eye(q + 1))
+    Lt = np.vander(xi, q + 1, increasing=True) @ co
+    dco = co[1:, :] * np.arange(1, q + 1)[:, None]
+    dLt = np.vander(xi, q, increasing=True) @ dco
+    return np.concatenate([nodes, xi, wx, Lt.ravel(), dLt.ravel()])
+
+
+class CutCellRule:
+    """Cut-element quadrature (src/trimming.py:749-766) with packed arrays."""
+
+    def __init__(self, q, elements, ptr, pts, wts, ncells):
+        self.q = q
+        self.elements = elements          # (ncut, 2) row-major element order
+        self.ptr = ptr                    # (ncut+1) int64
+        self.points = pts                 # (P, 2)
+        self.weights = wts                # (P,)
+        self.rules = {(int(e1), int(e2)): (pts[ptr[k]:ptr[k + 1]], wts[ptr[k]:ptr[k + 1]])
+                      for k, (e1, e2) in enumerate(elements)}
+        self.subcell_counts = {(int(e1), int(e2)): int(n) for (e1, e2), n in zip(elements, ncells)}
+
+    def element_rule(self, e1, e2):
+        return self.rules[(e1, e2)]
+
+    def total_points(self):
+        return int(self.ptr[-1])
+
+    def all_points(self):
+        return self.points
+
+
+def cut_cell_rule(config, q):
+    if q < 1:
+        raise ValueError("Lagrange degree q must be >= 1")
+    b1, b2 = config.basis2d.dir
+    e1, e2 = np.nonzero(config.element_class == 1)
+    el = np.ascontiguousarray(np.column_stack([e1, e2]).astype(np.int32))
+    arr, keep = curve_array(config.curves)
+    tabs = cell_tables(q)
+    bp1 = np.ascontiguousarray(b1.breakpoints, dtype=np.float64)
+    bp2 = np.ascontiguousarray(b2.breakpoints, dtype=np.float64)
+    lib = L.lib()
+    build = lib.tq_cutcell_build
+    build.argtypes = [C.POINTER(L.Curve), L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.i32, L.vp,
+                      C.POINTER(L.i32)]
+    build.restype = L.vp
+    st = L.i32(0)
+    h = build(arr, len(config.curves), bp1.ctypes.data_as(L.vp), b1.num_elements, bp2.ctypes.data_as(L.vp),
+              b2.num_elements, el.ctypes.data_as(L.vp), el.shape[0], q, tabs.ctypes.data_as(L.vp), C.byref(st))
+    if not h:
+        msg = lib.tq_last_error().decode(errors="replace")
+        raise L._EXC.get(st.value, RuntimeError)(msg)
+    lib.tq_cutcell_npoints.argtypes = [L.vp]
+    lib.tq_cutcell_npoints.restype = L.i64
+    npts = lib.tq_cutcell_npoints(h)
+    ptr = np.empty(el.shape[0] + 1, np.int64)
+    P = np.empty((npts, 2))
+    W = np.empty(npts)
+    nc = np.empty(el.shape[0], np.int32)
+    lib.tq_cutcell_copy.argtypes = [L.vp, L.vp, L.vp, L.vp, L.vp]
+    lib.tq_cutcell_copy(h, ptr.ctypes.data_as(L.vp), P.ctypes.data_as(L.vp), W.ctypes.data_as(L.vp),
+                        nc.ctypes.data_as(L.vp))
+    lib.tq_cutcell_free.argtypes = [L.vp]
+    lib.tq_cutcell_free(h)
+    return CutCellRule(q, el.astype(np.int64), ptr, P, W, nc)

@@ -1,10 +1,99 @@
-"""Raw (non-separable) rows: cut rows, c != 1 rows, the reference strategy."""
+"""Raw (non-separable) rows: orchestration of ``tq_raw_regular`` /
+``tq_raw_cutcells`` and of the DWQ routing.
+
+Which rows are raw (src/assembly.py:492-610):
+  * strategy ``reference``: every active row, element Gauss (GAUSS);
+  * c != 1 under wq/hybrid/dwq: interior rows by full-support sum
+    factorization over the standard rules (BOX with the full support box);
+  * cut rows: hybrid -> GAUSS; wq -> MASK (naive, masked sum factorization);
+    dwq -> BOX on the DWQ rule sets for eligible rows with a box, else GAUSS.
+Every raw row also collects the cut-element points (``tq_raw_cutcells``).
+"""
 
 from __future__ import annotations
 
-import numpy as np
+import ctypes as C
 
+import numpy as np
+import torch
+
+from . import _lib as L
 from ._lib import CUT, INTERIOR
+from .quadrature import build_dwq, gauss_legendre
+
+MODE_GAUSS, MODE_BOX, MODE_MASK = 0, 1, 2
+
+
+class RuleSetDev(C.Structure):
+    _fields_ = [("rules", L.Rules), ("lay", L.Layout), ("first", L.vp), ("vals", L.vp)]
+
+
+class RawCtx(C.Structure):
+    _fields_ = ([(k, L.i32) for k in ("n1", "n2", "p1", "p2", "nel1", "nel2")]
+                + [(k, L.vp) for k in ("el_first1", "el_last1", "el_first2", "el_last2", "ov_lo1", "ov_hi1",
+                                       "ov_lo2", "ov_hi2", "espan1", "espan2", "elem_class")]
+                + [("ng1", L.i32), ("ng2", L.i32)]
+                + [(k, L.vp) for k in ("ew1", "ev1", "ew2", "ev2", "em1", "em2", "cg", "sets1", "sets2")]
+                + [("nsets1", L.i32), ("nsets2", L.i32)]
+                + [(k, L.vp) for k in ("grids", "cutidx", "cut_ptr", "cut_cw", "cfirst1", "cvals1", "cfirst2",
+                                       "cvals2", "desc")]
+                + [("nraw", L.i32), ("nmax1", L.i32), ("nmax2", L.i32), ("raw", L.vp)])
+
+
+def _bind():
+    L.optional("tq_raw_regular", [RawCtx, L.i32, L.i32, L.vp])
+    L.optional("tq_raw_cutcells", [RawCtx, L.i32, L.i32, L.vp])
+    L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
+    L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
+    L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
+
+
+def cut_rows_host(f):
+    """Active cut functions in active (row-major) order -> function ids."""
+    fc = f.config.func_class.ravel()
+    act = f.active[: f.K].cpu().numpy()
+    return act[fc[act] == CUT].astype(np.int32)
+
+
+def route_cut_rows(f):
+    """DWQ routing on the GPU (src/trimming.py:545-586) -> (cut fids, routes)."""
+    _bind()
+    cut = cut_rows_host(f)
+    routes = np.full((cut.size, 8), -1, np.int32)
+    if cut.size:
+        u1, u2 = f.config.u_disc
+        du1 = L.dev(u1 if u1.size else np.zeros(1), torch.float64)
+        du2 = L.dev(u2 if u2.size else np.zeros(1), torch.float64)
+        rows = L.dev(cut, torch.int32)
+        out = torch.empty((cut.size, 8), dtype=torch.int32, device=f.dev)
+        L.call("tq_dwq_route", f.b1.device(), f.b2.device(), L.ptr(f.config.element_class_dev), L.ptr(du1),
+               u1.size, L.ptr(du2), u2.size, L.ptr(rows), cut.size, L.ptr(out), L.stream())
+        routes = out.cpu().numpy()
+    return cut, routes
+
+
+def build_dwq_sets(f, r1, r2):
+    """DWQ rule sets per (direction, u_disc) for eligible boxed cut rows
+    (src/assembly.py:460-488), fits on the GPU."""
+    cut, routes = route_cut_rows(f)
+    f._routes = (cut, routes)
+    needed = {}
+    n2 = f.b2.n
+    for fid, rt in zip(cut, routes):
+        if rt[0] != 1 or rt[3] < 0:
+            continue
+        ij = (int(fid) // n2, int(fid) % n2)
+        for d in (0, 1):
+            iu = rt[1 + d]
+            if iu >= 0:
+                needed.setdefault((d, float(f.config.u_disc[d][iu])), set()).add(ij[d])
+    dwq = {}
+    for key in sorted(needed):
+        d, u = key
+        basis = (f.b1, f.b2)[d]
+        base = (r1, r2)[d].layout
+        dwq[key] = build_dwq(basis, base, u, direction=d, only_rows=sorted(needed[key]))
+    return dwq
 
 
 def needs_raw(f):
@@ -13,10 +102,175 @@ def needs_raw(f):
     return bool(np.any(f.config.func_class == CUT))
 
 
-def build_dwq_sets(f, r1, r2):
-    return {}
+class _Setup:
+    """Device tables shared by the raw-row kernels of one formation."""
+
+    def __init__(self, f):
+        _bind()
+        self.keep = []
+        b1, b2 = f.b1, f.b2
+        cfg = f.config
+        dev = f.dev
+        self.f = f
+        # element Gauss tables, (p+1) points (src/assembly.py:198-211)
+        self.eg = []
+        for b in (b1, b2):
+            g = gauss_legendre(b.p + 1)
+            bp = b.breakpoints
+            mid, half = 0.5 * (bp[:-1] + bp[1:]), 0.5 * np.diff(bp)
+            X = mid[:, None] + half[:, None] * g.points[None, :]
+            Wt = half[:, None] * g.weights[None, :]
+            Xd = L.dev(X.ravel(), torch.float64)
+            _, vals = b.eval_device(Xd)
+            self.eg.append((X, L.dev(Wt.ravel(), torch.float64), vals, Xd))
+        self.cg = None
+        if not f.coeff.identity:
+            self.cg = f.coeff.grid_device(self.eg[0][3], self.eg[1][3])
+        # rule sets
+        self.sets = ([], [])
+        self.grids = None
+        if f.rules is not None:
+            r1, r2, dwq = f.rules
+            self.sets[0].append(r1)
+            self.sets[1].append(r2)
+            self.key_index = ({}, {})
+            for (d, u), rs in sorted(dwq.items()):
+                self.key_index[d][u] = len(self.sets[d])
+                self.sets[d].append(rs)
+            self.sets_dev = []
+            for d, b in enumerate((b1, b2)):
+                arr = (RuleSetDev * len(self.sets[d]))()
+                for k, rs in enumerate(self.sets[d]):
+                    first, vals = rs.basis_table()
+                    arr[k] = RuleSetDev(rs.device(), rs.layout.device(), L.ptr(first), L.ptr(vals))
+                t = torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(dev)
+                self.sets_dev.append(t)
+            self.nmax = []
+            for d, b in enumerate((b1, b2)):
+                m = 0
+                for rs in self.sets[d]:
+                    off = rs.layout.offsets
+                    m = max(m, int(np.max(off[b._el_last + 1] - off[b._el_first])))
+                self.nmax.append(m)
+            if not f.coeff.identity:
+                ptrs = np.zeros(len(self.sets[0]) * len(self.sets[1]), dtype=np.uint64)
+                for a, s1 in enumerate(self.sets[0]):
+                    for c, s2 in enumerate(self.sets[1]):
+                        g = f.coeff.grid_device(s1.layout.device_points(), s2.layout.device_points())
+                        self.keep.append(g)
+                        ptrs[a * len(self.sets[1]) + c] = g.data_ptr()
+                self.grids = torch.from_numpy(ptrs.view(np.int64)).to(dev)
+        else:
+            self.sets_dev = [None, None]
+            self.nmax = [1, 1]
+        # cut-element points (host C++ geometry, device basis tables)
+        self.cut = None
+        if cfg.cut_elements:
+            q = max(b1.p, b2.p)
+            rule = cfg.cut_cell_rule(q)
+            P = L.dev(rule.points.reshape(-1, 2), torch.float64)
+            Wd = L.dev(rule.weights, torch.float64)
+            f1, v1 = b1.eval_device(P[:, 0].contiguous())
+            f2, v2 = b2.eval_device(P[:, 1].contiguous())
+            cw = f.coeff.at_device(P) * Wd if not f.coeff.identity else Wd
+            cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
+            cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
+            self.cut = dict(idx=L.dev(cutidx, torch.int32), ptr=L.dev(rule.ptr, torch.int64), cw=cw.contiguous(),
+                            f1=f1, v1=v1, f2=f2, v2=v2, npts=rule.total_points())
+            f.report.n_cutcell_points = rule.total_points()
+
+    def ctx(self, desc, raw, nraw):
+        f = self.f
+        d1, d2 = f.b1.device_arrays(), f.b2.device_arrays()
+        cut = self.cut or {}
+        P = L.ptr
+        return RawCtx(f.b1.n, f.b2.n, f.b1.p, f.b2.p, f.b1.num_elements, f.b2.num_elements,
+                      P(d1["el_first"]), P(d1["el_last"]), P(d2["el_first"]), P(d2["el_last"]),
+                      P(d1["ov_lo"]), P(d1["ov_hi"]), P(d2["ov_lo"]), P(d2["ov_hi"]),
+                      P(d1["espan"]), P(d2["espan"]), P(f.config.element_class_dev),
+                      f.b1.p + 1, f.b2.p + 1,
+                      P(self.eg[0][1]), P(self.eg[0][2]), P(self.eg[1][1]), P(self.eg[1][2]), L.vp(0), L.vp(0),
+                      P(self.cg), P(self.sets_dev[0]), P(self.sets_dev[1]),
+                      len(self.sets[0]), len(self.sets[1]), P(self.grids),
+                      P(cut.get("idx")), P(cut.get("ptr")), P(cut.get("cw")), P(cut.get("f1")), P(cut.get("v1")),
+                      P(cut.get("f2")), P(cut.get("v2")), P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
+
+
+def _plan(f):
+    """Decide the raw rows and their descriptors (host, once per formation)."""
+    fc = f.config.func_class.ravel()
+    act = f.active[: f.K].cpu().numpy().astype(np.int64)
+    n2 = f.b2.n
+    is_cut = fc[act] == CUT
+    interior_raw = f.strategy == "reference" or not f.coeff.identity
+    rows_int = act[~is_cut] if interior_raw else np.empty(0, np.int64)
+    rows_cut = act[is_cut]
+    descs = []
+    # interior rows
+    if rows_int.size:
+        d = np.full((rows_int.size, 8), -1, np.int32)
+        d[:, 0] = rows_int
+        if f.strategy == "reference":
+            d[:, 1] = MODE_GAUSS
+        else:
+            i1, i2 = rows_int // n2, rows_int % n2
+            d[:, 1] = MODE_BOX
+            d[:, 2] = 0
+            d[:, 3] = 0
+            d[:, 4] = f.b1._el_first[i1]
+            d[:, 5] = f.b1._el_last[i1]
+            d[:, 6] = f.b2._el_first[i2]
+            d[:, 7] = f.b2._el_last[i2]
+        descs.append(d)
+    # cut rows
+    if rows_cut.size:
+        d = np.full((rows_cut.size, 8), -1, np.int32)
+        d[:, 0] = rows_cut
+        if f.strategy in ("reference", "hybrid"):
+            d[:, 1] = MODE_GAUSS
+        elif f.strategy == "wq":
+            d[:, 1] = MODE_MASK
+            d[:, 2] = 0
+            d[:, 3] = 0
+        else:  # dwq
+            cut, routes = f._routes
+            assert np.array_equal(cut, rows_cut)
+            setup = f._setup
+            for k, rt in enumerate(routes):
+                if rt[0] != 1 or rt[3] < 0:
+                    d[k, 1] = MODE_GAUSS
+                    continue
+                s = [0, 0]
+                for dd in (0, 1):
+                    if rt[1 + dd] >= 0:
+                        u = float(f.config.u_disc[dd][rt[1 + dd]])
+                        s[dd] = setup.key_index[dd][u]
+                d[k, 1:] = [MODE_BOX, s[0], s[1], rt[3], rt[4], rt[5], rt[6]]
+        descs.append(d)
+    desc = np.concatenate(descs) if descs else np.empty((0, 8), np.int32)
+    return desc, int(rows_int.size)
 
 
 def run_phase(f, phase):
-    if needs_raw(f):
-        raise NotImplementedError("raw rows not built yet")
+    if not needs_raw(f):
+        return
+    if phase == "interior":
+        f._setup = _Setup(f)
+        desc, nint = _plan(f)
+        f._nint = nint
+        f._ndesc = desc.shape[0]
+        f._desc = L.dev(desc, torch.int32)
+        W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
+        f.raw = torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64, device=f.dev)
+        slot = f.slot
+        slot[f._desc[:, 0].long()] = torch.arange(desc.shape[0], dtype=torch.int32, device=f.dev)
+        f.raw_list = f._desc[:, 0].contiguous()
+        f._ctx = f._setup.ctx(f._desc, f.raw, desc.shape[0])
+        if nint:
+            L.call("tq_raw_regular", f._ctx, 0, nint, L.stream())
+    elif phase == "cut":
+        if f._ndesc > f._nint:
+            L.call("tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
+    elif phase == "cutcells":
+        if f._setup.cut is not None:
+            L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())

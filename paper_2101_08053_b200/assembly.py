@@ -85,6 +85,42 @@ class CoefficientField:
         return L.dev(g, torch.float64)
 
 
+class GeometryMap:
+    """c = det J of a B-spline geometry map x(u,v) = sum N_i(u) N_j(v) P_ij,
+    evaluated on the GPU (``tq_coeff_grid`` / ``tq_coeff_points``).  Same
+    knot vector and degree in both directions; X, Y are (n, n) control nets."""
+
+    def __init__(self, knots, p, X, Y):
+        self.knots = np.ascontiguousarray(knots, dtype=float)
+        self.p = int(p)
+        self.X = np.ascontiguousarray(X, dtype=float)
+        self.Y = np.ascontiguousarray(Y, dtype=float)
+        self.n = self.X.shape[0]
+        self._dev = None
+
+    def device(self):
+        if self._dev is None:
+            from . import _rawrows
+            _rawrows._bind()
+            k, X, Y = (L.dev(a, torch.float64) for a in (self.knots, self.X.ravel(), self.Y.ravel()))
+            self._dev = (L.Coeff(1, self.p, self.n, L.ptr(k), L.ptr(X), L.ptr(Y)), (k, X, Y))
+        return self._dev[0]
+
+    def grid_device(self, x1, x2):
+        out = torch.empty((x1.numel(), x2.numel()), dtype=torch.float64, device=x1.device)
+        L.call("tq_coeff_grid", self.device(), L.ptr(x1), x1.numel(), L.ptr(x2), x2.numel(), L.ptr(out), L.stream())
+        return out
+
+    def at_device(self, P):
+        P = P.contiguous()
+        out = torch.empty(P.shape[0], dtype=torch.float64, device=P.device)
+        L.call("tq_coeff_points", self.device(), L.ptr(P), P.shape[0], L.vp(0), L.ptr(out), L.stream())
+        return out
+
+    def at_host(self, points):
+        return self.at_device(L.dev(np.atleast_2d(points), torch.float64)).cpu().numpy()
+
+
 class SparseMatrix:
     """Row-compressed symmetric mass matrix over the active functions
     (src/assembly.py:88-120).  ``device`` keeps the GPU CSR (indptr, indices,
@@ -204,6 +240,9 @@ class Formation:
                 from . import _rawrows
                 dwq = _rawrows.build_dwq_sets(self, r1, r2)
             rules = (r1, r2, dwq)
+        elif self.strategy == "dwq":
+            from . import _rawrows
+            self._routes = _rawrows.route_cut_rows(self)
         self.rules = rules
         self.report.n_wq_points = rules[0].layout.num_points + rules[1].layout.num_points
 
@@ -267,6 +306,8 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     """Run every formation phase on the device; returns (Formation, DeviceCSR)."""
     f = Formation(basis2d, config, coeff, strategy)
     rep = f.report
+    if config.cut_elements:   # shared geometry, outside the clock (src/assembly.py:505-508)
+        config.cut_cell_rule(max(basis2d.degrees))
     clk = _Clock()
     f.build_weights(rules)
     rep.t_weights = clk.lap()

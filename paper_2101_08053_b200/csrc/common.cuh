@@ -46,6 +46,16 @@ __host__ __device__ inline int upper_bound_d(const double* a, int n, double x) {
     return lo;
 }
 
+// searchsorted(a, x, side="right") on a sorted int array
+__host__ __device__ inline int upper_bound_d_int(const int32_t* a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 // searchsorted(a, x, side="left")
 __host__ __device__ inline int lower_bound_d(const double* a, int n, double x) {
     int lo = 0, hi = n;

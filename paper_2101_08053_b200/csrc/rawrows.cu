@@ -1,0 +1,316 @@
+// Subsystems (3)+(4): rows that are not separable -- cut rows (hybrid Gauss,
+// DWQ box + Gauss residual, naive masked WQ), rows with a coefficient c != 1,
+// and every row of the element-Gauss `reference` strategy.  Each row gets a
+// dense local block raw[r][(j1-i1+p1)*(2p2+1) + (j2-i2+p2)] (unsymmetrised
+// M_ij), consumed by the fused symmetrise/compact/CSR writer in rows.cu.
+//
+//  tq_raw_regular   <- sum_factor_row (src/assembly.py:218-252),
+//                      _Run.element_block (:310-332), _gauss_rows_by_element
+//                      (:623-643), _cut_regular_rows (:553-610), reference
+//                      strategy element loop (:522-528)
+//  tq_raw_cutcells  <- _Run.add_cut_blocks (:369-398)
+//  tq_coeff_grid / tq_coeff_points <- CoefficientField.grid / .at (:54-85)
+//                      for a B-spline geometry map (c = det J)
+//
+// One warp per row; the row block, the two weighted collocation slices and
+// the inner contraction live in shared memory.
+#include "common.cuh"
+
+namespace tq {
+
+struct RowDesc {
+    int fidx, mode, set1, set2, a1, b1, a2, b2;
+};
+
+__device__ inline double colloc_at(const tq_ruleset& s, int p, int k, int j) {
+    int r = j - s.first[k];
+    return (r >= 0 && r <= p) ? s.vals[(int64_t)k * (p + 1) + r] : 0.0;
+}
+
+// element of layout point k
+__device__ inline int elem_of_point(const tq_layout& lay, int k) {
+    return upper_bound_d_int(lay.offsets, lay.nel + 1, k) - 1;
+}
+
+// Gauss element-block entry (test local a, trial local b) of element (e1,e2)
+__device__ inline double gauss_entry(const tq_rawctx& c, int e1, int e2, int a1, int a2, int b1, int b2) {
+    const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+    if (!c.cg) {
+        // c == 1: the element block is the product of two 1-D element masses
+        double m1 = 0.0, m2 = 0.0;
+        for (int g = 0; g < c.ng1; ++g) {
+            const double* v = c.ev1 + ((int64_t)e1 * c.ng1 + g) * q1;
+            m1 += (v[a1] * v[b1]) * c.ew1[(int64_t)e1 * c.ng1 + g];
+        }
+        for (int g = 0; g < c.ng2; ++g) {
+            const double* v = c.ev2 + ((int64_t)e2 * c.ng2 + g) * q2;
+            m2 += (v[a2] * v[b2]) * c.ew2[(int64_t)e2 * c.ng2 + g];
+        }
+        return m1 * m2;
+    }
+    const int64_t ld = (int64_t)c.nel2 * c.ng2;
+    double acc = 0.0;
+    for (int g1 = 0; g1 < c.ng1; ++g1) {
+        const double* v1 = c.ev1 + ((int64_t)e1 * c.ng1 + g1) * q1;
+        double f1 = v1[a1] * v1[b1];
+        double w1 = c.ew1[(int64_t)e1 * c.ng1 + g1];
+        const double* cgr = c.cg + ((int64_t)e1 * c.ng1 + g1) * ld + (int64_t)e2 * c.ng2;
+        double part = 0.0;
+        for (int g2 = 0; g2 < c.ng2; ++g2) {
+            const double* v2 = c.ev2 + ((int64_t)e2 * c.ng2 + g2) * q2;
+            double cw = cgr[g2] * (w1 * c.ew2[(int64_t)e2 * c.ng2 + g2]);
+            part += (v2[a2] * v2[b2]) * cw;
+        }
+        acc += f1 * part;
+    }
+    return acc;
+}
+
+__global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
+    extern __shared__ double sm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
+    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * c.nmax1 + W1 + W2;
+    double* blk = sm + (size_t)wib * per;
+    double* B1 = blk + T;
+    double* B2 = B1 + c.nmax1 * W1;
+    double* inner = B2 + c.nmax2 * W2;
+    double* S1 = inner + W2 * c.nmax1;
+    double* S2 = S1 + W1;
+    const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+
+    for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
+        RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        for (int q = lane; q < T; q += 32) blk[q] = 0.0;
+        __syncwarp();
+        // -- element Gauss over interior support elements (GAUSS, BOX residual)
+        if (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX) {
+            for (int e1 = c.el_first1[i1]; e1 <= c.el_last1[i1]; ++e1) {
+                for (int e2 = c.el_first2[i2]; e2 <= c.el_last2[i2]; ++e2) {
+                    if (c.elem_class[(int64_t)e1 * c.nel2 + e2] != TQ_INTERIOR) continue;
+                    if (d.mode == TQ_ROW_BOX && d.a1 >= 0 && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2)
+                        continue;
+                    const int f1 = c.espan1[e1] - c.p1, f2 = c.espan2[e2] - c.p2;
+                    const int a1 = i1 - f1, a2 = i2 - f2;
+                    for (int q = lane; q < q1 * q2; q += 32) {
+                        int b1 = q / q2, b2 = q - (q / q2) * q2;
+                        double v = gauss_entry(c, e1, e2, a1, a2, b1, b2);
+                        blk[(f1 + b1 - i1 + c.p1) * W2 + (f2 + b2 - i2 + c.p2)] += v;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        // -- sum factorization (BOX, MASK)
+        if (d.mode == TQ_ROW_BOX || d.mode == TQ_ROW_MASK) {
+            const tq_ruleset s1 = c.sets1[d.set1];
+            const tq_ruleset s2 = c.sets2[d.set2];
+            const int k01 = s1.rules.k0[i1], k02 = s2.rules.k0[i2];
+            const int len1 = (int)(s1.rules.wptr[i1 + 1] - s1.rules.wptr[i1]);
+            const int len2 = (int)(s2.rules.wptr[i2 + 1] - s2.rules.wptr[i2]);
+            int lo1 = k01, hi1 = k01 + len1, lo2 = k02, hi2 = k02 + len2;
+            if (d.mode == TQ_ROW_BOX && d.a1 >= 0) {
+                lo1 = max(lo1, s1.lay.offsets[d.a1]);
+                hi1 = min(hi1, s1.lay.offsets[d.b1 + 1]);
+                lo2 = max(lo2, s2.lay.offsets[d.a2]);
+                hi2 = min(hi2, s2.lay.offsets[d.b2 + 1]);
+            }
+            const int n1 = hi1 - lo1, n2 = hi2 - lo2;
+            if (k01 >= 0 && k02 >= 0 && n1 > 0 && n2 > 0) {
+                const double* w1 = s1.rules.w + s1.rules.wptr[i1] + (lo1 - k01);
+                const double* w2 = s2.rules.w + s2.rules.wptr[i2] + (lo2 - k02);
+                const int jl1 = c.ov_lo1[i1], jh1 = c.ov_hi1[i1], jl2 = c.ov_lo2[i2], jh2 = c.ov_hi2[i2];
+                for (int q = lane; q < n1 * W1; q += 32) {
+                    int k = q / W1, o = q - (q / W1) * W1;
+                    int j = i1 - c.p1 + o;
+                    B1[q] = (j >= jl1 && j <= jh1) ? colloc_at(s1, c.p1, lo1 + k, j) * w1[k] : 0.0;
+                }
+                for (int q = lane; q < n2 * W2; q += 32) {
+                    int k = q / W2, o = q - (q / W2) * W2;
+                    int j = i2 - c.p2 + o;
+                    B2[q] = (j >= jl2 && j <= jh2) ? colloc_at(s2, c.p2, lo2 + k, j) * w2[k] : 0.0;
+                }
+                __syncwarp();
+                const double* G = c.grids ? c.grids[d.set1 * c.nsets2 + d.set2] : nullptr;
+                if (!G && d.mode == TQ_ROW_BOX) {
+                    // c == 1: the contraction factorizes into two 1-D sums
+                    for (int o = lane; o < W1; o += 32) {
+                        double acc = 0.0;
+                        for (int k = 0; k < n1; ++k) acc += B1[k * W1 + o];
+                        S1[o] = acc;
+                    }
+                    for (int o = lane; o < W2; o += 32) {
+                        double acc = 0.0;
+                        for (int k = 0; k < n2; ++k) acc += B2[k * W2 + o];
+                        S2[o] = acc;
+                    }
+                    __syncwarp();
+                    for (int q = lane; q < T; q += 32) {
+                        int o1 = q / W2, o2 = q - (q / W2) * W2;
+                        blk[q] += S1[o1] * S2[o2];
+                    }
+                } else {
+                    // inner[o2][k1] = sum_k2 B2[k2][o2] G[k1][k2] (mask)
+                    const int ld = s2.lay.npts;
+                    for (int q = lane; q < W2 * n1; q += 32) {
+                        int o2 = q / n1, k1 = q - (q / n1) * n1;
+                        int e1p = d.mode == TQ_ROW_MASK ? elem_of_point(s1.lay, lo1 + k1) : 0;
+                        double acc = 0.0;
+                        for (int k2 = 0; k2 < n2; ++k2) {
+                            double g = G ? G[(int64_t)(lo1 + k1) * ld + (lo2 + k2)] : 1.0;
+                            if (d.mode == TQ_ROW_MASK) {
+                                int e2p = elem_of_point(s2.lay, lo2 + k2);
+                                if (c.elem_class[(int64_t)e1p * c.nel2 + e2p] != TQ_INTERIOR) g = 0.0;
+                            }
+                            acc += B2[k2 * W2 + o2] * g;
+                        }
+                        inner[o2 * n1 + k1] = acc;
+                    }
+                    __syncwarp();
+                    for (int q = lane; q < T; q += 32) {
+                        int o1 = q / W2, o2 = q - (q / W2) * W2;
+                        double acc = 0.0;
+                        for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * n1 + k1];
+                        blk[q] += acc;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        double* dst = c.raw + (int64_t)r * T;
+        for (int q = lane; q < T; q += 32) dst[q] = blk[q];
+        __syncwarp();
+    }
+}
+
+__global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
+    extern __shared__ double sm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
+    double* blk = sm + (size_t)wib * T;
+    const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+    for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
+        RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const int ea1 = max(c.el_first1[i1] - 1, 0), eb1 = min(c.el_last1[i1] + 1, c.nel1 - 1);
+        const int ea2 = max(c.el_first2[i2] - 1, 0), eb2 = min(c.el_last2[i2] + 1, c.nel2 - 1);
+        bool any = false;
+        double* src = c.raw + (int64_t)r * T;
+        for (int e1 = ea1; e1 <= eb1; ++e1) {
+            for (int e2 = ea2; e2 <= eb2; ++e2) {
+                int id = c.cutidx[(int64_t)e1 * c.nel2 + e2];
+                if (id < 0) continue;
+                if (!any) {
+                    for (int q = lane; q < T; q += 32) blk[q] = src[q];
+                    __syncwarp();
+                    any = true;
+                }
+                for (int64_t pt = c.cut_ptr[id]; pt < c.cut_ptr[id + 1]; ++pt) {
+                    const int f1 = c.cfirst1[pt], f2 = c.cfirst2[pt];
+                    const int a1 = i1 - f1, a2 = i2 - f2;
+                    if (a1 < 0 || a1 > c.p1 || a2 < 0 || a2 > c.p2) continue;
+                    const double* v1 = c.cvals1 + pt * q1;
+                    const double* v2 = c.cvals2 + pt * q2;
+                    const double bi = v1[a1] * v2[a2];
+                    const double cw = c.cut_cw[pt];
+                    for (int q = lane; q < q1 * q2; q += 32) {
+                        int b1 = q / q2, b2 = q - (q / q2) * q2;
+                        blk[(f1 + b1 - i1 + c.p1) * W2 + (f2 + b2 - i2 + c.p2)] += bi * (cw * (v1[b1] * v2[b2]));
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (any) {
+            for (int q = lane; q < T; q += 32) src[q] = blk[q];
+            __syncwarp();
+        }
+    }
+}
+
+__device__ inline double detj(const tq_coeff& g, double u, double v) {
+    double N1[kMaxP + 1], D1[kMaxP + 1], N2[kMaxP + 1], D2[kMaxP + 1];
+    const int nk = g.n + g.p + 1;
+    int s1 = find_span(g.knots, nk, g.p, g.n, u), s2 = find_span(g.knots, nk, g.p, g.n, v);
+    basis_funs_ders_rt(g.knots, g.p, s1, u, N1, D1);
+    basis_funs_ders_rt(g.knots, g.p, s2, v, N2, D2);
+    double xu = 0, xv = 0, yu = 0, yv = 0;
+    for (int a = 0; a <= g.p; ++a)
+        for (int b = 0; b <= g.p; ++b) {
+            int64_t idx = (int64_t)(s1 - g.p + a) * g.n + (s2 - g.p + b);
+            double X = g.X[idx], Y = g.Y[idx];
+            xu += D1[a] * N2[b] * X;
+            xv += N1[a] * D2[b] * X;
+            yu += D1[a] * N2[b] * Y;
+            yv += N1[a] * D2[b] * Y;
+        }
+    return xu * yv - xv * yu;
+}
+
+__global__ void k_coeff_grid(tq_coeff g, const double* x1, int n1, const double* x2, int n2, double* out) {
+    int64_t total = (int64_t)n1 * n2;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int a = (int)(t / n2), b = (int)(t - (int64_t)a * n2);
+        out[t] = detj(g, x1[a], x2[b]);
+    }
+}
+
+__global__ void k_coeff_points(tq_coeff g, const double* P, int64_t n, const double* w, double* out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        double v = detj(g, P[2 * t], P[2 * t + 1]);
+        out[t] = w ? v * w[t] : v;
+    }
+}
+
+}  // namespace tq
+
+using namespace tq;
+
+static size_t regular_smem_per_warp(const tq_rawctx& c) {
+    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
+    return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * c.nmax1 + W1 + W2);
+}
+
+extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    if (r1 <= r0) return TQ_OK;
+    int wpb = 4;
+    size_t shm = regular_smem_per_warp(c) * wpb;
+    while (shm > 200 * 1024 && wpb > 1) { wpb /= 2; shm = regular_smem_per_warp(c) * wpb; }
+    if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_regular, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
+    k_raw_regular<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1);
+    TQ_LAUNCH_CHECK("k_raw_regular");
+    return TQ_OK;
+}
+
+extern "C" int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    if (r1 <= r0 || !c.cut_ptr) return TQ_OK;
+    int wpb = 4;
+    size_t shm = sizeof(double) * (2 * c.p1 + 1) * (2 * c.p2 + 1) * wpb;
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_cutcells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
+    k_raw_cutcells<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1);
+    TQ_LAUNCH_CHECK("k_raw_cutcells");
+    return TQ_OK;
+}
+
+extern "C" int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const double* x2, int32_t n2, double* out,
+                             void* stream) {
+    if ((int64_t)n1 * n2 == 0) return TQ_OK;
+    if (g.kind != TQ_COEFF_GEOMETRY || g.p > kMaxP) { set_error("unsupported coefficient field"); return TQ_EINVAL; }
+    k_coeff_grid<<<grid_for((int64_t)n1 * n2, 128), 128, 0, S(stream)>>>(g, x1, n1, x2, n2, out);
+    TQ_LAUNCH_CHECK("k_coeff_grid");
+    return TQ_OK;
+}
+
+extern "C" int tq_coeff_points(tq_coeff g, const double* pts, int64_t n, const double* w, double* out,
+                               void* stream) {
+    if (n == 0) return TQ_OK;
+    if (g.kind != TQ_COEFF_GEOMETRY || g.p > kMaxP) { set_error("unsupported coefficient field"); return TQ_EINVAL; }
+    k_coeff_points<<<grid_for(n, 128), 128, 0, S(stream)>>>(g, pts, n, w, out);
+    TQ_LAUNCH_CHECK("k_coeff_points");
+    return TQ_OK;
+}

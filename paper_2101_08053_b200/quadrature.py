@@ -386,3 +386,14 @@ def build_dwq(basis: Basis1D, layout: PointLayout, u_disc: float, direction=None
     L.call("tq_dwq_combine", L.ptr(rows), wanted.size, L.ptr(cp), L.ptr(ri), L.ptr(sv),
            L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(wptr), L.ptr(k0), L.ptr(w)), L.stream())
     return DiscontinuousRuleSet(basis, aug, wptr, k0, w, u, S, refined, layout, direction, regular_side)
+
+
+def rules_from_arrays(basis, points, offsets, k0, wptr, w, direction=None, u_disc=None):
+    """Import a weight table computed elsewhere (WQ weights are not
+    unique, so c != 1 parity compares against the same weights)."""
+    lay = PointLayout(basis.breakpoints, points=np.asarray(points, float), offsets=np.asarray(offsets, np.int64))
+    args = (basis, lay, L.dev(np.asarray(wptr, np.int64), torch.int64), L.dev(np.asarray(k0, np.int32), torch.int32),
+            L.dev(np.asarray(w, float) if len(w) else np.zeros(1), torch.float64))
+    if u_disc is None:
+        return WeightedRuleSet(*args, direction=direction)
+    return DiscontinuousRuleSet(*args, u_disc, None, None, None, direction=direction)

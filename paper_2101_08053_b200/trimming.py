@@ -108,12 +108,160 @@ class TrimConfiguration:
         a2, b2 = self.basis2d.dir[1].support_elements(i2)
         return a1, b1, a2, b2
 
+    def cut_cell_rule(self, q, cache=True):
+        """Cut-element quadrature, host-native C++ (src/trimming.py:588-594,1084-1111)."""
+        if cache and q in self._cut_rules:
+            return self._cut_rules[q]
+        from . import _classify
+        rule = _classify.cut_cell_rule(self, q)
+        if cache:
+            self._cut_rules[q] = rule
+        return rule
+
     def support_split(self, i1, i2):
         a1, b1, a2, b2 = self.support_block(i1, i2)
         blk = self.element_class[a1: b1 + 1, a2: b2 + 1]
         reg = [(a1 + r, a2 + c) for r, c in zip(*np.nonzero(blk == INTERIOR))]
         cut = [(a1 + r, a2 + c) for r, c in zip(*np.nonzero(blk == CUT))]
         return reg, cut
+
+
+# ---------------------------------------------------------------------------
+# trimming curves: descriptors for the device classifier / host decomposition
+# (src/trimming.py:69-351 and the harness closed curves, SURVEY F3/F5)
+# ---------------------------------------------------------------------------
+
+class TrimmingCurve:
+    """Oriented curve; the valid domain lies to the left (src/trimming.py:69-95)."""
+    straight = False
+    closed = False
+
+    def sample(self, n=257):
+        return self.evaluate(np.linspace(0.0, 1.0, n))
+
+    def descriptor(self):
+        raise NotImplementedError
+
+
+class LineTrim(TrimmingCurve):
+    """src/trimming.py:98-134."""
+    straight = True
+
+    def __init__(self, p0, p1):
+        self.p0 = np.asarray(p0, dtype=float)
+        self.p1 = np.asarray(p1, dtype=float)
+        self.d = self.p1 - self.p0
+        if np.hypot(*self.d) == 0.0:
+            raise ValueError("degenerate line segment")
+
+    def evaluate(self, t):
+        return self.p0 + np.multiply.outer(np.asarray(t, dtype=float), self.d)
+
+    def derivative(self, t):
+        t = np.asarray(t, dtype=float)
+        return np.broadcast_to(self.d, t.shape + (2,)).copy()
+
+    def descriptor(self):
+        return 1, 0, np.array([*self.p0, *self.p1])
+
+
+class CircleTrim(TrimmingCurve):
+    """Circular arc theta0 -> theta1 (src/trimming.py:137-201)."""
+
+    def __init__(self, center, radius, theta0=0.0, theta1=0.5 * np.pi):
+        self.center = np.asarray(center, dtype=float)
+        self.radius = float(radius)
+        self.theta0, self.theta1 = float(theta0), float(theta1)
+        if self.radius <= 0 or self.theta0 == self.theta1:
+            raise ValueError("degenerate circular arc")
+
+    def _th(self, t):
+        return self.theta0 + np.asarray(t, dtype=float) * (self.theta1 - self.theta0)
+
+    def evaluate(self, t):
+        th = self._th(t)
+        return self.center + self.radius * np.stack([np.cos(th), np.sin(th)], axis=-1)
+
+    def derivative(self, t):
+        th = self._th(t)
+        return self.radius * (self.theta1 - self.theta0) * np.stack([-np.sin(th), np.cos(th)], axis=-1)
+
+    def descriptor(self):
+        return 2, 0, np.array([*self.center, self.radius, self.theta0, self.theta1])
+
+
+class ClosedCircleTrim(CircleTrim):
+    """Full circle with a movable seam; ccw keeps the disc (harness)."""
+    closed = True
+
+    def __init__(self, center, radius, ccw=False, seam=np.pi):
+        self.ccw = bool(ccw)
+        self.seam = float(seam)
+        s = 1.0 if ccw else -1.0
+        super().__init__(center, radius, seam, seam + s * 2.0 * np.pi)
+
+    def descriptor(self):
+        return 3, 0, np.array([*self.center, self.radius, 1.0 if self.ccw else 0.0, self.seam,
+                               self.theta1 - self.theta0])
+
+
+class PeriodicBSplineTrim(TrimmingCurve):
+    """Closed uniform periodic cubic B-spline (harness); valid
+    side to the left of the control-polygon orientation."""
+    closed = True
+
+    def __init__(self, ctrl, shift=0.0):
+        self.ctrl = np.asarray(ctrl, dtype=float)
+        self.m = self.ctrl.shape[0]
+        self.shift = float(shift) % 1.0
+        P = self.ctrl
+        self.ccw = float(np.sum(P[:, 0] * np.roll(P[:, 1], -1) - np.roll(P[:, 0], -1) * P[:, 1])) > 0
+
+    def _pw(self):
+        m = self.m
+        G = self.ctrl[(np.arange(m)[:, None] + np.arange(4)[None, :]) % m]
+        P0, P1, P2, P3 = G[:, 0], G[:, 1], G[:, 2], G[:, 3]
+        return np.stack([(-P0 + 3.0 * P1 - 3.0 * P2 + P3) / 6.0, (3.0 * P0 - 6.0 * P1 + 3.0 * P2) / 6.0,
+                         (-3.0 * P0 + 3.0 * P2) / 6.0, (P0 + 4.0 * P1 + P2) / 6.0], axis=1)
+
+    def _seg(self, t):
+        s = ((np.asarray(t, dtype=float) + self.shift) % 1.0) * self.m
+        k = np.minimum(np.floor(s).astype(np.int64), self.m - 1)
+        return k, s - k
+
+    def evaluate(self, t):
+        k, u = self._seg(t)
+        c = self._pw()[k]
+        u = np.asarray(u)[..., None]
+        return ((c[..., 0, :] * u + c[..., 1, :]) * u + c[..., 2, :]) * u + c[..., 3, :]
+
+    def derivative(self, t):
+        k, u = self._seg(t)
+        c = self._pw()[k]
+        u = np.asarray(u)[..., None]
+        return self.m * ((3.0 * c[..., 0, :] * u + 2.0 * c[..., 1, :]) * u + c[..., 2, :])
+
+    def descriptor(self):
+        return 5, self.m, np.concatenate([[self.shift, 1.0 if self.ccw else 0.0], self.ctrl.ravel()])
+
+
+class BezierTrim(TrimmingCurve):
+    """Cubic Bezier trimming curve (src/trimming.py:204-351).  Not yet on the
+    device classifier (round-2 item); construction is supported."""
+
+    def __init__(self, control_points, anchors=((0.05, 0.05), (0.08, 0.03), (0.03, 0.09))):
+        self.ctrl = np.asarray(control_points, dtype=float)
+        if self.ctrl.shape != (4, 2):
+            raise ValueError("cubic Bezier needs 4 control points")
+        self.anchors = [np.asarray(a, dtype=float) for a in anchors]
+
+    def evaluate(self, t):
+        c0, c1, c2, c3 = self.ctrl
+        tt = np.asarray(t, dtype=float)[..., None]
+        return (1 - tt) ** 3 * c0 + 3 * (1 - tt) ** 2 * tt * c1 + 3 * (1 - tt) * tt ** 2 * c2 + tt ** 3 * c3
+
+    def descriptor(self):
+        raise NotImplementedError("BezierTrim is not on the device classification path yet")
 
 
 def classify_elements(basis2d: TensorBasis2D, curves) -> TrimConfiguration:
