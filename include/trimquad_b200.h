@@ -243,6 +243,48 @@ int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const double* x2, in
 int tq_coeff_points(tq_coeff g, const double* pts, int64_t n, const double* w, double* out,
                     void* stream);
 
+/* ---- L2 projection: RHS and error ---------------------------------------- */
+
+/* target f(x, y): kind 0 = values on the Gauss tensor grid (grid[r1*ld + r2]);
+ * kind 1 = sum_k terms[7k] * phi(terms[7k+1], terms[7k+2] x + terms[7k+3])
+ *                        * phi(terms[7k+4], terms[7k+5] y + terms[7k+6]),
+ * phi kinds 0 = 1, 1 = sin, 2 = cos, 3 = exp (evaluated in-kernel) */
+typedef struct {
+    int32_t kind, nterms;
+    const double* terms;
+    const double* grid;
+    int64_t ld;
+} tq_target;
+
+typedef struct {
+    int32_t n1, n2, p1, p2, nel1, nel2;
+    const int32_t* el_first1; const int32_t* el_last1;
+    const int32_t* el_first2; const int32_t* el_last2;
+    const int32_t* espan1; const int32_t* espan2;
+    const int8_t* elem_class;
+    int32_t g1n, g2n;                /* Gauss points per element (p+2 RHS, p+3 error) */
+    const double* x1; const double* w1; const double* v1;   /* nel*g, nel*g, nel*g*(p+1) */
+    const double* x2; const double* w2; const double* v2;
+    const double* cgrid; int64_t cld;   /* c on the Gauss tensor grid, NULL: c == 1 */
+    tq_target target;
+    const int32_t* active;
+    int32_t row_begin, row_end;
+    const int32_t* cutidx; const int64_t* cut_ptr;
+    const double* cut_fcw;           /* f c w per cut point (RHS) */
+    const double* cut_w;             /* w per cut point (error) */
+    const int32_t* cfirst1; const double* cvals1;
+    const int32_t* cfirst2; const double* cvals2;
+} tq_projctx;
+
+/* b over active rows [row_begin, row_end) (T: scratch (nel1*g1n) x n2). */
+int tq_rhs(tq_projctx c, double* T, const int32_t* cut_rows, int32_t ncut, double* b, void* stream);
+int tq_target_points(tq_target f, const double* P, const double* w, int64_t n, double* out, void* stream);
+/* (num, den) of the relative L2 error over interior elements [e_begin, e_end)
+ * (row-major ids) and cut points [p_begin, p_end); C is the n1 x n2
+ * coefficient grid (zeros off the active set). */
+int tq_l2_parts(tq_projctx c, const double* C, int64_t e_begin, int64_t e_end, int64_t p_begin,
+                int64_t p_end, const double* fpts, double* num_den, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

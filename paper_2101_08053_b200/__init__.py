@@ -16,4 +16,7 @@ from .trimming import ElementClass, TrimConfiguration, TrimmingConfigurationErro
 from .assembly import (STRATEGIES, CoefficientField, FormationReport, SparseMatrix, assemble_mass,
                        form_with_timings, sum_factor_op_count)
 
+from .projection import (ConditioningError, ProjectionProblem, SeparableTarget, assemble_rhs, default_target,
+                         l2_error, project, solve_spd)
+
 __version__ = "0.1.0"

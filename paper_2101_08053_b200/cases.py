@@ -16,6 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .assembly import CoefficientField, GeometryMap
+from .projection import SeparableTarget
 from .splines import Basis1D, TensorBasis2D, make_uniform_knots
 from .trimming import (BezierTrim, CircleTrim, ClosedCircleTrim, LineTrim, PeriodicBSplineTrim,
                        classify_elements)
@@ -87,16 +88,10 @@ def geometry_map(rng, nel=8, p=3, sigma=0.01):
     return GeometryMap(kn, p, X, Y)
 
 
-def f_config1(P):
-    return np.sin(2 * np.pi * P[:, 0]) * np.sin(2 * np.pi * P[:, 1])
-
-
-def f_config23(P):
-    return np.exp(P[:, 0] + P[:, 1])
-
-
-def f_config5(P):
-    return np.sin(2 * np.pi * P[:, 0]) * np.cos(3 * np.pi * P[:, 1])
+# BASELINE targets as device-evaluable separable forms
+f_config1 = SeparableTarget([(1.0, "sin", 2 * np.pi, 0.0, "sin", 2 * np.pi, 0.0)])
+f_config23 = SeparableTarget([(1.0, "exp", 1.0, 0.0, "exp", 1.0, 0.0)])
+f_config5 = SeparableTarget([(1.0, "sin", 2 * np.pi, 0.0, "cos", 3 * np.pi, 0.0)])
 
 
 def baseline_config(idx, seed=0, p=None, nel=None):

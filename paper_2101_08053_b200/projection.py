@@ -1,0 +1,304 @@
+"""L2 projection onto trimmed spline spaces: GPU RHS and error reduction.
+
+Drop-in for ``trimquad.projection`` (src/projection.py:27-331).
+``assemble_rhs`` and ``l2_error`` run on the GPU (``tq_rhs``,
+``tq_l2_parts``); targets given as ``SeparableTarget`` are evaluated inside
+the kernels, any other callable is evaluated on the host at the quadrature
+points and uploaded.  ``solve_spd`` is the reference's Jacobi-scaled
+Cholesky/CG (out of scope of the v1 GPU path).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import warnings
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+import torch
+
+from . import _lib as L
+from ._lib import CUT, INTERIOR
+from .assembly import CoefficientField, SparseMatrix, assemble_mass
+from .quadrature import gauss_legendre
+
+CONDITION_GUARD = 1e12   # src/projection.py:41
+DIRECT_LIMIT = 6000      # src/projection.py:44
+
+
+class ConditioningError(RuntimeError):
+    """src/projection.py:47-48."""
+
+
+_KIND = {"1": 0, "const": 0, "sin": 1, "cos": 2, "exp": 3}
+_NP = {0: lambda t: np.ones_like(t), 1: np.sin, 2: np.cos, 3: np.exp}
+
+
+class SeparableTarget:
+    """f(x, y) = sum_k c_k phi_k(a_k x + b_k) psi_k(d_k y + e_k), phi, psi in
+    {1, sin, cos, exp}: evaluated inside the GPU kernels.  Callable like the
+    reference's targets ((N,2) -> (N,))."""
+
+    def __init__(self, terms):
+        rows = []
+        for (coef, fx, ax, bx, fy, ay, by) in terms:
+            rows.append([coef, _KIND[fx], ax, bx, _KIND[fy], ay, by])
+        self.terms = np.asarray(rows, dtype=float)
+
+    def __call__(self, P):
+        P = np.atleast_2d(P)
+        out = np.zeros(P.shape[0])
+        for c, kx, ax, bx, ky, ay, by in self.terms:
+            out += c * _NP[int(kx)](ax * P[:, 0] + bx) * _NP[int(ky)](ay * P[:, 1] + by)
+        return out
+
+
+default_target = SeparableTarget([(1.0, "sin", 2.0, 0.0, "cos", 3.0, 0.0)])   # src/projection.py:51-54
+
+
+class ProjCtx(C.Structure):
+    _fields_ = ([(k, L.i32) for k in ("n1", "n2", "p1", "p2", "nel1", "nel2")]
+                + [(k, L.vp) for k in ("el_first1", "el_last1", "el_first2", "el_last2", "espan1", "espan2",
+                                       "elem_class")]
+                + [("g1n", L.i32), ("g2n", L.i32)]
+                + [(k, L.vp) for k in ("x1", "w1", "v1", "x2", "w2", "v2", "cgrid")]
+                + [("cld", L.i64)]
+                + [("t_kind", L.i32), ("t_nterms", L.i32), ("t_terms", L.vp), ("t_grid", L.vp), ("t_ld", L.i64)]
+                + [("active", L.vp), ("row_begin", L.i32), ("row_end", L.i32)]
+                + [(k, L.vp) for k in ("cutidx", "cut_ptr", "cut_fcw", "cut_w", "cfirst1", "cvals1", "cfirst2",
+                                       "cvals2")])
+
+
+class TargetStruct(C.Structure):
+    _fields_ = [("kind", L.i32), ("nterms", L.i32), ("terms", L.vp), ("grid", L.vp), ("ld", L.i64)]
+
+
+def _bind():
+    L.optional("tq_rhs", [ProjCtx, L.vp, L.vp, L.i32, L.vp, L.vp])
+    L.optional("tq_target_points", [TargetStruct, L.vp, L.vp, L.i64, L.vp, L.vp])
+    L.optional("tq_l2_parts", [ProjCtx, L.vp, L.i64, L.i64, L.i64, L.i64, L.vp, L.vp, L.vp])
+
+
+@dataclass
+class ProjectionProblem:
+    """src/projection.py:57-68."""
+    target: Callable
+    basis2d: object
+    config: object
+    strategy: str = "reference"
+    coeff: CoefficientField | None = None
+
+    def field(self):
+        return self.coeff or CoefficientField()
+
+
+class _Tables:
+    """Per-direction element Gauss tables with p + n_extra points, on the
+    device (src/projection.py:83-98)."""
+
+    def __init__(self, basis2d, n_extra):
+        self.dirs = []
+        for b in basis2d.dir:
+            g = gauss_legendre(b.p + n_extra)
+            bp = b.breakpoints
+            mid, half = 0.5 * (bp[:-1] + bp[1:]), 0.5 * np.diff(bp)
+            X = mid[:, None] + half[:, None] * g.points[None, :]
+            W = half[:, None] * g.weights[None, :]
+            Xd = L.dev(X.ravel(), torch.float64)
+            _, V = b.eval_device(Xd)
+            self.dirs.append((X, Xd, L.dev(W.ravel(), torch.float64), V, g.points.size))
+
+
+def _target_desc(target, tabs, keep):
+    """(kind, nterms, terms, grid, ld) for the kernels."""
+    if isinstance(target, SeparableTarget):
+        t = L.dev(target.terms.ravel(), torch.float64)
+        keep.append(t)
+        return 1, target.terms.shape[0], L.ptr(t), L.vp(0), 0
+    X1, X2 = tabs.dirs[0][0].ravel(), tabs.dirs[1][0].ravel()
+    P = np.column_stack([np.repeat(X1, X2.size), np.tile(X2, X1.size)])
+    g = L.dev(np.asarray(target(P), float), torch.float64)
+    keep.append(g)
+    return 0, 0, L.vp(0), L.ptr(g), X2.size
+
+
+def _target_points(target, P_dev, keep):
+    if isinstance(target, SeparableTarget):
+        t = L.dev(target.terms.ravel(), torch.float64)
+        keep.append(t)
+        out = torch.empty(P_dev.shape[0], dtype=torch.float64, device=P_dev.device)
+        L.call("tq_target_points", TargetStruct(1, target.terms.shape[0], L.ptr(t), L.vp(0), 0), L.ptr(P_dev),
+               L.vp(0), P_dev.shape[0], L.ptr(out), L.stream())
+        return out
+    return L.dev(np.asarray(target(P_dev.cpu().numpy()), float), torch.float64)
+
+
+class _CutPoints:
+    def __init__(self, config, basis2d):
+        b1, b2 = basis2d.dir
+        rule = config.cut_cell_rule(max(basis2d.degrees))
+        self.rule = rule
+        self.P = L.dev(rule.points.reshape(-1, 2), torch.float64).contiguous()
+        self.W = L.dev(rule.weights, torch.float64)
+        self.f1, self.v1 = b1.eval_device(self.P[:, 0].contiguous())
+        self.f2, self.v2 = b2.eval_device(self.P[:, 1].contiguous())
+        cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
+        cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
+        self.idx = L.dev(cutidx, torch.int32)
+        self.ptr = L.dev(rule.ptr, torch.int64)
+        self.n = rule.total_points()
+
+
+def _ctx(basis2d, config, tabs, tdesc, active, rb, re_, cgrid=None, cut=None, fcw=None):
+    b1, b2 = basis2d.dir
+    d1, d2 = b1.device_arrays(), b2.device_arrays()
+    (_, X1, W1, V1, g1), (_, X2, W2, V2, g2) = tabs.dirs
+    P = L.ptr
+    kind, nterms, terms, grid, ld = tdesc
+    return ProjCtx(b1.n, b2.n, b1.p, b2.p, b1.num_elements, b2.num_elements,
+                   P(d1["el_first"]), P(d1["el_last"]), P(d2["el_first"]), P(d2["el_last"]),
+                   P(d1["espan"]), P(d2["espan"]), P(config.element_class_dev), g1, g2,
+                   P(X1), P(W1), P(V1), P(X2), P(W2), P(V2), P(cgrid), X2.numel(),
+                   kind, nterms, terms, grid, ld, P(active), rb, re_,
+                   P(cut.idx if cut else None), P(cut.ptr if cut else None), P(fcw),
+                   P(cut.W if cut else None), P(cut.f1 if cut else None), P(cut.v1 if cut else None),
+                   P(cut.f2 if cut else None), P(cut.v2 if cut else None))
+
+
+def assemble_rhs_device(problem: ProjectionProblem, row_range=None):
+    """Load vector on the device over active rows (src/projection.py:101-145)."""
+    _bind()
+    basis2d, config = problem.basis2d, problem.config
+    coeff = problem.field()
+    idx, _ = config.active_index()
+    K = idx["K"]
+    rb, re_ = (0, K) if row_range is None else row_range
+    tabs = _Tables(basis2d, 2)
+    keep = []
+    tdesc = _target_desc(problem.target, tabs, keep)
+    cgrid = None if coeff.identity else coeff.grid_device(tabs.dirs[0][1], tabs.dirs[1][1])
+    cut = fcw = None
+    cut_rows = torch.empty(0, dtype=torch.int32, device=L.device())
+    if config.cut_elements:
+        cut = _CutPoints(config, basis2d)
+        fcw = _target_points(problem.target, cut.P, keep) * cut.W
+        if not coeff.identity:
+            fcw = fcw * coeff.at_device(cut.P)
+        act = idx["active"][rb:re_]
+        is_cut = config.func_class_dev.view(-1)[act.long()] == CUT
+        cut_rows = (torch.nonzero(is_cut).view(-1).to(torch.int32) + rb).contiguous()
+    b1, b2 = basis2d.dir
+    T = torch.empty((b1.num_elements * tabs.dirs[0][4], b2.n), dtype=torch.float64, device=L.device())
+    b = torch.empty(max(re_ - rb, 1), dtype=torch.float64, device=L.device())
+    ctx = _ctx(basis2d, config, tabs, tdesc, idx["active"], rb, re_, cgrid, cut, fcw)
+    L.call("tq_rhs", ctx, L.ptr(T), L.ptr(cut_rows), cut_rows.numel(), L.ptr(b), L.stream())
+    return b[: re_ - rb]
+
+
+def assemble_rhs(problem: ProjectionProblem) -> np.ndarray:
+    """src/projection.py:101-145 on the GPU; returns the host vector."""
+    return assemble_rhs_device(problem).cpu().numpy()
+
+
+def l2_error_parts_device(coeffs_dev, problem, elem_range=None, point_range=None):
+    """(num, den) device pair over an element range / cut-point range."""
+    _bind()
+    basis2d, config = problem.basis2d, problem.config
+    b1, b2 = basis2d.dir
+    idx, _ = config.active_index()
+    K = idx["K"]
+    Cg = torch.zeros(b1.n * b2.n, dtype=torch.float64, device=L.device())
+    Cg[idx["active"][:K].long()] = coeffs_dev
+    tabs = _Tables(basis2d, 3)
+    keep = []
+    tdesc = _target_desc(problem.target, tabs, keep)
+    cut = fpts = None
+    if config.cut_elements:
+        cut = _CutPoints(config, basis2d)
+        fpts = _target_points(problem.target, cut.P, keep)
+    ne = b1.num_elements * b2.num_elements
+    eb, ee = (0, ne) if elem_range is None else elem_range
+    pb, pe = (0, cut.n if cut else 0) if point_range is None else point_range
+    out = torch.zeros(2, dtype=torch.float64, device=L.device())
+    ctx = _ctx(basis2d, config, tabs, tdesc, idx["active"], 0, K, None, cut, None)
+    L.call("tq_l2_parts", ctx, L.ptr(Cg), eb, ee, pb, pe, L.ptr(fpts), L.ptr(out), L.stream())
+    return out
+
+
+def l2_error(coeffs, problem: ProjectionProblem, active=None) -> float:
+    """Relative L2 error (src/projection.py:221-260), reduced on the GPU."""
+    basis2d, config = problem.basis2d, problem.config
+    if active is not None and not np.array_equal(np.asarray(active), config.active_functions()):
+        raise ValueError("coefficients must be ordered like config.active_functions()")
+    nd = l2_error_parts_device(L.dev(np.asarray(coeffs, float), torch.float64), problem).cpu().numpy()
+    if nd[1] <= 0.0:
+        raise ValueError("target function has zero norm on the valid region")
+    return math.sqrt(nd[0] / nd[1])
+
+
+def solve_spd(M, b, guard=CONDITION_GUARD, stats=None):
+    """Jacobi-scaled dense Cholesky (n <= 6000) or CG to 1e-13
+    (src/projection.py:148-211), host-side as in the reference."""
+    A = M.data if isinstance(M, SparseMatrix) else sp.csr_matrix(M)
+    b = np.asarray(b, dtype=float)
+    n = A.shape[0]
+    d = A.diagonal()
+    if np.any(d <= 0.0):
+        raise ValueError("matrix is not positive definite (non-positive diagonal)")
+    s = 1.0 / np.sqrt(d)
+    As = sp.diags(s) @ A @ sp.diags(s)
+    bs = s * b
+    cond = math.nan
+    if n <= DIRECT_LIMIT:
+        D = As.toarray()
+        D = 0.5 * (D + D.T)
+        try:
+            cho = scipy.linalg.cho_factor(D, lower=True, check_finite=False)
+        except scipy.linalg.LinAlgError as err:
+            raise ValueError("matrix is not positive definite") from err
+        solve = lambda r: scipy.linalg.cho_solve(cho, r, check_finite=False)
+        op = spla.LinearOperator((n, n), matvec=solve, rmatvec=solve)
+        cond = float(spla.onenormest(op) * spla.onenormest(As))
+    else:
+        def solve(r):
+            x, info = spla.cg(As, r, rtol=1e-14, atol=0.0, maxiter=10 * n)
+            if info > 0:
+                x = x + spla.cg(As, r - As @ x, rtol=1e-10, atol=0.0, maxiter=n)[0]
+            return x
+    y = solve(bs)
+    bn = np.linalg.norm(bs) or 1.0
+    for _ in range(4):
+        r = bs - As @ y
+        if np.linalg.norm(r) <= 1e-14 * bn:
+            break
+        y = y + solve(r)
+    x = s * y
+    resid = np.linalg.norm(A @ x - b) / (np.linalg.norm(b) or 1.0)
+    if stats is not None:
+        stats["condition"] = cond
+        stats["residual"] = resid
+    if np.isfinite(cond) and cond > guard:
+        warnings.warn(f"scaled mass matrix condition estimate {cond:.2e} exceeds guard {guard:.0e}",
+                      RuntimeWarning, stacklevel=2)
+    if resid > 1e-13:
+        raise RuntimeError(f"solver residual {resid:.2e} above 1e-13")
+    return x
+
+
+def project(problem: ProjectionProblem, parallel=False, stats=None):
+    """Assemble (GPU), solve, return (x, M, b) (src/projection.py:263-279)."""
+    M = assemble_mass(problem.basis2d, problem.config, problem.coeff, strategy=problem.strategy)
+    b = assemble_rhs(problem)
+    local = {}
+    x = solve_spd(M, b, stats=local)
+    if stats is not None:
+        stats.update(local)
+    cond = local.get("condition", math.nan)
+    if np.isfinite(cond) and cond > CONDITION_GUARD:
+        raise ConditioningError(f"condition estimate {cond:.2e} above guard {CONDITION_GUARD:.0e}")
+    return x, M, b
