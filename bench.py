@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Headline benchmark: FP64 mass-matrix nonzeros formed per second.
+
+Workload (BASELINE.json config 5, the row-sharded configuration): unit square
+trimmed by the seeded periodic cubic B-spline (24 control points, seed 0),
+p = 4, 2048 x 2048 elements, c == 1, DWQ strategy, FP64; synthetic inputs.
+
+One step = one full formation pass on the GPU (the analogue of the
+reference's ``form_with_timings`` t_total: WQ/DWQ weights, DWQ routing,
+sum-factorized interior rows, cut rows, cut-cell rows, and the fused
+symmetrise / zero-drop / CSR write), with the classification and the
+cut-cell geometry resident beforehand (the reference also keeps them outside
+its clock, src/assembly.py:651-665).  Rows are sharded in contiguous blocks
+across ranks; no collective runs inside the formation.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "FP64 mass-matrix nonzeros formed/sec"
+UNIT = "nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nel", type=int, default=2048)
+    ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--strategy", default="dwq")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-nel", type=int, default=512, help="oracle sample size (mesh) for the CPU legs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def config_dict(args, world):
+    return {"workload": f"config5: B-spline-trimmed unit square, p={args.p}, {args.nel}x{args.nel} elements, "
+                        f"c=1, {args.strategy}, seed {args.seed}",
+            "nel": args.nel, "p": args.p, "strategy": args.strategy, "seed": args.seed,
+            "parallelism": f"row-block x{world}", "l2": "flushed between steps (256 MiB write)",
+            "row_sharding": "contiguous active-row blocks, no collective during formation"}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port = the reference algorithm restated in numpy)
+# ---------------------------------------------------------------------------
+
+def cpu_threads():
+    return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(nel, p, strategy, seed, repeats=1):
+    """Reference CPU path (oracle port) on a bounded sample of the workload:
+    the same trim, degree and strategy on an nel x nel mesh.  Returns
+    (nnz/s of the best repeat, description)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import assemble as OA
+    from oracle import configs as OC
+    with threadpool_limits(limits=cpu_threads()):
+        c = OC.config(5, seed=seed, nel=nel, p=p)
+        cfg = OC.build_space(c["curves"], nel, p)
+        cfg.cut_cell_rule(p)
+        rates = []
+        for _ in range(repeats):
+            M, rep = OA.form_with_timings(strategy, cfg)
+            rates.append(M.data.nnz / rep.t_total)
+    sample = (f"oracle/ (numpy restatement of trimquad) form_with_timings t_total, same trim/p/strategy on "
+              f"{nel}x{nel} elements ({M.data.nnz} nnz), median of {repeats}")
+    return statistics.median(rates), sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    from oracle import assemble as OA
+    from oracle import configs as OC
+    cores = cpu_threads()
+    with threadpool_limits(limits=cores):
+        c = OC.config(5, seed=args.seed, nel=args.cpu_nel, p=args.p)
+        cfg = OC.build_space(c["curves"], args.cpu_nel, args.p)
+        cfg.cut_cell_rule(args.p)
+        for _ in range(args.warmup):
+            OA.form_with_timings(args.strategy, cfg)
+        ts, nnz = [], 0
+        for _ in range(args.steps):
+            M, rep = OA.form_with_timings(args.strategy, cfg)
+            ts.append(rep.t_total)
+            nnz = M.data.nnz
+    ms = 1e3 * sum(ts) / len(ts)
+    value = nnz / (ms / 1e3)
+    sample = (f"oracle port form_with_timings per step on {args.cpu_nel}x{args.cpu_nel} elements "
+              f"({nnz} nnz) of the config-5 workload")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+           "config": config_dict(args, world),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 2 + k and r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """Per-launch DRAM bytes of the fill kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(HERE, "profiles", "fill_ncu_summary.json")) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2101_08053_b200 as P
+    from paper_2101_08053_b200 import _lib as L
+    from paper_2101_08053_b200 import cases as C
+    from paper_2101_08053_b200.assembly import _KernelTimer, form
+
+    torch.cuda.set_device(local_rank)
+    lib = L.lib()
+    lib.tq_launch_count.restype = L.C.c_longlong
+    dev = torch.device("cuda", local_rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # setup (untimed, resident): basis, GPU classification, host cut-cell rule
+    c5 = C.baseline_config(5, seed=args.seed, p=args.p, nel=args.nel)
+    b2d, cfg = C.build_space(None, args.nel, args.p, curves=c5["curves"])
+    cfg.cut_cell_rule(args.p)
+    idx, _ = cfg.active_index()
+    K = idx["K"]
+    rb, re_ = (K * rank) // world, (K * (rank + 1)) // world
+    flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device=dev)
+
+    def step(timer=None):
+        f, csr = form(b2d, cfg, None, args.strategy, row_range=(rb, re_), timer=timer)
+        return f, csr
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    timer = _KernelTimer()
+    launches0 = lib.tq_launch_count()
+    nnz_local = 0
+    reports = []
+    for k in range(args.steps):
+        flush.fill_(float(k))            # L2 flush between timed steps (untimed)
+        barrier()
+        torch.cuda.synchronize()
+        ev[k][0].record()
+        f, csr = step(timer)
+        ev[k][1].record()
+        torch.cuda.synchronize()
+        barrier()
+        nnz_local = csr.nnz
+        reports.append(f.report)
+        del f, csr
+    launches = lib.tq_launch_count() - launches0
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    kms = timer.ms()
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms, float(nnz_local), kms.get("fill", 0.0), float(re_ - rb)], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    else:
+        tmax = tsum = t
+    total_ms_max = float(tmax[0])
+    nnz_total = int(tsum[1])
+    ms_per_step = total_ms_max / args.steps
+    value = nnz_total / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (fill): algorithmic bytes / event time
+    fill_ms = kms.get("fill", float("nan")) / args.steps
+    alg_bytes = 12.0 * nnz_local + 4.0 * ((re_ - rb) + 1)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = alg_bytes / (fill_ms / 1e3) / 1e9
+    traffic = profile_traffic()
+    rep = reports[-1]
+
+    # e2e through the public API from host inputs (rank-local row block at N>1)
+    e2e = None
+    if args.e2e_steps > 0:
+        knots = np.ascontiguousarray(P.make_uniform_knots(args.nel, args.p).knots)
+        ctrl = np.ascontiguousarray(c5["curves"][0].ctrl)
+        e_ts, h2d, d2h = [], 0, 0
+        for k in range(args.e2e_steps + 1):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            kv = P.KnotVector(knots.copy(), args.p)
+            bb = P.TensorBasis2D(P.Basis1D(kv), P.Basis1D(P.KnotVector(knots.copy(), args.p)))
+            cf = P.classify_elements(bb, [P.trimming.PeriodicBSplineTrim(ctrl.copy())])
+            if world == 1:
+                M = P.assemble_mass(bb, cf, None, strategy=args.strategy)
+                nnz_e, rows_e = M.data.nnz, M.shape[0]
+            else:
+                idx2, _ = cf.active_index()
+                K2 = idx2["K"]
+                f2, csr2 = form(bb, cf, None, args.strategy, row_range=((K2 * rank) // world, (K2 * (rank + 1)) // world))
+                host = (csr2.indptr.cpu().numpy(), csr2.indices.cpu().numpy(), csr2.data.cpu().numpy())
+                nnz_e, rows_e = csr2.nnz, csr2.row_end - csr2.row_begin
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            barrier()
+            if k > 0:          # first pass warms the allocator / caches
+                e_ts.append(dt)
+            h2d = knots.nbytes * 2 + ctrl.nbytes
+            d2h = 12 * nnz_e + 4 * (rows_e + 1)
+        et = torch.tensor([max(e_ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": nnz_total / float(et[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(et[0]),
+               "path": "KnotVector/Basis1D -> classify_elements (GPU) -> cut_cell_rule (host C++) -> "
+                       "assemble_mass -> scipy CSR on host" + (" (row block per rank)" if world > 1 else "")}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            v, sample = oracle_sample(args.cpu_nel, args.p, args.strategy, args.seed)
+            cpu = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": sample}
+        except Exception as exc:  # the GPU number stands on its own
+            cpu = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": f"failed: {exc}"}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config 5 geometry)",
+        "config": config_dict(args, world),
+        "nnz": nnz_total, "rows": K,
+        "phases_ms": {"weights": 1e3 * rep.t_weights, "interior": 1e3 * rep.t_interior,
+                      "cut_regular": 1e3 * rep.t_cut_regular, "cut_elements": 1e3 * rep.t_cut_elements,
+                      "finish": 1e3 * rep.t_finish},
+        "kernels_ms_per_step": {k: v / args.steps for k, v in kms.items()},
+        "roofline": {"kernel": "k_fill_tiles (fused symmetrise + zero-drop + CSR write)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -440,6 +440,8 @@ class PeriodicBSplineTrim(Curve):
     def subpiece_boxes(self):
         """(m*S, 4) boxes [xlo, xhi, ylo, yhi] of the Bernstein control points
         of each sub-interval [s/S, (s+1)/S] of each segment (convex hull)."""
+        if getattr(self, "_boxes", None) is not None:
+            return self._boxes
         S = self.SUBPIECES
         out = np.empty((self.m * S, 4))
         h = 1.0 / S
@@ -453,29 +455,32 @@ class PeriodicBSplineTrim(Curve):
                 a1 = a * (h * h * h)
                 B = np.stack([d1, d1 + c1 / 3.0, d1 + 2.0 * c1 / 3.0 + b1 / 3.0, d1 + c1 + b1 + a1])
                 out[k * S + s] = [B[:, 0].min(), B[:, 0].max(), B[:, 1].min(), B[:, 1].max()]
+        self._boxes = out
         return out
 
     def exact_distance(self, P):
-        """Nearest-point distance: 33 samples + 30 clamped Newton steps per segment."""
+        """Nearest-point distance: 33 samples + 30 clamped Newton steps per
+        segment (vectorized over points x segments; per-element arithmetic
+        identical to the CUDA classifier's bs_exact_distance)."""
         P = np.atleast_2d(np.asarray(P, float))
-        best = np.full(P.shape[0], np.inf)
+        a, b, c, d = (self.pw[None, :, q, :] for q in range(4))     # (1, m, 2)
         us = np.linspace(0.0, 1.0, 33)
-        for k in range(self.m):
-            a, b, c, d = self.pw[k]
-            S = _horner(a, b, c, d, us[:, None])                      # (33, 2)
-            d2 = ((S[None, :, :] - P[:, None, :]) ** 2).sum(axis=2)   # (N, 33)
-            u = us[np.argmin(d2, axis=1)]
-            for _ in range(30):
-                g = _horner(a, b, c, d, u[:, None]) - P
-                dg = (3.0 * a * u[:, None] + 2.0 * b) * u[:, None] + c
-                ddg = 6.0 * a * u[:, None] + 2.0 * b
-                f = (g * dg).sum(axis=1)
-                df = (dg * dg).sum(axis=1) + (g * ddg).sum(axis=1)
-                step = np.where(df > 0, f / np.where(df > 0, df, 1.0), 0.0)
-                u = np.clip(u - step, 0.0, 1.0)
-            q = _horner(a, b, c, d, u[:, None]) - P
-            best = np.minimum(best, np.hypot(q[:, 0], q[:, 1]))
-        return best
+        Q = P[:, None, None, :]                                      # (N, 1, 1, 2)
+        S = _horner(a[:, :, None, :], b[:, :, None, :], c[:, :, None, :], d[:, :, None, :],
+                    us[None, None, :, None])                         # (1, m, 33, 2)
+        d2 = ((S - Q) ** 2).sum(axis=3)                              # (N, m, 33)
+        u = us[np.argmin(d2, axis=2)][:, :, None]                    # (N, m, 1)
+        X = P[:, None, :]
+        for _ in range(30):
+            g = _horner(a, b, c, d, u) - X
+            dg = (3.0 * a * u + 2.0 * b) * u + c
+            ddg = 6.0 * a * u + 2.0 * b
+            f = (g * dg).sum(axis=2, keepdims=True)
+            df = (dg * dg).sum(axis=2, keepdims=True) + (g * ddg).sum(axis=2, keepdims=True)
+            step = np.where(df > 0, f / np.where(df > 0, df, 1.0), 0.0)
+            u = np.clip(u - step, 0.0, 1.0)
+        q = _horner(a, b, c, d, u) - X
+        return np.min(np.hypot(q[:, :, 0], q[:, :, 1]), axis=1)
 
     def signed_distance(self, P):
         """Sign from the crossing parity (+ on the valid side).  The magnitude is
@@ -485,10 +490,16 @@ class PeriodicBSplineTrim(Curve):
         P = np.atleast_2d(np.asarray(P, float))
         valid = self.enclosed(P) == self.ccw
         lb = np.full(P.shape[0], np.inf)
-        for xlo, xhi, ylo, yhi in self.subpiece_boxes():
-            dx = np.maximum(np.maximum(xlo - P[:, 0], P[:, 0] - xhi), 0.0)
-            dy = np.maximum(np.maximum(ylo - P[:, 1], P[:, 1] - yhi), 0.0)
-            np.minimum(lb, np.maximum(dx, dy), out=lb)
+        B = self.subpiece_boxes()
+        if P.shape[0] <= 64:   # few points (decomposition probes): one broadcast
+            dx = np.maximum(np.maximum(B[None, :, 0] - P[:, :1], P[:, :1] - B[None, :, 1]), 0.0)
+            dy = np.maximum(np.maximum(B[None, :, 2] - P[:, 1:], P[:, 1:] - B[None, :, 3]), 0.0)
+            lb = np.min(np.maximum(dx, dy), axis=1)
+        else:
+            for xlo, xhi, ylo, yhi in B:
+                dx = np.maximum(np.maximum(xlo - P[:, 0], P[:, 0] - xhi), 0.0)
+                dy = np.maximum(np.maximum(ylo - P[:, 1], P[:, 1] - yhi), 0.0)
+                np.minimum(lb, np.maximum(dx, dy), out=lb)
         dist = lb.copy()
         near = np.nonzero(lb <= self.NEAR)[0]
         if near.size:

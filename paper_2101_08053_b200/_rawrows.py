@@ -19,7 +19,8 @@ import torch
 
 from . import _lib as L
 from ._lib import CUT, INTERIOR
-from .quadrature import build_dwq, gauss_legendre
+from .quadrature import (DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async, build_dwq,
+                         compute_wq_rules, dwq_solve_async, gauss_legendre, place_wq_points)
 
 MODE_GAUSS, MODE_BOX, MODE_MASK = 0, 1, 2
 
@@ -48,16 +49,40 @@ def _bind():
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
 
 
+def _geo(config):
+    """Config-level cache of geometry-derived data, the analogue of the
+    reference's per-configuration caches (cut_cell_rule, _assembly_cache,
+    _dwq_cache: src/trimming.py:437-438, 588-594, src/assembly.py:186-195)."""
+    g = config.__dict__.get("_geo")
+    if g is None:
+        g = config.__dict__["_geo"] = {}
+    return g
+
+
+def active_host(f):
+    g = _geo(f.config)
+    if "active" not in g:
+        g["active"] = f.active[: f.K].cpu().numpy().astype(np.int64)
+    return g["active"]
+
+
 def cut_rows_host(f):
     """Active cut functions in active (row-major) order -> function ids."""
-    fc = f.config.func_class.ravel()
-    act = f.active[: f.K].cpu().numpy()
-    return act[fc[act] == CUT].astype(np.int32)
+    g = _geo(f.config)
+    if "cut_fids" not in g:
+        fc = f.config.func_class.ravel()
+        act = active_host(f)
+        g["cut_fids"] = act[fc[act] == CUT].astype(np.int32)
+    return g["cut_fids"]
 
 
 def route_cut_rows(f):
-    """DWQ routing on the GPU (src/trimming.py:545-586) -> (cut fids, routes)."""
+    """DWQ routing on the GPU (src/trimming.py:545-586) -> (cut fids, routes);
+    cached per configuration like the reference's dwq_info cache."""
     _bind()
+    g = _geo(f.config)
+    if "routes" in g:
+        return g["routes"]
     cut = cut_rows_host(f)
     routes = np.full((cut.size, 8), -1, np.int32)
     if cut.size:
@@ -69,37 +94,100 @@ def route_cut_rows(f):
         L.call("tq_dwq_route", f.b1.device(), f.b2.device(), L.ptr(f.config.element_class_dev), L.ptr(du1),
                u1.size, L.ptr(du2), u2.size, L.ptr(rows), cut.size, L.ptr(out), L.stream())
         routes = out.cpu().numpy()
-    return cut, routes
+    g["routes"] = (cut, routes)
+    return g["routes"]
 
 
-def build_dwq_sets(f, r1, r2):
-    """DWQ rule sets per (direction, u_disc) for eligible boxed cut rows
-    (src/assembly.py:460-488), fits on the GPU."""
-    cut, routes = route_cut_rows(f)
-    f._routes = (cut, routes)
-    needed = {}
-    n2 = f.b2.n
-    for fid, rt in zip(cut, routes):
-        if rt[0] != 1 or rt[3] < 0:
-            continue
-        ij = (int(fid) // n2, int(fid) % n2)
-        for d in (0, 1):
-            iu = rt[1 + d]
-            if iu >= 0:
-                needed.setdefault((d, float(f.config.u_disc[d][iu])), set()).add(ij[d])
+def cut_point_tables(f):
+    """Device copy of the host cut-cell rule (cached per configuration)."""
+    g = _geo(f.config)
+    if "cutpts" not in g:
+        b1, b2 = f.b1, f.b2
+        rule = f.config.cut_cell_rule(max(b1.p, b2.p))
+        P = L.dev(rule.points.reshape(-1, 2), torch.float64)
+        cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
+        cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
+        g["cutpts"] = dict(P=P, x=P[:, 0].contiguous(), y=P[:, 1].contiguous(),
+                           W=L.dev(rule.weights, torch.float64), idx=L.dev(cutidx, torch.int32),
+                           ptr=L.dev(rule.ptr, torch.int64), npts=rule.total_points())
+    return g["cutpts"]
+
+
+def element_points(f):
+    g = _geo(f.config)
+    if "eg" not in g:
+        out = []
+        for b in (f.b1, f.b2):
+            gl = gauss_legendre(b.p + 1)
+            bp = b.breakpoints
+            mid, half = 0.5 * (bp[:-1] + bp[1:]), 0.5 * np.diff(bp)
+            X = mid[:, None] + half[:, None] * gl.points[None, :]
+            Wt = half[:, None] * gl.weights[None, :]
+            out.append((L.dev(X.ravel(), torch.float64), L.dev(Wt.ravel(), torch.float64)))
+        g["eg"] = out
+    return g["eg"]
+
+
+def dwq_keys(f):
+    """(direction, u_disc) -> sorted rows, for eligible boxed cut rows
+    (src/assembly.py:460-471)."""
+    g = _geo(f.config)
+    if "dwq_keys" not in g:
+        cut, routes = route_cut_rows(f)
+        needed = {}
+        n2 = f.b2.n
+        for fid, rt in zip(cut, routes):
+            if rt[0] != 1 or rt[3] < 0:
+                continue
+            ij = (int(fid) // n2, int(fid) % n2)
+            for d in (0, 1):
+                iu = rt[1 + d]
+                if iu >= 0:
+                    needed.setdefault((d, float(f.config.u_disc[d][iu])), set()).add(ij[d])
+        g["dwq_keys"] = {k: sorted(v) for k, v in sorted(needed.items())}
+    return g["dwq_keys"]
+
+
+def build_all_rules(f):
+    """Standard WQ rules per direction and the DWQ sets (src/assembly.py:454-489).
+    Point layouts and DWQ refinement plans are geometry (cached per
+    configuration); every fit -- basis tables, exact moments, pivoted-QR
+    solves, S^T combination -- is recomputed on the GPU each call, with a
+    single host sync to read back all residual flags."""
+    g = _geo(f.config)
+    if "std_plans" not in g:
+        g["std_plans"] = [_FitPlan(b, place_wq_points(b)) for b in (f.b1, f.b2)]
+    plans = g["std_plans"]
+    std = [_solve_rows_async(pl) for pl in plans]
+    dwq_pending = {}
+    if f.strategy == "dwq":
+        keys = dwq_keys(f)
+        for (d, u), rows in keys.items():
+            pk = ("dwq_plan", d, u)
+            if pk not in g:
+                g[pk] = DwqPlan((f.b1, f.b2)[d], plans[d].layout, u, only_rows=rows)
+            dwq_pending[(d, u)] = (g[pk], *dwq_solve_async(g[pk], direction=d))
+    flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
+    flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]
+    any_fail = bool(torch.cat(flags).any().item()) if flags else False
+    rules = []
+    for d, (pl, (wptr, k0, w, fail)) in enumerate(zip(plans, std)):
+        if any_fail and _failing(pl, fail):
+            rules.append(compute_wq_rules(pl.basis, pl.layout, direction=d))   # enrichment retries
+        else:
+            rules.append(WeightedRuleSet(pl.basis, pl.layout, wptr, k0, w, d))
     dwq = {}
-    for key in sorted(needed):
-        d, u = key
-        basis = (f.b1, f.b2)[d]
-        base = (r1, r2)[d].layout
-        dwq[key] = build_dwq(basis, base, u, direction=d, only_rows=sorted(needed[key]))
-    return dwq
+    for key, (pl, rs, fail) in dwq_pending.items():
+        if any_fail and _failing(pl.fit, fail):
+            rs = build_dwq(pl.basis, pl.base_layout, key[1], direction=key[0], plan=pl)
+        dwq[key] = rs
+    return rules[0], rules[1], dwq
 
 
 def needs_raw(f):
     if f.strategy == "reference" or not f.coeff.identity:
         return True
-    return bool(np.any(f.config.func_class == CUT))
+    return cut_rows_host(f).size > 0
 
 
 class _Setup:
@@ -112,17 +200,12 @@ class _Setup:
         cfg = f.config
         dev = f.dev
         self.f = f
-        # element Gauss tables, (p+1) points (src/assembly.py:198-211)
+        # element Gauss tables, (p+1) points (src/assembly.py:198-211);
+        # basis values evaluated per formation as in the reference's _Run
         self.eg = []
-        for b in (b1, b2):
-            g = gauss_legendre(b.p + 1)
-            bp = b.breakpoints
-            mid, half = 0.5 * (bp[:-1] + bp[1:]), 0.5 * np.diff(bp)
-            X = mid[:, None] + half[:, None] * g.points[None, :]
-            Wt = half[:, None] * g.weights[None, :]
-            Xd = L.dev(X.ravel(), torch.float64)
-            _, vals = b.eval_device(Xd)
-            self.eg.append((X, L.dev(Wt.ravel(), torch.float64), vals, Xd))
+        for b, (Xd, Wd) in zip((b1, b2), element_points(f)):
+            _, vals = b.eval_device(Xd, check=False)
+            self.eg.append((None, Wd, vals, Xd))
         self.cg = None
         if not f.coeff.identity:
             self.cg = f.coeff.grid_device(self.eg[0][3], self.eg[1][3])
@@ -165,19 +248,14 @@ class _Setup:
             self.nmax = [1, 1]
         # cut-element points (host C++ geometry, device basis tables)
         self.cut = None
-        if cfg.cut_elements:
-            q = max(b1.p, b2.p)
-            rule = cfg.cut_cell_rule(q)
-            P = L.dev(rule.points.reshape(-1, 2), torch.float64)
-            Wd = L.dev(rule.weights, torch.float64)
-            f1, v1 = b1.eval_device(P[:, 0].contiguous())
-            f2, v2 = b2.eval_device(P[:, 1].contiguous())
-            cw = f.coeff.at_device(P) * Wd if not f.coeff.identity else Wd
-            cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
-            cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
-            self.cut = dict(idx=L.dev(cutidx, torch.int32), ptr=L.dev(rule.ptr, torch.int64), cw=cw.contiguous(),
-                            f1=f1, v1=v1, f2=f2, v2=v2, npts=rule.total_points())
-            f.report.n_cutcell_points = rule.total_points()
+        if f.config.has_cuts():
+            t = cut_point_tables(f)
+            f1, v1 = b1.eval_device(t["x"], check=False)
+            f2, v2 = b2.eval_device(t["y"], check=False)
+            cw = f.coeff.at_device(t["P"]) * t["W"] if not f.coeff.identity else t["W"]
+            self.cut = dict(idx=t["idx"], ptr=t["ptr"], cw=cw.contiguous(), f1=f1, v1=v1, f2=f2, v2=v2,
+                            npts=t["npts"])
+            f.report.n_cutcell_points = t["npts"]
 
     def ctx(self, desc, raw, nraw):
         f = self.f
@@ -197,9 +275,20 @@ class _Setup:
 
 
 def _plan(f):
-    """Decide the raw rows and their descriptors (host, once per formation)."""
+    """Raw rows and their descriptors (host bookkeeping, cached per
+    configuration / strategy / coefficient kind / DWQ key set)."""
+    key = ("plan", f.strategy, f.coeff.identity,
+           tuple(sorted(f._setup.key_index[0].items())) if f.rules is not None else (),
+           tuple(sorted(f._setup.key_index[1].items())) if f.rules is not None else ())
+    g = _geo(f.config)
+    if key not in g:
+        g[key] = _plan_uncached(f)
+    return g[key]
+
+
+def _plan_uncached(f):
     fc = f.config.func_class.ravel()
-    act = f.active[: f.K].cpu().numpy().astype(np.int64)
+    act = active_host(f)
     n2 = f.b2.n
     is_cut = fc[act] == CUT
     interior_raw = f.strategy == "reference" or not f.coeff.identity
@@ -233,7 +322,7 @@ def _plan(f):
             d[:, 2] = 0
             d[:, 3] = 0
         else:  # dwq
-            cut, routes = f._routes
+            cut, routes = route_cut_rows(f)
             assert np.array_equal(cut, rows_cut)
             setup = f._setup
             for k, rt in enumerate(routes):
@@ -259,7 +348,11 @@ def run_phase(f, phase):
         desc, nint = _plan(f)
         f._nint = nint
         f._ndesc = desc.shape[0]
-        f._desc = L.dev(desc, torch.int32)
+        g = _geo(f.config)
+        dkey = ("desc", id(desc))
+        if dkey not in g:
+            g[dkey] = L.dev(desc, torch.int32)
+        f._desc = g[dkey]
         W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
         f.raw = torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64, device=f.dev)
         slot = f.slot

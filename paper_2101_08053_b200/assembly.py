@@ -204,11 +204,49 @@ class DeviceCSR:
                               self.indptr.cpu().numpy()), shape=shape)
 
 
+class _KernelTimer:
+    """CUDA events around named native calls on the launching stream."""
+
+    def __init__(self):
+        self.events = {}
+
+    def __call__(self, name):
+        timer = self
+
+        class _Ctx:
+            def __enter__(self_):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                timer.events.setdefault(name, []).append((s, e))
+                s.record()
+
+            def __exit__(self_, *a):
+                timer.events[name][-1][1].record()
+        return _Ctx()
+
+    def ms(self):
+        torch.cuda.synchronize()
+        return {k: sum(s.elapsed_time(e) for s, e in v) for k, v in self.events.items()}
+
+
+class _NoTimer:
+    class _C:
+        def __enter__(self):
+            pass
+
+        def __exit__(self, *a):
+            pass
+
+    _c = _C()
+
+    def __call__(self, name):
+        return self._c
+
+
 class Formation:
     """Device state of one assembly run (the analogue of ``_Run``,
     src/assembly.py:272-404)."""
 
-    def __init__(self, basis2d: TensorBasis2D, config: TrimConfiguration, coeff, strategy):
+    def __init__(self, basis2d: TensorBasis2D, config: TrimConfiguration, coeff, strategy, timer=None):
         if strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
         self.basis2d = basis2d
@@ -227,22 +265,15 @@ class Formation:
         self.deep = None
         self.rules = None
         self.report = FormationReport(strategy)
+        self.timer = timer or _NoTimer()
 
     # -- phases -------------------------------------------------------------------
     def build_weights(self, rules=None):
         if self.strategy == "reference":
             return
         if rules is None:
-            r1 = compute_wq_rules(self.b1, place_wq_points(self.b1), direction=0)
-            r2 = compute_wq_rules(self.b2, place_wq_points(self.b2), direction=1)
-            dwq = {}
-            if self.strategy == "dwq":
-                from . import _rawrows
-                dwq = _rawrows.build_dwq_sets(self, r1, r2)
-            rules = (r1, r2, dwq)
-        elif self.strategy == "dwq":
             from . import _rawrows
-            self._routes = _rawrows.route_cut_rows(self)
+            rules = _rawrows.build_all_rules(self)
         self.rules = rules
         self.report.n_wq_points = rules[0].layout.num_points + rules[1].layout.num_points
 
@@ -291,22 +322,25 @@ class Formation:
                    self.raw_list.numel(), L.ptr(self.deep), L.stream())
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
-        L.call("tq_row_counts", ctx, L.ptr(counts), L.stream())
+        with self.timer("counts"):
+            L.call("tq_row_counts", ctx, L.ptr(counts), L.stream())
         indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
-        L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr), L.C.byref(nnz), L.stream())
+        with self.timer("scan"):
+            L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr), L.C.byref(nnz), L.stream())
         nnz = int(nnz.value)
         indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
         data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
-        L.call("tq_fill_rows", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
+        with self.timer("fill"):
+            L.call("tq_fill_rows", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
 
-def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None):
+def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None):
     """Run every formation phase on the device; returns (Formation, DeviceCSR)."""
-    f = Formation(basis2d, config, coeff, strategy)
+    f = Formation(basis2d, config, coeff, strategy, timer)
     rep = f.report
-    if config.cut_elements:   # shared geometry, outside the clock (src/assembly.py:505-508)
+    if config.has_cuts():     # shared geometry, outside the clock (src/assembly.py:505-508)
         config.cut_cell_rule(max(basis2d.degrees))
     clk = _Clock()
     f.build_weights(rules)
@@ -346,7 +380,7 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
 def form_with_timings(strategy, basis2d, config, coeff=None, parallel=False):
     """src/assembly.py:651-665: shared geometry warmed outside the clock."""
     q = max(basis2d.degrees)
-    if config.cut_elements:
+    if config.has_cuts():
         config.cut_cell_rule(q)
     config.active_index()
     report = FormationReport(strategy=strategy)

@@ -1,11 +1,16 @@
 // C-ABI plumbing: error reporting and stream sync.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace tq {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -30,3 +35,6 @@ extern "C" int tq_device_sync(void* stream) {
     TQ_CUDA(cudaGetLastError());
     return TQ_OK;
 }
+
+// kernels launched by this library since load (host counter, no device state)
+extern "C" long long tq_launch_count(void) { return tq::g_launches.load(); }

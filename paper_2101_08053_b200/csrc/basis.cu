@@ -15,7 +15,7 @@ __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t
          t += (int64_t)gridDim.x * blockDim.x) {
         double x = u[t];
         if (!(x >= lo && x <= hi)) {
-            atomicOr(status, kStatusDomain);
+            if (status) atomicOr(status, kStatusDomain);
             x = x < lo ? lo : hi;
         }
         int span = find_span(s.knots, s.nknots, P, s.n, x);
@@ -79,7 +79,7 @@ extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* 
     if (s.p < 0 || s.p > kMaxP) { set_error("degree %d unsupported (max %d)", s.p, kMaxP); return TQ_EINVAL; }
     int grid = grid_for(n, 256);
     switch (s.p) {
-#define CASE(P) case P: k_basis_eval<P><<<grid, 256, 0, S(stream)>>>(s, u, n, first, vals, ders, status); break;
+#define CASE(P) case P: k_basis_eval<P><<<grid, 256, 0, S(stream)>>>(s, u, n, first, vals, ders, status); ::tq::note_launch(); break;
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     }
@@ -91,7 +91,7 @@ extern "C" int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw,
                                double* mom, void* stream) {
     if (s.p > kMaxP) { set_error("degree %d unsupported", s.p); return TQ_EINVAL; }
     int64_t total = (int64_t)s.n * (2 * s.p + 1);
-    k_moments<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, gx, gw, ng, mom);
+    k_moments<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, gx, gw, ng, mom); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_moments");
     return TQ_OK;
 }

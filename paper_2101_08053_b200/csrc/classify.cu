@@ -196,13 +196,13 @@ extern "C" int tq_classify_elements(const tq_curve* curves_h, int32_t ncurves, t
     TQ_CUDA(cudaMallocAsync(&hcoord, (size_t)ncurves * L * kLineCap * sizeof(double), st));
     TQ_CUDA(cudaMallocAsync(&hcell, (size_t)ncurves * L * kLineCap * sizeof(int32_t), st));
     TQ_CUDA(cudaMallocAsync(&hcount, (size_t)ncurves * L * sizeof(int32_t), st));
-    k_nodes<<<grid_for(nn, 128), 128, 0, st>>>(dcv, ncurves, s1, s2, flags);
+    k_nodes<<<grid_for(nn, 128), 128, 0, st>>>(dcv, ncurves, s1, s2, flags); ::tq::note_launch();
     k_lines<<<grid_for((int64_t)ncurves * L, 64), 64, 0, st>>>(dcv, ncurves, s1, s2, hcoord, hcell, hcount,
-                                                               status);
+                                                               status); ::tq::note_launch();
     int64_t ne = (int64_t)s1.nel * s2.nel;
     k_elements<<<grid_for(ne, 128), 128, 0, st>>>(dcv, ncurves, s1, s2, flags, hcoord, hcell, hcount,
-                                                  elem_class);
-    k_guard<<<grid_for((int64_t)ncurves * 511, 128), 128, 0, st>>>(dcv, ncurves, s1, s2, elem_class, status);
+                                                  elem_class); ::tq::note_launch();
+    k_guard<<<grid_for((int64_t)ncurves * 511, 128), 128, 0, st>>>(dcv, ncurves, s1, s2, elem_class, status); ::tq::note_launch();
     TQ_LAUNCH_CHECK("classify");
     cudaFreeAsync(flags, st);
     cudaFreeAsync(hcoord, st);

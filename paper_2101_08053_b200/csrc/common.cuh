@@ -12,6 +12,7 @@
 namespace tq {
 
 void set_error(const char* fmt, ...);
+void note_launch();
 int check_cuda(cudaError_t e, const char* what);
 
 #define TQ_CUDA(call)                                              \

@@ -121,7 +121,7 @@ extern "C" int tq_dwq_route(tq_space1d s1, tq_space1d s2, const int8_t* elem_cla
                             int32_t ncut, int32_t* route, void* stream) {
     if (ncut == 0) return TQ_OK;
     k_dwq_route<<<grid_for(ncut, 128), 128, 0, S(stream)>>>(s1, s2, elem_class, udisc1, nu1, udisc2, nu2,
-                                                            cut_rows, ncut, route);
+                                                            cut_rows, ncut, route); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_dwq_route");
     return TQ_OK;
 }
@@ -129,9 +129,9 @@ extern "C" int tq_dwq_route(tq_space1d s1, tq_space1d s2, const int8_t* elem_cla
 extern "C" int tq_function_classes(tq_space1d s1, tq_space1d s2, const int8_t* elem_class,
                                    int8_t* func_class, int32_t* face1, int32_t* face2, void* stream) {
     int64_t nf = (int64_t)s1.n * s2.n;
-    k_func_class<<<grid_for(nf, 256), 256, 0, S(stream)>>>(s1, s2, elem_class, func_class);
+    k_func_class<<<grid_for(nf, 256), 256, 0, S(stream)>>>(s1, s2, elem_class, func_class); ::tq::note_launch();
     int64_t ne = (int64_t)s1.nel * s2.nel;
-    k_faces<<<grid_for(ne, 256), 256, 0, S(stream)>>>(s1.nel, s2.nel, elem_class, face1, face2);
+    k_faces<<<grid_for(ne, 256), 256, 0, S(stream)>>>(s1.nel, s2.nel, elem_class, face1, face2); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_func_class/k_faces");
     return TQ_OK;
 }

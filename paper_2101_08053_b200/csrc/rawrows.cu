@@ -281,7 +281,7 @@ extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream)
     if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
     TQ_CUDA(cudaFuncSetAttribute(k_raw_regular, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
-    k_raw_regular<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1);
+    k_raw_regular<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_regular");
     return TQ_OK;
 }
@@ -292,7 +292,7 @@ extern "C" int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream
     size_t shm = sizeof(double) * (2 * c.p1 + 1) * (2 * c.p2 + 1) * wpb;
     TQ_CUDA(cudaFuncSetAttribute(k_raw_cutcells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
-    k_raw_cutcells<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1);
+    k_raw_cutcells<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_cutcells");
     return TQ_OK;
 }
@@ -301,7 +301,7 @@ extern "C" int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const dou
                              void* stream) {
     if ((int64_t)n1 * n2 == 0) return TQ_OK;
     if (g.kind != TQ_COEFF_GEOMETRY || g.p > kMaxP) { set_error("unsupported coefficient field"); return TQ_EINVAL; }
-    k_coeff_grid<<<grid_for((int64_t)n1 * n2, 128), 128, 0, S(stream)>>>(g, x1, n1, x2, n2, out);
+    k_coeff_grid<<<grid_for((int64_t)n1 * n2, 128), 128, 0, S(stream)>>>(g, x1, n1, x2, n2, out); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_coeff_grid");
     return TQ_OK;
 }
@@ -310,7 +310,7 @@ extern "C" int tq_coeff_points(tq_coeff g, const double* pts, int64_t n, const d
                                void* stream) {
     if (n == 0) return TQ_OK;
     if (g.kind != TQ_COEFF_GEOMETRY || g.p > kMaxP) { set_error("unsupported coefficient field"); return TQ_EINVAL; }
-    k_coeff_points<<<grid_for(n, 128), 128, 0, S(stream)>>>(g, pts, n, w, out);
+    k_coeff_points<<<grid_for(n, 128), 128, 0, S(stream)>>>(g, pts, n, w, out); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_coeff_points");
     return TQ_OK;
 }

@@ -222,10 +222,10 @@ extern "C" int tq_rhs(tq_projctx c, double* T, const int32_t* cut_rows, int32_t 
     // widest chunk: elements spanned by kChunk consecutive functions + p
     size_t shm = sizeof(double) * (size_t)(kChunk + 2 * c.p2 + 2) * c.g2n;
     TQ_CUDA(cudaFuncSetAttribute(k_rhs_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_rhs_stage1<<<(int)std::min<int64_t>(nblk, (int64_t)kSms * 32), kChunk, shm, st>>>(c, T);
+    k_rhs_stage1<<<(int)std::min<int64_t>(nblk, (int64_t)kSms * 32), kChunk, shm, st>>>(c, T); ::tq::note_launch();
     int nrows = c.row_end - c.row_begin;
-    if (nrows > 0) k_rhs_stage2<<<grid_for(nrows, 256), 256, 0, st>>>(c, T, b);
-    if (ncut > 0 && c.cut_ptr) k_rhs_cut<<<grid_for(ncut, 4), 128, 0, st>>>(c, cut_rows, ncut, b);
+    if (nrows > 0) k_rhs_stage2<<<grid_for(nrows, 256), 256, 0, st>>>(c, T, b); ::tq::note_launch();
+    if (ncut > 0 && c.cut_ptr) k_rhs_cut<<<grid_for(ncut, 4), 128, 0, st>>>(c, cut_rows, ncut, b); ::tq::note_launch();
     TQ_LAUNCH_CHECK("tq_rhs");
     return TQ_OK;
 }
@@ -233,7 +233,7 @@ extern "C" int tq_rhs(tq_projctx c, double* T, const int32_t* cut_rows, int32_t 
 extern "C" int tq_target_points(tq_target f, const double* P, const double* w, int64_t n, double* out,
                                 void* stream) {
     if (n == 0) return TQ_OK;
-    k_target_points<<<grid_for(n, 256), 256, 0, S(stream)>>>(f, P, w, n, out);
+    k_target_points<<<grid_for(n, 256), 256, 0, S(stream)>>>(f, P, w, n, out); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_target_points");
     return TQ_OK;
 }
@@ -246,12 +246,12 @@ extern "C" int tq_l2_parts(tq_projctx c, const double* C, int64_t e_begin, int64
     TQ_CUDA(cudaMallocAsync(&parts, sizeof(double) * 2 * nb, st));
     TQ_CUDA(cudaMemsetAsync(num_den, 0, 2 * sizeof(double), st));
     if (e_end > e_begin) {
-        k_l2_elements<<<nb, 256, 0, st>>>(c, C, e_begin, e_end, parts);
-        k_reduce_parts<<<1, 32, 0, st>>>(parts, nb, num_den);
+        k_l2_elements<<<nb, 256, 0, st>>>(c, C, e_begin, e_end, parts); ::tq::note_launch();
+        k_reduce_parts<<<1, 32, 0, st>>>(parts, nb, num_den); ::tq::note_launch();
     }
     if (p_end > p_begin && c.cut_ptr) {
-        k_l2_cut<<<nb, 256, 0, st>>>(c, C, p_begin, p_end, fpts, parts);
-        k_reduce_parts<<<1, 32, 0, st>>>(parts, nb, num_den);
+        k_l2_cut<<<nb, 256, 0, st>>>(c, C, p_begin, p_end, fpts, parts); ::tq::note_launch();
+        k_reduce_parts<<<1, 32, 0, st>>>(parts, nb, num_den); ::tq::note_launch();
     }
     TQ_LAUNCH_CHECK("tq_l2_parts");
     TQ_CUDA(cudaFreeAsync(parts, st));

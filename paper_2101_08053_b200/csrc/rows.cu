@@ -274,7 +274,7 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
                               tq_rules rules, double* a, void* stream) {
     int64_t total = (int64_t)s.n * (2 * s.p + 1);
     if (total == 0) return TQ_OK;
-    k_wq_products<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, lay, first, vals, rules, a);
+    k_wq_products<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, lay, first, vals, rules, a); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_wq_products");
     return TQ_OK;
 }
@@ -283,7 +283,7 @@ extern "C" int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream) {
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
     int grid = (int)std::min<int64_t>((nrows + kTileRows - 1) / kTileRows, (int64_t)kSms * 16);
-    k_row_counts<<<grid, 256, 0, S(stream)>>>(c, counts);
+    k_row_counts<<<grid, 256, 0, S(stream)>>>(c, counts); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts");
     return TQ_OK;
 }
@@ -296,12 +296,12 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     int tr = P <= 6 ? 64 : 32;
     int gridt = (int)std::min<int64_t>((nrows + tr - 1) / tr, (int64_t)kSms * 8);
     switch (P) {
-#define CASE(Q) case Q: k_fill_tiles<Q><<<gridt, 256, 0, S(stream)>>>(c, indptr, indices, data); break;
+#define CASE(Q) case Q: k_fill_tiles<Q><<<gridt, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch(); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
         default: {
             int grid = (int)std::min<int64_t>((nrows + 7) / 8, (int64_t)kSms * 32);
-            k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, indptr, indices, data);
+            k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch();
         }
     }
     TQ_LAUNCH_CHECK("k_fill_rows");
@@ -317,10 +317,10 @@ extern "C" int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_
     }
     int8_t* pos = nullptr;
     TQ_CUDA(cudaMallocAsync(&pos, c.n1 + c.n2, S(stream)));
-    k_pos<<<grid_for(c.n1, 128), 128, 0, S(stream)>>>(c.a1, c.n1, c.p1, c.ov_lo1, c.ov_hi1, pos);
-    k_pos<<<grid_for(c.n2, 128), 128, 0, S(stream)>>>(c.a2, c.n2, c.p2, c.ov_lo2, c.ov_hi2, pos + c.n1);
-    k_deep_init<<<grid_for(nf, 256), 256, 0, S(stream)>>>(c, func_class, pos, pos + c.n1, deep);
-    if (nraw > 0) k_deep_clear<<<grid_for(nraw, 128), 128, 0, S(stream)>>>(c, raw_rows, nraw, deep);
+    k_pos<<<grid_for(c.n1, 128), 128, 0, S(stream)>>>(c.a1, c.n1, c.p1, c.ov_lo1, c.ov_hi1, pos); ::tq::note_launch();
+    k_pos<<<grid_for(c.n2, 128), 128, 0, S(stream)>>>(c.a2, c.n2, c.p2, c.ov_lo2, c.ov_hi2, pos + c.n1); ::tq::note_launch();
+    k_deep_init<<<grid_for(nf, 256), 256, 0, S(stream)>>>(c, func_class, pos, pos + c.n1, deep); ::tq::note_launch();
+    if (nraw > 0) k_deep_clear<<<grid_for(nraw, 128), 128, 0, S(stream)>>>(c, raw_rows, nraw, deep); ::tq::note_launch();
     TQ_LAUNCH_CHECK("deep flags");
     TQ_CUDA(cudaFreeAsync(pos, S(stream)));
     return TQ_OK;

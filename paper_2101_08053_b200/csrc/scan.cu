@@ -131,9 +131,9 @@ int scan_generic(In in, int64_t n, Out out, int64_t* total_h, cudaStream_t st) {
     if (ntiles == 0) ntiles = 1;
     int64_t* tiles = nullptr;
     TQ_CUDA(cudaMallocAsync(&tiles, (ntiles + 1) * sizeof(int64_t), st));
-    k_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tiles);
-    k_scan_tiles<<<1, 1024, 0, st>>>(tiles, ntiles);
-    k_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tiles, out);
+    k_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tiles); ::tq::note_launch();
+    k_scan_tiles<<<1, 1024, 0, st>>>(tiles, ntiles); ::tq::note_launch();
+    k_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tiles, out); ::tq::note_launch();
     TQ_LAUNCH_CHECK("scan");
     if (total_h) {
         TQ_CUDA(cudaMemcpyAsync(total_h, tiles + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));

@@ -60,7 +60,7 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
         const int m = k1 - k0;
         const int j0 = s.ov_lo[i], t = s.ov_hi[i] - j0 + 1;
         if (m > mmax || t > tmax || wptr[i + 1] - wptr[i] != m) {
-            if (lane == 0) atomicOr(err, 1);
+            if (lane == 0) fail[r] = 2;   // bounds violation: reported through the fail flags
             continue;
         }
         // load A (t x m) and b
@@ -197,18 +197,10 @@ extern "C" int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, co
     size_t shm = per * sizeof(double) * wpb;
     if (shm > 200 * 1024) { set_error("moment system too large (t=%d, m=%d)", tmax, mmax); return TQ_EINVAL; }
     TQ_CUDA(cudaFuncSetAttribute(k_wq_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    int32_t* err = nullptr;
-    TQ_CUDA(cudaMallocAsync(&err, sizeof(int32_t), S(stream)));
-    TQ_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), S(stream)));
     int grid = (nrows + wpb - 1) / wpb;
     k_wq_solve<<<grid, 32 * wpb, shm, S(stream)>>>(s, lay, first, vals, mom, rows, nrows, tmax, mmax,
-                                                   wptr, k0, w, fail, err);
+                                                   wptr, k0, w, fail, nullptr); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_wq_solve");
-    int32_t herr = 0;
-    TQ_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, S(stream)));
-    TQ_CUDA(cudaFreeAsync(err, S(stream)));
-    TQ_CUDA(cudaStreamSynchronize(S(stream)));
-    if (herr) { set_error("moment system exceeds the declared bounds or weight slots"); return TQ_EINVAL; }
     return TQ_OK;
 }
 
@@ -217,7 +209,7 @@ extern "C" int tq_dwq_combine(const int32_t* rows, int32_t nrows, const int32_t*
                               tq_rules out_rules, void* stream) {
     if (nrows == 0) return TQ_OK;
     k_dwq_combine<<<grid_for(nrows, 64), 64, 0, S(stream)>>>(rows, nrows, s_colptr, s_rowidx, s_val,
-                                                             fine, out_rules);
+                                                             fine, out_rules); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_dwq_combine");
     return TQ_OK;
 }

@@ -110,7 +110,7 @@ class _Tables:
             X = mid[:, None] + half[:, None] * g.points[None, :]
             W = half[:, None] * g.weights[None, :]
             Xd = L.dev(X.ravel(), torch.float64)
-            _, V = b.eval_device(Xd)
+            _, V = b.eval_device(Xd, check=False)
             self.dirs.append((X, Xd, L.dev(W.ravel(), torch.float64), V, g.points.size))
 
 
@@ -145,8 +145,8 @@ class _CutPoints:
         self.rule = rule
         self.P = L.dev(rule.points.reshape(-1, 2), torch.float64).contiguous()
         self.W = L.dev(rule.weights, torch.float64)
-        self.f1, self.v1 = b1.eval_device(self.P[:, 0].contiguous())
-        self.f2, self.v2 = b2.eval_device(self.P[:, 1].contiguous())
+        self.f1, self.v1 = b1.eval_device(self.P[:, 0].contiguous(), check=False)
+        self.f2, self.v2 = b2.eval_device(self.P[:, 1].contiguous(), check=False)
         cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
         cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
         self.idx = L.dev(cutidx, torch.int32)
@@ -184,7 +184,7 @@ def assemble_rhs_device(problem: ProjectionProblem, row_range=None):
     cgrid = None if coeff.identity else coeff.grid_device(tabs.dirs[0][1], tabs.dirs[1][1])
     cut = fcw = None
     cut_rows = torch.empty(0, dtype=torch.int32, device=L.device())
-    if config.cut_elements:
+    if config.has_cuts():
         cut = _CutPoints(config, basis2d)
         fcw = _target_points(problem.target, cut.P, keep) * cut.W
         if not coeff.identity:
@@ -218,7 +218,7 @@ def l2_error_parts_device(coeffs_dev, problem, elem_range=None, point_range=None
     keep = []
     tdesc = _target_desc(problem.target, tabs, keep)
     cut = fpts = None
-    if config.cut_elements:
+    if config.has_cuts():
         cut = _CutPoints(config, basis2d)
         fpts = _target_points(problem.target, cut.P, keep)
     ne = b1.num_elements * b2.num_elements

@@ -141,19 +141,12 @@ def place_wq_points(basis: Basis1D) -> PointLayout:
     return _layout_from_counts(basis, _required_counts(basis))
 
 
-_mom_cache = {}
-
-
 def moments_device(basis: Basis1D):
-    """Banded exact 1-D mass matrix on the GPU, n x (2p+1) (cached per basis)."""
-    key = id(basis)
-    hit = _mom_cache.get(key)
-    if hit is not None and hit[0] is basis:
-        return hit[1]
+    """Banded exact 1-D mass matrix on the GPU, n x (2p+1); recomputed on
+    every call like mass_matrix_1d inside the reference's _solve_rows."""
     gx, gw = gauss_device(basis.p + 1)
     mom = torch.empty((basis.n, 2 * basis.p + 1), dtype=torch.float64, device=L.device())
     L.call("tq_moments_1d_g", basis.device(), L.ptr(gx), L.ptr(gw), basis.p + 1, L.ptr(mom), L.stream())
-    _mom_cache[key] = (basis, mom)
     return mom
 
 
@@ -220,7 +213,7 @@ class WeightedRuleSet:
     def basis_table(self):
         """(first, vals) of the basis at this layout's points (device)."""
         if self._basis_tab is None:
-            self._basis_tab = self.basis.eval_device(self.layout.device_points())
+            self._basis_tab = self.basis.eval_device(self.layout.device_points(), check=False)
         return self._basis_tab
 
 
@@ -249,29 +242,48 @@ def _row_lengths(basis, layout):
     return layout.offsets[e1 + 1] - layout.offsets[e0]
 
 
-def _solve_rows(basis: Basis1D, layout: PointLayout, which=None):
-    """GPU moment fits of the selected rows (src/quadrature.py:281-303).
-    Returns (wptr, k0, w device tensors, failing rows list)."""
+class _FitPlan:
+    """Host-side description of one batch of moment fits (sizes, row list,
+    weight offsets) with its device copies; depends on geometry only."""
+
+    def __init__(self, basis, layout, which=None):
+        self.basis, self.layout = basis, layout
+        lens = _row_lengths(basis, layout)
+        self.wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        self.rows_h = np.arange(basis.n, dtype=np.int32) if which is None else np.asarray(which, dtype=np.int32)
+        t = basis._ov_hi - basis._ov_lo + 1
+        self.tmax = int(t[self.rows_h].max()) if self.rows_h.size else 1
+        self.mmax = int(lens[self.rows_h].max()) if self.rows_h.size else 1
+        self.wptr = L.dev(self.wptr_h, torch.int64)
+        self.rows = L.dev(self.rows_h, torch.int32)
+
+
+def _solve_rows_async(plan: _FitPlan):
+    """Launch the GPU moment fits of a plan (src/quadrature.py:281-303).
+    Returns (wptr, k0, w, fail) device tensors; no host sync."""
+    basis, layout = plan.basis, plan.layout
     dev = L.device()
-    lens = _row_lengths(basis, layout)
-    wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    rows_h = np.arange(basis.n, dtype=np.int32) if which is None else np.asarray(which, dtype=np.int32)
-    wptr = L.dev(wptr_h, torch.int64)
     k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
-    w = torch.zeros(int(wptr_h[-1]), dtype=torch.float64, device=dev)
-    if rows_h.size == 0:
-        return wptr, k0, w, []
-    first, vals = basis.eval_device(layout.device_points())
-    mom = moments_device(basis)
-    t = basis._ov_hi - basis._ov_lo + 1
-    tmax = int(t[rows_h].max())
-    mmax = int(lens[rows_h].max())
-    fail = torch.zeros(rows_h.size, dtype=torch.int32, device=dev)
-    rows = L.dev(rows_h, torch.int32)
-    L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
-           L.ptr(rows), rows_h.size, tmax, mmax, L.ptr(wptr), L.ptr(k0), L.ptr(w), L.ptr(fail), L.stream())
-    failing = rows_h[fail.cpu().numpy() != 0].tolist()
-    return wptr, k0, w, failing
+    w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+    fail = torch.zeros(max(plan.rows_h.size, 1), dtype=torch.int32, device=dev)
+    if plan.rows_h.size:
+        first, vals = basis.eval_device(layout.device_points(), check=False)
+        mom = moments_device(basis)
+        L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
+               L.ptr(plan.rows), plan.rows_h.size, plan.tmax, plan.mmax, L.ptr(plan.wptr), L.ptr(k0), L.ptr(w),
+               L.ptr(fail), L.stream())
+    return plan.wptr, k0, w, fail
+
+
+def _failing(plan, fail):
+    return plan.rows_h[fail[: plan.rows_h.size].cpu().numpy() != 0].tolist() if plan.rows_h.size else []
+
+
+def _solve_rows(basis: Basis1D, layout: PointLayout, which=None):
+    """Synchronous variant: (wptr, k0, w device tensors, failing rows)."""
+    plan = _FitPlan(basis, layout, which)
+    wptr, k0, w, fail = _solve_rows_async(plan)
+    return wptr, k0, w, _failing(plan, fail)
 
 
 def _least_covered_element(basis, layout, i):
@@ -308,20 +320,26 @@ def _split_largest_gap(pts, a, b):
 
 
 def _augment_nested(layout: PointLayout, extra) -> PointLayout:
-    """Nested largest-gap augmentation, only where extra > 0 (src/quadrature.py:348-363)."""
+    """Nested largest-gap augmentation (src/quadrature.py:348-363); only the
+    elements with extra > 0 are rebuilt, the rest are spliced through."""
     extra = np.asarray(extra)
-    if not np.any(extra):
+    touched = np.nonzero(extra > 0)[0]
+    if touched.size == 0:
         return layout
-    groups = []
-    bp = layout.breakpoints
-    for e in range(layout.num_elements):
-        pts = layout.element_points(e)
-        if extra[e]:
-            pts = np.sort(pts)
-            for _ in range(int(extra[e])):
-                pts = np.sort(np.append(pts, _split_largest_gap(pts, bp[e], bp[e + 1])))
-        groups.append(pts)
-    return PointLayout(bp, groups)
+    bp, off, pts = layout.breakpoints, layout.offsets, layout.points
+    pieces, counts = [], np.diff(off).copy()
+    prev = 0
+    for e in touched:
+        pieces.append(pts[off[prev]: off[e]])
+        g = np.sort(pts[off[e]: off[e + 1]])
+        for _ in range(int(extra[e])):
+            g = np.sort(np.append(g, _split_largest_gap(g, bp[e], bp[e + 1])))
+        pieces.append(g)
+        counts[e] = g.size
+        prev = e + 1
+    pieces.append(pts[off[prev]:])
+    new_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return PointLayout(bp, points=np.concatenate(pieces), offsets=new_off)
 
 
 def dwq_layout(basis: Basis1D, layout: PointLayout, u: float):
@@ -330,62 +348,95 @@ def dwq_layout(basis: Basis1D, layout: PointLayout, u: float):
     refined, S = refine_to_c_minus_1(basis, u)
     need = _required_counts(refined)
     aug = _augment_nested(layout, np.maximum(need - layout.counts(), 0))
-    lens_needed = refined._ov_hi - refined._ov_lo + 1
-    for i in range(refined.n):
-        e0, e1 = refined.support_elements(i)
-        while aug.offsets[e1 + 1] - aug.offsets[e0] < lens_needed[i]:
+    t = refined._ov_hi - refined._ov_lo + 1
+    e0, e1 = refined._el_first, refined._el_last
+    short = np.nonzero(aug.offsets[e1 + 1] - aug.offsets[e0] < t)[0]
+    for i in short:        # top-up loop, in function order (usually empty)
+        i = int(i)
+        while aug.offsets[e1[i] + 1] - aug.offsets[e0[i]] < t[i]:
             bump = np.zeros(aug.num_elements, dtype=np.int64)
             bump[_least_covered_element(refined, aug, i)] = 1
             aug = _augment_nested(aug, bump)
     return refined, S, aug
 
 
+class DwqPlan:
+    """Geometry of one DWQ set (src/quadrature.py:382-418): refined basis,
+    subdivision matrix S, nested augmented layout, the refined rows to fit
+    and the output row layout.  Depends only on (basis, base layout, u_disc,
+    rows), never on weights."""
+
+    def __init__(self, basis, layout, u_disc, only_rows=None):
+        bp = basis.breakpoints
+        if not np.any(np.abs(bp - u_disc) <= 1e-12):
+            raise ValueError(f"{u_disc} is not a breakpoint of the basis")
+        self.basis, self.base_layout = basis, layout
+        self.u = float(bp[np.argmin(np.abs(bp - u_disc))])
+        self.refined, self.S, self.aug = dwq_layout(basis, layout, self.u)
+        Sc = self.S.matrix.tocsc()
+        Sc.sort_indices()
+        self.Sc = Sc
+        self.wanted = (np.arange(basis.n) if only_rows is None
+                       else np.array(sorted(set(int(r) for r in only_rows)), dtype=np.int64))
+        self.fine_needed = None
+        if only_rows is not None:
+            seen = set()
+            for j in self.wanted:
+                seen.update(Sc.indices[Sc.indptr[j]: Sc.indptr[j + 1]].tolist())
+            self.fine_needed = sorted(seen)
+        self._finalize()
+
+    def _finalize(self):
+        basis, aug = self.basis, self.aug
+        self.fit = _FitPlan(self.refined, aug, self.fine_needed)
+        lens = _row_lengths(basis, aug)
+        sel = np.zeros(basis.n, dtype=bool)
+        sel[self.wanted] = True
+        lens = np.where(sel, lens, 0)
+        self.wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        k0_h = np.where(sel, aug.offsets[basis._el_first], -1).astype(np.int32)
+        self.wptr, self.k0 = L.dev(self.wptr_h, torch.int64), L.dev(k0_h, torch.int32)
+        self.cp = L.dev(self.Sc.indptr.astype(np.int32), torch.int32)
+        self.ri = L.dev(self.Sc.indices.astype(np.int32), torch.int32)
+        self.sv = L.dev(self.Sc.data, torch.float64)
+        self.rows = L.dev(self.wanted.astype(np.int32), torch.int32)
+
+    def bump(self, failing):
+        """Enrichment retry of the refined fit (src/quadrature.py:420-432)."""
+        bump = np.zeros(self.aug.num_elements, dtype=np.int64)
+        for i in failing:
+            bump[_least_covered_element(self.refined, self.aug, i)] += 1
+        self.aug = _augment_nested(self.aug, bump)
+        self._finalize()
+
+
+def dwq_solve_async(plan: DwqPlan, direction=None, regular_side=None):
+    """Numeric part of DWQ on the GPU: refined fits, then w = S^T w~
+    (src/quadrature.py:420-444).  Returns (rule set, fail tensor)."""
+    fwptr, fk0, fw, fail = _solve_rows_async(plan.fit)
+    w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=L.device())
+    L.call("tq_dwq_combine", L.ptr(plan.rows), plan.wanted.size, L.ptr(plan.cp), L.ptr(plan.ri), L.ptr(plan.sv),
+           L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(plan.wptr), L.ptr(plan.k0), L.ptr(w)),
+           L.stream())
+    rs = DiscontinuousRuleSet(plan.basis, plan.aug, plan.wptr, plan.k0, w, plan.u, plan.S, plan.refined,
+                              plan.base_layout, direction, regular_side)
+    return rs, fail
+
+
 def build_dwq(basis: Basis1D, layout: PointLayout, u_disc: float, direction=None,
-              regular_side=None, only_rows=None) -> DiscontinuousRuleSet:
-    """Discontinuous WQ (src/quadrature.py:366-449): host layout, GPU fits of
-    the refined rows, GPU combination w = S^T w~."""
-    bp = basis.breakpoints
-    if not np.any(np.abs(bp - u_disc) <= 1e-12):
-        raise ValueError(f"{u_disc} is not a breakpoint of the basis")
-    u = float(bp[np.argmin(np.abs(bp - u_disc))])
-    refined, S, aug = dwq_layout(basis, layout, u)
-    Sc = S.matrix.tocsc()
-    Sc.sort_indices()
-    wanted = np.arange(basis.n) if only_rows is None else np.array(sorted(set(int(r) for r in only_rows)))
-    fine_needed = None
-    if only_rows is not None:
-        seen = set()
-        for j in wanted:
-            seen.update(Sc.indices[Sc.indptr[j]: Sc.indptr[j + 1]].tolist())
-        fine_needed = sorted(seen)
-    failing = []
+              regular_side=None, only_rows=None, plan=None) -> DiscontinuousRuleSet:
+    """Discontinuous WQ (src/quadrature.py:366-449): host layout plan, GPU
+    fits of the refined rows with enrichment retries, GPU w = S^T w~."""
+    plan = plan or DwqPlan(basis, layout, u_disc, only_rows)
     for attempt in range(MAX_RETRIES + 1):
-        fwptr, fk0, fw, failing = _solve_rows(refined, aug, fine_needed)
+        rs, fail = dwq_solve_async(plan, direction, regular_side)
+        failing = _failing(plan.fit, fail)
         if not failing:
-            break
+            return rs
         if attempt == MAX_RETRIES:
             raise RuleConstructionError(f"discontinuous rule fit failed for refined test functions "
-                                        f"{failing} at u_disc={u}")
-        bump = np.zeros(aug.num_elements, dtype=np.int64)
-        for i in failing:
-            bump[_least_covered_element(refined, aug, i)] += 1
-        aug = _augment_nested(aug, bump)
-    # output rows of the original functions over the augmented layout
-    lens = _row_lengths(basis, aug)
-    sel = np.zeros(basis.n, dtype=bool)
-    sel[wanted] = True
-    lens = np.where(sel, lens, 0)
-    wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    k0_h = np.where(sel, aug.offsets[basis._el_first], -1).astype(np.int32)
-    wptr, k0 = L.dev(wptr_h, torch.int64), L.dev(k0_h, torch.int32)
-    w = torch.zeros(int(wptr_h[-1]), dtype=torch.float64, device=L.device())
-    cp = L.dev(Sc.indptr.astype(np.int32), torch.int32)
-    ri = L.dev(Sc.indices.astype(np.int32), torch.int32)
-    sv = L.dev(Sc.data, torch.float64)
-    rows = L.dev(wanted.astype(np.int32), torch.int32)
-    L.call("tq_dwq_combine", L.ptr(rows), wanted.size, L.ptr(cp), L.ptr(ri), L.ptr(sv),
-           L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(wptr), L.ptr(k0), L.ptr(w)), L.stream())
-    return DiscontinuousRuleSet(basis, aug, wptr, k0, w, u, S, refined, layout, direction, regular_side)
+                                        f"{failing} at u_disc={plan.u}")
+        plan.bump(failing)
 
 
 def rules_from_arrays(basis, points, offsets, k0, wptr, w, direction=None, u_disc=None):

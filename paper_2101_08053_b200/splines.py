@@ -21,7 +21,13 @@ KNOT_TOL = 1e-12  # src/splines.py:29
 
 def _breakpoints(knots, tol=KNOT_TOL):
     """Unique values merging entries within tol of the running value
-    (src/splines.py:156-166)."""
+    (src/splines.py:156-166).  Vectorized when no gap lies in (0, tol]
+    (then the running-value rule and plain gap splitting coincide)."""
+    d = np.diff(knots)
+    if not np.any((d > 0) & (d <= tol)):
+        start = np.concatenate([[0], np.nonzero(d > tol)[0] + 1])
+        mult = np.diff(np.concatenate([start, [knots.size]])).astype(np.int64)
+        return knots[start], mult
     keep = [0]
     mult = [1]
     for k in range(1, knots.size):
@@ -167,16 +173,18 @@ class Basis1D:
         self.device()
         return self._dev[1]
 
-    def eval_device(self, u_dev, ders=False):
-        """GPU Cox-de Boor at device points -> (first int32, vals[, ders])."""
+    def eval_device(self, u_dev, ders=False, check=True):
+        """GPU Cox-de Boor at device points -> (first int32, vals[, ders]).
+        ``check`` reads the domain status back (a stream sync); internal
+        callers whose points are in the domain by construction skip it."""
         n = u_dev.numel()
         first = torch.empty(n, dtype=torch.int32, device=u_dev.device)
         vals = torch.empty((n, self.p + 1), dtype=torch.float64, device=u_dev.device)
         dv = torch.empty_like(vals) if ders else None
-        status = torch.zeros(1, dtype=torch.int32, device=u_dev.device)
+        status = torch.zeros(1, dtype=torch.int32, device=u_dev.device) if check else None
         L.call("tq_basis_eval", self.device(), L.ptr(u_dev), n, L.ptr(first), L.ptr(vals), L.ptr(dv),
                L.ptr(status), L.stream())
-        if int(status.item()) & 1:
+        if check and int(status.item()) & 1:
             raise ValueError("coordinate outside the knot domain")
         return (first, vals, dv) if ders else (first, vals)
 
@@ -274,14 +282,37 @@ def insert_knot(basis: Basis1D, ubar: float):
     return fine, SubdivisionMatrix(S, basis, fine)
 
 
+def _insertion_matrix(kn, p, ubar):
+    """Single-insertion map on a raw knot array (PAPER Eq. 9; the alpha rule
+    of src/splines.py:369-403)."""
+    n = kn.size - p - 1
+    l = int(np.clip(np.searchsorted(kn, ubar, side="right") - 1, p, n - 1))
+    k = np.arange(n + 1)
+    alpha = np.where(k <= l - p, 1.0, 0.0)
+    mid = np.arange(max(l - p + 1, 0), l + 1)
+    alpha[mid] = (ubar - kn[mid]) / (kn[mid + p] - kn[mid])
+    r = np.concatenate([np.arange(n), np.arange(1, n + 1)])
+    c = np.concatenate([np.arange(n), np.arange(n)])
+    S = sp.coo_matrix((np.concatenate([alpha[:n], 1.0 - alpha[1:]]), (r, c)), shape=(n + 1, n)).tocsr()
+    S.eliminate_zeros()
+    at = int(np.searchsorted(kn, ubar, side="right"))
+    return np.insert(kn, at, ubar), S
+
+
 def refine_to_c_minus_1(basis: Basis1D, u: float):
-    """Insert u up to multiplicity p+1 -> (refined basis, SubdivisionMatrix)."""
-    cur = basis
+    """Insert u up to multiplicity p+1 -> (refined basis, SubdivisionMatrix);
+    the composite of single insertions (src/splines.py:406-428)."""
+    kv = basis.kv
+    if not (kv.domain[0] <= u <= kv.domain[1]):
+        raise ValueError(f"insertion point {u} outside domain {kv.domain}")
+    kn = kv.knots
+    p = basis.p
     S = sp.identity(basis.n, format="csr")
-    for _ in range(basis.p + 1 - basis.kv.multiplicity_of(u)):
-        cur, step = insert_knot(cur, u)
-        S = step.matrix @ S
-    return cur, SubdivisionMatrix(S, basis, cur)
+    for _ in range(p + 1 - kv.multiplicity_of(u)):
+        kn, step = _insertion_matrix(kn, p, u)
+        S = step @ S
+    fine = Basis1D(KnotVector(kn, p))
+    return fine, SubdivisionMatrix(S, basis, fine)
 
 
 def make_uniform_knots(num_elements, degree, a=0.0, b=1.0):

@@ -78,6 +78,11 @@ class TrimConfiguration:
         e1, e2 = np.nonzero(self.element_class == CUT)
         return list(zip(e1.tolist(), e2.tolist()))
 
+    def has_cuts(self):
+        if not hasattr(self, "_has_cuts"):
+            self._has_cuts = bool(np.any(self.element_class == CUT))
+        return self._has_cuts
+
     @property
     def interior_elements(self):
         e1, e2 = np.nonzero(self.element_class == INTERIOR)
