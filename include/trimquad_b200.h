@@ -220,6 +220,12 @@ typedef struct {
     const double* cut_cw;            /* c * w per cut point */
     const int32_t* cfirst1; const double* cvals1;
     const int32_t* cfirst2; const double* cvals2;
+    const int32_t* grp_ptr;          /* ncut + 1: span-key groups of each cut element */
+    const int32_t* grp_key;          /* ngroups x 2: (first1, first2) of the group */
+    const int64_t* grp_pts;          /* ngroups + 1: ranges into grp_perm */
+    const int64_t* grp_perm;         /* cut points ordered by (element, key) */
+    double* grp_blocks;              /* ngroups x ((p1+1)(p2+1))^2 element blocks */
+    int32_t ngroups;
     const int32_t* desc;             /* nraw x 8: fidx, mode, set1, set2, a1, b1, a2, b2 */
     int32_t nraw;
     int32_t nmax1, nmax2;            /* max points of one rule row per direction */
@@ -232,8 +238,10 @@ typedef struct {
  * 522-528, 553-648). */
 int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
 
-/* cut-element part of raw rows [r0, r1) (accumulates).  Replaces
- * _Run.add_cut_blocks (src/assembly.py:369-398). */
+/* cut-element part of raw rows [r0, r1) (accumulates): element blocks
+ * B^T diag(c w) B per (cut element, span key) group, then a row gather.
+ * Replaces _Run.add_cut_blocks (src/assembly.py:369-398). */
+int tq_cut_blocks(tq_rawctx c, void* stream);
 int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
 
 /* coefficient c = det J of a B-spline geometry map on a tensor grid / at

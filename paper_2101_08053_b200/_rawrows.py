@@ -37,13 +37,15 @@ class RawCtx(C.Structure):
                 + [(k, L.vp) for k in ("ew1", "ev1", "ew2", "ev2", "em1", "em2", "cg", "sets1", "sets2")]
                 + [("nsets1", L.i32), ("nsets2", L.i32)]
                 + [(k, L.vp) for k in ("grids", "cutidx", "cut_ptr", "cut_cw", "cfirst1", "cvals1", "cfirst2",
-                                       "cvals2", "desc")]
+                                       "cvals2", "grp_ptr", "grp_key", "grp_pts", "grp_perm", "grp_blocks")]
+                + [("ngroups", L.i32), ("desc", L.vp)]
                 + [("nraw", L.i32), ("nmax1", L.i32), ("nmax2", L.i32), ("raw", L.vp)])
 
 
 def _bind():
     L.optional("tq_raw_regular", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_raw_cutcells", [RawCtx, L.i32, L.i32, L.vp])
+    L.optional("tq_cut_blocks", [RawCtx, L.vp])
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
@@ -101,15 +103,37 @@ def route_cut_rows(f):
 def cut_point_tables(f):
     """Device copy of the host cut-cell rule (cached per configuration)."""
     g = _geo(f.config)
-    if "cutpts" not in g:
+    rule = f.config.cut_cell_rule(max(f.b1.p, f.b2.p))
+    if g.get("cutpts_src") is not rule:      # rebuilt when the rule object changes
         b1, b2 = f.b1, f.b2
-        rule = f.config.cut_cell_rule(max(b1.p, b2.p))
         P = L.dev(rule.points.reshape(-1, 2), torch.float64)
         cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
         cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
-        g["cutpts"] = dict(P=P, x=P[:, 0].contiguous(), y=P[:, 1].contiguous(),
-                           W=L.dev(rule.weights, torch.float64), idx=L.dev(cutidx, torch.int32),
-                           ptr=L.dev(rule.ptr, torch.int64), npts=rule.total_points())
+        t = dict(P=P, x=P[:, 0].contiguous(), y=P[:, 1].contiguous(),
+                 W=L.dev(rule.weights, torch.float64), idx=L.dev(cutidx, torch.int32),
+                 ptr=L.dev(rule.ptr, torch.int64), npts=rule.total_points())
+        # span-key groups per cut element (src/assembly.py:380-388): points of
+        # one element grouped by (first1, first2), keys in np.unique order
+        f1, _ = b1.eval_device(t["x"], check=False)
+        f2, _ = b2.eval_device(t["y"], check=False)
+        f1, f2 = f1.cpu().numpy().astype(np.int64), f2.cpu().numpy().astype(np.int64)
+        gptr, gkey, gpts, perm = [0], [], [0], []
+        for k in range(rule.elements.shape[0]):
+            a, b = int(rule.ptr[k]), int(rule.ptr[k + 1])
+            keys = f1[a:b] * (b2.n + 1) + f2[a:b]
+            for key in np.unique(keys):
+                sel = np.nonzero(keys == key)[0] + a
+                perm.append(sel)
+                gkey.append((f1[sel[0]], f2[sel[0]]))
+                gpts.append(gpts[-1] + sel.size)
+            gptr.append(len(gkey))
+        t["grp_ptr"] = L.dev(np.asarray(gptr, np.int32), torch.int32)
+        t["grp_key"] = L.dev(np.asarray(gkey, np.int32).reshape(-1, 2), torch.int32)
+        t["grp_pts"] = L.dev(np.asarray(gpts, np.int64), torch.int64)
+        t["grp_perm"] = L.dev(np.concatenate(perm) if perm else np.zeros(1, np.int64), torch.int64)
+        t["ngroups"] = len(gkey)
+        g["cutpts"] = t
+        g["cutpts_src"] = rule
     return g["cutpts"]
 
 
@@ -253,8 +277,11 @@ class _Setup:
             f1, v1 = b1.eval_device(t["x"], check=False)
             f2, v2 = b2.eval_device(t["y"], check=False)
             cw = f.coeff.at_device(t["P"]) * t["W"] if not f.coeff.identity else t["W"]
+            Q = (b1.p + 1) * (b2.p + 1)
             self.cut = dict(idx=t["idx"], ptr=t["ptr"], cw=cw.contiguous(), f1=f1, v1=v1, f2=f2, v2=v2,
-                            npts=t["npts"])
+                            npts=t["npts"], grp_ptr=t["grp_ptr"], grp_key=t["grp_key"], grp_pts=t["grp_pts"],
+                            grp_perm=t["grp_perm"], ngroups=t["ngroups"],
+                            blocks=torch.empty(max(t["ngroups"], 1) * Q * Q, dtype=torch.float64, device=f.dev))
             f.report.n_cutcell_points = t["npts"]
 
     def ctx(self, desc, raw, nraw):
@@ -271,7 +298,9 @@ class _Setup:
                       P(self.cg), P(self.sets_dev[0]), P(self.sets_dev[1]),
                       len(self.sets[0]), len(self.sets[1]), P(self.grids),
                       P(cut.get("idx")), P(cut.get("ptr")), P(cut.get("cw")), P(cut.get("f1")), P(cut.get("v1")),
-                      P(cut.get("f2")), P(cut.get("v2")), P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
+                      P(cut.get("f2")), P(cut.get("v2")), P(cut.get("grp_ptr")), P(cut.get("grp_key")),
+                      P(cut.get("grp_pts")), P(cut.get("grp_perm")), P(cut.get("blocks")), cut.get("ngroups", 0),
+                      P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
 
 
 def _plan(f):
@@ -366,4 +395,5 @@ def run_phase(f, phase):
             L.call("tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells":
         if f._setup.cut is not None:
+            L.call("tq_cut_blocks", f._ctx, L.stream())
             L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())

@@ -14,6 +14,8 @@
 //
 // One warp per row; the row block, the two weighted collocation slices and
 // the inner contraction live in shared memory.
+#include <limits.h>
+
 #include "common.cuh"
 
 namespace tq {
@@ -184,47 +186,84 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     }
 }
 
-__global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
+// Element blocks of the cut elements: one block per (cut element, span key)
+// group, G[A][B] = sum_pts (c w) B_A B_B with A, B local (a1, a2) indices --
+// the B2d^T (cw B2d) of src/assembly.py:384-387.  Points staged in shared
+// memory 64 at a time; each thread owns entries of the Q x Q block.
+constexpr int kGrpStage = 64;
+
+__global__ void k_cut_blocks(tq_rawctx c) {
     extern __shared__ double sm[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
-    double* blk = sm + (size_t)wib * T;
-    const int q1 = c.p1 + 1, q2 = c.p2 + 1;
-    for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
+    const int q1 = c.p1 + 1, q2 = c.p2 + 1, Q = q1 * q2;
+    double* sv1 = sm;                       // kGrpStage x q1
+    double* sv2 = sv1 + kGrpStage * q1;     // kGrpStage x q2
+    double* scw = sv2 + kGrpStage * q2;     // kGrpStage
+    for (int g = blockIdx.x; g < c.ngroups; g += gridDim.x) {
+        const int64_t p0 = c.grp_pts[g], p1e = c.grp_pts[g + 1];
+        double acc[8];
+        for (int z = 0; z < 8; ++z) acc[z] = 0.0;
+        for (int64_t base = p0; base < p1e; base += kGrpStage) {
+            const int np = (int)(p1e - base < kGrpStage ? p1e - base : kGrpStage);
+            __syncthreads();
+            for (int q = threadIdx.x; q < np * (q1 + q2 + 1); q += blockDim.x) {
+                int k = q / (q1 + q2 + 1), o = q - k * (q1 + q2 + 1);
+                int64_t pt = c.grp_perm[base + k];
+                if (o < q1) sv1[k * q1 + o] = c.cvals1[pt * q1 + o];
+                else if (o < q1 + q2) sv2[k * q2 + (o - q1)] = c.cvals2[pt * q2 + (o - q1)];
+                else scw[k] = c.cut_cw[pt];
+            }
+            __syncthreads();
+            for (int z = 0; z < 8; ++z) {
+                int e = threadIdx.x + z * blockDim.x;
+                if (e >= Q * Q) break;
+                int A = e / Q, B = e - (e / Q) * Q;
+                int a1 = A / q2, a2 = A - (A / q2) * q2, b1 = B / q2, b2 = B - (B / q2) * q2;
+                double s = 0.0;
+                for (int k = 0; k < np; ++k)
+                    s += (sv1[k * q1 + a1] * sv2[k * q2 + a2]) * (scw[k] * (sv1[k * q1 + b1] * sv2[k * q2 + b2]));
+                acc[z] += s;
+            }
+        }
+        double* out = c.grp_blocks + (int64_t)g * Q * Q;
+        for (int z = 0; z < 8; ++z) {
+            int e = threadIdx.x + z * blockDim.x;
+            if (e < Q * Q) out[e] = acc[z];
+        }
+    }
+}
+
+// Row gather of the element blocks into the raw rows (warp per row).
+__global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int W2 = 2 * c.p2 + 1, T = (2 * c.p1 + 1) * W2;
+    const int q1 = c.p1 + 1, q2 = c.p2 + 1, Q = q1 * q2;
+    for (int r = r0 + blockIdx.x * wpb + (threadIdx.x >> 5); r < r1; r += gridDim.x * wpb) {
         RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
         const int ea1 = max(c.el_first1[i1] - 1, 0), eb1 = min(c.el_last1[i1] + 1, c.nel1 - 1);
         const int ea2 = max(c.el_first2[i2] - 1, 0), eb2 = min(c.el_last2[i2] + 1, c.nel2 - 1);
-        bool any = false;
-        double* src = c.raw + (int64_t)r * T;
-        for (int e1 = ea1; e1 <= eb1; ++e1) {
-            for (int e2 = ea2; e2 <= eb2; ++e2) {
-                int id = c.cutidx[(int64_t)e1 * c.nel2 + e2];
-                if (id < 0) continue;
-                if (!any) {
-                    for (int q = lane; q < T; q += 32) blk[q] = src[q];
-                    __syncwarp();
-                    any = true;
-                }
-                for (int64_t pt = c.cut_ptr[id]; pt < c.cut_ptr[id + 1]; ++pt) {
-                    const int f1 = c.cfirst1[pt], f2 = c.cfirst2[pt];
+        const int w2 = eb2 - ea2 + 1, nh = (eb1 - ea1 + 1) * w2;
+        double* dst = c.raw + (int64_t)r * T;
+        for (int h0 = 0; h0 < nh; h0 += 32) {
+            int h = h0 + lane;
+            int id = -1;
+            if (h < nh) id = c.cutidx[(int64_t)(ea1 + h / w2) * c.nel2 + (ea2 + h % w2)];
+            unsigned m = __ballot_sync(0xffffffffu, id >= 0);
+            while (m) {
+                int src = __ffs(m) - 1;
+                m &= m - 1;
+                int cid = __shfl_sync(0xffffffffu, id, src);
+                for (int g = c.grp_ptr[cid]; g < c.grp_ptr[cid + 1]; ++g) {
+                    const int f1 = c.grp_key[2 * g], f2 = c.grp_key[2 * g + 1];
                     const int a1 = i1 - f1, a2 = i2 - f2;
                     if (a1 < 0 || a1 > c.p1 || a2 < 0 || a2 > c.p2) continue;
-                    const double* v1 = c.cvals1 + pt * q1;
-                    const double* v2 = c.cvals2 + pt * q2;
-                    const double bi = v1[a1] * v2[a2];
-                    const double cw = c.cut_cw[pt];
-                    for (int q = lane; q < q1 * q2; q += 32) {
-                        int b1 = q / q2, b2 = q - (q / q2) * q2;
-                        blk[(f1 + b1 - i1 + c.p1) * W2 + (f2 + b2 - i2 + c.p2)] += bi * (cw * (v1[b1] * v2[b2]));
+                    const double* G = c.grp_blocks + ((int64_t)g * Q + (a1 * q2 + a2)) * Q;
+                    for (int B = lane; B < Q; B += 32) {
+                        int b1 = B / q2, b2 = B - (B / q2) * q2;
+                        dst[(f1 + b1 - i1 + c.p1) * W2 + (f2 + b2 - i2 + c.p2)] += G[B];
                     }
-                    __syncwarp();
                 }
             }
-        }
-        if (any) {
-            for (int q = lane; q < T; q += 32) src[q] = blk[q];
-            __syncwarp();
         }
     }
 }
@@ -286,13 +325,20 @@ extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream)
     return TQ_OK;
 }
 
+extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
+    if (c.ngroups <= 0) return TQ_OK;
+    const int Q = (c.p1 + 1) * (c.p2 + 1);
+    if (Q * Q > 8 * 1024) { set_error("degree too high for the cut-block kernel"); return TQ_EINVAL; }
+    size_t shm = sizeof(double) * kGrpStage * (c.p1 + c.p2 + 3);
+    k_cut_blocks<<<(int)std::min<int64_t>(c.ngroups, (int64_t)kSms * 16), 1024, shm, S(stream)>>>(c); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_cut_blocks");
+    return TQ_OK;
+}
+
 extern "C" int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
-    if (r1 <= r0 || !c.cut_ptr) return TQ_OK;
-    int wpb = 4;
-    size_t shm = sizeof(double) * (2 * c.p1 + 1) * (2 * c.p2 + 1) * wpb;
-    TQ_CUDA(cudaFuncSetAttribute(k_raw_cutcells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
-    k_raw_cutcells<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    if (r1 <= r0 || !c.cut_ptr || c.ngroups <= 0) return TQ_OK;
+    int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 16);
+    k_raw_cutcells<<<grid, 256, 0, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_cutcells");
     return TQ_OK;
 }

@@ -171,6 +171,63 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
             s_cb[t][o] = cb;
         }
         __syncthreads();
+        // phase 3a: uniform tile (all rows deep with full windows) -> the tile
+        // is one contiguous CSR span of nr*W*W entries: flat emit with
+        // 16-byte vector stores (int4 indices, 2 x double2 values per quad)
+        __shared__ int s_uniform;
+        if (threadIdx.x == 0) {
+            int u = 1;
+            for (int t = 0; t < nr; ++t)
+                u &= (s_deep[t] && s_geo[t][2] == W && s_geo[t][3] == W) ? 1 : 0;
+            s_uniform = u;
+        }
+        __syncthreads();
+        if (s_uniform) {
+            constexpr int WW = W * W;
+            const int n = nr * WW;
+            const int pos0 = s_pos[0];
+            const int head = (4 - (pos0 & 3)) & 3;
+            auto coord = [&](int e, int& t, int& q1, int& q2) {
+                t = e / WW;
+                int rem = e - t * WW;
+                q1 = rem / W;
+                q2 = rem - q1 * W;
+            };
+            auto value = [&](int t, int q1, int q2) {
+                return 0.5 * (s_f[t][0][q1] * s_f[t][2][q2] + s_f[t][1][q1] * s_f[t][3][q2]);
+            };
+            // ragged head and tail, scalar
+            const int nq = (n - head) >> 2;
+            const int tail0 = head + 4 * nq;
+            for (int e = threadIdx.x; e < head + (n - tail0); e += blockDim.x) {
+                int ee = e < head ? e : tail0 + (e - head);
+                if (ee >= n) continue;
+                int t, q1, q2;
+                coord(ee, t, q1, q2);
+                indices[pos0 + ee] = s_cb[t][q1] + q2;
+                data[pos0 + ee] = value(t, q1, q2);
+            }
+            int4* idx4 = reinterpret_cast<int4*>(indices + pos0 + head);
+            double2* dat2 = reinterpret_cast<double2*>(data + pos0 + head);
+            for (int k = threadIdx.x; k < nq; k += blockDim.x) {
+                int e = head + 4 * k;
+                int t, q1, q2;
+                coord(e, t, q1, q2);
+                int c[4];
+                double v[4];
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    c[z] = s_cb[t][q1] + q2;
+                    v[z] = value(t, q1, q2);
+                    if (++q2 == W) { q2 = 0; if (++q1 == W) { q1 = 0; ++t; } }
+                }
+                idx4[k] = make_int4(c[0], c[1], c[2], c[3]);
+                dat2[2 * k] = make_double2(v[0], v[1]);
+                dat2[2 * k + 1] = make_double2(v[2], v[3]);
+            }
+            __syncthreads();
+            continue;
+        }
         // phase 3: emit
         for (int t = warp; t < nr; t += nwarps) {
             int pos = s_pos[t];
@@ -294,9 +351,14 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     if (nrows <= 0) return TQ_OK;
     int P = (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0;
     int tr = P <= 6 ? 64 : 32;
-    int gridt = (int)std::min<int64_t>((nrows + tr - 1) / tr, (int64_t)kSms * 8);
+    auto wave = [&](const void* fn) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+        int64_t full = (int64_t)kSms * std::max(per_sm, 1);
+        return (int)std::min<int64_t>((nrows + tr - 1) / tr, full);
+    };
     switch (P) {
-#define CASE(Q) case Q: k_fill_tiles<Q><<<gridt, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch(); break;
+#define CASE(Q) case Q: k_fill_tiles<Q><<<wave((const void*)k_fill_tiles<Q>), 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch(); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
         default: {
