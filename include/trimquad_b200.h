@@ -169,6 +169,8 @@ typedef struct {
     const double* raw;           /* nslots * (2p1+1)*(2p2+1) */
     const int8_t* deep;          /* n1*n2: 1 = separable row whose window holds
                                     only separable rows with positive factors */
+    int8_t* rowfast;             /* per active row (written by tq_row_counts):
+                                    deep with full (2p+1)^2 windows */
     int32_t row_begin, row_end;  /* active rows [begin, end) */
 } tq_rowctx;
 

@@ -263,6 +263,7 @@ class Formation:
         self.raw = None
         self.raw_list = torch.empty(0, dtype=torch.int32, device=self.dev)   # raw-row function ids
         self.deep = None
+        self.rowfast = None
         self.rules = None
         self.report = FormationReport(strategy)
         self.timer = timer or _NoTimer()
@@ -308,7 +309,7 @@ class Formation:
                         L.ptr(self.a1 if self.a1 is not None else dummy),
                         L.ptr(self.a2 if self.a2 is not None else dummy),
                         L.ptr(self.raw if self.raw is not None else dummy),
-                        L.ptr(self.deep), row_begin, self.K if row_end is None else row_end)
+                        L.ptr(self.deep), L.ptr(self.rowfast), row_begin, self.K if row_end is None else row_end)
 
     def finish(self, row_begin=0, row_end=None) -> DeviceCSR:
         """Count -> scan -> fill: symmetrised, zero-dropped, sorted CSR rows
@@ -320,6 +321,7 @@ class Formation:
             self.deep = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
             L.call("tq_deep_flags", self.rowctx(), L.ptr(self.config.func_class_dev), L.ptr(self.raw_list),
                    self.raw_list.numel(), L.ptr(self.deep), L.stream())
+        self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
         with self.timer("counts"):

@@ -16,6 +16,8 @@
 //                  written by the cut-row / general-coefficient kernels.
 // The kept pattern is decided by value, (M_ij + M_ji) != 0, exactly the
 // scipy CSR-add zero drop of the reference.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace tq {
@@ -95,7 +97,9 @@ __global__ void k_row_counts(tq_rowctx c, int32_t* __restrict__ counts) {
                 int idx = c.active[r];
                 if (c.deep && c.deep[idx]) {
                     int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
-                    counts[r - c.row_begin] = (c.ov_hi1[i1] - c.ov_lo1[i1] + 1) * (c.ov_hi2[i2] - c.ov_lo2[i2] + 1);
+                    int t1 = c.ov_hi1[i1] - c.ov_lo1[i1] + 1, t2 = c.ov_hi2[i2] - c.ov_lo2[i2] + 1;
+                    counts[r - c.row_begin] = t1 * t2;
+                    if (c.rowfast) c.rowfast[r - c.row_begin] = (t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1) ? 1 : 0;
                 } else {
                     todo[atomicAdd(&ntodo, 1)] = r;
                 }
@@ -118,150 +122,213 @@ __global__ void k_row_counts(tq_rowctx c, int32_t* __restrict__ counts) {
     }
 }
 
-// Tile fill: a block stages kTileRows rows -- metadata (phase 1) and, for
-// deep rows, the 5(2P+1) direction factors and column bases (phase 2) -- in
-// shared memory, then each warp emits whole CSR rows from shared memory with
-// coalesced stores (phase 3).  Two dependent-load rounds per tile instead of
-// three per row.
+// ---------------------------------------------------------------------------
+// Fill kernel (separable path).  Work unit: a warp tile of 32 consecutive
+// active rows, assigned statically; the next tile's per-row words (active id,
+// CSR offset, fast flag from the count pass) are prefetched while the
+// current tile is processed.
+//
+//  regular tile -- 32 deep full-window rows on one i1-line with consecutive
+//    i2 (94% of the tiles at config 5): the direction-1 factors and column
+//    bases are shared by the whole tile and the direction-2 factors form one
+//    contiguous band, so a single round of coalesced loads feeds 32 rows.
+//    Rows are built in shared memory, kChunk rows at a time, lane -> (q1, q2)
+//    with q2 = lane % W fixed, and written to HBM by TMA bulk copies
+//    (cp.async.bulk.global.shared::cta), double-buffered per warp; the
+//    16-byte-unaligned ends go through plain stores.
+//  irregular tile -- recorded in a list and processed by k_fill_irregular,
+//    one warp per row over the whole GPU (these tiles cluster along the
+//    trimming curve; row-parallel processing keeps them off the critical path).
+// ---------------------------------------------------------------------------
+constexpr int kWarpRows = 32;
+
+template <int P>
+constexpr int fill_chunk() { return (2 * P + 1) * (2 * P + 1) <= 81 ? 4 : ((2 * P + 1) * (2 * P + 1) <= 169 ? 2 : 1); }
+
+template <int P>
+struct alignas(16) FillStage {
+    static constexpr int WW = (2 * P + 1) * (2 * P + 1);
+    double d[fill_chunk<P>() * WW + 2];
+    int x[fill_chunk<P>() * WW + 4];
+};
+
+template <int P>
+struct alignas(16) RegularSlice {
+    static constexpr int W = 2 * P + 1;
+    FillStage<P> stage[2];
+    double l1[W], l1t[W];
+    int lcb[W];
+    double band[(32 + 2 * P) * W];
+};
+
+template <int P>
+constexpr size_t fill_slice_bytes() { return (sizeof(RegularSlice<P>) + 15) / 16 * 16; }
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int P>
+__device__ __forceinline__ void emit_regular(const tq_rowctx& c, RegularSlice<P>& S, int lane, int i1, int i20,
+                                             int pos0, int& nbulk, int32_t* __restrict__ indices,
+                                             double* __restrict__ data) {
+    constexpr int W = 2 * P + 1, WW = W * W, R = 32 / W, CH = fill_chunk<P>(), n = CH * WW;
+    if (lane < W) {
+        const int j1 = i1 - P + lane;
+        S.l1[lane] = __ldg(c.a1 + (int64_t)i1 * W + lane);
+        S.l1t[lane] = __ldg(c.a1 + (int64_t)j1 * W + (2 * P - lane));
+        S.lcb[lane] = __ldg(c.col_of + (int64_t)j1 * c.n2 + (i20 - P));
+    }
+    const double* bsrc = c.a2 + (int64_t)(i20 - P) * W;
+    for (int q = lane; q < (32 + 2 * P) * W; q += 32) S.band[q] = __ldg(bsrc + q);
+    __syncwarp();
+    const bool act = lane < R * W;
+    const int q2 = lane % W, r0 = lane / W;
+    for (int k = 0; k < 32 / CH; ++k) {
+        FillStage<P>& st = S.stage[nbulk & 1];
+        if (lane == 0 && nbulk >= 2) bulk_wait_read1();   // last reader of this buffer is done
+        __syncwarp();
+        const int pos = pos0 + k * n;
+        const int offd = pos & 1, offx = pos & 3;
+        for (int tt = 0; tt < CH; ++tt) {
+            const int t = k * CH + tt;
+            const double a2 = S.band[(t + P) * W + q2], a2t = S.band[(t + q2) * W + (2 * P - q2)];
+#pragma unroll
+            for (int m = 0; m < (W + R - 1) / R; ++m) {
+                const int q1 = m * R + r0;
+                if (act && q1 < W) {
+                    const int e = tt * WW + q1 * W + q2;
+                    st.x[offx + e] = S.lcb[q1] + t + q2;
+                    st.d[offd + e] = 0.5 * (S.l1[q1] * a2 + S.l1t[q1] * a2t);
+                }
+            }
+        }
+        fence_async_shared();
+        __syncwarp();
+        const int sd = (pos + 1) & ~1, ed = (pos + n) & ~1;
+        const int sx = (pos + 3) & ~3, ex = (pos + n) & ~3;
+        if (lane == 0) {
+            bulk_store(data + sd, st.d + (sd - (pos & ~1)), (unsigned)(ed - sd) * 8u);
+            bulk_store(indices + sx, st.x + (sx - (pos & ~3)), (unsigned)(ex - sx) * 4u);
+            bulk_commit();
+        }
+        ++nbulk;
+        if (lane == 1 && sd > pos) data[pos] = st.d[offd];
+        if (lane == 2 && ed < pos + n) data[pos + n - 1] = st.d[offd + n - 1];
+        if (lane >= 3 && lane < 3 + (sx - pos)) indices[pos + lane - 3] = st.x[offx + lane - 3];
+        if (lane >= 8 && lane < 8 + (pos + n - ex)) indices[ex + lane - 8] = st.x[offx + (ex - pos) + lane - 8];
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* __restrict__ indptr,
-                                                     int32_t* __restrict__ indices, double* __restrict__ data) {
-    constexpr int W = 2 * P + 1;
-    constexpr int kTileRows = P <= 6 ? 64 : 32;
-    __shared__ int s_idx[kTileRows], s_pos[kTileRows], s_geo[kTileRows][4];  // j1lo j2lo t1 t2
-    __shared__ unsigned char s_deep[kTileRows];
-    __shared__ double s_f[kTileRows][4][W];   // A1 A1T A2 A2T
-    __shared__ int s_cb[kTileRows][W];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int R0 = c.row_begin + blockIdx.x * kTileRows; R0 < c.row_end; R0 += gridDim.x * kTileRows) {
-        const int nr = min(kTileRows, c.row_end - R0);
-        if (threadIdx.x < nr) {
-            int t = threadIdx.x, r = R0 + t;
-            int idx = __ldg(c.active + r);
-            int i1 = idx / c.n2, i2 = idx - i1 * c.n2;
-            s_idx[t] = idx;
-            s_pos[t] = __ldg(indptr + (r - c.row_begin));
-            s_deep[t] = c.deep ? __ldg(c.deep + idx) : 0;
-            s_geo[t][0] = __ldg(c.ov_lo1 + i1);
-            s_geo[t][1] = __ldg(c.ov_lo2 + i2);
-            s_geo[t][2] = __ldg(c.ov_hi1 + i1) - s_geo[t][0] + 1;
-            s_geo[t][3] = __ldg(c.ov_hi2 + i2) - s_geo[t][1] + 1;
+                                                     int32_t* __restrict__ indices, double* __restrict__ data,
+                                                     int* __restrict__ irr_list, int* __restrict__ irr_count) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    unsigned char* slice = smraw + fill_slice_bytes<P>() * wib;
+    const int nwarps = gridDim.x * wpb;
+    int nbulk = 0;
+    int R0 = c.row_begin + (blockIdx.x * wpb + wib) * kWarpRows;
+    int n_idx = 0, n_pos = 0, n_fast = 0;
+    if (R0 + lane < c.row_end) {
+        n_idx = __ldg(c.active + R0 + lane);
+        n_pos = __ldg(indptr + (R0 + lane - c.row_begin));
+        n_fast = c.rowfast ? __ldg(c.rowfast + (R0 + lane - c.row_begin)) : 0;
+    }
+    for (; R0 < c.row_end; R0 += nwarps * kWarpRows) {
+        const int nr = min(kWarpRows, c.row_end - R0);
+        const int my_idx = n_idx, my_pos = n_pos, my_fast = n_fast;
+        const int R1 = R0 + nwarps * kWarpRows;
+        if (R1 + lane < c.row_end) {
+            n_idx = __ldg(c.active + R1 + lane);
+            n_pos = __ldg(indptr + (R1 + lane - c.row_begin));
+            n_fast = c.rowfast ? __ldg(c.rowfast + (R1 + lane - c.row_begin)) : 0;
         }
-        __syncthreads();
-        // phase 2: factors of deep rows, (row, lane-slot) spread over the block
-        for (int q = threadIdx.x; q < nr * W; q += blockDim.x) {
-            int t = q / W, o = q - t * W;
-            if (!s_deep[t]) continue;
-            int idx = s_idx[t];
-            int i1 = idx / c.n2, i2 = idx - i1 * c.n2;
-            int j1 = i1 - P + o, j2 = i2 - P + o;
-            double A1 = 0.0, A1T = 0.0, A2 = 0.0, A2T = 0.0;
-            int cb = 0;
-            if (j1 >= s_geo[t][0] && j1 < s_geo[t][0] + s_geo[t][2]) {
-                A1 = __ldg(c.a1 + (int64_t)i1 * W + o);
-                A1T = __ldg(c.a1 + (int64_t)j1 * W + (2 * P - o));
-                cb = __ldg(c.col_of + (int64_t)j1 * c.n2 + s_geo[t][1]);
-            }
-            if (j2 >= s_geo[t][1] && j2 < s_geo[t][1] + s_geo[t][3]) {
-                A2 = __ldg(c.a2 + (int64_t)i2 * W + o);
-                A2T = __ldg(c.a2 + (int64_t)j2 * W + (2 * P - o));
-            }
-            s_f[t][0][o] = A1; s_f[t][1][o] = A1T; s_f[t][2][o] = A2; s_f[t][3][o] = A2T;
-            s_cb[t][o] = cb;
-        }
-        __syncthreads();
-        // phase 3a: uniform tile (all rows deep with full windows) -> the tile
-        // is one contiguous CSR span of nr*W*W entries: flat emit with
-        // 16-byte vector stores (int4 indices, 2 x double2 values per quad)
-        __shared__ int s_uniform;
-        if (threadIdx.x == 0) {
-            int u = 1;
-            for (int t = 0; t < nr; ++t)
-                u &= (s_deep[t] && s_geo[t][2] == W && s_geo[t][3] == W) ? 1 : 0;
-            s_uniform = u;
-        }
-        __syncthreads();
-        if (s_uniform) {
-            constexpr int WW = W * W;
-            const int n = nr * WW;
-            const int pos0 = s_pos[0];
-            const int head = (4 - (pos0 & 3)) & 3;
-            auto coord = [&](int e, int& t, int& q1, int& q2) {
-                t = e / WW;
-                int rem = e - t * WW;
-                q1 = rem / W;
-                q2 = rem - q1 * W;
-            };
-            auto value = [&](int t, int q1, int q2) {
-                return 0.5 * (s_f[t][0][q1] * s_f[t][2][q2] + s_f[t][1][q1] * s_f[t][3][q2]);
-            };
-            // ragged head and tail, scalar
-            const int nq = (n - head) >> 2;
-            const int tail0 = head + 4 * nq;
-            for (int e = threadIdx.x; e < head + (n - tail0); e += blockDim.x) {
-                int ee = e < head ? e : tail0 + (e - head);
-                if (ee >= n) continue;
-                int t, q1, q2;
-                coord(ee, t, q1, q2);
-                indices[pos0 + ee] = s_cb[t][q1] + q2;
-                data[pos0 + ee] = value(t, q1, q2);
-            }
-            int4* idx4 = reinterpret_cast<int4*>(indices + pos0 + head);
-            double2* dat2 = reinterpret_cast<double2*>(data + pos0 + head);
-            for (int k = threadIdx.x; k < nq; k += blockDim.x) {
-                int e = head + 4 * k;
-                int t, q1, q2;
-                coord(e, t, q1, q2);
-                int c[4];
-                double v[4];
-#pragma unroll
-                for (int z = 0; z < 4; ++z) {
-                    c[z] = s_cb[t][q1] + q2;
-                    v[z] = value(t, q1, q2);
-                    if (++q2 == W) { q2 = 0; if (++q1 == W) { q1 = 0; ++t; } }
-                }
-                idx4[k] = make_int4(c[0], c[1], c[2], c[3]);
-                dat2[2 * k] = make_double2(v[0], v[1]);
-                dat2[2 * k + 1] = make_double2(v[2], v[3]);
-            }
-            __syncthreads();
+        const int idx0 = __shfl_sync(0xffffffffu, my_idx, 0);
+        const bool regular = nr == 32 &&
+            __all_sync(0xffffffffu, my_fast && my_idx == idx0 + lane && my_idx / c.n2 == idx0 / c.n2);
+        if (regular) {
+            const int i1 = idx0 / c.n2;
+            emit_regular<P>(c, *reinterpret_cast<RegularSlice<P>*>(slice), lane, i1, idx0 - i1 * c.n2,
+                            __shfl_sync(0xffffffffu, my_pos, 0), nbulk, indices, data);
+            __syncwarp();
             continue;
         }
-        // phase 3: emit
-        for (int t = warp; t < nr; t += nwarps) {
-            int pos = s_pos[t];
-            int j1lo = s_geo[t][0], j2lo = s_geo[t][1], t1 = s_geo[t][2], t2 = s_geo[t][3];
-            int n = t1 * t2;
-            if (s_deep[t]) {
-                int idx = s_idx[t];
-                int i1 = idx / c.n2, i2 = idx - i1 * c.n2;
-                int off1 = j1lo - (i1 - P), off2 = j2lo - (i2 - P);
-                for (int e = lane; e < n; e += 32) {
-                    int q1 = (t2 == W) ? e / W : e / t2;
-                    int q2 = e - q1 * t2;
-                    int o1 = off1 + q1, o2 = off2 + q2;
-                    double v = s_f[t][0][o1] * s_f[t][2][o2] + s_f[t][1][o1] * s_f[t][3][o2];
-                    indices[pos + e] = s_cb[t][o1] + q2;
-                    data[pos + e] = 0.5 * v;
+        // irregular tile: handed to k_fill_irregular (row-parallel over the GPU)
+        if (lane == 0) irr_list[atomicAdd(irr_count, 1)] = R0;
+    }
+    if (lane == 0) bulk_wait_all();
+}
+
+// Rows of the irregular tiles, one warp per row over the whole GPU: deep
+// rows from their direction factors (lanes 0..2P hold A1, A1T, column base,
+// A2, A2T; entries built by shuffles), other rows through the value-based
+// symmetrise/compact path.
+template <int P>
+__global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32_t* __restrict__ indptr,
+                                                         int32_t* __restrict__ indices, double* __restrict__ data,
+                                                         const int* __restrict__ irr_list,
+                                                         const int* __restrict__ irr_count) {
+    constexpr int W = 2 * P + 1;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nrows = *irr_count * kWarpRows;
+    for (int u = warp; u < nrows; u += nw) {
+        const int r = irr_list[u / kWarpRows] + (u % kWarpRows);
+        if (r >= c.row_end) continue;
+        RowGeom g = row_geom(c, r);
+        int pos = __ldg(indptr + (r - c.row_begin));
+        const int n = g.t1 * g.t2;
+        if (c.deep[c.active[r]]) {
+            double A1 = 0.0, A1T = 0.0, A2 = 0.0, A2T = 0.0;
+            int CB = 0;
+            if (lane < W) {
+                const int j1 = g.i1 - P + lane, j2 = g.i2 - P + lane;
+                if (j1 >= g.j1lo && j1 < g.j1lo + g.t1) {
+                    A1 = __ldg(c.a1 + (int64_t)g.i1 * W + lane);
+                    A1T = __ldg(c.a1 + (int64_t)j1 * W + (2 * P - lane));
+                    CB = __ldg(c.col_of + (int64_t)j1 * c.n2 + g.j2lo);
                 }
-            } else {
-                RowGeom g = row_geom(c, R0 + t);
-                for (int e0 = 0; e0 < n; e0 += 32) {
-                    int e = e0 + lane;
-                    double v = 0.0;
-                    int col = e < n ? entry(c, g, e, v) : -1;
-                    unsigned m = __ballot_sync(0xffffffffu, col >= 0);
-                    if (col >= 0) {
-                        int at = pos + __popc(m & lt);
-                        indices[at] = col;
-                        data[at] = 0.5 * v;
-                    }
-                    pos += __popc(m);
+                if (j2 >= g.j2lo && j2 < g.j2lo + g.t2) {
+                    A2 = __ldg(c.a2 + (int64_t)g.i2 * W + lane);
+                    A2T = __ldg(c.a2 + (int64_t)j2 * W + (2 * P - lane));
                 }
             }
+            const int off1 = g.j1lo - (g.i1 - P), off2 = g.j2lo - (g.i2 - P);
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                const int ee = e < n ? e : n - 1;
+                const int q1 = ee / g.t2, q2 = ee - q1 * g.t2;
+                const int o1 = off1 + q1, o2 = off2 + q2;
+                const double a1 = __shfl_sync(0xffffffffu, A1, o1), a1t = __shfl_sync(0xffffffffu, A1T, o1);
+                const double a2 = __shfl_sync(0xffffffffu, A2, o2), a2t = __shfl_sync(0xffffffffu, A2T, o2);
+                const int cb = __shfl_sync(0xffffffffu, CB, o1);
+                if (e < n) {
+                    indices[pos + e] = cb + q2;
+                    data[pos + e] = 0.5 * (a1 * a2 + a1t * a2t);
+                }
+            }
+        } else {
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                double v = 0.0;
+                const int col = e < n ? entry(c, g, e, v) : -1;
+                const unsigned m = __ballot_sync(0xffffffffu, col >= 0);
+                if (col >= 0) {
+                    const int at = pos + __popc(m & lt);
+                    indices[at] = col;
+                    data[at] = 0.5 * v;
+                }
+                pos += __popc(m);
+            }
         }
-        __syncthreads();
     }
 }
 
@@ -350,15 +417,29 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
     int P = (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0;
-    int tr = P <= 6 ? 64 : 32;
-    auto wave = [&](const void* fn) {
+    int* irr = nullptr;   // [0] = count, [1..] = tile starts
+    const int ntiles = (nrows + kWarpRows - 1) / kWarpRows;
+    auto launch = [&](auto kern, auto kirr, size_t per_warp) -> int {
+        int wpb = 8;
+        while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
+        const size_t shm = per_warp * wpb;
+        TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
-        int64_t full = (int64_t)kSms * std::max(per_sm, 1);
-        return (int)std::min<int64_t>((nrows + tr - 1) / tr, full);
+        TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, shm));
+        const char* env = getenv("TQ_FILL_BPS");   // tuning knob (blocks per SM)
+        if (env && atoi(env) > 0) per_sm = std::min(per_sm, atoi(env));
+        const int64_t full = (int64_t)kSms * std::max(per_sm, 1);
+        const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
+        TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (ntiles + 1), S(stream)));
+        TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), S(stream)));
+        kern<<<grid, 32 * wpb, shm, S(stream)>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
+        kirr<<<kSms * 8, 256, 0, S(stream)>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
+        TQ_CUDA(cudaFreeAsync(irr, S(stream)));
+        return TQ_OK;
     };
+    int rc = TQ_OK;
     switch (P) {
-#define CASE(Q) case Q: k_fill_tiles<Q><<<wave((const void*)k_fill_tiles<Q>), 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch(); break;
+#define CASE(Q) case Q: rc = launch(k_fill_tiles<Q>, k_fill_irregular<Q>, fill_slice_bytes<Q>()); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
         default: {
@@ -366,6 +447,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
             k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch();
         }
     }
+    if (rc) return rc;
     TQ_LAUNCH_CHECK("k_fill_rows");
     return TQ_OK;
 }
