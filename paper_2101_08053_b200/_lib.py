@@ -132,12 +132,27 @@ def ptr(t):
     return vp(t.data_ptr()) if t is not None else vp(0)
 
 
+_pinned_keep = []
+
+
 def dev(x, dtype):
-    """Upload a host array (numpy) as a contiguous device tensor."""
+    """Upload a host array (numpy) as a contiguous device tensor.  Under CUDA
+    stream capture the source is pinned and kept alive (the replayed copy
+    reads it again)."""
     import numpy as np
-    a = np.ascontiguousarray(x)
-    t = torch.from_numpy(a).to(device=device(), dtype=dtype, non_blocking=False)
-    return t.contiguous()
+    a = np.array(x, copy=True) if not np.asarray(x).flags.writeable else np.ascontiguousarray(x)
+    src = torch.from_numpy(np.ascontiguousarray(a))
+    if torch.cuda.is_current_stream_capturing():
+        src = src.pin_memory()
+        _pinned_keep.append(src)
+        return src.to(device=device(), non_blocking=True).to(dtype)
+    return src.to(device=device(), dtype=dtype, non_blocking=False).contiguous()
+
+
+def dev_bytes(buf):
+    """Upload raw bytes (e.g. a ctypes struct array) as a uint8 device tensor."""
+    import numpy as np
+    return dev(np.frombuffer(bytes(buf), dtype=np.uint8), torch.uint8)
 
 
 def sync():

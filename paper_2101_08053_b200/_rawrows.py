@@ -193,7 +193,11 @@ def build_all_rules(f):
             dwq_pending[(d, u)] = (g[pk], *dwq_solve_async(g[pk], direction=d))
     flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
     flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]
-    any_fail = bool(torch.cat(flags).any().item()) if flags else False
+    if f.capture is not None:     # graph capture: flags checked after each replay
+        f._fail_flags = torch.cat(flags) if flags else None
+        any_fail = False
+    else:
+        any_fail = bool(torch.cat(flags).any().item()) if flags else False
     rules = []
     for d, (pl, (wptr, k0, w, fail)) in enumerate(zip(plans, std)):
         if any_fail and _failing(pl, fail):
@@ -250,7 +254,7 @@ class _Setup:
                 for k, rs in enumerate(self.sets[d]):
                     first, vals = rs.basis_table()
                     arr[k] = RuleSetDev(rs.device(), rs.layout.device(), L.ptr(first), L.ptr(vals))
-                t = torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(dev)
+                t = L.dev_bytes(bytearray(arr))
                 self.sets_dev.append(t)
             self.nmax = []
             for d, b in enumerate((b1, b2)):
@@ -266,7 +270,7 @@ class _Setup:
                         g = f.coeff.grid_device(s1.layout.device_points(), s2.layout.device_points())
                         self.keep.append(g)
                         ptrs[a * len(self.sets[1]) + c] = g.data_ptr()
-                self.grids = torch.from_numpy(ptrs.view(np.int64)).to(dev)
+                self.grids = L.dev(ptrs.view(np.int64), torch.int64)
         else:
             self.sets_dev = [None, None]
             self.nmax = [1, 1]

@@ -26,6 +26,7 @@ import torch
 
 from . import _lib as L
 from ._lib import CUT, EXTERIOR, INTERIOR
+from ._lib import RuleConstructionError as RuleConstructionError_
 from .quadrature import compute_wq_rules, place_wq_points
 from .splines import TensorBasis2D
 from .trimming import TrimConfiguration
@@ -177,13 +178,17 @@ class FormationReport:
 
 class _Clock:
     """Phase timer: device-synchronised wall clock (the reference's
-    perf_counter boundaries), plus CUDA events for the kernel-only figures."""
+    perf_counter boundaries).  Inactive (no syncs) under stream capture."""
 
-    def __init__(self):
-        torch.cuda.synchronize()
+    def __init__(self, active=True):
+        self.active = active
+        if active:
+            torch.cuda.synchronize()
         self.t = time.perf_counter()
 
     def lap(self):
+        if not self.active:
+            return 0.0
         torch.cuda.synchronize()
         now = time.perf_counter()
         dt, self.t = now - self.t, now
@@ -246,7 +251,8 @@ class Formation:
     """Device state of one assembly run (the analogue of ``_Run``,
     src/assembly.py:272-404)."""
 
-    def __init__(self, basis2d: TensorBasis2D, config: TrimConfiguration, coeff, strategy, timer=None):
+    def __init__(self, basis2d: TensorBasis2D, config: TrimConfiguration, coeff, strategy, timer=None,
+                 capture=None):
         if strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
         self.basis2d = basis2d
@@ -267,6 +273,9 @@ class Formation:
         self.rules = None
         self.report = FormationReport(strategy)
         self.timer = timer or _NoTimer()
+        # capture: None (eager) or dict(nnz=...) -- a CUDA-graph capture pass
+        # with no host syncs; sizes come from the preceding eager pass
+        self.capture = capture
 
     # -- phases -------------------------------------------------------------------
     def build_weights(self, rules=None):
@@ -329,8 +338,9 @@ class Formation:
         indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
         with self.timer("scan"):
-            L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr), L.C.byref(nnz), L.stream())
-        nnz = int(nnz.value)
+            L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr),
+                   None if self.capture else L.C.byref(nnz), L.stream())
+        nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
         data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
         with self.timer("fill"):
@@ -338,13 +348,14 @@ class Formation:
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
 
-def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None):
+def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None,
+         capture=None):
     """Run every formation phase on the device; returns (Formation, DeviceCSR)."""
-    f = Formation(basis2d, config, coeff, strategy, timer)
+    f = Formation(basis2d, config, coeff, strategy, timer, capture)
     rep = f.report
     if config.has_cuts():     # shared geometry, outside the clock (src/assembly.py:505-508)
         config.cut_cell_rule(max(basis2d.degrees))
-    clk = _Clock()
+    clk = _Clock(active=capture is None)
     f.build_weights(rules)
     rep.t_weights = clk.lap()
     f.interior_products()
@@ -360,6 +371,49 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     rep.t_total = rep.t_weights + rep.t_interior + rep.t_cut_regular + rep.t_cut_elements + rep.t_finish
     rep.nnz = csr.nnz
     return f, csr
+
+
+class GraphFormation:
+    """One formation pass captured as a CUDA graph and replayed.
+
+    The first call runs eagerly (it builds the cached geometry plans and
+    learns nnz and the fit status); the pass is then captured with no host
+    syncs and every ``run()`` replays all of its kernels -- weights, DWQ
+    sets, interior products, raw and cut rows, symmetrise/compact/CSR fill --
+    into the same static device buffers.  The moment-fit residual flags are
+    re-checked after each replay (``check()``)."""
+
+    def __init__(self, basis2d, config, coeff=None, strategy="dwq", row_range=None):
+        self.args = (basis2d, config, coeff, strategy)
+        self.row_range = row_range
+        f, csr = form(basis2d, config, coeff, strategy, row_range=row_range)
+        self.nnz = csr.nnz
+        self.report = f.report
+        del f, csr
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):   # warm the capture path once (allocator, attributes)
+            form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        lib = L.lib()
+        lib.tq_launch_count.restype = L.C.c_longlong
+        n0 = lib.tq_launch_count()
+        with torch.cuda.graph(self.graph):
+            self.f, self.csr = form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
+        self.launches_per_pass = int(lib.tq_launch_count() - n0)
+        torch.cuda.synchronize()
+
+    def run(self):
+        self.graph.replay()
+        return self.csr
+
+    def check(self):
+        flags = getattr(self.f, "_fail_flags", None)
+        if flags is not None and bool(flags.any().item()):
+            raise RuleConstructionError_("moment-fit residual above tolerance in a replayed pass")
 
 
 def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None, strategy="reference",

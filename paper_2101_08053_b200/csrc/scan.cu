@@ -151,25 +151,45 @@ __global__ void k_set_last(int32_t* indptr, int64_t n, const int64_t* total) {
 
 using namespace tq;
 
+__global__ void k_scan_finish(int32_t* indptr, int32_t nrows, const int64_t* total, int32_t* ovf) {
+    if (threadIdx.x == 0) {
+        int64_t t = *total;
+        if (t > 0x7fffffffLL) *ovf = 1;
+        indptr[nrows] = (int32_t)t;
+    }
+}
+
+// nnz_h == NULL: no host read-back (stream-capture safe; the caller knows nnz)
 extern "C" int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr, int64_t* nnz_h,
                               void* stream) {
     cudaStream_t st = S(stream);
-    int32_t* ovf = nullptr;
-    TQ_CUDA(cudaMallocAsync(&ovf, sizeof(int32_t), st));
+    int64_t ntiles = (nrows + kTile - 1) / kTile;
+    if (ntiles == 0) ntiles = 1;
+    int64_t* tiles = nullptr;
+    TQ_CUDA(cudaMallocAsync(&tiles, (ntiles + 2) * sizeof(int64_t), st));
+    int32_t* ovf = reinterpret_cast<int32_t*>(tiles + ntiles + 1);
     TQ_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
+    CountsIn in{counts};
+    k_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, nrows, tiles); ::tq::note_launch();
+    k_scan_tiles<<<1, 1024, 0, st>>>(tiles, ntiles); ::tq::note_launch();
+    k_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, nrows, tiles, IndptrOut{indptr, ovf}); ::tq::note_launch();
+    k_scan_finish<<<1, 32, 0, st>>>(indptr, nrows, tiles + ntiles, ovf); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("scan");
     int64_t total = 0;
-    int rc = scan_generic(CountsIn{counts}, nrows, IndptrOut{indptr, ovf}, &total, st);
-    if (rc) return rc;
-    if (total > 0x7fffffffLL) {
-        cudaFreeAsync(ovf, st);
-        set_error("nnz %lld does not fit int32 CSR indices", (long long)total);
-        return TQ_EOVERFLOW;
+    int32_t hovf = 0;
+    if (nnz_h) {
+        TQ_CUDA(cudaMemcpyAsync(&total, tiles + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     }
-    int32_t t32 = (int32_t)total;
-    TQ_CUDA(cudaMemcpyAsync(indptr + nrows, &t32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    TQ_CUDA(cudaFreeAsync(ovf, st));
-    TQ_CUDA(cudaStreamSynchronize(st));
-    *nnz_h = total;
+    TQ_CUDA(cudaFreeAsync(tiles, st));
+    if (nnz_h) {
+        TQ_CUDA(cudaStreamSynchronize(st));
+        if (hovf || total > 0x7fffffffLL) {
+            set_error("nnz %lld does not fit int32 CSR indices", (long long)total);
+            return TQ_EOVERFLOW;
+        }
+        *nnz_h = total;
+    }
     return TQ_OK;
 }
 
