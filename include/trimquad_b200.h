@@ -90,6 +90,8 @@ typedef struct {
 int tq_version(void);
 const char* tq_last_error(void);
 int tq_device_sync(void* stream);
+/* kernels launched by the library since it was loaded (host counter) */
+long long tq_launch_count(void);
 
 /* ---- subsystem (1): basis, moments, weights ------------------------------ */
 
@@ -252,6 +254,23 @@ int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const double* x2, in
                   double* out, void* stream);
 int tq_coeff_points(tq_coeff g, const double* pts, int64_t n, const double* w, double* out,
                     void* stream);
+
+/* ---- host-native cut-cell quadrature (geometry input of subsystem 3) ------ */
+
+/* Decompose every listed cut element (cut_el_h: ncut x 2 element indices,
+ * row-major order) against the curves (HOST data pointers) and place
+ * (q+1)^2 Gauss points per sub-cell.  tabs_h: q+1 Lobatto nodes on [0,1],
+ * q+1 Gauss nodes and weights on [0,1], the (q+1)x(q+1) Lagrange values and
+ * derivatives at the Gauss nodes.  Returns an opaque handle (NULL on failure,
+ * status in *status_h).  Replaces cut_cell_quadrature / decompose_cut_element
+ * (src/trimming.py:938-1111) with the closed-curve seam routing of SURVEY F3. */
+void* tq_cutcell_build(const tq_curve* curves_h, int32_t ncurves, const double* bp1_h, int32_t nel1,
+                       const double* bp2_h, int32_t nel2, const int32_t* cut_el_h, int32_t ncut,
+                       int32_t q, const double* tabs_h, int32_t* status_h);
+int64_t tq_cutcell_npoints(void* handle);
+/* ptr_h: ncut+1 point offsets; pts_h: npoints x 2; w_h: npoints; ncells_h: ncut */
+int tq_cutcell_copy(void* handle, int64_t* ptr_h, double* pts_h, double* w_h, int32_t* ncells_h);
+void tq_cutcell_free(void* handle);
 
 /* ---- L2 projection: RHS and error ---------------------------------------- */
 

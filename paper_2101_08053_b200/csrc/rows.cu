@@ -426,8 +426,6 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
         TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         int per_sm = 0;
         TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, shm));
-        const char* env = getenv("TQ_FILL_BPS");   // tuning knob (blocks per SM)
-        if (env && atoi(env) > 0) per_sm = std::min(per_sm, atoi(env));
         const int64_t full = (int64_t)kSms * std::max(per_sm, 1);
         const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
         TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (ntiles + 1), S(stream)));
