@@ -117,21 +117,21 @@ def cut_point_tables(f):
         f1, _ = b1.eval_device(t["x"], check=False)
         f2, _ = b2.eval_device(t["y"], check=False)
         f1, f2 = f1.cpu().numpy().astype(np.int64), f2.cpu().numpy().astype(np.int64)
-        gptr, gkey, gpts, perm = [0], [], [0], []
-        for k in range(rule.elements.shape[0]):
-            a, b = int(rule.ptr[k]), int(rule.ptr[k + 1])
-            keys = f1[a:b] * (b2.n + 1) + f2[a:b]
-            for key in np.unique(keys):
-                sel = np.nonzero(keys == key)[0] + a
-                perm.append(sel)
-                gkey.append((f1[sel[0]], f2[sel[0]]))
-                gpts.append(gpts[-1] + sel.size)
-            gptr.append(len(gkey))
-        t["grp_ptr"] = L.dev(np.asarray(gptr, np.int32), torch.int32)
-        t["grp_key"] = L.dev(np.asarray(gkey, np.int32).reshape(-1, 2), torch.int32)
-        t["grp_pts"] = L.dev(np.asarray(gpts, np.int64), torch.int64)
-        t["grp_perm"] = L.dev(np.concatenate(perm) if perm else np.zeros(1, np.int64), torch.int64)
-        t["ngroups"] = len(gkey)
+        ncut = rule.elements.shape[0]
+        elem = np.repeat(np.arange(ncut), np.diff(rule.ptr))
+        key = f1 * (b2.n + 1) + f2
+        perm = np.lexsort((np.arange(key.size), key, elem))      # stable: element, then key
+        ek = np.stack([elem[perm], key[perm]], axis=1)
+        start = np.nonzero(np.r_[True, np.any(ek[1:] != ek[:-1], axis=1)])[0] if key.size else np.zeros(0, int)
+        gpts = np.r_[start, key.size].astype(np.int64)
+        gelem = elem[perm][start]
+        gptr = np.searchsorted(gelem, np.arange(ncut + 1), side="left").astype(np.int32)
+        gkey = np.stack([f1[perm][start], f2[perm][start]], axis=1).astype(np.int32)
+        t["grp_ptr"] = L.dev(gptr, torch.int32)
+        t["grp_key"] = L.dev(gkey.reshape(-1, 2), torch.int32)
+        t["grp_pts"] = L.dev(gpts, torch.int64)
+        t["grp_perm"] = L.dev(perm.astype(np.int64) if perm.size else np.zeros(1, np.int64), torch.int64)
+        t["ngroups"] = int(start.size)
         g["cutpts"] = t
         g["cutpts_src"] = rule
     return g["cutpts"]

@@ -204,9 +204,21 @@ class DeviceCSR:
     row_end: int
     nnz: int
 
+    def to_host(self):
+        """(indptr, indices, data) as numpy arrays backed by pinned host
+        memory (torch's caching host allocator reuses freed blocks), copied
+        with asynchronous DMA."""
+        out = []
+        for t in (self.indptr, self.indices, self.data):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            out.append(h)
+        torch.cuda.current_stream().synchronize()
+        return tuple(h.numpy() for h in out)
+
     def to_scipy(self, shape):
-        return sp.csr_matrix((self.data.cpu().numpy(), self.indices.cpu().numpy(),
-                              self.indptr.cpu().numpy()), shape=shape)
+        ptr, ind, dat = self.to_host()
+        return sp.csr_matrix((dat, ind, ptr), shape=shape)
 
 
 class _KernelTimer:

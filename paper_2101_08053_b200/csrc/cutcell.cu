@@ -408,7 +408,11 @@ extern "C" void* tq_cutcell_build(const tq_curve* curves_h, int32_t ncurves, con
     T.L.assign(t, t + ng * (q + 1)); t += ng * (q + 1);
     T.dL.assign(t, t + ng * (q + 1));
     CutRule* R = new CutRule();
-    R->ptr.push_back(0);
+    // cells are independent: decompose in parallel (OpenMP), then concatenate
+    // in element order so the output is identical to a serial run
+    std::vector<std::vector<SubCell>> all(ncut);
+    std::vector<int> err(ncut, 0);
+#pragma omp parallel for schedule(dynamic, 16)
     for (int z = 0; z < ncut; ++z) {
         int e1 = cut_el_h[2 * z], e2 = cut_el_h[2 * z + 1];
         Bounds B{bp1_h[e1], bp1_h[e1 + 1], bp2_h[e2], bp2_h[e2 + 1]};
@@ -425,12 +429,7 @@ extern "C" void* tq_cutcell_build(const tq_curve* curves_h, int32_t ncurves, con
                 }
                 if (any) { found = c; ++nfound; }
             }
-            if (nfound != 1) {
-                set_error("cell (%d, %d) crossed by %d curves; exactly one supported", e1, e2, nfound);
-                *status_h = TQ_ETRIM;
-                delete R;
-                return nullptr;
-            }
+            if (nfound != 1) { err[z] = 3; continue; }
             which = found;
         }
         CurveC c = cv[which];
@@ -440,26 +439,33 @@ extern "C" void* tq_cutcell_build(const tq_curve* curves_h, int32_t ncurves, con
             double tol = 1e-10 * std::max(B.x1 - B.x0, B.y1 - B.y0);
             if (B.x0 - tol <= sx && sx <= B.x1 + tol && B.y0 - tol <= sy && sy <= B.y1 + tol) c = shifted(c);
         }
-        std::vector<SubCell> cells;
         try {
-            decompose(B, c, c.kind == TQ_CURVE_LINE, T, 0, cells);
+            decompose(B, c, c.kind == TQ_CURVE_LINE, T, 0, all[z]);
         } catch (TrimErr&) {
-            set_error("element (%d, %d): cannot decompose cell at maximum split depth 4", e1, e2);
-            *status_h = TQ_ETRIM;
-            delete R;
-            return nullptr;
+            err[z] = 1;
         } catch (Fold&) {
-            set_error("element (%d, %d): folded sub-cell", e1, e2);
+            err[z] = 2;
+        }
+    }
+    for (int z = 0; z < ncut; ++z) {
+        if (err[z]) {
+            int e1 = cut_el_h[2 * z], e2 = cut_el_h[2 * z + 1];
+            if (err[z] == 3) set_error("cell (%d, %d) is not crossed by exactly one curve", e1, e2);
+            else if (err[z] == 1) set_error("element (%d, %d): cannot decompose cell at maximum split depth 4", e1, e2);
+            else set_error("element (%d, %d): folded sub-cell", e1, e2);
             *status_h = TQ_ETRIM;
             delete R;
             return nullptr;
         }
-        for (auto& sc : cells) {
+    }
+    R->ptr.push_back(0);
+    for (int z = 0; z < ncut; ++z) {
+        for (auto& sc : all[z]) {
             R->P.insert(R->P.end(), sc.P.begin(), sc.P.end());
             R->W.insert(R->W.end(), sc.W.begin(), sc.W.end());
         }
         R->ptr.push_back((int64_t)R->W.size());
-        R->ncells.push_back((int32_t)cells.size());
+        R->ncells.push_back((int32_t)all[z].size());
     }
     return R;
 }

@@ -1,0 +1,22 @@
+"""Breakdown of the end-to-end public-API path on config 5 (dev aid)."""
+import sys, time; sys.path.insert(0, ".")
+import numpy as np, torch
+import paper_2101_08053_b200 as P
+from paper_2101_08053_b200 import cases as C, trimming as T
+from paper_2101_08053_b200.assembly import form
+c5 = C.baseline_config(5)
+knots = P.make_uniform_knots(2048, 4).knots.copy(); ctrl = c5["curves"][0].ctrl.copy()
+def run():
+    t = [time.perf_counter()]
+    bb = P.TensorBasis2D(P.Basis1D(P.KnotVector(knots, 4)), P.Basis1D(P.KnotVector(knots, 4)))
+    cf = P.classify_elements(bb, [T.PeriodicBSplineTrim(ctrl)]); torch.cuda.synchronize(); t.append(time.perf_counter())
+    cf.cut_cell_rule(4); t.append(time.perf_counter())
+    f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize(); t.append(time.perf_counter())
+    h = (csr.indptr.cpu().numpy(), csr.indices.cpu().numpy(), csr.data.cpu().numpy()); t.append(time.perf_counter())
+    import scipy.sparse as sp
+    M = sp.csr_matrix((h[2], h[1], h[0]), shape=(f.K, f.K)); t.append(time.perf_counter())
+    act = cf.active_functions(); t.append(time.perf_counter())
+    return np.diff(t)
+for k in range(3):
+    d = run()
+    print("classify %.3f cutcells %.3f form %.3f d2h %.3f scipy %.3f active %.3f total %.3f" % (*d, d.sum()))
