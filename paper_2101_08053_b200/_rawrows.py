@@ -172,6 +172,39 @@ def dwq_keys(f):
     return g["dwq_keys"]
 
 
+_SIDE = {}
+
+
+def _side_streams(n):
+    dev = torch.cuda.current_device()
+    lst = _SIDE.setdefault(dev, [])
+    while len(lst) < n:
+        lst.append(torch.cuda.Stream())
+    return lst[:n]
+
+
+class _forked:
+    """Run a block on a side stream that starts after the main stream."""
+
+    def __init__(self, main, side):
+        self.main, self.side = main, side
+
+    def __enter__(self):
+        self.side.wait_stream(self.main)
+        self.ctx = torch.cuda.stream(self.side)
+        self.ctx.__enter__()
+
+    def __exit__(self, *a):
+        self.ctx.__exit__(*a)
+
+
+def _keep_on(stream, tensors):
+    """Tensors made on a side stream and consumed on `stream`."""
+    for t in tensors:
+        if t is not None and not torch.cuda.is_current_stream_capturing():
+            t.record_stream(stream)
+
+
 def build_all_rules(f):
     """Standard WQ rules per direction and the DWQ sets (src/assembly.py:454-489).
     Point layouts and DWQ refinement plans are geometry (cached per
@@ -182,15 +215,30 @@ def build_all_rules(f):
     if "std_plans" not in g:
         g["std_plans"] = [_FitPlan(b, place_wq_points(b)) for b in (f.b1, f.b2)]
     plans = g["std_plans"]
-    std = [_solve_rows_async(pl) for pl in plans]
-    dwq_pending = {}
+    dplans = {}
     if f.strategy == "dwq":
-        keys = dwq_keys(f)
-        for (d, u), rows in keys.items():
+        for (d, u), rows in dwq_keys(f).items():
             pk = ("dwq_plan", d, u)
             if pk not in g:
                 g[pk] = DwqPlan((f.b1, f.b2)[d], plans[d].layout, u, only_rows=rows)
-            dwq_pending[(d, u)] = (g[pk], *dwq_solve_async(g[pk], direction=d))
+            dplans[(d, u)] = g[pk]
+    # the fit chains are independent: fork them onto side streams (parallel
+    # branches of the captured graph), join before anything consumes them
+    main = torch.cuda.current_stream()
+    sides = _side_streams(len(plans) + len(dplans))
+    std, dwq_pending = [], {}
+    for k, pl in enumerate(plans):
+        with _forked(main, sides[k]):
+            out = _solve_rows_async(pl)
+            _keep_on(main, out[1:])
+        std.append(out)
+    for k, (key, pl) in enumerate(dplans.items()):
+        with _forked(main, sides[len(plans) + k]):
+            rs, fail = dwq_solve_async(pl, direction=key[0])
+            _keep_on(main, (rs.w, fail))
+        dwq_pending[key] = (pl, rs, fail)
+    for st in sides:
+        main.wait_stream(st)
     flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
     flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]
     if f.capture is not None:     # graph capture: flags checked after each replay

@@ -35,11 +35,29 @@ __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t
     }
 }
 
+// Basis values and weights at the (p+1)-point element Gauss points:
+// tab[(e*ng + g)*(p+2) + k] = B_{span(e)-p+k}(x_eg) for k <= p, and the
+// mapped weight in slot p+1.
+__global__ void k_gauss_table(tq_space1d s, const double* __restrict__ gx, const double* __restrict__ gw,
+                              int ng, double* __restrict__ tab) {
+    const int p = s.p;
+    const int total = s.nel * ng;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int e = t / ng, g = t - e * ng;
+        const double a = s.bp[e], b = s.bp[e + 1];
+        const double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+        double N[kMaxP + 1];
+        basis_funs_rt(s.knots, p, s.espan[e], mid + half * gx[g], N);
+        double* out = tab + (int64_t)t * (p + 2);
+        for (int k = 0; k <= p; ++k) out[k] = N[k];
+        out[p + 1] = half * gw[g];
+    }
+}
+
 // Banded exact 1-D mass matrix: thread per (i, o), j = i - p + o; element
 // loop over the shared support in element order (the order np.add.at
-// accumulates element blocks in the reference).
-__global__ void k_moments(tq_space1d s, const double* __restrict__ gx, const double* __restrict__ gw,
-                          int ng, double* __restrict__ mom) {
+// accumulates element blocks in the reference), values from the table.
+__global__ void k_moments(tq_space1d s, const double* __restrict__ tab, int ng, double* __restrict__ mom) {
     const int p = s.p, W = 2 * p + 1;
     int64_t total = (int64_t)s.n * W;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -51,16 +69,12 @@ __global__ void k_moments(tq_space1d s, const double* __restrict__ gx, const dou
             int ea = max(s.el_first[i], s.el_first[j]);
             int eb = min(s.el_last[i], s.el_last[j]);
             for (int e = ea; e <= eb; ++e) {
-                double a = s.bp[e], b = s.bp[e + 1];
-                double mid = 0.5 * (a + b), half = 0.5 * (b - a);
-                int span = s.espan[e];
+                const int f = s.espan[e] - p;
+                const double* row = tab + (int64_t)e * ng * (p + 2);
                 double part = 0.0;
                 for (int g = 0; g < ng; ++g) {
-                    double x = mid + half * gx[g];
-                    double N[kMaxP + 1];
-                    basis_funs_rt(s.knots, p, span, x, N);
-                    double bi = N[i - (span - p)], bj = N[j - (span - p)];
-                    part += bi * bj * (half * gw[g]);
+                    const double* v = row + g * (p + 2);
+                    part += v[i - f] * v[j - f] * v[p + 1];
                 }
                 acc += part;
             }
@@ -90,8 +104,12 @@ extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* 
 extern "C" int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng,
                                double* mom, void* stream) {
     if (s.p > kMaxP) { set_error("degree %d unsupported", s.p); return TQ_EINVAL; }
+    double* tab = nullptr;
+    TQ_CUDA(cudaMallocAsync(&tab, sizeof(double) * (size_t)s.nel * ng * (s.p + 2), S(stream)));
+    k_gauss_table<<<grid_for((int64_t)s.nel * ng, 128), 128, 0, S(stream)>>>(s, gx, gw, ng, tab); ::tq::note_launch();
     int64_t total = (int64_t)s.n * (2 * s.p + 1);
-    k_moments<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, gx, gw, ng, mom); ::tq::note_launch();
+    k_moments<<<grid_for(total, 128), 128, 0, S(stream)>>>(s, tab, ng, mom); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_moments");
+    TQ_CUDA(cudaFreeAsync(tab, S(stream)));
     return TQ_OK;
 }
