@@ -246,6 +246,11 @@ int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
  * B^T diag(c w) B per (cut element, span key) group, then a row gather.
  * Replaces _Run.add_cut_blocks (src/assembly.py:369-398). */
 int tq_cut_blocks(tq_rawctx c, void* stream);
+/* element 1-D masses em[e][a][b] = sum_g w V_a V_b from element Gauss tables
+ * (ev: nel*ng*(p+1), ew: nel*ng) -- the c == 1 factors of _Run.element_block
+ * (src/assembly.py:310-332) */
+int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int32_t ng, int32_t p, double* em,
+                 void* stream);
 int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
 
 /* coefficient c = det J of a B-spline geometry map on a tensor grid / at

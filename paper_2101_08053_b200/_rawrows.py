@@ -46,6 +46,7 @@ def _bind():
     L.optional("tq_raw_regular", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_raw_cutcells", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_cut_blocks", [RawCtx, L.vp])
+    L.optional("tq_elem_mass", [L.vp, L.vp, L.i32, L.i32, L.i32, L.vp, L.vp])
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
@@ -279,9 +280,13 @@ class _Setup:
         # element Gauss tables, (p+1) points (src/assembly.py:198-211);
         # basis values evaluated per formation as in the reference's _Run
         self.eg = []
+        self.em = []
         for b, (Xd, Wd) in zip((b1, b2), element_points(f)):
             _, vals = b.eval_device(Xd, check=False)
             self.eg.append((None, Wd, vals, Xd))
+            em = torch.empty(b.num_elements * (b.p + 1) ** 2, dtype=torch.float64, device=dev)
+            L.call("tq_elem_mass", L.ptr(vals), L.ptr(Wd), b.num_elements, b.p + 1, b.p, L.ptr(em), L.stream())
+            self.em.append(em)
         self.cg = None
         if not f.coeff.identity:
             self.cg = f.coeff.grid_device(self.eg[0][3], self.eg[1][3])
@@ -346,7 +351,8 @@ class _Setup:
                       P(d1["ov_lo"]), P(d1["ov_hi"]), P(d2["ov_lo"]), P(d2["ov_hi"]),
                       P(d1["espan"]), P(d2["espan"]), P(f.config.element_class_dev),
                       f.b1.p + 1, f.b2.p + 1,
-                      P(self.eg[0][1]), P(self.eg[0][2]), P(self.eg[1][1]), P(self.eg[1][2]), L.vp(0), L.vp(0),
+                      P(self.eg[0][1]), P(self.eg[0][2]), P(self.eg[1][1]), P(self.eg[1][2]), P(self.em[0]),
+                      P(self.em[1]),
                       P(self.cg), P(self.sets_dev[0]), P(self.sets_dev[1]),
                       len(self.sets[0]), len(self.sets[1]), P(self.grids),
                       P(cut.get("idx")), P(cut.get("ptr")), P(cut.get("cw")), P(cut.get("f1")), P(cut.get("v1")),

@@ -39,16 +39,7 @@ __device__ inline double gauss_entry(const tq_rawctx& c, int e1, int e2, int a1,
     const int q1 = c.p1 + 1, q2 = c.p2 + 1;
     if (!c.cg) {
         // c == 1: the element block is the product of two 1-D element masses
-        double m1 = 0.0, m2 = 0.0;
-        for (int g = 0; g < c.ng1; ++g) {
-            const double* v = c.ev1 + ((int64_t)e1 * c.ng1 + g) * q1;
-            m1 += (v[a1] * v[b1]) * c.ew1[(int64_t)e1 * c.ng1 + g];
-        }
-        for (int g = 0; g < c.ng2; ++g) {
-            const double* v = c.ev2 + ((int64_t)e2 * c.ng2 + g) * q2;
-            m2 += (v[a2] * v[b2]) * c.ew2[(int64_t)e2 * c.ng2 + g];
-        }
-        return m1 * m2;
+        return c.em1[((int64_t)e1 * q1 + a1) * q1 + b1] * c.em2[((int64_t)e2 * q2 + a2) * q2 + b2];
     }
     const int64_t ld = (int64_t)c.nel2 * c.ng2;
     double acc = 0.0;
@@ -66,6 +57,22 @@ __device__ inline double gauss_entry(const tq_rawctx& c, int e1, int e2, int a1,
         acc += f1 * part;
     }
     return acc;
+}
+
+// element 1-D masses em[e][a][b] = sum_g w_g V[g][a] V[g][b] (c == 1 Gauss blocks)
+__global__ void k_elem_mass(const double* __restrict__ ev, const double* __restrict__ ew, int nel, int ng, int p,
+                            double* __restrict__ em) {
+    const int q = p + 1;
+    const int64_t total = (int64_t)nel * q * q;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(t / (q * q)), r = (int)(t - (int64_t)e * q * q), a = r / q, b = r - (r / q) * q;
+        double m = 0.0;
+        for (int g = 0; g < ng; ++g) {
+            const double* v = ev + ((int64_t)e * ng + g) * q;
+            m += (v[a] * v[b]) * ew[(int64_t)e * ng + g];
+        }
+        em[t] = m;
+    }
 }
 
 __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
@@ -198,10 +205,15 @@ __global__ void k_cut_blocks(tq_rawctx c) {
     double* sv1 = sm;                       // kGrpStage x q1
     double* sv2 = sv1 + kGrpStage * q1;     // kGrpStage x q2
     double* scw = sv2 + kGrpStage * q2;     // kGrpStage
+    // thread owns (A, b1) and accumulates the q2 entries B = (b1, 0..q2-1)
+    const int nt = Q * q1;
     for (int g = blockIdx.x; g < c.ngroups; g += gridDim.x) {
         const int64_t p0 = c.grp_pts[g], p1e = c.grp_pts[g + 1];
-        double acc[8];
-        for (int z = 0; z < 8; ++z) acc[z] = 0.0;
+        const int tid = threadIdx.x;
+        const int A = tid / q1, b1 = tid - (tid / q1) * q1;
+        const int a1 = A / q2, a2 = A - (A / q2) * q2;
+        double acc[kMaxP + 1];
+        for (int z = 0; z < q2; ++z) acc[z] = 0.0;
         for (int64_t base = p0; base < p1e; base += kGrpStage) {
             const int np = (int)(p1e - base < kGrpStage ? p1e - base : kGrpStage);
             __syncthreads();
@@ -213,21 +225,18 @@ __global__ void k_cut_blocks(tq_rawctx c) {
                 else scw[k] = c.cut_cw[pt];
             }
             __syncthreads();
-            for (int z = 0; z < 8; ++z) {
-                int e = threadIdx.x + z * blockDim.x;
-                if (e >= Q * Q) break;
-                int A = e / Q, B = e - (e / Q) * Q;
-                int a1 = A / q2, a2 = A - (A / q2) * q2, b1 = B / q2, b2 = B - (B / q2) * q2;
-                double s = 0.0;
-                for (int k = 0; k < np; ++k)
-                    s += (sv1[k * q1 + a1] * sv2[k * q2 + a2]) * (scw[k] * (sv1[k * q1 + b1] * sv2[k * q2 + b2]));
-                acc[z] += s;
+            if (tid < nt) {
+                for (int k = 0; k < np; ++k) {
+                    const double* v2 = sv2 + k * q2;
+                    const double s = (sv1[k * q1 + a1] * v2[a2]) * scw[k] * sv1[k * q1 + b1];
+#pragma unroll 4
+                    for (int z = 0; z < q2; ++z) acc[z] += s * v2[z];
+                }
             }
         }
-        double* out = c.grp_blocks + (int64_t)g * Q * Q;
-        for (int z = 0; z < 8; ++z) {
-            int e = threadIdx.x + z * blockDim.x;
-            if (e < Q * Q) out[e] = acc[z];
+        if (tid < nt) {
+            double* out = c.grp_blocks + ((int64_t)g * Q + A) * Q + b1 * q2;
+            for (int z = 0; z < q2; ++z) out[z] = acc[z];
         }
     }
 }
@@ -325,12 +334,22 @@ extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream)
     return TQ_OK;
 }
 
+extern "C" int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int32_t ng, int32_t p, double* em,
+                            void* stream) {
+    if ((int64_t)nel * (p + 1) * (p + 1) == 0) return TQ_OK;
+    k_elem_mass<<<grid_for((int64_t)nel * (p + 1) * (p + 1), 128), 128, 0, S(stream)>>>(ev, ew, nel, ng, p, em); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_elem_mass");
+    return TQ_OK;
+}
+
 extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
     if (c.ngroups <= 0) return TQ_OK;
     const int Q = (c.p1 + 1) * (c.p2 + 1);
-    if (Q * Q > 8 * 1024) { set_error("degree too high for the cut-block kernel"); return TQ_EINVAL; }
+    const int nt = Q * (c.p1 + 1);
+    if (nt > 1024) { set_error("degree too high for the cut-block kernel"); return TQ_EINVAL; }
+    const int bs = (nt + 31) / 32 * 32;
     size_t shm = sizeof(double) * kGrpStage * (c.p1 + c.p2 + 3);
-    k_cut_blocks<<<(int)std::min<int64_t>(c.ngroups, (int64_t)kSms * 16), 1024, shm, S(stream)>>>(c); ::tq::note_launch();
+    k_cut_blocks<<<(int)std::min<int64_t>(c.ngroups, (int64_t)kSms * 32), bs, shm, S(stream)>>>(c); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_cut_blocks");
     return TQ_OK;
 }
