@@ -182,6 +182,10 @@ int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows
                   int32_t nraw, int8_t* deep, void* stream);
 
 int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
+/* the two passes of tq_row_counts, separately launchable so the deep pass can
+ * overlap the raw-row kernels: `work` = caller scratch of nrows + 1 ints */
+int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream);
+int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream);
 int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,

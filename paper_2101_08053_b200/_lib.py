@@ -87,6 +87,8 @@ def lib():
         "tq_dwq_combine": ([vp, i32, vp, vp, vp, Rules, Rules, vp], i32),
         "tq_wq_products": ([Space1D, Layout, vp, vp, Rules, vp, vp], i32),
         "tq_row_counts": ([RowCtx, vp, vp], i32),
+        "tq_row_counts_deep": ([RowCtx, vp, vp, vp], i32),
+        "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),

@@ -332,9 +332,10 @@ class Formation:
                         L.ptr(self.raw if self.raw is not None else dummy),
                         L.ptr(self.deep), L.ptr(self.rowfast), row_begin, self.K if row_end is None else row_end)
 
-    def finish(self, row_begin=0, row_end=None) -> DeviceCSR:
+    def finish(self, row_begin=0, row_end=None, join=None) -> DeviceCSR:
         """Count -> scan -> fill: symmetrised, zero-dropped, sorted CSR rows
-        [row_begin, row_end) (src/assembly.py:400-404)."""
+        [row_begin, row_end) (src/assembly.py:400-404).  ``join``: a side
+        stream still computing the raw rows; the deep-row pass overlaps it."""
         row_end = self.K if row_end is None else row_end
         nrows = row_end - row_begin
         if self.deep is None and self.a1 is not None:
@@ -345,8 +346,12 @@ class Formation:
         self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
+        work = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         with self.timer("counts"):
-            L.call("tq_row_counts", ctx, L.ptr(counts), L.stream())
+            L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            if join is not None:
+                torch.cuda.current_stream().wait_stream(join)
+            L.call("tq_row_counts_rest", ctx, L.ptr(counts), L.ptr(work), L.stream())
         indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
         with self.timer("scan"):
@@ -362,7 +367,12 @@ class Formation:
 
 def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None,
          capture=None):
-    """Run every formation phase on the device; returns (Formation, DeviceCSR)."""
+    """Run every formation phase on the device; returns (Formation, DeviceCSR).
+
+    Eager passes run the phases in order with synchronised phase timers (the
+    reference's FormationReport boundaries).  A capture pass (``capture`` =
+    dict(nnz=...), used by GraphFormation) schedules the cut-row chain on a
+    side stream, overlapping the deep-row flags and counts."""
     f = Formation(basis2d, config, coeff, strategy, timer, capture)
     rep = f.report
     if config.has_cuts():     # shared geometry, outside the clock (src/assembly.py:505-508)
@@ -373,13 +383,22 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     f.interior_products()
     f.raw_rows("interior")
     rep.t_interior = clk.lap()
-    f.raw_rows("cut")
-    rep.t_cut_regular = clk.lap()
-    f.raw_rows("cutcells")
-    rep.t_cut_elements = clk.lap()
     rb, re_ = (0, f.K) if row_range is None else row_range
-    csr = f.finish(rb, re_)
-    rep.t_finish = clk.lap()
+    if capture is not None:
+        from ._rawrows import _forked, _side_streams
+        main = torch.cuda.current_stream()
+        side = _side_streams(1)[0]
+        with _forked(main, side):
+            f.raw_rows("cut")
+            f.raw_rows("cutcells")
+        csr = f.finish(rb, re_, join=side)
+    else:
+        f.raw_rows("cut")
+        rep.t_cut_regular = clk.lap()
+        f.raw_rows("cutcells")
+        rep.t_cut_elements = clk.lap()
+        csr = f.finish(rb, re_)
+        rep.t_finish = clk.lap()
     rep.t_total = rep.t_weights + rep.t_interior + rep.t_cut_regular + rep.t_cut_elements + rep.t_finish
     rep.nnz = csr.nnz
     return f, csr

@@ -81,44 +81,43 @@ __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e
     return v != 0.0 ? col : -1;
 }
 
-constexpr int kTileRows = 64;
+// Counts, pass 1 (thread per row, no raw values needed): deep rows are
+// counted arithmetically and flagged fast when their window is full; other
+// rows are appended to a list for pass 2.
+__global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int* __restrict__ list,
+                                  int* __restrict__ nlist) {
+    for (int r = c.row_begin + blockIdx.x * blockDim.x + threadIdx.x; r < c.row_end; r += gridDim.x * blockDim.x) {
+        const int idx = __ldg(c.active + r);
+        if (c.deep && __ldg(c.deep + idx)) {
+            const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
+            const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
+            const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
+            counts[r - c.row_begin] = t1 * t2;
+            if (c.rowfast) c.rowfast[r - c.row_begin] = (t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1) ? 1 : 0;
+        } else {
+            list[atomicAdd(nlist, 1)] = r;
+        }
+    }
+}
 
-// counts: one thread per row for the deep test, the warp for the rest
-__global__ void k_row_counts(tq_rowctx c, int32_t* __restrict__ counts) {
-    __shared__ int todo[kTileRows];
-    __shared__ int ntodo;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int R0 = c.row_begin + blockIdx.x * kTileRows; R0 < c.row_end; R0 += gridDim.x * kTileRows) {
-        if (threadIdx.x == 0) ntodo = 0;
-        __syncthreads();
-        if (threadIdx.x < kTileRows) {
-            int r = R0 + threadIdx.x;
-            if (r < c.row_end) {
-                int idx = c.active[r];
-                if (c.deep && c.deep[idx]) {
-                    int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
-                    int t1 = c.ov_hi1[i1] - c.ov_lo1[i1] + 1, t2 = c.ov_hi2[i2] - c.ov_lo2[i2] + 1;
-                    counts[r - c.row_begin] = t1 * t2;
-                    if (c.rowfast) c.rowfast[r - c.row_begin] = (t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1) ? 1 : 0;
-                } else {
-                    todo[atomicAdd(&ntodo, 1)] = r;
-                }
-            }
+// Counts, pass 2 (warp per listed row): value-based symmetric zero test.
+__global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, const int* __restrict__ list,
+                                  const int* __restrict__ nlist) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int n_rows = *nlist;
+    for (int q = warp; q < n_rows; q += nw) {
+        const int r = list[q];
+        RowGeom g = row_geom(c, r);
+        const int n = g.t1 * g.t2;
+        int cnt = 0;
+        for (int e0 = 0; e0 < n; e0 += 32) {
+            const int e = e0 + lane;
+            double v;
+            const bool keep = e < n && entry(c, g, e, v) >= 0;
+            cnt += __popc(__ballot_sync(0xffffffffu, keep));
         }
-        __syncthreads();
-        for (int q = warp; q < ntodo; q += nwarps) {
-            int r = todo[q];
-            RowGeom g = row_geom(c, r);
-            int n = g.t1 * g.t2, cnt = 0;
-            for (int e0 = 0; e0 < n; e0 += 32) {
-                int e = e0 + lane;
-                double v;
-                bool keep = e < n && entry(c, g, e, v) >= 0;
-                cnt += __popc(__ballot_sync(0xffffffffu, keep));
-            }
-            if (lane == 0) counts[r - c.row_begin] = cnt;
-        }
-        __syncthreads();
+        if (lane == 0) counts[r - c.row_begin] = cnt;
     }
 }
 
@@ -403,13 +402,33 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
     return TQ_OK;
 }
 
+// pass 1 only needs the deep flags; pass 2 needs the raw rows.  `work`:
+// caller scratch of (row_end - row_begin + 1) ints.
+extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream) {
+    int nrows = c.row_end - c.row_begin;
+    TQ_CUDA(cudaMemsetAsync(work, 0, sizeof(int32_t), S(stream)));
+    if (nrows <= 0) return TQ_OK;
+    k_row_counts_deep<<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, counts, work + 1, work); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_deep");
+    return TQ_OK;
+}
+
+extern "C" int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream) {
+    if (c.row_end <= c.row_begin) return TQ_OK;
+    k_row_counts_list<<<kSms * 16, 256, 0, S(stream)>>>(c, counts, work + 1, work); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_list");
+    return TQ_OK;
+}
+
 extern "C" int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream) {
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
-    int grid = (int)std::min<int64_t>((nrows + kTileRows - 1) / kTileRows, (int64_t)kSms * 16);
-    k_row_counts<<<grid, 256, 0, S(stream)>>>(c, counts); ::tq::note_launch();
-    TQ_LAUNCH_CHECK("k_row_counts");
-    return TQ_OK;
+    int32_t* work = nullptr;
+    TQ_CUDA(cudaMallocAsync(&work, sizeof(int32_t) * (nrows + 1), S(stream)));
+    int rc = tq_row_counts_deep(c, counts, work, stream);
+    if (!rc) rc = tq_row_counts_rest(c, counts, work, stream);
+    TQ_CUDA(cudaFreeAsync(work, S(stream)));
+    return rc;
 }
 
 extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
