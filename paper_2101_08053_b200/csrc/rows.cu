@@ -148,7 +148,7 @@ template <int P>
 struct alignas(16) FillStage {
     static constexpr int WW = (2 * P + 1) * (2 * P + 1);
     double d[fill_chunk<P>() * WW + 2];
-    int x[fill_chunk<P>() * WW + 4];
+    alignas(16) int x[fill_chunk<P>() * WW + 4];
 };
 
 template <int P>
@@ -163,6 +163,23 @@ struct alignas(16) RegularSlice {
 template <int P>
 constexpr size_t fill_slice_bytes() { return (sizeof(RegularSlice<P>) + 15) / 16 * 16; }
 
+// side stream and fork/join events of the fill (host objects, one set per device)
+static cudaStream_t side_stream() {
+    static cudaStream_t s[64] = {};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!s[d]) cudaStreamCreateWithFlags(&s[d], cudaStreamNonBlocking);
+    return s[d];
+}
+static cudaEvent_t make_event(cudaEvent_t* slot) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!slot[d]) cudaEventCreateWithFlags(&slot[d], cudaEventDisableTiming);
+    return slot[d];
+}
+static cudaEvent_t fork_event() { static cudaEvent_t e[64] = {}; return make_event(e); }
+static cudaEvent_t join_event() { static cudaEvent_t e[64] = {}; return make_event(e); }
+
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  :: "l"(gdst), "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes) : "memory");
@@ -172,11 +189,14 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Emit a run of L (<= 32) consecutive fast rows (i1, i20 .. i20+L-1), CSR
+// start pos0 (rows have exactly (2P+1)^2 entries, so the run is one span).
 template <int P>
-__device__ __forceinline__ void emit_regular(const tq_rowctx& c, RegularSlice<P>& S, int lane, int i1, int i20,
-                                             int pos0, int& nbulk, int32_t* __restrict__ indices,
-                                             double* __restrict__ data) {
-    constexpr int W = 2 * P + 1, WW = W * W, R = 32 / W, CH = fill_chunk<P>(), n = CH * WW;
+__device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S, int lane, int i1, int i20, int L,
+                                         int pos0, int& nbulk, int32_t* __restrict__ indices,
+                                         double* __restrict__ data) {
+    constexpr int W = 2 * P + 1, WW = W * W, R = 32 / W, CH = fill_chunk<P>();
+    __syncwarp();
     if (lane < W) {
         const int j1 = i1 - P + lane;
         S.l1[lane] = __ldg(c.a1 + (int64_t)i1 * W + lane);
@@ -184,17 +204,19 @@ __device__ __forceinline__ void emit_regular(const tq_rowctx& c, RegularSlice<P>
         S.lcb[lane] = __ldg(c.col_of + (int64_t)j1 * c.n2 + (i20 - P));
     }
     const double* bsrc = c.a2 + (int64_t)(i20 - P) * W;
-    for (int q = lane; q < (32 + 2 * P) * W; q += 32) S.band[q] = __ldg(bsrc + q);
+    for (int q = lane; q < (L + 2 * P) * W; q += 32) S.band[q] = __ldg(bsrc + q);
     __syncwarp();
     const bool act = lane < R * W;
     const int q2 = lane % W, r0 = lane / W;
-    for (int k = 0; k < 32 / CH; ++k) {
+    for (int k = 0; k * CH < L; ++k) {
+        const int rows = min(CH, L - k * CH);
+        const int n = rows * WW;
         FillStage<P>& st = S.stage[nbulk & 1];
         if (lane == 0 && nbulk >= 2) bulk_wait_read1();   // last reader of this buffer is done
         __syncwarp();
-        const int pos = pos0 + k * n;
+        const int pos = pos0 + k * CH * WW;
         const int offd = pos & 1, offx = pos & 3;
-        for (int tt = 0; tt < CH; ++tt) {
+        for (int tt = 0; tt < rows; ++tt) {
             const int t = k * CH + tt;
             const double a2 = S.band[(t + P) * W + q2], a2t = S.band[(t + q2) * W + (2 * P - q2)];
 #pragma unroll
@@ -212,25 +234,26 @@ __device__ __forceinline__ void emit_regular(const tq_rowctx& c, RegularSlice<P>
         const int sd = (pos + 1) & ~1, ed = (pos + n) & ~1;
         const int sx = (pos + 3) & ~3, ex = (pos + n) & ~3;
         if (lane == 0) {
-            bulk_store(data + sd, st.d + (sd - (pos & ~1)), (unsigned)(ed - sd) * 8u);
-            bulk_store(indices + sx, st.x + (sx - (pos & ~3)), (unsigned)(ex - sx) * 4u);
+            if (ed > sd) bulk_store(data + sd, st.d + (sd - (pos & ~1)), (unsigned)(ed - sd) * 8u);
+            if (ex > sx) bulk_store(indices + sx, st.x + (sx - (pos & ~3)), (unsigned)(ex - sx) * 4u);
             bulk_commit();
         }
         ++nbulk;
         if (lane == 1 && sd > pos) data[pos] = st.d[offd];
-        if (lane == 2 && ed < pos + n) data[pos + n - 1] = st.d[offd + n - 1];
-        if (lane >= 3 && lane < 3 + (sx - pos)) indices[pos + lane - 3] = st.x[offx + lane - 3];
-        if (lane >= 8 && lane < 8 + (pos + n - ex)) indices[ex + lane - 8] = st.x[offx + (ex - pos) + lane - 8];
+        if (lane == 2 && ed < pos + n && ed >= sd) data[pos + n - 1] = st.d[offd + n - 1];
+        if (lane >= 3 && lane < 3 + min(sx - pos, n)) indices[pos + lane - 3] = st.x[offx + lane - 3];
+        if (lane >= 8 && ex >= sx && lane < 8 + (pos + n - ex)) indices[ex + lane - 8] = st.x[offx + (ex - pos) + lane - 8];
     }
 }
 
 template <int P>
 __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* __restrict__ indptr,
                                                      int32_t* __restrict__ indices, double* __restrict__ data,
-                                                     int* __restrict__ irr_list, int* __restrict__ irr_count) {
+                                                     int* __restrict__ irr_rows, int* __restrict__ irr_count) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    unsigned char* slice = smraw + fill_slice_bytes<P>() * wib;
+    RegularSlice<P>& S = *reinterpret_cast<RegularSlice<P>*>(smraw + fill_slice_bytes<P>() * wib);
+    const unsigned lt = (1u << lane) - 1u;
     const int nwarps = gridDim.x * wpb;
     int nbulk = 0;
     int R0 = c.row_begin + (blockIdx.x * wpb + wib) * kWarpRows;
@@ -241,26 +264,42 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
         n_fast = c.rowfast ? __ldg(c.rowfast + (R0 + lane - c.row_begin)) : 0;
     }
     for (; R0 < c.row_end; R0 += nwarps * kWarpRows) {
-        const int nr = min(kWarpRows, c.row_end - R0);
-        const int my_idx = n_idx, my_pos = n_pos, my_fast = n_fast;
+        const bool valid = R0 + lane < c.row_end;
+        const int my_idx = n_idx, my_pos = n_pos, my_fast = valid ? n_fast : 0;
         const int R1 = R0 + nwarps * kWarpRows;
         if (R1 + lane < c.row_end) {
             n_idx = __ldg(c.active + R1 + lane);
             n_pos = __ldg(indptr + (R1 + lane - c.row_begin));
             n_fast = c.rowfast ? __ldg(c.rowfast + (R1 + lane - c.row_begin)) : 0;
         }
-        const int idx0 = __shfl_sync(0xffffffffu, my_idx, 0);
-        const bool regular = nr == 32 &&
-            __all_sync(0xffffffffu, my_fast && my_idx == idx0 + lane && my_idx / c.n2 == idx0 / c.n2);
-        if (regular) {
-            const int i1 = idx0 / c.n2;
-            emit_regular<P>(c, *reinterpret_cast<RegularSlice<P>*>(slice), lane, i1, idx0 - i1 * c.n2,
-                            __shfl_sync(0xffffffffu, my_pos, 0), nbulk, indices, data);
-            __syncwarp();
-            continue;
+        // rows that are not fast go to the row-parallel irregular kernel
+        const unsigned slow = __ballot_sync(0xffffffffu, valid && !my_fast);
+        if (slow) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(irr_count, __popc(slow));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (valid && !my_fast) irr_rows[base + __popc(slow & lt)] = R0 + lane;
         }
-        // irregular tile: handed to k_fill_irregular (row-parallel over the GPU)
-        if (lane == 0) irr_list[atomicAdd(irr_count, 1)] = R0;
+        // runs of consecutive fast rows on one i1-line: start where the
+        // previous lane is not fast, not consecutive, or on another line
+        const int prev_idx = __shfl_up_sync(0xffffffffu, my_idx, 1);
+        const int prev_fast = __shfl_up_sync(0xffffffffu, my_fast, 1);
+        const bool start = my_fast && (lane == 0 || !prev_fast || my_idx != prev_idx + 1 ||
+                                       my_idx / c.n2 != prev_idx / c.n2);
+        unsigned starts = __ballot_sync(0xffffffffu, start);
+        const unsigned fastm = __ballot_sync(0xffffffffu, my_fast != 0);
+        while (starts) {
+            const int s0 = __ffs(starts) - 1;
+            starts &= starts - 1;
+            // run length: consecutive fast lanes from s0 until the next start or a slow lane
+            const unsigned after = (fastm >> s0);
+            const unsigned stop_mask = (~after) | ((starts >> s0) & ~1u);
+            const int L = stop_mask ? __ffs(stop_mask) - 1 : 32 - s0;
+            const int idx0 = __shfl_sync(0xffffffffu, my_idx, s0);
+            const int pos0 = __shfl_sync(0xffffffffu, my_pos, s0);
+            const int i1 = idx0 / c.n2;
+            emit_run<P>(c, S, lane, i1, idx0 - i1 * c.n2, L, pos0, nbulk, indices, data);
+        }
     }
     if (lane == 0) bulk_wait_all();
 }
@@ -272,16 +311,15 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
 template <int P>
 __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32_t* __restrict__ indptr,
                                                          int32_t* __restrict__ indices, double* __restrict__ data,
-                                                         const int* __restrict__ irr_list,
+                                                         const int* __restrict__ irr_rows,
                                                          const int* __restrict__ irr_count) {
     constexpr int W = 2 * P + 1;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    const int nrows = *irr_count * kWarpRows;
+    const int nrows = *irr_count;
     for (int u = warp; u < nrows; u += nw) {
-        const int r = irr_list[u / kWarpRows] + (u % kWarpRows);
-        if (r >= c.row_end) continue;
+        const int r = irr_rows[u];
         RowGeom g = row_geom(c, r);
         int pos = __ldg(indptr + (r - c.row_begin));
         const int n = g.t1 * g.t2;
@@ -436,8 +474,8 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
     int P = (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0;
-    int* irr = nullptr;   // [0] = count, [1..] = tile starts
-    const int ntiles = (nrows + kWarpRows - 1) / kWarpRows;
+    int* irr = nullptr;   // [0] = count, [1..] = rows for the irregular kernel
+    cudaStream_t st = S(stream);
     auto launch = [&](auto kern, auto kirr, size_t per_warp) -> int {
         int wpb = 8;
         while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
@@ -447,11 +485,11 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
         TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, shm));
         const int64_t full = (int64_t)kSms * std::max(per_sm, 1);
         const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
-        TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (ntiles + 1), S(stream)));
-        TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), S(stream)));
-        kern<<<grid, 32 * wpb, shm, S(stream)>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
-        kirr<<<kSms * 8, 256, 0, S(stream)>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
-        TQ_CUDA(cudaFreeAsync(irr, S(stream)));
+        TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (nrows + 1), st));
+        TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), st));
+        kern<<<grid, 32 * wpb, shm, st>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
+        kirr<<<kSms * 8, 256, 0, st>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
+        TQ_CUDA(cudaFreeAsync(irr, st));
         return TQ_OK;
     };
     int rc = TQ_OK;
