@@ -92,6 +92,9 @@ const char* tq_last_error(void);
 int tq_device_sync(void* stream);
 /* kernels launched by the library since it was loaded (host counter) */
 long long tq_launch_count(void);
+/* timeline probe: stamps[slot] = device global timer (ns), in stream order
+   (diagnostic; not counted as a launch) */
+int tq_debug_stamp(unsigned long long* stamps, int32_t slot, void* stream);
 
 /* ---- subsystem (1): basis, moments, weights ------------------------------ */
 

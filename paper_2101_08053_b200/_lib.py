@@ -81,6 +81,7 @@ def lib():
         "tq_version": ([], i32),
         "tq_last_error": ([], C.c_char_p),
         "tq_device_sync": ([vp], i32),
+        "tq_debug_stamp": ([vp, i32, vp], i32),
         "tq_basis_eval": ([Space1D, vp, i64, vp, vp, vp, vp, vp], i32),
         "tq_moments_1d_g": ([Space1D, vp, vp, i32, vp, vp], i32),
         "tq_wq_solve": ([Space1D, Layout, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp], i32),
@@ -118,6 +119,23 @@ def call(name, *args):
     if rc != TQ_OK:
         msg = lib().tq_last_error().decode(errors="replace")
         raise _EXC.get(rc, RuntimeError)(f"{name}: {msg}")
+
+
+class Stamps:
+    """Timeline probe (TQ_STAMPS=1): device global-timer stamps recorded in
+    stream order at named points; ``report()`` gives µs from the first."""
+
+    def __init__(self, n=64):
+        self.buf = torch.zeros(n, dtype=torch.int64, device=device())
+        self.names = []
+
+    def __call__(self, name):
+        self.names.append(name)
+        call("tq_debug_stamp", ptr(self.buf), len(self.names) - 1, stream())
+
+    def report(self):
+        t = self.buf[:len(self.names)].cpu().numpy()
+        return {n: (int(v) - int(t[0])) / 1e3 for n, v in zip(self.names, t)}
 
 
 def device():

@@ -327,19 +327,10 @@ class _Setup:
         else:
             self.sets_dev = [None, None]
             self.nmax = [1, 1]
-        # cut-element points (host C++ geometry, device basis tables)
-        self.cut = None
-        if f.config.has_cuts():
-            t = cut_point_tables(f)
-            f1, v1 = b1.eval_device(t["x"], check=False)
-            f2, v2 = b2.eval_device(t["y"], check=False)
-            cw = f.coeff.at_device(t["P"]) * t["W"] if not f.coeff.identity else t["W"]
-            Q = (b1.p + 1) * (b2.p + 1)
-            self.cut = dict(idx=t["idx"], ptr=t["ptr"], cw=cw.contiguous(), f1=f1, v1=v1, f2=f2, v2=v2,
-                            npts=t["npts"], grp_ptr=t["grp_ptr"], grp_key=t["grp_key"], grp_pts=t["grp_pts"],
-                            grp_perm=t["grp_perm"], ngroups=t["ngroups"],
-                            blocks=torch.empty(max(t["ngroups"], 1) * Q * Q, dtype=torch.float64, device=f.dev))
-            f.report.n_cutcell_points = t["npts"]
+        # cut-element points (host C++ geometry, device basis tables); taken
+        # from the pass-start launch when the pass made one
+        pre = getattr(f, "_cut_pre", None)
+        self.cut = pre if pre is not None else (_cut_tables(f) if f.config.has_cuts() else None)
 
     def ctx(self, desc, raw, nraw):
         f = self.f
@@ -359,6 +350,59 @@ class _Setup:
                       P(cut.get("f2")), P(cut.get("v2")), P(cut.get("grp_ptr")), P(cut.get("grp_key")),
                       P(cut.get("grp_pts")), P(cut.get("grp_perm")), P(cut.get("blocks")), cut.get("ngroups", 0),
                       P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
+
+
+def _cut_tables(f):
+    """Cut-element point tables, their basis values and weights (no
+    dependence on the WQ fits)."""
+    b1, b2 = f.b1, f.b2
+    t = cut_point_tables(f)
+    f1, v1 = b1.eval_device(t["x"], check=False)
+    f2, v2 = b2.eval_device(t["y"], check=False)
+    cw = f.coeff.at_device(t["P"]) * t["W"] if not f.coeff.identity else t["W"]
+    Q = (b1.p + 1) * (b2.p + 1)
+    f.report.n_cutcell_points = t["npts"]
+    return dict(idx=t["idx"], ptr=t["ptr"], cw=cw.contiguous(), f1=f1, v1=v1, f2=f2, v2=v2,
+                npts=t["npts"], grp_ptr=t["grp_ptr"], grp_key=t["grp_key"], grp_pts=t["grp_pts"],
+                grp_perm=t["grp_perm"], ngroups=t["ngroups"],
+                blocks=torch.empty(max(t["ngroups"], 1) * Q * Q, dtype=torch.float64, device=f.dev))
+
+
+def _cut_blocks_ctx(f, cut):
+    P = L.ptr
+    return RawCtx(n1=f.b1.n, n2=f.b2.n, p1=f.b1.p, p2=f.b2.p, nel1=f.b1.num_elements, nel2=f.b2.num_elements,
+                  cutidx=P(cut["idx"]), cut_ptr=P(cut["ptr"]), cut_cw=P(cut["cw"]), cfirst1=P(cut["f1"]),
+                  cvals1=P(cut["v1"]), cfirst2=P(cut["f2"]), cvals2=P(cut["v2"]), grp_ptr=P(cut["grp_ptr"]),
+                  grp_key=P(cut["grp_key"]), grp_pts=P(cut["grp_pts"]), grp_perm=P(cut["grp_perm"]),
+                  grp_blocks=P(cut["blocks"]), ngroups=cut["ngroups"])
+
+
+_NAMED = {}
+
+
+def prelaunch_cut_blocks(f):
+    """Launch the cut-element blocks at the start of a captured pass on
+    their own stream: they depend only on geometry, so they overlap the
+    WQ fits.  The cut-cell gather joins the stream (``join_cut_blocks``)."""
+    if not f.config.has_cuts() or not needs_raw(f):
+        return
+    _bind()
+    dev = torch.cuda.current_device()
+    s = _NAMED.setdefault((dev, "cut_blocks"), torch.cuda.Stream())
+    with _forked(torch.cuda.current_stream(), s):
+        cut = _cut_tables(f)
+        L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())
+        from .assembly import _stamp
+        _stamp("cutpre:blocks")
+    f._cut_pre = cut
+    f._cut_stream = s
+
+
+def join_cut_blocks(f):
+    s = getattr(f, "_cut_stream", None)
+    if s is not None:
+        torch.cuda.current_stream().wait_stream(s)
+        f._cut_stream = None
 
 
 def _plan(f):
@@ -453,5 +497,7 @@ def run_phase(f, phase):
             L.call("tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells":
         if f._setup.cut is not None:
-            L.call("tq_cut_blocks", f._ctx, L.stream())
+            if getattr(f, "_cut_pre", None) is None:
+                L.call("tq_cut_blocks", f._ctx, L.stream())
+            join_cut_blocks(f)
             L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())

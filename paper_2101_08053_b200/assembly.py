@@ -343,26 +343,40 @@ class Formation:
             self.deep = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
             L.call("tq_deep_flags", self.rowctx(), L.ptr(self.config.func_class_dev), L.ptr(self.raw_list),
                    self.raw_list.numel(), L.ptr(self.deep), L.stream())
+            _stamp("deep_flags")
         self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
         work = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         with self.timer("counts"):
             L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            _stamp("counts_deep")
             if join is not None:
                 torch.cuda.current_stream().wait_stream(join)
+            _stamp("join")
             L.call("tq_row_counts_rest", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            _stamp("counts_rest")
         indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
         with self.timer("scan"):
             L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr),
                    None if self.capture else L.C.byref(nnz), L.stream())
+        _stamp("scan")
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
         data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
         with self.timer("fill"):
             L.call("tq_fill_rows", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
+        _stamp("fill")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
+
+
+STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
+
+
+def _stamp(name):
+    if STAMPS is not None:
+        STAMPS(name)
 
 
 def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None,
@@ -378,10 +392,17 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     if config.has_cuts():     # shared geometry, outside the clock (src/assembly.py:505-508)
         config.cut_cell_rule(max(basis2d.degrees))
     clk = _Clock(active=capture is None)
+    _stamp("start")
+    if capture is not None:
+        from ._rawrows import prelaunch_cut_blocks
+        prelaunch_cut_blocks(f)
     f.build_weights(rules)
+    _stamp("weights")
     rep.t_weights = clk.lap()
     f.interior_products()
+    _stamp("products")
     f.raw_rows("interior")
+    _stamp("raw_interior")
     rep.t_interior = clk.lap()
     rb, re_ = (0, f.K) if row_range is None else row_range
     if capture is not None:
@@ -390,7 +411,9 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
         side = _side_streams(1)[0]
         with _forked(main, side):
             f.raw_rows("cut")
+            _stamp("side:raw_cut")
             f.raw_rows("cutcells")
+            _stamp("side:cutcells")
         csr = f.finish(rb, re_, join=side)
     else:
         f.raw_rows("cut")

@@ -38,3 +38,17 @@ extern "C" int tq_device_sync(void* stream) {
 
 // kernels launched by this library since load (host counter, no device state)
 extern "C" long long tq_launch_count(void) { return tq::g_launches.load(); }
+
+// Timeline probe: writes the device global timer (ns) into stamps[slot] in
+// stream order.  Used to read phase boundaries out of a replayed graph.
+__global__ void k_stamp(unsigned long long* stamps, int slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[slot] = t;
+}
+
+extern "C" int tq_debug_stamp(unsigned long long* stamps, int32_t slot, void* stream) {
+    k_stamp<<<1, 1, 0, tq::S(stream)>>>(stamps, slot);
+    TQ_LAUNCH_CHECK("k_stamp");
+    return TQ_OK;
+}

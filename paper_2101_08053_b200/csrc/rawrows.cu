@@ -193,50 +193,63 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     }
 }
 
-// Element blocks of the cut elements: one block per (cut element, span key)
-// group, G[A][B] = sum_pts (c w) B_A B_B with A, B local (a1, a2) indices --
-// the B2d^T (cw B2d) of src/assembly.py:384-387.  Points staged in shared
-// memory 64 at a time; each thread owns entries of the Q x Q block.
-constexpr int kGrpStage = 64;
-
+// Element blocks of the cut elements: one warp per (cut element, span key)
+// group, G[A][B] = sum_pts (c w) B_A B_B with A = (a1, a2), B = (b1, b2)
+// local indices -- the B2d^T (cw B2d) of src/assembly.py:384-387.  A group
+// holds ~q^2 points and Q^2 entries, so the work is tiny and latency-bound:
+// lane l owns the (a1, b1) pair l (+32, ...) and keeps the Q2 x Q2 (a2, b2)
+// accumulators in registers; points are staged 32 at a time in warp-private
+// shared memory (one lane gathers one point through the group permutation).
+template <int Q2>
 __global__ void k_cut_blocks(tq_rawctx c) {
     extern __shared__ double sm[];
-    const int q1 = c.p1 + 1, q2 = c.p2 + 1, Q = q1 * q2;
-    double* sv1 = sm;                       // kGrpStage x q1
-    double* sv2 = sv1 + kGrpStage * q1;     // kGrpStage x q2
-    double* scw = sv2 + kGrpStage * q2;     // kGrpStage
-    // thread owns (A, b1) and accumulates the q2 entries B = (b1, 0..q2-1)
-    const int nt = Q * q1;
-    for (int g = blockIdx.x; g < c.ngroups; g += gridDim.x) {
-        const int64_t p0 = c.grp_pts[g], p1e = c.grp_pts[g + 1];
-        const int tid = threadIdx.x;
-        const int A = tid / q1, b1 = tid - (tid / q1) * q1;
-        const int a1 = A / q2, a2 = A - (A / q2) * q2;
-        double acc[kMaxP + 1];
-        for (int z = 0; z < q2; ++z) acc[z] = 0.0;
-        for (int64_t base = p0; base < p1e; base += kGrpStage) {
-            const int np = (int)(p1e - base < kGrpStage ? p1e - base : kGrpStage);
-            __syncthreads();
-            for (int q = threadIdx.x; q < np * (q1 + q2 + 1); q += blockDim.x) {
-                int k = q / (q1 + q2 + 1), o = q - k * (q1 + q2 + 1);
-                int64_t pt = c.grp_perm[base + k];
-                if (o < q1) sv1[k * q1 + o] = c.cvals1[pt * q1 + o];
-                else if (o < q1 + q2) sv2[k * q2 + (o - q1)] = c.cvals2[pt * q2 + (o - q1)];
-                else scw[k] = c.cut_cw[pt];
-            }
-            __syncthreads();
-            if (tid < nt) {
-                for (int k = 0; k < np; ++k) {
-                    const double* v2 = sv2 + k * q2;
-                    const double s = (sv1[k * q1 + a1] * v2[a2]) * scw[k] * sv1[k * q1 + b1];
-#pragma unroll 4
-                    for (int z = 0; z < q2; ++z) acc[z] += s * v2[z];
+    const int q1 = c.p1 + 1, Q = q1 * Q2, st = q1 + Q2 + 1;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    double* sp = sm + wib * 32 * st;
+    for (int g = blockIdx.x * wpb + wib; g < c.ngroups; g += gridDim.x * wpb) {
+        const int64_t p0 = c.grp_pts[g], pe = c.grp_pts[g + 1];
+        for (int pr0 = 0; pr0 < q1 * q1; pr0 += 32) {
+            const int pr = pr0 + lane;
+            const bool act = pr < q1 * q1;
+            const int a1 = act ? pr / q1 : 0, b1 = act ? pr - (pr / q1) * q1 : 0;
+            double acc[Q2 * Q2];
+#pragma unroll
+            for (int z = 0; z < Q2 * Q2; ++z) acc[z] = 0.0;
+            for (int64_t base = p0; base < pe; base += 32) {
+                const int np = (int)(pe - base < 32 ? pe - base : 32);
+                __syncwarp();
+                if (lane < np) {
+                    const int64_t pt = c.grp_perm[base + lane];
+                    double* d = sp + lane * st;
+                    for (int o = 0; o < q1; ++o) d[o] = c.cvals1[pt * q1 + o];
+#pragma unroll
+                    for (int o = 0; o < Q2; ++o) d[q1 + o] = c.cvals2[pt * Q2 + o];
+                    d[q1 + Q2] = c.cut_cw[pt];
+                }
+                __syncwarp();
+                if (act) {
+                    for (int k = 0; k < np; ++k) {
+                        const double* d = sp + k * st;
+                        const double s = (d[q1 + Q2] * d[a1]) * d[b1];
+                        double v2[Q2];
+#pragma unroll
+                        for (int o = 0; o < Q2; ++o) v2[o] = d[q1 + o];
+#pragma unroll
+                        for (int a2 = 0; a2 < Q2; ++a2) {
+                            const double u = s * v2[a2];
+#pragma unroll
+                            for (int b2 = 0; b2 < Q2; ++b2) acc[a2 * Q2 + b2] = fma(u, v2[b2], acc[a2 * Q2 + b2]);
+                        }
+                    }
                 }
             }
-        }
-        if (tid < nt) {
-            double* out = c.grp_blocks + ((int64_t)g * Q + A) * Q + b1 * q2;
-            for (int z = 0; z < q2; ++z) out[z] = acc[z];
+            if (act) {
+                double* out = c.grp_blocks + (int64_t)g * Q * Q;
+#pragma unroll
+                for (int a2 = 0; a2 < Q2; ++a2)
+#pragma unroll
+                    for (int b2 = 0; b2 < Q2; ++b2) out[(a1 * Q2 + a2) * Q + b1 * Q2 + b2] = acc[a2 * Q2 + b2];
+            }
         }
     }
 }
@@ -344,12 +357,16 @@ extern "C" int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int
 
 extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
     if (c.ngroups <= 0) return TQ_OK;
-    const int Q = (c.p1 + 1) * (c.p2 + 1);
-    const int nt = Q * (c.p1 + 1);
-    if (nt > 1024) { set_error("degree too high for the cut-block kernel"); return TQ_EINVAL; }
-    const int bs = (nt + 31) / 32 * 32;
-    size_t shm = sizeof(double) * kGrpStage * (c.p1 + c.p2 + 3);
-    k_cut_blocks<<<(int)std::min<int64_t>(c.ngroups, (int64_t)kSms * 32), bs, shm, S(stream)>>>(c); ::tq::note_launch();
+    if (c.p1 < 1 || c.p1 > kMaxP || c.p2 < 1 || c.p2 > kMaxP) { set_error("degree out of range"); return TQ_EINVAL; }
+    constexpr int wpb = 4;
+    const size_t shm = sizeof(double) * wpb * 32 * (c.p1 + c.p2 + 3);
+    const int grid = (int)std::min<int64_t>((c.ngroups + wpb - 1) / wpb, (int64_t)kSms * 64);
+    switch (c.p2 + 1) {
+#define TQ_CB(Q2) case Q2: k_cut_blocks<Q2><<<grid, 32 * wpb, shm, S(stream)>>>(c); break;
+        TQ_CB(2) TQ_CB(3) TQ_CB(4) TQ_CB(5) TQ_CB(6) TQ_CB(7) TQ_CB(8) TQ_CB(9) TQ_CB(10) TQ_CB(11)
+#undef TQ_CB
+    }
+    ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_cut_blocks");
     return TQ_OK;
 }

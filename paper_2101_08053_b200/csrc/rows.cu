@@ -477,12 +477,20 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     int* irr = nullptr;   // [0] = count, [1..] = rows for the irregular kernel
     cudaStream_t st = S(stream);
     auto launch = [&](auto kern, auto kirr, size_t per_warp) -> int {
-        int wpb = 8;
-        while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
+        // launch configuration cached per kernel instance (host calls kept
+        // off the per-pass path)
+        static int cached_wpb[kMaxP + 1] = {}, cached_per_sm[kMaxP + 1] = {};
+        int wpb = cached_wpb[P];
+        int per_sm = cached_per_sm[P];
+        if (!wpb) {
+            wpb = 8;
+            while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
+            TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * wpb)));
+            TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, per_warp * wpb));
+            cached_wpb[P] = wpb;
+            cached_per_sm[P] = per_sm;
+        }
         const size_t shm = per_warp * wpb;
-        TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        int per_sm = 0;
-        TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, shm));
         const int64_t full = (int64_t)kSms * std::max(per_sm, 1);
         const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
         TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (nrows + 1), st));
