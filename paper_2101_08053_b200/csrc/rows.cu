@@ -155,30 +155,11 @@ template <int P>
 struct alignas(16) RegularSlice {
     static constexpr int W = 2 * P + 1;
     FillStage<P> stage[2];
-    double l1[W], l1t[W];
-    int lcb[W];
     double band[(32 + 2 * P) * W];
 };
 
 template <int P>
 constexpr size_t fill_slice_bytes() { return (sizeof(RegularSlice<P>) + 15) / 16 * 16; }
-
-// side stream and fork/join events of the fill (host objects, one set per device)
-static cudaStream_t side_stream() {
-    static cudaStream_t s[64] = {};
-    int d = 0;
-    cudaGetDevice(&d);
-    if (!s[d]) cudaStreamCreateWithFlags(&s[d], cudaStreamNonBlocking);
-    return s[d];
-}
-static cudaEvent_t make_event(cudaEvent_t* slot) {
-    int d = 0;
-    cudaGetDevice(&d);
-    if (!slot[d]) cudaEventCreateWithFlags(&slot[d], cudaEventDisableTiming);
-    return slot[d];
-}
-static cudaEvent_t fork_event() { static cudaEvent_t e[64] = {}; return make_event(e); }
-static cudaEvent_t join_event() { static cudaEvent_t e[64] = {}; return make_event(e); }
 
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
@@ -195,19 +176,24 @@ template <int P>
 __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S, int lane, int i1, int i20, int L,
                                          int pos0, int& nbulk, int32_t* __restrict__ indices,
                                          double* __restrict__ data) {
-    constexpr int W = 2 * P + 1, WW = W * W, R = 32 / W, CH = fill_chunk<P>();
+    constexpr int W = 2 * P + 1, WW = W * W, R = 32 / W, CH = fill_chunk<P>(), M = (W + R - 1) / R;
     __syncwarp();
-    if (lane < W) {
-        const int j1 = i1 - P + lane;
-        S.l1[lane] = __ldg(c.a1 + (int64_t)i1 * W + lane);
-        S.l1t[lane] = __ldg(c.a1 + (int64_t)j1 * W + (2 * P - lane));
-        S.lcb[lane] = __ldg(c.col_of + (int64_t)j1 * c.n2 + (i20 - P));
+    const bool act = lane < R * W;
+    const int q2 = lane % W, r0 = lane / W;
+    // direction-1 factors and column bases of this lane's q1 = m R + r0 (fixed for the run)
+    double rl1[M], rl1t[M];
+    int rcb[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int q1 = m * R + r0, j1 = i1 - P + q1;
+        const bool ok = act && q1 < W;
+        rl1[m] = ok ? __ldg(c.a1 + (int64_t)i1 * W + q1) : 0.0;
+        rl1t[m] = ok ? __ldg(c.a1 + (int64_t)j1 * W + (2 * P - q1)) : 0.0;
+        rcb[m] = ok ? __ldg(c.col_of + (int64_t)j1 * c.n2 + (i20 - P)) : 0;
     }
     const double* bsrc = c.a2 + (int64_t)(i20 - P) * W;
     for (int q = lane; q < (L + 2 * P) * W; q += 32) S.band[q] = __ldg(bsrc + q);
     __syncwarp();
-    const bool act = lane < R * W;
-    const int q2 = lane % W, r0 = lane / W;
     for (int k = 0; k * CH < L; ++k) {
         const int rows = min(CH, L - k * CH);
         const int n = rows * WW;
@@ -220,12 +206,12 @@ __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S,
             const int t = k * CH + tt;
             const double a2 = S.band[(t + P) * W + q2], a2t = S.band[(t + q2) * W + (2 * P - q2)];
 #pragma unroll
-            for (int m = 0; m < (W + R - 1) / R; ++m) {
+            for (int m = 0; m < M; ++m) {
                 const int q1 = m * R + r0;
                 if (act && q1 < W) {
                     const int e = tt * WW + q1 * W + q2;
-                    st.x[offx + e] = S.lcb[q1] + t + q2;
-                    st.d[offd + e] = 0.5 * (S.l1[q1] * a2 + S.l1t[q1] * a2t);
+                    st.x[offx + e] = rcb[m] + t + q2;
+                    st.d[offd + e] = 0.5 * (rl1[m] * a2 + rl1t[m] * a2t);
                 }
             }
         }
