@@ -13,7 +13,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtq_b200.so")
+LIB_PATH = os.environ.get("TQ_LIB") or os.path.join(HERE, "libtq_b200.so")   # TQ_LIB: A/B builds
 
 TQ_OK, TQ_EINVAL, TQ_ERULE, TQ_ETRIM, TQ_EPATTERN, TQ_ECUDA, TQ_EOVERFLOW = range(7)
 INTERIOR, CUT, EXTERIOR = 0, 1, 2
