@@ -186,13 +186,22 @@ int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows
 
 int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
 /* the two passes of tq_row_counts, separately launchable so the deep pass can
- * overlap the raw-row kernels: `work` = caller scratch of nrows + 1 ints */
+ * overlap the raw-row kernels.  `work` = caller scratch of 2*nrows + 2 ints:
+ * work[0] = |A|, work[1] = |B|, list A (rows needing the value-based count)
+ * at work + 2, list B (deep rows with a partial window) at work + 2 + nrows */
 int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream);
 int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream);
 int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                  void* stream);
+/* tq_fill_rows split in two after tq_row_counts_deep/_rest: tq_fill_fast
+ * writes the fast rows (every row when the context has no separable
+ * factors), tq_fill_listed the rows of lists A and B in `work`.  They write
+ * disjoint rows and may run concurrently on two streams. */
+int tq_fill_fast(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data, void* stream);
+int tq_fill_listed(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
+                   const int32_t* work, void* stream);
 
 
 /* ---- raw (non-separable) rows ------------------------------------------ */

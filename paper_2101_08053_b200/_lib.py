@@ -92,6 +92,8 @@ def lib():
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_fill_listed": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),
         "tq_deep_flags": ([RowCtx, vp, vp, i32, vp, vp], i32),
     }

@@ -380,6 +380,11 @@ def _cut_blocks_ctx(f, cut):
 _NAMED = {}
 
 
+def _named_stream(name):
+    dev = torch.cuda.current_device()
+    return _NAMED.setdefault((dev, name), torch.cuda.Stream())
+
+
 def prelaunch_cut_blocks(f):
     """Launch the cut-element blocks at the start of a captured pass on
     their own stream: they depend only on geometry, so they overlap the
@@ -387,8 +392,7 @@ def prelaunch_cut_blocks(f):
     if not f.config.has_cuts() or not needs_raw(f):
         return
     _bind()
-    dev = torch.cuda.current_device()
-    s = _NAMED.setdefault((dev, "cut_blocks"), torch.cuda.Stream())
+    s = _named_stream("cut_blocks")
     with _forked(torch.cuda.current_stream(), s):
         cut = _cut_tables(f)
         L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())

@@ -332,6 +332,21 @@ class Formation:
                         L.ptr(self.raw if self.raw is not None else dummy),
                         L.ptr(self.deep), L.ptr(self.rowfast), row_begin, self.K if row_end is None else row_end)
 
+    def fill(self, ctx, indptr, indices, data):
+        """Fast rows by warp tiles on the current stream; the rows listed by
+        the count pass concurrently on a side stream."""
+        from ._rawrows import _named_stream
+        main = torch.cuda.current_stream()
+        side = _named_stream("fill_listed")
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            L.call("tq_fill_listed", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.ptr(self.work), L.stream())
+        L.call("tq_fill_fast", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
+        main.wait_stream(side)
+        if not torch.cuda.is_current_stream_capturing():
+            for t in (indptr, indices, data, self.work):
+                t.record_stream(side)
+
     def finish(self, row_begin=0, row_end=None, join=None) -> DeviceCSR:
         """Count -> scan -> fill: symmetrised, zero-dropped, sorted CSR rows
         [row_begin, row_end) (src/assembly.py:400-404).  ``join``: a side
@@ -347,7 +362,7 @@ class Formation:
         self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
-        work = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
+        work = torch.empty(2 * nrows + 2, dtype=torch.int32, device=self.dev)
         with self.timer("counts"):
             L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_deep")
@@ -365,8 +380,9 @@ class Formation:
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
         data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
+        self.work = work
         with self.timer("fill"):
-            L.call("tq_fill_rows", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
+            self.fill(ctx, indptr, indices, data)
         _stamp("fill")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 

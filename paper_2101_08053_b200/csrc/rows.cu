@@ -83,9 +83,10 @@ __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e
 
 // Counts, pass 1 (thread per row, no raw values needed): deep rows are
 // counted arithmetically and flagged fast when their window is full; other
-// rows are appended to a list for pass 2.
+// rows are appended to list A (counted by pass 2), deep rows with a partial
+// window to list B (both lists feed the row-parallel fill).
 __global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int* __restrict__ list,
-                                  int* __restrict__ nlist) {
+                                  int* __restrict__ nlist, int* __restrict__ listb, int* __restrict__ nlistb) {
     for (int r = c.row_begin + blockIdx.x * blockDim.x + threadIdx.x; r < c.row_end; r += gridDim.x * blockDim.x) {
         const int idx = __ldg(c.active + r);
         if (c.deep && __ldg(c.deep + idx)) {
@@ -93,7 +94,9 @@ __global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int
             const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
             const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
             counts[r - c.row_begin] = t1 * t2;
-            if (c.rowfast) c.rowfast[r - c.row_begin] = (t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1) ? 1 : 0;
+            const bool full = t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1;
+            if (c.rowfast) c.rowfast[r - c.row_begin] = full ? 1 : 0;
+            if (!(full && c.rowfast)) listb[atomicAdd(nlistb, 1)] = r;
         } else {
             list[atomicAdd(nlist, 1)] = r;
         }
@@ -259,7 +262,8 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
             n_fast = c.rowfast ? __ldg(c.rowfast + (R1 + lane - c.row_begin)) : 0;
         }
         // rows that are not fast go to the row-parallel irregular kernel
-        const unsigned slow = __ballot_sync(0xffffffffu, valid && !my_fast);
+        // (listed here unless the count pass already listed them)
+        const unsigned slow = irr_rows ? __ballot_sync(0xffffffffu, valid && !my_fast) : 0u;
         if (slow) {
             int base = 0;
             if (lane == 0) base = atomicAdd(irr_count, __popc(slow));
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
     if (lane == 0) bulk_wait_all();
 }
 
-// Rows of the irregular tiles, one warp per row over the whole GPU: deep
+// Listed rows (list A then list B), one warp per row over the whole GPU: deep
 // rows from their direction factors (lanes 0..2P hold A1, A1T, column base,
 // A2, A2T; entries built by shuffles), other rows through the value-based
 // symmetrise/compact path.
@@ -298,14 +302,16 @@ template <int P>
 __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32_t* __restrict__ indptr,
                                                          int32_t* __restrict__ indices, double* __restrict__ data,
                                                          const int* __restrict__ irr_rows,
-                                                         const int* __restrict__ irr_count) {
+                                                         const int* __restrict__ irr_count,
+                                                         const int* __restrict__ irr_rows_b,
+                                                         const int* __restrict__ irr_count_b) {
     constexpr int W = 2 * P + 1;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    const int nrows = *irr_count;
+    const int na = *irr_count, nrows = na + (irr_count_b ? *irr_count_b : 0);
     for (int u = warp; u < nrows; u += nw) {
-        const int r = irr_rows[u];
+        const int r = u < na ? irr_rows[u] : irr_rows_b[u - na];
         RowGeom g = row_geom(c, r);
         int pos = __ldg(indptr + (r - c.row_begin));
         const int n = g.t1 * g.t2;
@@ -427,19 +433,21 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
 }
 
 // pass 1 only needs the deep flags; pass 2 needs the raw rows.  `work`:
-// caller scratch of (row_end - row_begin + 1) ints.
+// caller scratch of 2 (row_end - row_begin) + 2 ints: [0] = |A|, [1] = |B|,
+// list A at work + 2, list B at work + 2 + nrows.
 extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream) {
     int nrows = c.row_end - c.row_begin;
-    TQ_CUDA(cudaMemsetAsync(work, 0, sizeof(int32_t), S(stream)));
+    TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
-    k_row_counts_deep<<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, counts, work + 1, work); ::tq::note_launch();
+    k_row_counts_deep<<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, counts, work + 2, work, work + 2 + nrows,
+                                                                    work + 1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_deep");
     return TQ_OK;
 }
 
 extern "C" int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream) {
     if (c.row_end <= c.row_begin) return TQ_OK;
-    k_row_counts_list<<<kSms * 16, 256, 0, S(stream)>>>(c, counts, work + 1, work); ::tq::note_launch();
+    k_row_counts_list<<<kSms * 16, 256, 0, S(stream)>>>(c, counts, work + 2, work); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_list");
     return TQ_OK;
 }
@@ -448,7 +456,7 @@ extern "C" int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream) {
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
     int32_t* work = nullptr;
-    TQ_CUDA(cudaMallocAsync(&work, sizeof(int32_t) * (nrows + 1), S(stream)));
+    TQ_CUDA(cudaMallocAsync(&work, sizeof(int32_t) * (2 * (int64_t)nrows + 2), S(stream)));
     int rc = tq_row_counts_deep(c, counts, work, stream);
     if (!rc) rc = tq_row_counts_rest(c, counts, work, stream);
     TQ_CUDA(cudaFreeAsync(work, S(stream)));
@@ -482,7 +490,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
         TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (nrows + 1), st));
         TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), st));
         kern<<<grid, 32 * wpb, shm, st>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
-        kirr<<<kSms * 8, 256, 0, st>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
+        kirr<<<kSms * 8, 256, 0, st>>>(c, indptr, indices, data, irr + 1, irr, nullptr, nullptr); ::tq::note_launch();
         TQ_CUDA(cudaFreeAsync(irr, st));
         return TQ_OK;
     };
@@ -498,6 +506,64 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     }
     if (rc) return rc;
     TQ_LAUNCH_CHECK("k_fill_rows");
+    return TQ_OK;
+}
+
+// Split fill (used with the lists of tq_row_counts_deep): runs of fast rows
+// by warp tiles, and the listed rows by the row-parallel kernel; the two
+// write disjoint rows and may run concurrently on different streams.
+template <int P>
+static int fill_fast_launch(const tq_rowctx& c, const int32_t* indptr, int32_t* indices, double* data,
+                            cudaStream_t st) {
+    static int cached_wpb = 0, cached_per_sm = 0;
+    const size_t per_warp = fill_slice_bytes<P>();
+    if (!cached_wpb) {
+        int wpb = 8, per_sm = 0;
+        while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
+        TQ_CUDA(cudaFuncSetAttribute(k_fill_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * wpb)));
+        TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_tiles<P>, 32 * wpb, per_warp * wpb));
+        cached_wpb = wpb;
+        cached_per_sm = per_sm;
+    }
+    const int wpb = cached_wpb, nrows = c.row_end - c.row_begin;
+    const int64_t full = (int64_t)kSms * std::max(cached_per_sm, 1);
+    const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
+    k_fill_tiles<P><<<grid, 32 * wpb, per_warp * wpb, st>>>(c, indptr, indices, data, nullptr, nullptr); ::tq::note_launch();
+    return TQ_OK;
+}
+
+static int fill_P(const tq_rowctx& c) { return (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0; }
+
+extern "C" int tq_fill_fast(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    if (nrows <= 0) return TQ_OK;
+    int rc = TQ_OK;
+    switch (fill_P(c)) {
+#define CASE(Q) case Q: rc = fill_fast_launch<Q>(c, indptr, indices, data, S(stream)); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+        default: {   // no separable factors: every row through the generic fill
+            int grid = (int)std::min<int64_t>((nrows + 7) / 8, (int64_t)kSms * 32);
+            k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch();
+        }
+    }
+    if (rc) return rc;
+    TQ_LAUNCH_CHECK("tq_fill_fast");
+    return TQ_OK;
+}
+
+extern "C" int tq_fill_listed(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
+                              const int32_t* work, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    if (nrows <= 0) return TQ_OK;
+    switch (fill_P(c)) {
+#define CASE(Q) case Q: k_fill_irregular<Q><<<kSms * 8, 256, 0, S(stream)>>>(c, indptr, indices, data, work + 2, \
+            work, work + 2 + nrows, work + 1); ::tq::note_launch(); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+        default: return TQ_OK;   // tq_fill_fast covered every row
+    }
+    TQ_LAUNCH_CHECK("tq_fill_listed");
     return TQ_OK;
 }
 
