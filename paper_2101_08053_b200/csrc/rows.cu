@@ -145,7 +145,9 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 constexpr int kWarpRows = 32;
 
 template <int P>
-constexpr int fill_chunk() { return (2 * P + 1) * (2 * P + 1) <= 81 ? 4 : ((2 * P + 1) * (2 * P + 1) <= 169 ? 2 : 1); }
+constexpr int fill_chunk() {   // rows per bulk copy: ~7.8 KB of staged entries (measured best at P = 4)
+    return 648 / ((2 * P + 1) * (2 * P + 1)) < 1 ? 1 : (648 / ((2 * P + 1) * (2 * P + 1)) > 32 ? 32 : 648 / ((2 * P + 1) * (2 * P + 1)));
+}
 
 template <int P>
 struct alignas(16) FillStage {
@@ -518,12 +520,23 @@ static int fill_fast_launch(const tq_rowctx& c, const int32_t* indptr, int32_t* 
     static int cached_wpb = 0, cached_per_sm = 0;
     const size_t per_warp = fill_slice_bytes<P>();
     if (!cached_wpb) {
-        int wpb = 8, per_sm = 0;
-        while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
-        TQ_CUDA(cudaFuncSetAttribute(k_fill_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * wpb)));
-        TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_tiles<P>, 32 * wpb, per_warp * wpb));
-        cached_wpb = wpb;
-        cached_per_sm = per_sm;
+        // warps per block maximising resident warps per SM (shared memory bound)
+        int dev = 0, smem_max = 0;
+        TQ_CUDA(cudaGetDevice(&dev));
+        TQ_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        TQ_CUDA(cudaFuncSetAttribute(k_fill_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        int best_w = 0;
+        for (int wpb = 1; wpb <= 8; ++wpb) {
+            if (per_warp * wpb > (size_t)smem_max) break;
+            int per_sm = 0;
+            TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_tiles<P>, 32 * wpb, per_warp * wpb));
+            if (per_sm * wpb > best_w || (per_sm * wpb == best_w && wpb > cached_wpb)) {
+                best_w = per_sm * wpb;
+                cached_wpb = wpb;
+                cached_per_sm = per_sm;
+            }
+        }
+        if (!cached_wpb) { set_error("fill staging does not fit in shared memory"); return TQ_EINVAL; }
     }
     const int wpb = cached_wpb, nrows = c.row_end - c.row_begin;
     const int64_t full = (int64_t)kSms * std::max(cached_per_sm, 1);
