@@ -19,7 +19,7 @@ import torch
 
 from . import _lib as L
 from ._lib import CUT, INTERIOR
-from .quadrature import (DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async, build_dwq,
+from .quadrature import (DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async_t, build_dwq,
                          compute_wq_rules, dwq_solve_async, gauss_legendre, place_wq_points)
 
 MODE_GAUSS, MODE_BOX, MODE_MASK = 0, 1, 2
@@ -228,15 +228,20 @@ def build_all_rules(f):
     main = torch.cuda.current_stream()
     sides = _side_streams(len(plans) + len(dplans))
     std, dwq_pending = [], {}
+    tables = []
     for k, pl in enumerate(plans):
         with _forked(main, sides[k]):
-            out = _solve_rows_async(pl)
-            _keep_on(main, out[1:])
+            out, tab = _solve_rows_async_t(pl)
+            _keep_on(main, out[1:] + (tab or ()))
         std.append(out)
+        tables.append(tab)
     for k, (key, pl) in enumerate(dplans.items()):
         with _forked(main, sides[len(plans) + k]):
             rs, fail = dwq_solve_async(pl, direction=key[0])
-            _keep_on(main, (rs.w, fail))
+            # basis table of the set's own basis at its points (geometry-only;
+            # built here so it overlaps the fits)
+            tab = rs.basis_table()
+            _keep_on(main, (rs.w, fail) + tuple(tab))
         dwq_pending[key] = (pl, rs, fail)
     for st in sides:
         main.wait_stream(st)
@@ -252,7 +257,10 @@ def build_all_rules(f):
         if any_fail and _failing(pl, fail):
             rules.append(compute_wq_rules(pl.basis, pl.layout, direction=d))   # enrichment retries
         else:
-            rules.append(WeightedRuleSet(pl.basis, pl.layout, wptr, k0, w, d))
+            rs = WeightedRuleSet(pl.basis, pl.layout, wptr, k0, w, d)
+            if tables[d] is not None:
+                rs._basis_tab = tables[d]      # the fit's own table at the same points
+            rules.append(rs)
     dwq = {}
     for key, (pl, rs, fail) in dwq_pending.items():
         if any_fail and _failing(pl.fit, fail):
@@ -279,14 +287,8 @@ class _Setup:
         self.f = f
         # element Gauss tables, (p+1) points (src/assembly.py:198-211);
         # basis values evaluated per formation as in the reference's _Run
-        self.eg = []
-        self.em = []
-        for b, (Xd, Wd) in zip((b1, b2), element_points(f)):
-            _, vals = b.eval_device(Xd, check=False)
-            self.eg.append((None, Wd, vals, Xd))
-            em = torch.empty(b.num_elements * (b.p + 1) ** 2, dtype=torch.float64, device=dev)
-            L.call("tq_elem_mass", L.ptr(vals), L.ptr(Wd), b.num_elements, b.p + 1, b.p, L.ptr(em), L.stream())
-            self.em.append(em)
+        pre = getattr(f, "_elem_pre", None)
+        self.eg, self.em = pre if pre is not None else _elem_tables(f)
         self.cg = None
         if not f.coeff.identity:
             self.cg = f.coeff.grid_device(self.eg[0][3], self.eg[1][3])
@@ -352,6 +354,20 @@ class _Setup:
                       P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
 
 
+def _elem_tables(f):
+    """Element Gauss tables ((p+1) points, src/assembly.py:198-211) and the
+    per-element 1-D mass blocks; basis values evaluated per formation as in
+    the reference's _Run."""
+    eg, em = [], []
+    for b, (Xd, Wd) in zip((f.b1, f.b2), element_points(f)):
+        _, vals = b.eval_device(Xd, check=False)
+        eg.append((None, Wd, vals, Xd))
+        m = torch.empty(b.num_elements * (b.p + 1) ** 2, dtype=torch.float64, device=f.dev)
+        L.call("tq_elem_mass", L.ptr(vals), L.ptr(Wd), b.num_elements, b.p + 1, b.p, L.ptr(m), L.stream())
+        em.append(m)
+    return eg, em
+
+
 def _cut_tables(f):
     """Cut-element point tables, their basis values and weights (no
     dependence on the WQ fits)."""
@@ -394,10 +410,18 @@ def prelaunch_cut_blocks(f):
     _bind()
     s = _named_stream("cut_blocks")
     with _forked(torch.cuda.current_stream(), s):
+        f._elem_pre = _elem_tables(f)
+        f._elem_event = torch.cuda.Event()
+        f._elem_event.record()
         cut = _cut_tables(f)
         L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())
         from .assembly import _stamp
         _stamp("cutpre:blocks")
+    # tensors made here are consumed on the main and raw side streams
+    tensors = [t for t in cut.values() if isinstance(t, torch.Tensor)]
+    tensors += [t for e in f._elem_pre[0] for t in e if isinstance(t, torch.Tensor)] + list(f._elem_pre[1])
+    for st in (torch.cuda.current_stream(), _side_streams(1)[0]):
+        _keep_on(st, tensors)
     f._cut_pre = cut
     f._cut_stream = s
 
@@ -490,10 +514,15 @@ def run_phase(f, phase):
         f._desc = g[dkey]
         W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
         f.raw = torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64, device=f.dev)
-        slot = f.slot
-        slot[f._desc[:, 0].long()] = torch.arange(desc.shape[0], dtype=torch.int32, device=f.dev)
-        f.raw_list = f._desc[:, 0].contiguous()
+        skey = ("slot", id(desc))
+        if skey not in g:
+            slot = torch.full_like(f.slot, -1)
+            slot[f._desc[:, 0].long()] = torch.arange(desc.shape[0], dtype=torch.int32, device=f.dev)
+            g[skey] = (slot, f._desc[:, 0].contiguous())
+        f.slot, f.raw_list = g[skey]
         f._ctx = f._setup.ctx(f._desc, f.raw, desc.shape[0])
+        if getattr(f, "_elem_pre", None) is not None:
+            torch.cuda.current_stream().wait_event(f._elem_event)   # tables from the pass-start stream
         if nint:
             L.call("tq_raw_regular", f._ctx, 0, nint, L.stream())
     elif phase == "cut":

@@ -276,7 +276,13 @@ class Formation:
         self.col_of, self.active, self.K = idx["col_of"], idx["active"], idx["K"]
         self.dev = L.device()
         n1, n2 = basis2d.shape
-        self.slot = torch.full((n1 * n2,), -1, dtype=torch.int32, device=self.dev)
+        # raw-row slot per function (-1: separable); geometry, cached per
+        # configuration -- the raw phase swaps in the map of its row plan
+        from ._rawrows import _geo
+        g = _geo(config)
+        if "slot_none" not in g:
+            g["slot_none"] = torch.full((n1 * n2,), -1, dtype=torch.int32, device=self.dev)
+        self.slot = g["slot_none"]
         self.a1 = self.a2 = None
         self.raw = None
         self.raw_list = torch.empty(0, dtype=torch.int32, device=self.dev)   # raw-row function ids

@@ -258,21 +258,29 @@ class _FitPlan:
         self.rows = L.dev(self.rows_h, torch.int32)
 
 
-def _solve_rows_async(plan: _FitPlan):
+def _solve_rows_async_t(plan: _FitPlan):
     """Launch the GPU moment fits of a plan (src/quadrature.py:281-303).
-    Returns (wptr, k0, w, fail) device tensors; no host sync."""
+    Returns ((wptr, k0, w, fail), (first, vals) basis table at the layout
+    points or None) as device tensors; no host sync."""
     basis, layout = plan.basis, plan.layout
     dev = L.device()
     k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
     w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
     fail = torch.zeros(max(plan.rows_h.size, 1), dtype=torch.int32, device=dev)
+    tab = None
     if plan.rows_h.size:
-        first, vals = basis.eval_device(layout.device_points(), check=False)
+        tab = basis.eval_device(layout.device_points(), check=False)
+        first, vals = tab
         mom = moments_device(basis)
         L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
                L.ptr(plan.rows), plan.rows_h.size, plan.tmax, plan.mmax, L.ptr(plan.wptr), L.ptr(k0), L.ptr(w),
                L.ptr(fail), L.stream())
-    return plan.wptr, k0, w, fail
+    return (plan.wptr, k0, w, fail), tab
+
+
+def _solve_rows_async(plan: _FitPlan):
+    """(wptr, k0, w, fail) of ``_solve_rows_async_t``."""
+    return _solve_rows_async_t(plan)[0]
 
 
 def _failing(plan, fail):
