@@ -183,6 +183,12 @@ typedef struct {
  * positive direction factors (the fill then needs no per-entry gathers) */
 int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows,
                   int32_t nraw, int8_t* deep, void* stream);
+/* tq_deep_flags in two parts: the geometric flag (interior, not raw, no raw
+ * row in the window; depends only on the row plan, so callers may keep it)
+ * and the per-pass positivity of the direction factors a1, a2 */
+int tq_deep_geometry(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows,
+                     int32_t nraw, int8_t* geo, void* stream);
+int tq_deep_apply(tq_rowctx c, const int8_t* geo, int8_t* deep, void* stream);
 
 int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
 /* the two passes of tq_row_counts, separately launchable so the deep pass can
@@ -193,6 +199,10 @@ int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream
 int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream);
 int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
+/* the same with caller scratch of tq_scan_workspace_bytes(nrows) bytes */
+int64_t tq_scan_workspace_bytes(int32_t nrows);
+int tq_scan_indptr_ws(const int32_t* counts, int32_t nrows, int32_t* indptr, void* ws,
+                      int64_t* nnz_h, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                  void* stream);
 /* tq_fill_rows split in two after tq_row_counts_deep/_rest: tq_fill_fast
@@ -257,6 +267,11 @@ typedef struct {
  * the element loop of the reference strategy (src/assembly.py:218-252,
  * 522-528, 553-648). */
 int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+/* tq_raw_regular in two launches: the element-Gauss part (writes the row
+ * blocks; element tables only, no WQ rules) and the sum-factorization part
+ * (adds onto them).  Bit-identical to the fused call. */
+int tq_raw_gauss(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+int tq_raw_sumfactor(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
 
 /* cut-element part of raw rows [r0, r1) (accumulates): element blocks
  * B^T diag(c w) B per (cut element, span key) group, then a row gather.

@@ -91,11 +91,15 @@ def lib():
         "tq_row_counts_deep": ([RowCtx, vp, vp, vp], i32),
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
+        "tq_scan_workspace_bytes": ([i32], i64),
+        "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_fill_listed": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),
         "tq_deep_flags": ([RowCtx, vp, vp, i32, vp, vp], i32),
+        "tq_deep_geometry": ([RowCtx, vp, vp, i32, vp, vp], i32),
+        "tq_deep_apply": ([RowCtx, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

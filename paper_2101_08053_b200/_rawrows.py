@@ -46,6 +46,8 @@ def _bind():
     L.optional("tq_raw_regular", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_raw_cutcells", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_cut_blocks", [RawCtx, L.vp])
+    L.optional("tq_raw_gauss", [RawCtx, L.i32, L.i32, L.vp])
+    L.optional("tq_raw_sumfactor", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_elem_mass", [L.vp, L.vp, L.i32, L.i32, L.i32, L.vp, L.vp])
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
@@ -180,7 +182,9 @@ def _side_streams(n):
     dev = torch.cuda.current_device()
     lst = _SIDE.setdefault(dev, [])
     while len(lst) < n:
-        lst.append(torch.cuda.Stream())
+        # high priority: the fit chains are short latency-bound kernels that
+        # must not queue behind the bulk raw-row work of the pass-start stream
+        lst.append(torch.cuda.Stream(priority=-3))
     return lst[:n]
 
 
@@ -288,21 +292,20 @@ class _Setup:
         # element Gauss tables, (p+1) points (src/assembly.py:198-211);
         # basis values evaluated per formation as in the reference's _Run
         pre = getattr(f, "_elem_pre", None)
-        self.eg, self.em = pre if pre is not None else _elem_tables(f)
-        self.cg = None
-        if not f.coeff.identity:
-            self.cg = f.coeff.grid_device(self.eg[0][3], self.eg[1][3])
+        self.eg, self.em, self.cg = pre if pre is not None else _elem_tables(f)
         # rule sets
         self.sets = ([], [])
         self.grids = None
+        self.key_index = _key_index(f)
         if f.rules is not None:
             r1, r2, dwq = f.rules
             self.sets[0].append(r1)
             self.sets[1].append(r2)
-            self.key_index = ({}, {})
+            ki = ({}, {})
             for (d, u), rs in sorted(dwq.items()):
-                self.key_index[d][u] = len(self.sets[d])
+                ki[d][u] = len(self.sets[d])
                 self.sets[d].append(rs)
+            self.key_index = ki       # imported rules may carry extra keys
             self.sets_dev = []
             for d, b in enumerate((b1, b2)):
                 arr = (RuleSetDev * len(self.sets[d]))()
@@ -355,9 +358,9 @@ class _Setup:
 
 
 def _elem_tables(f):
-    """Element Gauss tables ((p+1) points, src/assembly.py:198-211) and the
-    per-element 1-D mass blocks; basis values evaluated per formation as in
-    the reference's _Run."""
+    """Element Gauss tables ((p+1) points, src/assembly.py:198-211), the
+    per-element 1-D mass blocks and (c != 1) the coefficient on the Gauss
+    grid; basis values evaluated per formation as in the reference's _Run."""
     eg, em = [], []
     for b, (Xd, Wd) in zip((f.b1, f.b2), element_points(f)):
         _, vals = b.eval_device(Xd, check=False)
@@ -365,7 +368,33 @@ def _elem_tables(f):
         m = torch.empty(b.num_elements * (b.p + 1) ** 2, dtype=torch.float64, device=f.dev)
         L.call("tq_elem_mass", L.ptr(vals), L.ptr(Wd), b.num_elements, b.p + 1, b.p, L.ptr(m), L.stream())
         em.append(m)
-    return eg, em
+    cg = None if f.coeff.identity else f.coeff.grid_device(eg[0][3], eg[1][3])
+    return eg, em, cg
+
+
+def _key_index(f):
+    """Rule-set index per DWQ key and direction: 0 = standard rules, then
+    the DWQ sets in sorted key order (geometry: known before the fits)."""
+    ki = ({}, {})
+    if f.strategy == "dwq":
+        cnt = [1, 1]
+        for d, u in sorted(dwq_keys(f)):
+            ki[d][u] = cnt[d]
+            cnt[d] += 1
+    return ki
+
+
+def _gauss_ctx(f, eg, em, cg, desc, raw, nraw):
+    """Context of the element-Gauss part of the raw rows (no rule sets)."""
+    d1, d2 = f.b1.device_arrays(), f.b2.device_arrays()
+    P = L.ptr
+    return RawCtx(n1=f.b1.n, n2=f.b2.n, p1=f.b1.p, p2=f.b2.p, nel1=f.b1.num_elements, nel2=f.b2.num_elements,
+                  el_first1=P(d1["el_first"]), el_last1=P(d1["el_last"]), el_first2=P(d2["el_first"]),
+                  el_last2=P(d2["el_last"]), ov_lo1=P(d1["ov_lo"]), ov_hi1=P(d1["ov_hi"]), ov_lo2=P(d2["ov_lo"]),
+                  ov_hi2=P(d2["ov_hi"]), espan1=P(d1["espan"]), espan2=P(d2["espan"]),
+                  elem_class=P(f.config.element_class_dev), ng1=f.b1.p + 1, ng2=f.b2.p + 1,
+                  ew1=P(eg[0][1]), ev1=P(eg[0][2]), ew2=P(eg[1][1]), ev2=P(eg[1][2]), em1=P(em[0]), em2=P(em[1]),
+                  cg=P(cg), desc=P(desc), nraw=nraw, nmax1=1, nmax2=1, raw=P(raw))
 
 
 def _cut_tables(f):
@@ -396,31 +425,52 @@ def _cut_blocks_ctx(f, cut):
 _NAMED = {}
 
 
-def _named_stream(name):
+def _named_stream(name, priority=0):
+    """Cached side stream.  Priorities (lower = more urgent): fit chains -3,
+    the captured main chain -2, the bulk pass-start streams 0."""
     dev = torch.cuda.current_device()
-    return _NAMED.setdefault((dev, name), torch.cuda.Stream())
+    key = (dev, name)
+    if key not in _NAMED:
+        _NAMED[key] = torch.cuda.Stream(priority=priority)
+    return _NAMED[key]
 
 
-def prelaunch_cut_blocks(f):
-    """Launch the cut-element blocks at the start of a captured pass on
-    their own stream: they depend only on geometry, so they overlap the
-    WQ fits.  The cut-cell gather joins the stream (``join_cut_blocks``)."""
-    if not f.config.has_cuts() or not needs_raw(f):
+def prelaunch_geometry(f):
+    """Start the WQ-independent raw-row work of a captured pass on its own
+    stream, overlapping the fits: element tables, the element-Gauss part of
+    every raw row (tq_raw_gauss), the cut-element tables and blocks.  The
+    interior phase waits for the Gauss part (event), the cut-cell gather
+    joins the stream (``join_cut_blocks``)."""
+    if not needs_raw(f):
         return
     _bind()
     s = _named_stream("cut_blocks")
-    with _forked(torch.cuda.current_stream(), s):
-        f._elem_pre = _elem_tables(f)
+    main = torch.cuda.current_stream()
+    with _forked(main, s):
+        f._elem_pre = eg, em, cg = _elem_tables(f)
+        desc_dev, ndesc = _desc_dev(f)
+        f._desc_pre = desc_dev
+        W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
+        f._raw_pre = torch.empty((max(ndesc, 1), W), dtype=torch.float64, device=f.dev)
+        if ndesc:
+            L.call("tq_raw_gauss", _gauss_ctx(f, eg, em, cg, desc_dev, f._raw_pre, ndesc), 0, ndesc, L.stream())
         f._elem_event = torch.cuda.Event()
         f._elem_event.record()
-        cut = _cut_tables(f)
-        L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())
+    # cut-element tables and blocks: an independent chain on a second stream
+    s2 = _named_stream("cut_blocks2")
+    cut = None
+    with _forked(main, s2):
+        if f.config.has_cuts():
+            cut = _cut_tables(f)
+            L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())
         from .assembly import _stamp
         _stamp("cutpre:blocks")
+    s.wait_stream(s2)         # one stream to join later
     # tensors made here are consumed on the main and raw side streams
-    tensors = [t for t in cut.values() if isinstance(t, torch.Tensor)]
-    tensors += [t for e in f._elem_pre[0] for t in e if isinstance(t, torch.Tensor)] + list(f._elem_pre[1])
-    for st in (torch.cuda.current_stream(), _side_streams(1)[0]):
+    tensors = [t for t in (cut or {}).values() if isinstance(t, torch.Tensor)]
+    tensors += [t for e in eg for t in e if isinstance(t, torch.Tensor)] + list(em) + [f._raw_pre]
+    tensors += [cg] if cg is not None else []
+    for st in (main, _side_streams(1)[0]):
         _keep_on(st, tensors)
     f._cut_pre = cut
     f._cut_stream = s
@@ -436,16 +486,26 @@ def join_cut_blocks(f):
 def _plan(f):
     """Raw rows and their descriptors (host bookkeeping, cached per
     configuration / strategy / coefficient kind / DWQ key set)."""
-    key = ("plan", f.strategy, f.coeff.identity,
-           tuple(sorted(f._setup.key_index[0].items())) if f.rules is not None else (),
-           tuple(sorted(f._setup.key_index[1].items())) if f.rules is not None else ())
+    setup = getattr(f, "_setup", None)
+    ki = setup.key_index if setup is not None else _key_index(f)
+    key = ("plan", f.strategy, f.coeff.identity, tuple(sorted(ki[0].items())), tuple(sorted(ki[1].items())))
     g = _geo(f.config)
     if key not in g:
-        g[key] = _plan_uncached(f)
+        g[key] = _plan_uncached(f, ki)
     return g[key]
 
 
-def _plan_uncached(f):
+def _desc_dev(f):
+    """Device copy of the row plan's descriptors (cached) and its size."""
+    desc, _ = _plan(f)
+    g = _geo(f.config)
+    dkey = ("desc", id(desc))
+    if dkey not in g:
+        g[dkey] = L.dev(desc, torch.int32)
+    return g[dkey], desc.shape[0]
+
+
+def _plan_uncached(f, key_index):
     fc = f.config.func_class.ravel()
     act = active_host(f)
     n2 = f.b2.n
@@ -483,7 +543,6 @@ def _plan_uncached(f):
         else:  # dwq
             cut, routes = route_cut_rows(f)
             assert np.array_equal(cut, rows_cut)
-            setup = f._setup
             for k, rt in enumerate(routes):
                 if rt[0] != 1 or rt[3] < 0:
                     d[k, 1] = MODE_GAUSS
@@ -492,7 +551,7 @@ def _plan_uncached(f):
                 for dd in (0, 1):
                     if rt[1 + dd] >= 0:
                         u = float(f.config.u_disc[dd][rt[1 + dd]])
-                        s[dd] = setup.key_index[dd][u]
+                        s[dd] = key_index[dd][u]
                 d[k, 1:] = [MODE_BOX, s[0], s[1], rt[3], rt[4], rt[5], rt[6]]
         descs.append(d)
     desc = np.concatenate(descs) if descs else np.empty((0, 8), np.int32)
@@ -508,12 +567,13 @@ def run_phase(f, phase):
         f._nint = nint
         f._ndesc = desc.shape[0]
         g = _geo(f.config)
-        dkey = ("desc", id(desc))
-        if dkey not in g:
-            g[dkey] = L.dev(desc, torch.int32)
-        f._desc = g[dkey]
+        f._desc, _ = _desc_dev(f)
+        if getattr(f, "_raw_pre", None) is not None and f._desc is not f._desc_pre:
+            raise RuntimeError("row plan changed between the pass-start launch and the raw phase")
         W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
-        f.raw = torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64, device=f.dev)
+        pre = getattr(f, "_raw_pre", None)
+        f.raw = pre if pre is not None else torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64,
+                                                        device=f.dev)
         skey = ("slot", id(desc))
         if skey not in g:
             slot = torch.full_like(f.slot, -1)
@@ -521,13 +581,14 @@ def run_phase(f, phase):
             g[skey] = (slot, f._desc[:, 0].contiguous())
         f.slot, f.raw_list = g[skey]
         f._ctx = f._setup.ctx(f._desc, f.raw, desc.shape[0])
-        if getattr(f, "_elem_pre", None) is not None:
-            torch.cuda.current_stream().wait_event(f._elem_event)   # tables from the pass-start stream
+        if pre is not None:
+            torch.cuda.current_stream().wait_event(f._elem_event)   # Gauss part from the pass-start stream
         if nint:
-            L.call("tq_raw_regular", f._ctx, 0, nint, L.stream())
+            L.call("tq_raw_sumfactor" if pre is not None else "tq_raw_regular", f._ctx, 0, nint, L.stream())
     elif phase == "cut":
         if f._ndesc > f._nint:
-            L.call("tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
+            L.call("tq_raw_sumfactor" if getattr(f, "_raw_pre", None) is not None else "tq_raw_regular",
+                   f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells":
         if f._setup.cut is not None:
             if getattr(f, "_cut_pre", None) is None:

@@ -343,7 +343,7 @@ class Formation:
         the count pass concurrently on a side stream."""
         from ._rawrows import _named_stream
         main = torch.cuda.current_stream()
-        side = _named_stream("fill_listed")
+        side = _named_stream("fill_listed", priority=-2)
         side.wait_stream(main)
         with torch.cuda.stream(side):
             L.call("tq_fill_listed", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.ptr(self.work), L.stream())
@@ -359,11 +359,21 @@ class Formation:
         stream still computing the raw rows; the deep-row pass overlaps it."""
         row_end = self.K if row_end is None else row_end
         nrows = row_end - row_begin
+        from ._rawrows import join_cut_blocks
+        join_cut_blocks(self)         # the pass-start stream rejoins (capture)
         if self.deep is None and self.a1 is not None:
             n1, n2 = self.basis2d.shape
+            # geometric flags: cached per row plan (keyed by its raw-row list)
+            from ._rawrows import _geo
+            g = _geo(self.config)
+            gkey = ("deep_geo", id(self.raw_list) if self.raw_list.numel() else None)
+            if gkey not in g:
+                geo = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
+                L.call("tq_deep_geometry", self.rowctx(), L.ptr(self.config.func_class_dev), L.ptr(self.raw_list),
+                       self.raw_list.numel(), L.ptr(geo), L.stream())
+                g[gkey] = (geo, self.raw_list)     # the list is kept alive with its key
             self.deep = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
-            L.call("tq_deep_flags", self.rowctx(), L.ptr(self.config.func_class_dev), L.ptr(self.raw_list),
-                   self.raw_list.numel(), L.ptr(self.deep), L.stream())
+            L.call("tq_deep_apply", self.rowctx(), L.ptr(g[gkey][0]), L.ptr(self.deep), L.stream())
             _stamp("deep_flags")
         self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
@@ -416,8 +426,8 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     clk = _Clock(active=capture is None)
     _stamp("start")
     if capture is not None:
-        from ._rawrows import prelaunch_cut_blocks
-        prelaunch_cut_blocks(f)
+        from ._rawrows import prelaunch_geometry
+        prelaunch_geometry(f)
     f.build_weights(rules)
     _stamp("weights")
     rep.t_weights = clk.lap()
@@ -477,7 +487,9 @@ class GraphFormation:
         lib = L.lib()
         lib.tq_launch_count.restype = L.C.c_longlong
         n0 = lib.tq_launch_count()
-        with torch.cuda.graph(self.graph):
+        from ._rawrows import _named_stream
+        cap = _named_stream("capture", priority=-2)      # the main chain outranks the bulk side streams
+        with torch.cuda.graph(self.graph, stream=cap):
             self.f, self.csr = form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
         self.launches_per_pass = int(lib.tq_launch_count() - n0)
         torch.cuda.synchronize()

@@ -75,6 +75,11 @@ __global__ void k_elem_mass(const double* __restrict__ ev, const double* __restr
     }
 }
 
+// PARTS: 1 = element-Gauss part only (writes the row block; needs no WQ
+// rules), 2 = sum-factorization part only (adds onto the stored block),
+// 3 = both.  Split or fused, each entry sees the same additions in the same
+// order, so the results are bit-identical.
+template <int PARTS>
 __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -91,10 +96,16 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
         RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
-        for (int q = lane; q < T; q += 32) blk[q] = 0.0;
+        if (PARTS == 2 && d.mode == TQ_ROW_GAUSS) continue;     // nothing to add
+        if (PARTS == 2) {
+            const double* src = c.raw + (int64_t)r * T;
+            for (int q = lane; q < T; q += 32) blk[q] = src[q];
+        } else {
+            for (int q = lane; q < T; q += 32) blk[q] = 0.0;
+        }
         __syncwarp();
         // -- element Gauss over interior support elements (GAUSS, BOX residual)
-        if (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX) {
+        if ((PARTS & 1) && (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX)) {
             for (int e1 = c.el_first1[i1]; e1 <= c.el_last1[i1]; ++e1) {
                 for (int e2 = c.el_first2[i2]; e2 <= c.el_last2[i2]; ++e2) {
                     if (c.elem_class[(int64_t)e1 * c.nel2 + e2] != TQ_INTERIOR) continue;
@@ -112,7 +123,7 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
             }
         }
         // -- sum factorization (BOX, MASK)
-        if (d.mode == TQ_ROW_BOX || d.mode == TQ_ROW_MASK) {
+        if ((PARTS & 2) && (d.mode == TQ_ROW_BOX || d.mode == TQ_ROW_MASK)) {
             const tq_ruleset s1 = c.sets1[d.set1];
             const tq_ruleset s2 = c.sets2[d.set2];
             const int k01 = s1.rules.k0[i1], k02 = s2.rules.k0[i2];
@@ -334,17 +345,30 @@ static size_t regular_smem_per_warp(const tq_rawctx& c) {
     return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * c.nmax1 + W1 + W2);
 }
 
-extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+template <int PARTS>
+static int raw_regular_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
     if (r1 <= r0) return TQ_OK;
     int wpb = 4;
     size_t shm = regular_smem_per_warp(c) * wpb;
     while (shm > 200 * 1024 && wpb > 1) { wpb /= 2; shm = regular_smem_per_warp(c) * wpb; }
     if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
-    TQ_CUDA(cudaFuncSetAttribute(k_raw_regular, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_regular<PARTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int grid = (int)std::min<int64_t>((r1 - r0 + wpb - 1) / wpb, (int64_t)kSms * 32);
-    k_raw_regular<<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    k_raw_regular<PARTS><<<grid, 32 * wpb, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_regular");
     return TQ_OK;
+}
+
+extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    return raw_regular_launch<3>(c, r0, r1, stream);
+}
+
+extern "C" int tq_raw_gauss(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    return raw_regular_launch<1>(c, r0, r1, stream);
+}
+
+extern "C" int tq_raw_sumfactor(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    return raw_regular_launch<2>(c, r0, r1, stream);
 }
 
 extern "C" int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int32_t ng, int32_t p, double* em,

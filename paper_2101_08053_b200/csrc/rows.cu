@@ -87,19 +87,37 @@ __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e
 // window to list B (both lists feed the row-parallel fill).
 __global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int* __restrict__ list,
                                   int* __restrict__ nlist, int* __restrict__ listb, int* __restrict__ nlistb) {
-    for (int r = c.row_begin + blockIdx.x * blockDim.x + threadIdx.x; r < c.row_end; r += gridDim.x * blockDim.x) {
-        const int idx = __ldg(c.active + r);
-        if (c.deep && __ldg(c.deep + idx)) {
-            const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
-            const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
-            const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
-            counts[r - c.row_begin] = t1 * t2;
-            const bool full = t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1;
-            if (c.rowfast) c.rowfast[r - c.row_begin] = full ? 1 : 0;
-            if (!(full && c.rowfast)) listb[atomicAdd(nlistb, 1)] = r;
-        } else {
-            list[atomicAdd(nlist, 1)] = r;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // grid-stride loop with a warp-uniform trip count (the appends are warp-aggregated)
+    const int n = c.row_end - c.row_begin, stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int r = c.row_begin + base + threadIdx.x;
+        bool to_a = false, to_b = false;
+        if (r < c.row_end) {
+            const int idx = __ldg(c.active + r);
+            if (c.deep && __ldg(c.deep + idx)) {
+                const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
+                const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
+                const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
+                counts[r - c.row_begin] = t1 * t2;
+                const bool full = t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1;
+                if (c.rowfast) c.rowfast[r - c.row_begin] = full ? 1 : 0;
+                to_b = !(full && c.rowfast);
+            } else {
+                to_a = true;
+            }
         }
+        const unsigned ma = __ballot_sync(0xffffffffu, to_a), mb = __ballot_sync(0xffffffffu, to_b);
+        int ba = 0, bb = 0;
+        if (lane == 0) {
+            if (ma) ba = atomicAdd(nlist, __popc(ma));
+            if (mb) bb = atomicAdd(nlistb, __popc(mb));
+        }
+        ba = __shfl_sync(0xffffffffu, ba, 0);
+        bb = __shfl_sync(0xffffffffu, bb, 0);
+        if (to_a) list[ba + __popc(ma & lt)] = r;
+        if (to_b) listb[bb + __popc(mb & lt)] = r;
     }
 }
 
@@ -388,26 +406,41 @@ __global__ void k_fill_rows(tq_rowctx c, const int32_t* __restrict__ indptr, int
     }
 }
 
-// 1-D positivity of a direction's factors over each window
-__global__ void k_pos(const double* __restrict__ a, int n, int p, const int32_t* __restrict__ ov_lo,
-                      const int32_t* __restrict__ ov_hi, int8_t* __restrict__ pos) {
-    const int W = 2 * p + 1;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// both directions in one launch: threads [0, n1) direction 1, [n1, n1+n2) direction 2
+__global__ void k_pos2(tq_rowctx c, int8_t* __restrict__ pos) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < c.n1) {
         bool ok = true;
-        for (int j = ov_lo[i]; j <= ov_hi[i]; ++j)
-            ok = ok && a[(int64_t)i * W + (j - i + p)] > 0.0 && a[(int64_t)j * W + (i - j + p)] > 0.0;
-        pos[i] = ok;
+        for (int j = c.ov_lo1[t]; j <= c.ov_hi1[t]; ++j)
+            ok = ok && c.a1[(int64_t)t * (2 * c.p1 + 1) + (j - t + c.p1)] > 0.0 &&
+                 c.a1[(int64_t)j * (2 * c.p1 + 1) + (t - j + c.p1)] > 0.0;
+        pos[t] = ok;
+    } else if (t < c.n1 + c.n2) {
+        const int i = t - c.n1;
+        bool ok = true;
+        for (int j = c.ov_lo2[i]; j <= c.ov_hi2[i]; ++j)
+            ok = ok && c.a2[(int64_t)i * (2 * c.p2 + 1) + (j - i + c.p2)] > 0.0 &&
+                 c.a2[(int64_t)j * (2 * c.p2 + 1) + (i - j + c.p2)] > 0.0;
+        pos[t] = ok;
     }
 }
 
-__global__ void k_deep_init(tq_rowctx c, const int8_t* __restrict__ fc, const int8_t* __restrict__ pos1,
-                            const int8_t* __restrict__ pos2, int8_t* __restrict__ deep) {
+// geometric part of the deep flag: interior, not raw (separable)
+__global__ void k_deep_init(tq_rowctx c, const int8_t* __restrict__ fc, int8_t* __restrict__ geo) {
     int64_t total = (int64_t)c.n1 * c.n2;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int i1 = (int)(t / c.n2), i2 = (int)(t - (int64_t)i1 * c.n2);
-        deep[t] = (fc[t] == TQ_INTERIOR && c.slot[t] < 0 && pos1[i1] && pos2[i2]) ? 1 : 0;
-    }
+         t += (int64_t)gridDim.x * blockDim.x)
+        geo[t] = (fc[t] == TQ_INTERIOR && c.slot[t] < 0) ? 1 : 0;
+}
+
+// deep = geometric flag && positive factors in both directions (row i1 per blockIdx.y)
+__global__ void k_deep_apply(tq_rowctx c, const int8_t* __restrict__ geo, const int8_t* __restrict__ pos,
+                             int8_t* __restrict__ deep) {
+    const int i1 = blockIdx.y;
+    const bool p1 = pos[i1];
+    const int64_t base = (int64_t)i1 * c.n2;
+    for (int i2 = blockIdx.x * blockDim.x + threadIdx.x; i2 < c.n2; i2 += gridDim.x * blockDim.x)
+        deep[base + i2] = (p1 && geo[base + i2] && pos[c.n1 + i2]) ? 1 : 0;
 }
 
 // a raw row j spoils the fast path of every row i with j in window(i), i.e.
@@ -580,20 +613,38 @@ extern "C" int tq_fill_listed(tq_rowctx c, const int32_t* indptr, int32_t* indic
     return TQ_OK;
 }
 
-extern "C" int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows, int32_t nraw,
-                             int8_t* deep, void* stream) {
+// geometric part (cacheable per row plan): interior && not raw && no raw row in the window
+extern "C" int tq_deep_geometry(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows, int32_t nraw,
+                                int8_t* geo, void* stream) {
     int64_t nf = (int64_t)c.n1 * c.n2;
+    if (nf == 0) return TQ_OK;
+    k_deep_init<<<grid_for(nf, 256), 256, 0, S(stream)>>>(c, func_class, geo); ::tq::note_launch();
+    if (nraw > 0) { k_deep_clear<<<grid_for(nraw, 128), 128, 0, S(stream)>>>(c, raw_rows, nraw, geo); ::tq::note_launch(); }
+    TQ_LAUNCH_CHECK("deep geometry");
+    return TQ_OK;
+}
+
+// per pass: deep = geo && positive direction factors (a1, a2 of the context)
+extern "C" int tq_deep_apply(tq_rowctx c, const int8_t* geo, int8_t* deep, void* stream) {
+    int64_t nf = (int64_t)c.n1 * c.n2;
+    if (nf == 0) return TQ_OK;
     if (!c.a1 || !c.a2) {
         TQ_CUDA(cudaMemsetAsync(deep, 0, nf, S(stream)));
         return TQ_OK;
     }
     int8_t* pos = nullptr;
     TQ_CUDA(cudaMallocAsync(&pos, c.n1 + c.n2, S(stream)));
-    k_pos<<<grid_for(c.n1, 128), 128, 0, S(stream)>>>(c.a1, c.n1, c.p1, c.ov_lo1, c.ov_hi1, pos); ::tq::note_launch();
-    k_pos<<<grid_for(c.n2, 128), 128, 0, S(stream)>>>(c.a2, c.n2, c.p2, c.ov_lo2, c.ov_hi2, pos + c.n1); ::tq::note_launch();
-    k_deep_init<<<grid_for(nf, 256), 256, 0, S(stream)>>>(c, func_class, pos, pos + c.n1, deep); ::tq::note_launch();
-    if (nraw > 0) k_deep_clear<<<grid_for(nraw, 128), 128, 0, S(stream)>>>(c, raw_rows, nraw, deep); ::tq::note_launch();
-    TQ_LAUNCH_CHECK("deep flags");
+    k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos); ::tq::note_launch();
+    dim3 grid((unsigned)std::min<int64_t>((c.n2 + 255) / 256, 4), (unsigned)c.n1);
+    k_deep_apply<<<grid, 256, 0, S(stream)>>>(c, geo, pos, deep); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("deep apply");
     TQ_CUDA(cudaFreeAsync(pos, S(stream)));
     return TQ_OK;
+}
+
+extern "C" int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows, int32_t nraw,
+                             int8_t* deep, void* stream) {
+    if (!c.a1 || !c.a2) return tq_deep_apply(c, nullptr, deep, stream);
+    int rc = tq_deep_geometry(c, func_class, raw_rows, nraw, deep, stream);   // in place: geo -> deep
+    return rc ? rc : tq_deep_apply(c, deep, deep, stream);
 }

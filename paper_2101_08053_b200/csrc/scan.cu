@@ -3,8 +3,13 @@
 //  tq_scan_indptr  <- the indptr of _Pattern / scipy CSR   src/assembly.py:154-166
 //  tq_active_index <- active_functions + col_of            src/trimming.py:514-517,
 //                                                          src/assembly.py:150-153
-// Three-phase tiled scan (tile sums -> scan of tile sums -> tile rescan).
+// Row pointer: one cooperative kernel (slab sums, grid barrier, rescan).  Active index: three-phase
+// tiled scan (tile sums -> scan of tile sums -> tile rescan).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tq {
 
@@ -12,10 +17,6 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kTile = kScanThreads * kScanItems;
 
-struct CountsIn {
-    const int32_t* v;
-    __device__ int64_t operator()(int64_t i) const { return v[i]; }
-};
 struct ActiveIn {
     const int8_t* fc;
     __device__ int64_t operator()(int64_t i) const { return fc[i] != TQ_EXTERIOR ? 1 : 0; }
@@ -108,14 +109,6 @@ __global__ void k_tile_apply(In in, int64_t n, const int64_t* tile_off, Out out)
     }
 }
 
-struct IndptrOut {
-    int32_t* indptr;
-    int32_t* overflow;
-    __device__ void operator()(int64_t i, int64_t v, int64_t excl) const {
-        if (excl > 0x7fffffffLL) atomicOr(overflow, 1);
-        indptr[i] = (int32_t)excl;
-    }
-};
 struct ActiveOut {
     int32_t* col_of;
     int32_t* active;
@@ -143,46 +136,177 @@ int scan_generic(In in, int64_t n, Out out, int64_t* total_h, cudaStream_t st) {
     return TQ_OK;
 }
 
-__global__ void k_set_last(int32_t* indptr, int64_t n, const int64_t* total) {
-    indptr[n] = (int32_t)(*total);
+
+// Row-pointer scan in one cooperative kernel: every block owns a contiguous
+// slab of the counts (all blocks co-resident), sums it, meets the others at
+// one grid barrier, takes its prefix from the block sums before it, and
+// rescans its slab (second read served by L2) writing indptr with int4
+// stores.  No look-back chain and no second launch.
+constexpr int kCoopThreads = 512;
+
+__device__ __forceinline__ int4 load4(const int32_t* p, int64_t i, int64_t hi, bool aligned) {
+    if (aligned && i + 3 < hi) return __ldg(reinterpret_cast<const int4*>(p + i));
+    int4 q = make_int4(0, 0, 0, 0);
+    if (i < hi) q.x = p[i];
+    if (i + 1 < hi) q.y = p[i + 1];
+    if (i + 2 < hi) q.z = p[i + 2];
+    if (i + 3 < hi) q.w = p[i + 3];
+    return q;
+}
+
+// block-wide sum of one value per thread (result in every thread)
+__device__ __forceinline__ long long block_sum(long long v, long long* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    long long t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    return t;
+}
+
+__global__ void __launch_bounds__(kCoopThreads) k_scan_coop(const int32_t* __restrict__ counts, int32_t n,
+                                                           int32_t* __restrict__ indptr,
+                                                           long long* __restrict__ blocksums, int32_t* ovf,
+                                                           int64_t* total_out) {
+    __shared__ long long red[kCoopThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t slab = (((int64_t)n + gridDim.x - 1) / gridDim.x + 3) / 4 * 4;
+    const int64_t lo = min((int64_t)n, (int64_t)blockIdx.x * slab), hi = min((int64_t)n, lo + slab);
+    const bool in_al = (reinterpret_cast<uintptr_t>(counts) & 15) == 0;
+    const bool out_al = (reinterpret_cast<uintptr_t>(indptr) & 15) == 0;
+    // phase 1: slab sum (kSeg int4 per thread in flight)
+    constexpr int kSeg = 4, kRound = 4 * kCoopThreads * kSeg;
+    long long s = 0;
+    for (int64_t base = lo; base < hi; base += kRound) {
+        int4 q[kSeg];
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) q[j] = load4(counts, base + 4 * (j * kCoopThreads + threadIdx.x), hi, in_al);
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) s += (long long)q[j].x + q[j].y + q[j].z + q[j].w;
+    }
+    const long long mine = block_sum(s, red);
+    if (threadIdx.x == 0) blocksums[blockIdx.x] = mine;
+    cg::this_grid().sync();
+    // phase 2: prefix of this slab
+    long long p = 0;
+    for (int k = threadIdx.x; k < (int)blockIdx.x; k += kCoopThreads) p += blocksums[k];
+    long long carry = block_sum(p, red);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const long long tot = carry + mine;
+        if (tot > 0x7fffffffLL) *ovf = 1;
+        indptr[n] = (int32_t)tot;
+        *total_out = tot;
+    }
+    // phase 3: rescan, kSeg warp-striped segments per round scanned together
+    __shared__ long long wseg[kSeg][kCoopThreads / 32];
+    bool over = false;
+    for (int64_t base = lo; base < hi; base += kRound) {
+        int4 q[kSeg];
+        long long t[kSeg], x[kSeg];
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) {
+            q[j] = load4(counts, base + 4 * (j * kCoopThreads + threadIdx.x), hi, in_al);
+            t[j] = (long long)q[j].x + q[j].y + q[j].z + q[j].w;
+            x[j] = t[j];
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int j = 0; j < kSeg; ++j) {
+                const long long y = __shfl_up_sync(0xffffffffu, x[j], off);
+                if (lane >= off) x[j] += y;
+            }
+        }
+        __syncthreads();
+        if (lane == 31) {
+#pragma unroll
+            for (int j = 0; j < kSeg; ++j) wseg[j][w] = x[j];
+        }
+        __syncthreads();
+        long long segbase = carry;
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) {
+            long long woff = 0, tot = 0;
+            for (int k = 0; k < kCoopThreads / 32; ++k) {
+                const long long z = wseg[j][k];
+                woff += k < w ? z : 0;
+                tot += z;
+            }
+            const int64_t i = base + 4 * (j * kCoopThreads + threadIdx.x);
+            const long long e0 = segbase + woff + (x[j] - t[j]), e1 = e0 + q[j].x, e2 = e1 + q[j].y, e3 = e2 + q[j].z;
+            over |= i < hi && e3 > 0x7fffffffLL;
+            if (out_al && i + 3 < hi) {
+                *reinterpret_cast<int4*>(indptr + i) = make_int4((int)e0, (int)e1, (int)e2, (int)e3);
+            } else {
+                if (i < hi) indptr[i] = (int32_t)e0;
+                if (i + 1 < hi) indptr[i + 1] = (int32_t)e1;
+                if (i + 2 < hi) indptr[i + 2] = (int32_t)e2;
+                if (i + 3 < hi) indptr[i + 3] = (int32_t)e3;
+            }
+            segbase += tot;
+        }
+        carry = segbase;
+    }
+    if (over) atomicOr(ovf, 1);
 }
 
 }  // namespace tq
 
 using namespace tq;
 
-__global__ void k_scan_finish(int32_t* indptr, int32_t nrows, const int64_t* total, int32_t* ovf) {
-    if (threadIdx.x == 0) {
-        int64_t t = *total;
-        if (t > 0x7fffffffLL) *ovf = 1;
-        indptr[nrows] = (int32_t)t;
+
+static int coop_grid() {
+    static int g[64] = {};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!g[d]) {
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_coop, kCoopThreads, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        g[d] = std::max(per_sm, 1) * std::max(sms, 1);
     }
+    return g[d];
 }
 
+extern "C" int64_t tq_scan_workspace_bytes(int32_t nrows) {
+    (void)nrows;
+    return (int64_t)(coop_grid() + 2) * (int64_t)sizeof(int64_t);
+}
+
+// `ws`: caller scratch of tq_scan_workspace_bytes(nrows) bytes.
 // nnz_h == NULL: no host read-back (stream-capture safe; the caller knows nnz)
-extern "C" int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr, int64_t* nnz_h,
-                              void* stream) {
+extern "C" int tq_scan_indptr_ws(const int32_t* counts, int32_t nrows, int32_t* indptr, void* ws_v,
+                                 int64_t* nnz_h, void* stream) {
     cudaStream_t st = S(stream);
-    int64_t ntiles = (nrows + kTile - 1) / kTile;
-    if (ntiles == 0) ntiles = 1;
-    int64_t* tiles = nullptr;
-    TQ_CUDA(cudaMallocAsync(&tiles, (ntiles + 2) * sizeof(int64_t), st));
-    int32_t* ovf = reinterpret_cast<int32_t*>(tiles + ntiles + 1);
-    TQ_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
-    CountsIn in{counts};
-    k_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, nrows, tiles); ::tq::note_launch();
-    k_scan_tiles<<<1, 1024, 0, st>>>(tiles, ntiles); ::tq::note_launch();
-    k_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, nrows, tiles, IndptrOut{indptr, ovf}); ::tq::note_launch();
-    k_scan_finish<<<1, 32, 0, st>>>(indptr, nrows, tiles + ntiles, ovf); ::tq::note_launch();
-    TQ_LAUNCH_CHECK("scan");
-    int64_t total = 0;
-    int32_t hovf = 0;
-    if (nnz_h) {
-        TQ_CUDA(cudaMemcpyAsync(&total, tiles + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        TQ_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    // workspace: [total i64][ovf i32, pad][block sums i64 x grid]
+    int64_t* ws = static_cast<int64_t*>(ws_v);
+    int32_t* ovf = reinterpret_cast<int32_t*>(ws + 1);
+    long long* blocksums = reinterpret_cast<long long*>(ws + 2);
+    TQ_CUDA(cudaMemsetAsync(ws, 0, 2 * sizeof(int64_t), st));
+    if (nrows > 0) {
+        // blocks: co-resident (cooperative launch), >= ~4096 counts each
+        const int grid = (int)std::min<int64_t>(coop_grid(), std::max<int64_t>((nrows + 4095) / 4096, 1));
+        const int32_t* a0 = counts;
+        int32_t a1 = nrows;
+        int32_t* a2 = indptr;
+        long long* a3 = blocksums;
+        int32_t* a4 = ovf;
+        int64_t* a5 = ws;
+        void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5};
+        TQ_CUDA(cudaLaunchCooperativeKernel((const void*)k_scan_coop, grid, kCoopThreads, args, 0, st));
+        ::tq::note_launch();
+    } else {
+        TQ_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int32_t), st));
     }
-    TQ_CUDA(cudaFreeAsync(tiles, st));
+    TQ_LAUNCH_CHECK("scan");
     if (nnz_h) {
+        int64_t total = 0;
+        int32_t hovf = 0;
+        TQ_CUDA(cudaMemcpyAsync(&total, ws, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         TQ_CUDA(cudaStreamSynchronize(st));
         if (hovf || total > 0x7fffffffLL) {
             set_error("nnz %lld does not fit int32 CSR indices", (long long)total);
@@ -191,6 +315,17 @@ extern "C" int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* ind
         *nnz_h = total;
     }
     return TQ_OK;
+}
+
+// as tq_scan_indptr_ws with a stream-ordered workspace of its own
+extern "C" int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr, int64_t* nnz_h,
+                              void* stream) {
+    cudaStream_t st = S(stream);
+    void* ws = nullptr;
+    TQ_CUDA(cudaMallocAsync(&ws, tq_scan_workspace_bytes(nrows), st));
+    const int rc = tq_scan_indptr_ws(counts, nrows, indptr, ws, nnz_h, stream);
+    TQ_CUDA(cudaFreeAsync(ws, st));
+    return rc;
 }
 
 extern "C" int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* col_of, int32_t* active,

@@ -4,7 +4,7 @@ rows = list(csv.reader(l for l in open(sys.argv[1]) if l.startswith('"')))
 h = rows[0]; ki = h.index("Kernel Name"); vi = h.index("Metric Value"); ui = h.index("Metric Unit")
 tot = collections.defaultdict(float); cnt = collections.Counter()
 for r in rows[1:]:
-    v = float(r[vi].replace(",", "")); v = v / 1e3 if r[ui] == "nsecond" else (v * 1e3 if r[ui] == "msecond" else v)
+    v = float(r[vi].replace(",", "")); v = {"ns": v / 1e3, "nsecond": v / 1e3, "ms": v * 1e3, "msecond": v * 1e3}.get(r[ui], v)
     name = r[ki].split("(")[0].split("<")[0]
     tot[name] += v; cnt[name] += 1
 T = sum(tot.values())

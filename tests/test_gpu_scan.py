@@ -1,0 +1,52 @@
+"""Row-pointer scan (tq_scan_indptr, single-pass decoupled look-back) against
+numpy's cumulative sum: empty and tiny inputs, every tile boundary case,
+long look-back chains, unaligned pointers, and the int32 overflow error."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def scan(counts, capture=False, offset=0):
+    from paper_2101_08053_b200 import _lib as L
+    n = counts.size
+    buf = torch.zeros(n + offset + 1, dtype=torch.int32, device="cuda")
+    buf[offset:offset + n] = torch.from_numpy(counts.astype(np.int32)).cuda()
+    out = torch.full((n + offset + 1,), -7, dtype=torch.int32, device="cuda")
+    nnz = L.i64(0)
+    L.call("tq_scan_indptr", L.ptr(buf[offset:]), n, L.ptr(out[offset:]), None if capture else L.C.byref(nnz),
+           L.stream())
+    torch.cuda.synchronize()
+    return out[offset:offset + n + 1].cpu().numpy(), int(nnz.value)
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 1023, 1024, 1025, 4096 + 7, 33 * 1024 + 1, 3_078_139])
+def test_scan_matches_cumsum(n):
+    rng = np.random.default_rng(n)
+    counts = rng.integers(0, 100, size=n)
+    got, nnz = scan(counts)
+    ref = np.concatenate([[0], np.cumsum(counts)])
+    assert np.array_equal(got, ref)
+    assert nnz == ref[-1]
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_scan_unaligned_pointers(offset):
+    counts = np.random.default_rng(offset).integers(0, 9, size=5000)
+    got, nnz = scan(counts, offset=offset)
+    assert np.array_equal(got, np.concatenate([[0], np.cumsum(counts)]))
+
+
+def test_scan_overflow_raises():
+    counts = np.full(3, 2**30, dtype=np.int64)
+    with pytest.raises(OverflowError):
+        scan(counts)
+
+
+def test_scan_repeatable_and_capture_mode():
+    counts = np.random.default_rng(5).integers(0, 200, size=200_000)
+    a, _ = scan(counts)
+    b, _ = scan(counts, capture=True)       # no host read-back: same device result
+    assert np.array_equal(a, b)
