@@ -66,9 +66,24 @@ class CutCellRule:
         self.ptr = ptr                    # (ncut+1) int64
         self.points = pts                 # (P, 2)
         self.weights = wts                # (P,)
-        self.rules = {(int(e1), int(e2)): (pts[ptr[k]:ptr[k + 1]], wts[ptr[k]:ptr[k + 1]])
-                      for k, (e1, e2) in enumerate(elements)}
-        self.subcell_counts = {(int(e1), int(e2)): int(n) for (e1, e2), n in zip(elements, ncells)}
+        self._ncells = ncells
+        self._rules = None
+        self._counts = None
+
+    @property
+    def rules(self):
+        """{(e1, e2): (points, weights)} views (built on first use)."""
+        if self._rules is None:
+            pts, wts, ptr = self.points, self.weights, self.ptr
+            self._rules = {(int(e1), int(e2)): (pts[ptr[k]:ptr[k + 1]], wts[ptr[k]:ptr[k + 1]])
+                           for k, (e1, e2) in enumerate(self.elements)}
+        return self._rules
+
+    @property
+    def subcell_counts(self):
+        if self._counts is None:
+            self._counts = {(int(e1), int(e2)): int(n) for (e1, e2), n in zip(self.elements, self._ncells)}
+        return self._counts
 
     def element_rule(self, e1, e2):
         return self.rules[(e1, e2)]
@@ -84,8 +99,15 @@ def cut_cell_rule(config, q):
     if q < 1:
         raise ValueError("Lagrange degree q must be >= 1")
     b1, b2 = config.basis2d.dir
-    e1, e2 = np.nonzero(config.element_class == 1)
-    el = np.ascontiguousarray(np.column_stack([e1, e2]).astype(np.int32))
+    # cut elements (class 1) in row-major order (found on the device when the
+    # classes live there; host-only configurations use the host array)
+    dev = getattr(config, "element_class_dev", None)
+    if dev is not None:
+        nz = torch.nonzero(dev.reshape(config.element_class.shape) == 1)
+        el = np.ascontiguousarray(nz.to(torch.int32).cpu().numpy()).reshape(-1, 2)
+    else:
+        e1, e2 = np.nonzero(config.element_class == 1)
+        el = np.ascontiguousarray(np.column_stack([e1, e2]).astype(np.int32))
     arr, keep = curve_array(config.curves)
     tabs = cell_tables(q)
     bp1 = np.ascontiguousarray(b1.breakpoints, dtype=np.float64)

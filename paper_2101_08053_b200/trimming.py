@@ -62,6 +62,7 @@ class TrimConfiguration:
         self._cut_rules = {}
         self._dwq_cache = {}
         self._active = None
+        self._active_fns = None
         self._cum_int = None
 
     @property
@@ -89,11 +90,19 @@ class TrimConfiguration:
         return list(zip(e1.tolist(), e2.tolist()))
 
     def active_functions(self):
-        """src/trimming.py:514-517 (row-major), from the device index."""
-        idx, _ = self.active_index()
-        act = idx["active"][: idx["K"]].cpu().numpy().astype(np.int64)
-        n2 = self.basis2d.shape[1]
-        return np.column_stack([act // n2, act % n2])
+        """src/trimming.py:514-517 (row-major): (K, 2) int64 (i1, i2) pairs,
+        built on the device from the active index and copied once through
+        pinned memory (cached: geometry)."""
+        if self._active_fns is None:
+            idx, _ = self.active_index()
+            act = idx["active"][: idx["K"]].long()
+            n2 = self.basis2d.shape[1]
+            pairs = torch.stack((act // n2, act % n2), dim=1)
+            h = torch.empty(pairs.shape, dtype=torch.int64, pin_memory=True)
+            h.copy_(pairs, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            self._active_fns = (h, h.numpy())
+        return self._active_fns[1]
 
     def active_index(self):
         """Device col_of (n1*n2), active list (K) -- tq_active_index."""

@@ -12,11 +12,16 @@ def run():
     cf = P.classify_elements(bb, [T.PeriodicBSplineTrim(ctrl)]); torch.cuda.synchronize(); t.append(time.perf_counter())
     cf.cut_cell_rule(4); t.append(time.perf_counter())
     f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize(); t.append(time.perf_counter())
-    h = (csr.indptr.cpu().numpy(), csr.indices.cpu().numpy(), csr.data.cpu().numpy()); t.append(time.perf_counter())
+    h = csr.to_host(); t.append(time.perf_counter())
     import scipy.sparse as sp
     M = sp.csr_matrix((h[2], h[1], h[0]), shape=(f.K, f.K)); t.append(time.perf_counter())
     act = cf.active_functions(); t.append(time.perf_counter())
     return np.diff(t)
+import cProfile, pstats
 for k in range(3):
+    d = run()
+pr = cProfile.Profile(); pr.enable(); d = run(); pr.disable()
+pstats.Stats(pr).sort_stats("cumtime").print_stats(30)
+for k in range(2):
     d = run()
     print("classify %.3f cutcells %.3f form %.3f d2h %.3f scipy %.3f active %.3f total %.3f" % (*d, d.sum()))
