@@ -95,13 +95,27 @@ class CutCellRule:
         return self.points
 
 
-def cut_cell_rule(config, q):
+_POOL = None
+
+
+def submit(fn, *args):
+    """Run ``fn(*args)`` on the module's worker thread (host geometry)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="tq-cutcells")
+    return _POOL.submit(fn, *args)
+
+
+def cut_cell_rule(config, q, host_only=False):
+    """Cut-element quadrature of the configuration (host C++).  ``host_only``:
+    find the cut elements on the host (worker threads issue no CUDA work)."""
     if q < 1:
         raise ValueError("Lagrange degree q must be >= 1")
     b1, b2 = config.basis2d.dir
     # cut elements (class 1) in row-major order (found on the device when the
     # classes live there; host-only configurations use the host array)
-    dev = getattr(config, "element_class_dev", None)
+    dev = None if host_only else getattr(config, "element_class_dev", None)
     if dev is not None:
         nz = torch.nonzero(dev.reshape(config.element_class.shape) == 1)
         el = np.ascontiguousarray(nz.to(torch.int32).cpu().numpy()).reshape(-1, 2)

@@ -421,8 +421,8 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     side stream, overlapping the deep-row flags and counts."""
     f = Formation(basis2d, config, coeff, strategy, timer, capture)
     rep = f.report
-    if config.has_cuts():     # shared geometry, outside the clock (src/assembly.py:505-508)
-        config.cut_cell_rule(max(basis2d.degrees))
+    if config.has_cuts():     # shared geometry (src/assembly.py:505-508): built on a worker
+        config.cut_cell_rule_async(max(basis2d.degrees))   # thread while the fits run
     clk = _Clock(active=capture is None)
     _stamp("start")
     if capture is not None:

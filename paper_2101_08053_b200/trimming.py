@@ -60,6 +60,7 @@ class TrimConfiguration:
         self.u_disc = (np.asarray(b1.breakpoints[1:-1][face1], dtype=float),
                        np.asarray(b2.breakpoints[1:-1][face2], dtype=float))
         self._cut_rules = {}
+        self._cut_pending = {}
         self._dwq_cache = {}
         self._active = None
         self._active_fns = None
@@ -126,11 +127,23 @@ class TrimConfiguration:
         """Cut-element quadrature, host-native C++ (src/trimming.py:588-594,1084-1111)."""
         if cache and q in self._cut_rules:
             return self._cut_rules[q]
-        from . import _classify
-        rule = _classify.cut_cell_rule(self, q)
+        pending = self._cut_pending.pop(q, None) if cache else None
+        if pending is not None:           # started by cut_cell_rule_async
+            rule = pending.result()
+        else:
+            from . import _classify
+            rule = _classify.cut_cell_rule(self, q)
         if cache:
             self._cut_rules[q] = rule
         return rule
+
+    def cut_cell_rule_async(self, q):
+        """Start building the cut-element quadrature on a worker thread (the
+        C++ decomposition runs without the GIL); ``cut_cell_rule(q)`` joins."""
+        if q in self._cut_rules or q in self._cut_pending or not self.has_cuts():
+            return
+        from . import _classify
+        self._cut_pending[q] = _classify.submit(_classify.cut_cell_rule, self, q, True)
 
     def support_split(self, i1, i2):
         a1, b1, a2, b2 = self.support_block(i1, i2)

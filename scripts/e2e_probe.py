@@ -10,12 +10,15 @@ def run():
     t = [time.perf_counter()]
     bb = P.TensorBasis2D(P.Basis1D(P.KnotVector(knots, 4)), P.Basis1D(P.KnotVector(knots, 4)))
     cf = P.classify_elements(bb, [T.PeriodicBSplineTrim(ctrl)]); torch.cuda.synchronize(); t.append(time.perf_counter())
-    cf.cut_cell_rule(4); t.append(time.perf_counter())
+    t.append(time.perf_counter())    # cut cells: built inside form (worker thread)
     f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize(); t.append(time.perf_counter())
     h = csr.to_host(); t.append(time.perf_counter())
     import scipy.sparse as sp
     M = sp.csr_matrix((h[2], h[1], h[0]), shape=(f.K, f.K)); t.append(time.perf_counter())
     act = cf.active_functions(); t.append(time.perf_counter())
+    r = f.report
+    print("  phases: weights %.1f interior %.1f cut %.1f cutel %.1f finish %.1f ms" % (
+        r.t_weights * 1e3, r.t_interior * 1e3, r.t_cut_regular * 1e3, r.t_cut_elements * 1e3, r.t_finish * 1e3))
     return np.diff(t)
 import cProfile, pstats
 for k in range(3):
