@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-nel", type=int, default=512, help="oracle sample size (mesh) for the CPU legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -320,7 +320,7 @@ def run_ours(args, rank, world, local_rank):
             if rank == 0:
                 h2d = knots.nbytes * 2 + ctrl.nbytes
                 d2h = 12 * nnz_e + 4 * (rows_e + 1)
-        et = torch.tensor([max(e_ts)], dtype=torch.float64, device=dev)
+        et = torch.tensor([sum(e_ts) / len(e_ts)], dtype=torch.float64, device=dev)   # mean step; max over ranks
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": nnz_total / float(et[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -98,12 +98,23 @@ class CutCellRule:
 _POOL = None
 
 
+def _worker_init():
+    """The worker's OpenMP team leaves two cores to the launching thread
+    (nthreads is a per-thread setting of the OpenMP runtime)."""
+    import os
+    try:
+        gomp = C.CDLL("libgomp.so.1")
+        gomp.omp_set_num_threads(max(1, len(os.sched_getaffinity(0)) - 2))
+    except OSError:
+        pass
+
+
 def submit(fn, *args):
     """Run ``fn(*args)`` on the module's worker thread (host geometry)."""
     global _POOL
     if _POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="tq-cutcells")
+        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="tq-cutcells", initializer=_worker_init)
     return _POOL.submit(fn, *args)
 
 

@@ -72,12 +72,13 @@ def active_host(f):
 
 
 def cut_rows_host(f):
-    """Active cut functions in active (row-major) order -> function ids."""
+    """Active cut functions in active (row-major) order -> function ids
+    (filtered on the device; only the cut rows come back)."""
     g = _geo(f.config)
     if "cut_fids" not in g:
-        fc = f.config.func_class.ravel()
-        act = active_host(f)
-        g["cut_fids"] = act[fc[act] == CUT].astype(np.int32)
+        act = f.active[: f.K]
+        fc = f.config.func_class_dev.reshape(-1)
+        g["cut_fids"] = act[fc[act.long()] == CUT].cpu().numpy().astype(np.int32)
     return g["cut_fids"]
 
 
@@ -506,13 +507,15 @@ def _desc_dev(f):
 
 
 def _plan_uncached(f, key_index):
-    fc = f.config.func_class.ravel()
-    act = active_host(f)
     n2 = f.b2.n
-    is_cut = fc[act] == CUT
     interior_raw = f.strategy == "reference" or not f.coeff.identity
-    rows_int = act[~is_cut] if interior_raw else np.empty(0, np.int64)
-    rows_cut = act[is_cut]
+    rows_cut = cut_rows_host(f).astype(np.int64)
+    if interior_raw:
+        fc = f.config.func_class.ravel()
+        act = active_host(f)
+        rows_int = act[fc[act] != CUT]
+    else:
+        rows_int = np.empty(0, np.int64)
     descs = []
     # interior rows
     if rows_int.size:
@@ -543,16 +546,19 @@ def _plan_uncached(f, key_index):
         else:  # dwq
             cut, routes = route_cut_rows(f)
             assert np.array_equal(cut, rows_cut)
-            for k, rt in enumerate(routes):
-                if rt[0] != 1 or rt[3] < 0:
-                    d[k, 1] = MODE_GAUSS
-                    continue
-                s = [0, 0]
-                for dd in (0, 1):
-                    if rt[1 + dd] >= 0:
-                        u = float(f.config.u_disc[dd][rt[1 + dd]])
-                        s[dd] = key_index[dd][u]
-                d[k, 1:] = [MODE_BOX, s[0], s[1], rt[3], rt[4], rt[5], rt[6]]
+            box = (routes[:, 0] == 1) & (routes[:, 3] >= 0)
+            d[~box, 1] = MODE_GAUSS
+            d[box, 1] = MODE_BOX
+            for dd in (0, 1):
+                # rule-set index per u_disc position (0: no discontinuity inside)
+                ud = f.config.u_disc[dd]
+                lut = np.array([key_index[dd].get(float(u), -1) for u in ud] + [0], np.int32)
+                iu = routes[:, 1 + dd]
+                sidx = np.where(iu >= 0, lut[np.where(iu >= 0, iu, ud.size)], 0)
+                if np.any(box & (sidx < 0)):
+                    raise KeyError("missing DWQ rule set for a boxed cut row")
+                d[box, 2 + dd] = sidx[box]
+            d[box, 4:8] = routes[box, 3:7]
         descs.append(d)
     desc = np.concatenate(descs) if descs else np.empty((0, 8), np.int32)
     return desc, int(rows_int.size)

@@ -10,7 +10,9 @@ def run():
     t = [time.perf_counter()]
     bb = P.TensorBasis2D(P.Basis1D(P.KnotVector(knots, 4)), P.Basis1D(P.KnotVector(knots, 4)))
     cf = P.classify_elements(bb, [T.PeriodicBSplineTrim(ctrl)]); torch.cuda.synchronize(); t.append(time.perf_counter())
-    t.append(time.perf_counter())    # cut cells: built inside form (worker thread)
+    if "sync" in sys.argv:
+        cf.cut_cell_rule(4)
+    t.append(time.perf_counter())    # cut cells: built inside form (worker thread) unless "sync"
     f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize(); t.append(time.perf_counter())
     h = csr.to_host(); t.append(time.perf_counter())
     import scipy.sparse as sp
@@ -20,11 +22,18 @@ def run():
     print("  phases: weights %.1f interior %.1f cut %.1f cutel %.1f finish %.1f ms" % (
         r.t_weights * 1e3, r.t_interior * 1e3, r.t_cut_regular * 1e3, r.t_cut_elements * 1e3, r.t_finish * 1e3))
     return np.diff(t)
-import cProfile, pstats
 for k in range(3):
     d = run()
-pr = cProfile.Profile(); pr.enable(); d = run(); pr.disable()
-pstats.Stats(pr).sort_stats("cumtime").print_stats(30)
-for k in range(2):
-    d = run()
+import gc
+gct = []
+_t = [0.0]
+def _cb(phase, info):
+    if phase == "start": _t[0] = time.perf_counter()
+    else: gct.append((info["generation"], time.perf_counter() - _t[0]))
+gc.callbacks.append(_cb)
+tot = []
+for k in range(6):
+    d = run(); tot.append(d.sum())
     print("classify %.3f cutcells %.3f form %.3f d2h %.3f scipy %.3f active %.3f total %.3f" % (*d, d.sum()))
+print("median total %.1f ms" % (1e3 * np.median(tot)))
+print("gc pauses (gen, ms):", [(g, round(1e3 * d, 1)) for g, d in gct if d > 1e-3])

@@ -9,7 +9,6 @@ knots = P.make_uniform_knots(2048, 4).knots.copy(); ctrl = c5["curves"][0].ctrl.
 def fresh():
     bb = P.TensorBasis2D(P.Basis1D(P.KnotVector(knots, 4)), P.Basis1D(P.KnotVector(knots, 4)))
     cf = P.classify_elements(bb, [T.PeriodicBSplineTrim(ctrl)])
-    cf.cut_cell_rule(4)
     torch.cuda.synchronize()
     return bb, cf
 for _ in range(2):
@@ -18,4 +17,5 @@ bb, cf = fresh()
 pr = cProfile.Profile(); pr.enable()
 f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+st = pstats.Stats(pr)
+st.sort_stats("cumtime").print_stats("paper_2101_08053_b200", 40)
