@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-nel", type=int, default=512, help="oracle sample size (mesh) for the CPU legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--profile-eager", action="store_true",
+                    help="ncu mode: run the captured schedule eagerly each step (ncu cannot profile launches "
+                         "made under stream capture); numbers printed in this mode are not bench values")
     return ap.parse_args()
 
 
@@ -212,7 +215,26 @@ def run_ours(args, rank, world, local_rank):
     # the timed step: one full formation pass captured as a CUDA graph
     # (GraphFormation: every kernel of the pass replays each step) plus the
     # host read-back of the moment-fit residual flags
-    gf = GraphFormation(b2d, cfg, None, args.strategy, row_range=(rb, re_))
+    if args.profile_eager:
+        class _Eager:     # same kernels and schedule as the captured pass, launched eagerly
+            def __init__(self):
+                f, csr = form(b2d, cfg, None, args.strategy, row_range=(rb, re_))
+                self.nnz, self.report = csr.nnz, f.report
+                self.cap = {"nnz": csr.nnz}
+                lib.tq_launch_count.restype = L.C.c_longlong
+                n0 = lib.tq_launch_count()
+                self.run()
+                self.launches_per_pass = int(lib.tq_launch_count() - n0)
+
+            def run(self):
+                self.f, self.csr = form(b2d, cfg, None, args.strategy, row_range=(rb, re_), capture=self.cap)
+                return self.csr
+
+            def check(self):
+                pass
+        gf = _Eager()
+    else:
+        gf = GraphFormation(b2d, cfg, None, args.strategy, row_range=(rb, re_))
     rep = gf.report
 
     def step():
@@ -255,13 +277,16 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         gather_ms = 1e3 * (time.perf_counter() - g0)
 
-    # fill kernel alone (the roofline kernel), warm, on the captured pass's buffers
-    # (captured as its own small graph so the timing is pure device time)
+    # fill kernels alone (the roofline kernels) on the captured pass's buffers
     kms = {}
     ctx = gf.f.rowctx(rb, re_)
-    fill_graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(fill_graph):
-        gf.f.fill(ctx, gf.csr.indptr, gf.csr.indices, gf.csr.data)
+    # (its two launches -- tiles, and the listed rows forked onto a second
+    # stream and joined -- timed between events on the launching stream)
+    class _FillEager:
+        def replay(self):
+            gf.f.fill(ctx, gf.csr.indptr, gf.csr.indices, gf.csr.data)
+    fill_graph = _FillEager()
+    fill_graph.replay()
     fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(21)]
     for s_, e_ in fe:
         flush.fill_(1.0)
@@ -347,7 +372,8 @@ def run_ours(args, rank, world, local_rank):
         "eager_phases_ms": {"weights": 1e3 * rep.t_weights, "interior": 1e3 * rep.t_interior,
                             "cut_regular": 1e3 * rep.t_cut_regular, "cut_elements": 1e3 * rep.t_cut_elements,
                             "finish": 1e3 * rep.t_finish},
-        "step": "CUDA-graph replay of one full formation pass + residual-flag read-back",
+        "step": ("eager run of the captured schedule (--profile-eager: ncu mode, not a bench value)"
+                 if args.profile_eager else "CUDA-graph replay of one full formation pass + residual-flag read-back"),
         "kernels_ms_per_step": {k: v / args.steps for k, v in kms.items()},
         "roofline": {"kernel": "fill: k_fill_tiles with k_fill_irregular concurrent (fused symmetrise + zero-drop + CSR write)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
