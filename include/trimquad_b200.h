@@ -350,6 +350,26 @@ int tq_target_points(tq_target f, const double* P, const double* w, int64_t n, d
 int tq_l2_parts(tq_projctx c, const double* C, int64_t e_begin, int64_t e_end, int64_t p_begin,
                 int64_t p_end, const double* fpts, double* num_den, void* stream);
 
+/* ---- subsystem (6): SPD solve of the projection (device CSR) ------------ */
+
+/* diag[i] = A_ii of a CSR with sorted columns (A.diagonal(),
+ * src/projection.py:159) */
+int tq_csr_diag(const int32_t* indptr, const int32_t* indices, const double* data, int32_t n,
+                double* diag, void* stream);
+/* y = diag(sl) A diag(sr) x; sl / sr may be NULL (identity).  As @ y and
+ * A @ x of src/projection.py:196-201 */
+int tq_spmv(const int32_t* indptr, const int32_t* indices, const double* data, int32_t n,
+            const double* sl, const double* sr, const double* x, double* y, void* stream);
+/* conjugate gradients on As = diag(s) A diag(s) from x0 = 0, scipy's cg
+ * iteration (src/projection.py:180-186: rtol, atol = 0, maxiter): one
+ * cooperative kernel.  `work`: tq_cg_workspace_bytes(n) bytes.  iters_dev
+ * receives the iterations run (== maxiter: not converged), rnorm_dev the
+ * final ||r|| (device scalars, no host sync). */
+int64_t tq_cg_workspace_bytes(int32_t n);
+int tq_cg_scaled(const int32_t* indptr, const int32_t* indices, const double* data, int32_t n,
+                 const double* s, const double* b, double* x, double rtol, int32_t maxiter,
+                 void* work, int32_t* iters_dev, double* rnorm_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

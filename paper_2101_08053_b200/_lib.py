@@ -100,6 +100,10 @@ def lib():
         "tq_deep_flags": ([RowCtx, vp, vp, i32, vp, vp], i32),
         "tq_deep_geometry": ([RowCtx, vp, vp, i32, vp, vp], i32),
         "tq_deep_apply": ([RowCtx, vp, vp, vp], i32),
+        "tq_csr_diag": ([vp, vp, vp, i32, vp, vp], i32),
+        "tq_spmv": ([vp, vp, vp, i32, vp, vp, vp, vp, vp], i32),
+        "tq_cg_workspace_bytes": ([i32], i64),
+        "tq_cg_scaled": ([vp, vp, vp, i32, vp, vp, vp, C.c_double, i32, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -242,34 +242,33 @@ def l2_error(coeffs, problem: ProjectionProblem, active=None) -> float:
 
 
 def solve_spd(M, b, guard=CONDITION_GUARD, stats=None):
-    """Jacobi-scaled dense Cholesky (n <= 6000) or CG to 1e-13
-    (src/projection.py:148-211), host-side as in the reference."""
+    """Solve the SPD mass system to relative residual 1e-13 (src/projection.py:148-211).
+
+    Jacobi scaling As = S A S, then dense Cholesky with a condition estimate
+    for n <= DIRECT_LIMIT (host scipy, as in the reference), else conjugate
+    gradients on the device CSR (``tq_cg_scaled``: the reference's scipy cg
+    iteration as one cooperative kernel), with the same fallback solve,
+    iterative refinement and final residual check."""
     A = M.data if isinstance(M, SparseMatrix) else sp.csr_matrix(M)
     b = np.asarray(b, dtype=float)
     n = A.shape[0]
+    if n > DIRECT_LIMIT:
+        return _solve_spd_device(M, A, b, guard, stats)
     d = A.diagonal()
     if np.any(d <= 0.0):
         raise ValueError("matrix is not positive definite (non-positive diagonal)")
     s = 1.0 / np.sqrt(d)
     As = sp.diags(s) @ A @ sp.diags(s)
     bs = s * b
-    cond = math.nan
-    if n <= DIRECT_LIMIT:
-        D = As.toarray()
-        D = 0.5 * (D + D.T)
-        try:
-            cho = scipy.linalg.cho_factor(D, lower=True, check_finite=False)
-        except scipy.linalg.LinAlgError as err:
-            raise ValueError("matrix is not positive definite") from err
-        solve = lambda r: scipy.linalg.cho_solve(cho, r, check_finite=False)
-        op = spla.LinearOperator((n, n), matvec=solve, rmatvec=solve)
-        cond = float(spla.onenormest(op) * spla.onenormest(As))
-    else:
-        def solve(r):
-            x, info = spla.cg(As, r, rtol=1e-14, atol=0.0, maxiter=10 * n)
-            if info > 0:
-                x = x + spla.cg(As, r - As @ x, rtol=1e-10, atol=0.0, maxiter=n)[0]
-            return x
+    D = As.toarray()
+    D = 0.5 * (D + D.T)
+    try:
+        cho = scipy.linalg.cho_factor(D, lower=True, check_finite=False)
+    except scipy.linalg.LinAlgError as err:
+        raise ValueError("matrix is not positive definite") from err
+    solve = lambda r: scipy.linalg.cho_solve(cho, r, check_finite=False)
+    op = spla.LinearOperator((n, n), matvec=solve, rmatvec=solve)
+    cond = float(spla.onenormest(op) * spla.onenormest(As))
     y = solve(bs)
     bn = np.linalg.norm(bs) or 1.0
     for _ in range(4):
@@ -279,15 +278,89 @@ def solve_spd(M, b, guard=CONDITION_GUARD, stats=None):
         y = y + solve(r)
     x = s * y
     resid = np.linalg.norm(A @ x - b) / (np.linalg.norm(b) or 1.0)
+    return _finish_solve(x, resid, cond, guard, stats)
+
+
+def _finish_solve(x, resid, cond, guard, stats, extra=None):
     if stats is not None:
         stats["condition"] = cond
         stats["residual"] = resid
+        stats.update(extra or {})
     if np.isfinite(cond) and cond > guard:
         warnings.warn(f"scaled mass matrix condition estimate {cond:.2e} exceeds guard {guard:.0e}",
-                      RuntimeWarning, stacklevel=2)
+                      RuntimeWarning, stacklevel=3)
     if resid > 1e-13:
         raise RuntimeError(f"solver residual {resid:.2e} above 1e-13")
     return x
+
+
+class _DeviceSystem:
+    """The CSR operator on the device (formed there, or uploaded once) with
+    its Jacobi scaling and CG workspace."""
+
+    def __init__(self, M, A):
+        dev = L.device()
+        csr = M.device if isinstance(M, SparseMatrix) else None
+        if csr is not None and getattr(csr, "row_begin", 0) == 0 and csr.indptr.numel() == A.shape[0] + 1:
+            self.indptr, self.indices, self.data = csr.indptr, csr.indices, csr.data
+        else:     # host matrix: one upload
+            self.indptr = L.dev(A.indptr.astype(np.int32), torch.int32)
+            self.indices = L.dev(A.indices.astype(np.int32), torch.int32)
+            self.data = L.dev(A.data.astype(np.float64), torch.float64)
+        self.n = n = A.shape[0]
+        self.diag = torch.empty(n, dtype=torch.float64, device=dev)
+        L.call("tq_csr_diag", L.ptr(self.indptr), L.ptr(self.indices), L.ptr(self.data), n, L.ptr(self.diag),
+               L.stream())
+        self.work = torch.empty(int(L.lib().tq_cg_workspace_bytes(n)) // 8 + 1, dtype=torch.float64, device=dev)
+        self.iters = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.rnorm = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def spmv(self, x, sl=None, sr=None):
+        y = torch.empty_like(x)
+        L.call("tq_spmv", L.ptr(self.indptr), L.ptr(self.indices), L.ptr(self.data), self.n, L.ptr(sl), L.ptr(sr),
+               L.ptr(x), L.ptr(y), L.stream())
+        return y
+
+    def cg(self, s, rhs, rtol, maxiter):
+        x = torch.empty_like(rhs)
+        L.call("tq_cg_scaled", L.ptr(self.indptr), L.ptr(self.indices), L.ptr(self.data), self.n, L.ptr(s),
+               L.ptr(rhs), L.ptr(x), float(rtol), int(maxiter), L.ptr(self.work), L.ptr(self.iters),
+               L.ptr(self.rnorm), L.stream())
+        return x, int(self.iters.item())
+
+
+def _solve_spd_device(M, A, b, guard, stats):
+    """CG branch of src/projection.py:179-201 on the device."""
+    S = _DeviceSystem(M, A)
+    n = S.n
+    d = S.diag
+    if bool((d <= 0.0).any().item()):
+        raise ValueError("matrix is not positive definite (non-positive diagonal)")
+    s = torch.rsqrt(d)
+    bd = L.dev(b, torch.float64)
+    bs = s * bd
+    its = []
+
+    def solve(r):
+        x, it = S.cg(s, r, 1e-14, 10 * n)
+        its.append(it)
+        if it >= 10 * n:         # scipy info > 0: one more solve on the residual
+            x2, it2 = S.cg(s, r - S.spmv(x, s, s), 1e-10, n)
+            its.append(it2)
+            x = x + x2
+        return x
+
+    y = solve(bs)
+    bn = float(torch.linalg.vector_norm(bs)) or 1.0
+    for _ in range(4):
+        r = bs - S.spmv(y, s, s)
+        if float(torch.linalg.vector_norm(r)) <= 1e-14 * bn:
+            break
+        y = y + solve(r)
+    xd = s * y
+    resid = float(torch.linalg.vector_norm(S.spmv(xd) - bd)) / (float(torch.linalg.vector_norm(bd)) or 1.0)
+    x = xd.cpu().numpy()
+    return _finish_solve(x, resid, math.nan, guard, stats, {"cg_iterations": its, "device": True})
 
 
 def project(problem: ProjectionProblem, parallel=False, stats=None):
