@@ -17,6 +17,6 @@ from .assembly import (STRATEGIES, CoefficientField, FormationReport, SparseMatr
                        form_with_timings, sum_factor_op_count)
 
 from .projection import (ConditioningError, ProjectionProblem, SeparableTarget, assemble_rhs, default_target,
-                         l2_error, project, solve_spd)
+                         l2_error, project, solve_spd, run_convergence_study, ConvergenceRecord)
 
 __version__ = "0.1.0"

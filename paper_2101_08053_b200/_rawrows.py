@@ -496,6 +496,39 @@ def _plan(f):
     return g[key]
 
 
+def gauss_element_count(f):
+    """Distinct interior elements whose element-Gauss block the strategy
+    computes (FormationReport.n_gauss_elements; src/assembly.py:310-332):
+    the supports of GAUSS rows and the residual (outside-box) supports of
+    BOX rows, interior elements only.  Geometry of the row plan, cached."""
+    desc, _ = _plan(f)
+    g = _geo(f.config)
+    key = ("ngauss", id(desc))
+    if key not in g:
+        sel = desc[(desc[:, 1] == MODE_GAUSS) | (desc[:, 1] == MODE_BOX)]
+        b1, b2 = f.b1, f.b2
+        ec = f.config.element_class
+        mark = np.zeros(ec.shape, bool)
+        if sel.shape[0]:
+            i1, i2 = sel[:, 0] // b2.n, sel[:, 0] % b2.n
+            o1 = np.arange(b1.p + 1)
+            o2 = np.arange(b2.p + 1)
+            e1 = b1._el_first[i1][:, None, None] + o1[None, :, None]
+            e2 = b2._el_first[i2][:, None, None] + o2[None, None, :]
+            e1, e2 = np.broadcast_arrays(e1, e2)
+            ok = (e1 <= b1._el_last[i1][:, None, None]) & (e2 <= b2._el_last[i2][:, None, None])
+            e1c = np.minimum(e1, ec.shape[0] - 1)
+            e2c = np.minimum(e2, ec.shape[1] - 1)
+            ok &= ec[e1c, e2c] == INTERIOR
+            box = (sel[:, 1] == MODE_BOX) & (sel[:, 4] >= 0)
+            inbox = (box[:, None, None] & (e1 >= sel[:, 4, None, None]) & (e1 <= sel[:, 5, None, None])
+                     & (e2 >= sel[:, 6, None, None]) & (e2 <= sel[:, 7, None, None]))
+            ok &= ~inbox
+            mark[e1c[ok], e2c[ok]] = True
+        g[key] = int(mark.sum())
+    return g[key]
+
+
 def _desc_dev(f):
     """Device copy of the row plan's descriptors (cached) and its size."""
     desc, _ = _plan(f)
@@ -572,6 +605,7 @@ def run_phase(f, phase):
         desc, nint = _plan(f)
         f._nint = nint
         f._ndesc = desc.shape[0]
+        f.report.n_gauss_elements = gauss_element_count(f)
         g = _geo(f.config)
         f._desc, _ = _desc_dev(f)
         if getattr(f, "_raw_pre", None) is not None and f._desc is not f._desc_pre:

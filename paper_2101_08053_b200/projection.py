@@ -375,3 +375,49 @@ def project(problem: ProjectionProblem, parallel=False, stats=None):
     if np.isfinite(cond) and cond > CONDITION_GUARD:
         raise ConditioningError(f"condition estimate {cond:.2e} above guard {CONDITION_GUARD:.0e}")
     return x, M, b
+
+
+@dataclass
+class ConvergenceRecord:
+    """One projection error of a convergence study (src/projection.py:71-80)."""
+    case: str
+    strategy: str
+    degree: int
+    mesh: int
+    h: float
+    dofs: int
+    l2_rel: float
+    rate: float        # against the previous mesh of the same (strategy, degree); nan first
+
+
+def run_convergence_study(case, strategies, degrees, meshes, target=None, parallel=False):
+    """Projection errors over a mesh sequence (src/projection.py:288-333).
+
+    For each (degree, mesh) the load vector is assembled once (GPU) and
+    shared by the strategies; each strategy forms its mass matrix (GPU),
+    solves (device CG above DIRECT_LIMIT) and measures the relative L2
+    error (GPU).  rate = log(e_prev / e) / log(n / n_prev)."""
+    from .cases import TrimCase, build_space, make_case
+    case = case if isinstance(case, TrimCase) else make_case(case)
+    target = target or default_target
+    out, last = [], {}
+    for p in degrees:
+        for nel in meshes:
+            basis2d, config = build_space(case, nel, p)
+            problem = ProjectionProblem(target, basis2d, config)
+            b = assemble_rhs(problem)
+            for strategy in strategies:
+                M = assemble_mass(basis2d, config, strategy=strategy, parallel=parallel)
+                st = {}
+                x = solve_spd(M, b, stats=st)
+                cond = st.get("condition", math.nan)
+                if np.isfinite(cond) and cond > CONDITION_GUARD:
+                    raise ConditioningError(f"{case.name} p={p} n={nel} {strategy}: condition {cond:.2e} "
+                                            f"above guard {CONDITION_GUARD:.0e}")
+                err = l2_error(x, problem, active=M.active)
+                prev = last.get((strategy, p))
+                rate = math.log(prev[1] / err) / math.log(nel / prev[0]) if prev else math.nan
+                last[(strategy, p)] = (nel, err)
+                out.append(ConvergenceRecord(case.name, strategy, p, nel, 1.0 / nel, int(M.shape[0]), err, rate))
+    return out
+
