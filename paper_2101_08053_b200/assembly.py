@@ -20,6 +20,8 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
+import contextlib
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -312,13 +314,19 @@ class Formation:
         """Direction-wise WQ contractions a_d (c == 1)."""
         if not self.separable():
             return
+        from ._rawrows import _forked, _keep_on, _named_stream
+        main = torch.cuda.current_stream()
+        side = _named_stream("products", priority=-2)
         out = []
-        for b, r in zip((self.b1, self.b2), self.rules[:2]):
+        for d, (b, r) in enumerate(zip((self.b1, self.b2), self.rules[:2])):
             first, vals = r.basis_table()
             a = torch.empty((b.n, 2 * b.p + 1), dtype=torch.float64, device=self.dev)
-            L.call("tq_wq_products", b.device(), r.layout.device(), L.ptr(first), L.ptr(vals), r.device(),
-                   L.ptr(a), L.stream())
+            with _forked(main, side) if d == 1 else contextlib.nullcontext():   # the two directions overlap
+                L.call("tq_wq_products", b.device(), r.layout.device(), L.ptr(first), L.ptr(vals), r.device(),
+                       L.ptr(a), L.stream())
             out.append(a)
+        main.wait_stream(side)
+        _keep_on(main, out[1:])
         self.a1, self.a2 = out
 
     def raw_rows(self, phase):

@@ -84,12 +84,13 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
-    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * c.nmax1 + W1 + W2;
+    const int ni = c.nmax1 > c.p1 + 1 ? c.nmax1 : c.p1 + 1;    // inner rows (sum factorization / Gauss stage 1)
+    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * ni + W1 + W2;
     double* blk = sm + (size_t)wib * per;
     double* B1 = blk + T;
     double* B2 = B1 + c.nmax1 * W1;
     double* inner = B2 + c.nmax2 * W2;
-    double* S1 = inner + W2 * c.nmax1;
+    double* S1 = inner + W2 * ni;
     double* S2 = S1 + W1;
     const int q1 = c.p1 + 1, q2 = c.p2 + 1;
 
@@ -105,7 +106,48 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
         }
         __syncwarp();
         // -- element Gauss over interior support elements (GAUSS, BOX residual)
-        if ((PARTS & 1) && (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX)) {
+        if ((PARTS & 1) && (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX) && !c.cg) {
+            // c == 1: every element block is em1 (x) em2, so the row's block
+            // is a two-stage contraction over its (p1+1) x (p2+1) element grid:
+            //   inner[k1][o2] = sum_e2 [interior, outside box] em2[e2][a2][b2(o2)]
+            //   blk[o1][o2]   = sum_k1 em1[e1][a1][b1(o1)] inner[k1][o2]
+            // (dependency chains of <= p+1 terms instead of a warp-serial
+            // loop over the elements; same terms, grouped by e1)
+            const int ef1 = c.el_first1[i1], ne1 = c.el_last1[i1] - ef1 + 1;
+            const int ef2 = c.el_first2[i2], el2 = c.el_last2[i2];
+            const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
+            const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+            for (int t = lane; t < ne1 * W2; t += 32) {
+                const int k1 = t / W2, o2 = t - (t / W2) * W2;
+                const int e1 = ef1 + k1, j2 = i2 - c.p2 + o2;
+                double acc = 0.0;
+                if (j2 >= 0 && j2 < c.n2) {
+                    for (int e2 = ef2; e2 <= el2; ++e2) {
+                        if (c.elem_class[(int64_t)e1 * c.nel2 + e2] != TQ_INTERIOR) continue;
+                        if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) continue;
+                        const int f2 = c.espan2[e2] - c.p2, b2 = j2 - f2;
+                        if (b2 < 0 || b2 > c.p2) continue;
+                        acc += c.em2[((int64_t)e2 * q2 + (i2 - f2)) * q2 + b2];
+                    }
+                }
+                inner[t] = acc;
+            }
+            __syncwarp();
+            for (int q = lane; q < T; q += 32) {
+                const int o1 = q / W2, o2 = q - (q / W2) * W2;
+                const int j1 = i1 - c.p1 + o1;
+                double acc = 0.0;
+                if (j1 >= 0 && j1 < c.n1) {
+                    for (int k1 = 0; k1 < ne1; ++k1) {
+                        const int e1 = ef1 + k1, f1 = c.espan1[e1] - c.p1, b1 = j1 - f1;
+                        if (b1 < 0 || b1 > c.p1) continue;
+                        acc += c.em1[((int64_t)e1 * q1 + (i1 - f1)) * q1 + b1] * inner[k1 * W2 + o2];
+                    }
+                }
+                blk[q] += acc;
+            }
+            __syncwarp();
+        } else if ((PARTS & 1) && (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX)) {
             for (int e1 = c.el_first1[i1]; e1 <= c.el_last1[i1]; ++e1) {
                 for (int e2 = c.el_first2[i2]; e2 <= c.el_last2[i2]; ++e2) {
                     if (c.elem_class[(int64_t)e1 * c.nel2 + e2] != TQ_INTERIOR) continue;
@@ -342,7 +384,8 @@ using namespace tq;
 
 static size_t regular_smem_per_warp(const tq_rawctx& c) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
-    return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * c.nmax1 + W1 + W2);
+    const int ni = std::max(c.nmax1, c.p1 + 1);
+    return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * ni + W1 + W2);
 }
 
 template <int PARTS>

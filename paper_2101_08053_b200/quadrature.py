@@ -258,15 +258,23 @@ class _FitPlan:
         self.rows = L.dev(self.rows_h, torch.int32)
 
 
-def _solve_rows_async_t(plan: _FitPlan):
+def _solve_rows_async_t(plan: _FitPlan, init=None):
     """Launch the GPU moment fits of a plan (src/quadrature.py:281-303).
     Returns ((wptr, k0, w, fail), (first, vals) basis table at the layout
-    points or None) as device tensors; no host sync."""
+    points or None) as device tensors; no host sync.  The solve writes k0,
+    the weights and the fail flag of every plan row; rows outside the plan
+    are initialised (k0 = -1, w = 0) only when ``init`` (default: the plan
+    leaves rows out), so a full plan launches no fill kernels."""
     basis, layout = plan.basis, plan.layout
     dev = L.device()
-    k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
-    w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
-    fail = torch.zeros(max(plan.rows_h.size, 1), dtype=torch.int32, device=dev)
+    init = plan.rows_h.size < basis.n if init is None else init
+    if init:
+        k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
+        w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+    else:
+        k0 = torch.empty((basis.n,), dtype=torch.int32, device=dev)
+        w = torch.empty(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+    fail = (torch.empty if plan.rows_h.size else torch.zeros)(max(plan.rows_h.size, 1), dtype=torch.int32, device=dev)
     tab = None
     if plan.rows_h.size:
         tab = basis.eval_device(layout.device_points(), check=False)
@@ -278,9 +286,9 @@ def _solve_rows_async_t(plan: _FitPlan):
     return (plan.wptr, k0, w, fail), tab
 
 
-def _solve_rows_async(plan: _FitPlan):
+def _solve_rows_async(plan: _FitPlan, init=None):
     """(wptr, k0, w, fail) of ``_solve_rows_async_t``."""
-    return _solve_rows_async_t(plan)[0]
+    return _solve_rows_async_t(plan, init)[0]
 
 
 def _failing(plan, fail):
@@ -421,8 +429,10 @@ class DwqPlan:
 def dwq_solve_async(plan: DwqPlan, direction=None, regular_side=None):
     """Numeric part of DWQ on the GPU: refined fits, then w = S^T w~
     (src/quadrature.py:420-444).  Returns (rule set, fail tensor)."""
-    fwptr, fk0, fw, fail = _solve_rows_async(plan.fit)
-    w = torch.zeros(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=L.device())
+    # refined fits: read only by the combine, and only on their own rows
+    fwptr, fk0, fw, fail = _solve_rows_async(plan.fit, init=False)
+    # the combine writes every wanted row; other rows have empty ranges
+    w = torch.empty(max(int(plan.wptr_h[-1]), 1), dtype=torch.float64, device=L.device())
     L.call("tq_dwq_combine", L.ptr(plan.rows), plan.wanted.size, L.ptr(plan.cp), L.ptr(plan.ri), L.ptr(plan.sv),
            L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(plan.wptr), L.ptr(plan.k0), L.ptr(w)),
            L.stream())
