@@ -295,6 +295,14 @@ def run_ours(args, rank, world, local_rank):
         e_.record()
     torch.cuda.synchronize()
     kms["fill"] = float(np.median([s_.elapsed_time(e_) for s_, e_ in fe[1:]])) * args.steps
+    # the tiles kernel alone (diagnostic: the listed rows excluded)
+    for s_, e_ in fe:
+        flush.fill_(1.0)
+        s_.record()
+        L.call("tq_fill_fast", ctx, L.ptr(gf.csr.indptr), L.ptr(gf.csr.indices), L.ptr(gf.csr.data), L.stream())
+        e_.record()
+    torch.cuda.synchronize()
+    kms["fill_tiles_only"] = float(np.median([s_.elapsed_time(e_) for s_, e_ in fe[1:]])) * args.steps
     t = torch.tensor([total_ms, float(nnz_local), kms.get("fill", 0.0), float(re_ - rb)], dtype=torch.float64,
                      device=dev)
     if world > 1:

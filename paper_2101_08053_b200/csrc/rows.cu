@@ -161,6 +161,9 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 //    trimming curve; row-parallel processing keeps them off the critical path).
 // ---------------------------------------------------------------------------
 constexpr int kWarpRows = 32;
+#ifndef TQ_FILL_STAGES
+#define TQ_FILL_STAGES 2
+#endif
 
 template <int P>
 constexpr int fill_chunk() {   // rows per bulk copy: ~7.8 KB of staged entries (measured best at P = 4)
@@ -175,9 +178,12 @@ struct alignas(16) FillStage {
 };
 
 template <int P>
+constexpr int fill_stages() { return TQ_FILL_STAGES; }
+
+template <int P>
 struct alignas(16) RegularSlice {
     static constexpr int W = 2 * P + 1;
-    FillStage<P> stage[2];
+    FillStage<P> stage[fill_stages<P>()];
     double band[(32 + 2 * P) * W];
 };
 
@@ -190,6 +196,8 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigne
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -220,8 +228,9 @@ __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S,
     for (int k = 0; k * CH < L; ++k) {
         const int rows = min(CH, L - k * CH);
         const int n = rows * WW;
-        FillStage<P>& st = S.stage[nbulk & 1];
-        if (lane == 0 && nbulk >= 2) bulk_wait_read1();   // last reader of this buffer is done
+        constexpr int NS = fill_stages<P>();
+        FillStage<P>& st = S.stage[nbulk % NS];
+        if (lane == 0 && nbulk >= NS) bulk_wait_read<NS - 1>();   // last reader of this buffer is done
         __syncwarp();
         const int pos = pos0 + k * CH * WW;
         const int offd = pos & 1, offx = pos & 3;

@@ -46,9 +46,10 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
                            double* __restrict__ wout, int32_t* __restrict__ fail, int32_t* err) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    const int per = tmax * mmax + tmax + 2 * mmax;  // A, b, w + perm(as double slots)
+    const int per = 2 * tmax * mmax + tmax + 2 * mmax;  // A, A0, b, w + perm (as double slots)
     double* A = smem + (size_t)wib * per;           // column-major, ld = t
-    double* b = A + tmax * mmax;
+    double* A0 = A + tmax * mmax;                   // untouched copy for the residual check
+    double* b = A0 + tmax * mmax;
     double* w = b + tmax;
     int* perm = reinterpret_cast<int*>(w + mmax);
     const int p = s.p, W = 2 * p + 1;
@@ -66,7 +67,9 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
         // load A (t x m) and b
         for (int q = lane; q < t * m; q += 32) {
             int c = q / t, rr = q % t;
-            A[c * t + rr] = colloc(first, vals, p, k0 + c, j0 + rr);
+            const double a = colloc(first, vals, p, k0 + c, j0 + rr);
+            A[c * t + rr] = a;
+            A0[c * t + rr] = a;
         }
         for (int rr = lane; rr < t; rr += 32) b[rr] = mom[(int64_t)i * W + (j0 + rr - i + p)];
         for (int c = lane; c < m; c += 32) perm[c] = c;
@@ -146,7 +149,7 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
         double rmax = 0.0, bmax = 0.0;
         for (int rr = lane; rr < t; rr += 32) {
             double acc = 0.0;
-            for (int c = 0; c < m; ++c) acc += colloc(first, vals, p, k0 + c, j0 + rr) * w[c];
+            for (int c = 0; c < m; ++c) acc += A0[c * t + rr] * w[c];
             double bb = mom[(int64_t)i * W + (j0 + rr - i + p)];
             rmax = fmax(rmax, fabs(acc - bb));
             bmax = fmax(bmax, fabs(bb));
@@ -193,7 +196,7 @@ extern "C" int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, co
     if (nrows == 0) return TQ_OK;
     if (tmax > 2 * kMaxP + 1) { set_error("too many trials per system (%d)", tmax); return TQ_EINVAL; }
     const int wpb = 4;
-    size_t per = (size_t)tmax * mmax + tmax + 2 * mmax;
+    size_t per = 2 * (size_t)tmax * mmax + tmax + 2 * mmax;
     size_t shm = per * sizeof(double) * wpb;
     if (shm > 200 * 1024) { set_error("moment system too large (t=%d, m=%d)", tmax, mmax); return TQ_EINVAL; }
     TQ_CUDA(cudaFuncSetAttribute(k_wq_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
