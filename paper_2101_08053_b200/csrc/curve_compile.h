@@ -30,6 +30,22 @@ inline bool compile_curves(const tq_curve* in, int n, std::vector<CurveC>& out, 
             case TQ_CURVE_CLOSED_CIRCLE:
                 for (int k = 0; k < 6; ++k) c.prm[k] = d.data[k];
                 break;
+            case TQ_CURVE_BEZIER: {
+                // power basis in numpy's operation order (oracle BezierTrim.pw)
+                c.o_pw = (int)buf.size();
+                buf.resize(buf.size() + 14);
+                const double* P = d.data;
+                for (int ax = 0; ax < 2; ++ax) {
+                    const double c0 = P[ax], c1 = P[2 + ax], c2 = P[4 + ax], c3 = P[6 + ax];
+                    double* q = buf.data() + c.o_pw + 4 * ax;
+                    q[0] = ((-c0 + 3.0 * c1) - 3.0 * c2) + c3;
+                    q[1] = (3.0 * c0 - 6.0 * c1) + 3.0 * c2;
+                    q[2] = -3.0 * c0 + 3.0 * c1;
+                    q[3] = c0;
+                }
+                for (int k = 0; k < 6; ++k) buf[c.o_pw + 8 + k] = d.data[8 + k];
+                break;
+            }
             case TQ_CURVE_BSPLINE: {
                 const int m = d.m;
                 c.m = m;

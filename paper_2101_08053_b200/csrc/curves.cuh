@@ -152,6 +152,203 @@ TQ_HD inline double bs_signed_distance(const CurveC& c, double x0, double y0) {
     return valid ? dist : -dist;
 }
 
+// ---------------------------------------------------------------- cubic Bezier
+// (src/trimming.py:204-351; oracle/trim.py BezierTrim).  buf at o_pw: the
+// power-basis coefficients per axis {a b c d}_x {a b c d}_y, then the three
+// ray-casting anchors (x, y).
+
+// numpy's a t**3 + b t**2 + c t + d, left to right
+TQ_HD inline double bz_axis(const double* q, double t) {
+    const double t2 = t * t;
+    return ((q[0] * (t2 * t) + q[1] * t2) + q[2] * t) + q[3];
+}
+TQ_HD inline double bz_daxis(const double* q, double t) {
+    return ((3.0 * q[0]) * (t * t) + (2.0 * q[1]) * t) + q[2];
+}
+TQ_HD inline void bz_eval(const CurveC& c, double t, double& x, double& y) {
+    const double* q = c.buf + c.o_pw;
+    x = bz_axis(q, t);
+    y = bz_axis(q + 4, t);
+}
+TQ_HD inline void bz_deriv(const CurveC& c, double t, double& dx, double& dy) {
+    const double* q = c.buf + c.o_pw;
+    dx = bz_daxis(q, t);
+    dy = bz_daxis(q + 4, t);
+}
+
+// value and derivative of the monic-normalised polynomial c[0..deg]
+TQ_HD inline void poly_eval(const double* c, int deg, double x, double& f, double& df) {
+    f = c[0];
+    df = 0.0;
+    for (int k = 1; k <= deg; ++k) {
+        df = df * x + f;
+        f = f * x + c[k];
+    }
+}
+
+// Real roots of a dense polynomial, highest coefficient first, with the
+// semantics of src/trimming.py:354-368 (scale by max |c|, drop leading
+// coefficients below 1e-14, keep roots whose imaginary part is < 1e-9, as
+// their real part).  Closed forms, each real root polished by Newton
+// steps on the scaled polynomial.  Returns the count (ascending).
+TQ_HD inline int real_roots(const double* coef, int ncoef, double* out) {
+    double scale = 0.0;
+    for (int k = 0; k < ncoef; ++k) scale = fmax(scale, fabs(coef[k]));
+    if (scale == 0.0) return 0;
+    double c[4];
+    int first = -1;
+    for (int k = 0; k < ncoef; ++k) {
+        const double v = coef[k] / scale;
+        if (first < 0 && fabs(v) > 1e-14) first = k;
+        if (first >= 0) c[k - first] = v;
+    }
+    if (first < 0) return 0;
+    const int deg = ncoef - 1 - first;
+    if (deg < 1) return 0;
+    int n = 0;
+    if (deg == 1) {
+        out[n++] = -c[1] / c[0];
+    } else if (deg == 2) {
+        const double a = c[0], b = c[1], cc = c[2];
+        const double disc = b * b - 4.0 * a * cc;
+        if (disc >= 0.0) {
+            const double sq = sqrt(disc);
+            const double qq = -0.5 * (b + (b >= 0.0 ? sq : -sq));
+            double r1 = qq / a, r2 = qq != 0.0 ? cc / qq : -b / a - r1;
+            out[n++] = r1;
+            out[n++] = r2;
+        } else if (sqrt(-disc) / (2.0 * fabs(a)) < 1e-9) {
+            out[n++] = -b / (2.0 * a);
+            out[n++] = -b / (2.0 * a);
+        }
+    } else {
+        const double B = c[1] / c[0], C = c[2] / c[0], D = c[3] / c[0];
+        const double p = C - B * B / 3.0, q = (2.0 * B * B * B) / 27.0 - (B * C) / 3.0 + D;
+        const double delta = (q * q) / 4.0 + (p * p * p) / 27.0;
+        if (delta > 0.0) {            // one real root and a complex pair
+            const double sq = sqrt(delta);
+            const double u = cbrt(-0.5 * q + sq), v = cbrt(-0.5 * q - sq);
+            const double t = u + v;
+            out[n++] = t - B / 3.0;
+            if (fabs(u - v) * 0.8660254037844386 < 1e-9) {
+                out[n++] = -0.5 * t - B / 3.0;
+                out[n++] = -0.5 * t - B / 3.0;
+            }
+        } else if (p == 0.0) {        // triple root
+            out[n++] = -B / 3.0;
+            out[n++] = -B / 3.0;
+            out[n++] = -B / 3.0;
+        } else {                      // three real roots (trigonometric form)
+            const double r = 2.0 * sqrt(-p / 3.0);
+            double arg = (3.0 * q) / (p * r);
+            arg = arg < -1.0 ? -1.0 : (arg > 1.0 ? 1.0 : arg);
+            const double phi = acos(arg) / 3.0;
+            for (int k = 0; k < 3; ++k) out[n++] = r * cos(phi - 2.0943951023931957 * k) - B / 3.0;
+        }
+    }
+    // Newton polish on the scaled polynomial (bounded steps)
+    for (int k = 0; k < n; ++k) {
+        double x = out[k];
+        for (int it = 0; it < 3; ++it) {
+            double f, df;
+            poly_eval(c, deg, x, f, df);
+            if (df == 0.0) break;
+            const double xn = x - f / df;
+            if (!(fabs(xn - x) <= 1e-6 * fmax(1.0, fabs(x)))) break;
+            x = xn;
+        }
+        out[k] = x;
+    }
+    for (int a = 1; a < n; ++a)       // ascending
+        for (int b = a; b > 0 && out[b - 1] > out[b]; --b) { double t = out[b]; out[b] = out[b - 1]; out[b - 1] = t; }
+    return n;
+}
+
+// nearest curve parameter: 129 samples, then <= 30 clamped Newton steps
+TQ_HD inline double bz_nearest(const CurveC& c, double px, double py) {
+    const double* q = c.buf + c.o_pw;
+    double t = 0.0, best = INFINITY;
+    for (int s = 0; s < 129; ++s) {
+        const double ts = s / 128.0;
+        const double dx = bz_axis(q, ts) - px, dy = bz_axis(q + 4, ts) - py;
+        const double d2 = dx * dx + dy * dy;
+        if (d2 < best) { best = d2; t = ts; }
+    }
+    for (int it = 0; it < 30; ++it) {
+        const double gx = bz_axis(q, t) - px, gy = bz_axis(q + 4, t) - py;
+        const double dgx = bz_daxis(q, t), dgy = bz_daxis(q + 4, t);
+        const double ddx = 6.0 * q[0] * t + 2.0 * q[1], ddy = 6.0 * q[4] * t + 2.0 * q[5];
+        const double f = gx * dgx + gy * dgy;
+        const double df = (dgx * dgx + dgy * dgy) + (gx * ddx + gy * ddy);
+        if (df <= 0.0) break;
+        double tn = t - f / df;
+        tn = tn < 0.0 ? 0.0 : (tn > 1.0 ? 1.0 : tn);
+        const bool done = fabs(tn - t) < 1e-15;
+        t = tn;
+        if (done) break;
+    }
+    return t;
+}
+
+TQ_HD inline bool bz_tangent_side(const CurveC& c, double px, double py) {
+    const double t = bz_nearest(c, px, py);
+    double x, y, dx, dy;
+    bz_eval(c, t, x, y);
+    bz_deriv(c, t, dx, dy);
+    return dx * (py - y) - dy * (px - x) >= 0.0;
+}
+
+// crossing parity of the segment pt -> anchor; returns 0 untrustworthy,
+// 1 outside, 2 inside
+TQ_HD inline int bz_parity(const CurveC& c, double px, double py, double ax, double ay) {
+    const double* q = c.buf + c.o_pw;
+    const double dx = ax - px, dy = ay - py;
+    // cr(v) = d x v for v = a, b, c, (d - pt)
+    double co[4];
+    for (int k = 0; k < 4; ++k) {
+        const double vx = k < 3 ? q[k] : q[3] - px, vy = k < 3 ? q[4 + k] : q[7] - py;
+        co[k] = dx * vy - dy * vx;
+    }
+    double roots[3];
+    const int nr = real_roots(co, 4, roots);
+    if (nr == 0) return 2;
+    double ts[3];
+    int nt = 0;
+    for (int k = 0; k < nr; ++k)
+        if (roots[k] > -1e-12 && roots[k] < 1.0 + 1e-12) ts[nt++] = roots[k];
+    for (int k = 1; k < nt; ++k)
+        if (ts[k] - ts[k - 1] < 1e-8) return 0;        // grazing: near-coincident roots
+    const double dd = dx * dx + dy * dy;
+    int crossings = 0;
+    for (int k = 0; k < nt; ++k) {
+        const double tc = ts[k] < 0.0 ? 0.0 : (ts[k] > 1.0 ? 1.0 : ts[k]);
+        double x, y;
+        bz_eval(c, tc, x, y);
+        const double sp = ((x - px) * dx + (y - py) * dy) / dd;
+        if (fabs(sp) < 1e-9) return bz_tangent_side(c, px, py) ? 2 : 1;
+        if (fabs(sp - 1.0) < 1e-9) return 0;
+        if (0.0 < sp && sp < 1.0) ++crossings;
+    }
+    return (crossings % 2 == 0) ? 2 : 1;
+}
+
+TQ_HD inline bool bz_inside(const CurveC& c, double px, double py) {
+    const double* an = c.buf + c.o_pw + 8;
+    for (int k = 0; k < 3; ++k) {
+        const int r = bz_parity(c, px, py, an[2 * k], an[2 * k + 1]);
+        if (r) return r == 2;
+    }
+    return bz_tangent_side(c, px, py);
+}
+
+TQ_HD inline double bz_signed_distance(const CurveC& c, double px, double py) {
+    const bool ins = bz_inside(c, px, py);
+    double x, y;
+    bz_eval(c, bz_nearest(c, px, py), x, y);
+    const double d = hypot(x - px, y - py);
+    return ins ? d : -d;
+}
+
 // ---------------------------------------------------------------- generic
 TQ_HD inline void curve_eval(const CurveC& c, double t, double& x, double& y) {
     switch (c.kind) {
@@ -168,6 +365,9 @@ TQ_HD inline void curve_eval(const CurveC& c, double t, double& x, double& y) {
             y = c.prm[1] + c.prm[2] * sin(th);
             return;
         }
+        case TQ_CURVE_BEZIER:
+            bz_eval(c, t, x, y);
+            return;
         default:
             bs_eval(c, t, x, y);
     }
@@ -188,6 +388,9 @@ TQ_HD inline void curve_deriv(const CurveC& c, double t, double& dx, double& dy)
             dy = c.prm[2] * span * cos(th);
             return;
         }
+        case TQ_CURVE_BEZIER:
+            bz_deriv(c, t, dx, dy);
+            return;
         default:
             bs_deriv(c, t, dx, dy);
     }
@@ -207,6 +410,8 @@ TQ_HD inline double curve_signed_distance(const CurveC& c, double x, double y) {
             double r = hypot(x - c.prm[0], y - c.prm[1]);
             return (c.prm[3] != 0.0 ? 1.0 : -1.0) * (c.prm[2] - r);
         }
+        case TQ_CURVE_BEZIER:
+            return bz_signed_distance(c, x, y);
         default:
             return bs_signed_distance(c, x, y);
     }
@@ -276,6 +481,52 @@ TQ_HD inline int curve_intersect_line(const CurveC& c, int axis, double level, d
                         *overflow = 1;
                     }
                 }
+            }
+            return n;
+        }
+        case TQ_CURVE_BEZIER: {
+            // roots of the axis polynomial - level, clamped and Newton-polished,
+            // tangential touches dropped, duplicates merged (src/trimming.py:324-351)
+            const double* q = c.buf + c.o_pw;
+            const double* qa = axis == 0 ? q : q + 4;
+            const double* qo = axis == 0 ? q + 4 : q;
+            double co[4] = {qa[0], qa[1], qa[2], qa[3] - level};
+            double pmax = 0.0;
+            for (int k = 0; k < 8; ++k) pmax = fmax(pmax, fabs(q[k]));
+            const double dmin = 1e-9 * fmax(pmax, 1.0);
+            double roots[3], tt[3], tc[3];
+            bool tg[3];
+            const int nr = real_roots(co, 4, roots);
+            int m = 0;
+            for (int k = 0; k < nr; ++k) {
+                double t = roots[k];
+                if (!(t >= -1e-9 && t <= 1.0 + 1e-9)) continue;
+                t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+                for (int it = 0; it < 3; ++it) {
+                    const double f = bz_axis(qa, t) - level, df = bz_daxis(qa, t);
+                    if (fabs(df) < 1e-14) break;
+                    t = t - f / df;
+                    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+                }
+                tt[m] = t;
+                tc[m] = bz_axis(qo, t);
+                tg[m] = fabs(bz_daxis(qa, t)) < dmin;
+                ++m;
+            }
+            for (int a = 1; a < m; ++a)        // stable sort by cross coordinate
+                for (int b = a; b > 0 && tc[b - 1] > tc[b]; --b) {
+                    double x = tt[b]; tt[b] = tt[b - 1]; tt[b - 1] = x;
+                    x = tc[b]; tc[b] = tc[b - 1]; tc[b - 1] = x;
+                    bool g = tg[b]; tg[b] = tg[b - 1]; tg[b - 1] = g;
+                }
+            double lastc = 0.0;
+            bool have = false;
+            for (int a = 0; a < m; ++a) {
+                if (have && fabs(tc[a] - lastc) < 1e-12) continue;
+                have = true;
+                lastc = tc[a];
+                if (tg[a]) continue;
+                if (n < cap) { ht[n] = tt[a]; hc[n] = tc[a]; ++n; } else { *overflow = 1; }
             }
             return n;
         }

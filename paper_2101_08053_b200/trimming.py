@@ -273,22 +273,35 @@ class PeriodicBSplineTrim(TrimmingCurve):
 
 
 class BezierTrim(TrimmingCurve):
-    """Cubic Bezier trimming curve (src/trimming.py:204-351).  Not yet on the
-    device classifier (round-2 item); construction is supported."""
+    """Cubic Bezier trimming curve with its endpoints on the domain boundary
+    (src/trimming.py:204-351).  The device predicates (csrc/curves.cuh
+    bz_*) classify points by crossing parity of the segment to a valid
+    anchor (cubic roots), with the reference's grazing retries and
+    nearest-point tangent fallback."""
 
     def __init__(self, control_points, anchors=((0.05, 0.05), (0.08, 0.03), (0.03, 0.09))):
         self.ctrl = np.asarray(control_points, dtype=float)
         if self.ctrl.shape != (4, 2):
             raise ValueError("cubic Bezier needs 4 control points")
+        c0, c1, c2, c3 = self.ctrl
+        # power-basis coefficients, highest degree first (same as the reference)
+        self._pow = np.stack([-c0 + 3 * c1 - 3 * c2 + c3, 3 * c0 - 6 * c1 + 3 * c2, -3 * c0 + 3 * c1, c0])
         self.anchors = [np.asarray(a, dtype=float) for a in anchors]
+        if len(self.anchors) != 3:
+            raise ValueError("the device predicates take three anchors")
 
     def evaluate(self, t):
-        c0, c1, c2, c3 = self.ctrl
+        a, b, c, d = self._pow
         tt = np.asarray(t, dtype=float)[..., None]
-        return (1 - tt) ** 3 * c0 + 3 * (1 - tt) ** 2 * tt * c1 + 3 * (1 - tt) * tt ** 2 * c2 + tt ** 3 * c3
+        return a * tt ** 3 + b * tt ** 2 + c * tt + d
+
+    def derivative(self, t):
+        a, b, c, _ = self._pow
+        tt = np.asarray(t, dtype=float)[..., None]
+        return 3 * a * tt ** 2 + 2 * b * tt + c
 
     def descriptor(self):
-        raise NotImplementedError("BezierTrim is not on the device classification path yet")
+        return 4, 0, np.concatenate([self.ctrl.ravel(), np.concatenate(self.anchors)])
 
 
 def classify_elements(basis2d: TensorBasis2D, curves) -> TrimConfiguration:

@@ -78,3 +78,44 @@ def test_no_active_functions():
         R = OA.assemble_mass(ocfg, strategy=strategy).data
         M = P.assemble_mass(b2d, cfg, strategy=strategy).data
         assert M.shape == R.shape == (0, 0) and M.nnz == R.nnz == 0
+
+
+def _inject_oracle_cut_rule(cfg, ocfg, q):
+    """The oracle's cut-cell points in place of the native ones (the
+    per-entry bars are for the kernels; the native decomposition differs
+    by ulps, which sliver sub-cells amplify -- DESIGN §3)."""
+    from paper_2101_08053_b200._classify import CutCellRule
+    orule = ocfg.cut_cell_rule(q)
+    keys = sorted(orule.rules)
+    el = np.array(keys, np.int64).reshape(-1, 2)
+    pts = [orule.rules[k][0] for k in keys]
+    ptr = np.concatenate([[0], np.cumsum([x.shape[0] for x in pts])]).astype(np.int64)
+    P = np.vstack(pts) if pts else np.empty((0, 2))
+    W = np.concatenate([orule.rules[k][1] for k in keys]) if keys else np.empty(0)
+    cfg._cut_rules[q] = CutCellRule(q, el, ptr, P, W, np.zeros(len(keys), np.int32))
+
+
+@pytest.mark.parametrize("nel,p", [(24, 2), (48, 3)])
+def test_corner_bezier_larger_meshes(nel, p):
+    """The cubic-Bezier case on the device classifier beyond the golden
+    sizes: classes and u_disc bit-exact, dwq values against the oracle
+    (native cut cells: rel-Frobenius; oracle cut cells injected: per entry)."""
+    from oracle import assemble as OA
+    P, b2d, cfg, ocfg = _pair("corner", nel, p)
+    assert np.array_equal(cfg.element_class, ocfg.element_class)
+    assert np.array_equal(cfg.func_class, ocfg.func_class)
+    assert np.array_equal(cfg.u_disc[0], ocfg.u_disc[0]) and np.array_equal(cfg.u_disc[1], ocfg.u_disc[1])
+    R = OA.assemble_mass(ocfg, strategy="dwq").data
+    M = P.assemble_mass(b2d, cfg, strategy="dwq").data
+    assert np.array_equal(M.indptr, R.indptr) and np.array_equal(M.indices, R.indices)
+    assert np.linalg.norm(M.data - R.data) <= 1e-12 * np.linalg.norm(R.data)
+    _inject_oracle_cut_rule(cfg, ocfg, p)
+    assert_matrix_close(P.assemble_mass(b2d, cfg, strategy="dwq").data, R)
+
+
+def test_cli_mass_corner(tmp_path):
+    from tests.test_cli import read_csv
+    from paper_2101_08053_b200.cli import main
+    assert main(["mass", "--case", "corner", "--degrees", "2", "--meshes", "8", "--out", str(tmp_path)]) == 0
+    _, rows = read_csv(tmp_path / "mass_corner_n8.csv")
+    assert float(rows[0][4]) <= 1e-12 and float(rows[0][5]) <= 1e-12
