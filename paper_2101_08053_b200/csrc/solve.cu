@@ -44,18 +44,31 @@ __device__ __forceinline__ double cg_grid_total(const double* part, double* red)
     return cg_block_sum(v, red);
 }
 
-// row i of y = sl .* (A (sr .* x)); warp-collective, returns the row value
-__device__ __forceinline__ double spmv_row(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                                           const double* __restrict__ data, const double* __restrict__ sr,
-                                           const double* x, int i, int lane) {
+// row i of y = A (sr .* x) on a half-warp (hl = lane within the half, 0..15):
+// rounds of 128 entries, all index/value loads issued before the dependent
+// gathers; a warp carries two rows, so more bytes are in flight per warp.
+// Returns the row value in every lane of the half.
+__device__ __forceinline__ double spmv_row_half(const int32_t* __restrict__ indptr,
+                                                const int32_t* __restrict__ indices,
+                                                const double* __restrict__ data, const double* __restrict__ sr,
+                                                const double* x, int i, int hl, bool valid) {
     double acc = 0.0;
-    const int a = indptr[i], b = indptr[i + 1];
-    for (int k = a + lane; k < b; k += 32) {
-        const int j = indices[k];
-        acc += data[k] * (sr ? sr[j] * x[j] : x[j]);
+    const int a = valid ? indptr[i] : 0, b = valid ? indptr[i + 1] : 0;
+    for (int k0 = a; k0 < b; k0 += 128) {
+        int j[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 16 * u + hl;
+            j[u] = k < b ? __ldcs(indices + k) : -1;   // the matrix streams once per product
+            v[u] = k < b ? __ldcs(data + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j[u] >= 0) acc += v[u] * (sr ? sr[j[u]] * x[j[u]] : x[j[u]]);
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     return acc;
 }
 
@@ -77,11 +90,15 @@ __global__ void k_csr_diag(const int32_t* __restrict__ indptr, const int32_t* __
 __global__ void k_spmv(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                        const double* __restrict__ data, int n, const double* __restrict__ sl,
                        const double* __restrict__ sr, const double* __restrict__ x, double* __restrict__ y) {
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-        const double v = spmv_row(indptr, indices, data, sr, x, i, lane);
-        if (lane == 0) y[i] = sl ? sl[i] * v : v;
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    const int halves = (gridDim.x * blockDim.x) >> 4;
+    // uniform trip count per warp (the shuffles need all 32 lanes)
+    const int h0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    for (int base = h0 & ~1; base < n; base += halves) {
+        const int i = base + ((lane >> 4) & 1);
+        const bool valid = i < n;
+        const double v = spmv_row_half(indptr, indices, data, sr, x, i, hl, valid);
+        if (valid && hl == 0) y[i] = sl ? sl[i] * v : v;
     }
 }
 
@@ -90,6 +107,7 @@ struct CgState {
     double* r;
     double* p;
     double* q;
+    double* sp;       // s .* p (the SpMV gathers one vector)
     double* part_a;   // [grid]
     double* part_b;   // [grid]
     int32_t* iters;   // out: iterations run (== maxiter: not converged)
@@ -126,15 +144,22 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_scaled(const int32_t* __restr
         if (rr == 0.0 || sqrt(rr) < atol) break;   // same value on every block (b = 0: x = 0, as scipy)
         const double rho = rr;
         const double beta = it > 0 ? rho / rho_prev : 0.0;
-        for (int i = tid; i < n; i += nthreads) st.p[i] = it > 0 ? st.r[i] + beta * st.p[i] : st.r[i];
+        for (int i = tid; i < n; i += nthreads) {
+            const double pi = it > 0 ? st.r[i] + beta * st.p[i] : st.r[i];
+            st.p[i] = pi;
+            st.sp[i] = s[i] * pi;
+        }
         grid.sync();
-        // q = As p, p . q
+        // q = As p = s .* (A (s .* p)), p . q
         loc = 0.0;
-        for (int i = warp; i < n; i += nwarps) {
-            const double vi = s[i] * spmv_row(indptr, indices, data, s, st.p, i, lane);
-            if (lane == 0) {
-                st.q[i] = vi;
-                loc += st.p[i] * vi;
+        for (int base = 2 * warp; base < n; base += 2 * nwarps) {
+            const int i = base + (lane >> 4);
+            const bool valid = i < n;
+            const double vi = spmv_row_half(indptr, indices, data, nullptr, st.sp, i, lane & 15, valid);
+            if (valid && (lane & 15) == 0) {
+                const double qi = s[i] * vi;
+                st.q[i] = qi;
+                loc += st.p[i] * qi;
             }
         }
         v = cg_block_sum(loc, red);
@@ -208,7 +233,7 @@ extern "C" int tq_cg_scaled(const int32_t* indptr, const int32_t* indices, const
     const int grid = (int)std::min<int64_t>(cg_grid(), std::max<int64_t>(((int64_t)n * 4 + kCgThreads - 1) / kCgThreads, 1));
     double* w = static_cast<double*>(work);
     const int64_t nn = std::max(n, 1);
-    CgState st{x, w, w + nn, w + 2 * nn, w + 4 * nn, w + 4 * nn + cg_grid(), iters_dev, rnorm_dev};
+    CgState st{x, w, w + nn, w + 2 * nn, w + 3 * nn, w + 4 * nn, w + 4 * nn + cg_grid(), iters_dev, rnorm_dev};
     const int32_t* a0 = indptr;
     const int32_t* a1 = indices;
     const double* a2 = data;
