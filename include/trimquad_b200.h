@@ -307,6 +307,17 @@ int64_t tq_cutcell_npoints(void* handle);
 /* ptr_h: ncut+1 point offsets; pts_h: npoints x 2; w_h: npoints; ncells_h: ncut */
 int tq_cutcell_copy(void* handle, int64_t* ptr_h, double* pts_h, double* w_h, int32_t* ncells_h);
 void tq_cutcell_free(void* handle);
+/* the same decomposition on the device, one thread per cut element, in two
+ * calls.  Count pass (pts == NULL): ptr[z+1] = points of element z (ptr[0]
+ * caller-zeroed), ncells[z] = sub-cells, status[z] = 0 ok / 1 max split
+ * depth / 2 folded / 3 not crossed by exactly one curve / 4 capacity.  The
+ * caller turns ptr into offsets (inclusive scan of ptr[1..]) and calls again
+ * with pts (2 per point) and w to write.  bp1/bp2 breakpoints, cut_el
+ * (ncut x 2 int32, row-major element order) and the outputs are device
+ * arrays; curves and tabs (as for tq_cutcell_build) are host arrays. */
+int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
+                      const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t* ptr,
+                      double* pts, double* w, int32_t* ncells, int32_t* status, void* stream);
 
 /* ---- L2 projection: RHS and error ---------------------------------------- */
 

@@ -9,6 +9,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from ._lib import TrimmingConfigurationError
 
 TQ_CURVE_LINE, TQ_CURVE_ARC, TQ_CURVE_CLOSED_CIRCLE, TQ_CURVE_BEZIER, TQ_CURVE_BSPLINE = 1, 2, 3, 4, 5
 
@@ -118,11 +119,65 @@ def submit(fn, *args):
     return _POOL.submit(fn, *args)
 
 
-def cut_cell_rule(config, q, host_only=False):
-    """Cut-element quadrature of the configuration (host C++).  ``host_only``:
-    find the cut elements on the host (worker threads issue no CUDA work)."""
+_CUT_ERRORS = {1: "cannot decompose cell at maximum split depth 4", 2: "folded sub-cell",
+               3: "cell is not crossed by exactly one curve", 4: "cut-cell capacity exceeded"}
+
+
+def cut_cell_rule_device(config, q):
+    """Cut-element quadrature decomposed on the GPU (tq_cutcell_device, one
+    thread per cut element; same decomposition as the host C++).  The
+    rule's device arrays are kept on it (``rule.dev``) for the formation."""
     if q < 1:
         raise ValueError("Lagrange degree q must be >= 1")
+    b1, b2 = config.basis2d.dir
+    ec = config.element_class_dev.reshape(b1.num_elements, b2.num_elements)
+    el = torch.nonzero(ec == 1).to(torch.int32).contiguous()
+    ncut = el.shape[0]
+    dev = el.device
+    arr, keep = curve_array(config.curves)
+    tabs = cell_tables(q)
+    lib = L.lib()
+    fn = lib.tq_cutcell_device
+    fn.argtypes = [C.POINTER(L.Curve), L.i32, L.vp, L.vp, L.vp, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp]
+    fn.restype = L.i32
+    bp1, bp2 = b1.device_arrays()["bp"], b2.device_arrays()["bp"]
+    ptr = torch.zeros(ncut + 1, dtype=torch.int64, device=dev)
+    ncells = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
+    status = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
+
+    def run(pts, w):
+        rc = fn(arr, len(config.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q,
+                tabs.ctypes.data_as(L.vp), L.ptr(ptr), L.ptr(pts), L.ptr(w), L.ptr(ncells), L.ptr(status),
+                L.stream())
+        if rc != L.TQ_OK:
+            raise L._EXC.get(rc, RuntimeError)(lib.tq_last_error().decode(errors="replace"))
+
+    run(None, None)                              # count pass
+    if ncut:
+        bad = torch.nonzero(status[:ncut]).flatten()
+        if bad.numel():
+            z = int(bad[0])
+            e1, e2 = (int(v) for v in el[z].tolist())
+            raise TrimmingConfigurationError(f"element ({e1}, {e2}): {_CUT_ERRORS.get(int(status[z]), 'error')}")
+        ptr[1:] = torch.cumsum(ptr[1:], 0)
+    npts = int(ptr[-1].item())
+    P = torch.empty((max(npts, 1), 2), dtype=torch.float64, device=dev)
+    W = torch.empty(max(npts, 1), dtype=torch.float64, device=dev)
+    run(P, W)                                    # write pass
+    rule = CutCellRule(q, el.long().cpu().numpy().reshape(-1, 2), ptr.cpu().numpy(), P[:npts].cpu().numpy(),
+                       W[:npts].cpu().numpy(), ncells[:ncut].cpu().numpy())
+    rule.dev = dict(P=P[:npts], W=W[:npts], ptr=ptr, el=el)
+    return rule
+
+
+def cut_cell_rule(config, q, host_only=False):
+    """Cut-element quadrature of the configuration.  On the device when the
+    classes live there (tq_cutcell_device); ``host_only`` (worker threads,
+    host-only configurations) runs the host C++ decomposition."""
+    if q < 1:
+        raise ValueError("Lagrange degree q must be >= 1")
+    if not host_only and getattr(config, "element_class_dev", None) is not None:
+        return cut_cell_rule_device(config, q)
     b1, b2 = config.basis2d.dir
     # cut elements (class 1) in row-major order (found on the device when the
     # classes live there; host-only configurations use the host array)

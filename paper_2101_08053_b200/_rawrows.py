@@ -110,12 +110,16 @@ def cut_point_tables(f):
     rule = f.config.cut_cell_rule(max(f.b1.p, f.b2.p))
     if g.get("cutpts_src") is not rule:      # rebuilt when the rule object changes
         b1, b2 = f.b1, f.b2
-        P = L.dev(rule.points.reshape(-1, 2), torch.float64)
+        ddev = getattr(rule, "dev", None)       # decomposed on the device: no upload
+        if ddev is not None:
+            P, Wd, ptr_d = ddev["P"], ddev["W"], ddev["ptr"]
+        else:
+            P = L.dev(rule.points.reshape(-1, 2), torch.float64)
+            Wd, ptr_d = L.dev(rule.weights, torch.float64), L.dev(rule.ptr, torch.int64)
         cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
         cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
         t = dict(P=P, x=P[:, 0].contiguous(), y=P[:, 1].contiguous(),
-                 W=L.dev(rule.weights, torch.float64), idx=L.dev(cutidx, torch.int32),
-                 ptr=L.dev(rule.ptr, torch.int64), npts=rule.total_points())
+                 W=Wd, idx=L.dev(cutidx, torch.int32), ptr=ptr_d, npts=rule.total_points())
         # span-key groups per cut element (src/assembly.py:380-388): points of
         # one element grouped by (first1, first2), keys in np.unique order
         f1, _ = b1.eval_device(t["x"], check=False)

@@ -142,6 +142,8 @@ class TrimConfiguration:
         C++ decomposition runs without the GIL); ``cut_cell_rule(q)`` joins."""
         if q in self._cut_rules or q in self._cut_pending or not self.has_cuts():
             return
+        if self.element_class_dev is not None and self.element_class_dev.is_cuda:
+            return          # decomposed on the device on first use (tq_cutcell_device)
         from . import _classify
         self._cut_pending[q] = _classify.submit(_classify.cut_cell_rule, self, q, True)
 
