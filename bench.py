@@ -358,7 +358,8 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": nnz_total / float(et[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(et[0]),
-               "path": "KnotVector/Basis1D -> classify_elements (GPU) -> cut_cell_rule (host C++) -> "
+               "step_seconds": [round(x, 4) for x in e_ts],
+               "path": "KnotVector/Basis1D -> classify_elements (GPU) -> cut-cell decomposition (GPU) -> "
                        + ("assemble_mass" if world == 1 else "assemble_mass_distributed (NCCL gather to rank 0)")
                        + " -> scipy CSR on host"}
 

@@ -609,7 +609,6 @@ def run_phase(f, phase):
         desc, nint = _plan(f)
         f._nint = nint
         f._ndesc = desc.shape[0]
-        f.report.n_gauss_elements = gauss_element_count(f)
         g = _geo(f.config)
         f._desc, _ = _desc_dev(f)
         if getattr(f, "_raw_pre", None) is not None and f._desc is not f._desc_pre:

@@ -521,6 +521,9 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
         raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
     f, csr = form(basis2d, config, coeff, strategy, rules)
     if report is not None:
+        # report-only geometry count (cached per row plan), off the formation path
+        from ._rawrows import gauss_element_count, needs_raw
+        f.report.n_gauss_elements = gauss_element_count(f) if needs_raw(f) else 0
         for k, v in f.report.__dict__.items():
             if k != "strategy":
                 setattr(report, k, v)

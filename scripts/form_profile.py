@@ -18,4 +18,4 @@ pr = cProfile.Profile(); pr.enable()
 f, csr = form(bb, cf, None, "dwq"); torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("cumtime").print_stats("paper_2101_08053_b200", 40)
+st.sort_stats("tottime").print_stats(30)
