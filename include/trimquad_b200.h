@@ -113,11 +113,13 @@ int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng
  * layout `lay` with basis values (first, vals) at its points.  Writes
  * rules.w (at wptr offsets), rules.k0, and fail[r] = 1 where the residual
  * exceeds 1e-12 max|b|.  Replaces _solve_rows/_qr_basic_solve
- * (src/quadrature.py:263-303). */
+ * (src/quadrature.py:263-303).  `products` (nullable, n x (2p+1)): the
+ * direction products a[i][j-i+p] = sum_k w_i[k] B_j(x_k) of the solved rows,
+ * bit-identical to tq_wq_products on the same rules. */
 int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, const double* vals,
                 const double* mom, const int32_t* rows, int32_t nrows,
                 int32_t tmax, int32_t mmax, int64_t* wptr, int32_t* k0, double* w,
-                int32_t* fail, void* stream);
+                int32_t* fail, double* products, void* stream);
 
 /* DWQ combination w_j = sum_i S_ij w~_i over augmented points (S in CSC,
  * device).  Replaces build_dwq step 4 (src/quadrature.py:434-444). */

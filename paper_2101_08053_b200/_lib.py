@@ -84,7 +84,7 @@ def lib():
         "tq_debug_stamp": ([vp, i32, vp], i32),
         "tq_basis_eval": ([Space1D, vp, i64, vp, vp, vp, vp, vp], i32),
         "tq_moments_1d_g": ([Space1D, vp, vp, i32, vp, vp], i32),
-        "tq_wq_solve": ([Space1D, Layout, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp], i32),
+        "tq_wq_solve": ([Space1D, Layout, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp], i32),
         "tq_dwq_combine": ([vp, i32, vp, vp, vp, Rules, Rules, vp], i32),
         "tq_wq_products": ([Space1D, Layout, vp, vp, Rules, vp, vp], i32),
         "tq_row_counts": ([RowCtx, vp, vp], i32),

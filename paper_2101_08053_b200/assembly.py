@@ -314,6 +314,10 @@ class Formation:
         """Direction-wise WQ contractions a_d (c == 1)."""
         if not self.separable():
             return
+        pre = [getattr(r, "_products", None) for r in self.rules[:2]]
+        if all(a is not None for a in pre):      # written by the fits (tq_wq_solve)
+            self.a1, self.a2 = pre
+            return
         from ._rawrows import _forked, _keep_on, _named_stream
         main = torch.cuda.current_stream()
         side = _named_stream("products", priority=-2)

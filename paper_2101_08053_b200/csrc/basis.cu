@@ -6,11 +6,20 @@
 
 namespace tq {
 
+// The knot vector is staged in shared memory when it fits (the span search
+// is a chain of dependent loads: from shared memory instead of L2).
 template <int P>
 __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t n,
                              int32_t* __restrict__ first, double* __restrict__ vals,
-                             double* __restrict__ ders, int32_t* status) {
-    const double lo = s.knots[0], hi = s.knots[s.nknots - 1];
+                             double* __restrict__ ders, int32_t* status, int staged) {
+    extern __shared__ double skn[];
+    const double* kn = s.knots;
+    if (staged) {
+        for (int k = threadIdx.x; k < s.nknots; k += blockDim.x) skn[k] = s.knots[k];
+        __syncthreads();
+        kn = skn;
+    }
+    const double lo = kn[0], hi = kn[s.nknots - 1];
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         double x = u[t];
@@ -18,16 +27,16 @@ __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t
             if (status) atomicOr(status, kStatusDomain);
             x = x < lo ? lo : hi;
         }
-        int span = find_span(s.knots, s.nknots, P, s.n, x);
+        int span = find_span(kn, s.nknots, P, s.n, x);
         double N[P + 1];
         if (ders) {
             double D[kMaxP + 1];
             double Nr[kMaxP + 1];
-            basis_funs_ders_rt(s.knots, P, span, x, Nr, D);
+            basis_funs_ders_rt(kn, P, span, x, Nr, D);
 #pragma unroll
             for (int k = 0; k <= P; ++k) { N[k] = Nr[k]; ders[t * (P + 1) + k] = D[k]; }
         } else {
-            basis_funs<P>(s.knots, span, x, N);
+            basis_funs<P>(kn, span, x, N);
         }
         first[t] = span - P;
 #pragma unroll
@@ -92,8 +101,11 @@ extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* 
     if (n == 0) return TQ_OK;
     if (s.p < 0 || s.p > kMaxP) { set_error("degree %d unsupported (max %d)", s.p, kMaxP); return TQ_EINVAL; }
     int grid = grid_for(n, 256);
+    const size_t kbytes = sizeof(double) * (size_t)s.nknots;
+    const int staged = kbytes <= 32 * 1024;
+    const size_t shm = staged ? kbytes : 0;
     switch (s.p) {
-#define CASE(P) case P: k_basis_eval<P><<<grid, 256, 0, S(stream)>>>(s, u, n, first, vals, ders, status); ::tq::note_launch(); break;
+#define CASE(P) case P: k_basis_eval<P><<<grid, 256, shm, S(stream)>>>(s, u, n, first, vals, ders, status, staged); ::tq::note_launch(); break;
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     }

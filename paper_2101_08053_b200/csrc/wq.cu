@@ -43,7 +43,7 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
                            const double* __restrict__ vals, const double* __restrict__ mom,
                            const int32_t* __restrict__ rows, int nrows, int tmax, int mmax,
                            const int64_t* __restrict__ wptr, int32_t* __restrict__ k0out,
-                           double* __restrict__ wout, int32_t* __restrict__ fail, int32_t* err) {
+                           double* __restrict__ wout, int32_t* __restrict__ fail, double* __restrict__ prod) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int per = 2 * tmax * mmax + tmax + 2 * mmax;  // A, A0, b, w + perm (as double slots)
@@ -145,11 +145,20 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
             for (int k = 0; k < rank; ++k) w[perm[k]] = z[k];
         }
         __syncwarp();
-        // residual with the original system (src/quadrature.py:299-301)
+        // residual with the original system (src/quadrature.py:299-301).
+        // (A w)[j] = sum_k w_k B_j(x_k) is also the direction product of
+        // sum_factor_row (src/assembly.py:245-252): written out when asked
+        // (same terms, same order as tq_wq_products -> bit-identical)
         double rmax = 0.0, bmax = 0.0;
+        if (prod)
+            for (int o = lane; o < W; o += 32) {
+                const int j = i - p + o;
+                if (j < j0 || j >= j0 + t) prod[(int64_t)i * W + o] = 0.0;
+            }
         for (int rr = lane; rr < t; rr += 32) {
             double acc = 0.0;
             for (int c = 0; c < m; ++c) acc += A0[c * t + rr] * w[c];
+            if (prod) prod[(int64_t)i * W + (j0 + rr - i + p)] = acc;
             double bb = mom[(int64_t)i * W + (j0 + rr - i + p)];
             rmax = fmax(rmax, fabs(acc - bb));
             bmax = fmax(bmax, fabs(bb));
@@ -192,7 +201,7 @@ using namespace tq;
 extern "C" int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, const double* vals,
                            const double* mom, const int32_t* rows, int32_t nrows, int32_t tmax,
                            int32_t mmax, int64_t* wptr, int32_t* k0, double* w, int32_t* fail,
-                           void* stream) {
+                           double* products, void* stream) {
     if (nrows == 0) return TQ_OK;
     if (tmax > 2 * kMaxP + 1) { set_error("too many trials per system (%d)", tmax); return TQ_EINVAL; }
     const int wpb = 4;
@@ -202,7 +211,7 @@ extern "C" int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, co
     TQ_CUDA(cudaFuncSetAttribute(k_wq_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int grid = (nrows + wpb - 1) / wpb;
     k_wq_solve<<<grid, 32 * wpb, shm, S(stream)>>>(s, lay, first, vals, mom, rows, nrows, tmax, mmax,
-                                                   wptr, k0, w, fail, nullptr); ::tq::note_launch();
+                                                   wptr, k0, w, fail, products); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_wq_solve");
     return TQ_OK;
 }

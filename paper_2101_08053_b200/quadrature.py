@@ -258,7 +258,7 @@ class _FitPlan:
         self.rows = L.dev(self.rows_h, torch.int32)
 
 
-def _solve_rows_async_t(plan: _FitPlan, init=None):
+def _solve_rows_async_t(plan: _FitPlan, init=None, products=None):
     """Launch the GPU moment fits of a plan (src/quadrature.py:281-303).
     Returns ((wptr, k0, w, fail), (first, vals) basis table at the layout
     points or None) as device tensors; no host sync.  The solve writes k0,
@@ -282,7 +282,7 @@ def _solve_rows_async_t(plan: _FitPlan, init=None):
         mom = moments_device(basis)
         L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
                L.ptr(plan.rows), plan.rows_h.size, plan.tmax, plan.mmax, L.ptr(plan.wptr), L.ptr(k0), L.ptr(w),
-               L.ptr(fail), L.stream())
+               L.ptr(fail), L.ptr(products), L.stream())
     return (plan.wptr, k0, w, fail), tab
 
 

@@ -11,10 +11,13 @@ c5 = C.baseline_config(5, nel=nel)
 b2d, cfg = C.build_space(None, nel, 4, curves=c5["curves"])
 if "stamps" in sys.argv:
     from paper_2101_08053_b200 import _lib as L, assembly as A
-    gf = GraphFormation(b2d, cfg, None, "dwq")     # plans warmed
+    world = int(sys.argv[sys.argv.index("world") + 1]) if "world" in sys.argv else 1
+    K = cfg.active_index()[0]["K"]
+    rr = (0, K // world)
+    gf = GraphFormation(b2d, cfg, None, "dwq", row_range=rr)     # plans warmed
     del gf
     A.STAMPS = L.Stamps()
-    gf = GraphFormation(b2d, cfg, None, "dwq")
+    gf = GraphFormation(b2d, cfg, None, "dwq", row_range=rr)
     # the capture pass is the last set of stamps recorded
     names = A.STAMPS.names
     k = len(names) - 1 - names[::-1].index("start")
