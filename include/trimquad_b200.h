@@ -190,6 +190,9 @@ int tq_deep_flags(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows
  * and the per-pass positivity of the direction factors a1, a2 */
 int tq_deep_geometry(tq_rowctx c, const int8_t* func_class, const int32_t* raw_rows,
                      int32_t nraw, int8_t* geo, void* stream);
+/* tq_deep_apply writes the flags of the direction-1 lines spanned by the
+ * context's rows [row_begin, row_end) (the only ones the counts and the fill
+ * of that row block read); flags on other lines are left unchanged */
 int tq_deep_apply(tq_rowctx c, const int8_t* geo, int8_t* deep, void* stream);
 
 int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);

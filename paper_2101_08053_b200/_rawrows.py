@@ -418,13 +418,40 @@ def _cut_tables(f):
                 blocks=torch.empty(max(t["ngroups"], 1) * Q * Q, dtype=torch.float64, device=f.dev))
 
 
-def _cut_blocks_ctx(f, cut):
+def _group_range(f, cut):
+    """Span-key groups of the cut elements a row block reads: elements in
+    the supports of the block's raw-row window (cut elements and their
+    groups are stored in row-major element order: one contiguous range)."""
+    win = line_window(f)
+    if win is None:
+        return 0, cut["ngroups"]
+    g = _geo(f.config)
+    key = ("groups", win, id(cut["grp_ptr"]))
+    if key not in g:
+        rule = f.config.cut_cell_rule(max(f.b1.p, f.b2.p))
+        e1 = rule.elements[:, 0]
+        # the gather reads one element beyond each raw row's support
+        lo_e = max(int(f.b1._el_first[win[0]]) - 1, 0) if win[1] >= win[0] else 0
+        hi_e = min(int(f.b1._el_last[win[1]]) + 1, f.b1.num_elements - 1) if win[1] >= win[0] else -1
+        c0 = int(np.searchsorted(e1, lo_e, side="left"))
+        c1 = int(np.searchsorted(e1, hi_e, side="right"))
+        gp = cut["grp_ptr"].cpu().numpy()
+        g[key] = (int(gp[c0]), int(gp[c1]))
+    return g[key]
+
+
+def _cut_blocks_ctx(f, cut, groups=None):
+    """tq_cut_blocks context; ``groups`` = (g0, g1) restricts the launch to
+    that group range (pointer offsets, no kernel change)."""
     P = L.ptr
+    g0, g1 = groups if groups is not None else (0, cut["ngroups"])
+    Q = (f.b1.p + 1) * (f.b2.p + 1)
     return RawCtx(n1=f.b1.n, n2=f.b2.n, p1=f.b1.p, p2=f.b2.p, nel1=f.b1.num_elements, nel2=f.b2.num_elements,
                   cutidx=P(cut["idx"]), cut_ptr=P(cut["ptr"]), cut_cw=P(cut["cw"]), cfirst1=P(cut["f1"]),
                   cvals1=P(cut["v1"]), cfirst2=P(cut["f2"]), cvals2=P(cut["v2"]), grp_ptr=P(cut["grp_ptr"]),
-                  grp_key=P(cut["grp_key"]), grp_pts=P(cut["grp_pts"]), grp_perm=P(cut["grp_perm"]),
-                  grp_blocks=P(cut["blocks"]), ngroups=cut["ngroups"])
+                  grp_key=P(cut["grp_key"]), grp_pts=L.vp(cut["grp_pts"].data_ptr() + 8 * g0),
+                  grp_perm=P(cut["grp_perm"]), grp_blocks=L.vp(cut["blocks"].data_ptr() + 8 * Q * Q * g0),
+                  ngroups=max(g1 - g0, 0))
 
 
 _NAMED = {}
@@ -467,7 +494,7 @@ def prelaunch_geometry(f):
     with _forked(main, s2):
         if f.config.has_cuts():
             cut = _cut_tables(f)
-            L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut), L.stream())
+            L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.stream())
         from .assembly import _stamp
         _stamp("cutpre:blocks")
     s.wait_stream(s2)         # one stream to join later
@@ -488,9 +515,9 @@ def join_cut_blocks(f):
         f._cut_stream = None
 
 
-def _plan(f):
-    """Raw rows and their descriptors (host bookkeeping, cached per
-    configuration / strategy / coefficient kind / DWQ key set)."""
+def _plan_full(f):
+    """Raw rows and their descriptors for the whole matrix (host bookkeeping,
+    cached per configuration / strategy / coefficient kind / DWQ key set)."""
     setup = getattr(f, "_setup", None)
     ki = setup.key_index if setup is not None else _key_index(f)
     key = ("plan", f.strategy, f.coeff.identity, tuple(sorted(ki[0].items())), tuple(sorted(ki[1].items())))
@@ -500,12 +527,50 @@ def _plan(f):
     return g[key]
 
 
+def line_window(f):
+    """Direction-1 lines [lo, hi] whose raw rows a row block needs: its own
+    lines and the partner lines within p1 (|j1 - i1| <= p1 for every entry
+    of a block row).  None: the whole matrix."""
+    rr = getattr(f, "row_range", None)
+    if rr is None or (rr[0] <= 0 and rr[1] >= f.K):
+        return None
+    g = _geo(f.config)
+    key = ("lines", tuple(rr))
+    if key not in g:
+        n2 = f.b2.n
+        if rr[1] <= rr[0]:
+            g[key] = (0, -1)
+        else:
+            a = int(f.active[rr[0]].item()) // n2
+            b = int(f.active[rr[1] - 1].item()) // n2
+            g[key] = (max(a - f.b1.p, 0), min(b + f.b1.p, f.b1.n - 1))
+    return g[key]
+
+
+def _plan(f):
+    """The raw-row plan of this formation: the whole matrix, or -- for a row
+    block (multi-GPU sharding) -- only the raw rows on the block's line
+    window, so each rank forms the raw rows its block reads."""
+    desc, nint = _plan_full(f)
+    win = line_window(f)
+    if win is None:
+        return desc, nint
+    g = _geo(f.config)
+    key = ("plan_window", id(desc), win)
+    if key not in g:
+        i1 = desc[:, 0] // f.b2.n
+        keep = (i1 >= win[0]) & (i1 <= win[1])
+        g[key] = (desc[keep], int(np.count_nonzero(keep[:nint])), desc)   # (the full plan kept alive)
+    d, n, _ = g[key]
+    return d, n
+
+
 def gauss_element_count(f):
     """Distinct interior elements whose element-Gauss block the strategy
     computes (FormationReport.n_gauss_elements; src/assembly.py:310-332):
     the supports of GAUSS rows and the residual (outside-box) supports of
     BOX rows, interior elements only.  Geometry of the row plan, cached."""
-    desc, _ = _plan(f)
+    desc, _ = _plan_full(f)
     g = _geo(f.config)
     key = ("ngauss", id(desc))
     if key not in g:
@@ -635,6 +700,7 @@ def run_phase(f, phase):
     elif phase == "cutcells":
         if f._setup.cut is not None:
             if getattr(f, "_cut_pre", None) is None:
-                L.call("tq_cut_blocks", f._ctx, L.stream())
+                L.call("tq_cut_blocks", _cut_blocks_ctx(f, f._setup.cut, _group_range(f, f._setup.cut)),
+                       L.stream())
             join_cut_blocks(f)
             L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())

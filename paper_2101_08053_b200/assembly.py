@@ -385,7 +385,8 @@ class Formation:
                        self.raw_list.numel(), L.ptr(geo), L.stream())
                 g[gkey] = (geo, self.raw_list)     # the list is kept alive with its key
             self.deep = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
-            L.call("tq_deep_apply", self.rowctx(), L.ptr(g[gkey][0]), L.ptr(self.deep), L.stream())
+            L.call("tq_deep_apply", self.rowctx(row_begin, row_end), L.ptr(g[gkey][0]), L.ptr(self.deep),
+                   L.stream())
             _stamp("deep_flags")
         self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
@@ -432,6 +433,7 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     dict(nnz=...), used by GraphFormation) schedules the cut-row chain on a
     side stream, overlapping the deep-row flags and counts."""
     f = Formation(basis2d, config, coeff, strategy, timer, capture)
+    f.row_range = row_range        # a row block forms only the raw rows its rows read
     rep = f.report
     if config.has_cuts():     # shared geometry (src/assembly.py:505-508): built on a worker
         config.cut_cell_rule_async(max(basis2d.degrees))   # thread while the fits run

@@ -446,6 +446,9 @@ __global__ void k_deep_init(tq_rowctx c, const int8_t* __restrict__ fc, int8_t* 
 __global__ void k_deep_apply(tq_rowctx c, const int8_t* __restrict__ geo, const int8_t* __restrict__ pos,
                              int8_t* __restrict__ deep) {
     const int i1 = blockIdx.y;
+    // only the lines of the context's row block are read (counts, fill)
+    if (c.row_end > c.row_begin &&
+        (i1 < c.active[c.row_begin] / c.n2 || i1 > c.active[c.row_end - 1] / c.n2)) return;
     const bool p1 = pos[i1];
     const int64_t base = (int64_t)i1 * c.n2;
     for (int i2 = blockIdx.x * blockDim.x + threadIdx.x; i2 < c.n2; i2 += gridDim.x * blockDim.x)
