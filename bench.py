@@ -73,23 +73,26 @@ def cpu_threads():
     return len(os.sched_getaffinity(0))
 
 
-def oracle_sample(nel, p, strategy, seed, repeats=1):
+def oracle_sample(nel, p, strategy, seed, repeats=3, threads=None):
     """Reference CPU path (oracle port) on a bounded sample of the workload:
-    the same trim, degree and strategy on an nel x nel mesh.  Returns
-    (nnz/s of the best repeat, description)."""
+    the same trim, degree and strategy on an nel x nel mesh, after one
+    warm-up, with ``threads`` BLAS threads (default: all host cores).
+    Returns (median nnz/s over the repeats, description)."""
     from threadpoolctl import threadpool_limits
     from oracle import assemble as OA
     from oracle import configs as OC
-    with threadpool_limits(limits=cpu_threads()):
+    threads = threads or cpu_threads()
+    with threadpool_limits(limits=threads):
         c = OC.config(5, seed=seed, nel=nel, p=p)
         cfg = OC.build_space(c["curves"], nel, p)
         cfg.cut_cell_rule(p)
+        OA.form_with_timings(strategy, cfg)          # warm-up (SURVEY 8d: median after warm-up)
         rates = []
         for _ in range(repeats):
             M, rep = OA.form_with_timings(strategy, cfg)
             rates.append(M.data.nnz / rep.t_total)
     sample = (f"oracle/ (numpy restatement of trimquad) form_with_timings t_total, same trim/p/strategy on "
-              f"{nel}x{nel} elements ({M.data.nnz} nnz), median of {repeats}")
+              f"{nel}x{nel} elements ({M.data.nnz} nnz), {threads} thread(s), median of {repeats} after a warm-up")
     return statistics.median(rates), sample
 
 
@@ -369,7 +372,9 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu:
         try:
             v, sample = oracle_sample(args.cpu_nel, args.p, args.strategy, args.seed)
-            cpu = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": sample}
+            v1, sample1 = oracle_sample(args.cpu_nel, args.p, args.strategy, args.seed, repeats=1, threads=1)
+            cpu = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": sample,
+                   "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": sample1}}
         except Exception as exc:  # the GPU number stands on its own
             cpu = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": f"failed: {exc}"}
     out = {
