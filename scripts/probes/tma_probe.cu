@@ -9,7 +9,7 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigne
                  :: "l"(gdst), "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes) : "memory");
 }
 
-__global__ void k_probe(int nrows, int ch, int ns, int touch, int32_t* idx, double* dat) {
+__global__ void k_probe(int nrows, int ch, int ns, int touch, int32_t* idx, double* dat, int unaligned) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int n = ch * 81;
@@ -35,21 +35,38 @@ __global__ void k_probe(int nrows, int ch, int ns, int touch, int32_t* idx, doub
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-            const int64_t pos = (int64_t)cidx * ((ch * 81 + 3) / 4 * 4);
-            bulk_store(dat + pos, d, (unsigned)((m * 8 + 15) / 16 * 16));
-            bulk_store(idx + pos, x, (unsigned)((m * 4 + 15) / 16 * 16));
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (!unaligned) {
+            if (lane == 0) {
+                const int64_t pos = (int64_t)cidx * ((ch * 81 + 3) / 4 * 4);
+                bulk_store(dat + pos, d, (unsigned)((m * 8 + 15) / 16 * 16));
+                bulk_store(idx + pos, x, (unsigned)((m * 4 + 15) / 16 * 16));
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else {
+            // chunks shifted by 0..3 entries, so neighbouring chunks (other warps)
+            // overlap and share partial sectors; aligned interior by TMA, ragged
+            // ends by plain stores -- the cost of cross-warp partial sectors
+            const int64_t pos = (int64_t)cidx * ch * 81 + ((cidx * 5) & 3);
+            const int64_t sd = (pos + 1) & ~1LL, ed = (pos + m) & ~1LL, sx = (pos + 3) & ~3LL, ex = (pos + m) & ~3LL;
+            if (lane == 0) {
+                if (ed > sd) bulk_store(dat + sd, d, (unsigned)(ed - sd) * 8u);
+                if (ex > sx) bulk_store(idx + sx, x, (unsigned)(ex - sx) * 4u);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (lane == 1 && sd > pos) dat[pos] = 1.0;
+            if (lane == 2 && ed < pos + m) dat[pos + m - 1] = 1.0;
+            if (lane >= 3 && lane < 3 + (sx - pos)) idx[pos + lane - 3] = 1;
+            if (lane >= 8 && lane < 8 + (pos + m - ex)) idx[ex + lane - 8] = 1;
         }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-extern "C" int probe(int nrows, int ch, int ns, int wpb, int bps, int touch, int32_t* idx, double* dat) {
+extern "C" int probe(int nrows, int ch, int ns, int wpb, int bps, int touch, int32_t* idx, double* dat, int unaligned) {
     const size_t stage_bytes = ((size_t)ch * 81 * 12 + 15) / 16 * 16;
     const size_t shm = stage_bytes * ns * wpb;
     if (shm > 227 * 1024) return -1;
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-    k_probe<<<148 * bps, 32 * wpb, shm>>>(nrows, ch, ns, touch, idx, dat);
+    k_probe<<<148 * bps, 32 * wpb, shm>>>(nrows, ch, ns, touch, idx, dat, unaligned);
     return (int)cudaGetLastError();
 }
