@@ -81,6 +81,41 @@ __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e
     return v != 0.0 ? col : -1;
 }
 
+// U chunks of 32 entries of row g at once (lane's entries e0 + 32u + lane):
+// col_of, slot and the row's own raw value depend only on the column, so they
+// are issued together; only the partner's raw value waits for slot[j] -- two
+// dependent load levels per 32U entries instead of three per 32.  col[u] =
+// kept column or -1, v[u] = M_ij + M_ji (same expression as entry()).
+template <int U>
+__device__ __forceinline__ void entries_batch(const tq_rowctx& c, const RowGeom& g, int e0, int lane, int n,
+                                              int* col, double* v) {
+    int cl[U], sj[U], j1[U], j2[U];
+    double vi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int e = e0 + 32 * u + lane;
+        const bool valid = e < n;
+        const int ee = valid ? e : 0;
+        const int q1 = ee / g.t2;
+        j1[u] = g.j1lo + q1;
+        j2[u] = g.j2lo + (ee - q1 * g.t2);
+        const int jidx = j1[u] * c.n2 + j2[u];
+        cl[u] = valid ? __ldg(c.col_of + jidx) : -1;
+        sj[u] = valid ? __ldg(c.slot + jidx) : -1;
+        vi[u] = valid ? raw_value(c, g.i1, g.i2, g.s_i, j1[u], j2[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        col[u] = -1;
+        v[u] = 0.0;
+        if (cl[u] >= 0) {
+            const double w = vi[u] + raw_value(c, j1[u], j2[u], sj[u], g.i1, g.i2);
+            v[u] = w;
+            col[u] = w != 0.0 ? cl[u] : -1;
+        }
+    }
+}
+
 // Counts, pass 1 (thread per row, no raw values needed): deep rows are
 // counted arithmetically and flagged fast when their window is full; other
 // rows are appended to list A (counted by pass 2), deep rows with a partial
@@ -132,11 +167,12 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
         RowGeom g = row_geom(c, r);
         const int n = g.t1 * g.t2;
         int cnt = 0;
-        for (int e0 = 0; e0 < n; e0 += 32) {
-            const int e = e0 + lane;
-            double v;
-            const bool keep = e < n && entry(c, g, e, v) >= 0;
-            cnt += __popc(__ballot_sync(0xffffffffu, keep));
+        for (int e0 = 0; e0 < n; e0 += 96) {
+            int col[3];
+            double v[3];
+            entries_batch<3>(c, g, e0, lane, n, col, v);
+#pragma unroll
+            for (int u = 0; u < 3; ++u) cnt += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
         }
         if (lane == 0) counts[r - c.row_begin] = cnt;
     }
@@ -374,17 +410,20 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
                 }
             }
         } else {
-            for (int e0 = 0; e0 < n; e0 += 32) {
-                const int e = e0 + lane;
-                double v = 0.0;
-                const int col = e < n ? entry(c, g, e, v) : -1;
-                const unsigned m = __ballot_sync(0xffffffffu, col >= 0);
-                if (col >= 0) {
-                    const int at = pos + __popc(m & lt);
-                    indices[at] = col;
-                    data[at] = 0.5 * v;
+            for (int e0 = 0; e0 < n; e0 += 96) {
+                int col[3];
+                double v[3];
+                entries_batch<3>(c, g, e0, lane, n, col, v);
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {       // entries stay in column order
+                    const unsigned m = __ballot_sync(0xffffffffu, col[u] >= 0);
+                    if (col[u] >= 0) {
+                        const int at = pos + __popc(m & lt);
+                        indices[at] = col[u];
+                        data[at] = 0.5 * v[u];
+                    }
+                    pos += __popc(m);
                 }
-                pos += __popc(m);
             }
         }
     }
