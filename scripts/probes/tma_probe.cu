@@ -18,7 +18,14 @@ __global__ void k_probe(int nrows, int ch, int ns, int touch, int32_t* idx, doub
     const int nchunks = (nrows + ch - 1) / ch;
     const int nw = gridDim.x * wpb;
     int k = 0;
-    for (int cidx = blockIdx.x * wpb + wib; cidx < nchunks; cidx += nw, ++k) {
+    // unaligned >= 2: each warp writes `unaligned` consecutive chunks (a tile)
+    // before moving to its next tile -- the fill kernel's order
+    const int per = unaligned >= 2 ? unaligned : 1;
+    for (int it = 0;; ++it, ++k) {
+        const int tile = blockIdx.x * wpb + wib + (it / per) * nw;
+        const int cidx = tile * per + (it % per);
+        if (tile * per >= nchunks) break;
+        if (cidx >= nchunks) continue;
         unsigned char* st = mine + (size_t)(k % ns) * stage_bytes;
         if (lane == 0 && k >= ns) {
             if (ns == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -30,12 +37,20 @@ __global__ void k_probe(int nrows, int ch, int ns, int touch, int32_t* idx, doub
         const int m = rows * 81;
         double* d = reinterpret_cast<double*>(st);
         int* x = reinterpret_cast<int*>(st + (size_t)n * 8);
-        if (touch) {
+        if (touch == 1) {
             for (int e = lane; e < m; e += 32) { d[e] = (double)e; x[e] = e; }
+        } else if (touch == 2) {      // constant payload
+            for (int e = lane; e < m; e += 32) { d[e] = 1.0; x[e] = 7; }
+        } else if (touch == 3) {      // incompressible-looking payload
+            for (int e = lane; e < m; e += 32) {
+                const unsigned long long h = (unsigned long long)(cidx * 1315423911u + e) * 0x9E3779B97F4A7C15ull;
+                d[e] = __longlong_as_double((long long)(h >> 2) | 0x3000000000000000ll);
+                x[e] = (int)(h >> 33);
+            }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (!unaligned) {
+        if (unaligned != 1) {
             if (lane == 0) {
                 const int64_t pos = (int64_t)cidx * ((ch * 81 + 3) / 4 * 4);
                 bulk_store(dat + pos, d, (unsigned)((m * 8 + 15) / 16 * 16));

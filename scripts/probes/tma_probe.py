@@ -11,7 +11,7 @@ for touch in touches:
     for ch in ((8,) if "quick" in sys.argv else (2, 4, 8, 16)):
         for ns in ((2,) if "quick" in sys.argv else (2, 3, 4)):
             for wpb, bps in ((6, 2), (8, 1)) if "quick" in sys.argv else ((8, 1), (8, 2), (4, 4), (16, 1)):
-              for un in (0, 1):
+              for un in ((0, 4, 16) if "quick" in sys.argv else (0, 1)):
                 args = (nrows, ch, ns, wpb, bps, touch, C.c_void_p(idx.data_ptr()), C.c_void_p(dat.data_ptr()), un)
                 if lib.probe(*args) != 0:
                     continue
