@@ -237,13 +237,18 @@ def build_all_rules(f):
     main = torch.cuda.current_stream()
     sides = _side_streams(len(plans) + len(dplans))
     std, dwq_pending = [], {}
-    tables = []
+    tables, prods = [], []
+    sep = f.strategy != "reference" and f.coeff.identity       # the direction products are needed
     for k, pl in enumerate(plans):
         with _forked(main, sides[k]):
-            out, tab = _solve_rows_async_t(pl)
-            _keep_on(main, out[1:] + (tab or ()))
+            full = pl.rows_h.size == pl.basis.n
+            prod = (torch.empty((pl.basis.n, 2 * pl.basis.p + 1), dtype=torch.float64, device=f.dev)
+                    if sep and full else None)
+            out, tab = _solve_rows_async_t(pl, products=prod)
+            _keep_on(main, out[1:] + (tab or ()) + ((prod,) if prod is not None else ()))
         std.append(out)
         tables.append(tab)
+        prods.append(prod)
     for k, (key, pl) in enumerate(dplans.items()):
         with _forked(main, sides[len(plans) + k]):
             rs, fail = dwq_solve_async(pl, direction=key[0])
@@ -269,6 +274,7 @@ def build_all_rules(f):
             rs = WeightedRuleSet(pl.basis, pl.layout, wptr, k0, w, d)
             if tables[d] is not None:
                 rs._basis_tab = tables[d]      # the fit's own table at the same points
+            rs._products = prods[d]            # direction products written by the solve
             rules.append(rs)
     dwq = {}
     for key, (pl, rs, fail) in dwq_pending.items():
