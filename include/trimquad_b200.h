@@ -202,6 +202,12 @@ int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
  * at work + 2, list B (deep rows with a partial window) at work + 2 + nrows */
 int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream);
 int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream);
+/* tq_row_counts_deep from the geometric flags of tq_deep_geometry and the
+ * per-line factor positivity (computed here into `pos`, n1 + n2 bytes of
+ * caller scratch); c.deep is not read.  The lists then carry the deep /
+ * not-deep split that tq_fill_listed uses, so no deep array is formed. */
+int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* counts, int32_t* work,
+                      void* stream);
 int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
 /* the same with caller scratch of tq_scan_workspace_bytes(nrows) bytes */

@@ -89,6 +89,7 @@ def lib():
         "tq_wq_products": ([Space1D, Layout, vp, vp, Rules, vp, vp], i32),
         "tq_row_counts": ([RowCtx, vp, vp], i32),
         "tq_row_counts_deep": ([RowCtx, vp, vp, vp], i32),
+        "tq_row_counts_geo": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
         "tq_scan_workspace_bytes": ([i32], i64),

@@ -384,16 +384,22 @@ class Formation:
                 L.call("tq_deep_geometry", self.rowctx(), L.ptr(self.config.func_class_dev), L.ptr(self.raw_list),
                        self.raw_list.numel(), L.ptr(geo), L.stream())
                 g[gkey] = (geo, self.raw_list)     # the list is kept alive with its key
-            self.deep = torch.empty(n1 * n2, dtype=torch.int8, device=self.dev)
-            L.call("tq_deep_apply", self.rowctx(row_begin, row_end), L.ptr(g[gkey][0]), L.ptr(self.deep),
-                   L.stream())
+            # the count pass applies the factor positivity inline and hands the
+            # deep / not-deep split to the fill through its row lists: the
+            # context carries the geometric flags, no deep array is formed
+            self.deep = g[gkey][0]
             _stamp("deep_flags")
-        self.rowfast = torch.zeros(max(nrows, 1), dtype=torch.int8, device=self.dev)
+        self.rowfast = torch.empty(max(nrows, 1), dtype=torch.int8, device=self.dev)   # written for every row
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
         work = torch.empty(2 * nrows + 2, dtype=torch.int32, device=self.dev)
         with self.timer("counts"):
-            L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            if self.a1 is not None:
+                pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
+                L.call("tq_row_counts_geo", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(counts), L.ptr(work),
+                       L.stream())
+            else:
+                L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_deep")
             if join is not None:
                 torch.cuda.current_stream().wait_stream(join)

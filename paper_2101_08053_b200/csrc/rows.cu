@@ -120,8 +120,14 @@ __device__ __forceinline__ void entries_batch(const tq_rowctx& c, const RowGeom&
 // counted arithmetically and flagged fast when their window is full; other
 // rows are appended to list A (counted by pass 2), deep rows with a partial
 // window to list B (both lists feed the row-parallel fill).
-__global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int* __restrict__ list,
-                                  int* __restrict__ nlist, int* __restrict__ listb, int* __restrict__ nlistb) {
+// GEO: deep = geo[idx] && pos[i1] && pos[n1 + i2] from the geometric flags
+// and the per-line factor positivity (no deep array is formed); otherwise
+// c.deep holds complete deep flags.
+template <bool GEO>
+__global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, const int8_t* __restrict__ pos,
+                                  int32_t* __restrict__ counts,
+                                  int* __restrict__ list, int* __restrict__ nlist, int* __restrict__ listb,
+                                  int* __restrict__ nlistb) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     // grid-stride loop with a warp-uniform trip count (the appends are warp-aggregated)
@@ -131,8 +137,11 @@ __global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int
         bool to_a = false, to_b = false;
         if (r < c.row_end) {
             const int idx = __ldg(c.active + r);
-            if (c.deep && __ldg(c.deep + idx)) {
-                const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
+            const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
+            bool deep;
+            if (GEO) deep = __ldg(geo + idx) && __ldg(pos + i1) && __ldg(pos + c.n1 + i2);
+            else deep = c.deep && __ldg(c.deep + idx);
+            if (deep) {
                 const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
                 const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
                 counts[r - c.row_begin] = t1 * t2;
@@ -140,6 +149,7 @@ __global__ void k_row_counts_deep(tq_rowctx c, int32_t* __restrict__ counts, int
                 if (c.rowfast) c.rowfast[r - c.row_begin] = full ? 1 : 0;
                 to_b = !(full && c.rowfast);
             } else {
+                if (c.rowfast) c.rowfast[r - c.row_begin] = 0;
                 to_a = true;
             }
         }
@@ -380,7 +390,9 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
         RowGeom g = row_geom(c, r);
         int pos = __ldg(indptr + (r - c.row_begin));
         const int n = g.t1 * g.t2;
-        if (c.deep[c.active[r]]) {
+        // deep rows: list B when the count pass gave the lists, else the flags
+        const bool deep_row = irr_rows_b ? u >= na : c.deep[c.active[r]] != 0;
+        if (deep_row) {
             double A1 = 0.0, A1T = 0.0, A2 = 0.0, A2T = 0.0;
             int CB = 0;
             if (lane < W) {
@@ -525,9 +537,25 @@ extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, v
     int nrows = c.row_end - c.row_begin;
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
-    k_row_counts_deep<<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, counts, work + 2, work, work + 2 + nrows,
-                                                                    work + 1); ::tq::note_launch();
+    k_row_counts_deep<false><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, nullptr, nullptr, counts, work + 2, work,
+                                                                           work + 2 + nrows, work + 1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_deep");
+    return TQ_OK;
+}
+
+// as tq_row_counts_deep, from the geometric deep flags of tq_deep_geometry
+// and the per-line factor positivity (k_pos2 of a1, a2; c.deep is not read).
+// `pos`: caller scratch of n1 + n2 bytes.
+extern "C" int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* counts, int32_t* work,
+                                 void* stream) {
+    int nrows = c.row_end - c.row_begin;
+    TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
+    if (nrows <= 0) return TQ_OK;
+    if (!c.a1 || !c.a2) { set_error("tq_row_counts_geo needs the separable factors"); return TQ_EINVAL; }
+    k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos); ::tq::note_launch();
+    k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
+                                                                          work + 2 + nrows, work + 1); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_geo");
     return TQ_OK;
 }
 
