@@ -13,6 +13,7 @@ Every raw row also collects the cut-element points (``tq_raw_cutcells``).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -465,7 +466,8 @@ _NAMED = {}
 
 def _named_stream(name, priority=0):
     """Cached side stream.  Priorities (lower = more urgent): fit chains -3,
-    the captured main chain -2, the bulk pass-start streams 0."""
+    the captured main chain and the Gauss part of the raw rows -2, the
+    cut-element tables and blocks 0."""
     dev = torch.cuda.current_device()
     key = (dev, name)
     if key not in _NAMED:
@@ -482,7 +484,8 @@ def prelaunch_geometry(f):
     if not needs_raw(f):
         return
     _bind()
-    s = _named_stream("cut_blocks")
+    # priority of the main chain: the Gauss part gates the cut-row chain (measured best)
+    s = _named_stream("cut_blocks", priority=-2)
     main = torch.cuda.current_stream()
     with _forked(main, s):
         f._elem_pre = eg, em, cg = _elem_tables(f)
@@ -695,14 +698,16 @@ def run_phase(f, phase):
             g[skey] = (slot, f._desc[:, 0].contiguous())
         f.slot, f.raw_list = g[skey]
         f._ctx = f._setup.ctx(f._desc, f.raw, desc.shape[0])
-        if pre is not None:
-            torch.cuda.current_stream().wait_event(f._elem_event)   # Gauss part from the pass-start stream
         if nint:
+            if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
+                torch.cuda.current_stream().wait_event(f._elem_event)
             L.call("tq_raw_sumfactor" if pre is not None else "tq_raw_regular", f._ctx, 0, nint, L.stream())
     elif phase == "cut":
         if f._ndesc > f._nint:
-            L.call("tq_raw_sumfactor" if getattr(f, "_raw_pre", None) is not None else "tq_raw_regular",
-                   f._ctx, f._nint, f._ndesc, L.stream())
+            pre = getattr(f, "_raw_pre", None) is not None
+            if pre:
+                torch.cuda.current_stream().wait_event(f._elem_event)
+            L.call("tq_raw_sumfactor" if pre else "tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells":
         if f._setup.cut is not None:
             if getattr(f, "_cut_pre", None) is None:
