@@ -465,9 +465,9 @@ _NAMED = {}
 
 
 def _named_stream(name, priority=0):
-    """Cached side stream.  Priorities (lower = more urgent): fit chains -3,
-    the captured main chain and the Gauss part of the raw rows -2, the
-    cut-element tables and blocks 0."""
+    """Cached side stream.  Priorities (lower = more urgent): fit chains -3;
+    the captured main chain and the pass-start streams (Gauss part of the raw
+    rows, cut-element blocks: both gate the cut-row chain) -2."""
     dev = torch.cuda.current_device()
     key = (dev, name)
     if key not in _NAMED:
@@ -498,7 +498,7 @@ def prelaunch_geometry(f):
         f._elem_event = torch.cuda.Event()
         f._elem_event.record()
     # cut-element tables and blocks: an independent chain on a second stream
-    s2 = _named_stream("cut_blocks2")
+    s2 = _named_stream("cut_blocks2", priority=-2)
     cut = None
     with _forked(main, s2):
         if f.config.has_cuts():
