@@ -13,7 +13,6 @@ Every raw row also collects the cut-element points (``tq_raw_cutcells``).
 from __future__ import annotations
 
 import ctypes as C
-import os
 
 import numpy as np
 import torch
