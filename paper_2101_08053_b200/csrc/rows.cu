@@ -61,11 +61,14 @@ __device__ inline RowGeom row_geom(const tq_rowctx& c, int r) {
     return g;
 }
 
-// unsymmetrised value of row (i1,i2) at column (j1,j2)
+// unsymmetrised value of row (i1,i2) at column (j1,j2).  Every symmetrised
+// entry is formed as round(round(M_ij) + round(M_ji)) -- explicitly rounded
+// products and sum, never contracted into an FMA -- so M_ij and M_ji are
+// the same double (the reference's 0.5 (M + M^T) is exactly symmetric).
 __device__ __forceinline__ double raw_value(const tq_rowctx& c, int i1, int i2, int s_i, int j1, int j2) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
     const int o1 = j1 - i1 + c.p1, o2 = j2 - i2 + c.p2;
-    if (s_i < 0) return __ldg(c.a1 + (int64_t)i1 * W1 + o1) * __ldg(c.a2 + (int64_t)i2 * W2 + o2);
+    if (s_i < 0) return __dmul_rn(__ldg(c.a1 + (int64_t)i1 * W1 + o1), __ldg(c.a2 + (int64_t)i2 * W2 + o2));
     return __ldg(c.raw + (int64_t)s_i * (W1 * W2) + o1 * W2 + o2);
 }
 
@@ -77,7 +80,7 @@ __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e
     int col = __ldg(c.col_of + jidx);
     if (col < 0) return -1;
     int s_j = __ldg(c.slot + jidx);
-    v = raw_value(c, g.i1, g.i2, g.s_i, j1, j2) + raw_value(c, j1, j2, s_j, g.i1, g.i2);
+    v = __dadd_rn(raw_value(c, g.i1, g.i2, g.s_i, j1, j2), raw_value(c, j1, j2, s_j, g.i1, g.i2));
     return v != 0.0 ? col : -1;
 }
 
@@ -109,7 +112,7 @@ __device__ __forceinline__ void entries_batch(const tq_rowctx& c, const RowGeom&
         col[u] = -1;
         v[u] = 0.0;
         if (cl[u] >= 0) {
-            const double w = vi[u] + raw_value(c, j1[u], j2[u], sj[u], g.i1, g.i2);
+            const double w = __dadd_rn(vi[u], raw_value(c, j1[u], j2[u], sj[u], g.i1, g.i2));
             v[u] = w;
             col[u] = w != 0.0 ? cl[u] : -1;
         }
@@ -289,7 +292,7 @@ __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S,
                 if (act && q1 < W) {
                     const int e = tt * WW + q1 * W + q2;
                     st.x[offx + e] = rcb[m] + t + q2;
-                    st.d[offd + e] = 0.5 * (rl1[m] * a2 + rl1t[m] * a2t);
+                    st.d[offd + e] = 0.5 * __dadd_rn(__dmul_rn(rl1[m], a2), __dmul_rn(rl1t[m], a2t));
                 }
             }
         }
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
                 const int cb = __shfl_sync(0xffffffffu, CB, o1);
                 if (e < n) {
                     indices[pos + e] = cb + q2;
-                    data[pos + e] = 0.5 * (a1 * a2 + a1t * a2t);
+                    data[pos + e] = 0.5 * __dadd_rn(__dmul_rn(a1, a2), __dmul_rn(a1t, a2t));
                 }
             }
         } else {
