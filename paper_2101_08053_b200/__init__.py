@@ -7,7 +7,7 @@ The public names mirror the reference package ``trimquad``
 (src/__init__.py:8-32).
 """
 
-from .splines import (Basis1D, KnotVector, SubdivisionMatrix, TensorBasis2D, insert_knot,
+from .splines import (Basis1D, KnotVector, SubdivisionMatrix, TensorBasis2D, insert_knot, subdivision_matrix_to,
                       make_uniform_basis, make_uniform_knots)
 from .quadrature import (DiscontinuousRuleSet, GaussRule, PointLayout, RuleConstructionError,
                          WeightedRuleSet, build_dwq, compute_wq_rules, exact_moments, gauss_legendre,

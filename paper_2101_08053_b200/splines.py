@@ -299,6 +299,39 @@ def _insertion_matrix(kn, p, ubar):
     return np.insert(kn, at, ubar), S
 
 
+def _multiset_difference(a, b, tol=KNOT_TOL):
+    """Values of the sorted knot sequence ``a`` not matched by ``b`` (multiset
+    semantics within the knot tolerance): a two-pointer walk over the two
+    sorted sequences."""
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    out, j = [], 0
+    for v in a:
+        while j < b.size and b[j] < v - tol:
+            j += 1
+        if j < b.size and abs(b[j] - v) <= tol:
+            j += 1
+        else:
+            out.append(v)
+    return np.asarray(out, float)
+
+
+def subdivision_matrix_to(basis: Basis1D, target_knots) -> SubdivisionMatrix:
+    """Composite subdivision map onto a nested, finer knot vector of the same
+    degree (src/splines.py:406-428): the product of single knot insertions,
+    in ascending order of the missing knots.  ``target_knots``: a KnotVector
+    or a knot sequence; it must contain the source knots as a multiset."""
+    target = target_knots if isinstance(target_knots, KnotVector) else KnotVector(target_knots, basis.p)
+    if target.degree != basis.p:
+        raise ValueError("target knot vector must have the same degree")
+    if _multiset_difference(basis.kv.knots, target.knots).size:
+        raise ValueError("target knot vector is not a refinement of the source")
+    current, S = basis, sp.identity(basis.n, format="csr")
+    for ubar in _multiset_difference(target.knots, basis.kv.knots):
+        current, step = insert_knot(current, float(ubar))
+        S = step.matrix @ S
+    return SubdivisionMatrix(S, basis, current)
+
+
 def refine_to_c_minus_1(basis: Basis1D, u: float):
     """Insert u up to multiplicity p+1 -> (refined basis, SubdivisionMatrix);
     the composite of single insertions (src/splines.py:406-428)."""
