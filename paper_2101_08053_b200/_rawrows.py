@@ -116,30 +116,41 @@ def cut_point_tables(f):
         else:
             P = L.dev(rule.points.reshape(-1, 2), torch.float64)
             Wd, ptr_d = L.dev(rule.weights, torch.float64), L.dev(rule.ptr, torch.int64)
-        cutidx = np.full(b1.num_elements * b2.num_elements, -1, np.int32)
-        cutidx[rule.elements[:, 0] * b2.num_elements + rule.elements[:, 1]] = np.arange(rule.elements.shape[0])
+        dev = f.dev
+        ncut = rule.elements.shape[0]
+        el = ddev["el"] if ddev is not None else L.dev(rule.elements.astype(np.int32).reshape(-1, 2), torch.int32)
+        cutidx = torch.full((b1.num_elements * b2.num_elements,), -1, dtype=torch.int32, device=dev)
+        if ncut:
+            cutidx[el[:, 0].long() * b2.num_elements + el[:, 1].long()] = torch.arange(
+                ncut, dtype=torch.int32, device=dev)
         t = dict(P=P, x=P[:, 0].contiguous(), y=P[:, 1].contiguous(),
-                 W=Wd, idx=L.dev(cutidx, torch.int32), ptr=ptr_d, npts=rule.total_points())
+                 W=Wd, idx=cutidx, ptr=ptr_d, npts=rule.total_points())
         # span-key groups per cut element (src/assembly.py:380-388): points of
-        # one element grouped by (first1, first2), keys in np.unique order
+        # one element grouped by (first1, first2), keys in np.unique order --
+        # a stable sort by (element, key) on the device (= np.lexsort with the
+        # point index as the last key)
         f1, _ = b1.eval_device(t["x"], check=False)
         f2, _ = b2.eval_device(t["y"], check=False)
-        f1, f2 = f1.cpu().numpy().astype(np.int64), f2.cpu().numpy().astype(np.int64)
-        ncut = rule.elements.shape[0]
-        elem = np.repeat(np.arange(ncut), np.diff(rule.ptr))
-        key = f1 * (b2.n + 1) + f2
-        perm = np.lexsort((np.arange(key.size), key, elem))      # stable: element, then key
-        ek = np.stack([elem[perm], key[perm]], axis=1)
-        start = np.nonzero(np.r_[True, np.any(ek[1:] != ek[:-1], axis=1)])[0] if key.size else np.zeros(0, int)
-        gpts = np.r_[start, key.size].astype(np.int64)
+        npts = int(t["npts"])
+        elem = torch.repeat_interleave(torch.arange(ncut, device=dev), (ptr_d[1:] - ptr_d[:-1]).long())
+        key = f1.long() * (b2.n + 1) + f2.long()
+        comp = elem * (b1.n * (b2.n + 1) + b2.n + 1) + key
+        comp_s, perm = torch.sort(comp, stable=True)
+        if npts:
+            first = torch.ones(npts, dtype=torch.bool, device=dev)
+            first[1:] = comp_s[1:] != comp_s[:-1]
+            start = torch.nonzero(first).flatten()
+        else:
+            start = torch.zeros(0, dtype=torch.int64, device=dev)
+        gpts = torch.cat([start, torch.tensor([npts], dtype=torch.int64, device=dev)])
         gelem = elem[perm][start]
-        gptr = np.searchsorted(gelem, np.arange(ncut + 1), side="left").astype(np.int32)
-        gkey = np.stack([f1[perm][start], f2[perm][start]], axis=1).astype(np.int32)
-        t["grp_ptr"] = L.dev(gptr, torch.int32)
-        t["grp_key"] = L.dev(gkey.reshape(-1, 2), torch.int32)
-        t["grp_pts"] = L.dev(gpts, torch.int64)
-        t["grp_perm"] = L.dev(perm.astype(np.int64) if perm.size else np.zeros(1, np.int64), torch.int64)
-        t["ngroups"] = int(start.size)
+        gptr = torch.searchsorted(gelem, torch.arange(ncut + 1, device=dev), right=False).to(torch.int32)
+        gkey = torch.stack([f1[perm][start], f2[perm][start]], dim=1).to(torch.int32).contiguous()
+        t["grp_ptr"] = gptr
+        t["grp_key"] = gkey
+        t["grp_pts"] = gpts.contiguous()
+        t["grp_perm"] = perm.contiguous() if npts else torch.zeros(1, dtype=torch.int64, device=dev)
+        t["ngroups"] = int(start.numel())
         g["cutpts"] = t
         g["cutpts_src"] = rule
     return g["cutpts"]
@@ -166,17 +177,19 @@ def dwq_keys(f):
     g = _geo(f.config)
     if "dwq_keys" not in g:
         cut, routes = route_cut_rows(f)
-        needed = {}
         n2 = f.b2.n
-        for fid, rt in zip(cut, routes):
-            if rt[0] != 1 or rt[3] < 0:
+        box = (routes[:, 0] == 1) & (routes[:, 3] >= 0)
+        ij = (cut.astype(np.int64) // n2, cut.astype(np.int64) % n2)
+        needed = {}
+        for d in (0, 1):
+            iu = routes[:, 1 + d]
+            sel = box & (iu >= 0)
+            if not np.any(sel):
                 continue
-            ij = (int(fid) // n2, int(fid) % n2)
-            for d in (0, 1):
-                iu = rt[1 + d]
-                if iu >= 0:
-                    needed.setdefault((d, float(f.config.u_disc[d][iu])), set()).add(ij[d])
-        g["dwq_keys"] = {k: sorted(v) for k, v in sorted(needed.items())}
+            pairs = np.unique(np.stack([iu[sel], ij[d][sel]], axis=1), axis=0)   # (u index, row), sorted
+            for k in np.unique(pairs[:, 0]):
+                needed[(d, float(f.config.u_disc[d][k]))] = pairs[pairs[:, 0] == k, 1].tolist()
+        g["dwq_keys"] = {k: v for k, v in sorted(needed.items())}
     return g["dwq_keys"]
 
 
