@@ -338,14 +338,57 @@ def refine_to_c_minus_1(basis: Basis1D, u: float):
     kv = basis.kv
     if not (kv.domain[0] <= u <= kv.domain[1]):
         raise ValueError(f"insertion point {u} outside domain {kv.domain}")
-    kn = kv.knots
-    p = basis.p
-    S = sp.identity(basis.n, format="csr")
-    for _ in range(p + 1 - kv.multiplicity_of(u)):
-        kn, step = _insertion_matrix(kn, p, u)
-        S = step @ S
-    fine = Basis1D(KnotVector(kn, p))
+    kn, S = _repeated_insertion(kv.knots, basis.p, u, basis.p + 1 - kv.multiplicity_of(u))
+    fine = Basis1D(KnotVector(kn, basis.p))
     return fine, SubdivisionMatrix(S, basis, fine)
+
+
+def _repeated_insertion(kn, p, u, r):
+    """Composite of r insertions of the same knot u (the product of the
+    single-insertion maps of _insertion_matrix, bit-identical).  Outside a
+    window around u the map is the identity above and an identity shifted by
+    r below, so only that window is composed, densely: a step's new row k is
+    alpha_k row_k + (1 - alpha_k) row_{k-1}, the two-term sum of the sparse
+    product."""
+    kn = np.asarray(kn, float)
+    n = kn.size - p - 1
+    if r <= 0:
+        return kn.copy(), sp.identity(n, format="csr")
+    l0 = int(np.clip(np.searchsorted(kn, u, side="right") - 1, p, n - 1))
+    lo = max(l0 - p, 0)
+    w = l0 - lo + 1
+    B = np.eye(w)                        # rows = coefficients lo .., cols = source lo .. l0
+    for _ in range(r):
+        nc = kn.size - p - 1
+        l = int(np.clip(np.searchsorted(kn, u, side="right") - 1, p, nc - 1))
+        nb = B.shape[0]
+        new = np.zeros((nb + 1, w))
+        for k in range(nb + 1):
+            g = lo + k                   # global coefficient index after the insertion
+            if g <= l - p:
+                new[k] = B[k]
+            elif g >= l + 1:
+                new[k] = B[k - 1]
+            else:
+                a = (u - kn[g]) / (kn[g + p] - kn[g])
+                new[k] = a * B[k] + (1.0 - a) * B[k - 1]
+        B = new
+        kn = np.insert(kn, int(np.searchsorted(kn, u, side="right")), u)
+    nb = B.shape[0]
+    rows = [np.arange(lo)]
+    cols = [np.arange(lo)]
+    vals = [np.ones(lo)]
+    bi, bj = np.nonzero(B)
+    rows.append(lo + bi)
+    cols.append(lo + bj)
+    vals.append(B[bi, bj])
+    tail = np.arange(lo + nb, n + r)
+    rows.append(tail)
+    cols.append(tail - r)
+    vals.append(np.ones(tail.size))
+    S = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n + r, n))
+    S.sort_indices()
+    return kn, S
 
 
 def make_uniform_knots(num_elements, degree, a=0.0, b=1.0):

@@ -44,3 +44,28 @@ def test_subdivision_rejects_non_refinements():
         S.subdivision_matrix_to(b, S.make_uniform_knots(3, 2))     # drops interior knots
     with pytest.raises(ValueError):
         S.subdivision_matrix_to(b, S.make_uniform_knots(8, 3))     # other degree
+
+
+@pytest.mark.parametrize("p,nel", [(1, 5), (2, 7), (3, 9), (4, 12), (6, 10)])
+def test_repeated_insertion_equals_product_of_single_insertions(p, nel):
+    """refine_to_c_minus_1 composes the insertions in a window; it must be
+    bit-identical to the product of the single-insertion maps."""
+    import scipy.sparse as sp
+    from paper_2101_08053_b200 import splines as S
+    b = S.make_uniform_basis(nel, p)
+    rng = np.random.default_rng(p)
+    bps = b.breakpoints[1:-1]
+    for u in list(rng.choice(bps, size=min(3, bps.size), replace=False)) + [0.0, 1.0, float(bps[0])]:
+        fine, sub = S.refine_to_c_minus_1(b, float(u))
+        kn, M = b.kv.knots, sp.identity(b.n, format="csr")
+        for _ in range(p + 1 - b.kv.multiplicity_of(float(u))):
+            kn, step = S._insertion_matrix(kn, p, float(u))
+            M = step @ M
+        M.eliminate_zeros()
+        M.sort_indices()              # the sparse product leaves rows unsorted
+        A = sub.matrix.tocsr()
+        A.eliminate_zeros()
+        A.sort_indices()
+        assert np.array_equal(fine.kv.knots, kn)
+        assert np.array_equal(A.indptr, M.indptr) and np.array_equal(A.indices, M.indices)
+        assert np.array_equal(A.data, M.data)
