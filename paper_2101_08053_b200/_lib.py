@@ -136,7 +136,7 @@ class Stamps:
     """Timeline probe (TQ_STAMPS=1): device global-timer stamps recorded in
     stream order at named points; ``report()`` gives µs from the first."""
 
-    def __init__(self, n=64):
+    def __init__(self, n=1024):
         self.buf = torch.zeros(n, dtype=torch.int64, device=device())
         self.names = []
 

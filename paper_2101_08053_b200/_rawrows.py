@@ -12,6 +12,7 @@ Every raw row also collects the cut-element points (``tq_raw_cutcells``).
 
 from __future__ import annotations
 
+import os
 import ctypes as C
 
 import numpy as np
@@ -19,7 +20,7 @@ import torch
 
 from . import _lib as L
 from ._lib import CUT, INTERIOR
-from .quadrature import (DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async_t, build_dwq,
+from .quadrature import (_TAG as _QT, _st, DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async_t, build_dwq,
                          compute_wq_rules, dwq_solve_async, gauss_legendre, place_wq_points)
 
 MODE_GAUSS, MODE_BOX, MODE_MASK = 0, 1, 2
@@ -202,7 +203,7 @@ def _side_streams(n):
     while len(lst) < n:
         # high priority: the fit chains are short latency-bound kernels that
         # must not queue behind the bulk raw-row work of the pass-start stream
-        lst.append(torch.cuda.Stream(priority=-3))
+        lst.append(torch.cuda.Stream(priority=int(os.environ.get("TQ_PRIO_FITS", -3))))
     return lst[:n]
 
 
@@ -254,6 +255,7 @@ def build_all_rules(f):
     sep = f.strategy != "reference" and f.coeff.identity       # the direction products are needed
     for k, pl in enumerate(plans):
         with _forked(main, sides[k]):
+            _QT[0] = f"s{k}:"
             full = pl.rows_h.size == pl.basis.n
             prod = (torch.empty((pl.basis.n, 2 * pl.basis.p + 1), dtype=torch.float64, device=f.dev)
                     if sep and full else None)
@@ -264,14 +266,18 @@ def build_all_rules(f):
         prods.append(prod)
     for k, (key, pl) in enumerate(dplans.items()):
         with _forked(main, sides[len(plans) + k]):
+            _QT[0] = f"d{k}:"
             rs, fail = dwq_solve_async(pl, direction=key[0])
             # basis table of the set's own basis at its points (geometry-only;
             # built here so it overlaps the fits)
             tab = rs.basis_table()
+            _st("table")
             _keep_on(main, (rs.w, fail) + tuple(tab))
         dwq_pending[key] = (pl, rs, fail)
+    _QT[0] = ""
     for st in sides:
         main.wait_stream(st)
+    _st("fits_joined")
     flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
     flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]
     if f.capture is not None:     # graph capture: flags checked after each replay
@@ -483,6 +489,7 @@ def _named_stream(name, priority=0):
     dev = torch.cuda.current_device()
     key = (dev, name)
     if key not in _NAMED:
+        priority = int(os.environ.get("TQ_PRIO_" + name.upper(), priority))   # tuning knob
         _NAMED[key] = torch.cuda.Stream(priority=priority)
     return _NAMED[key]
 
@@ -501,12 +508,14 @@ def prelaunch_geometry(f):
     main = torch.cuda.current_stream()
     with _forked(main, s):
         f._elem_pre = eg, em, cg = _elem_tables(f)
+        _st("preA:elem")
         desc_dev, ndesc = _desc_dev(f)
         f._desc_pre = desc_dev
         W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
         f._raw_pre = torch.empty((max(ndesc, 1), W), dtype=torch.float64, device=f.dev)
         if ndesc:
             L.call("tq_raw_gauss", _gauss_ctx(f, eg, em, cg, desc_dev, f._raw_pre, ndesc), 0, ndesc, L.stream())
+        _st("preA:gauss")
         f._elem_event = torch.cuda.Event()
         f._elem_event.record()
     # cut-element tables and blocks: an independent chain on a second stream
@@ -515,6 +524,7 @@ def prelaunch_geometry(f):
     with _forked(main, s2):
         if f.config.has_cuts():
             cut = _cut_tables(f)
+            _st("preB:tables")
             L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.stream())
         from .assembly import _stamp
         _stamp("cutpre:blocks")

@@ -175,21 +175,47 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
     }
 }
 
+// warp per wanted row, lane per output weight: each lane accumulates its
+// weight over the S entries of the row in entry order (the same additions,
+// in the same order, as a serial dst[q] += s_ij w~ loop -- bit-identical),
+// in a register instead of through memory.
 __global__ void k_dwq_combine(const int32_t* __restrict__ rows, int nrows, const int32_t* __restrict__ colptr,
                               const int32_t* __restrict__ rowidx, const double* __restrict__ sval,
                               tq_rules fine, tq_rules out) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
-        int j = rows[r];
-        int64_t o0 = out.wptr[j], o1 = out.wptr[j + 1];
-        int k0 = out.k0[j];
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < nrows; r += nwarps) {
+        const int j = rows[r];
+        const int64_t o0 = out.wptr[j];
+        const int len = (int)(out.wptr[j + 1] - o0), k0 = out.k0[j];
+        const int c0 = colptr[j], nent = colptr[j + 1] - c0;
         double* dst = const_cast<double*>(out.w) + o0;
-        for (int64_t q = 0; q < o1 - o0; ++q) dst[q] = 0.0;
-        for (int q = colptr[j]; q < colptr[j + 1]; ++q) {
-            int i = rowidx[q];
-            double sij = sval[q];
-            int fk0 = fine.k0[i];
-            int64_t f0 = fine.wptr[i], f1 = fine.wptr[i + 1];
-            for (int64_t kk = 0; kk < f1 - f0; ++kk) dst[fk0 - k0 + kk] += sij * fine.w[f0 + kk];
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            const int q = q0 + lane;
+            double acc = 0.0;
+            for (int e0 = 0; e0 < nent; e0 += 32) {
+                // the row's S entries and their fine rows, one per lane
+                int fi = 0, fk0 = 0, flen = 0;
+                int64_t f0 = 0;
+                double sij = 0.0;
+                if (e0 + lane < nent) {
+                    fi = rowidx[c0 + e0 + lane];
+                    sij = sval[c0 + e0 + lane];
+                    fk0 = fine.k0[fi];
+                    f0 = fine.wptr[fi];
+                    flen = (int)(fine.wptr[fi + 1] - f0);
+                }
+                const int ne = min(32, nent - e0);
+                for (int e = 0; e < ne; ++e) {
+                    const double s_e = __shfl_sync(0xffffffffu, sij, e);
+                    const int off = __shfl_sync(0xffffffffu, fk0, e) - k0;
+                    const int fl = __shfl_sync(0xffffffffu, flen, e);
+                    const int64_t fb = __shfl_sync(0xffffffffu, f0, e);
+                    const int kk = q - off;
+                    if (q < len && kk >= 0 && kk < fl) acc += s_e * fine.w[fb + kk];
+                }
+            }
+            if (q < len) dst[q] = acc;
         }
     }
 }
@@ -220,8 +246,9 @@ extern "C" int tq_dwq_combine(const int32_t* rows, int32_t nrows, const int32_t*
                               const int32_t* s_rowidx, const double* s_val, tq_rules fine,
                               tq_rules out_rules, void* stream) {
     if (nrows == 0) return TQ_OK;
-    k_dwq_combine<<<grid_for(nrows, 64), 64, 0, S(stream)>>>(rows, nrows, s_colptr, s_rowidx, s_val,
-                                                             fine, out_rules); ::tq::note_launch();
+    k_dwq_combine<<<grid_for((int64_t)nrows * 32, 128), 128, 0, S(stream)>>>(rows, nrows, s_colptr, s_rowidx,
+                                                                              s_val, fine, out_rules);
+    ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_dwq_combine");
     return TQ_OK;
 }

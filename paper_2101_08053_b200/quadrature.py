@@ -141,6 +141,15 @@ def place_wq_points(basis: Basis1D) -> PointLayout:
     return _layout_from_counts(basis, _required_counts(basis))
 
 
+_TAG = [""]     # timeline probe: prefix of the fit-chain stamps
+
+
+def _st(name):
+    from . import assembly as A
+    if A.STAMPS is not None:
+        A.STAMPS(_TAG[0] + name)
+
+
 def moments_device(basis: Basis1D):
     """Banded exact 1-D mass matrix on the GPU, n x (2p+1); recomputed on
     every call like mass_matrix_1d inside the reference's _solve_rows."""
@@ -278,11 +287,14 @@ def _solve_rows_async_t(plan: _FitPlan, init=None, products=None):
     tab = None
     if plan.rows_h.size:
         tab = basis.eval_device(layout.device_points(), check=False)
+        _st("eval")
         first, vals = tab
         mom = moments_device(basis)
+        _st("mom")
         L.call("tq_wq_solve", basis.device(), layout.device(), L.ptr(first), L.ptr(vals), L.ptr(mom),
                L.ptr(plan.rows), plan.rows_h.size, plan.tmax, plan.mmax, L.ptr(plan.wptr), L.ptr(k0), L.ptr(w),
                L.ptr(fail), L.ptr(products), L.stream())
+        _st("solve")
     return (plan.wptr, k0, w, fail), tab
 
 
@@ -436,6 +448,7 @@ def dwq_solve_async(plan: DwqPlan, direction=None, regular_side=None):
     L.call("tq_dwq_combine", L.ptr(plan.rows), plan.wanted.size, L.ptr(plan.cp), L.ptr(plan.ri), L.ptr(plan.sv),
            L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)), L.Rules(L.ptr(plan.wptr), L.ptr(plan.k0), L.ptr(w)),
            L.stream())
+    _st("combine")
     rs = DiscontinuousRuleSet(plan.basis, plan.aug, plan.wptr, plan.k0, w, plan.u, plan.S, plan.refined,
                               plan.base_layout, direction, regular_side)
     return rs, fail
