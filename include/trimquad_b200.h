@@ -179,7 +179,21 @@ typedef struct {
     int8_t* rowfast;             /* per active row (written by tq_row_counts):
                                     deep with full (2p+1)^2 windows */
     int32_t row_begin, row_end;  /* active rows [begin, end) */
+    /* optional (NULL: the fill reads a complete indptr): per-row counts and
+       per-32-row tile sums.  The count passes write the tile sums,
+       tq_scan_tiles turns them into tile bases in place, and the fill kernels
+       then derive each row's offset from its tile base and the counts before
+       it in the tile, writing indptr[0 .. nrows) themselves. */
+    const int32_t* counts;
+    int32_t* tiles;              /* TQ_TILE_INTS(nrows) ints: the sums, then
+                                    the bases (tq_tile_bases) */
 } tq_rowctx;
+
+/* tile-mode buffer: ntiles sums (padded to a multiple of 4 for vector
+   loads), then ntiles bases, the total and an overflow flag */
+#define TQ_TILE_PAD(nrows) ((((nrows) + 31) / 32 + 3) / 4 * 4)
+#define TQ_TILE_INTS(nrows) (TQ_TILE_PAD(nrows) + ((nrows) + 31) / 32 + 2)
+static inline int32_t* tq_tile_bases(int32_t* tiles, int32_t nrows) { return tiles + TQ_TILE_PAD(nrows); }
 
 /* deep-row flags: deep[i] = separable(i) && no raw row in window(i) &&
  * positive direction factors (the fill then needs no per-entry gathers) */
@@ -214,13 +228,18 @@ int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
 int64_t tq_scan_workspace_bytes(int32_t nrows);
 int tq_scan_indptr_ws(const int32_t* counts, int32_t nrows, int32_t* indptr, void* ws,
                       int64_t* nnz_h, void* stream);
+/* tile mode (c.counts, c.tiles set, after the count passes): exclusive scan
+ * of the tile sums -> tile bases (second half of c.tiles); indptr[nrows] = nnz.  nnz_h: as
+ * tq_scan_indptr.  The fill kernels then write indptr[0 .. nrows). */
+int tq_scan_tiles(tq_rowctx c, int32_t* indptr, int64_t* nnz_h, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                  void* stream);
 /* tq_fill_rows split in two after tq_row_counts_deep/_rest: tq_fill_fast
  * writes the fast rows (every row when the context has no separable
  * factors), tq_fill_listed the rows of lists A and B in `work`.  They write
- * disjoint rows and may run concurrently on two streams. */
-int tq_fill_fast(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data, void* stream);
+ * disjoint rows and may run concurrently on two streams.  In tile mode
+ * tq_fill_fast also writes indptr[0 .. nrows) (every row's offset). */
+int tq_fill_fast(tq_rowctx c, int32_t* indptr, int32_t* indices, double* data, void* stream);
 int tq_fill_listed(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                    const int32_t* work, void* stream);
 

@@ -63,7 +63,7 @@ class RowCtx(C.Structure):
     _fields_ = [("n1", i32), ("n2", i32), ("p1", i32), ("p2", i32),
                 ("ov_lo1", vp), ("ov_hi1", vp), ("ov_lo2", vp), ("ov_hi2", vp),
                 ("col_of", vp), ("active", vp), ("slot", vp), ("a1", vp), ("a2", vp), ("raw", vp),
-                ("deep", vp), ("rowfast", vp), ("row_begin", i32), ("row_end", i32)]
+                ("deep", vp), ("rowfast", vp), ("row_begin", i32), ("row_end", i32), ("counts", vp), ("tiles", vp)]
 
 
 _lib = None
@@ -95,6 +95,7 @@ def lib():
         "tq_scan_workspace_bytes": ([i32], i64),
         "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_scan_tiles": ([RowCtx, vp, C.POINTER(i64), vp], i32),
         "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_fill_listed": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),
@@ -157,6 +158,16 @@ def device():
 
 def stream():
     return vp(torch.cuda.current_stream().cuda_stream)
+
+
+def tile_pad(nrows):
+    """TQ_TILE_PAD of the header: tile sums (padded), then the bases."""
+    return ((nrows + 31) // 32 + 3) // 4 * 4
+
+
+def tile_ints(nrows):
+    """TQ_TILE_INTS: ints of a tile-mode buffer (tq_rowctx.tiles)."""
+    return tile_pad(nrows) + (nrows + 31) // 32 + 2
 
 
 def ptr(t):

@@ -362,7 +362,7 @@ class Formation:
         L.call("tq_fill_fast", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
         main.wait_stream(side)
         if not torch.cuda.is_current_stream_capturing():
-            for t in (indptr, indices, data, self.work):
+            for t in (indptr, indices, data, self.work) + self._count_bufs:
                 t.record_stream(side)
 
     def finish(self, row_begin=0, row_end=None, join=None) -> DeviceCSR:
@@ -393,6 +393,11 @@ class Formation:
         ctx = self.rowctx(row_begin, row_end)
         counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
         work = torch.empty(2 * nrows + 2, dtype=torch.int32, device=self.dev)
+        # tile mode: the count passes leave per-32-row sums, one small scan
+        # turns them into bases and the fill derives (and writes) indptr
+        tiles = torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=self.dev)
+        ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
+        self._count_bufs = (counts, tiles)
         with self.timer("counts"):
             if self.a1 is not None:
                 pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
@@ -409,8 +414,7 @@ class Formation:
         indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
         with self.timer("scan"):
-            L.call("tq_scan_indptr", L.ptr(counts), nrows, L.ptr(indptr),
-                   None if self.capture else L.C.byref(nnz), L.stream())
+            L.call("tq_scan_tiles", ctx, L.ptr(indptr), None if self.capture else L.C.byref(nnz), L.stream())
         _stamp("scan")
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)

@@ -79,13 +79,19 @@ __global__ void k_elem_mass(const double* __restrict__ ev, const double* __restr
 // rules), 2 = sum-factorization part only (adds onto the stored block),
 // 3 = both.  Split or fused, each entry sees the same additions in the same
 // order, so the results are bit-identical.
+// doubles per warp for the staged element window (em slices, spans, flags)
+__host__ __device__ inline int regular_window_slots(int p1, int p2) {
+    const int q1 = p1 + 1, q2 = p2 + 1;
+    return q1 * q1 + q2 * q2 + (q1 + q2 + q1 * q2 + 1) / 2 + 1;
+}
+
 template <int PARTS>
 __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
     const int ni = c.nmax1 > c.p1 + 1 ? c.nmax1 : c.p1 + 1;    // inner rows (sum factorization / Gauss stage 1)
-    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * ni + W1 + W2;
+    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * ni + W1 + W2 + regular_window_slots(c.p1, c.p2);
     double* blk = sm + (size_t)wib * per;
     double* B1 = blk + T;
     double* B2 = B1 + c.nmax1 * W1;
@@ -93,6 +99,12 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     double* S1 = inner + W2 * ni;
     double* S2 = S1 + W1;
     const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+    // element window of the c == 1 Gauss stage
+    double* E1 = S2 + W2;
+    double* E2 = E1 + q1 * q1;
+    int* F1 = reinterpret_cast<int*>(E2 + q2 * q2);
+    int* F2 = F1 + q1;
+    int* MK = F2 + q2;
 
     for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
         RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
@@ -113,21 +125,41 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
             //   blk[o1][o2]   = sum_k1 em1[e1][a1][b1(o1)] inner[k1][o2]
             // (dependency chains of <= p+1 terms instead of a warp-serial
             // loop over the elements; same terms, grouped by e1)
+            // The row's element window (spans, interior flags, em slices) is
+            // staged first with independent loads; both stages then read
+            // shared memory only.
             const int ef1 = c.el_first1[i1], ne1 = c.el_last1[i1] - ef1 + 1;
-            const int ef2 = c.el_first2[i2], el2 = c.el_last2[i2];
+            const int ef2 = c.el_first2[i2], ne2 = c.el_last2[i2] - ef2 + 1;
             const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
-            const int q1 = c.p1 + 1, q2 = c.p2 + 1;
+            for (int l = lane; l < ne1 * q1; l += 32) {
+                const int k1 = l / q1, b1 = l - k1 * q1, e1 = ef1 + k1;
+                const int f1 = c.espan1[e1] - c.p1;
+                if (b1 == 0) F1[k1] = f1;
+                E1[l] = c.em1[((int64_t)e1 * q1 + (i1 - f1)) * q1 + b1];
+            }
+            for (int l = lane; l < ne2 * q2; l += 32) {
+                const int k2 = l / q2, b2 = l - k2 * q2, e2 = ef2 + k2;
+                const int f2 = c.espan2[e2] - c.p2;
+                if (b2 == 0) F2[k2] = f2;
+                E2[l] = c.em2[((int64_t)e2 * q2 + (i2 - f2)) * q2 + b2];
+            }
+            for (int l = lane; l < ne1 * ne2; l += 32) {
+                const int k1 = l / ne2, e1 = ef1 + k1, e2 = ef2 + (l - k1 * ne2);
+                bool ok = c.elem_class[(int64_t)e1 * c.nel2 + e2] == TQ_INTERIOR;
+                if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) ok = false;
+                MK[l] = ok ? 1 : 0;
+            }
+            __syncwarp();
             for (int t = lane; t < ne1 * W2; t += 32) {
                 const int k1 = t / W2, o2 = t - (t / W2) * W2;
-                const int e1 = ef1 + k1, j2 = i2 - c.p2 + o2;
+                const int j2 = i2 - c.p2 + o2;
                 double acc = 0.0;
                 if (j2 >= 0 && j2 < c.n2) {
-                    for (int e2 = ef2; e2 <= el2; ++e2) {
-                        if (c.elem_class[(int64_t)e1 * c.nel2 + e2] != TQ_INTERIOR) continue;
-                        if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) continue;
-                        const int f2 = c.espan2[e2] - c.p2, b2 = j2 - f2;
+                    for (int k2 = 0; k2 < ne2; ++k2) {
+                        if (!MK[k1 * ne2 + k2]) continue;
+                        const int b2 = j2 - F2[k2];
                         if (b2 < 0 || b2 > c.p2) continue;
-                        acc += c.em2[((int64_t)e2 * q2 + (i2 - f2)) * q2 + b2];
+                        acc += E2[k2 * q2 + b2];
                     }
                 }
                 inner[t] = acc;
@@ -139,9 +171,9 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
                 double acc = 0.0;
                 if (j1 >= 0 && j1 < c.n1) {
                     for (int k1 = 0; k1 < ne1; ++k1) {
-                        const int e1 = ef1 + k1, f1 = c.espan1[e1] - c.p1, b1 = j1 - f1;
+                        const int b1 = j1 - F1[k1];
                         if (b1 < 0 || b1 > c.p1) continue;
-                        acc += c.em1[((int64_t)e1 * q1 + (i1 - f1)) * q1 + b1] * inner[k1 * W2 + o2];
+                        acc += E1[k1 * q1 + b1] * inner[k1 * W2 + o2];
                     }
                 }
                 blk[q] += acc;
@@ -385,7 +417,8 @@ using namespace tq;
 static size_t regular_smem_per_warp(const tq_rawctx& c) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
     const int ni = std::max(c.nmax1, c.p1 + 1);
-    return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * ni + W1 + W2);
+    return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * ni + W1 + W2 +
+                             regular_window_slots(c.p1, c.p2));
 }
 
 template <int PARTS>

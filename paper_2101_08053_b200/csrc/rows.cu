@@ -44,6 +44,14 @@ __global__ void k_wq_products(tq_space1d s, tq_layout lay, const int32_t* __rest
     }
 }
 
+// tile mode: offset of row r = its tile base + the counts of the rows before
+// it in the tile (warp-collective; every lane gets the value)
+__device__ __forceinline__ int tile_offset(const tq_rowctx& c, int r, int lane) {
+    const int rel = r - c.row_begin;
+    const int cnt = lane < (rel & 31) ? __ldg(c.counts + ((rel & ~31) + lane)) : 0;
+    return __ldg((c.tiles + TQ_TILE_PAD(c.row_end - c.row_begin)) + (rel >> 5)) + __reduce_add_sync(0xffffffffu, cnt);
+}
+
 struct RowGeom {
     int i1, i2, s_i, j1lo, j2lo, t1, t2;
 };
@@ -138,6 +146,7 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
     for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
         const int r = c.row_begin + base + threadIdx.x;
         bool to_a = false, to_b = false;
+        int mycount = 0;      // list-A rows: added by pass 2
         if (r < c.row_end) {
             const int idx = __ldg(c.active + r);
             const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
@@ -148,6 +157,7 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
                 const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
                 const int t2 = __ldg(c.ov_hi2 + i2) - __ldg(c.ov_lo2 + i2) + 1;
                 counts[r - c.row_begin] = t1 * t2;
+                mycount = t1 * t2;
                 const bool full = t1 == 2 * c.p1 + 1 && t2 == 2 * c.p2 + 1;
                 if (c.rowfast) c.rowfast[r - c.row_begin] = full ? 1 : 0;
                 to_b = !(full && c.rowfast);
@@ -166,6 +176,11 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
         bb = __shfl_sync(0xffffffffu, bb, 0);
         if (to_a) list[ba + __popc(ma & lt)] = r;
         if (to_b) listb[bb + __popc(mb & lt)] = r;
+        if (c.tiles) {          // warp = one 32-row tile (base is a multiple of the block size)
+            const int tsum = __reduce_add_sync(0xffffffffu, mycount);
+            const int t = (base + threadIdx.x) >> 5;
+            if (lane == 0 && (t << 5) < n) c.tiles[t] = tsum;
+        }
     }
 }
 
@@ -187,7 +202,10 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 #pragma unroll
             for (int u = 0; u < 3; ++u) cnt += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
         }
-        if (lane == 0) counts[r - c.row_begin] = cnt;
+        if (lane == 0) {
+            counts[r - c.row_begin] = cnt;
+            if (c.tiles) atomicAdd(c.tiles + ((r - c.row_begin) >> 5), cnt);
+        }
     }
 }
 
@@ -314,7 +332,7 @@ __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S,
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* __restrict__ indptr,
+__global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __restrict__ indptr,
                                                      int32_t* __restrict__ indices, double* __restrict__ data,
                                                      int* __restrict__ irr_rows, int* __restrict__ irr_count) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -324,21 +342,38 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, const int32_t* 
     const int nwarps = gridDim.x * wpb;
     int nbulk = 0;
     int R0 = c.row_begin + (blockIdx.x * wpb + wib) * kWarpRows;
-    int n_idx = 0, n_pos = 0, n_fast = 0;
+    // tile mode: the per-row word is the count, the offset comes from the
+    // tile base + an exclusive warp scan (and is written to indptr here)
+    const bool tm = c.tiles != nullptr;
+    int n_idx = 0, n_pos = 0, n_fast = 0, n_tb = 0;
     if (R0 + lane < c.row_end) {
         n_idx = __ldg(c.active + R0 + lane);
-        n_pos = __ldg(indptr + (R0 + lane - c.row_begin));
+        n_pos = __ldg((tm ? c.counts : indptr) + (R0 + lane - c.row_begin));
         n_fast = c.rowfast ? __ldg(c.rowfast + (R0 + lane - c.row_begin)) : 0;
     }
+    const int32_t* tbase = tm ? (c.tiles + TQ_TILE_PAD(c.row_end - c.row_begin)) : nullptr;
+    if (tm && R0 < c.row_end) n_tb = __ldg(tbase + ((R0 - c.row_begin) >> 5));
     for (; R0 < c.row_end; R0 += nwarps * kWarpRows) {
         const bool valid = R0 + lane < c.row_end;
-        const int my_idx = n_idx, my_pos = n_pos, my_fast = valid ? n_fast : 0;
+        int my_pos = n_pos;
+        const int my_idx = n_idx, my_fast = valid ? n_fast : 0;
+        if (tm) {
+            int x = my_pos;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off) x += y;
+            }
+            my_pos = n_tb + x - my_pos;
+            if (valid) indptr[R0 + lane - c.row_begin] = my_pos;
+        }
         const int R1 = R0 + nwarps * kWarpRows;
         if (R1 + lane < c.row_end) {
             n_idx = __ldg(c.active + R1 + lane);
-            n_pos = __ldg(indptr + (R1 + lane - c.row_begin));
+            n_pos = __ldg((tm ? c.counts : indptr) + (R1 + lane - c.row_begin));
             n_fast = c.rowfast ? __ldg(c.rowfast + (R1 + lane - c.row_begin)) : 0;
         }
+        if (tm && R1 < c.row_end) n_tb = __ldg(tbase + ((R1 - c.row_begin) >> 5));
         // rows that are not fast go to the row-parallel irregular kernel
         // (listed here unless the count pass already listed them)
         const unsigned slow = irr_rows ? __ballot_sync(0xffffffffu, valid && !my_fast) : 0u;
@@ -391,7 +426,7 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
     for (int u = warp; u < nrows; u += nw) {
         const int r = u < na ? irr_rows[u] : irr_rows_b[u - na];
         RowGeom g = row_geom(c, r);
-        int pos = __ldg(indptr + (r - c.row_begin));
+        int pos = c.tiles ? tile_offset(c, r, lane) : __ldg(indptr + (r - c.row_begin));
         const int n = g.t1 * g.t2;
         // deep rows: list B when the count pass gave the lists, else the flags
         const bool deep_row = irr_rows_b ? u >= na : c.deep[c.active[r]] != 0;
@@ -445,14 +480,20 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
 }
 
 // generic fill (unequal degrees or no separable factors)
-__global__ void k_fill_rows(tq_rowctx c, const int32_t* __restrict__ indptr, int32_t* __restrict__ indices,
+__global__ void k_fill_rows(tq_rowctx c, int32_t* __restrict__ indptr, int32_t* __restrict__ indices,
                             double* __restrict__ data) {
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     for (int r = c.row_begin + blockIdx.x * wpb + (threadIdx.x >> 5); r < c.row_end; r += gridDim.x * wpb) {
         RowGeom g = row_geom(c, r);
-        int pos = indptr[r - c.row_begin];
+        int pos;
+        if (c.tiles) {
+            pos = tile_offset(c, r, lane);
+            if (lane == 0) indptr[r - c.row_begin] = pos;
+        } else {
+            pos = indptr[r - c.row_begin];
+        }
         int n = g.t1 * g.t2;
         for (int e0 = 0; e0 < n; e0 += 32) {
             int e = e0 + lane;
@@ -584,6 +625,8 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
                             void* stream) {
     int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
+    if (c.tiles) { set_error("tq_fill_rows reads a complete indptr (tile mode: tq_fill_fast + tq_fill_listed)"); return TQ_EINVAL; }
+    int32_t* ip = const_cast<int32_t*>(indptr);   // read only here
     int P = (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0;
     int* irr = nullptr;   // [0] = count, [1..] = rows for the irregular kernel
     cudaStream_t st = S(stream);
@@ -606,8 +649,8 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
         const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
         TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (nrows + 1), st));
         TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), st));
-        kern<<<grid, 32 * wpb, shm, st>>>(c, indptr, indices, data, irr + 1, irr); ::tq::note_launch();
-        kirr<<<kSms * 8, 256, 0, st>>>(c, indptr, indices, data, irr + 1, irr, nullptr, nullptr); ::tq::note_launch();
+        kern<<<grid, 32 * wpb, shm, st>>>(c, ip, indices, data, irr + 1, irr); ::tq::note_launch();
+        kirr<<<kSms * 8, 256, 0, st>>>(c, ip, indices, data, irr + 1, irr, nullptr, nullptr); ::tq::note_launch();
         TQ_CUDA(cudaFreeAsync(irr, st));
         return TQ_OK;
     };
@@ -618,7 +661,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
 #undef CASE
         default: {
             int grid = (int)std::min<int64_t>((nrows + 7) / 8, (int64_t)kSms * 32);
-            k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, indptr, indices, data); ::tq::note_launch();
+            k_fill_rows<<<grid, 256, 0, S(stream)>>>(c, ip, indices, data); ::tq::note_launch();
         }
     }
     if (rc) return rc;
@@ -630,7 +673,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
 // by warp tiles, and the listed rows by the row-parallel kernel; the two
 // write disjoint rows and may run concurrently on different streams.
 template <int P>
-static int fill_fast_launch(const tq_rowctx& c, const int32_t* indptr, int32_t* indices, double* data,
+static int fill_fast_launch(const tq_rowctx& c, int32_t* indptr, int32_t* indices, double* data,
                             cudaStream_t st) {
     static int cached_wpb = 0, cached_per_sm = 0;
     const size_t per_warp = fill_slice_bytes<P>();
@@ -662,7 +705,7 @@ static int fill_fast_launch(const tq_rowctx& c, const int32_t* indptr, int32_t* 
 
 static int fill_P(const tq_rowctx& c) { return (c.p1 == c.p2 && c.a1 && c.deep) ? c.p1 : 0; }
 
-extern "C" int tq_fill_fast(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data, void* stream) {
+extern "C" int tq_fill_fast(tq_rowctx c, int32_t* indptr, int32_t* indices, double* data, void* stream) {
     const int nrows = c.row_end - c.row_begin;
     if (nrows <= 0) return TQ_OK;
     int rc = TQ_OK;

@@ -50,3 +50,34 @@ def test_scan_repeatable_and_capture_mode():
     a, _ = scan(counts)
     b, _ = scan(counts, capture=True)       # no host read-back: same device result
     assert np.array_equal(a, b)
+
+
+def scan_tiles(tile_sums, nrows):
+    """tq_scan_tiles on given tile sums (tile mode of the row pointer)."""
+    from paper_2101_08053_b200 import _lib as L
+    tiles = torch.full((L.tile_ints(nrows),), -3, dtype=torch.int32, device="cuda")
+    tiles[:len(tile_sums)] = torch.from_numpy(np.asarray(tile_sums, np.int32)).cuda()
+    counts = torch.zeros(max(nrows, 1), dtype=torch.int32, device="cuda")
+    indptr = torch.full((nrows + 1,), -7, dtype=torch.int32, device="cuda")
+    ctx = L.RowCtx()
+    ctx.row_begin, ctx.row_end = 5, 5 + nrows
+    ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
+    nnz = L.i64(0)
+    L.call("tq_scan_tiles", ctx, L.ptr(indptr), L.C.byref(nnz), L.stream())
+    torch.cuda.synchronize()
+    return tiles[L.tile_pad(nrows):].cpu().numpy(), indptr.cpu().numpy(), int(nnz.value)
+
+
+@pytest.mark.parametrize("nrows", [0, 1, 31, 32, 33, 4096, 4096 * 32 + 5, 3_078_139])
+def test_scan_tiles_matches_cumsum(nrows):
+    ntiles = (nrows + 31) // 32
+    sums = np.random.default_rng(nrows).integers(0, 32 * 81, size=ntiles)
+    tiles, indptr, nnz = scan_tiles(sums, nrows)
+    ref = np.concatenate([[0], np.cumsum(sums)])
+    assert np.array_equal(tiles[:ntiles], ref[:-1])       # exclusive bases
+    assert indptr[nrows] == ref[-1] and nnz == ref[-1]
+
+
+def test_scan_tiles_overflow_raises():
+    with pytest.raises(OverflowError):
+        scan_tiles(np.full(3, 2**30), 96)
