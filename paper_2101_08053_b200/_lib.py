@@ -96,6 +96,8 @@ def lib():
         "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_scan_tiles": ([RowCtx, vp, C.POINTER(i64), vp], i32),
+        "tq_scan_tiles_head": ([RowCtx, vp], i32),
+        "tq_fill_fast_part": ([RowCtx, vp, vp, vp, i32, i32, vp], i32),
         "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_fill_listed": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_active_index": ([vp, i64, vp, vp, C.POINTER(i32), vp], i32),
@@ -166,8 +168,9 @@ def tile_pad(nrows):
 
 
 def tile_ints(nrows):
-    """TQ_TILE_INTS: ints of a tile-mode buffer (tq_rowctx.tiles)."""
-    return tile_pad(nrows) + (nrows + 31) // 32 + 2
+    """TQ_TILE_INTS: ints of a tile-mode buffer (tq_rowctx.tiles): sums |
+    bases, total, overflow | head bases | four control words."""
+    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 6
 
 
 def ptr(t):

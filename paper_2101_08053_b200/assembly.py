@@ -17,6 +17,7 @@ The symmetrised, zero-dropped CSR is then counted, scanned and filled.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -350,16 +351,20 @@ class Formation:
                         L.ptr(self.raw if self.raw is not None else dummy),
                         L.ptr(self.deep), L.ptr(self.rowfast), row_begin, self.K if row_end is None else row_end)
 
-    def fill(self, ctx, indptr, indices, data):
+    def fill(self, ctx, indptr, indices, data, part=0):
         """Fast rows by warp tiles on the current stream; the rows listed by
         the count pass concurrently on a side stream."""
         from ._rawrows import _named_stream
         main = torch.cuda.current_stream()
-        side = _named_stream("fill_listed", priority=-2)
+        # lowest priority: the tile fill's warps dispatch first, the listed
+        # rows take the slots it leaves (measured best)
+        side = _named_stream("fill_listed", priority=0)
         side.wait_stream(main)
         with torch.cuda.stream(side):
             L.call("tq_fill_listed", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.ptr(self.work), L.stream())
-        L.call("tq_fill_fast", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), L.stream())
+            _stamp("fill_listed")
+        L.call("tq_fill_fast_part", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), part, 0, L.stream())
+        _stamp("fill_tiles")
         main.wait_stream(side)
         if not torch.cuda.is_current_stream_capturing():
             for t in (indptr, indices, data, self.work) + self._count_bufs:
@@ -406,27 +411,57 @@ class Formation:
             else:
                 L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_deep")
+            head = None
+            if self.capture is not None and HEAD_FILL:
+                # the output exists before the scan (nnz known): the tiles
+                # before the first list-A row have final offsets now -- fill
+                # them on a low-priority stream with a capped grid while the
+                # raw rows and count pass 2 finish
+                out = self._alloc_out(nrows, self.capture["nnz"])
+                L.call("tq_scan_tiles_head", ctx, L.stream())
+                main = torch.cuda.current_stream()
+                from ._rawrows import _named_stream
+                head = _named_stream("fill_head", priority=0)
+                head.wait_stream(main)
+                with torch.cuda.stream(head):
+                    L.call("tq_fill_fast_part", ctx, *map(L.ptr, out), 1, HEAD_BLOCKS_PER_SM, L.stream())
+                    _stamp("head_fill")
             if join is not None:
                 torch.cuda.current_stream().wait_stream(join)
             _stamp("join")
             L.call("tq_row_counts_rest", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_rest")
-        indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
         nnz = L.i64(0)
+        if head is None:
+            indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
+        else:
+            indptr, indices, data = out
         with self.timer("scan"):
             L.call("tq_scan_tiles", ctx, L.ptr(indptr), None if self.capture else L.C.byref(nnz), L.stream())
         _stamp("scan")
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)
-        indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
-        data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
+        if head is None:
+            indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev)
+            data = torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev)
         self.work = work
         with self.timer("fill"):
-            self.fill(ctx, indptr, indices, data)
+            self.fill(ctx, indptr, indices, data, part=0 if head is None else 2)
+        if head is not None:
+            torch.cuda.current_stream().wait_stream(head)
         _stamp("fill")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
+    def _alloc_out(self, nrows, nnz):
+        return (torch.empty(nrows + 1, dtype=torch.int32, device=self.dev),
+                torch.empty(max(nnz, 1), dtype=torch.int32, device=self.dev),
+                torch.empty(max(nnz, 1), dtype=torch.float64, device=self.dev))
+
 
 STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
+# captured passes fill the tiles before the first list-A row early, on a
+# low-priority stream with this many fill blocks per SM (tuning knobs)
+HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "1"))
+HEAD_BLOCKS_PER_SM = int(os.environ.get("TQ_HEAD_BPS", "3"))
 
 
 def _stamp(name):

@@ -15,7 +15,21 @@ __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t
     extern __shared__ double skn[];
     const double* kn = s.knots;
     if (staged) {
-        for (int k = threadIdx.x; k < s.nknots; k += blockDim.x) skn[k] = s.knots[k];
+        // all loads in flight before the stores (not one latency per knot)
+        constexpr int U = 8;
+        for (int k0 = threadIdx.x; k0 < s.nknots; k0 += U * blockDim.x) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * blockDim.x;
+                v[u] = k < s.nknots ? __ldg(s.knots + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * blockDim.x;
+                if (k < s.nknots) skn[k] = v[u];
+            }
+        }
         __syncthreads();
         kn = skn;
     }

@@ -135,6 +135,15 @@ __host__ __device__ inline void basis_funs_ders_rt(const double* kn, int p, int 
     }
 }
 
+// tile mode: number of head tiles (those before the tile holding the first
+// list-A row; all tiles when list A is empty), from count pass 1's control word
+__device__ __forceinline__ int head_tiles(const tq_rowctx& c) {
+    const int n = c.row_end - c.row_begin;
+    const int enc = c.tiles[TQ_TILE_CTL(n)];
+    if (enc == 0) return TQ_TILE_NT(n);
+    return ((0x7fffffff - enc) - c.row_begin) >> 5;
+}
+
 inline int grid_for(int64_t work, int per_block) {
     int64_t g = (work + per_block - 1) / per_block;
     if (g < 1) g = 1;

@@ -180,31 +180,101 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
             const int tsum = __reduce_add_sync(0xffffffffu, mycount);
             const int t = (base + threadIdx.x) >> 5;
             if (lane == 0 && (t << 5) < n) c.tiles[t] = tsum;
+            // first list-A row (encoded INT_MAX - row: the largest code wins)
+            const unsigned enc = __reduce_max_sync(0xffffffffu, to_a ? (unsigned)(0x7fffffff - r) : 0u);
+            if (lane == 0 && enc) atomicMax(reinterpret_cast<unsigned*>(c.tiles + TQ_TILE_CTL(n)), enc);
         }
     }
 }
 
-// Counts, pass 2 (warp per listed row): value-based symmetric zero test.
+// The entries of R rows at once, 3 chunks of 32 per row (rows of <= 96
+// entries): the column-only loads of all 3R chunks are issued together, then
+// the partners' raw values -- two dependent load levels for R rows.
+template <int R>
+__device__ __forceinline__ void entries_rows(const tq_rowctx& c, const RowGeom* g, const bool* ok, int lane,
+                                             int* col, double* v) {
+    constexpr int U = 3 * R;
+    int cl[U], sj[U], j1[U], j2[U];
+    double vi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const RowGeom& G = g[u / 3];
+        const int n = G.t1 * G.t2;
+        const int e = 32 * (u % 3) + lane;
+        const bool valid = ok[u / 3] && e < n;
+        const int ee = valid ? e : 0;
+        const int q1 = ee / G.t2;
+        j1[u] = G.j1lo + q1;
+        j2[u] = G.j2lo + (ee - q1 * G.t2);
+        const int jidx = j1[u] * c.n2 + j2[u];
+        cl[u] = valid ? __ldg(c.col_of + jidx) : -1;
+        sj[u] = valid ? __ldg(c.slot + jidx) : -1;
+        vi[u] = valid ? raw_value(c, G.i1, G.i2, G.s_i, j1[u], j2[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const RowGeom& G = g[u / 3];
+        col[u] = -1;
+        v[u] = 0.0;
+        if (cl[u] >= 0) {
+            const double w = __dadd_rn(vi[u], raw_value(c, j1[u], j2[u], sj[u], G.i1, G.i2));
+            v[u] = w;
+            col[u] = w != 0.0 ? cl[u] : -1;
+        }
+    }
+}
+
+// Counts, pass 2 (warp per kRowsPass2 listed rows): value-based symmetric
+// zero test.  The rows' geometry and entry loads are issued together (the
+// pass is a chain of dependent loads per row); rows of more than 96 entries
+// (p > 4) go one at a time.
+constexpr int kRowsPass2 = 2;
+
 __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, const int* __restrict__ list,
                                   const int* __restrict__ nlist) {
+    constexpr int R = kRowsPass2;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const int n_rows = *nlist;
-    for (int q = warp; q < n_rows; q += nw) {
-        const int r = list[q];
-        RowGeom g = row_geom(c, r);
-        const int n = g.t1 * g.t2;
-        int cnt = 0;
-        for (int e0 = 0; e0 < n; e0 += 96) {
-            int col[3];
-            double v[3];
-            entries_batch<3>(c, g, e0, lane, n, col, v);
+    for (int q0 = warp * R; q0 < n_rows; q0 += nw * R) {
+        int r[R], cnt[R];
+        bool ok[R];
+        RowGeom g[R];
+        bool small = true;
 #pragma unroll
-            for (int u = 0; u < 3; ++u) cnt += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
+        for (int k = 0; k < R; ++k) {
+            ok[k] = q0 + k < n_rows;
+            r[k] = ok[k] ? list[q0 + k] : list[q0];
+            g[k] = row_geom(c, r[k]);
+            small = small && g[k].t1 * g[k].t2 <= 96;
+            cnt[k] = 0;
+        }
+        if (small) {
+            int col[3 * R];
+            double v[3 * R];
+            entries_rows<R>(c, g, ok, lane, col, v);
+#pragma unroll
+            for (int u = 0; u < 3 * R; ++u) cnt[u / 3] += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
+        } else {
+            for (int k = 0; k < R; ++k) {
+                if (!ok[k]) continue;
+                const int n = g[k].t1 * g[k].t2;
+                for (int e0 = 0; e0 < n; e0 += 96) {
+                    int col[3];
+                    double v[3];
+                    entries_batch<3>(c, g[k], e0, lane, n, col, v);
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) cnt[k] += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
+                }
+            }
         }
         if (lane == 0) {
-            counts[r - c.row_begin] = cnt;
-            if (c.tiles) atomicAdd(c.tiles + ((r - c.row_begin) >> 5), cnt);
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if (!ok[k]) continue;
+                counts[r[k] - c.row_begin] = cnt[k];
+                if (c.tiles) atomicAdd(c.tiles + ((r[k] - c.row_begin) >> 5), cnt[k]);
+            }
         }
     }
 }
@@ -334,27 +404,50 @@ __device__ __forceinline__ void emit_run(const tq_rowctx& c, RegularSlice<P>& S,
 template <int P>
 __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __restrict__ indptr,
                                                      int32_t* __restrict__ indices, double* __restrict__ data,
-                                                     int* __restrict__ irr_rows, int* __restrict__ irr_count) {
+                                                     int* __restrict__ irr_rows, int* __restrict__ irr_count,
+                                                     int part) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     RegularSlice<P>& S = *reinterpret_cast<RegularSlice<P>*>(smraw + fill_slice_bytes<P>() * wib);
     const unsigned lt = (1u << lane) - 1u;
     const int nwarps = gridDim.x * wpb;
     int nbulk = 0;
-    int R0 = c.row_begin + (blockIdx.x * wpb + wib) * kWarpRows;
     // tile mode: the per-row word is the count, the offset comes from the
-    // tile base + an exclusive warp scan (and is written to indptr here)
+    // tile base + an exclusive warp scan (and is written to indptr here).
+    // part 1 / 2: the tiles before / from the first list-A tile.
     const bool tm = c.tiles != nullptr;
+    const int nr = c.row_end - c.row_begin;
+    int rlo = c.row_begin, rhi = c.row_end;
+    const int32_t* tbase = tm ? (c.tiles + TQ_TILE_PAD(nr)) : nullptr;
+    if (tm && part) {
+        const int split = min(c.row_end, c.row_begin + kWarpRows * head_tiles(c));
+        if (part == 1) {
+            rhi = split;
+            tbase = c.tiles + TQ_TILE_HEAD(nr);
+        } else {
+            rlo = split;
+        }
+    }
+    // tiles: dynamically assigned in tile mode (a counter per part; warps
+    // that start late, beside other kernels, just take fewer tiles), else a
+    // static stride.  The next tile is claimed one ahead for the prefetch.
+    int* ctr = tm ? c.tiles + TQ_TILE_CTL(nr) + (part == 1 ? 2 : 1) : nullptr;
+    auto next_tile = [&](int cur) -> int {
+        if (!ctr) return cur + nwarps * kWarpRows;
+        int t = 0;
+        if (lane == 0) t = atomicAdd(ctr, 1);
+        return rlo + kWarpRows * __shfl_sync(0xffffffffu, t, 0);
+    };
+    int R0 = ctr ? next_tile(0) : rlo + (blockIdx.x * wpb + wib) * kWarpRows;
     int n_idx = 0, n_pos = 0, n_fast = 0, n_tb = 0;
-    if (R0 + lane < c.row_end) {
+    if (R0 + lane < rhi) {
         n_idx = __ldg(c.active + R0 + lane);
         n_pos = __ldg((tm ? c.counts : indptr) + (R0 + lane - c.row_begin));
         n_fast = c.rowfast ? __ldg(c.rowfast + (R0 + lane - c.row_begin)) : 0;
     }
-    const int32_t* tbase = tm ? (c.tiles + TQ_TILE_PAD(c.row_end - c.row_begin)) : nullptr;
-    if (tm && R0 < c.row_end) n_tb = __ldg(tbase + ((R0 - c.row_begin) >> 5));
-    for (; R0 < c.row_end; R0 += nwarps * kWarpRows) {
-        const bool valid = R0 + lane < c.row_end;
+    if (tm && R0 < rhi) n_tb = __ldg(tbase + ((R0 - c.row_begin) >> 5));
+    for (int R1; R0 < rhi; R0 = R1) {
+        const bool valid = R0 + lane < rhi;
         int my_pos = n_pos;
         const int my_idx = n_idx, my_fast = valid ? n_fast : 0;
         if (tm) {
@@ -367,13 +460,13 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
             my_pos = n_tb + x - my_pos;
             if (valid) indptr[R0 + lane - c.row_begin] = my_pos;
         }
-        const int R1 = R0 + nwarps * kWarpRows;
-        if (R1 + lane < c.row_end) {
+        R1 = next_tile(R0);
+        if (R1 + lane < rhi) {
             n_idx = __ldg(c.active + R1 + lane);
             n_pos = __ldg((tm ? c.counts : indptr) + (R1 + lane - c.row_begin));
             n_fast = c.rowfast ? __ldg(c.rowfast + (R1 + lane - c.row_begin)) : 0;
         }
-        if (tm && R1 < c.row_end) n_tb = __ldg(tbase + ((R1 - c.row_begin) >> 5));
+        if (tm && R1 < rhi) n_tb = __ldg(tbase + ((R1 - c.row_begin) >> 5));
         // rows that are not fast go to the row-parallel irregular kernel
         // (listed here unless the count pass already listed them)
         const unsigned slow = irr_rows ? __ballot_sync(0xffffffffu, valid && !my_fast) : 0u;
@@ -580,6 +673,7 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
 extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream) {
     int nrows = c.row_end - c.row_begin;
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
+    if (c.tiles && nrows > 0) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 4 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     k_row_counts_deep<false><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, nullptr, nullptr, counts, work + 2, work,
                                                                            work + 2 + nrows, work + 1); ::tq::note_launch();
@@ -596,6 +690,7 @@ extern "C" int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, in
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     if (!c.a1 || !c.a2) { set_error("tq_row_counts_geo needs the separable factors"); return TQ_EINVAL; }
+    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 4 * sizeof(int32_t), S(stream)));
     k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos); ::tq::note_launch();
     k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
                                                                           work + 2 + nrows, work + 1); ::tq::note_launch();
@@ -649,7 +744,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
         const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
         TQ_CUDA(cudaMallocAsync(&irr, sizeof(int) * (nrows + 1), st));
         TQ_CUDA(cudaMemsetAsync(irr, 0, sizeof(int), st));
-        kern<<<grid, 32 * wpb, shm, st>>>(c, ip, indices, data, irr + 1, irr); ::tq::note_launch();
+        kern<<<grid, 32 * wpb, shm, st>>>(c, ip, indices, data, irr + 1, irr, 0); ::tq::note_launch();
         kirr<<<kSms * 8, 256, 0, st>>>(c, ip, indices, data, irr + 1, irr, nullptr, nullptr); ::tq::note_launch();
         TQ_CUDA(cudaFreeAsync(irr, st));
         return TQ_OK;
@@ -674,7 +769,7 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
 // write disjoint rows and may run concurrently on different streams.
 template <int P>
 static int fill_fast_launch(const tq_rowctx& c, int32_t* indptr, int32_t* indices, double* data,
-                            cudaStream_t st) {
+                            cudaStream_t st, int part = 0, int blocks_per_sm = 0) {
     static int cached_wpb = 0, cached_per_sm = 0;
     const size_t per_warp = fill_slice_bytes<P>();
     if (!cached_wpb) {
@@ -697,9 +792,12 @@ static int fill_fast_launch(const tq_rowctx& c, int32_t* indptr, int32_t* indice
         if (!cached_wpb) { set_error("fill staging does not fit in shared memory"); return TQ_EINVAL; }
     }
     const int wpb = cached_wpb, nrows = c.row_end - c.row_begin;
-    const int64_t full = (int64_t)kSms * std::max(cached_per_sm, 1);
+    int per_sm = std::max(cached_per_sm, 1);
+    if (blocks_per_sm > 0) per_sm = std::min(per_sm, blocks_per_sm);
+    const int64_t full = (int64_t)kSms * per_sm;
     const int grid = (int)std::min<int64_t>((nrows + wpb * kWarpRows - 1) / (wpb * kWarpRows), full);
-    k_fill_tiles<P><<<grid, 32 * wpb, per_warp * wpb, st>>>(c, indptr, indices, data, nullptr, nullptr); ::tq::note_launch();
+    k_fill_tiles<P><<<grid, 32 * wpb, per_warp * wpb, st>>>(c, indptr, indices, data, nullptr, nullptr, part);
+    ::tq::note_launch();
     return TQ_OK;
 }
 
@@ -720,6 +818,27 @@ extern "C" int tq_fill_fast(tq_rowctx c, int32_t* indptr, int32_t* indices, doub
     }
     if (rc) return rc;
     TQ_LAUNCH_CHECK("tq_fill_fast");
+    return TQ_OK;
+}
+
+extern "C" int tq_fill_fast_part(tq_rowctx c, int32_t* indptr, int32_t* indices, double* data, int32_t part,
+                                 int32_t blocks_per_sm, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    if (nrows <= 0) return TQ_OK;
+    if (part < 0 || part > 2 || (part && !c.tiles)) { set_error("fill part %d needs tile mode", part); return TQ_EINVAL; }
+    const int P = fill_P(c);
+    if (P == 0) {            // generic fill: every row in part 0 / 2
+        if (part == 1) return TQ_OK;
+        return tq_fill_fast(c, indptr, indices, data, stream);
+    }
+    int rc = TQ_OK;
+    switch (P) {
+#define CASE(Q) case Q: rc = fill_fast_launch<Q>(c, indptr, indices, data, S(stream), part, blocks_per_sm); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    }
+    if (rc) return rc;
+    TQ_LAUNCH_CHECK("tq_fill_fast_part");
     return TQ_OK;
 }
 

@@ -261,12 +261,18 @@ __global__ void __launch_bounds__(kCoopThreads) k_scan_coop(const int32_t* __res
 // the second half of the buffer (the sums stay readable by the other blocks).
 constexpr int kTileScanThreads = 1024;
 
-__global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(const int32_t* __restrict__ sums, int ntiles,
-                                                                int32_t* __restrict__ bases,
-                                                                int32_t* __restrict__ indptr_last) {
+// HEAD: only the head tiles (before the first list-A tile), into the head
+// bases; no total.
+template <bool HEAD>
+__global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(tq_rowctx c, int32_t* __restrict__ indptr_last) {
     __shared__ long long red[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int t0 = blockIdx.x * kTileScanThreads;
+    const int nr = c.row_end - c.row_begin;
+    const int32_t* __restrict__ sums = c.tiles;
+    const int ntiles = HEAD ? head_tiles(c) : TQ_TILE_NT(nr);
+    int32_t* __restrict__ bases = c.tiles + (HEAD ? TQ_TILE_HEAD(nr) : TQ_TILE_PAD(nr));
+    if (HEAD && t0 >= ntiles) return;
     // sum of the tiles before this block: [0, t0), t0 a multiple of 1024
     long long before = 0;
     {
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(const int32_t* 
     }
     const long long e = base + woff + x - v;
     if (i < ntiles) bases[i] = (int32_t)e;
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    if (!HEAD && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
         const long long total = base + btot;
         *indptr_last = (int32_t)total;
         bases[ntiles] = (int32_t)total;
@@ -331,7 +337,7 @@ extern "C" int tq_scan_tiles(tq_rowctx c, int32_t* indptr, int64_t* nnz_h, void*
     const int ntiles = (nrows + 31) / 32;
     int32_t* bases = tq_tile_bases(c.tiles, nrows);
     const int grid = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
-    k_scan_tiles<<<grid, kTileScanThreads, 0, st>>>(c.tiles, ntiles, bases, indptr + nrows); ::tq::note_launch();
+    k_scan_tiles<false><<<grid, kTileScanThreads, 0, st>>>(c, indptr + nrows); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_scan_tiles");
     if (nnz_h) {
         int32_t h[2] = {0, 0};
@@ -420,5 +426,15 @@ extern "C" int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* 
     int rc = scan_generic(ActiveIn{func_class}, nfun, ActiveOut{col_of, active}, &total, S(stream));
     if (rc) return rc;
     *K_h = (int32_t)total;
+    return TQ_OK;
+}
+
+extern "C" int tq_scan_tiles_head(tq_rowctx c, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    if (!c.tiles || !c.counts) { set_error("tq_scan_tiles_head needs the context's counts and tiles"); return TQ_EINVAL; }
+    if (nrows <= 0) return TQ_OK;
+    const int grid = (TQ_TILE_NT(nrows) + kTileScanThreads - 1) / kTileScanThreads;
+    k_scan_tiles<true><<<grid, kTileScanThreads, 0, S(stream)>>>(c, nullptr); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_scan_tiles_head");
     return TQ_OK;
 }

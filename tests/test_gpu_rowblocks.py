@@ -20,7 +20,7 @@ def _space(kind):
 
 @pytest.mark.parametrize("kind,strategy", [("bspline", "dwq"), ("ccircle", "hybrid"), ("corner", "dwq"),
                                            ("line", "wq")])
-@pytest.mark.parametrize("world", [2, 5])
+@pytest.mark.parametrize("world", [1, 2, 5])
 def test_row_blocks_match_full_matrix(kind, strategy, world):
     import torch
     from paper_2101_08053_b200.assembly import GraphFormation, form
