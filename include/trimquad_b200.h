@@ -190,15 +190,16 @@ typedef struct {
 } tq_rowctx;
 
 /* tile-mode buffer layout (ints): the tile sums (padded to a multiple of 4
-   for vector loads) | the tile bases, the total, an overflow flag | the head
-   bases (tiles before the first list-A row, final after count pass 1) | four
-   control words (the first list-A row, encoded INT_MAX - row, 0 = none; the
-   fill's tile counters), zeroed by the count pass */
+   for vector loads) | the tile bases, the total, an overflow flag | the early
+   bases (head tiles before the first list-A row and tail tiles after the last
+   one: final after count pass 1, the tail ones given nnz) | eight control
+   words: first list-A row (encoded INT_MAX - row, 0 = none), last list-A row
+   + 1 (0 = none), the fill's tile counters; zeroed by the count pass */
 #define TQ_TILE_NT(nrows) (((nrows) + 31) / 32)
 #define TQ_TILE_PAD(nrows) ((TQ_TILE_NT(nrows) + 3) / 4 * 4)
-#define TQ_TILE_HEAD(nrows) (TQ_TILE_PAD(nrows) + TQ_TILE_NT(nrows) + 2)
-#define TQ_TILE_CTL(nrows) (TQ_TILE_HEAD(nrows) + TQ_TILE_NT(nrows))
-#define TQ_TILE_INTS(nrows) (TQ_TILE_CTL(nrows) + 4)
+#define TQ_TILE_EARLY(nrows) (TQ_TILE_PAD(nrows) + TQ_TILE_NT(nrows) + 2)
+#define TQ_TILE_CTL(nrows) (TQ_TILE_EARLY(nrows) + TQ_TILE_NT(nrows))
+#define TQ_TILE_INTS(nrows) (TQ_TILE_CTL(nrows) + 8)
 static inline int32_t* tq_tile_bases(int32_t* tiles, int32_t nrows) { return tiles + TQ_TILE_PAD(nrows); }
 
 /* deep-row flags: deep[i] = separable(i) && no raw row in window(i) &&
@@ -246,16 +247,20 @@ int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* d
  * disjoint rows and may run concurrently on two streams.  In tile mode
  * tq_fill_fast also writes indptr[0 .. nrows) (every row's offset). */
 int tq_fill_fast(tq_rowctx c, int32_t* indptr, int32_t* indices, double* data, void* stream);
-/* tile mode, split around the listed rows: part 1 = the tiles before the one
- * holding the first list-A row (after count pass 1 and tq_scan_tiles_head;
- * may run concurrently with the raw rows and pass 2), part 2 = the remaining
- * tiles (after tq_scan_tiles); part 0 = all.  blocks_per_sm > 0 caps the
- * grid (a part running beside other kernels). */
+/* tile mode, split around the listed rows: part 1 = the early tiles (before
+ * the tile holding the first list-A row and after the one holding the last;
+ * after count pass 1 and tq_scan_tiles_early, may run concurrently with the
+ * raw rows and count pass 2), part 2 = the tiles in between (after
+ * tq_scan_tiles); part 0 = all.  blocks_per_sm > 0 caps the grid (a part
+ * running beside other kernels). */
 int tq_fill_fast_part(tq_rowctx c, int32_t* indptr, int32_t* indices, double* data, int32_t part,
                       int32_t blocks_per_sm, void* stream);
-/* head bases: exclusive scan of the tile sums before the first list-A tile
- * (count pass 1 has written them all) */
-int tq_scan_tiles_head(tq_rowctx c, void* stream);
+/* early bases after count pass 1: head tiles by prefix sums and, with
+ * tail != 0, the tail tiles as nnz - suffix sums.  nnz (>= 0) is the count
+ * known in advance (a captured pass, which sized the output with it):
+ * tq_scan_tiles later checks the total against it, a mismatch sets the flag
+ * word TQ_TILE_CTL + 4.  nnz < 0: unknown (head only, no check). */
+int tq_scan_tiles_early(tq_rowctx c, int64_t nnz, int32_t tail, void* stream);
 int tq_fill_listed(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                    const int32_t* work, void* stream);
 

@@ -96,7 +96,7 @@ def lib():
         "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_scan_tiles": ([RowCtx, vp, C.POINTER(i64), vp], i32),
-        "tq_scan_tiles_head": ([RowCtx, vp], i32),
+        "tq_scan_tiles_early": ([RowCtx, i64, i32, vp], i32),
         "tq_fill_fast_part": ([RowCtx, vp, vp, vp, i32, i32, vp], i32),
         "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_fill_listed": ([RowCtx, vp, vp, vp, vp, vp], i32),
@@ -167,10 +167,15 @@ def tile_pad(nrows):
     return ((nrows + 31) // 32 + 3) // 4 * 4
 
 
+def tile_ctl(nrows):
+    """TQ_TILE_CTL: first control word of a tile-mode buffer."""
+    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 2
+
+
 def tile_ints(nrows):
     """TQ_TILE_INTS: ints of a tile-mode buffer (tq_rowctx.tiles): sums |
-    bases, total, overflow | head bases | four control words."""
-    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 6
+    bases, total, overflow | early bases | eight control words."""
+    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 10
 
 
 def ptr(t):

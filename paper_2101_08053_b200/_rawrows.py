@@ -280,8 +280,17 @@ def build_all_rules(f):
     _st("fits_joined")
     flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
     flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]
-    if f.capture is not None:     # graph capture: flags checked after each replay
-        f._fail_flags = torch.cat(flags) if flags else None
+    if f.capture is not None:
+        # graph capture: the replay reduces the flags on a side stream (off
+        # the critical path, joined at the end of the pass); the host reads
+        # the one status word after the replay (GraphFormation.check)
+        f._fail_any = None
+        if flags:
+            s = _named_stream("fit_status", priority=0)
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                f._fail_any = torch.cat(flags).any()
+            f._status_streams = getattr(f, "_status_streams", []) + [s]
         any_fail = False
     else:
         any_fail = bool(torch.cat(flags).any().item()) if flags else False

@@ -403,6 +403,7 @@ class Formation:
         tiles = torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=self.dev)
         ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
         self._count_bufs = (counts, tiles)
+        self._nrows = nrows
         with self.timer("counts"):
             if self.a1 is not None:
                 pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
@@ -414,11 +415,12 @@ class Formation:
             head = None
             if self.capture is not None and HEAD_FILL:
                 # the output exists before the scan (nnz known): the tiles
-                # before the first list-A row have final offsets now -- fill
-                # them on a low-priority stream with a capped grid while the
-                # raw rows and count pass 2 finish
+                # before the first / after the last list-A row have final
+                # offsets now (the tail ones from nnz; the full scan checks
+                # it) -- fill them on a low-priority stream with a capped grid
+                # while the raw rows and count pass 2 finish
                 out = self._alloc_out(nrows, self.capture["nnz"])
-                L.call("tq_scan_tiles_head", ctx, L.stream())
+                L.call("tq_scan_tiles_early", ctx, self.capture["nnz"], EARLY_TAIL, L.stream())
                 main = torch.cuda.current_stream()
                 from ._rawrows import _named_stream
                 head = _named_stream("fill_head", priority=0)
@@ -448,6 +450,8 @@ class Formation:
             self.fill(ctx, indptr, indices, data, part=0 if head is None else 2)
         if head is not None:
             torch.cuda.current_stream().wait_stream(head)
+        for st in getattr(self, "_status_streams", []):       # status reductions rejoin
+            torch.cuda.current_stream().wait_stream(st)
         _stamp("fill")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
@@ -462,6 +466,10 @@ STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
 # low-priority stream with this many fill blocks per SM (tuning knobs)
 HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "1"))
 HEAD_BLOCKS_PER_SM = int(os.environ.get("TQ_HEAD_BPS", "3"))
+# ... and the tiles after the last list-A row too (their offsets from the
+# captured nnz): measured slower at config 5 (the early fill then delays the
+# latency-bound count pass 2), off by default
+EARLY_TAIL = int(os.environ.get("TQ_EARLY_TAIL", "0"))
 
 
 def _stamp(name):
@@ -558,9 +566,13 @@ class GraphFormation:
         return self.csr
 
     def check(self):
-        flags = getattr(self.f, "_fail_flags", None)
-        if flags is not None and bool(flags.any().item()):
+        """Status of the last replay (host reads after the pass; the
+        reductions ran inside the graph)."""
+        fail = getattr(self.f, "_fail_any", None)
+        if fail is not None and bool(fail.item()):
             raise RuleConstructionError_("moment-fit residual above tolerance in a replayed pass")
+        if int(self.f._count_bufs[1][L.tile_ctl(self.f._nrows) + 4].item()):
+            raise RuntimeError("replayed pass formed a different nnz than the captured one")
 
 
 def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None, strategy="reference",

@@ -144,6 +144,20 @@ __device__ __forceinline__ int head_tiles(const tq_rowctx& c) {
     return ((0x7fffffff - enc) - c.row_begin) >> 5;
 }
 
+// first tail tile (after the tile holding the last list-A row; NT: no tail)
+__device__ __forceinline__ int tail_first_raw(const tq_rowctx& c) {
+    const int n = c.row_end - c.row_begin;
+    const int last1 = c.tiles[TQ_TILE_CTL(n) + 1];
+    if (last1 == 0) return TQ_TILE_NT(n);
+    return ((last1 - 1 - c.row_begin) >> 5) + 1;
+}
+
+// ... when the early scan gave the tail tiles bases (control word 7), else NT
+__device__ __forceinline__ int tail_first(const tq_rowctx& c) {
+    const int n = c.row_end - c.row_begin;
+    return c.tiles[TQ_TILE_CTL(n) + 7] ? tail_first_raw(c) : TQ_TILE_NT(n);
+}
+
 inline int grid_for(int64_t work, int per_block) {
     int64_t g = (work + per_block - 1) / per_block;
     if (g < 1) g = 1;

@@ -183,6 +183,9 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
             // first list-A row (encoded INT_MAX - row: the largest code wins)
             const unsigned enc = __reduce_max_sync(0xffffffffu, to_a ? (unsigned)(0x7fffffff - r) : 0u);
             if (lane == 0 && enc) atomicMax(reinterpret_cast<unsigned*>(c.tiles + TQ_TILE_CTL(n)), enc);
+            // last list-A row + 1
+            const unsigned last1 = __reduce_max_sync(0xffffffffu, to_a ? (unsigned)(r + 1) : 0u);
+            if (lane == 0 && last1) atomicMax(reinterpret_cast<unsigned*>(c.tiles + TQ_TILE_CTL(n) + 1), last1);
         }
     }
 }
@@ -414,31 +417,35 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
     int nbulk = 0;
     // tile mode: the per-row word is the count, the offset comes from the
     // tile base + an exclusive warp scan (and is written to indptr here).
-    // part 1 / 2: the tiles before / from the first list-A tile.
+    // Tiles are numbered within the part (part 1: head then tail tiles,
+    // part 2: the tiles in between) and assigned dynamically from a counter
+    // per part -- warps that start late, beside other kernels, just take
+    // fewer tiles; the next tile is claimed one ahead for the prefetch.
+    // Without tile mode: all tiles, static stride.
     const bool tm = c.tiles != nullptr;
-    const int nr = c.row_end - c.row_begin;
-    int rlo = c.row_begin, rhi = c.row_end;
+    const int nr = c.row_end - c.row_begin, NT = (nr + kWarpRows - 1) / kWarpRows;
     const int32_t* tbase = tm ? (c.tiles + TQ_TILE_PAD(nr)) : nullptr;
+    int tA = NT, tB = NT;
     if (tm && part) {
-        const int split = min(c.row_end, c.row_begin + kWarpRows * head_tiles(c));
-        if (part == 1) {
-            rhi = split;
-            tbase = c.tiles + TQ_TILE_HEAD(nr);
-        } else {
-            rlo = split;
-        }
+        tA = head_tiles(c);
+        tB = max(tail_first(c), tA);
+        if (part == 1) tbase = c.tiles + TQ_TILE_EARLY(nr);
     }
-    // tiles: dynamically assigned in tile mode (a counter per part; warps
-    // that start late, beside other kernels, just take fewer tiles), else a
-    // static stride.  The next tile is claimed one ahead for the prefetch.
-    int* ctr = tm ? c.tiles + TQ_TILE_CTL(nr) + (part == 1 ? 2 : 1) : nullptr;
-    auto next_tile = [&](int cur) -> int {
-        if (!ctr) return cur + nwarps * kWarpRows;
+    const int ntp = part == 1 ? tA + (NT - tB) : part == 2 ? tB - tA : NT;   // tiles in this part
+    int* ctr = tm ? c.tiles + TQ_TILE_CTL(nr) + (part == 1 ? 3 : 2) : nullptr;
+    auto tile_row = [&](int t) -> int {       // part-local tile -> first row (row_end: done)
+        if (t >= ntp) return c.row_end;
+        const int tile = part == 1 ? (t < tA ? t : tB + (t - tA)) : part == 2 ? tA + t : t;
+        return c.row_begin + kWarpRows * tile;
+    };
+    int tcur = blockIdx.x * wpb + wib;
+    if (ctr) {
         int t = 0;
         if (lane == 0) t = atomicAdd(ctr, 1);
-        return rlo + kWarpRows * __shfl_sync(0xffffffffu, t, 0);
-    };
-    int R0 = ctr ? next_tile(0) : rlo + (blockIdx.x * wpb + wib) * kWarpRows;
+        tcur = __shfl_sync(0xffffffffu, t, 0);
+    }
+    const int rhi = c.row_end;
+    int R0 = tile_row(tcur);
     int n_idx = 0, n_pos = 0, n_fast = 0, n_tb = 0;
     if (R0 + lane < rhi) {
         n_idx = __ldg(c.active + R0 + lane);
@@ -460,7 +467,14 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
             my_pos = n_tb + x - my_pos;
             if (valid) indptr[R0 + lane - c.row_begin] = my_pos;
         }
-        R1 = next_tile(R0);
+        if (ctr) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(ctr, 1);
+            tcur = __shfl_sync(0xffffffffu, t, 0);
+        } else {
+            tcur += nwarps;
+        }
+        R1 = tile_row(tcur);
         if (R1 + lane < rhi) {
             n_idx = __ldg(c.active + R1 + lane);
             n_pos = __ldg((tm ? c.counts : indptr) + (R1 + lane - c.row_begin));
@@ -673,7 +687,7 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
 extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream) {
     int nrows = c.row_end - c.row_begin;
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
-    if (c.tiles && nrows > 0) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 4 * sizeof(int32_t), S(stream)));
+    if (c.tiles && nrows > 0) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     k_row_counts_deep<false><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, nullptr, nullptr, counts, work + 2, work,
                                                                            work + 2 + nrows, work + 1); ::tq::note_launch();
@@ -690,7 +704,7 @@ extern "C" int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, in
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     if (!c.a1 || !c.a2) { set_error("tq_row_counts_geo needs the separable factors"); return TQ_EINVAL; }
-    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 4 * sizeof(int32_t), S(stream)));
+    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
     k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos); ::tq::note_launch();
     k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
                                                                           work + 2 + nrows, work + 1); ::tq::note_launch();

@@ -261,23 +261,15 @@ __global__ void __launch_bounds__(kCoopThreads) k_scan_coop(const int32_t* __res
 // the second half of the buffer (the sums stay readable by the other blocks).
 constexpr int kTileScanThreads = 1024;
 
-// HEAD: only the head tiles (before the first list-A tile), into the head
-// bases; no total.
-template <bool HEAD>
-__global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(tq_rowctx c, int32_t* __restrict__ indptr_last) {
-    __shared__ long long red[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int t0 = blockIdx.x * kTileScanThreads;
-    const int nr = c.row_end - c.row_begin;
-    const int32_t* __restrict__ sums = c.tiles;
-    const int ntiles = HEAD ? head_tiles(c) : TQ_TILE_NT(nr);
-    int32_t* __restrict__ bases = c.tiles + (HEAD ? TQ_TILE_HEAD(nr) : TQ_TILE_PAD(nr));
-    if (HEAD && t0 >= ntiles) return;
-    // sum of the tiles before this block: [0, t0), t0 a multiple of 1024
-    long long before = 0;
-    {
-        const int4* s4 = reinterpret_cast<const int4*>(sums);
-        const int n4 = t0 >> 2;
+// MODE 0: every tile -> bases, total, overflow flag (and the check against
+// the nnz the early scan was given).  MODE 1 (grid 2G): blocks [0, G) the
+// head tiles (prefix sums), blocks [G, 2G) the tail tiles (nnz - suffix
+// sums), both into the early bases.
+__device__ __forceinline__ long long sum_range(const int32_t* __restrict__ sums, int lo, int hi) {
+    long long acc = 0;
+    if (lo < hi && (lo & 3) == 0) {          // vector loads from an aligned start
+        const int4* s4 = reinterpret_cast<const int4*>(sums + lo);
+        const int n4 = (hi - lo) >> 2;
         constexpr int U = 8;
         for (int q0 = threadIdx.x; q0 < n4; q0 += U * kTileScanThreads) {
             int4 v[U];
@@ -287,37 +279,78 @@ __global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(tq_rowctx c, in
                 v[u] = q < n4 ? __ldg(s4 + q) : make_int4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) before += (long long)v[u].x + v[u].y + v[u].z + v[u].w;
+            for (int u = 0; u < U; ++u) acc += (long long)v[u].x + v[u].y + v[u].z + v[u].w;
         }
+        lo += n4 << 2;
     }
-    const int i = t0 + threadIdx.x;
-    const int v = i < ntiles ? __ldg(sums + i) : 0;
-    // block: total of `before`, inclusive scan of v
+    constexpr int U = 8;
+    for (int k0 = lo + threadIdx.x; k0 < hi; k0 += U * kTileScanThreads) {
+        int v[U];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) before += __shfl_xor_sync(0xffffffffu, before, off);
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u * kTileScanThreads;
+            v[u] = k < hi ? __ldg(sums + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u];
+    }
+    return acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTileScanThreads) k_scan_tiles(tq_rowctx c, int32_t* __restrict__ indptr_last,
+                                                                long long nnz, int with_tail) {
+    __shared__ long long red[32];
+    __shared__ long long wtot[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nr = c.row_end - c.row_begin, NT = TQ_TILE_NT(nr);
+    const int32_t* __restrict__ sums = c.tiles;
+    int32_t* ctl = c.tiles + TQ_TILE_CTL(nr);
+    const int G = (NT + kTileScanThreads - 1) / kTileScanThreads;
+    const bool tail = MODE == 1 && (int)blockIdx.x >= G;
+    int lo, hi;                                  // this launch's tile range
+    if (MODE == 0) { lo = 0; hi = NT; }
+    else if (!tail) { lo = 0; hi = head_tiles(c); }
+    else { lo = with_tail ? max(tail_first_raw(c), head_tiles(c)) : NT; hi = NT; }
+    const int t0 = lo + (tail ? (int)blockIdx.x - G : (int)blockIdx.x) * kTileScanThreads;
+    if (t0 >= hi) return;
+    // head / full: the sum of every tile before the block; tail: after it
+    long long outside = tail ? sum_range(sums, t0 + kTileScanThreads, hi) : sum_range(sums, 0, t0);
+    const int i = t0 + threadIdx.x;
+    const int v = i < hi ? __ldg(sums + i) : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) outside += __shfl_xor_sync(0xffffffffu, outside, off);
     long long x = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const long long y = __shfl_up_sync(0xffffffffu, x, off);
         if (lane >= off) x += y;
     }
-    __shared__ long long wtot[32];
     if (lane == 31) wtot[w] = x;
-    if (lane == 0) red[w] = before;
+    if (lane == 0) red[w] = outside;
     __syncthreads();
-    long long base = 0, woff = 0, btot = 0;
+    long long out = 0, woff = 0, btot = 0;
     for (int k = 0; k < 32; ++k) {
-        base += red[k];
+        out += red[k];
         woff += k < w ? wtot[k] : 0;
         btot += wtot[k];
     }
-    const long long e = base + woff + x - v;
-    if (i < ntiles) bases[i] = (int32_t)e;
-    if (!HEAD && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        const long long total = base + btot;
+    const long long excl = woff + x - v;                 // within the block
+    int32_t* __restrict__ bases = c.tiles + (MODE == 0 ? TQ_TILE_PAD(nr) : TQ_TILE_EARLY(nr));
+    if (i < hi) bases[i] = (int32_t)(tail ? nnz - (out + btot - excl) : out + excl);
+    if (MODE == 0 && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const long long total = out + btot;
         *indptr_last = (int32_t)total;
-        bases[ntiles] = (int32_t)total;
-        bases[ntiles + 1] = total > 0x7fffffffLL ? 1 : 0;   // overflow flag
+        bases[NT] = (int32_t)total;
+        bases[NT + 1] = total > 0x7fffffffLL ? 1 : 0;   // overflow flag
+        if (ctl[6] && total != (long long)ctl[5]) ctl[4] = 1;   // early tail bases assumed another nnz
+    }
+    if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (nnz >= 0) {                                // the count the caller expects
+            ctl[5] = (int32_t)nnz;
+            ctl[6] = 1;
+        }
+        ctl[7] = with_tail;                            // the tail tiles are early
     }
 }
 
@@ -337,7 +370,7 @@ extern "C" int tq_scan_tiles(tq_rowctx c, int32_t* indptr, int64_t* nnz_h, void*
     const int ntiles = (nrows + 31) / 32;
     int32_t* bases = tq_tile_bases(c.tiles, nrows);
     const int grid = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
-    k_scan_tiles<false><<<grid, kTileScanThreads, 0, st>>>(c, indptr + nrows); ::tq::note_launch();
+    k_scan_tiles<0><<<grid, kTileScanThreads, 0, st>>>(c, indptr + nrows, -1, 0); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_scan_tiles");
     if (nnz_h) {
         int32_t h[2] = {0, 0};
@@ -429,12 +462,13 @@ extern "C" int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* 
     return TQ_OK;
 }
 
-extern "C" int tq_scan_tiles_head(tq_rowctx c, void* stream) {
+extern "C" int tq_scan_tiles_early(tq_rowctx c, int64_t nnz, int32_t tail, void* stream) {
     const int nrows = c.row_end - c.row_begin;
-    if (!c.tiles || !c.counts) { set_error("tq_scan_tiles_head needs the context's counts and tiles"); return TQ_EINVAL; }
+    if (!c.tiles || !c.counts) { set_error("tq_scan_tiles_early needs the context's counts and tiles"); return TQ_EINVAL; }
+    if (nnz > 0x7fffffffLL || (tail && nnz < 0)) { set_error("nnz %lld out of range", (long long)nnz); return TQ_EINVAL; }
     if (nrows <= 0) return TQ_OK;
-    const int grid = (TQ_TILE_NT(nrows) + kTileScanThreads - 1) / kTileScanThreads;
-    k_scan_tiles<true><<<grid, kTileScanThreads, 0, S(stream)>>>(c, nullptr); ::tq::note_launch();
-    TQ_LAUNCH_CHECK("k_scan_tiles_head");
+    const int G = (TQ_TILE_NT(nrows) + kTileScanThreads - 1) / kTileScanThreads;
+    k_scan_tiles<1><<<2 * G, kTileScanThreads, 0, S(stream)>>>(c, nullptr, nnz, tail ? 1 : 0); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_scan_tiles_early");
     return TQ_OK;
 }
