@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-nel", type=int, default=512, help="oracle sample size (mesh) for the CPU legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--profile-eager", action="store_true",
                     help="ncu mode: run the captured schedule eagerly each step (ncu cannot profile launches "
                          "made under stream capture); numbers printed in this mode are not bench values")
@@ -331,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
     if args.e2e_steps > 0:
         knots = np.ascontiguousarray(P.make_uniform_knots(args.nel, args.p).knots)
         ctrl = np.ascontiguousarray(c5["curves"][0].ctrl)
-        e_ts, h2d, d2h = [], 0, 0
+        e_ts, e_ph, h2d, d2h = [], [], 0, 0
         for k in range(args.e2e_steps + 1):
             barrier()
             torch.cuda.synchronize()
@@ -339,6 +339,7 @@ def run_ours(args, rank, world, local_rank):
             kv = P.KnotVector(knots.copy(), args.p)
             bb = P.TensorBasis2D(P.Basis1D(kv), P.Basis1D(P.KnotVector(knots.copy(), args.p)))
             cf = P.classify_elements(bb, [P.trimming.PeriodicBSplineTrim(ctrl.copy())])
+            t1 = time.perf_counter()
             if world == 1:
                 M = P.assemble_mass(bb, cf, None, strategy=args.strategy)
             else:   # row blocks formed per GPU, NCCL gather to rank 0, host copy there
@@ -346,12 +347,14 @@ def run_ours(args, rank, world, local_rank):
                 M = assemble_mass_distributed(bb, cf, None, strategy=args.strategy)
             nnz_e = M.data.nnz if M is not None else 0
             rows_e = M.shape[0] if M is not None else 0
+            t2 = time.perf_counter()
             del M
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             barrier()
             if k > 0:          # first pass warms the allocator / caches
                 e_ts.append(dt)
+                e_ph.append((round(t1 - t0, 4), round(t2 - t1, 4), round(time.perf_counter() - t2, 4)))
             if rank == 0:
                 h2d = knots.nbytes * 2 + ctrl.nbytes
                 d2h = 12 * nnz_e + 4 * (rows_e + 1)
@@ -361,6 +364,9 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": nnz_total / float(et[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(et[0]),
                "step_seconds": [round(x, 4) for x in e_ts],
+               "median_seconds": float(np.median(e_ts)),
+               "phase_seconds": {"classify": [p[0] for p in e_ph], "assemble_mass": [p[1] for p in e_ph],
+                                 "release": [p[2] for p in e_ph]},
                "path": "KnotVector/Basis1D -> classify_elements (GPU) -> cut-cell decomposition (GPU) -> "
                        + ("assemble_mass" if world == 1 else "assemble_mass_distributed (NCCL gather to rank 0)")
                        + " -> scipy CSR on host"}
@@ -386,7 +392,7 @@ def run_ours(args, rank, world, local_rank):
                             "cut_regular": 1e3 * rep.t_cut_regular, "cut_elements": 1e3 * rep.t_cut_elements,
                             "finish": 1e3 * rep.t_finish},
         "step": ("eager run of the captured schedule (--profile-eager: ncu mode, not a bench value)"
-                 if args.profile_eager else "CUDA-graph replay of one full formation pass + residual-flag read-back"),
+                 if args.profile_eager else "CUDA-graph replay of one full formation pass (its status -- fit flags, nnz -- reduced in the graph, read after each step)"),
         "kernels_ms_per_step": {k: v / args.steps for k, v in kms.items()},
         "roofline": {"kernel": "fill: k_fill_tiles with k_fill_irregular concurrent (fused symmetrise + zero-drop + CSR write)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",

@@ -132,10 +132,22 @@ class SparseMatrix:
 
     def __init__(self, data, active, basis2d, device=None):
         self.data = data
-        self.active = active
+        self._active = active          # (K, 2) array, or a callable producing it on first use
         self.basis2d = basis2d
         self.symmetric = True
         self.device = device
+
+    @property
+    def active(self):
+        """(K, 2) active (i1, i2) pairs in row order (src/assembly.py:88-120),
+        fetched from the device on first access."""
+        if callable(self._active):
+            self._active = self._active()
+        return self._active
+
+    @active.setter
+    def active(self, value):
+        self._active = value
 
     @property
     def shape(self):
@@ -377,7 +389,6 @@ class Formation:
         row_end = self.K if row_end is None else row_end
         nrows = row_end - row_begin
         from ._rawrows import join_cut_blocks
-        join_cut_blocks(self)         # the pass-start stream rejoins (capture)
         if self.deep is None and self.a1 is not None:
             n1, n2 = self.basis2d.shape
             # geometric flags: cached per row plan (keyed by its raw-row list)
@@ -428,6 +439,10 @@ class Formation:
                 with torch.cuda.stream(head):
                     L.call("tq_fill_fast_part", ctx, *map(L.ptr, out), 1, HEAD_BLOCKS_PER_SM, L.stream())
                     _stamp("head_fill")
+            # count pass 2 reads raw values: the pass-start stream (Gauss
+            # parts, cut-element blocks) and the cut-row side stream rejoin
+            # here, after pass 1 (which needs neither)
+            join_cut_blocks(self)
             if join is not None:
                 torch.cuda.current_stream().wait_stream(join)
             _stamp("join")
@@ -592,7 +607,7 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
                 setattr(report, k, v)
         report.strategy = strategy
     M = csr.to_scipy((f.K, f.K))
-    return SparseMatrix(M, config.active_functions(), basis2d, device=csr)
+    return SparseMatrix(M, config.active_functions, basis2d, device=csr)
 
 
 def form_with_timings(strategy, basis2d, config, coeff=None, parallel=False):

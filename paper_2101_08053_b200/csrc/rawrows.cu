@@ -15,6 +15,7 @@
 // One warp per row; the row block, the two weighted collocation slices and
 // the inner contraction live in shared memory.
 #include <limits.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -410,6 +411,92 @@ __global__ void k_coeff_points(tq_coeff g, const double* P, int64_t n, const dou
     }
 }
 
+
+// The c == 1 element-Gauss part (PARTS == 1) for p1 == p2 == P: the same
+// window staging, terms and summation order as the generic kernel, with
+// compile-time extents (constant divisions, unrolled predicated element
+// loops) -- the generic version is integer/branch bound.  Rows of other
+// modes get a zero block.
+template <int P>
+__global__ void __launch_bounds__(256) k_raw_gauss_sep(tq_rawctx c, int r0, int r1) {
+    constexpr int Q = P + 1, W = 2 * P + 1, T = W * W, WPB = 8;
+    __shared__ double sE1[WPB][Q * Q], sE2[WPB][Q * Q], sIn[WPB][Q * W];
+    __shared__ int sF1[WPB][Q], sF2[WPB][Q], sMK[WPB][Q * Q];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* E1 = sE1[wib];
+    double* E2 = sE2[wib];
+    double* inner = sIn[wib];
+    int* F1 = sF1[wib];
+    int* F2 = sF2[wib];
+    int* MK = sMK[wib];
+    for (int r = r0 + blockIdx.x * WPB + wib; r < r1; r += gridDim.x * WPB) {
+        const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - i1 * c.n2;
+        double* dst = c.raw + (int64_t)r * T;
+        if (d.mode != TQ_ROW_GAUSS && d.mode != TQ_ROW_BOX) {
+            for (int q = lane; q < T; q += 32) dst[q] = 0.0;
+            continue;
+        }
+        const int ef1 = c.el_first1[i1], ne1 = c.el_last1[i1] - ef1 + 1;
+        const int ef2 = c.el_first2[i2], ne2 = c.el_last2[i2] - ef2 + 1;
+        const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
+        for (int l = lane; l < Q * Q; l += 32) {
+            const int k = l / Q, b = l - k * Q;
+            if (k < ne1) {
+                const int e1 = ef1 + k, f1 = c.espan1[e1] - P;
+                if (b == 0) F1[k] = f1;
+                E1[l] = c.em1[((int64_t)e1 * Q + (i1 - f1)) * Q + b];
+            }
+            if (k < ne2) {
+                const int e2 = ef2 + k, f2 = c.espan2[e2] - P;
+                if (b == 0) F2[k] = f2;
+                E2[l] = c.em2[((int64_t)e2 * Q + (i2 - f2)) * Q + b];
+            }
+            // interior flag of element (ef1 + k, ef2 + b), outside the box
+            bool ok = false;
+            if (k < ne1 && b < ne2) {
+                const int e1 = ef1 + k, e2 = ef2 + b;
+                ok = c.elem_class[(int64_t)e1 * c.nel2 + e2] == TQ_INTERIOR;
+                if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) ok = false;
+            }
+            MK[l] = ok ? 1 : 0;
+        }
+        __syncwarp();
+        for (int t = lane; t < Q * W; t += 32) {
+            const int k1 = t / W, o2 = t - k1 * W;
+            const int j2 = i2 - P + o2;
+            double acc = 0.0;
+            if (k1 < ne1 && j2 >= 0 && j2 < c.n2) {
+#pragma unroll
+                for (int k2 = 0; k2 < Q; ++k2) {
+                    if (k2 >= ne2 || !MK[k1 * Q + k2]) continue;
+                    const int b2 = j2 - F2[k2];
+                    if (b2 < 0 || b2 > P) continue;
+                    acc += E2[k2 * Q + b2];
+                }
+            }
+            inner[t] = acc;
+        }
+        __syncwarp();
+        for (int q = lane; q < T; q += 32) {
+            const int o1 = q / W, o2 = q - o1 * W;
+            const int j1 = i1 - P + o1;
+            double acc = 0.0;
+            if (j1 >= 0 && j1 < c.n1) {
+#pragma unroll
+                for (int k1 = 0; k1 < Q; ++k1) {
+                    if (k1 >= ne1) continue;
+                    const int b1 = j1 - F1[k1];
+                    if (b1 < 0 || b1 > P) continue;
+                    acc += E1[k1 * Q + b1] * inner[k1 * W + o2];
+                }
+            }
+            dst[q] = 0.0 + acc;          // the generic kernel's zeroed block plus the sum
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace tq
 
 using namespace tq;
@@ -440,6 +527,18 @@ extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream)
 }
 
 extern "C" int tq_raw_gauss(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    static const bool generic = getenv("TQ_RAW_GAUSS_GENERIC") != nullptr;   // A/B and the parity test
+    if (r1 > r0 && !generic && !c.cg && c.p1 == c.p2 && c.p1 >= 1 && c.p1 <= 8) {
+        const int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 16);
+        switch (c.p1) {
+#define CASE(Q) case Q: k_raw_gauss_sep<Q><<<grid, 256, 0, S(stream)>>>(c, r0, r1); break;
+            CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+        }
+        ::tq::note_launch();
+        TQ_LAUNCH_CHECK("k_raw_gauss_sep");
+        return TQ_OK;
+    }
     return raw_regular_launch<1>(c, r0, r1, stream);
 }
 

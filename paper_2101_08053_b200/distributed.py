@@ -102,7 +102,7 @@ def assemble_mass_distributed(basis2d, config, coeff=None, strategy="dwq", root=
         return None
     ptr, ind, dat = (t.cpu().numpy() for t in out)
     M = sp.csr_matrix((dat, ind, ptr), shape=(f.K, f.K))
-    return SparseMatrix(M, config.active_functions(), basis2d)
+    return SparseMatrix(M, config.active_functions, basis2d)
 
 
 def l2_error_distributed(coeffs, problem, group=None):
