@@ -52,6 +52,23 @@ __device__ __forceinline__ int tile_offset(const tq_rowctx& c, int r, int lane) 
     return __ldg((c.tiles + TQ_TILE_PAD(c.row_end - c.row_begin)) + (rel >> 5)) + __reduce_add_sync(0xffffffffu, cnt);
 }
 
+// floor(x / n) for 0 <= x < 2^24 and n >= 1: float reciprocal, one
+// correction step (exact: the float estimate is off by at most one)
+__device__ __forceinline__ int fdiv24(int x, int n, float inv) {
+    int q = __float2int_rz(__int2float_rn(x) * inv);
+    const int r = x - q * n;
+    q += (r >= n) - (r < 0);
+    return q;
+}
+
+// i1 = idx / n2 for a function index (float path when n1 * n2 < 2^24)
+__device__ __forceinline__ int row_of(const tq_rowctx& c, int idx) {
+    return c.n1 * c.n2 < (1 << 24) ? fdiv24(idx, c.n2, __frcp_rn((float)c.n2)) : idx / c.n2;
+}
+
+// q1 = e / t2 for a window entry (e < 2^24)
+__device__ __forceinline__ int win_div(int e, int t2, float inv_t2) { return fdiv24(e, t2, inv_t2); }
+
 struct RowGeom {
     int i1, i2, s_i, j1lo, j2lo, t1, t2;
 };
@@ -59,7 +76,7 @@ struct RowGeom {
 __device__ inline RowGeom row_geom(const tq_rowctx& c, int r) {
     RowGeom g;
     int idx = c.active[r];
-    g.i1 = idx / c.n2;
+    g.i1 = row_of(c, idx);
     g.i2 = idx - g.i1 * c.n2;
     g.s_i = c.slot[idx];
     g.j1lo = c.ov_lo1[g.i1];
@@ -82,7 +99,7 @@ __device__ __forceinline__ double raw_value(const tq_rowctx& c, int i1, int i2, 
 
 // symmetrised sum M_ij + M_ji for column j; returns col index or -1
 __device__ __forceinline__ int entry(const tq_rowctx& c, const RowGeom& g, int e, double& v) {
-    int q1 = e / g.t2;
+    int q1 = win_div(e, g.t2, __frcp_rn((float)g.t2));
     int j1 = g.j1lo + q1, j2 = g.j2lo + (e - q1 * g.t2);
     int jidx = j1 * c.n2 + j2;
     int col = __ldg(c.col_of + jidx);
@@ -107,7 +124,7 @@ __device__ __forceinline__ void entries_batch(const tq_rowctx& c, const RowGeom&
         const int e = e0 + 32 * u + lane;
         const bool valid = e < n;
         const int ee = valid ? e : 0;
-        const int q1 = ee / g.t2;
+        const int q1 = win_div(ee, g.t2, __frcp_rn((float)g.t2));
         j1[u] = g.j1lo + q1;
         j2[u] = g.j2lo + (ee - q1 * g.t2);
         const int jidx = j1[u] * c.n2 + j2[u];
@@ -149,7 +166,7 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
         int mycount = 0;      // list-A rows: added by pass 2
         if (r < c.row_end) {
             const int idx = __ldg(c.active + r);
-            const int i1 = idx / c.n2, i2 = idx - (idx / c.n2) * c.n2;
+            const int i1 = row_of(c, idx), i2 = idx - i1 * c.n2;
             bool deep;
             if (GEO) deep = __ldg(geo + idx) && __ldg(pos + i1) && __ldg(pos + c.n1 + i2);
             else deep = c.deep && __ldg(c.deep + idx);
@@ -206,7 +223,7 @@ __device__ __forceinline__ void entries_rows(const tq_rowctx& c, const RowGeom* 
         const int e = 32 * (u % 3) + lane;
         const bool valid = ok[u / 3] && e < n;
         const int ee = valid ? e : 0;
-        const int q1 = ee / G.t2;
+        const int q1 = win_div(ee, G.t2, __frcp_rn((float)G.t2));
         j1[u] = G.j1lo + q1;
         j2[u] = G.j2lo + (ee - q1 * G.t2);
         const int jidx = j1[u] * c.n2 + j2[u];
@@ -556,7 +573,7 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
             for (int e0 = 0; e0 < n; e0 += 32) {
                 const int e = e0 + lane;
                 const int ee = e < n ? e : n - 1;
-                const int q1 = ee / g.t2, q2 = ee - q1 * g.t2;
+                const int q1 = win_div(ee, g.t2, __frcp_rn((float)g.t2)), q2 = ee - q1 * g.t2;
                 const int o1 = off1 + q1, o2 = off2 + q2;
                 const double a1 = __shfl_sync(0xffffffffu, A1, o1), a1t = __shfl_sync(0xffffffffu, A1T, o1);
                 const double a2 = __shfl_sync(0xffffffffu, A2, o2), a2t = __shfl_sync(0xffffffffu, A2T, o2);
