@@ -477,9 +477,11 @@ class Formation:
 
 
 STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
-# captured passes fill the tiles before the first list-A row early, on a
-# low-priority stream with this many fill blocks per SM (tuning knobs)
-HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "1"))
+# captured passes can fill the tiles before the first list-A row early, on a
+# low-priority stream with this many fill blocks per SM (tuning knobs; off by
+# default since the single-stage fill: the early fill's memory traffic slows
+# the latency-bound count pass 2 by more than it saves, measured at config 5)
+HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "0"))
 HEAD_BLOCKS_PER_SM = int(os.environ.get("TQ_HEAD_BPS", "3"))
 # ... and the tiles after the last list-A row too (their offsets from the
 # captured nnz): measured slower at config 5 (the early fill then delays the

@@ -311,7 +311,7 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 //    contiguous band, so a single round of coalesced loads feeds 32 rows.
 //    Rows are built in shared memory, kChunk rows at a time, lane -> (q1, q2)
 //    with q2 = lane % W fixed, and written to HBM by TMA bulk copies
-//    (cp.async.bulk.global.shared::cta), double-buffered per warp; the
+//    (cp.async.bulk.global.shared::cta), one staging buffer per warp (more resident warps beat double buffering); the
 //    16-byte-unaligned ends go through plain stores.
 //  irregular tile -- recorded in a list and processed by k_fill_irregular,
 //    one warp per row over the whole GPU (these tiles cluster along the
@@ -319,12 +319,15 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 // ---------------------------------------------------------------------------
 constexpr int kWarpRows = 32;
 #ifndef TQ_FILL_STAGES
-#define TQ_FILL_STAGES 2
+#define TQ_FILL_STAGES 1     // one staging buffer per warp: more resident warps beat double buffering (measured)
 #endif
 
+#ifndef TQ_FILL_ENTRIES
+#define TQ_FILL_ENTRIES 891
+#endif
 template <int P>
-constexpr int fill_chunk() {   // rows per bulk copy: ~7.8 KB of staged entries (measured best at P = 4)
-    return 648 / ((2 * P + 1) * (2 * P + 1)) < 1 ? 1 : (648 / ((2 * P + 1) * (2 * P + 1)) > 32 ? 32 : 648 / ((2 * P + 1) * (2 * P + 1)));
+constexpr int fill_chunk() {   // rows per bulk copy: ~10.7 KB of staged entries (11 rows at P = 4, measured best)
+    return TQ_FILL_ENTRIES / ((2 * P + 1) * (2 * P + 1)) < 1 ? 1 : (TQ_FILL_ENTRIES / ((2 * P + 1) * (2 * P + 1)) > 32 ? 32 : TQ_FILL_ENTRIES / ((2 * P + 1) * (2 * P + 1)));
 }
 
 template <int P>
