@@ -369,6 +369,20 @@ void tq_cutcell_free(void* handle);
 int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
                       const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t* ptr,
                       double* pts, double* w, int32_t* ncells, int32_t* status, void* stream);
+/* single-decomposition schedule.  Slot pass: element z writes up to `cap`
+ * points into slot_pts[2*cap*z ..] / slot_w[cap*z ..] and, as the count
+ * pass above, ptr[z+1], ncells[z] and status[z] (its full count, also when
+ * it exceeds cap).  The caller scans ptr, then the pack call copies every
+ * slot within capacity to its offsets and, when any_overflow != 0,
+ * decomposes again (write mode) the elements whose count exceeds cap. */
+int tq_cutcell_device_slots(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
+                            const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t cap,
+                            double* slot_pts, double* slot_w, int64_t* ptr, int32_t* ncells, int32_t* status,
+                            void* stream);
+int tq_cutcell_device_pack(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
+                           const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t cap,
+                           const double* slot_pts, const double* slot_w, const int64_t* ptr, double* pts,
+                           double* w, int32_t any_overflow, void* stream);
 
 /* ---- L2 projection: RHS and error ---------------------------------------- */
 

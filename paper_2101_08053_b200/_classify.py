@@ -59,17 +59,41 @@ def cell_tables(q):
 
 
 class CutCellRule:
-    """Cut-element quadrature (src/trimming.py:749-766) with packed arrays."""
+    """Cut-element quadrature (src/trimming.py:749-766) with packed arrays.
+    A rule decomposed on the device keeps its arrays there (``dev``); the
+    host copies are made on first use."""
 
-    def __init__(self, q, elements, ptr, pts, wts, ncells):
+    def __init__(self, q, elements, ptr, pts, wts, ncells, dev=None):
         self.q = q
         self.elements = elements          # (ncut, 2) row-major element order
-        self.ptr = ptr                    # (ncut+1) int64
-        self.points = pts                 # (P, 2)
-        self.weights = wts                # (P,)
-        self._ncells = ncells
+        self._host = None if dev is not None else (ptr, pts, wts, ncells)
+        self.dev = dev
+        self._npts = int(ptr[-1]) if dev is None else dev["npts"]
         self._rules = None
         self._counts = None
+
+    def _h(self):
+        if self._host is None:
+            d = self.dev
+            self._host = (d["ptr"].cpu().numpy(), d["P"].cpu().numpy(), d["W"].cpu().numpy(),
+                          d["ncells"].cpu().numpy())
+        return self._host
+
+    @property
+    def ptr(self):                        # (ncut+1) int64
+        return self._h()[0]
+
+    @property
+    def points(self):                     # (P, 2)
+        return self._h()[1]
+
+    @property
+    def weights(self):                    # (P,)
+        return self._h()[2]
+
+    @property
+    def _ncells(self):
+        return self._h()[3]
 
     @property
     def rules(self):
@@ -90,7 +114,7 @@ class CutCellRule:
         return self.rules[(e1, e2)]
 
     def total_points(self):
-        return int(self.ptr[-1])
+        return self._npts
 
     def all_points(self):
         return self.points
@@ -123,10 +147,18 @@ _CUT_ERRORS = {1: "cannot decompose cell at maximum split depth 4", 2: "folded s
                3: "cell is not crossed by exactly one curve", 4: "cut-cell capacity exceeded"}
 
 
-def cut_cell_rule_device(config, q):
-    """Cut-element quadrature decomposed on the GPU (tq_cutcell_device, one
-    thread per cut element; same decomposition as the host C++).  The
-    rule's device arrays are kept on it (``rule.dev``) for the formation."""
+# slot capacity of the single-decomposition schedule, in sub-cells of
+# (q+1)^2 points (config 5 averages 1.7 sub-cells per cut element)
+SLOT_CELLS = 4
+
+
+def cut_cell_rule_device(config, q, slot_cells=None):
+    """Cut-element quadrature decomposed on the GPU (one thread per cut
+    element; same decomposition as the host C++): one decomposition into
+    fixed-capacity slots (tq_cutcell_device_slots), one read-back of the
+    status and point count, then the slots are packed to their offsets
+    (tq_cutcell_device_pack; overflowing elements are decomposed again).
+    The rule's device arrays are kept on it (``rule.dev``)."""
     if q < 1:
         raise ValueError("Lagrange degree q must be >= 1")
     b1, b2 = config.basis2d.dir
@@ -136,38 +168,37 @@ def cut_cell_rule_device(config, q):
     dev = el.device
     arr, keep = curve_array(config.curves)
     tabs = cell_tables(q)
-    lib = L.lib()
-    fn = lib.tq_cutcell_device
-    fn.argtypes = [C.POINTER(L.Curve), L.i32, L.vp, L.vp, L.vp, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp]
-    fn.restype = L.i32
     bp1, bp2 = b1.device_arrays()["bp"], b2.device_arrays()["bp"]
+    cap = (SLOT_CELLS if slot_cells is None else slot_cells) * (q + 1) ** 2
     ptr = torch.zeros(ncut + 1, dtype=torch.int64, device=dev)
     ncells = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
     status = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
-
-    def run(pts, w):
-        rc = fn(arr, len(config.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q,
-                tabs.ctypes.data_as(L.vp), L.ptr(ptr), L.ptr(pts), L.ptr(w), L.ptr(ncells), L.ptr(status),
-                L.stream())
-        if rc != L.TQ_OK:
-            raise L._EXC.get(rc, RuntimeError)(lib.tq_last_error().decode(errors="replace"))
-
-    run(None, None)                              # count pass
+    sP = torch.empty(max(ncut, 1) * cap * 2, dtype=torch.float64, device=dev)
+    sW = torch.empty(max(ncut, 1) * cap, dtype=torch.float64, device=dev)
+    common = (arr, len(config.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q, tabs.ctypes.data_as(L.vp), cap)
+    L.call("tq_cutcell_device_slots", *common, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(ncells), L.ptr(status),
+           L.stream())
+    over = 0
     if ncut:
-        bad = torch.nonzero(status[:ncut]).flatten()
-        if bad.numel():
+        cnt = ptr[1:]
+        summary = torch.stack([status[:ncut].max().to(torch.int64), cnt.max(), cnt.sum()]).cpu().tolist()
+        if summary[0]:
+            bad = torch.nonzero(status[:ncut]).flatten()
             z = int(bad[0])
             e1, e2 = (int(v) for v in el[z].tolist())
             raise TrimmingConfigurationError(f"element ({e1}, {e2}): {_CUT_ERRORS.get(int(status[z]), 'error')}")
-        ptr[1:] = torch.cumsum(ptr[1:], 0)
-    npts = int(ptr[-1].item())
+        over = int(summary[1] > cap)
+        ptr[1:] = torch.cumsum(cnt, 0)
+        npts = int(summary[2])
+    else:
+        npts = 0
     P = torch.empty((max(npts, 1), 2), dtype=torch.float64, device=dev)
     W = torch.empty(max(npts, 1), dtype=torch.float64, device=dev)
-    run(P, W)                                    # write pass
-    rule = CutCellRule(q, el.long().cpu().numpy().reshape(-1, 2), ptr.cpu().numpy(), P[:npts].cpu().numpy(),
-                       W[:npts].cpu().numpy(), ncells[:ncut].cpu().numpy())
-    rule.dev = dict(P=P[:npts], W=W[:npts], ptr=ptr, el=el)
-    return rule
+    L.call("tq_cutcell_device_pack", *common, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(P), L.ptr(W), over,
+           L.stream())
+    elements = el.long().cpu().numpy().reshape(-1, 2)
+    return CutCellRule(q, elements, None, None, None, None,
+                       dev=dict(P=P[:npts], W=W[:npts], ptr=ptr, el=el, ncells=ncells[:ncut], npts=npts))
 
 
 def cut_cell_rule(config, q, host_only=False):

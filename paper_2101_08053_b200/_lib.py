@@ -108,6 +108,11 @@ def lib():
         "tq_spmv": ([vp, vp, vp, i32, vp, vp, vp, vp, vp], i32),
         "tq_cg_workspace_bytes": ([i32], i64),
         "tq_cg_scaled": ([vp, vp, vp, i32, vp, vp, vp, C.c_double, i32, vp, vp, vp, vp], i32),
+        "tq_cutcell_device": ([C.POINTER(Curve), i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp], i32),
+        "tq_cutcell_device_slots": ([C.POINTER(Curve), i32, vp, vp, vp, i32, i32, vp, i64, vp, vp, vp, vp, vp,
+                                     vp], i32),
+        "tq_cutcell_device_pack": ([C.POINTER(Curve), i32, vp, vp, vp, i32, i32, vp, i64, vp, vp, vp, vp, vp, i32,
+                                    vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -368,6 +368,13 @@ class Formation:
         the count pass concurrently on a side stream."""
         from ._rawrows import _named_stream
         main = torch.cuda.current_stream()
+        ev_side = None
+        if FILL_EVENTS is not None:
+            # fill-start timing event (external: an event node when captured)
+            # on its own branch, so no node is added to the fill's critical path
+            ev_side = _named_stream("fill_event", priority=0)
+            ev_side.wait_stream(main)
+            FILL_EVENTS[0].record(ev_side)
         # lowest priority: the tile fill's warps dispatch first, the listed
         # rows take the slots it leaves (measured best)
         side = _named_stream("fill_listed", priority=0)
@@ -378,6 +385,8 @@ class Formation:
         L.call("tq_fill_fast_part", ctx, L.ptr(indptr), L.ptr(indices), L.ptr(data), part, 0, L.stream())
         _stamp("fill_tiles")
         main.wait_stream(side)
+        if ev_side is not None:
+            main.wait_stream(ev_side)
         if not torch.cuda.is_current_stream_capturing():
             for t in (indptr, indices, data, self.work) + self._count_bufs:
                 t.record_stream(side)
@@ -495,19 +504,20 @@ def _stamp(name):
 
 
 def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_range=None, timer=None,
-         capture=None):
+         capture=None, timed=True):
     """Run every formation phase on the device; returns (Formation, DeviceCSR).
 
     Eager passes run the phases in order with synchronised phase timers (the
     reference's FormationReport boundaries).  A capture pass (``capture`` =
     dict(nnz=...), used by GraphFormation) schedules the cut-row chain on a
-    side stream, overlapping the deep-row flags and counts."""
+    side stream, overlapping the deep-row flags and counts.  ``timed=False``
+    drops the phase clock's synchronisations (nobody reads the report)."""
     f = Formation(basis2d, config, coeff, strategy, timer, capture)
     f.row_range = row_range        # a row block forms only the raw rows its rows read
     rep = f.report
     if config.has_cuts():     # shared geometry (src/assembly.py:505-508): built on a worker
         config.cut_cell_rule_async(max(basis2d.degrees))   # thread while the fits run
-    clk = _Clock(active=capture is None)
+    clk = _Clock(active=capture is None and timed)
     _stamp("start")
     if capture is not None:
         from ._rawrows import prelaunch_geometry
@@ -543,6 +553,11 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     return f, csr
 
 
+# (start,) timing event recorded where the fill starts while a pass is
+# captured (GraphFormation(fill_events=...)); None otherwise
+FILL_EVENTS = None
+
+
 class GraphFormation:
     """One formation pass captured as a CUDA graph and replayed.
 
@@ -553,7 +568,12 @@ class GraphFormation:
     into the same static device buffers.  The moment-fit residual flags are
     re-checked after each replay (``check()``)."""
 
-    def __init__(self, basis2d, config, coeff=None, strategy="dwq", row_range=None):
+    def __init__(self, basis2d, config, coeff=None, strategy="dwq", row_range=None, fill_events=None):
+        """``fill_events``: an optional 1-tuple holding a timing event
+        created with ``external=True``; it is captured where the fill
+        (tiles and listed rows) starts, on a side branch of the graph, so an
+        event recorded after the replay times the fill inside the step."""
+        global FILL_EVENTS
         self.args = (basis2d, config, coeff, strategy)
         self.row_range = row_range
         f, csr = form(basis2d, config, coeff, strategy, row_range=row_range)
@@ -573,8 +593,12 @@ class GraphFormation:
         n0 = lib.tq_launch_count()
         from ._rawrows import _named_stream
         cap = _named_stream("capture", priority=-2)      # the main chain outranks the bulk side streams
-        with torch.cuda.graph(self.graph, stream=cap):
-            self.f, self.csr = form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
+        FILL_EVENTS = fill_events
+        try:
+            with torch.cuda.graph(self.graph, stream=cap):
+                self.f, self.csr = form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
+        finally:
+            FILL_EVENTS = None
         self.launches_per_pass = int(lib.tq_launch_count() - n0)
         torch.cuda.synchronize()
 
@@ -599,7 +623,7 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
     parallel); ``rules`` imports precomputed weight tables."""
     if strategy not in STRATEGIES:
         raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
-    f, csr = form(basis2d, config, coeff, strategy, rules)
+    f, csr = form(basis2d, config, coeff, strategy, rules, timed=report is not None)
     if report is not None:
         # report-only geometry count (cached per row plan), off the formation path
         from ._rawrows import gauss_element_count, needs_raw

@@ -11,8 +11,16 @@
 // quads) or a 4-way split, depth <= 4.  Exceptions become status codes,
 // recursion an explicit depth-first stack (the host's visiting order),
 // vectors fixed-capacity arrays; a sub-decomposition that folds rolls its
-// output back.  Two passes: count the points of every element, then write
-// them at the scanned offsets.  Compiled with -fmad=false like the host code.
+// output back.  Compiled with -fmad=false like the host code.
+//
+// Two schedules:
+//  * tq_cutcell_device: count the points of every element, then write them
+//    at the scanned offsets (two full decompositions);
+//  * tq_cutcell_device_slots + tq_cutcell_device_pack: one decomposition per
+//    element into a fixed-capacity slot (and its count), then a warp-per-
+//    element copy of the slots to the scanned offsets; only elements whose
+//    points overflow their slot are decomposed again, in write mode.
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -49,8 +57,9 @@ struct Sink {
     double* W;
     int64_t pos;
     int cells;
+    int64_t cap;      // writes stop at cap (slot mode); counting goes on
     __device__ void put(double x, double y, double w) {
-        if (P) {
+        if (P && pos < cap) {
             P[2 * pos] = x;
             P[2 * pos + 1] = y;
             W[pos] = w;
@@ -421,12 +430,17 @@ __device__ inline CurveC shifted(const CurveC& c) {
 }
 
 // status: 0 ok, 1 max split depth, 2 folded, 3 not crossed by exactly one curve, 4 capacity
+// mode 0: count (P null) or write at ptr[z] (P set); mode 1: write into the
+// element's slot of `cap` points and count; mode 2: write at ptr[z] only the
+// elements whose count overflowed their slot
 __global__ void k_cutcells(const CurveC* __restrict__ cvs, int ncurves, const double* __restrict__ bp1,
                            const double* __restrict__ bp2, const int32_t* __restrict__ cut_el, int ncut,
                            Tabs T, int64_t* __restrict__ ptr, double* __restrict__ P, double* __restrict__ W,
-                           int32_t* __restrict__ ncells, int32_t* __restrict__ status) {
+                           int32_t* __restrict__ ncells, int32_t* __restrict__ status, int mode, int64_t cap) {
     const int z = blockIdx.x * blockDim.x + threadIdx.x;
     if (z >= ncut) return;
+    if (mode == 2 && ptr[z + 1] - ptr[z] <= cap) return;
+    const bool count = mode == 1 || P == nullptr;
     const int e1 = cut_el[2 * z], e2 = cut_el[2 * z + 1];
     const Bd B{bp1[e1], bp1[e1 + 1], bp2[e2], bp2[e2 + 1]};
     int which = 0;
@@ -443,7 +457,10 @@ __global__ void k_cutcells(const CurveC* __restrict__ cvs, int ncurves, const do
         }
         if (nfound != 1) {
             status[z] = 3;
-            if (!P) ptr[z + 1] = 0;
+            if (count) {
+                ptr[z + 1] = 0;
+                ncells[z] = 0;
+            }
             return;
         }
         which = found;
@@ -455,13 +472,30 @@ __global__ void k_cutcells(const CurveC* __restrict__ cvs, int ncurves, const do
         const double tol = 1e-10 * fmax(B.x1 - B.x0, B.y1 - B.y0);
         if (B.x0 - tol <= sx && sx <= B.x1 + tol && B.y0 - tol <= sy && sy <= B.y1 + tol) cv = shifted(cv);
     }
-    Sink s{P, W, P ? ptr[z] : 0, 0};
+    Sink s = mode == 1 ? Sink{P + 2 * cap * z, W + cap * z, 0, 0, cap}
+                       : Sink{P, W, P ? ptr[z] : 0, 0, INT64_MAX};
     const int r = decompose(B, cv, cv.kind == TQ_CURVE_LINE, T, s);
+    if (mode == 2) return;
     status[z] = r == kWrote ? 0 : (r == kTrim ? 1 : (r == kFold ? 2 : 4));
-    if (!P) {
+    if (count) {
         ptr[z + 1] = r == kWrote ? s.pos : 0;
         ncells[z] = r == kWrote ? s.cells : 0;
     }
+}
+
+// warp per element: slot -> scanned offsets (elements within capacity)
+__global__ void k_cutcell_pack(const double* __restrict__ sP, const double* __restrict__ sW, int64_t cap,
+                               const int64_t* __restrict__ ptr, int ncut, double* __restrict__ P,
+                               double* __restrict__ W) {
+    const int lane = threadIdx.x & 31;
+    const int z = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (z >= ncut) return;
+    const int64_t o = ptr[z], n = ptr[z + 1] - o;
+    if (n > cap) return;
+    const double* sp = sP + 2 * cap * z;
+    const double* sw = sW + cap * z;
+    for (int64_t k = lane; k < 2 * n; k += 32) P[2 * o + k] = sp[k];
+    for (int64_t k = lane; k < n; k += 32) W[o + k] = sw[k];
 }
 
 }  // namespace ccd
@@ -469,12 +503,15 @@ __global__ void k_cutcells(const CurveC* __restrict__ cvs, int ncurves, const do
 
 using namespace tq;
 
-extern "C" int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
-                                 const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t* ptr,
-                                 double* pts, double* w, int32_t* ncells, int32_t* status, void* stream) {
-    if (ncut <= 0) return TQ_OK;
+namespace {
+
+// one upload of curve tables, curve structs and cell tables; runs `launch`
+// with them, frees the upload and synchronises the stream (the host
+// staging buffer must outlive the copy)
+template <class F>
+int with_uploaded(const tq_curve* curves_h, int32_t ncurves, int32_t q, const double* tabs_h, cudaStream_t st,
+                  F&& launch) {
     if (q < 1 || q > ccd::kQMax) { set_error("cut-cell Lagrange degree %d outside 1..%d", q, ccd::kQMax); return TQ_EINVAL; }
-    cudaStream_t st = S(stream);
     std::vector<CurveC> cv;
     std::vector<double> buf;
     if (!compile_curves(curves_h, ncurves, cv, buf)) {
@@ -483,7 +520,6 @@ extern "C" int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, cons
     }
     const int ng = q + 1;
     const size_t ntab = (size_t)(q + 1) + 2 * ng + 2 * (size_t)ng * (q + 1);
-    // one upload: curve tables, curve structs, cell tables
     const size_t nb = std::max<size_t>(buf.size(), 1);
     const size_t bytes = nb * sizeof(double) + cv.size() * sizeof(CurveC) + ntab * sizeof(double);
     std::vector<unsigned char> host(bytes);
@@ -499,11 +535,58 @@ extern "C" int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, cons
     TQ_CUDA(cudaMemcpyAsync(dev, host.data(), bytes, cudaMemcpyHostToDevice, st));
     ccd::Tabs T{q, dtab, dtab + (q + 1), dtab + (q + 1) + ng, dtab + (q + 1) + 2 * ng,
                 dtab + (q + 1) + 2 * ng + ng * (q + 1)};
-    ccd::k_cutcells<<<(ncut + 63) / 64, 64, 0, st>>>(dcv, ncurves, bp1, bp2, cut_el, ncut, T, ptr, pts, w, ncells,
-                                                     status);
-    ::tq::note_launch();
+    launch(dcv, T);
     TQ_LAUNCH_CHECK("k_cutcells");
     TQ_CUDA(cudaFreeAsync(dev, st));
-    TQ_CUDA(cudaStreamSynchronize(st));      // the host staging buffer must outlive the copy
+    TQ_CUDA(cudaStreamSynchronize(st));
     return TQ_OK;
+}
+
+constexpr int kCutBlock = 16;     // 5.3 K cut elements at config 5: spread over every SM
+
+}  // namespace
+
+extern "C" int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
+                                 const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t* ptr,
+                                 double* pts, double* w, int32_t* ncells, int32_t* status, void* stream) {
+    if (ncut <= 0) return TQ_OK;
+    cudaStream_t st = S(stream);
+    return with_uploaded(curves_h, ncurves, q, tabs_h, st, [&](const CurveC* dcv, const ccd::Tabs& T) {
+        ccd::k_cutcells<<<(ncut + kCutBlock - 1) / kCutBlock, kCutBlock, 0, st>>>(
+            dcv, ncurves, bp1, bp2, cut_el, ncut, T, ptr, pts, w, ncells, status, 0, 0);
+        ::tq::note_launch();
+    });
+}
+
+extern "C" int tq_cutcell_device_slots(const tq_curve* curves_h, int32_t ncurves, const double* bp1,
+                                       const double* bp2, const int32_t* cut_el, int32_t ncut, int32_t q,
+                                       const double* tabs_h, int64_t cap, double* slot_pts, double* slot_w,
+                                       int64_t* ptr, int32_t* ncells, int32_t* status, void* stream) {
+    if (ncut <= 0) return TQ_OK;
+    if (cap < 1) { set_error("cut-cell slot capacity must be >= 1"); return TQ_EINVAL; }
+    cudaStream_t st = S(stream);
+    return with_uploaded(curves_h, ncurves, q, tabs_h, st, [&](const CurveC* dcv, const ccd::Tabs& T) {
+        ccd::k_cutcells<<<(ncut + kCutBlock - 1) / kCutBlock, kCutBlock, 0, st>>>(
+            dcv, ncurves, bp1, bp2, cut_el, ncut, T, ptr, slot_pts, slot_w, ncells, status, 1, cap);
+        ::tq::note_launch();
+    });
+}
+
+extern "C" int tq_cutcell_device_pack(const tq_curve* curves_h, int32_t ncurves, const double* bp1,
+                                      const double* bp2, const int32_t* cut_el, int32_t ncut, int32_t q,
+                                      const double* tabs_h, int64_t cap, const double* slot_pts,
+                                      const double* slot_w, const int64_t* ptr, double* pts, double* w,
+                                      int32_t any_overflow, void* stream) {
+    if (ncut <= 0) return TQ_OK;
+    cudaStream_t st = S(stream);
+    ccd::k_cutcell_pack<<<(ncut + 7) / 8, 256, 0, st>>>(slot_pts, slot_w, cap, ptr, ncut, pts, w);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_cutcell_pack");
+    if (!any_overflow) return TQ_OK;
+    return with_uploaded(curves_h, ncurves, q, tabs_h, st, [&](const CurveC* dcv, const ccd::Tabs& T) {
+        ccd::k_cutcells<<<(ncut + kCutBlock - 1) / kCutBlock, kCutBlock, 0, st>>>(
+            dcv, ncurves, bp1, bp2, cut_el, ncut, T, const_cast<int64_t*>(ptr), pts, w, nullptr, nullptr, 2,
+            cap);
+        ::tq::note_launch();
+    });
 }

@@ -35,6 +35,43 @@ def test_device_matches_host_decomposition(kind, nel, q):
         assert np.array_equal(rd.points, rh.points) and np.array_equal(rd.weights, rh.weights)
 
 
+@pytest.mark.parametrize("slot_cells", [1, 2])
+@pytest.mark.parametrize("kind,nel,q", [("corner", 10, 3), ("bspline", 128, 4), ("ccircle", 64, 3)])
+def test_slot_overflow_matches_two_pass(kind, nel, q, slot_cells):
+    """Small slots force the re-decomposition of overflowing elements
+    (tq_cutcell_device_pack, any_overflow); the packed rule equals the
+    two-pass schedule (tq_cutcell_device) bit for bit."""
+    import ctypes as Ct
+    import torch
+    from paper_2101_08053_b200 import _classify as K, _lib as L
+    b2d, cfg = _space(kind, nel, min(q, 6))
+    rd = K.cut_cell_rule_device(cfg, q, slot_cells=slot_cells)
+    d = rd.dev
+    n = np.diff(rd.ptr)
+    assert slot_cells > 1 or n.max() > (q + 1) ** 2          # some element overflowed its slot
+    # two-pass schedule on the same elements
+    b1, b2 = cfg.basis2d.dir
+    el = d["el"]
+    ncut = el.shape[0]
+    arr, keep = K.curve_array(cfg.curves)
+    tabs = K.cell_tables(q)
+    bp1, bp2 = b1.device_arrays()["bp"], b2.device_arrays()["bp"]
+    ptr = torch.zeros(ncut + 1, dtype=torch.int64, device=el.device)
+    nc = torch.zeros(ncut, dtype=torch.int32, device=el.device)
+    st = torch.zeros(ncut, dtype=torch.int32, device=el.device)
+    args = (arr, len(cfg.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q, tabs.ctypes.data_as(L.vp))
+    L.call("tq_cutcell_device", *args, L.ptr(ptr), None, None, L.ptr(nc), L.ptr(st), L.stream())
+    ptr[1:] = torch.cumsum(ptr[1:], 0)
+    npts = int(ptr[-1])
+    P = torch.empty((npts, 2), dtype=torch.float64, device=el.device)
+    W = torch.empty(npts, dtype=torch.float64, device=el.device)
+    L.call("tq_cutcell_device", *args, L.ptr(ptr), L.ptr(P), L.ptr(W), L.ptr(nc), L.ptr(st), L.stream())
+    assert int(st.abs().sum()) == 0
+    assert np.array_equal(rd.ptr, ptr.cpu().numpy())
+    assert np.array_equal(rd._ncells, nc.cpu().numpy())
+    assert np.array_equal(rd.points, P.cpu().numpy()) and np.array_equal(rd.weights, W.cpu().numpy())
+
+
 def test_product_uses_device_rule():
     b2d, cfg = _space("ccircle", 32, 3)
     rule = cfg.cut_cell_rule(3)
