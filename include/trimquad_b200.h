@@ -229,6 +229,14 @@ int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* 
  * not-deep split that tq_fill_listed uses, so no deep array is formed. */
 int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* counts, int32_t* work,
                       void* stream);
+/* speculative count pass 1 (tq_row_counts_geo with every line's factors
+ * assumed positive; needs no factor, so it can run before the fits) and its
+ * check: tq_row_counts_verify computes the positivity (pos: n1+n2 bytes,
+ * bad: 1 int scratch) and, only if some line is not positive, redoes the
+ * pass exactly as tq_row_counts_geo (device-side guard). */
+int tq_row_counts_spec(tq_rowctx c, const int8_t* geo, int32_t* counts, int32_t* work, void* stream);
+int tq_row_counts_verify(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* bad, int32_t* counts,
+                         int32_t* work, void* stream);
 int tq_scan_indptr(const int32_t* counts, int32_t nrows, int32_t* indptr,
                    int64_t* nnz_h, void* stream);
 /* the same with caller scratch of tq_scan_workspace_bytes(nrows) bytes */

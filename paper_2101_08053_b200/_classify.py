@@ -214,7 +214,7 @@ def cut_cell_rule(config, q, host_only=False):
     # classes live there; host-only configurations use the host array)
     dev = None if host_only else getattr(config, "element_class_dev", None)
     if dev is not None:
-        nz = torch.nonzero(dev.reshape(config.element_class.shape) == 1)
+        nz = torch.nonzero(dev.reshape(config.num_elements) == 1)
         el = np.ascontiguousarray(nz.to(torch.int32).cpu().numpy()).reshape(-1, 2)
     else:
         e1, e2 = np.nonzero(config.element_class == 1)

@@ -91,6 +91,8 @@ def lib():
         "tq_row_counts_deep": ([RowCtx, vp, vp, vp], i32),
         "tq_row_counts_geo": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
+        "tq_row_counts_spec": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_row_counts_verify": ([RowCtx, vp, vp, vp, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
         "tq_scan_workspace_bytes": ([i32], i64),
         "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
@@ -188,20 +190,27 @@ def ptr(t):
 
 
 _pinned_keep = []
+_PAGEABLE_UPLOADS = os.environ.get("TQ_PAGEABLE_UPLOADS", "0") == "1"     # A/B knob
 
 
 def dev(x, dtype):
-    """Upload a host array (numpy) as a contiguous device tensor.  Under CUDA
-    stream capture the source is pinned and kept alive (the replayed copy
-    reads it again)."""
+    """Upload a host array (numpy) as a contiguous device tensor: staged in
+    pinned memory and copied asynchronously on the current stream (no host
+    sync; torch's caching host allocator keeps the staging block until the
+    copy has run).  Under CUDA stream capture the pinned source is kept alive
+    for good (every replay reads it again)."""
     import numpy as np
     a = np.array(x, copy=True) if not np.asarray(x).flags.writeable else np.ascontiguousarray(x)
     src = torch.from_numpy(np.ascontiguousarray(a))
+    if src.numel() == 0:
+        return torch.empty(src.shape, dtype=dtype, device=device())
+    if _PAGEABLE_UPLOADS and not torch.cuda.is_current_stream_capturing():
+        return src.to(device=device(), dtype=dtype, non_blocking=False).contiguous()
+    src = src.pin_memory()
     if torch.cuda.is_current_stream_capturing():
-        src = src.pin_memory()
         _pinned_keep.append(src)
-        return src.to(device=device(), non_blocking=True).to(dtype)
-    return src.to(device=device(), dtype=dtype, non_blocking=False).contiguous()
+    out = src.to(device=device(), non_blocking=True)
+    return out if out.dtype == dtype else out.to(dtype)
 
 
 def dev_bytes(buf):

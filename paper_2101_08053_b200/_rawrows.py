@@ -548,6 +548,56 @@ def prelaunch_geometry(f):
     f._cut_stream = s
 
 
+# count pass 1 launched speculatively at pass start (captured passes).  Off:
+# measured 0.737 -> 0.743 ms per step at config 5 -- the pre-fill phase is
+# throughput-bound across its concurrent streams, so starting the pass
+# earlier only delays the pass-start streams (the cut-row chain gates the
+# join).  Kept (and tested) for passes where the count pass is the gate.
+SPEC_COUNTS = os.environ.get("TQ_SPEC_COUNTS", "0") == "1"
+
+
+def prelaunch_counts(f):
+    """Count pass 1 of a captured pass at pass start, on its own stream,
+    overlapping the fits: it reads only the cached geometric deep flags and
+    assumes every line's factors positive (tq_row_counts_spec); ``finish``
+    checks the positivity once the factors exist and redoes the pass on the
+    device only if some line is not positive (tq_row_counts_verify).  Needs
+    the geometry cached by an earlier eager pass of the same plan."""
+    if not SPEC_COUNTS or not f.separable():
+        return
+    g = _geo(f.config)
+    raw_list = f.raw_list
+    if needs_raw(f):
+        desc, _ = _plan(f)
+        skey = ("slot", id(desc))
+        if skey not in g:
+            return
+        raw_list = g[skey][1]
+    gkey = ("deep_geo", id(raw_list) if raw_list.numel() else None)
+    if gkey not in g:
+        return
+    rb, re_ = (0, f.K) if f.row_range is None else f.row_range
+    nrows = re_ - rb
+    f.deep = g[gkey][0]
+    spec = dict(rows=(rb, re_),
+                rowfast=torch.empty(max(nrows, 1), dtype=torch.int8, device=f.dev),
+                counts=torch.empty(max(nrows, 1), dtype=torch.int32, device=f.dev),
+                work=torch.empty(2 * nrows + 2, dtype=torch.int32, device=f.dev),
+                tiles=torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=f.dev),
+                bad=torch.empty(1, dtype=torch.int32, device=f.dev))
+    f.rowfast = spec["rowfast"]
+    ctx = f.rowctx(rb, re_)
+    ctx.counts, ctx.tiles = L.ptr(spec["counts"]), L.ptr(spec["tiles"])
+    s = _named_stream("counts_spec", priority=-2)
+    main = torch.cuda.current_stream()
+    with _forked(main, s):
+        L.call("tq_row_counts_spec", ctx, L.ptr(f.deep), L.ptr(spec["counts"]), L.ptr(spec["work"]), L.stream())
+        from .assembly import _stamp
+        _stamp("spec:counts")
+    spec["stream"] = s
+    f._spec = spec
+
+
 def join_cut_blocks(f):
     s = getattr(f, "_cut_stream", None)
     if s is not None:

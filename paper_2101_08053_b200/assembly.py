@@ -414,18 +414,30 @@ class Formation:
             # context carries the geometric flags, no deep array is formed
             self.deep = g[gkey][0]
             _stamp("deep_flags")
-        self.rowfast = torch.empty(max(nrows, 1), dtype=torch.int8, device=self.dev)   # written for every row
+        spec = getattr(self, "_spec", None)
+        if spec is not None and (spec["rows"] != (row_begin, row_end) or self.a1 is None):
+            raise RuntimeError("speculative count pass launched for another row range")
+        if spec is not None:       # count pass 1 ran at pass start (prelaunch_counts)
+            self.rowfast, counts, work, tiles = spec["rowfast"], spec["counts"], spec["work"], spec["tiles"]
+        else:
+            self.rowfast = torch.empty(max(nrows, 1), dtype=torch.int8, device=self.dev)   # written for every row
+            counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
+            work = torch.empty(2 * nrows + 2, dtype=torch.int32, device=self.dev)
+            # tile mode: the count passes leave per-32-row sums, one small scan
+            # turns them into bases and the fill derives (and writes) indptr
+            tiles = torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=self.dev)
         ctx = self.rowctx(row_begin, row_end)
-        counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
-        work = torch.empty(2 * nrows + 2, dtype=torch.int32, device=self.dev)
-        # tile mode: the count passes leave per-32-row sums, one small scan
-        # turns them into bases and the fill derives (and writes) indptr
-        tiles = torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=self.dev)
         ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
         self._count_bufs = (counts, tiles)
         self._nrows = nrows
         with self.timer("counts"):
-            if self.a1 is not None:
+            if spec is not None:
+                # the factors exist now: positivity check, redo only if a line is not positive
+                torch.cuda.current_stream().wait_stream(spec["stream"])
+                pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
+                L.call("tq_row_counts_verify", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(spec["bad"]),
+                       L.ptr(counts), L.ptr(work), L.stream())
+            elif self.a1 is not None:
                 pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
                 L.call("tq_row_counts_geo", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(counts), L.ptr(work),
                        L.stream())
@@ -520,7 +532,8 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     clk = _Clock(active=capture is None and timed)
     _stamp("start")
     if capture is not None:
-        from ._rawrows import prelaunch_geometry
+        from ._rawrows import prelaunch_counts, prelaunch_geometry
+        prelaunch_counts(f)
         prelaunch_geometry(f)
     f.build_weights(rules)
     _stamp("weights")

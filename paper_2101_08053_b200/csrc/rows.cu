@@ -151,11 +151,15 @@ __device__ __forceinline__ void entries_batch(const tq_rowctx& c, const RowGeom&
 // GEO: deep = geo[idx] && pos[i1] && pos[n1 + i2] from the geometric flags
 // and the per-line factor positivity (no deep array is formed); otherwise
 // c.deep holds complete deep flags.
-template <bool GEO>
+// SPEC (with GEO): every line's factors assumed positive (pos not read) --
+// the speculative pass launched before the factors exist; tq_row_counts_verify
+// redoes the pass (guard != 0) only when some line is not positive.
+template <bool GEO, bool SPEC = false>
 __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, const int8_t* __restrict__ pos,
                                   int32_t* __restrict__ counts,
                                   int* __restrict__ list, int* __restrict__ nlist, int* __restrict__ listb,
-                                  int* __restrict__ nlistb) {
+                                  int* __restrict__ nlistb, const int* __restrict__ guard = nullptr) {
+    if (guard && *guard == 0) return;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     // grid-stride loop with a warp-uniform trip count (the appends are warp-aggregated)
@@ -168,7 +172,8 @@ __global__ void k_row_counts_deep(tq_rowctx c, const int8_t* __restrict__ geo, c
             const int idx = __ldg(c.active + r);
             const int i1 = row_of(c, idx), i2 = idx - i1 * c.n2;
             bool deep;
-            if (GEO) deep = __ldg(geo + idx) && __ldg(pos + i1) && __ldg(pos + c.n1 + i2);
+            if (GEO && SPEC) deep = __ldg(geo + idx);
+            else if (GEO) deep = __ldg(geo + idx) && __ldg(pos + i1) && __ldg(pos + c.n1 + i2);
             else deep = c.deep && __ldg(c.deep + idx);
             if (deep) {
                 const int t1 = __ldg(c.ov_hi1 + i1) - __ldg(c.ov_lo1 + i1) + 1;
@@ -638,21 +643,35 @@ __global__ void k_fill_rows(tq_rowctx c, int32_t* __restrict__ indptr, int32_t* 
 }
 
 // both directions in one launch: threads [0, n1) direction 1, [n1, n1+n2) direction 2
-__global__ void k_pos2(tq_rowctx c, int8_t* __restrict__ pos) {
+// per-line factor positivity; `bad` (optional) counts the non-positive lines
+__global__ void k_pos2(tq_rowctx c, int8_t* __restrict__ pos, int* __restrict__ bad = nullptr) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = true;
     if (t < c.n1) {
-        bool ok = true;
         for (int j = c.ov_lo1[t]; j <= c.ov_hi1[t]; ++j)
             ok = ok && c.a1[(int64_t)t * (2 * c.p1 + 1) + (j - t + c.p1)] > 0.0 &&
                  c.a1[(int64_t)j * (2 * c.p1 + 1) + (t - j + c.p1)] > 0.0;
         pos[t] = ok;
     } else if (t < c.n1 + c.n2) {
         const int i = t - c.n1;
-        bool ok = true;
         for (int j = c.ov_lo2[i]; j <= c.ov_hi2[i]; ++j)
             ok = ok && c.a2[(int64_t)i * (2 * c.p2 + 1) + (j - i + c.p2)] > 0.0 &&
                  c.a2[(int64_t)j * (2 * c.p2 + 1) + (i - j + c.p2)] > 0.0;
         pos[t] = ok;
+    }
+    if (bad && !ok) atomicAdd(bad, 1);
+}
+
+// before the redo of a speculative pass (only when some line is not
+// positive): the list counters and the first/last list-A words start over
+__global__ void k_counts_reset_if_bad(const int* __restrict__ bad, int32_t* __restrict__ work,
+                                      int32_t* __restrict__ ctl) {
+    if (*bad == 0) return;
+    work[0] = 0;
+    work[1] = 0;
+    if (ctl) {
+        ctl[0] = 0;
+        ctl[1] = 0;
     }
 }
 
@@ -729,6 +748,39 @@ extern "C" int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, in
     k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
                                                                           work + 2 + nrows, work + 1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_geo");
+    return TQ_OK;
+}
+
+// Speculative count pass 1: tq_row_counts_geo with every line's factors
+// assumed positive, launched from the cached geometric flags before the fits
+// (it needs no factor).  tq_row_counts_verify, after the factors, computes the
+// positivity and redoes the pass only if some line is not positive (device-
+// side guard: no host decision, graph-capturable).  `bad`: 1 int of scratch.
+extern "C" int tq_row_counts_spec(tq_rowctx c, const int8_t* geo, int32_t* counts, int32_t* work, void* stream) {
+    int nrows = c.row_end - c.row_begin;
+    TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
+    if (nrows <= 0) return TQ_OK;
+    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
+    k_row_counts_deep<true, true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, nullptr, counts, work + 2,
+                                                                                work, work + 2 + nrows, work + 1);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_spec");
+    return TQ_OK;
+}
+
+extern "C" int tq_row_counts_verify(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* bad, int32_t* counts,
+                                    int32_t* work, void* stream) {
+    int nrows = c.row_end - c.row_begin;
+    if (nrows <= 0) return TQ_OK;
+    if (!c.a1 || !c.a2) { set_error("tq_row_counts_verify needs the separable factors"); return TQ_EINVAL; }
+    TQ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), S(stream)));
+    k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos, bad); ::tq::note_launch();
+    k_counts_reset_if_bad<<<1, 1, 0, S(stream)>>>(bad, work, c.tiles ? c.tiles + TQ_TILE_CTL(nrows) : nullptr);
+    ::tq::note_launch();
+    k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
+                                                                          work + 2 + nrows, work + 1, bad);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_verify");
     return TQ_OK;
 }
 

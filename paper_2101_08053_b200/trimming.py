@@ -43,6 +43,14 @@ def _integral_image(a):
     return out
 
 
+def _host_copy(t):
+    """Device tensor -> numpy array backed by pinned memory (one DMA)."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
+
+
 class TrimConfiguration:
     """Element and function classification of a trimmed tensor space
     (src/trimming.py:428-594).  Classes are produced on the GPU; host copies
@@ -54,8 +62,8 @@ class TrimConfiguration:
         self.curves = list(curves)
         self.element_class_dev = element_class_dev
         self.func_class_dev = func_class_dev
-        self.element_class = element_class_dev.cpu().numpy()
-        self.func_class = func_class_dev.cpu().numpy()
+        self._element_class = None       # host copies: made on first use
+        self._func_class = None
         b1, b2 = basis2d.dir
         self.u_disc = (np.asarray(b1.breakpoints[1:-1][face1], dtype=float),
                        np.asarray(b2.breakpoints[1:-1][face2], dtype=float))
@@ -67,8 +75,22 @@ class TrimConfiguration:
         self._cum_int = None
 
     @property
+    def element_class(self):
+        """Host copy of the element classes (int8 nel1 x nel2; D2H on first use)."""
+        if self._element_class is None:
+            self._element_class = _host_copy(self.element_class_dev)
+        return self._element_class
+
+    @property
+    def func_class(self):
+        """Host copy of the function classes (int8 n1 x n2; D2H on first use)."""
+        if self._func_class is None:
+            self._func_class = _host_copy(self.func_class_dev)
+        return self._func_class
+
+    @property
     def num_elements(self):
-        return self.element_class.shape
+        return tuple(self.element_class_dev.shape)
 
     def element_bounds(self, e1, e2):
         bp1 = self.basis2d.dir[0].breakpoints
@@ -82,7 +104,10 @@ class TrimConfiguration:
 
     def has_cuts(self):
         if not hasattr(self, "_has_cuts"):
-            self._has_cuts = bool(np.any(self.element_class == CUT))
+            if self._element_class is not None:
+                self._has_cuts = bool(np.any(self._element_class == CUT))
+            else:        # on the device: one flag read back
+                self._has_cuts = bool((self.element_class_dev == CUT).any().item())
         return self._has_cuts
 
     @property

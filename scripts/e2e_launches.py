@@ -22,8 +22,9 @@ def call():
     return M, (round(t1 - t0, 4), round(t2 - t1, 4), round(t3 - t2, 4))
 for _ in range(2):
     call()
-for _ in range(5):
-    print("classify / cut cells / assemble_mass s:", call()[1])
+import numpy as np
+ts = np.array([call()[1] for _ in range(12)])
+print("classify / cut cells / assemble_mass s: median", np.median(ts, 0), "min", ts.min(0))
 if "prof" in sys.argv:
     torch.cuda.cudart().cudaProfilerStart()
     call()

@@ -45,3 +45,63 @@ def test_gauss_part_specialisation_bit_identical(tmp_path, kind, nel, p, strateg
         out[mode] = [z[k] for k in ("arr_0", "arr_1", "arr_2")]
     for a, b in zip(out["sep"], out["generic"]):
         assert np.array_equal(a, b)
+
+
+def _count_state(f, ctx_fn, call):
+    """Run one count-pass-1 variant into fresh buffers; returns the per-row
+    outputs (lists sorted: their append order is scheduling-dependent)."""
+    import torch
+    from paper_2101_08053_b200 import _lib as L
+    K = f.K
+    counts = torch.full((K,), -7, dtype=torch.int32, device=f.dev)
+    work = torch.zeros(2 * K + 2, dtype=torch.int32, device=f.dev)
+    tiles = torch.zeros(L.tile_ints(K), dtype=torch.int32, device=f.dev)
+    f.rowfast = torch.full((K,), 9, dtype=torch.int8, device=f.dev)
+    ctx = ctx_fn()
+    ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
+    call(ctx, counts, work)
+    torch.cuda.synchronize()
+    w = work.cpu().numpy()
+    na, nb = int(w[0]), int(w[1])
+    la = np.sort(w[2:2 + na])
+    lb = np.sort(w[2 + K:2 + K + nb])
+    deep = np.ones(K, bool)
+    deep[la] = False
+    c = counts.cpu().numpy()
+    ctl = L.tile_ctl(K)
+    t = tiles.cpu().numpy()
+    return dict(counts=c[deep], la=la, lb=lb, rowfast=f.rowfast.cpu().numpy(), tiles=t[:(K + 31) // 32],
+                ctl=t[ctl:ctl + 2])
+
+
+@pytest.mark.parametrize("kind,nel,p", [("bspline", 96, 4), ("corner", 24, 2)])
+@pytest.mark.parametrize("spoil", [False, True])
+def test_speculative_count_pass(kind, nel, p, spoil):
+    """tq_row_counts_spec + tq_row_counts_verify against tq_row_counts_geo:
+    identical rows, lists, tile sums and first/last list-A words -- with all
+    lines positive (no redo) and with a factor entry zeroed (the device-side
+    redo runs)."""
+    import torch
+    from paper_2101_08053_b200 import _lib as L, cases as C
+    from paper_2101_08053_b200.assembly import form
+    if kind == "bspline":
+        b2d, cfg = C.build_space(None, nel, p, curves=C.baseline_config(5)["curves"])
+    else:
+        b2d, cfg = C.build_space(kind, nel, p)
+    f, _ = form(b2d, cfg, None, "dwq")
+    assert f.a1 is not None and f.deep is not None
+    if spoil:        # one non-positive line: the speculation is wrong there
+        f.a1 = f.a1.clone()
+        f.a1[f.b1.n // 2, f.b1.p + 1] = 0.0
+    pos = torch.empty(f.b1.n + f.b2.n, dtype=torch.int8, device=f.dev)
+    bad = torch.empty(1, dtype=torch.int32, device=f.dev)
+    ref = _count_state(f, f.rowctx, lambda ctx, c, w: L.call(
+        "tq_row_counts_geo", ctx, L.ptr(f.deep), L.ptr(pos), L.ptr(c), L.ptr(w), L.stream()))
+
+    def spec(ctx, c, w):
+        L.call("tq_row_counts_spec", ctx, L.ptr(f.deep), L.ptr(c), L.ptr(w), L.stream())
+        L.call("tq_row_counts_verify", ctx, L.ptr(f.deep), L.ptr(pos), L.ptr(bad), L.ptr(c), L.ptr(w), L.stream())
+    got = _count_state(f, f.rowctx, spec)
+    assert (int(bad.item()) > 0) == spoil
+    for k in ref:
+        assert np.array_equal(ref[k], got[k]), k
