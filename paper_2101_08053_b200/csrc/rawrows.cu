@@ -92,7 +92,9 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
     const int ni = c.nmax1 > c.p1 + 1 ? c.nmax1 : c.p1 + 1;    // inner rows (sum factorization / Gauss stage 1)
-    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * ni + W1 + W2 + regular_window_slots(c.p1, c.p2);
+    // c != 1: the row's coefficient window is staged too (regular_smem_per_warp)
+    const int per = T + c.nmax1 * W1 + c.nmax2 * W2 + W2 * ni + W1 + W2 + regular_window_slots(c.p1, c.p2) +
+                    (c.grids ? c.nmax1 * c.nmax2 : 0);
     double* blk = sm + (size_t)wib * per;
     double* B1 = blk + T;
     double* B2 = B1 + c.nmax1 * W1;
@@ -106,6 +108,7 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
     int* F1 = reinterpret_cast<int*>(E2 + q2 * q2);
     int* F2 = F1 + q1;
     int* MK = F2 + q2;
+    double* GS = S2 + W2 + regular_window_slots(c.p1, c.p2);    // n1 x n2 coefficient window (c != 1)
 
     for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
         RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
@@ -245,6 +248,35 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
                         int o1 = q / W2, o2 = q - (q / W2) * W2;
                         blk[q] += S1[o1] * S2[o2];
                     }
+                } else if (G) {
+                    // inner[o2][k1] = sum_k2 B2[k2][o2] G[k1][k2] (mask), with the
+                    // row's n1 x n2 window of G (and the mask) staged first:
+                    // one coalesced run per k1 instead of a global load per term
+                    const int ld = s2.lay.npts;
+                    for (int q = lane; q < n1 * n2; q += 32) {
+                        const int k1 = q / n2, k2 = q - k1 * n2;
+                        double g = G[(int64_t)(lo1 + k1) * ld + (lo2 + k2)];
+                        if (d.mode == TQ_ROW_MASK) {
+                            const int e1p = elem_of_point(s1.lay, lo1 + k1), e2p = elem_of_point(s2.lay, lo2 + k2);
+                            if (c.elem_class[(int64_t)e1p * c.nel2 + e2p] != TQ_INTERIOR) g = 0.0;
+                        }
+                        GS[q] = g;
+                    }
+                    __syncwarp();
+                    for (int q = lane; q < W2 * n1; q += 32) {
+                        const int o2 = q / n1, k1 = q - (q / n1) * n1;
+                        const double* gr = GS + k1 * n2;
+                        double acc = 0.0;
+                        for (int k2 = 0; k2 < n2; ++k2) acc += B2[k2 * W2 + o2] * gr[k2];
+                        inner[o2 * n1 + k1] = acc;
+                    }
+                    __syncwarp();
+                    for (int q = lane; q < T; q += 32) {
+                        int o1 = q / W2, o2 = q - (q / W2) * W2;
+                        double acc = 0.0;
+                        for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * n1 + k1];
+                        blk[q] += acc;
+                    }
                 } else {
                     // inner[o2][k1] = sum_k2 B2[k2][o2] G[k1][k2] (mask)
                     const int ld = s2.lay.npts;
@@ -276,6 +308,211 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
         double* dst = c.raw + (int64_t)r * T;
         for (int q = lane; q < T; q += 32) dst[q] = blk[q];
         __syncwarp();
+    }
+}
+
+// The c != 1 element-Gauss part (PARTS == 1 with a coefficient grid): one
+// warp per row, sum factorization over the row's (p1+1) x (p2+1) support
+// elements instead of a (p+1)^2-point loop per block entry.  For each
+// support column e1 (skipped when none of its elements is interior and
+// outside the box):
+//   inner[g1][o2] = sum_{e2 ok} sum_g2 c(e1,g1,e2,g2) w2 V2(e2,g2,a2) V2(e2,g2,b2)
+//   blk[o1][o2]  += sum_g1 w1 V1(e1,g1,a1) V1(e1,g1,b1) inner[g1][o2]
+// (o2 = j2 - i2 + p2, j2 = f2(e2) + b2; o1 likewise): ~(p+1)^4 (2 + (2p+1)/(p+1))
+// FMA per column instead of (p+1)^6.  The row's element window (spans,
+// flags, direction-2 values) is staged once, the column's c slice (one
+// contiguous run per g1) and direction-1 products per column; every stage
+// reads shared memory only.  MASK rows get an all-zero block, like the
+// generic kernel.  Same terms as _Run.element_block (src/assembly.py:310-332)
+// summed in a different order (not bit-identical to the generic kernel).
+__host__ __device__ inline int gauss_coef_slots(int p1, int p2, int ng1, int ng2) {
+    const int q1 = p1 + 1, q2 = p2 + 1, W1 = 2 * p1 + 1, W2 = 2 * p2 + 1;
+    return W1 * W2                       // blk
+           + q2 * ng2 * q2               // V2 window
+           + q2 * ng2                    // w2 V2(a2)
+           + ng1 * q2 * ng2              // c slice x w2 V2(a2), one column
+           + ng1 * W2                    // inner
+           + ng1 * q1                    // w1 V1(a1) V1(b1)
+           + (q1 + q2 + q1 * q2 + 1) / 2 + 1;   // spans and flags (ints)
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int r1) {
+    // one block of NT threads per row (the row's windows are shared by the
+    // whole block: NT/32 times the parallelism of a warp per row for the
+    // same shared memory)
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int p1 = c.p1, p2 = c.p2, q1 = p1 + 1, q2 = p2 + 1, W2 = 2 * p2 + 1, T = (2 * p1 + 1) * W2;
+    const int ng1 = c.ng1, ng2 = c.ng2;
+    double* blk = sm;
+    double* V2 = blk + T;                   // [k2][g2][b2]
+    double* A2 = V2 + q2 * ng2 * q2;        // [k2][g2]
+    double* CV = A2 + q2 * ng2;             // [g1][k2][g2]
+    double* inner = CV + ng1 * q2 * ng2;    // [g1][o2]
+    double* P1 = inner + ng1 * W2;          // [g1][b1]
+    int* F1 = reinterpret_cast<int*>(P1 + ng1 * q1);
+    int* F2 = F1 + q1;
+    int* MK = F2 + q2;
+    const int64_t ld = (int64_t)c.nel2 * ng2;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        double* dst = c.raw + (int64_t)r * T;
+        bool work = d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX;
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const int ef1 = c.el_first1[i1], ne1 = c.el_last1[i1] - ef1 + 1;
+        const int ef2 = c.el_first2[i2], ne2 = c.el_last2[i2] - ef2 + 1;
+        bool mine = false;
+        if (work) {
+            const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
+            for (int k = tid; k < ne1; k += NT) F1[k] = c.espan1[ef1 + k] - p1;
+            for (int k = tid; k < ne2; k += NT) F2[k] = c.espan2[ef2 + k] - p2;
+            for (int l = tid; l < ne1 * ne2; l += NT) {
+                const int k1 = l / ne2, e1 = ef1 + k1, e2 = ef2 + (l - k1 * ne2);
+                bool ok = c.elem_class[(int64_t)e1 * c.nel2 + e2] == TQ_INTERIOR;
+                if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) ok = false;
+                MK[l] = ok ? 1 : 0;
+                mine = mine || ok;
+            }
+        }
+        // rows whose box covers every interior support element (all the
+        // interior rows of the c != 1 BOX plan) have no Gauss part
+        if (!__syncthreads_or(mine)) {
+            for (int q = tid; q < T; q += NT) dst[q] = 0.0;
+            continue;
+        }
+        for (int q = tid; q < T; q += NT) blk[q] = 0.0;
+        // direction-2 window: the elements are consecutive, so their value
+        // tables are one contiguous run
+        const double* v2src = c.ev2 + (int64_t)ef2 * ng2 * q2;
+        for (int l = tid; l < ne2 * ng2 * q2; l += NT) V2[l] = v2src[l];
+        __syncthreads();
+        for (int l = tid; l < ne2 * ng2; l += NT) {
+            const int k2 = l / ng2;
+            A2[l] = c.ew2[(int64_t)ef2 * ng2 + l] * V2[l * q2 + (i2 - F2[k2])];
+        }
+        __syncthreads();
+        for (int k1 = 0; k1 < ne1; ++k1) {
+            bool any = false;
+            for (int k2 = 0; k2 < ne2; ++k2) any = any || MK[k1 * ne2 + k2];
+            if (!any) continue;                 // uniform across the block
+            const int e1 = ef1 + k1, a1 = i1 - F1[k1];
+            for (int l = tid; l < ng1 * ne2 * ng2; l += NT) {
+                const int g1 = l / (ne2 * ng2), m = l - g1 * (ne2 * ng2);
+                CV[l] = c.cg[((int64_t)e1 * ng1 + g1) * ld + (int64_t)ef2 * ng2 + m] * A2[m];
+            }
+            for (int l = tid; l < ng1 * q1; l += NT) {
+                const int g1 = l / q1, b1 = l - g1 * q1;
+                const double* v = c.ev1 + ((int64_t)e1 * ng1 + g1) * q1;
+                P1[l] = (c.ew1[(int64_t)e1 * ng1 + g1] * v[a1]) * v[b1];
+            }
+            __syncthreads();
+            for (int t = tid; t < ng1 * W2; t += NT) {
+                const int g1 = t / W2, o2 = t - g1 * W2;
+                const int j2 = i2 - p2 + o2;
+                double acc = 0.0;
+                for (int k2 = 0; k2 < ne2; ++k2) {
+                    const int b2 = j2 - F2[k2];
+                    if (b2 < 0 || b2 > p2 || !MK[k1 * ne2 + k2]) continue;
+                    const double* cv = CV + (g1 * ne2 + k2) * ng2;
+                    const double* v2 = V2 + k2 * ng2 * q2 + b2;
+                    for (int g2 = 0; g2 < ng2; ++g2) acc += cv[g2] * v2[g2 * q2];
+                }
+                inner[t] = acc;
+            }
+            __syncthreads();
+            for (int t = tid; t < q1 * W2; t += NT) {
+                const int b1 = t / W2, o2 = t - b1 * W2;
+                double acc = 0.0;
+                for (int g1 = 0; g1 < ng1; ++g1) acc += P1[g1 * q1 + b1] * inner[g1 * W2 + o2];
+                blk[(F1[k1] + b1 - i1 + p1) * W2 + o2] += acc;
+            }
+            __syncthreads();
+        }
+        for (int q = tid; q < T; q += NT) dst[q] = blk[q];
+        __syncthreads();
+    }
+}
+
+// The c != 1 sum-factorization part (PARTS == 2 with coefficient grids): one
+// block of NT threads per row; the weighted collocation slices and the row's
+// n1 x n2 coefficient window (masked for MASK rows) are staged in shared
+// memory, then inner[o2][k1] = sum_k2 B2[k2][o2] G[k1][k2] and
+// M[o1][o2] += sum_k1 B1[k1][o1] inner[o2][k1] -- the additions of the
+// warp-per-row kernel in the same order (sum_factor_row, src/assembly.py:218-252).
+__host__ __device__ inline int sf_coef_slots(const tq_rawctx& c) {
+    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
+    return c.nmax1 * W1 + c.nmax2 * W2 + c.nmax1 * c.nmax2 + W2 * c.nmax1;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1) {
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
+    double* B1 = sm;
+    double* B2 = B1 + c.nmax1 * W1;
+    double* GS = B2 + c.nmax2 * W2;
+    double* inner = GS + c.nmax1 * c.nmax2;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        if (d.mode != TQ_ROW_BOX && d.mode != TQ_ROW_MASK) continue;     // uniform: nothing to add
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const tq_ruleset s1 = c.sets1[d.set1];
+        const tq_ruleset s2 = c.sets2[d.set2];
+        const int k01 = s1.rules.k0[i1], k02 = s2.rules.k0[i2];
+        const int len1 = (int)(s1.rules.wptr[i1 + 1] - s1.rules.wptr[i1]);
+        const int len2 = (int)(s2.rules.wptr[i2 + 1] - s2.rules.wptr[i2]);
+        int lo1 = k01, hi1 = k01 + len1, lo2 = k02, hi2 = k02 + len2;
+        if (d.mode == TQ_ROW_BOX && d.a1 >= 0) {
+            lo1 = max(lo1, s1.lay.offsets[d.a1]);
+            hi1 = min(hi1, s1.lay.offsets[d.b1 + 1]);
+            lo2 = max(lo2, s2.lay.offsets[d.a2]);
+            hi2 = min(hi2, s2.lay.offsets[d.b2 + 1]);
+        }
+        const int n1 = hi1 - lo1, n2 = hi2 - lo2;
+        if (!(k01 >= 0 && k02 >= 0 && n1 > 0 && n2 > 0)) continue;       // uniform
+        const double* w1 = s1.rules.w + s1.rules.wptr[i1] + (lo1 - k01);
+        const double* w2 = s2.rules.w + s2.rules.wptr[i2] + (lo2 - k02);
+        const int jl1 = c.ov_lo1[i1], jh1 = c.ov_hi1[i1], jl2 = c.ov_lo2[i2], jh2 = c.ov_hi2[i2];
+        for (int q = tid; q < n1 * W1; q += NT) {
+            const int k = q / W1, o = q - (q / W1) * W1;
+            const int j = i1 - c.p1 + o;
+            B1[q] = (j >= jl1 && j <= jh1) ? colloc_at(s1, c.p1, lo1 + k, j) * w1[k] : 0.0;
+        }
+        for (int q = tid; q < n2 * W2; q += NT) {
+            const int k = q / W2, o = q - (q / W2) * W2;
+            const int j = i2 - c.p2 + o;
+            B2[q] = (j >= jl2 && j <= jh2) ? colloc_at(s2, c.p2, lo2 + k, j) * w2[k] : 0.0;
+        }
+        const double* G = c.grids[d.set1 * c.nsets2 + d.set2];
+        const int ld = s2.lay.npts;
+        for (int q = tid; q < n1 * n2; q += NT) {
+            const int k1 = q / n2, k2 = q - k1 * n2;
+            double g = G[(int64_t)(lo1 + k1) * ld + (lo2 + k2)];
+            if (d.mode == TQ_ROW_MASK) {
+                const int e1p = elem_of_point(s1.lay, lo1 + k1), e2p = elem_of_point(s2.lay, lo2 + k2);
+                if (c.elem_class[(int64_t)e1p * c.nel2 + e2p] != TQ_INTERIOR) g = 0.0;
+            }
+            GS[q] = g;
+        }
+        __syncthreads();
+        for (int q = tid; q < W2 * n1; q += NT) {
+            const int o2 = q / n1, k1 = q - (q / n1) * n1;
+            const double* gr = GS + k1 * n2;
+            double acc = 0.0;
+            for (int k2 = 0; k2 < n2; ++k2) acc += B2[k2 * W2 + o2] * gr[k2];
+            inner[o2 * n1 + k1] = acc;
+        }
+        __syncthreads();
+        double* dst = c.raw + (int64_t)r * T;
+        for (int q = tid; q < T; q += NT) {
+            const int o1 = q / W2, o2 = q - (q / W2) * W2;
+            double acc = 0.0;
+            for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * n1 + k1];
+            dst[q] += acc;
+        }
+        __syncthreads();
     }
 }
 
@@ -404,6 +641,59 @@ __global__ void k_coeff_grid(tq_coeff g, const double* x1, int n1, const double*
     }
 }
 
+// Tensor grids: a block covers kCgA x kCgB grid points; the spans and
+// basis values (and derivatives) of its kCgA + kCgB grid lines are computed
+// once into shared memory, then every point is the (p+1)^2 contraction of
+// detj with the same arithmetic (per-point results identical to detj).
+constexpr int kCgA = 16, kCgB = 128;
+
+__global__ void __launch_bounds__(256) k_coeff_grid_tiled(tq_coeff g, const double* __restrict__ x1, int n1,
+                                                          const double* __restrict__ x2, int n2,
+                                                          double* __restrict__ out) {
+    constexpr int P1 = kMaxP + 1;
+    __shared__ double Na[kCgA][P1], Da[kCgA][P1], Nb[kCgB][P1], Db[kCgB][P1];
+    __shared__ int sa[kCgA], sb[kCgB];
+    const int a0 = blockIdx.y * kCgA, b0 = blockIdx.x * kCgB;
+    const int nk = g.n + g.p + 1;
+    for (int t = threadIdx.x; t < kCgA + kCgB; t += blockDim.x) {
+        const bool isa = t < kCgA;
+        const int l = isa ? t : t - kCgA;
+        const int gi = (isa ? a0 : b0) + l;
+        if (gi >= (isa ? n1 : n2)) continue;
+        const double u = isa ? x1[gi] : x2[gi];
+        const int sp = find_span(g.knots, nk, g.p, g.n, u);
+        double N[P1], D[P1];
+        basis_funs_ders_rt(g.knots, g.p, sp, u, N, D);
+        double* No = isa ? Na[l] : Nb[l];
+        double* Do = isa ? Da[l] : Db[l];
+        for (int k = 0; k <= g.p; ++k) {
+            No[k] = N[k];
+            Do[k] = D[k];
+        }
+        (isa ? sa : sb)[l] = sp;
+    }
+    __syncthreads();
+    const int bl = threadIdx.x % kCgB;
+    const int b = b0 + bl;
+    if (b >= n2) return;
+    for (int al = threadIdx.x / kCgB; al < kCgA; al += blockDim.x / kCgB) {
+        const int a = a0 + al;
+        if (a >= n1) break;
+        const int s1 = sa[al], s2 = sb[bl];
+        double xu = 0, xv = 0, yu = 0, yv = 0;
+        for (int i = 0; i <= g.p; ++i)
+            for (int j = 0; j <= g.p; ++j) {
+                const int64_t idx = (int64_t)(s1 - g.p + i) * g.n + (s2 - g.p + j);
+                const double X = __ldg(g.X + idx), Y = __ldg(g.Y + idx);
+                xu += Da[al][i] * Nb[bl][j] * X;
+                xv += Na[al][i] * Db[bl][j] * X;
+                yu += Da[al][i] * Nb[bl][j] * Y;
+                yv += Na[al][i] * Db[bl][j] * Y;
+            }
+        out[(int64_t)a * n2 + b] = xu * yv - xv * yu;
+    }
+}
+
 __global__ void k_coeff_points(tq_coeff g, const double* P, int64_t n, const double* w, double* out) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         double v = detj(g, P[2 * t], P[2 * t + 1]);
@@ -505,7 +795,7 @@ static size_t regular_smem_per_warp(const tq_rawctx& c) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
     const int ni = std::max(c.nmax1, c.p1 + 1);
     return sizeof(double) * ((size_t)W1 * W2 + (size_t)c.nmax1 * W1 + (size_t)c.nmax2 * W2 + (size_t)W2 * ni + W1 + W2 +
-                             regular_window_slots(c.p1, c.p2));
+                             regular_window_slots(c.p1, c.p2) + (c.grids ? (size_t)c.nmax1 * c.nmax2 : 0));
 }
 
 template <int PARTS>
@@ -522,7 +812,38 @@ static int raw_regular_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* 
     return TQ_OK;
 }
 
+constexpr int kCoefRowThreads = 128;     // threads per row of the c != 1 raw-row kernels
+
+static int raw_gauss_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
+    if (r1 <= r0) return TQ_OK;
+    const size_t shm = sizeof(double) * gauss_coef_slots(c.p1, c.p2, c.ng1, c.ng2);
+    if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_gauss_coef<kCoefRowThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)shm));
+    const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 32);
+    k_raw_gauss_coef<kCoefRowThreads><<<grid, kCoefRowThreads, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_raw_gauss_coef");
+    return TQ_OK;
+}
+
+static int raw_sf_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
+    if (r1 <= r0) return TQ_OK;
+    const size_t shm = sizeof(double) * sf_coef_slots(c);
+    if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_sf_coef<kCoefRowThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)shm));
+    const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 32);
+    k_raw_sf_coef<kCoefRowThreads><<<grid, kCoefRowThreads, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_raw_sf_coef");
+    return TQ_OK;
+}
+
 extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    if (c.cg) {     // c != 1: the sum-factorized element-Gauss kernel, then the WQ part onto it
+        int rc = raw_gauss_coef_launch(c, r0, r1, stream);
+        if (rc) return rc;
+        return c.grids ? raw_sf_coef_launch(c, r0, r1, stream) : raw_regular_launch<2>(c, r0, r1, stream);
+    }
     return raw_regular_launch<3>(c, r0, r1, stream);
 }
 
@@ -539,10 +860,12 @@ extern "C" int tq_raw_gauss(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
         TQ_LAUNCH_CHECK("k_raw_gauss_sep");
         return TQ_OK;
     }
+    if (c.cg) return raw_gauss_coef_launch(c, r0, r1, stream);
     return raw_regular_launch<1>(c, r0, r1, stream);
 }
 
 extern "C" int tq_raw_sumfactor(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
+    if (c.grids) return raw_sf_coef_launch(c, r0, r1, stream);
     return raw_regular_launch<2>(c, r0, r1, stream);
 }
 
@@ -582,7 +905,14 @@ extern "C" int tq_coeff_grid(tq_coeff g, const double* x1, int32_t n1, const dou
                              void* stream) {
     if ((int64_t)n1 * n2 == 0) return TQ_OK;
     if (g.kind != TQ_COEFF_GEOMETRY || g.p > kMaxP) { set_error("unsupported coefficient field"); return TQ_EINVAL; }
-    k_coeff_grid<<<grid_for((int64_t)n1 * n2, 128), 128, 0, S(stream)>>>(g, x1, n1, x2, n2, out); ::tq::note_launch();
+    static const bool pointwise = getenv("TQ_COEFF_POINTWISE") != nullptr;    // A/B and the parity test
+    if (pointwise) {
+        k_coeff_grid<<<grid_for((int64_t)n1 * n2, 128), 128, 0, S(stream)>>>(g, x1, n1, x2, n2, out);
+    } else {
+        const dim3 grid((n2 + kCgB - 1) / kCgB, (n1 + kCgA - 1) / kCgA);
+        k_coeff_grid_tiled<<<grid, 256, 0, S(stream)>>>(g, x1, n1, x2, n2, out);
+    }
+    ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_coeff_grid");
     return TQ_OK;
 }

@@ -105,3 +105,32 @@ def test_speculative_count_pass(kind, nel, p, spoil):
     assert (int(bad.item()) > 0) == spoil
     for k in ref:
         assert np.array_equal(ref[k], got[k]), k
+
+
+
+def test_tiled_coefficient_grid_matches_pointwise(tmp_path):
+    """k_coeff_grid_tiled (line tables in shared memory) against the
+    per-point detj kernel (TQ_COEFF_POINTWISE, read when the library loads):
+    identical values on ragged grid sizes, including points on knots."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2101_08053_b200 import cases as C, assembly as A
+rng = np.random.default_rng(3)
+geo = C.geometry_map(np.random.default_rng(0))
+x1 = torch.tensor(np.sort(np.concatenate([rng.uniform(0, 1, 37), np.linspace(0, 1, 9)])), device="cuda")
+x2 = torch.tensor(np.sort(np.concatenate([rng.uniform(0, 1, 301), [0.0, 0.5, 1.0]])), device="cuda")
+np.save(sys.argv[1], geo.grid_device(x1, x2).cpu().numpy())
+""".format(root=root)
+    out = {}
+    for mode in ("tiled", "pointwise"):
+        env = dict(os.environ)
+        env.pop("TQ_COEFF_POINTWISE", None)
+        if mode == "pointwise":
+            env["TQ_COEFF_POINTWISE"] = "1"
+        f = tmp_path / f"{mode}.npy"
+        subprocess.run([sys.executable, "-c", script, str(f)], check=True, env=env, timeout=600)
+        out[mode] = np.load(f)
+    assert out["tiled"].shape == (46, 304)
+    assert np.array_equal(out["tiled"], out["pointwise"])
