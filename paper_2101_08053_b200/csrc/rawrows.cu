@@ -336,6 +336,15 @@ __host__ __device__ inline int gauss_coef_slots(int p1, int p2, int ng1, int ng2
            + (q1 + q2 + q1 * q2 + 1) / 2 + 1;   // spans and flags (ints)
 }
 
+// A BOX row whose box is its whole support (the interior rows of the c != 1
+// BOX plan) has no element-Gauss part: the Gauss kernel leaves its block
+// untouched and the sum-factorization kernel writes it (0 + x == x: the
+// same values as zero-then-add).
+__device__ __forceinline__ bool full_box_row(const tq_rawctx& c, const RowDesc& d, int i1, int i2) {
+    return d.mode == TQ_ROW_BOX && d.a1 == c.el_first1[i1] && d.b1 == c.el_last1[i1] && d.a2 == c.el_first2[i2] &&
+           d.b2 == c.el_last2[i2];
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int r1) {
     // one block of NT threads per row (the row's windows are shared by the
@@ -360,6 +369,7 @@ __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int 
         double* dst = c.raw + (int64_t)r * T;
         bool work = d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX;
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        if (full_box_row(c, d, i1, i2)) continue;        // uniform: written by k_raw_sf_coef
         const int ef1 = c.el_first1[i1], ne1 = c.el_last1[i1] - ef1 + 1;
         const int ef2 = c.el_first2[i2], ne2 = c.el_last2[i2] - ef2 + 1;
         bool mine = false;
@@ -440,9 +450,11 @@ __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int 
 // memory, then inner[o2][k1] = sum_k2 B2[k2][o2] G[k1][k2] and
 // M[o1][o2] += sum_k1 B1[k1][o1] inner[o2][k1] -- the additions of the
 // warp-per-row kernel in the same order (sum_factor_row, src/assembly.py:218-252).
+// (the coefficient window and inner have odd row strides: the column
+// accesses of the two contractions are bank-conflict free)
 __host__ __device__ inline int sf_coef_slots(const tq_rawctx& c) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
-    return c.nmax1 * W1 + c.nmax2 * W2 + c.nmax1 * c.nmax2 + W2 * c.nmax1;
+    return c.nmax1 * W1 + c.nmax2 * W2 + c.nmax1 * (c.nmax2 | 1) + W2 * (c.nmax1 | 1);
 }
 
 template <int NT>
@@ -453,7 +465,7 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
     double* B1 = sm;
     double* B2 = B1 + c.nmax1 * W1;
     double* GS = B2 + c.nmax2 * W2;
-    double* inner = GS + c.nmax1 * c.nmax2;
+    double* inner = GS + c.nmax1 * (c.nmax2 | 1);
     for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
         const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
         if (d.mode != TQ_ROW_BOX && d.mode != TQ_ROW_MASK) continue;     // uniform: nothing to add
@@ -471,7 +483,13 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
             hi2 = min(hi2, s2.lay.offsets[d.b2 + 1]);
         }
         const int n1 = hi1 - lo1, n2 = hi2 - lo2;
-        if (!(k01 >= 0 && k02 >= 0 && n1 > 0 && n2 > 0)) continue;       // uniform
+        const int ldg = n2 | 1, ldi = n1 | 1;            // odd strides
+        const bool write = full_box_row(c, d, i1, i2);
+        if (!(k01 >= 0 && k02 >= 0 && n1 > 0 && n2 > 0)) {       // uniform
+            if (write)
+                for (int q = tid; q < T; q += NT) c.raw[(int64_t)r * T + q] = 0.0;
+            continue;
+        }
         const double* w1 = s1.rules.w + s1.rules.wptr[i1] + (lo1 - k01);
         const double* w2 = s2.rules.w + s2.rules.wptr[i2] + (lo2 - k02);
         const int jl1 = c.ov_lo1[i1], jh1 = c.ov_hi1[i1], jl2 = c.ov_lo2[i2], jh2 = c.ov_hi2[i2];
@@ -494,23 +512,24 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
                 const int e1p = elem_of_point(s1.lay, lo1 + k1), e2p = elem_of_point(s2.lay, lo2 + k2);
                 if (c.elem_class[(int64_t)e1p * c.nel2 + e2p] != TQ_INTERIOR) g = 0.0;
             }
-            GS[q] = g;
+            GS[k1 * ldg + k2] = g;
         }
         __syncthreads();
         for (int q = tid; q < W2 * n1; q += NT) {
             const int o2 = q / n1, k1 = q - (q / n1) * n1;
-            const double* gr = GS + k1 * n2;
+            const double* gr = GS + k1 * ldg;
             double acc = 0.0;
             for (int k2 = 0; k2 < n2; ++k2) acc += B2[k2 * W2 + o2] * gr[k2];
-            inner[o2 * n1 + k1] = acc;
+            inner[o2 * ldi + k1] = acc;
         }
         __syncthreads();
         double* dst = c.raw + (int64_t)r * T;
         for (int q = tid; q < T; q += NT) {
             const int o1 = q / W2, o2 = q - (q / W2) * W2;
             double acc = 0.0;
-            for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * n1 + k1];
-            dst[q] += acc;
+            for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * ldi + k1];
+            if (write) dst[q] = acc;
+            else dst[q] += acc;
         }
         __syncthreads();
     }
@@ -572,6 +591,69 @@ __global__ void k_cut_blocks(tq_rawctx c) {
                 for (int a2 = 0; a2 < Q2; ++a2)
 #pragma unroll
                     for (int b2 = 0; b2 < Q2; ++b2) out[(a1 * Q2 + a2) * Q + b1 * Q2 + b2] = acc[a2 * Q2 + b2];
+            }
+        }
+    }
+}
+
+// The same element blocks with one block of kCbThreads per group (large
+// degrees: q^2 (a1, b1) pairs x Q2^2 accumulators no longer fit a warp):
+// a thread owns one (a1, b1) pair and kCbA2 consecutive a2 -- kCbA2 x Q2
+// accumulators -- and the group's points are staged kCbChunk at a time for
+// the whole block.  Per output the additions are those of k_cut_blocks in
+// the same order (bit-identical).
+constexpr int kCbThreads = 256, kCbChunk = 64, kCbA2 = 3;
+
+template <int Q2>
+__global__ void __launch_bounds__(kCbThreads) k_cut_blocks_wide(tq_rawctx c) {
+    extern __shared__ double sm[];
+    constexpr int S = (Q2 + kCbA2 - 1) / kCbA2;          // a2 subsets per (a1, b1)
+    const int q1 = c.p1 + 1, Q = q1 * Q2, st = q1 + Q2 + 1;
+    const int ntask = q1 * q1 * S;
+    for (int g = blockIdx.x; g < c.ngroups; g += gridDim.x) {
+        const int64_t p0 = c.grp_pts[g], pe = c.grp_pts[g + 1];
+        for (int t0 = 0; t0 < ntask; t0 += kCbThreads) {      // one pass when q1^2 S <= kCbThreads
+            const int t = t0 + threadIdx.x;
+            const bool act = t < ntask;
+            const int pr = act ? t / S : 0, sub = act ? t - (t / S) * S : 0;
+            const int a1 = pr / q1, b1 = pr - (pr / q1) * q1, a20 = sub * kCbA2;
+            double acc[kCbA2 * Q2];
+#pragma unroll
+            for (int z = 0; z < kCbA2 * Q2; ++z) acc[z] = 0.0;
+            for (int64_t base = p0; base < pe; base += kCbChunk) {
+                const int np = (int)(pe - base < kCbChunk ? pe - base : kCbChunk);
+                __syncthreads();
+                for (int l = threadIdx.x; l < np * st; l += kCbThreads) {
+                    const int k = l / st, o = l - k * st;
+                    const int64_t pt = c.grp_perm[base + k];
+                    sm[l] = o < q1 ? c.cvals1[pt * q1 + o] : (o < q1 + Q2 ? c.cvals2[pt * Q2 + (o - q1)] : c.cut_cw[pt]);
+                }
+                __syncthreads();
+                if (act) {
+                    for (int k = 0; k < np; ++k) {
+                        const double* d = sm + k * st;
+                        const double s = (d[q1 + Q2] * d[a1]) * d[b1];
+                        double v2[Q2];
+#pragma unroll
+                        for (int o = 0; o < Q2; ++o) v2[o] = d[q1 + o];
+#pragma unroll
+                        for (int z = 0; z < kCbA2; ++z) {
+                            if (a20 + z >= Q2) break;
+                            const double u = s * d[q1 + a20 + z];     // (no runtime index into v2: registers)
+#pragma unroll
+                            for (int b2 = 0; b2 < Q2; ++b2) acc[z * Q2 + b2] = fma(u, v2[b2], acc[z * Q2 + b2]);
+                        }
+                    }
+                }
+            }
+            if (act) {
+                double* out = c.grp_blocks + (int64_t)g * Q * Q;
+#pragma unroll
+                for (int z = 0; z < kCbA2; ++z) {
+                    if (a20 + z >= Q2) break;
+#pragma unroll
+                    for (int b2 = 0; b2 < Q2; ++b2) out[(a1 * Q2 + a20 + z) * Q + b1 * Q2 + b2] = acc[z * Q2 + b2];
+                }
             }
         }
     }
@@ -877,9 +959,26 @@ extern "C" int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int
     return TQ_OK;
 }
 
+// q2 from which the cut-element blocks use a block per group (env
+// TQ_CUT_BLOCKS_WIDE_FROM overrides: the A/B knob and the parity test)
+static const int kCutBlocksWideFrom = getenv("TQ_CUT_BLOCKS_WIDE_FROM") ? atoi(getenv("TQ_CUT_BLOCKS_WIDE_FROM")) : 7;
+
 extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
     if (c.ngroups <= 0) return TQ_OK;
     if (c.p1 < 1 || c.p1 > kMaxP || c.p2 < 1 || c.p2 > kMaxP) { set_error("degree out of range"); return TQ_EINVAL; }
+    if (c.p2 + 1 >= kCutBlocksWideFrom) {       // large degrees: a block per group
+        const size_t shm = sizeof(double) * kCbChunk * (c.p1 + c.p2 + 3);
+        const int grid = (int)std::min<int64_t>(c.ngroups, (int64_t)kSms * 64);
+        switch (c.p2 + 1) {
+#define TQ_CBW(Q2) case Q2: k_cut_blocks_wide<Q2><<<grid, kCbThreads, shm, S(stream)>>>(c); break;
+            TQ_CBW(5) TQ_CBW(6) TQ_CBW(7) TQ_CBW(8) TQ_CBW(9) TQ_CBW(10) TQ_CBW(11)
+#undef TQ_CBW
+            default: set_error("degree out of range"); return TQ_EINVAL;
+        }
+        ::tq::note_launch();
+        TQ_LAUNCH_CHECK("k_cut_blocks_wide");
+        return TQ_OK;
+    }
     constexpr int wpb = 4;
     const size_t shm = sizeof(double) * wpb * 32 * (c.p1 + c.p2 + 3);
     const int grid = (int)std::min<int64_t>((c.ngroups + wpb - 1) / wpb, (int64_t)kSms * 64);

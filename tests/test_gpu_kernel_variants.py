@@ -134,3 +134,25 @@ np.save(sys.argv[1], geo.grid_device(x1, x2).cpu().numpy())
         out[mode] = np.load(f)
     assert out["tiled"].shape == (46, 304)
     assert np.array_equal(out["tiled"], out["pointwise"])
+
+
+@pytest.mark.parametrize("kind,nel,p,strategy", [("bspline", 48, 6, "dwq"), ("bspline", 32, 8, "hybrid"),
+                                                 ("corner", 12, 7, "hybrid")])
+def test_wide_cut_blocks_bit_identical(tmp_path, kind, nel, p, strategy):
+    """Block-per-group cut-element blocks (k_cut_blocks_wide, q2 >= 7)
+    against the warp-per-group kernel (forced with TQ_CUT_BLOCKS_WIDE_FROM,
+    read when the library loads): the whole formation, bit for bit."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("wide", "warp"):
+        env = dict(os.environ)
+        env.pop("TQ_CUT_BLOCKS_WIDE_FROM", None)
+        if mode == "warp":
+            env["TQ_CUT_BLOCKS_WIDE_FROM"] = "99"
+        f = tmp_path / f"{mode}.npz"
+        subprocess.run([sys.executable, "-c", _SCRIPT.format(root=root), kind, str(nel), str(p), strategy, str(f)],
+                       check=True, env=env, timeout=600)
+        z = np.load(f)
+        out[mode] = [z[k] for k in ("arr_0", "arr_1", "arr_2")]
+    for a, b in zip(out["wide"], out["warp"]):
+        assert np.array_equal(a, b)
