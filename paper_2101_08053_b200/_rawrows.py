@@ -354,12 +354,14 @@ class _Setup:
                 t = L.dev_bytes(bytearray(arr))
                 self.sets_dev.append(t)
             self.nmax = []
+            self.nmax_std = []      # the standard rules alone (interior rows read set 0 only)
             for d, b in enumerate((b1, b2)):
-                m = 0
+                ms = []
                 for rs in self.sets[d]:
                     off = rs.layout.offsets
-                    m = max(m, int(np.max(off[b._el_last + 1] - off[b._el_first])))
-                self.nmax.append(m)
+                    ms.append(int(np.max(off[b._el_last + 1] - off[b._el_first])))
+                self.nmax.append(max(ms))
+                self.nmax_std.append(ms[0])
             if not f.coeff.identity:
                 ptrs = np.zeros(len(self.sets[0]) * len(self.sets[1]), dtype=np.uint64)
                 for a, s1 in enumerate(self.sets[0]):
@@ -371,6 +373,7 @@ class _Setup:
         else:
             self.sets_dev = [None, None]
             self.nmax = [1, 1]
+            self.nmax_std = [1, 1]
         # cut-element points (host C++ geometry, device basis tables); taken
         # from the pass-start launch when the pass made one
         pre = getattr(f, "_cut_pre", None)
@@ -782,7 +785,12 @@ def run_phase(f, phase):
         if nint:
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)
-            L.call("tq_raw_sumfactor" if pre is not None else "tq_raw_regular", f._ctx, 0, nint, L.stream())
+            # interior rows read the standard rules only: their launch sizes its
+            # per-row workspace by those (more rows resident per SM)
+            ctx_int = RawCtx.from_buffer_copy(f._ctx)
+            ctx_int.nmax1, ctx_int.nmax2 = f._setup.nmax_std
+            f._ctx_int = ctx_int
+            L.call("tq_raw_sumfactor" if pre is not None else "tq_raw_regular", ctx_int, 0, nint, L.stream())
     elif phase == "cut":
         if f._ndesc > f._nint:
             pre = getattr(f, "_raw_pre", None) is not None

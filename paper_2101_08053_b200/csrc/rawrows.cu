@@ -345,15 +345,17 @@ __device__ __forceinline__ bool full_box_row(const tq_rawctx& c, const RowDesc& 
            d.b2 == c.el_last2[i2];
 }
 
-template <int NT>
+template <int NT, int P>
 __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int r1) {
     // one block of NT threads per row (the row's windows are shared by the
     // whole block: NT/32 times the parallelism of a warp per row for the
-    // same shared memory)
+    // same shared memory).  P > 0: p1 == p2 == P and P + 1 Gauss points per
+    // element at compile time (constant divisors in the index arithmetic).
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
-    const int p1 = c.p1, p2 = c.p2, q1 = p1 + 1, q2 = p2 + 1, W2 = 2 * p2 + 1, T = (2 * p1 + 1) * W2;
-    const int ng1 = c.ng1, ng2 = c.ng2;
+    const int p1 = P ? P : c.p1, p2 = P ? P : c.p2, q1 = p1 + 1, q2 = p2 + 1, W2 = 2 * p2 + 1,
+              T = (2 * p1 + 1) * W2;
+    const int ng1 = P ? P + 1 : c.ng1, ng2 = P ? P + 1 : c.ng2;
     double* blk = sm;
     double* V2 = blk + T;                   // [k2][g2][b2]
     double* A2 = V2 + q2 * ng2 * q2;        // [k2][g2]
@@ -457,11 +459,14 @@ __host__ __device__ inline int sf_coef_slots(const tq_rawctx& c) {
     return c.nmax1 * W1 + c.nmax2 * W2 + c.nmax1 * (c.nmax2 | 1) + W2 * (c.nmax1 | 1);
 }
 
-template <int NT>
+// P > 0: p1 == p2 == P at compile time (window sizes constant: the index
+// arithmetic of every stage divides by constants); P == 0: runtime degrees.
+template <int NT, int P>
 __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1) {
     extern __shared__ double sm[];
     const int tid = threadIdx.x;
-    const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1, T = W1 * W2;
+    const int W1 = P ? 2 * P + 1 : 2 * c.p1 + 1, W2 = P ? 2 * P + 1 : 2 * c.p2 + 1, T = W1 * W2;
+    const int p1 = P ? P : c.p1, p2 = P ? P : c.p2;
     double* B1 = sm;
     double* B2 = B1 + c.nmax1 * W1;
     double* GS = B2 + c.nmax2 * W2;
@@ -495,13 +500,13 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
         const int jl1 = c.ov_lo1[i1], jh1 = c.ov_hi1[i1], jl2 = c.ov_lo2[i2], jh2 = c.ov_hi2[i2];
         for (int q = tid; q < n1 * W1; q += NT) {
             const int k = q / W1, o = q - (q / W1) * W1;
-            const int j = i1 - c.p1 + o;
-            B1[q] = (j >= jl1 && j <= jh1) ? colloc_at(s1, c.p1, lo1 + k, j) * w1[k] : 0.0;
+            const int j = i1 - p1 + o;
+            B1[q] = (j >= jl1 && j <= jh1) ? colloc_at(s1, p1, lo1 + k, j) * w1[k] : 0.0;
         }
         for (int q = tid; q < n2 * W2; q += NT) {
             const int k = q / W2, o = q - (q / W2) * W2;
-            const int j = i2 - c.p2 + o;
-            B2[q] = (j >= jl2 && j <= jh2) ? colloc_at(s2, c.p2, lo2 + k, j) * w2[k] : 0.0;
+            const int j = i2 - p2 + o;
+            B2[q] = (j >= jl2 && j <= jh2) ? colloc_at(s2, p2, lo2 + k, j) * w2[k] : 0.0;
         }
         const double* G = c.grids[d.set1 * c.nsets2 + d.set2];
         const int ld = s2.lay.npts;
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
         }
         __syncthreads();
         for (int q = tid; q < W2 * n1; q += NT) {
-            const int o2 = q / n1, k1 = q - (q / n1) * n1;
+            const int k1 = q / W2, o2 = q - k1 * W2;
             const double* gr = GS + k1 * ldg;
             double acc = 0.0;
             for (int k2 = 0; k2 < n2; ++k2) acc += B2[k2 * W2 + o2] * gr[k2];
@@ -896,28 +901,61 @@ static int raw_regular_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* 
 
 constexpr int kCoefRowThreads = 128;     // threads per row of the c != 1 raw-row kernels
 
-static int raw_gauss_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
-    if (r1 <= r0) return TQ_OK;
+template <int P>
+static int raw_gauss_coef_launch_p(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
     const size_t shm = sizeof(double) * gauss_coef_slots(c.p1, c.p2, c.ng1, c.ng2);
     if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
-    TQ_CUDA(cudaFuncSetAttribute(k_raw_gauss_coef<kCoefRowThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_gauss_coef<kCoefRowThreads, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)shm));
     const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 32);
-    k_raw_gauss_coef<kCoefRowThreads><<<grid, kCoefRowThreads, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    k_raw_gauss_coef<kCoefRowThreads, P><<<grid, kCoefRowThreads, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_gauss_coef");
     return TQ_OK;
 }
 
-static int raw_sf_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
+static int raw_gauss_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
     if (r1 <= r0) return TQ_OK;
+    if (c.p1 == c.p2 && c.ng1 == c.p1 + 1 && c.ng2 == c.p2 + 1) {
+        switch (c.p1) {
+#define TQ_GCP(Q) case Q: return raw_gauss_coef_launch_p<Q>(c, r0, r1, stream);
+            TQ_GCP(1) TQ_GCP(2) TQ_GCP(3) TQ_GCP(4) TQ_GCP(5) TQ_GCP(6) TQ_GCP(7) TQ_GCP(8)
+#undef TQ_GCP
+            default: break;
+        }
+    }
+    return raw_gauss_coef_launch_p<0>(c, r0, r1, stream);
+}
+
+template <int NT, int P>
+static int raw_sf_coef_launch_p(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
     const size_t shm = sizeof(double) * sf_coef_slots(c);
     if (shm > 200 * 1024) { set_error("raw-row workspace too large"); return TQ_EINVAL; }
-    TQ_CUDA(cudaFuncSetAttribute(k_raw_sf_coef<kCoefRowThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)shm));
+    TQ_CUDA(cudaFuncSetAttribute(k_raw_sf_coef<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 32);
-    k_raw_sf_coef<kCoefRowThreads><<<grid, kCoefRowThreads, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    k_raw_sf_coef<NT, P><<<grid, NT, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_sf_coef");
     return TQ_OK;
+}
+
+template <int NT>
+static int raw_sf_coef_launch_nt(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
+    if (c.p1 == c.p2) {
+        switch (c.p1) {
+#define TQ_SFP(Q) case Q: return raw_sf_coef_launch_p<NT, Q>(c, r0, r1, stream);
+            TQ_SFP(1) TQ_SFP(2) TQ_SFP(3) TQ_SFP(4) TQ_SFP(5) TQ_SFP(6) TQ_SFP(7) TQ_SFP(8)
+#undef TQ_SFP
+            default: break;
+        }
+    }
+    return raw_sf_coef_launch_p<NT, 0>(c, r0, r1, stream);
+}
+
+static int raw_sf_coef_launch(const tq_rawctx& c, int32_t r0, int32_t r1, void* stream) {
+    if (r1 <= r0) return TQ_OK;
+    static const int nt = getenv("TQ_SF_ROW_THREADS") ? atoi(getenv("TQ_SF_ROW_THREADS")) : kCoefRowThreads;
+    if (nt == 64) return raw_sf_coef_launch_nt<64>(c, r0, r1, stream);
+    if (nt == 256) return raw_sf_coef_launch_nt<256>(c, r0, r1, stream);
+    return raw_sf_coef_launch_nt<kCoefRowThreads>(c, r0, r1, stream);
 }
 
 extern "C" int tq_raw_regular(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
