@@ -454,6 +454,8 @@ __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int 
 // warp-per-row kernel in the same order (sum_factor_row, src/assembly.py:218-252).
 // (the coefficient window and inner have odd row strides: the column
 // accesses of the two contractions are bank-conflict free)
+constexpr int kSfOB = 4;      // outputs per thread along the window in the c != 1 contractions
+
 __host__ __device__ inline int sf_coef_slots(const tq_rawctx& c) {
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
     return c.nmax1 * W1 + c.nmax2 * W2 + c.nmax1 * (c.nmax2 | 1) + W2 * (c.nmax1 | 1);
@@ -520,21 +522,60 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
             GS[k1 * ldg + k2] = g;
         }
         __syncthreads();
-        for (int q = tid; q < W2 * n1; q += NT) {
-            const int k1 = q / W2, o2 = q - k1 * W2;
-            const double* gr = GS + k1 * ldg;
-            double acc = 0.0;
-            for (int k2 = 0; k2 < n2; ++k2) acc += B2[k2 * W2 + o2] * gr[k2];
-            inner[o2 * ldi + k1] = acc;
+        // stage 1: a thread owns one k1 and kSfOB consecutive o2 (lanes run
+        // over k1: the column reads of G are conflict-free, the B2 reads
+        // broadcast; one G load feeds kSfOB FMAs)
+        {
+            int KT = 32;                               // power of two >= n1
+            while (KT < n1) KT *= 2;
+            const int ng = (W2 + kSfOB - 1) / kSfOB;
+            for (int q = tid; q < KT * ng; q += NT) {
+                const int k1 = q & (KT - 1), og = q / KT;
+                if (k1 >= n1) continue;
+                const int o0 = og * kSfOB;
+                const double* gr = GS + k1 * ldg;
+                double acc[kSfOB];
+#pragma unroll
+                for (int z = 0; z < kSfOB; ++z) acc[z] = 0.0;
+                for (int k2 = 0; k2 < n2; ++k2) {
+                    const double g = gr[k2];
+                    const double* b2 = B2 + k2 * W2 + o0;
+#pragma unroll
+                    for (int z = 0; z < kSfOB; ++z)
+                        if (o0 + z < W2) acc[z] += b2[z] * g;
+                }
+#pragma unroll
+                for (int z = 0; z < kSfOB; ++z)
+                    if (o0 + z < W2) inner[(o0 + z) * ldi + k1] = acc[z];
+            }
         }
         __syncthreads();
+        // stage 2: a thread owns one o2 and kSfOB consecutive o1 (one inner
+        // load feeds kSfOB FMAs; the B1 reads broadcast)
         double* dst = c.raw + (int64_t)r * T;
-        for (int q = tid; q < T; q += NT) {
-            const int o1 = q / W2, o2 = q - (q / W2) * W2;
-            double acc = 0.0;
-            for (int k1 = 0; k1 < n1; ++k1) acc += B1[k1 * W1 + o1] * inner[o2 * ldi + k1];
-            if (write) dst[q] = acc;
-            else dst[q] += acc;
+        {
+            const int ng = (W1 + kSfOB - 1) / kSfOB;
+            for (int q = tid; q < W2 * ng; q += NT) {
+                const int og = q / W2, o2 = q - og * W2, o0 = og * kSfOB;
+                const double* in = inner + o2 * ldi;
+                double acc[kSfOB];
+#pragma unroll
+                for (int z = 0; z < kSfOB; ++z) acc[z] = 0.0;
+                for (int k1 = 0; k1 < n1; ++k1) {
+                    const double v = in[k1];
+                    const double* b1 = B1 + k1 * W1 + o0;
+#pragma unroll
+                    for (int z = 0; z < kSfOB; ++z)
+                        if (o0 + z < W1) acc[z] += b1[z] * v;
+                }
+#pragma unroll
+                for (int z = 0; z < kSfOB; ++z) {
+                    if (o0 + z >= W1) break;
+                    const int qq = (o0 + z) * W2 + o2;
+                    if (write) dst[qq] = acc[z];
+                    else dst[qq] += acc[z];
+                }
+            }
         }
         __syncthreads();
     }
