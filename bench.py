@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-nel", type=int, default=512, help="oracle sample size (mesh) for the CPU legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the secondary config-4 (c = det J, p = 6/8) formation measurement")
     ap.add_argument("--no-fill-events", action="store_true",
                     help="do not capture timing events around the fill (the roofline falls back to the standalone fill)")
     ap.add_argument("--profile-eager", action="store_true",
@@ -189,6 +191,61 @@ def profile_traffic():
             return json.load(fh).get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def config4_secondary(p, nel=256, steps=20, seed=0):
+    """BASELINE config 4 (B-spline trim, c = det J of the perturbed geometry
+    map, DWQ): one formation pass as a CUDA graph, replayed with L2 flushed
+    between steps, against the algorithmic roofline of SURVEY §8(d):
+    B_alg = 12 nnz + 4 (rows + 1) + 8 N1 N2 (coefficient grid) over the
+    measured HBM peak, F_alg = 2 sum over interior rows of
+    sum_factor_op_count over the measured DFMA peak."""
+    import torch
+    from paper_2101_08053_b200 import cases as C
+    from paper_2101_08053_b200.assembly import GraphFormation
+    c4 = C.baseline_config(4, seed=seed, p=p, nel=nel)
+    b2d, cfg = C.build_space(None, nel, p, curves=c4["curves"])
+    gf = GraphFormation(b2d, cfg, c4["coeff"], "dwq")
+    K = cfg.active_index()[0]["K"]
+    flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        gf.run()
+    ts = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        gf.run()
+        e_.record()
+        torch.cuda.synchronize()
+        gf.check()
+        ts.append(s_.elapsed_time(e_))
+    ms = float(np.mean(ts))
+    r1, r2 = gf.f.rules[0], gf.f.rules[1]
+    b1, b2 = b2d.dir
+    act = cfg.active_functions()
+    fc = cfg.func_class
+    inter = act[fc[act[:, 0], act[:, 1]] == 0]
+    i1, i2 = inter[:, 0], inter[:, 1]
+    n1 = np.diff(r1.wptr.cpu().numpy())[i1].astype(np.float64)     # rule-row lengths (standard rules)
+    n2 = np.diff(r2.wptr.cpu().numpy())[i2].astype(np.float64)
+    t1 = (b1._ov_hi - b1._ov_lo + 1)[i1].astype(np.float64)
+    t2 = (b2._ov_hi - b2._ov_lo + 1)[i2].astype(np.float64)
+    F = 2.0 * float(np.sum(t2 * n1 * n2 + t1 * t2 * n1))
+    B = 12.0 * gf.nnz + 4.0 * (K + 1) + 8.0 * r1.layout.num_points * r2.layout.num_points
+    bw = measured_peak_hbm()[0] * 1e9
+    try:
+        pf = float(json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                               "fp64_peaks.json")))["dfma_tflops"]) * 1e12
+    except Exception:
+        pf = 33.6e12
+    t_star = max(B / bw, F / pf)
+    return {"workload": f"config4: B-spline trim, c = det J, p={p}, {nel}x{nel} elements, dwq, seed {seed}",
+            "rows": int(K), "nnz": int(gf.nnz), "ms_per_step": ms, "value": gf.nnz / (ms / 1e3), "unit": "nnz/s",
+            "B_alg": B, "F_alg": F, "T_star_us": 1e6 * t_star, "bound": "fp64" if F / pf > B / bw else "hbm",
+            "step_frac_of_roofline": t_star / (ms / 1e3),
+            "step": "CUDA-graph replay of one full formation pass, L2 flushed between steps, mean of "
+                    f"{steps}"}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -389,6 +446,14 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
+    secondary = None
+    if world == 1 and not args.no_config4 and not args.profile_eager:
+        secondary = {}
+        for p4 in (6, 8):
+            try:
+                secondary[f"config4_p{p4}"] = config4_secondary(p4)
+            except Exception as exc:  # the headline stands on its own
+                secondary[f"config4_p{p4}"] = {"failed": str(exc)}
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
@@ -420,6 +485,7 @@ def run_ours(args, rank, world, local_rank):
         "gather_ms": gather_ms,
         "clocks": clocks,
         "e2e": e2e,
+        "secondary": secondary,
         "cpu_baseline": cpu,
     }
     print(json.dumps(out), flush=True)
