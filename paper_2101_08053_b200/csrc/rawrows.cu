@@ -469,6 +469,8 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
     const int tid = threadIdx.x;
     const int W1 = P ? 2 * P + 1 : 2 * c.p1 + 1, W2 = P ? 2 * P + 1 : 2 * c.p2 + 1, T = W1 * W2;
     const int p1 = P ? P : c.p1, p2 = P ? P : c.p2;
+    // outputs per thread along the window: a third of it (P > 0), else kSfOB
+    constexpr int OB = P ? (2 * P + 3) / 3 : kSfOB;
     double* B1 = sm;
     double* B2 = B1 + c.nmax1 * W1;
     double* GS = B2 + c.nmax2 * W2;
@@ -522,54 +524,54 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
             GS[k1 * ldg + k2] = g;
         }
         __syncthreads();
-        // stage 1: a thread owns one k1 and kSfOB consecutive o2 (lanes run
+        // stage 1: a thread owns one k1 and OB consecutive o2 (lanes run
         // over k1: the column reads of G are conflict-free, the B2 reads
-        // broadcast; one G load feeds kSfOB FMAs)
+        // broadcast; one G load feeds OB FMAs)
         {
             int KT = 32;                               // power of two >= n1
             while (KT < n1) KT *= 2;
-            const int ng = (W2 + kSfOB - 1) / kSfOB;
+            const int ng = (W2 + OB - 1) / OB;
             for (int q = tid; q < KT * ng; q += NT) {
                 const int k1 = q & (KT - 1), og = q / KT;
                 if (k1 >= n1) continue;
-                const int o0 = og * kSfOB;
+                const int o0 = og * OB;
                 const double* gr = GS + k1 * ldg;
-                double acc[kSfOB];
+                double acc[OB];
 #pragma unroll
-                for (int z = 0; z < kSfOB; ++z) acc[z] = 0.0;
+                for (int z = 0; z < OB; ++z) acc[z] = 0.0;
                 for (int k2 = 0; k2 < n2; ++k2) {
                     const double g = gr[k2];
                     const double* b2 = B2 + k2 * W2 + o0;
 #pragma unroll
-                    for (int z = 0; z < kSfOB; ++z)
+                    for (int z = 0; z < OB; ++z)
                         if (o0 + z < W2) acc[z] += b2[z] * g;
                 }
 #pragma unroll
-                for (int z = 0; z < kSfOB; ++z)
+                for (int z = 0; z < OB; ++z)
                     if (o0 + z < W2) inner[(o0 + z) * ldi + k1] = acc[z];
             }
         }
         __syncthreads();
-        // stage 2: a thread owns one o2 and kSfOB consecutive o1 (one inner
-        // load feeds kSfOB FMAs; the B1 reads broadcast)
+        // stage 2: a thread owns one o2 and OB consecutive o1 (one inner
+        // load feeds OB FMAs; the B1 reads broadcast)
         double* dst = c.raw + (int64_t)r * T;
         {
-            const int ng = (W1 + kSfOB - 1) / kSfOB;
+            const int ng = (W1 + OB - 1) / OB;
             for (int q = tid; q < W2 * ng; q += NT) {
-                const int og = q / W2, o2 = q - og * W2, o0 = og * kSfOB;
+                const int og = q / W2, o2 = q - og * W2, o0 = og * OB;
                 const double* in = inner + o2 * ldi;
-                double acc[kSfOB];
+                double acc[OB];
 #pragma unroll
-                for (int z = 0; z < kSfOB; ++z) acc[z] = 0.0;
+                for (int z = 0; z < OB; ++z) acc[z] = 0.0;
                 for (int k1 = 0; k1 < n1; ++k1) {
                     const double v = in[k1];
                     const double* b1 = B1 + k1 * W1 + o0;
 #pragma unroll
-                    for (int z = 0; z < kSfOB; ++z)
+                    for (int z = 0; z < OB; ++z)
                         if (o0 + z < W1) acc[z] += b1[z] * v;
                 }
 #pragma unroll
-                for (int z = 0; z < kSfOB; ++z) {
+                for (int z = 0; z < OB; ++z) {
                     if (o0 + z >= W1) break;
                     const int qq = (o0 + z) * W2 + o2;
                     if (write) dst[qq] = acc[z];
