@@ -650,7 +650,7 @@ __global__ void k_cut_blocks(tq_rawctx c) {
 // accumulators -- and the group's points are staged kCbChunk at a time for
 // the whole block.  Per output the additions are those of k_cut_blocks in
 // the same order (bit-identical).
-constexpr int kCbThreads = 256, kCbChunk = 64, kCbA2 = 3;
+constexpr int kCbThreads = 256, kCbChunk = 256, kCbA2 = 3;
 
 template <int Q2>
 __global__ void __launch_bounds__(kCbThreads) k_cut_blocks_wide(tq_rawctx c) {
@@ -671,10 +671,15 @@ __global__ void __launch_bounds__(kCbThreads) k_cut_blocks_wide(tq_rawctx c) {
             for (int64_t base = p0; base < pe; base += kCbChunk) {
                 const int np = (int)(pe - base < kCbChunk ? pe - base : kCbChunk);
                 __syncthreads();
-                for (int l = threadIdx.x; l < np * st; l += kCbThreads) {
-                    const int k = l / st, o = l - k * st;
+                // a thread stages whole points: one permutation lookup, then
+                // q1 + Q2 + 1 independent loads
+                for (int k = threadIdx.x; k < np; k += kCbThreads) {
                     const int64_t pt = c.grp_perm[base + k];
-                    sm[l] = o < q1 ? c.cvals1[pt * q1 + o] : (o < q1 + Q2 ? c.cvals2[pt * Q2 + (o - q1)] : c.cut_cw[pt]);
+                    double* d = sm + k * st;
+                    for (int o = 0; o < q1; ++o) d[o] = c.cvals1[pt * q1 + o];
+#pragma unroll
+                    for (int o = 0; o < Q2; ++o) d[q1 + o] = c.cvals2[pt * Q2 + o];
+                    d[q1 + Q2] = c.cut_cw[pt];
                 }
                 __syncthreads();
                 if (act) {
