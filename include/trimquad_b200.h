@@ -88,6 +88,9 @@ typedef struct {
 } tq_coeff;
 
 int tq_version(void);
+/* keep freed cudaMallocAsync memory in the device's default pool (release
+ * threshold = max) so scratch allocations of later calls re-map nothing */
+int tq_pool_keep(int32_t device);
 const char* tq_last_error(void);
 int tq_device_sync(void* stream);
 /* kernels launched by the library since it was loaded (host counter) */

@@ -79,6 +79,7 @@ def lib():
     L = C.CDLL(LIB_PATH)
     sig = {
         "tq_version": ([], i32),
+        "tq_pool_keep": ([i32], i32),
         "tq_last_error": ([], C.c_char_p),
         "tq_device_sync": ([vp], i32),
         "tq_debug_stamp": ([vp, i32, vp], i32),
@@ -159,10 +160,17 @@ class Stamps:
         return {n: (int(v) - int(t[0])) / 1e3 for n, v in zip(self.names, t)}
 
 
+_POOLS_KEPT = set()
+
+
 def device():
     if not torch.cuda.is_available():
         raise RuntimeError("trimquad_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
-    return torch.device("cuda", torch.cuda.current_device())
+    d = torch.cuda.current_device()
+    if d not in _POOLS_KEPT:      # once per device: freed scratch stays in the stream-ordered pool
+        _POOLS_KEPT.add(d)
+        lib().tq_pool_keep(d)
+    return torch.device("cuda", d)
 
 
 def stream():

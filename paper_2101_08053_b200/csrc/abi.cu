@@ -28,6 +28,18 @@ int check_cuda(cudaError_t e, const char* what) {
 
 extern "C" int tq_version(void) { return 1; }
 
+// Keep freed stream-ordered allocations (cudaMallocAsync scratch of the
+// classification, cut-cell and scan entry points) in the device's default
+// pool instead of returning them to the driver at every synchronisation
+// (the default release threshold is 0): a later call re-maps nothing.
+extern "C" int tq_pool_keep(int32_t device) {
+    cudaMemPool_t pool;
+    TQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    TQ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    return TQ_OK;
+}
+
 extern "C" const char* tq_last_error(void) { return tq::g_err; }
 
 extern "C" int tq_device_sync(void* stream) {
