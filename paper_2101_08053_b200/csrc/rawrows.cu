@@ -776,20 +776,31 @@ __global__ void k_coeff_grid(tq_coeff g, const double* x1, int n1, const double*
     }
 }
 
-// Tensor grids: a block covers kCgA x kCgB grid points; the spans and
-// basis values (and derivatives) of its kCgA + kCgB grid lines are computed
-// once into shared memory, then every point is the (p+1)^2 contraction of
-// detj with the same arithmetic (per-point results identical to detj).
-constexpr int kCgA = 16, kCgB = 128;
+// Tensor grids: a block covers kCgA x kCgB grid points.  The spans and
+// basis values (and derivatives) of its grid lines are computed once into
+// shared memory; then the control net is contracted along direction 2 for
+// every b-line of the tile (XB[i][b] = sum_j N_j(x2_b) X[i][j], and with the
+// derivatives), and each point is a (p+1)-term contraction per partial
+// derivative: 4 (p+1) multiply-adds instead of 4 (p+1)^2.  (Same terms as
+// detj, summed in a different order.)  Tiles whose a-lines touch more than
+// kCgR control rows fall back to the per-point contraction.
+constexpr int kCgA = 32, kCgB = 64, kCgR = 12;
 
 __global__ void __launch_bounds__(256) k_coeff_grid_tiled(tq_coeff g, const double* __restrict__ x1, int n1,
                                                           const double* __restrict__ x2, int n2,
                                                           double* __restrict__ out) {
     constexpr int P1 = kMaxP + 1;
     __shared__ double Na[kCgA][P1], Da[kCgA][P1], Nb[kCgB][P1], Db[kCgB][P1];
+    __shared__ double XB[kCgR][kCgB], XDB[kCgR][kCgB], YB[kCgR][kCgB], YDB[kCgR][kCgB];
     __shared__ int sa[kCgA], sb[kCgB];
+    __shared__ int rng[2];
     const int a0 = blockIdx.y * kCgA, b0 = blockIdx.x * kCgB;
     const int nk = g.n + g.p + 1;
+    if (threadIdx.x == 0) {
+        rng[0] = INT_MAX;
+        rng[1] = INT_MIN;
+    }
+    __syncthreads();
     for (int t = threadIdx.x; t < kCgA + kCgB; t += blockDim.x) {
         const bool isa = t < kCgA;
         const int l = isa ? t : t - kCgA;
@@ -806,14 +817,49 @@ __global__ void __launch_bounds__(256) k_coeff_grid_tiled(tq_coeff g, const doub
             Do[k] = D[k];
         }
         (isa ? sa : sb)[l] = sp;
+        if (isa) {
+            atomicMin(&rng[0], sp - g.p);
+            atomicMax(&rng[1], sp);
+        }
     }
     __syncthreads();
-    const int bl = threadIdx.x % kCgB;
-    const int b = b0 + bl;
-    if (b >= n2) return;
-    for (int al = threadIdx.x / kCgB; al < kCgA; al += blockDim.x / kCgB) {
-        const int a = a0 + al;
-        if (a >= n1) break;
+    const int i0 = rng[0], R = rng[1] - rng[0] + 1;
+    const int nbl = min(kCgB, n2 - b0), nal = min(kCgA, n1 - a0);
+    if (R <= kCgR) {
+        for (int t = threadIdx.x; t < R * nbl; t += blockDim.x) {
+            const int ii = t / nbl, bl = t - ii * nbl;
+            const double* Xr = g.X + (int64_t)(i0 + ii) * g.n + (sb[bl] - g.p);
+            const double* Yr = g.Y + (int64_t)(i0 + ii) * g.n + (sb[bl] - g.p);
+            double xb = 0, xdb = 0, yb = 0, ydb = 0;
+            for (int j = 0; j <= g.p; ++j) {
+                const double X = __ldg(Xr + j), Y = __ldg(Yr + j);
+                xb += Nb[bl][j] * X;
+                xdb += Db[bl][j] * X;
+                yb += Nb[bl][j] * Y;
+                ydb += Db[bl][j] * Y;
+            }
+            XB[ii][bl] = xb;
+            XDB[ii][bl] = xdb;
+            YB[ii][bl] = yb;
+            YDB[ii][bl] = ydb;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nal * nbl; t += blockDim.x) {
+            const int al = t / nbl, bl = t - al * nbl;
+            const int r0 = sa[al] - g.p - i0;
+            double xu = 0, xv = 0, yu = 0, yv = 0;
+            for (int i = 0; i <= g.p; ++i) {
+                xu += Da[al][i] * XB[r0 + i][bl];
+                xv += Na[al][i] * XDB[r0 + i][bl];
+                yu += Da[al][i] * YB[r0 + i][bl];
+                yv += Na[al][i] * YDB[r0 + i][bl];
+            }
+            out[(int64_t)(a0 + al) * n2 + b0 + bl] = xu * yv - xv * yu;
+        }
+        return;
+    }
+    for (int t = threadIdx.x; t < nal * nbl; t += blockDim.x) {      // wide tile: per point
+        const int al = t / nbl, bl = t - al * nbl;
         const int s1 = sa[al], s2 = sb[bl];
         double xu = 0, xv = 0, yu = 0, yv = 0;
         for (int i = 0; i <= g.p; ++i)
@@ -825,7 +871,7 @@ __global__ void __launch_bounds__(256) k_coeff_grid_tiled(tq_coeff g, const doub
                 yu += Da[al][i] * Nb[bl][j] * Y;
                 yv += Na[al][i] * Db[bl][j] * Y;
             }
-        out[(int64_t)a * n2 + b] = xu * yv - xv * yu;
+        out[(int64_t)(a0 + al) * n2 + b0 + bl] = xu * yv - xv * yu;
     }
 }
 
