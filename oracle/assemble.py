@@ -156,14 +156,24 @@ class _Run:
         ok = comp >= 0
         self.add(np.full(int(ok.sum()), row), comp[ok], blk.ravel()[ok])
 
-    def finish(self):
-        """0.5*(M+M^T), zero-drop, sorted (src/assembly.py:400-404)."""
+    def flush(self):
+        """Sum the accumulated contributions into the CSR -- the analogue of
+        the reference's ``flush`` scatter (src/assembly.py:299-306), which
+        ``assemble_mass`` runs INSIDE its clock (:525-546)."""
         if self.R:
             r, c, v = np.concatenate(self.R), np.concatenate(self.C), np.concatenate(self.V)
         else:
             r = c = np.empty(0, np.int64)
             v = np.empty(0)
+        self.R, self.C, self.V = [], [], []
         M = sp.csr_matrix((v, (r, c)), shape=(self.K, self.K))
+        self._M = M if getattr(self, "_M", None) is None else self._M + M
+
+    def finish(self):
+        """0.5*(M+M^T), zero-drop, sorted (src/assembly.py:400-404)."""
+        self.flush()
+        M = self._M
+        self._M = None
         M = 0.5 * (M + M.T)
         M.sort_indices()
         return Mass(M.tocsr(), self.act)
@@ -387,6 +397,7 @@ def assemble_mass(cfg: TrimConfig, coeff: Coeff | None = None, strategy="referen
         t3 = time.perf_counter()
         run.report.t_cut_regular = t3 - t2
     add_cut_blocks(run, cut_rule)
+    run.flush()               # the scatter is timed, as in the reference
     t4 = time.perf_counter()
     run.report.t_cut_elements = t4 - t3
     run.report.t_total = t4 - t0

@@ -12,7 +12,7 @@ are applied from the outside, without editing the reference:
 * q<=6 cap lift (F4) -- ``cut_cell_quadrature`` re-bound without the cap,
   otherwise calling the reference's ``decompose_cut_element``.
 
-Usage:  python tests/golden/make_golden.py [--big]
+Usage:  python tests/golden/make_golden.py [--big | --huge | --p4small | --l2aug config5_256,config5]
 """
 
 from __future__ import annotations
@@ -179,11 +179,120 @@ def dump_case(out, tag, b2d, cfg, strategies, target, coeff=None, full=True, pro
     return mats
 
 
+def _row_sample(M, rows):
+    """Sampled rows of a CSR: (rows, ptr, indices, data, sum_j |M_ij|)."""
+    rows = np.asarray(rows, np.int64)
+    lens = M.indptr[rows + 1] - M.indptr[rows]
+    idx = np.concatenate([M.indices[M.indptr[r]:M.indptr[r + 1]] for r in rows])
+    dat = np.concatenate([M.data[M.indptr[r]:M.indptr[r + 1]] for r in rows])
+    absum = np.array([np.abs(M.data[M.indptr[r]:M.indptr[r + 1]]).sum() for r in rows])
+    return rows, np.concatenate([[0], np.cumsum(lens)]), idx, dat, absum
+
+
+def dump_huge(tag, nel, p, curve, target, strategies=("dwq",), nsample=256, seed=0):
+    """Headline-size golden (config 5, VERDICT r1 'Next' #1): every integer
+    output as a full array (they compress to a few hundred KB) or a sha256,
+    the pattern sha256 + per-row nnz, the Frobenius norm, ``nsample`` uniform
+    rows plus ``nsample`` rows of cut functions (values, columns, sum |M_ij|),
+    the diagonal at every sampled row and column, the RHS's norms and sampled entries, and the
+    reference's own phase timings (this container's CPU)."""
+    t0 = time.perf_counter()
+    d = {}
+    b2d = RS.TensorBasis2D(RS.make_uniform_basis(nel, p), RS.make_uniform_basis(nel, p))
+    cfg = RT.classify_elements(b2d, [curve])
+    d["t_classify"] = time.perf_counter() - t0
+    print(f"  {tag}: classified in {d['t_classify']:.1f}s", flush=True)
+    d["element_class"] = np.asarray(cfg.element_class, np.int8)
+    d["func_class"] = np.asarray(cfg.func_class, np.int8)
+    d["u_disc1"], d["u_disc2"] = cfg.u_disc
+    act = cfg.active_functions()
+    d["active_hash"], d["n_active"] = sha(np.asarray(act, np.int64)), act.shape[0]
+    q = max(b2d.degrees)
+    t1 = time.perf_counter()
+    el, ptr, P, W = cut_rule_arrays(cfg, q)
+    d["t_cutcells"] = time.perf_counter() - t1
+    # the full cut-cell rule (a few MB): lets the GPU test inject the
+    # reference's own points and apply the per-entry bars
+    d["cut_el"], d["cut_ptr"], d["cut_pts"], d["cut_w"] = el, ptr, P, W
+    rng = np.random.default_rng(seed)
+    print(f"  {tag}: cut cells {el.shape[0]} elements, {P.shape[0]} points ({d['t_cutcells']:.1f}s)", flush=True)
+    fc_act = d["func_class"][act[:, 0], act[:, 1]]
+    cut_rows = np.nonzero(fc_act == int(RT.ElementClass.CUT))[0]
+    rows = np.unique(np.concatenate([rng.integers(0, act.shape[0], nsample),
+                                     rng.choice(cut_rows, min(nsample, cut_rows.size), replace=False)]))
+    M = None
+    for s in strategies:
+        t1 = time.perf_counter()
+        M, rep = RA.form_with_timings(s, b2d, cfg, None)
+        M = M.data
+        d[f"{s}_t_wall"] = time.perf_counter() - t1
+        d[f"{s}_report"] = np.array([rep.t_weights, rep.t_interior, rep.t_cut_regular,
+                                     rep.t_cut_elements, rep.t_total])
+        d[f"{s}_hash"] = sha(M.indptr, M.indices)
+        d[f"{s}_nnz"] = M.nnz
+        d[f"{s}_fro"] = float(sp.linalg.norm(M))
+        d[f"{s}_row_nnz"] = np.diff(M.indptr).astype(np.uint8)
+        (d[f"{s}_rows"], d[f"{s}_rowsptr"], d[f"{s}_rowsidx"], d[f"{s}_rowsdata"],
+         d[f"{s}_rowsabs"]) = _row_sample(M, rows)
+        # the diagonal wherever the per-entry bar sqrt(M_ii M_jj) needs it
+        dg = np.unique(np.concatenate([rows, d[f"{s}_rowsidx"]]))
+        d[f"{s}_diag_idx"], d[f"{s}_diag"] = dg, M.diagonal()[dg]
+        print(f"  {tag} {s}: nnz={M.nnz} t_total={rep.t_total:.1f}s wall={d[f'{s}_t_wall']:.1f}s", flush=True)
+        np.savez_compressed(os.path.join(HERE, f"{tag}.npz"), **d)
+    if target is not None:
+        t1 = time.perf_counter()
+        prob = RP.ProjectionProblem(target, b2d, cfg, strategy=strategies[-1])
+        b = RP.assemble_rhs(prob)
+        d["t_rhs"] = time.perf_counter() - t1
+        d["rhs_norm2"], d["rhs_sum"], d["rhs_maxabs"] = float(np.linalg.norm(b)), float(b.sum()), float(np.abs(b).max())
+        rr = np.unique(np.concatenate([rows, rng.integers(0, b.size, 4096)]))
+        d["rhs_rows"], d["rhs_vals"] = rr, b[rr]
+        d["rhs_rowsabs"] = np.abs(M[rr]).sum(axis=1).A1 if M is not None else np.zeros(rr.size)
+        print(f"  {tag}: rhs ({d['t_rhs']:.1f}s)", flush=True)
+    np.savez_compressed(os.path.join(HERE, f"{tag}.npz"), **d)
+    print(f"  {tag}: done in {time.perf_counter() - t0:.1f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also configs 3/4 (minutes)")
+    ap.add_argument("--huge", action="store_true", help="only the config-5 headline golden (~15 min, ~30 GB)")
+    ap.add_argument("--p4small", action="store_true", help="only the full small B-spline p=4 goldens")
+    ap.add_argument("--l2aug", default="", help="comma list of config5* goldens to add a seeded l2_error to")
     args = ap.parse_args()
     t_all = time.perf_counter()
+    if args.l2aug:
+        # l2_error of a seeded coefficient vector (src/projection.py:221-260)
+        # added to the config-5 recipe goldens (a solve at 2048^2 is out of
+        # the reference's reach; the error functional is what is pinned)
+        c5 = OC.config(5)
+        bs = HarnessCurve(c5["curves"][0])
+        for tag in args.l2aug.split(","):
+            path = os.path.join(HERE, f"{tag}.npz")
+            d = dict(np.load(path))
+            nel = 2048 if tag == "config5" else int(tag.split("_")[1])
+            b2d, cfg = space(nel, 4, [bs])
+            prob = RP.ProjectionProblem(OC.f_config5, b2d, cfg, strategy="dwq")
+            t1 = time.perf_counter()
+            x = np.random.default_rng(5).standard_normal(int(d["n_active"]))
+            d["l2_coeffs_seed"], d["l2"] = 5, RP.l2_error(x, prob)
+            d["t_l2"] = time.perf_counter() - t1
+            np.savez_compressed(path, **d)
+            print(f"  {tag}: l2 = {float(d['l2']):.17g} ({d['t_l2']:.1f}s)", flush=True)
+        return
+    if args.huge or args.p4small:
+        c5 = OC.config(5)
+        bs = HarnessCurve(c5["curves"][0])
+        if args.p4small:
+            for nel in (48,):
+                b2d, cfg = space(nel, 4, [bs])
+                dump_case(None, f"bspline_{nel}_4", b2d, cfg, ("reference", "hybrid", "dwq"), OC.f_config5)
+            b2d, cfg = space(256, 4, [bs])
+            dump_huge("config5_256", 256, 4, bs, OC.f_config5, strategies=("hybrid", "dwq"))
+        if args.huge:
+            dump_huge("config5", 2048, 4, bs, OC.f_config5)
+        print(f"done in {time.perf_counter() - t_all:.1f}s")
+        return
 
     # 1. 1-D weighted-quadrature rules and DWQ rules (weights pinned bit-exact)
     d = {}

@@ -14,8 +14,18 @@ def load(tag):
 
 
 def tags():
+    """Full/sampled goldens in the dump_case format (headline goldens excluded)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "*.npz"))
-                  if not os.path.basename(p).startswith("rules_"))
+                  if not os.path.basename(p).startswith(("rules_", "config5")))
+
+
+def headline_tags():
+    """Config-5 recipe goldens in the dump_huge format (make_golden.py --huge/--p4small)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "config5*.npz")))
+
+
+def headline_nel(tag):
+    return 2048 if tag == "config5" else int(tag.split("_")[1])
 
 
 def describe(tag):
