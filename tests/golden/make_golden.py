@@ -231,6 +231,10 @@ def dump_huge(tag, nel, p, curve, target, strategies=("dwq",), nsample=256, seed
         d[f"{s}_hash"] = sha(M.indptr, M.indices)
         d[f"{s}_nnz"] = M.nnz
         d[f"{s}_fro"] = float(sp.linalg.norm(M))
+        # scipy's norm is one BLAS dot: its rounding depends on the host's
+        # thread blocking (1.5e-12 relative at 248 M terms); numpy's pairwise
+        # sum is deterministic and accurate to ~log2(n) eps
+        d[f"{s}_fro_pairwise"] = float(np.sqrt(np.sum(M.data * M.data)))
         d[f"{s}_row_nnz"] = np.diff(M.indptr).astype(np.uint8)
         (d[f"{s}_rows"], d[f"{s}_rowsptr"], d[f"{s}_rowsidx"], d[f"{s}_rowsdata"],
          d[f"{s}_rowsabs"]) = _row_sample(M, rows)
@@ -249,6 +253,14 @@ def dump_huge(tag, nel, p, curve, target, strategies=("dwq",), nsample=256, seed
         d["rhs_rows"], d["rhs_vals"] = rr, b[rr]
         d["rhs_rowsabs"] = np.abs(M[rr]).sum(axis=1).A1 if M is not None else np.zeros(rr.size)
         print(f"  {tag}: rhs ({d['t_rhs']:.1f}s)", flush=True)
+        # l2_error of a seeded coefficient vector (src/projection.py:221-260):
+        # a solve at 2048^2 is out of the reference's reach, the error
+        # functional is what is pinned
+        t1 = time.perf_counter()
+        x = np.random.default_rng(5).standard_normal(b.size)
+        d["l2_coeffs_seed"], d["l2"] = 5, RP.l2_error(x, prob)
+        d["t_l2"] = time.perf_counter() - t1
+        print(f"  {tag}: l2 = {float(d['l2']):.17g} ({d['t_l2']:.1f}s)", flush=True)
     np.savez_compressed(os.path.join(HERE, f"{tag}.npz"), **d)
     print(f"  {tag}: done in {time.perf_counter() - t0:.1f}s", flush=True)
 
