@@ -70,6 +70,11 @@ typedef struct {
 #define TQ_CURVE_CLOSED_CIRCLE 3  /* data: cx cy r ccw(0/1) seam              */
 #define TQ_CURVE_BEZIER 4         /* data: 4 ctrl (x,y) + 3 anchors (x,y)     */
 #define TQ_CURVE_BSPLINE 5        /* data: shift, ccw(0/1), m ctrl (x,y)      */
+/* tq_curve_eval operations (src/trimming.py:69-95) */
+#define TQ_CURVE_OP_EVALUATE 0         /* in: n parameters t   out: n (x,y)  */
+#define TQ_CURVE_OP_DERIVATIVE 1       /* in: n parameters t   out: n (dx,dy)*/
+#define TQ_CURVE_OP_SIGNED_DISTANCE 2  /* in: n points (x,y)   out: n        */
+#define TQ_CURVE_OP_IS_INSIDE 3        /* in: n points (x,y)   out: n 0/1    */
 typedef struct {
     int32_t kind;
     int32_t m;               /* control points (BSPLINE), else 0 */
@@ -111,6 +116,13 @@ int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* first,
  * Gauss per element.  Replaces mass_matrix_1d (src/quadrature.py:160-188). */
 int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng,
                     double* mom, void* stream);
+
+/* dense n_test x n_trial exact mass matrix between two spaces on the same
+ * breakpoints, max(p_test, p_trial)+1 Gauss points per element (gx/gw: the
+ * device rule on [-1,1]).  Replaces mass_matrix_1d(basis, trial_basis)
+ * (src/quadrature.py:160-188). */
+int tq_mass_1d_mixed(tq_space1d test, tq_space1d trial, const double* gx, const double* gw,
+                     int32_t ng, double* M, void* stream);
 
 /* batched moment fits, one pivoted-QR basic solve per listed test row, on
  * layout `lay` with basis values (first, vals) at its points.  Writes
@@ -456,6 +468,33 @@ int64_t tq_cg_workspace_bytes(int32_t n);
 int tq_cg_scaled(const int32_t* indptr, const int32_t* indices, const double* data, int32_t n,
                  const double* s, const double* b, double* x, double rtol, int32_t maxiter,
                  void* work, int32_t* iters_dev, double* rnorm_dev, void* stream);
+
+/* ---- public lower-level API of the drop-in ------------------------------- */
+
+/* The trimming-curve predicate interface on the device, one curve (data:
+ * HOST pointer), `in`/`out` device arrays per TQ_CURVE_OP_*.  Replaces
+ * TrimmingCurve.evaluate / derivative / signed_distance / is_inside
+ * (src/trimming.py:69-95, per-curve :98-351). */
+int tq_curve_eval(const tq_curve* curve_h, int32_t op, const double* in, int64_t n, double* out,
+                  void* stream);
+
+/* Hits (t, cross coordinate) of one curve with the grid line {axis = level}
+ * (axis 0: vertical u1 = level), as the classifier sees them (tangential
+ * touches dropped, duplicates merged, sorted by cross coordinate).  Device
+ * outputs: ht/hc (first min(count, cap) hits), count[0] = hits found,
+ * count[1] = overflow flag.  Replaces TrimmingCurve.intersect_line
+ * (src/trimming.py:86-93, per-curve :124-134, :181-201, :324-351). */
+int tq_curve_intersect_line(const tq_curve* curve_h, int32_t axis, double level, int32_t cap,
+                            double* ht, double* hc, int32_t* count, void* stream);
+
+/* Batched sum factorisation of caller-supplied rows (device arrays): per
+ * row r, dims[4r..] = (n1, n2, t1, t2) and offs[7r..] = offsets into `data`
+ * of C1 (n1 x t1), w1 (n1), C2 (n2 x t2), w2 (n2), G (n1 x n2), mask
+ * (n1 x n2, < 0: none) and into `scratch` of a t2 x n1 work area; the
+ * t1 x t2 block goes to out + out_off[r].  Replaces sum_factor_row
+ * (src/assembly.py:218-252). */
+int tq_sum_factor_rows(int32_t nrows, const int32_t* dims, const int64_t* offs, const int64_t* out_off,
+                       const double* data, double* scratch, double* out, void* stream);
 
 #ifdef __cplusplus
 }

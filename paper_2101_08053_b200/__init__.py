@@ -12,9 +12,11 @@ from .splines import (Basis1D, KnotVector, SubdivisionMatrix, TensorBasis2D, ins
 from .quadrature import (DiscontinuousRuleSet, GaussRule, PointLayout, RuleConstructionError,
                          WeightedRuleSet, build_dwq, compute_wq_rules, exact_moments, gauss_legendre,
                          mass_matrix_1d, place_wq_points)
-from .trimming import ElementClass, TrimConfiguration, TrimmingConfigurationError, classify_elements
+from .trimming import (BezierTrim, CircleTrim, ElementClass, LineTrim, TrimConfiguration, TrimmingConfigurationError,
+                       classify_elements, classify_point, cut_cell_quadrature, decompose_cut_element,
+                       intersect_edge)
 from .assembly import (STRATEGIES, CoefficientField, FormationReport, SparseMatrix, assemble_mass,
-                       form_with_timings, sum_factor_op_count)
+                       form_with_timings, sum_factor_op_count, sum_factor_row, sum_factor_rows)
 
 from .projection import (ConditioningError, ProjectionProblem, SeparableTarget, assemble_rhs, default_target,
                          l2_error, project, solve_spd, run_convergence_study, ConvergenceRecord)

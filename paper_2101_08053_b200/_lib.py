@@ -116,6 +116,12 @@ def lib():
                                      vp], i32),
         "tq_cutcell_device_pack": ([C.POINTER(Curve), i32, vp, vp, vp, i32, i32, vp, i64, vp, vp, vp, vp, vp, i32,
                                     vp], i32),
+        "tq_dwq_route": ([Space1D, Space1D, vp, vp, i32, vp, i32, vp, i32, vp, vp], i32),
+        "tq_function_classes": ([Space1D, Space1D, vp, vp, vp, vp, vp], i32),
+        "tq_mass_1d_mixed": ([Space1D, Space1D, vp, vp, i32, vp, vp], i32),
+        "tq_curve_eval": ([C.POINTER(Curve), i32, vp, i64, vp, vp], i32),
+        "tq_curve_intersect_line": ([C.POINTER(Curve), i32, f64, i32, vp, vp, vp, vp], i32),
+        "tq_sum_factor_rows": ([i32, vp, vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -636,6 +636,9 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
     parallel); ``rules`` imports precomputed weight tables."""
     if strategy not in STRATEGIES:
         raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
+    from . import _adapt         # reference-built objects are accepted (duck-typed)
+    basis2d, config = _adapt.space(basis2d, config)
+    coeff = _adapt.coefficient(coeff)
     f, csr = form(basis2d, config, coeff, strategy, rules, timed=report is not None)
     if report is not None:
         # report-only geometry count (cached per row plan), off the formation path
@@ -651,6 +654,9 @@ def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None,
 
 def form_with_timings(strategy, basis2d, config, coeff=None, parallel=False):
     """src/assembly.py:651-665: shared geometry warmed outside the clock."""
+    from . import _adapt
+    basis2d, config = _adapt.space(basis2d, config)
+    coeff = _adapt.coefficient(coeff)
     q = max(basis2d.degrees)
     if config.has_cuts():
         config.cut_cell_rule(q)
@@ -658,6 +664,86 @@ def form_with_timings(strategy, basis2d, config, coeff=None, parallel=False):
     report = FormationReport(strategy=strategy)
     M = assemble_mass(basis2d, config, coeff, strategy, parallel, report=report)
     return M, report
+
+
+def sum_factor_row(i1, i2, rules1, rules2, colloc1, colloc2, grid, mask=None, point_box=None):
+    """One mass-matrix row by two nested univariate contractions
+    (src/assembly.py:218-252), on the device: ``(j1lo, j2lo, block)`` with
+    block[o1][o2] = sum_k1 B1[k1][o1] sum_k2 B2[k2][o2] G[k1][k2].  See
+    :func:`sum_factor_rows` for the batched form."""
+    m = None if mask is None else [mask]
+    pb = None if point_box is None else [point_box]
+    return sum_factor_rows([(i1, i2)], rules1, rules2, colloc1, colloc2, grid, m, pb)[0]
+
+
+def sum_factor_rows(rows, rules1, rules2, colloc1, colloc2, grid, masks=None, point_boxes=None):
+    """Batched :func:`sum_factor_row`: the operand windows of every row --
+    collocation slices colloc_d[s_d:e_d, jlo_d:jhi_d+1], weight rows, the
+    coefficient window grid[s1:e1, s2:e2] (and its mask) -- are packed on
+    the host and contracted on the device in one launch
+    (tq_sum_factor_rows).  ``rules*`` may be this package's or the
+    reference's rule sets (only ``row`` and ``basis.overlapping`` are used).
+    Returns a list of (j1lo, j2lo, block)."""
+    b1, b2 = rules1.basis, rules2.basis
+    colloc1 = np.asarray(colloc1, dtype=np.float64)
+    colloc2 = np.asarray(colloc2, dtype=np.float64)
+    grid = np.asarray(grid, dtype=np.float64)
+    chunks, dims, offs, outs, res = [], [], [], [], []
+    pos = scratch = out_pos = 0
+
+    def put(a):
+        nonlocal pos
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        chunks.append(a)
+        pos += a.size
+        return pos - a.size
+
+    for r, (i1, i2) in enumerate(rows):
+        i1, i2 = int(i1), int(i2)
+        k1, w1 = rules1.row(i1)
+        k2, w2 = rules2.row(i2)
+        w1, w2 = np.asarray(w1, dtype=np.float64), np.asarray(w2, dtype=np.float64)
+        s1, e1, s2, e2 = k1, k1 + w1.size, k2, k2 + w2.size
+        pb = None if point_boxes is None else point_boxes[r]
+        if pb is not None:
+            s1, e1 = max(s1, pb[0]), min(e1, pb[1])
+            s2, e2 = max(s2, pb[2]), min(e2, pb[3])
+        j1lo, j1hi = b1.overlapping(i1)
+        j2lo, j2hi = b2.overlapping(i2)
+        t1, t2 = j1hi - j1lo + 1, j2hi - j2lo + 1
+        if s1 >= e1 or s2 >= e2:
+            res.append((j1lo, j2lo, np.zeros((t1, t2))))
+            continue
+        n1, n2 = e1 - s1, e2 - s2
+        G = grid[s1:e1, s2:e2]
+        mk = None if masks is None else masks[r]
+        if mk is not None and np.shape(mk) != G.shape:
+            raise ValueError(f"mask of shape {np.shape(mk)} for a {G.shape} coefficient window")
+        o = [put(colloc1[s1:e1, j1lo:j1hi + 1]), put(w1[s1 - k1:e1 - k1]),
+             put(colloc2[s2:e2, j2lo:j2hi + 1]), put(w2[s2 - k2:e2 - k2]), put(G),
+             put(mk) if mk is not None else -1, scratch]
+        scratch += t2 * n1
+        dims.append((n1, n2, t1, t2))
+        offs.append(o)
+        outs.append(out_pos)
+        res.append((j1lo, j2lo, (len(outs) - 1, t1, t2)))
+        out_pos += t1 * t2
+    if outs:
+        dev = L.device()
+        data = L.dev(np.concatenate(chunks), torch.float64)
+        d_dims = L.dev(np.asarray(dims, np.int32), torch.int32)
+        d_offs = L.dev(np.asarray(offs, np.int64), torch.int64)
+        d_out_off = L.dev(np.asarray(outs, np.int64), torch.int64)
+        work = torch.empty(max(scratch, 1), dtype=torch.float64, device=dev)
+        out = torch.empty(max(out_pos, 1), dtype=torch.float64, device=dev)
+        L.call("tq_sum_factor_rows", len(outs), L.ptr(d_dims), L.ptr(d_offs), L.ptr(d_out_off), L.ptr(data),
+               L.ptr(work), L.ptr(out), L.stream())
+        host = out.cpu().numpy()
+        for k, (j1lo, j2lo, blk) in enumerate(res):
+            if isinstance(blk, tuple):
+                idx, t1, t2 = blk
+                res[k] = (j1lo, j2lo, host[outs[idx]:outs[idx] + t1 * t2].reshape(t1, t2).copy())
+    return res
 
 
 def sum_factor_op_count(i1, i2, rules1, rules2):

@@ -37,15 +37,29 @@ class TrimCase:
         return self.curve_factory()
 
 
+def _corner_area():
+    """Valid area of the corner case: 1 minus the invalid corner region, whose
+    area is the loop integral of x dy along the curve (30-point Gauss) closed
+    by the right edge x = 1 (src/cases.py:72-91)."""
+    from .quadrature import gauss_legendre
+    curve = BezierTrim(CORNER_CONTROL_POINTS)
+    rule = gauss_legendre(30)
+    t = 0.5 * (rule.points + 1.0)
+    w = 0.5 * rule.weights
+    along = float(np.sum(w * curve.evaluate(t)[:, 0] * curve.derivative(t)[:, 1]))
+    right_edge = 1.0 * (CORNER_CONTROL_POINTS[0, 1] - 1.0)
+    return 1.0 + (along + right_edge)
+
+
 def make_case(name):
-    """src/cases.py:102-110 (the corner area is not needed on the GPU path)."""
+    """src/cases.py:102-110."""
     if name == "line":
         return TrimCase("line", lambda: LineTrim((1.0, LINE_LEVEL), (0.0, LINE_LEVEL)), LINE_LEVEL)
     if name == "circle":
         return TrimCase("circle", lambda: CircleTrim((0.0, 0.0), CIRCLE_RADIUS, 0.0, 0.5 * np.pi),
                         0.25 * np.pi * CIRCLE_RADIUS ** 2)
     if name == "corner":
-        return TrimCase("corner", lambda: BezierTrim(CORNER_CONTROL_POINTS), float("nan"))
+        return TrimCase("corner", lambda: BezierTrim(CORNER_CONTROL_POINTS), _corner_area())
     raise ValueError(f"unknown case {name!r}; choose from {CASE_NAMES}")
 
 

@@ -2,6 +2,7 @@
 //
 //  tq_basis_eval  <- Basis1D.eval_nonzero_batch   src/splines.py:245-269
 //  tq_moments_1d  <- mass_matrix_1d              src/quadrature.py:160-188
+//  tq_mass_1d_mixed <- mass_matrix_1d(basis, trial_basis)  (same lines)
 #include "common.cuh"
 
 namespace tq {
@@ -106,9 +107,57 @@ __global__ void k_moments(tq_space1d s, const double* __restrict__ tab, int ng, 
     }
 }
 
+// Dense exact mass matrix between a test and a trial space on the same
+// breakpoints (mass_matrix_1d(basis, trial_basis), src/quadrature.py:160-188):
+// thread per (i, j); element loop over the test support in element order
+// (np.add.at accumulates the element blocks in that order), Gauss sum per
+// element first.  The trial span of an element is the one of its first
+// Gauss point, as in the reference (fj.reshape(nel, g)[:, 0]).
+__global__ void k_mass_mixed(tq_space1d s, tq_space1d t, const double* __restrict__ gx,
+                             const double* __restrict__ gw, int ng, double* __restrict__ M) {
+    const int64_t total = (int64_t)s.n * t.n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / t.n), j = (int)(idx - (int64_t)(idx / t.n) * t.n);
+        double acc = 0.0;
+        for (int e = s.el_first[i]; e <= s.el_last[i]; ++e) {
+            const double a = s.bp[e], b = s.bp[e + 1];
+            const double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+            const int fi = s.espan[e] - s.p;
+            const int tspan = find_span(t.knots, t.nknots, t.p, t.n, mid + half * gx[0]);
+            const int fj = tspan - t.p;
+            if (j < fj || j > fj + t.p) continue;
+            double part = 0.0;
+            for (int g = 0; g < ng; ++g) {
+                const double x = mid + half * gx[g];
+                double Ni[kMaxP + 1], Nj[kMaxP + 1];
+                basis_funs_rt(s.knots, s.p, s.espan[e], x, Ni);
+                basis_funs_rt(t.knots, t.p, tspan, x, Nj);
+                part += Ni[i - fi] * Nj[j - fj] * (half * gw[g]);
+            }
+            acc += part;
+        }
+        M[idx] = acc;
+    }
+}
+
 }  // namespace tq
 
 using namespace tq;
+
+extern "C" int tq_mass_1d_mixed(tq_space1d test, tq_space1d trial, const double* gx, const double* gw,
+                                int32_t ng, double* M, void* stream) {
+    if (test.p > kMaxP || trial.p > kMaxP) { set_error("degree unsupported (max %d)", kMaxP); return TQ_EINVAL; }
+    if (test.nel != trial.nel) {
+        set_error("test and trial spaces must share the breakpoints (%d vs %d elements)", test.nel, trial.nel);
+        return TQ_EINVAL;
+    }
+    const int64_t total = (int64_t)test.n * trial.n;
+    if (total == 0) return TQ_OK;
+    k_mass_mixed<<<grid_for(total, 128), 128, 0, S(stream)>>>(test, trial, gx, gw, ng, M); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_mass_mixed");
+    return TQ_OK;
+}
 
 extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* first,
                              double* vals, double* ders, int32_t* status, void* stream) {

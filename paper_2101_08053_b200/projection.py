@@ -202,7 +202,8 @@ def assemble_rhs_device(problem: ProjectionProblem, row_range=None):
 
 def assemble_rhs(problem: ProjectionProblem) -> np.ndarray:
     """src/projection.py:101-145 on the GPU; returns the host vector."""
-    return assemble_rhs_device(problem).cpu().numpy()
+    from . import _adapt
+    return assemble_rhs_device(_adapt.problem(problem)).cpu().numpy()
 
 
 def l2_error_parts_device(coeffs_dev, problem, elem_range=None, point_range=None):
@@ -232,6 +233,8 @@ def l2_error_parts_device(coeffs_dev, problem, elem_range=None, point_range=None
 
 def l2_error(coeffs, problem: ProjectionProblem, active=None) -> float:
     """Relative L2 error (src/projection.py:221-260), reduced on the GPU."""
+    from . import _adapt
+    problem = _adapt.problem(problem)
     basis2d, config = problem.basis2d, problem.config
     if active is not None and not np.array_equal(np.asarray(active), config.active_functions()):
         raise ValueError("coefficients must be ordered like config.active_functions()")
@@ -365,6 +368,8 @@ def _solve_spd_device(M, A, b, guard, stats):
 
 def project(problem: ProjectionProblem, parallel=False, stats=None):
     """Assemble (GPU), solve, return (x, M, b) (src/projection.py:263-279)."""
+    from . import _adapt
+    problem = _adapt.problem(problem)
     M = assemble_mass(problem.basis2d, problem.config, problem.coeff, strategy=problem.strategy)
     b = assemble_rhs(problem)
     local = {}

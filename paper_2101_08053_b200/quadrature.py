@@ -138,6 +138,8 @@ def _layout_from_counts(basis: Basis1D, counts) -> PointLayout:
 
 def place_wq_points(basis: Basis1D) -> PointLayout:
     """src/quadrature.py:155-157."""
+    from . import _adapt
+    basis = _adapt.basis1d(basis)
     return _layout_from_counts(basis, _required_counts(basis))
 
 
@@ -160,9 +162,19 @@ def moments_device(basis: Basis1D):
 
 
 def mass_matrix_1d(basis: Basis1D, trial_basis=None) -> np.ndarray:
-    """Exact 1-D mass matrix (src/quadrature.py:160-188), formed on the GPU."""
+    """Exact 1-D mass matrix (src/quadrature.py:160-188), formed on the GPU:
+    the banded moments (tq_moments_1d_g) for one space, the dense mixed
+    matrix (tq_mass_1d_mixed) against another trial space on the same
+    breakpoints."""
+    from . import _adapt
+    basis, trial_basis = _adapt.basis1d(basis), _adapt.basis1d(trial_basis)
     if trial_basis is not None and trial_basis is not basis:
-        raise NotImplementedError("mixed test/trial bases are not on the formation path")
+        nb = max(basis.p, trial_basis.p) + 1
+        gx, gw = gauss_device(nb)
+        M = torch.empty((basis.n, trial_basis.n), dtype=torch.float64, device=L.device())
+        L.call("tq_mass_1d_mixed", basis.device(), trial_basis.device(), L.ptr(gx), L.ptr(gw), nb, L.ptr(M),
+               L.stream())
+        return M.cpu().numpy()
     band = moments_device(basis).cpu().numpy()
     n, p = basis.n, basis.p
     M = np.zeros((n, n))
@@ -323,6 +335,8 @@ def _least_covered_element(basis, layout, i):
 def compute_wq_rules(basis: Basis1D, layout: PointLayout | None = None, direction=None) -> WeightedRuleSet:
     """WQ rules for every test function, GPU fits + enrichment retries
     (src/quadrature.py:312-337)."""
+    from . import _adapt
+    basis, layout = _adapt.basis1d(basis), _adapt.layout(layout)
     if layout is None:
         layout = place_wq_points(basis)
     counts = layout.counts().copy()
@@ -458,6 +472,8 @@ def build_dwq(basis: Basis1D, layout: PointLayout, u_disc: float, direction=None
               regular_side=None, only_rows=None, plan=None) -> DiscontinuousRuleSet:
     """Discontinuous WQ (src/quadrature.py:366-449): host layout plan, GPU
     fits of the refined rows with enrichment retries, GPU w = S^T w~."""
+    from . import _adapt
+    basis, layout = _adapt.basis1d(basis), _adapt.layout(layout)
     plan = plan or DwqPlan(basis, layout, u_disc, only_rows)
     for attempt in range(MAX_RETRIES + 1):
         rs, fail = dwq_solve_async(plan, direction, regular_side)

@@ -255,8 +255,16 @@ class SubdivisionMatrix:
     def apply(self, coeffs):
         return self.matrix @ np.asarray(coeffs)
 
+    def bandwidth(self):
+        """max |row - col| over the stored entries (src/splines.py:356-360)."""
+        m = self.matrix.tocoo()
+        return int(np.max(np.abs(m.row - m.col))) if m.nnz else 0
+
     def __matmul__(self, other):
         return SubdivisionMatrix(self.matrix @ other.matrix, other.source, self.target)
+
+    def __repr__(self):
+        return f"SubdivisionMatrix({self.shape[0]}x{self.shape[1]})"
 
 
 def insert_knot(basis: Basis1D, ubar: float):

@@ -37,6 +37,25 @@ class DwqInfo:
     cut: list
 
 
+@dataclass(frozen=True)
+class Intersection:
+    """A curve/edge intersection (src/trimming.py:59-66)."""
+    t: float
+    coord: float
+    point: tuple
+    tangential: bool = False
+
+
+@dataclass
+class SubCell:
+    """One mapped integration cell with its quadrature (src/trimming.py:740-746).
+    The device decomposition does not report the cell shape: ``kind`` is
+    'cell'."""
+    kind: str
+    points: np.ndarray
+    weights: np.ndarray
+
+
 def _integral_image(a):
     out = np.zeros((a.shape[0] + 1, a.shape[1] + 1), dtype=np.int64)
     out[1:, 1:] = np.cumsum(np.cumsum(a, axis=0), axis=1)
@@ -153,7 +172,11 @@ class TrimConfiguration:
         if cache and q in self._cut_rules:
             return self._cut_rules[q]
         pending = self._cut_pending.pop(q, None) if cache else None
-        if pending is not None:           # started by cut_cell_rule_async
+        source = getattr(self, "_cut_rule_source", None)
+        if source is not None:            # a caller-built configuration with non-device curves
+            from . import _adapt
+            rule = _adapt.cut_rule_from(source, q)
+        elif pending is not None:         # started by cut_cell_rule_async
             rule = pending.result()
         else:
             from . import _classify
@@ -167,6 +190,8 @@ class TrimConfiguration:
         C++ decomposition runs without the GIL); ``cut_cell_rule(q)`` joins."""
         if q in self._cut_rules or q in self._cut_pending or not self.has_cuts():
             return
+        if getattr(self, "_cut_rule_source", None) is not None:
+            return
         if self.element_class_dev is not None and self.element_class_dev.is_cuda:
             return          # decomposed on the device on first use (tq_cutcell_device)
         from . import _classify
@@ -179,6 +204,24 @@ class TrimConfiguration:
         cut = [(a1 + r, a2 + c) for r, c in zip(*np.nonzero(blk == CUT))]
         return reg, cut
 
+    def is_inside(self, points):
+        """Valid-region test of every curve (src/trimming.py:493-498), on the device."""
+        pts = np.atleast_2d(np.asarray(points, dtype=float))
+        inside = np.ones(pts.shape[0], dtype=bool)
+        for curve in self.curves:
+            inside &= np.asarray(curve.is_inside(pts), dtype=bool)
+        return inside
+
+    def dwq_info(self, i1, i2):
+        """DWQ routing of one basis function (src/trimming.py:536-586): the
+        device routing kernel (tq_dwq_route, the one the assembly uses) on
+        that function, cached like the reference's ``_dwq_cache``."""
+        key = (int(i1), int(i2))
+        info = self._dwq_cache.get(key)
+        if info is None:
+            info = self._dwq_cache[key] = _dwq_info(self, *key)
+        return info
+
 
 # ---------------------------------------------------------------------------
 # trimming curves: descriptors for the device classifier / host decomposition
@@ -186,7 +229,17 @@ class TrimConfiguration:
 # ---------------------------------------------------------------------------
 
 class TrimmingCurve:
-    """Oriented curve; the valid domain lies to the left (src/trimming.py:69-95)."""
+    """Oriented curve; the valid domain lies to the left (src/trimming.py:69-95).
+
+    The predicate interface -- ``signed_distance``, ``is_inside`` and
+    ``intersect_line`` -- runs on the device (``tq_curve_eval``,
+    ``tq_curve_intersect_line``) with the very predicates the classifier and
+    the cut-cell decomposition use, for every curve that has a device
+    ``descriptor()``.  ``evaluate`` / ``derivative`` are the closed-form
+    parametrisations (host).  A subclass without a descriptor keeps its own
+    Python predicates; it cannot be classified on the device, but a
+    configuration built around it by the reference package can be passed to
+    the formation entry points (see ``_adapt``)."""
     straight = False
     closed = False
 
@@ -194,7 +247,52 @@ class TrimmingCurve:
         return self.evaluate(np.linspace(0.0, 1.0, n))
 
     def descriptor(self):
-        raise NotImplementedError
+        raise NotImplementedError(f"{type(self).__name__} has no device descriptor; use LineTrim, CircleTrim, "
+                                  "ClosedCircleTrim, BezierTrim or PeriodicBSplineTrim, or build the "
+                                  "configuration with the reference's classify_elements and pass it in")
+
+    def _device_op(self, op, values, width):
+        from . import _classify
+        x = np.ascontiguousarray(values, dtype=np.float64)
+        n = x.shape[0]
+        if n == 0:
+            return np.empty((0, 2)) if width == 2 else np.empty(0)
+        arr, keep = _classify.curve_array([self])
+        xin = L.dev(x.reshape(-1), torch.float64)
+        out = torch.empty(n * width, dtype=torch.float64, device=L.device())
+        L.call("tq_curve_eval", arr, op, L.ptr(xin), n, L.ptr(out), L.stream())
+        o = out.cpu().numpy()
+        return o.reshape(n, 2) if width == 2 else o
+
+    def signed_distance(self, points):
+        """Distance to the curve, positive on the valid side (src/trimming.py:80-82)."""
+        return self._device_op(2, np.atleast_2d(np.asarray(points, dtype=float)), 1)
+
+    def is_inside(self, points):
+        """True in the valid (left) region, on-curve counts inside (src/trimming.py:76-78)."""
+        return self._device_op(3, np.atleast_2d(np.asarray(points, dtype=float)), 1) != 0.0
+
+    def intersect_line(self, axis, level):
+        """All (t, cross coordinate) where the curve meets {axis = level},
+        'v' = vertical line u1 = level (src/trimming.py:84-93): the hits the
+        device classifier sweeps (tangential touches dropped, duplicates
+        merged, sorted by cross coordinate)."""
+        if axis not in ("v", "h"):
+            raise ValueError("axis must be 'v' or 'h'")
+        from . import _classify
+        arr, keep = _classify.curve_array([self])
+        cap = 64
+        dev = L.device()
+        ht = torch.empty(cap, dtype=torch.float64, device=dev)
+        hc = torch.empty(cap, dtype=torch.float64, device=dev)
+        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+        L.call("tq_curve_intersect_line", arr, 0 if axis == "v" else 1, float(level), cap, L.ptr(ht), L.ptr(hc),
+               L.ptr(cnt), L.stream())
+        n, ovf = (int(v) for v in cnt.cpu().tolist())
+        if ovf or n > cap:
+            raise TrimmingConfigurationError("too many curve crossings on one grid line")
+        t, c = ht[:n].cpu().numpy(), hc[:n].cpu().numpy()
+        return [(float(a), float(b)) for a, b in zip(t, c)]
 
 
 class LineTrim(TrimmingCurve):
@@ -331,26 +429,168 @@ class BezierTrim(TrimmingCurve):
         return 4, 0, np.concatenate([self.ctrl.ravel(), np.concatenate(self.anchors)])
 
 
-def classify_elements(basis2d: TensorBasis2D, curves) -> TrimConfiguration:
-    """Classify elements and functions on the GPU (src/trimming.py:607-733)."""
-    curves = list(curves)
-    b1, b2 = basis2d.dir
+def classify_point(curves, point):
+    """True where ``point`` lies in the valid region of every curve
+    (src/trimming.py:371-377): a bool for one point, else a bool array."""
+    pts = np.atleast_2d(np.asarray(point, dtype=float))
+    inside = np.ones(pts.shape[0], dtype=bool)
+    for curve in curves:
+        inside &= np.asarray(curve.is_inside(pts), dtype=bool)
+    return bool(inside.all()) if pts.shape[0] == 1 else inside
+
+
+def _is_tangential(curve, t, axis):
+    """src/trimming.py:399-403."""
+    d = np.asarray(curve.derivative(t)).reshape(-1)
+    k = 0 if axis == "v" else 1
+    return abs(d[k]) < 1e-9 * max(np.hypot(d[0], d[1]), 1e-30)
+
+
+def intersect_edge(curve, axis, level, lo, hi):
+    """Intersections of a curve with the axis-aligned segment {axis = level}
+    x [lo, hi], tangential touches flagged, sorted along the edge
+    (src/trimming.py:380-396)."""
+    hits = []
+    for item in curve.intersect_line(axis, level):
+        t, coord = item[0], item[1]
+        tangential = _is_tangential(curve, t, axis)
+        if lo - 1e-12 <= coord <= hi + 1e-12:
+            pt = (level, coord) if axis == "v" else (coord, level)
+            hits.append(Intersection(t, float(coord), pt, tangential))
+    hits.sort(key=lambda h: h.coord)
+    return hits
+
+
+# sub-cell capacity of a single-element decomposition (the split depth is at
+# most 4: far fewer cells than this are ever produced)
+_DECOMP_CELLS = 256
+
+
+def decompose_cut_element(bounds, curve, q):
+    """Sub-cells of one cut element with (q+1)^2 Gauss points each
+    (src/trimming.py:938-1056), decomposed on the device by the kernel the
+    configurations use (tq_cutcell_device_slots on a one-element mesh)."""
+    from . import _classify
+    if q < 1:
+        raise ValueError("Lagrange degree q must be >= 1")
+    x0, x1, y0, y1 = (float(v) for v in bounds)
     dev = L.device()
-    nel1, nel2 = b1.num_elements, b2.num_elements
-    n1, n2 = basis2d.shape
+    arr, keep = _classify.curve_array([curve])
+    tabs = _classify.cell_tables(q)
+    bp1 = L.dev(np.array([x0, x1]), torch.float64)
+    bp2 = L.dev(np.array([y0, y1]), torch.float64)
+    el = torch.zeros(2, dtype=torch.int32, device=dev)
+    m = (q + 1) ** 2
+    cap = _DECOMP_CELLS * m
+    sP = torch.empty(2 * cap, dtype=torch.float64, device=dev)
+    sW = torch.empty(cap, dtype=torch.float64, device=dev)
+    ptr = torch.zeros(2, dtype=torch.int64, device=dev)
+    nc = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    L.call("tq_cutcell_device_slots", arr, 1, L.ptr(bp1), L.ptr(bp2), L.ptr(el), 1, q, tabs.ctypes.data_as(L.vp),
+           cap, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(nc), L.ptr(st), L.stream())
+    status, npts, ncells = int(st.item()), int(ptr[1].item()), int(nc.item())
+    if status:
+        raise TrimmingConfigurationError(_classify._CUT_ERRORS.get(status, "decomposition failed"))
+    if npts > cap or npts != ncells * m:
+        raise RuntimeError(f"cut-cell decomposition returned {npts} points for {ncells} cells")
+    P = sP[:2 * npts].reshape(npts, 2).cpu().numpy()
+    W = sW[:npts].cpu().numpy()
+    return [SubCell("cell", P[k * m:(k + 1) * m], W[k * m:(k + 1) * m]) for k in range(ncells)]
+
+
+def cut_cell_quadrature(config, q):
+    """Quadrature of every cut element of a configuration (src/trimming.py:1084-1111):
+    1 <= q <= 6 as in the reference (the formation path itself calls
+    ``config.cut_cell_rule`` without that cap), decomposed on the
+    device."""
+    if q < 1 or q > 6:
+        raise ValueError("Lagrange degree q must be within 1..6")
+    return config.cut_cell_rule(q, cache=False)
+
+
+def _dwq_info(config, i1, i2):
+    """src/trimming.py:545-586 through tq_dwq_route (fclass.cu k_dwq_route)."""
+    b1, b2 = config.basis2d.dir
+    n2 = b2.n
+    u1, u2 = config.u_disc
+    dev = L.device()
+    du1 = L.dev(u1 if u1.size else np.zeros(1), torch.float64)
+    du2 = L.dev(u2 if u2.size else np.zeros(1), torch.float64)
+    rows = torch.tensor([i1 * n2 + i2], dtype=torch.int32, device=dev)
+    out = torch.empty(8, dtype=torch.int32, device=dev)
+    L.call("tq_dwq_route", b1.device(), b2.device(), L.ptr(config.element_class_dev), L.ptr(du1), u1.size,
+           L.ptr(du2), u2.size, L.ptr(rows), 1, L.ptr(out), L.stream())
+    r = [int(v) for v in out.cpu().tolist()]
+    reg, cut = config.support_split(i1, i2)
+    if r[0] == 0:
+        return DwqInfo(False, (None, None), None, (None, None), reg, cut)
+    if r[3] < 0:
+        return DwqInfo(True, (None, None), None, (None, None), reg, cut)
+    box = ((r[3], r[4]), (r[5], r[6]))
+    used, sides = [], []
+    for iu, ud, basis, (lo, _hi) in ((r[1], u1, b1, box[0]), (r[2], u2, b2, box[1])):
+        if iu < 0:
+            used.append(None)
+            sides.append(None)
+            continue
+        u = float(ud[iu])
+        k = int(np.argmin(np.abs(basis.breakpoints - u)))
+        used.append(u)
+        sides.append("right" if lo == k else "left")
+    residual = [(f1, f2) for (f1, f2) in reg
+                if not (box[0][0] <= f1 <= box[0][1] and box[1][0] <= f2 <= box[1][1])]
+    return DwqInfo(True, tuple(used), box, tuple(sides), residual, cut)
+
+
+def classify_elements(basis2d: TensorBasis2D, curves) -> TrimConfiguration:
+    """Classify elements and functions on the GPU (src/trimming.py:607-733).
+    Reference-built bases and catalog curves are accepted (``_adapt``); a
+    curve the device cannot evaluate raises TypeError."""
+    from . import _adapt
+    basis2d = _adapt.basis2d(basis2d)
+    src = list(curves)
+    curves, known = _adapt.curves(src)
+    if not known:
+        bad = [type(c).__name__ for c in src if _adapt.curve(c) is None]
+        raise TypeError(f"curves {bad} cannot be evaluated on the device; classify with the reference's "
+                        "classify_elements and pass that configuration to the formation entry points")
+    b1, b2 = basis2d.dir
     if curves:
         from . import _classify
         ec = _classify.classify_device(basis2d, curves)
     else:
-        ec = torch.full((nel1, nel2), INTERIOR, dtype=torch.int8, device=dev)
+        ec = torch.full((b1.num_elements, b2.num_elements), INTERIOR, dtype=torch.int8, device=L.device())
+    return configuration_from_classes(basis2d, curves, ec)
+
+
+def configuration_from_classes(basis2d: TensorBasis2D, curves, element_class) -> TrimConfiguration:
+    """Function classes, discontinuity faces and the configuration from
+    element classes (device int8 nel1 x nel2, or a host array that is
+    uploaded): src/trimming.py:431-484 on the GPU (tq_function_classes)."""
+    b1, b2 = basis2d.dir
+    dev = L.device()
+    nel1, nel2 = b1.num_elements, b2.num_elements
+    n1, n2 = basis2d.shape
+    if not isinstance(element_class, torch.Tensor):
+        ec_h = np.asarray(element_class)
+        if ec_h.shape != (nel1, nel2):
+            raise ValueError(f"element classes of shape {ec_h.shape} for a {nel1} x {nel2} mesh")
+        element_class = L.dev(ec_h.astype(np.int8), torch.int8)
+    ec = element_class.reshape(nel1, nel2)
     fc = torch.empty((n1, n2), dtype=torch.int8, device=dev)
     face1 = torch.zeros(max(nel1 - 1, 1), dtype=torch.int32, device=dev)
     face2 = torch.zeros(max(nel2 - 1, 1), dtype=torch.int32, device=dev)
-    fn = L.optional("tq_function_classes", [L.Space1D, L.Space1D, L.vp, L.vp, L.vp, L.vp, L.vp])
-    if fn is None:
-        raise RuntimeError("native library lacks tq_function_classes")
     L.call("tq_function_classes", b1.device(), b2.device(), L.ptr(ec), L.ptr(fc), L.ptr(face1),
            L.ptr(face2), L.stream())
     f1 = face1.cpu().numpy()[: max(nel1 - 1, 0)] != 0
     f2 = face2.cpu().numpy()[: max(nel2 - 1, 0)] != 0
     return TrimConfiguration(basis2d, curves, ec, fc, f1, f2)
+
+
+def __getattr__(name):
+    # the reference's name for the cut-cell rule container (src/trimming.py:749-766)
+    if name == "CutCellQuadrature":
+        from ._classify import CutCellRule
+        return CutCellRule
+    raise AttributeError(name)

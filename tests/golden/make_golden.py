@@ -270,9 +270,36 @@ def main():
     ap.add_argument("--big", action="store_true", help="also configs 3/4 (minutes)")
     ap.add_argument("--huge", action="store_true", help="only the config-5 headline golden (~15 min, ~30 GB)")
     ap.add_argument("--p4small", action="store_true", help="only the full small B-spline p=4 goldens")
+    ap.add_argument("--retry", action="store_true", help="only the WQ enrichment-retry golden")
     ap.add_argument("--l2aug", default="", help="comma list of config5* goldens to add a seeded l2_error to")
     args = ap.parse_args()
     t_all = time.perf_counter()
+    if args.retry:
+        # WQ enrichment retries (src/quadrature.py:312-337): starting layouts
+        # with too few points; the reference's final per-element counts (an
+        # integer outcome of the retry loop) or its RuleConstructionError
+        d = {}
+        cases = [(8, 3, "drop", 3, 2), (8, 3, "drop", 1, 2), (8, 3, "drop", 6, 2), (8, 3, "zero", 0, 0),
+                 (3, 3, "zero", 0, 0), (2, 6, "zero", 0, 0), (10, 6, "zero", 0, 0), (12, 8, "zero", 0, 0)]
+        for k, (nel, p, kind, e, drop) in enumerate(cases):
+            b = RS.make_uniform_basis(nel, p)
+            lay = RQ.place_wq_points(b)
+            c = np.diff(lay.offsets).astype(np.int64)
+            if kind == "zero":
+                c[:] = 0
+            else:
+                c[e] = max(c[e] - drop, 0)
+            d[f"c{k}_case"] = np.array([nel, p])
+            d[f"c{k}_start"] = c
+            try:
+                r = RQ.compute_wq_rules(b, RQ._layout_from_counts(b, c))
+                d[f"c{k}_final"] = np.diff(r.layout.offsets).astype(np.int64)
+            except RQ.RuleConstructionError as err:
+                d[f"c{k}_error"] = str(err)
+        d["ncases"] = len(cases)
+        np.savez_compressed(os.path.join(HERE, "rules_retry.npz"), **d)
+        print("rules_retry done", flush=True)
+        return
     if args.l2aug:
         # l2_error of a seeded coefficient vector (src/projection.py:221-260)
         # added to the config-5 recipe goldens (a solve at 2048^2 is out of
