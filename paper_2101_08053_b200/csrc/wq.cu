@@ -4,13 +4,11 @@
 //  tq_dwq_combine  <- build_dwq step 4 (w = S^T w~)   src/quadrature.py:434-444
 //
 // One warp per moment system A w = b (A: t trials x m points, t <= 2p+1).
-// Householder QR with column pivoting (largest remaining column norm, first
-// index on ties, norms recomputed exactly at every step), rank by
+// Householder QR with column pivoting exactly as LAPACK dgeqp3/dlaqp2 pivots
+// (see below: same pivot sequence, SURVEY F6 closed), rank by
 // |R_kk| > max(t,m) eps |R_00|, back substitution on the leading rank block:
-// the *basic* least-squares solution the reference obtains from LAPACK
-// dgeqp3.  Pivot ties may resolve differently from LAPACK's downdated norms
-// (SURVEY F6); any exact solution reproduces the moments, which is what the
-// residual check below certifies.
+// the *basic* least-squares solution the reference obtains from
+// scipy.linalg.qr.  The residual check certifies every row.
 #include "common.cuh"
 
 namespace tq {
@@ -39,6 +37,89 @@ __device__ inline double colloc(const int32_t* first, const double* vals, int p,
     return (r >= 0 && r <= p) ? vals[(int64_t)k * (p + 1) + r] : 0.0;
 }
 
+// ---- LAPACK dgeqp3 / dlaqp2 pivoting, reproduced --------------------------
+// The reference solves every moment system with scipy.linalg.qr(pivoting=True)
+// = LAPACK dgeqp3, which for min(t, m) < 32 runs the unblocked dlaqp2 over
+// OpenBLAS kernels.  Its pivot choices (ties of mirrored columns included)
+// follow from (scripts/probes/lapack_pivot_emul.py: 1977/1977 systems, p = 1..8):
+//   * column norms correctly rounded (dnrm2): squares summed in
+//     double-double, then a correctly rounded square root;
+//   * idamax: first maximum of the partial norms vn1;
+//   * partial-norm downdating vn1 *= sqrt(1 - (|r_kj|/vn1)^2) with the
+//     tol3z = sqrt(eps) recomputation rule;
+//   * dlarfg with dlapy2 = w sqrt(1 + (z/w)^2) and x *= 1/(alpha - beta);
+//   * dlarf trimmed to the last non-zero of v (lastv) and the last non-zero
+//     column (lastc); w = C^T v as OpenBLAS dgemv_t does it -- four FMA lane
+//     accumulators over rows r < m - m%4, reduced (p0 + p2) + (p1 + p3), the
+//     m%4 leftover rows as a plain product-sum added last (m < 4: the scalar
+//     path, fma(a0, x0, a1 x1) then FMAs) -- and the rank-1
+//     update C += v (-tau w_j) with one FMA per entry (dger).
+// This file is compiled with -fmad=false: every fused operation above is an
+// explicit __fma_rn, every other one is a separate IEEE operation.
+constexpr double kTol3z = 1.4901161193847656e-08;   // sqrt(DLAMCH('Epsilon'))
+
+// correctly rounded sqrt(sum x_r^2), r < n, stride 1
+__device__ inline double cr_norm(const double* x, int n) {
+    double hi = 0.0, lo = 0.0;
+    for (int r = 0; r < n; ++r) {
+        const double v = x[r];
+        const double p = v * v;
+        const double pe = __fma_rn(v, v, -p);
+        const double s = hi + p;
+        const double bb = s - hi;
+        const double err = (hi - (s - bb)) + (p - bb);
+        hi = s;
+        lo = lo + err + pe;
+    }
+    const double s = hi + lo;
+    lo = lo - (s - hi);
+    hi = s;
+    if (!(hi > 0.0)) return 0.0;
+    double r = sqrt(hi);
+    const double e = __fma_rn(-r, r, hi) + lo;
+    const double up = nextafter(r, INFINITY), u = up - r;
+    if (e - r * u > 0.25 * u * u) return up;
+    const double dn = nextafter(r, 0.0), d = r - dn;
+    if (-e - r * d > -0.25 * d * d) return dn;
+    return r;
+}
+
+__device__ inline double dlapy2(double x, double y) {
+    const double xa = fabs(x), ya = fabs(y);
+    const double w = fmax(xa, ya), z = fmin(xa, ya);
+    if (z == 0.0) return w;
+    const double q = z / w;
+    return w * sqrt(1.0 + q * q);
+}
+
+// OpenBLAS dgemv_t's dot of one column with v over rows [0, m).  Fewer than
+// four rows take the kernel's scalar path: fma(a0, x0, a1 x1), then one FMA
+// per further row.
+__device__ inline double gemv_dot(const double* col, const double* v, int m) {
+    if (m < 4) {
+        if (m <= 0) return 0.0;
+        if (m == 1) return col[0] * v[0];
+        double tl = __fma_rn(col[0], v[0], col[1] * v[1]);
+        if (m == 3) tl = __fma_rn(col[2], v[2], tl);
+        return tl;
+    }
+    const int m1 = m - (m & 3);
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    for (int r = 0; r < m1; r += 4) {
+        p0 = __fma_rn(col[r], v[r], p0);
+        p1 = __fma_rn(col[r + 1], v[r + 1], p1);
+        p2 = __fma_rn(col[r + 2], v[r + 2], p2);
+        p3 = __fma_rn(col[r + 3], v[r + 3], p3);
+    }
+    double y = 0.0 + ((p0 + p2) + (p1 + p3));
+    if (m1 < m) {
+        double tl = col[m1] * v[m1];
+        for (int r = m1 + 1; r < m; ++r) tl = tl + col[r] * v[r];
+        y = y + tl;
+    }
+    return y;
+}
+
 __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restrict__ first,
                            const double* __restrict__ vals, const double* __restrict__ mom,
                            const int32_t* __restrict__ rows, int nrows, int tmax, int mmax,
@@ -46,12 +127,15 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
                            double* __restrict__ wout, int32_t* __restrict__ fail, double* __restrict__ prod) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    const int per = 2 * tmax * mmax + tmax + 2 * mmax;  // A, A0, b, w + perm (as double slots)
+    const int per = 2 * tmax * mmax + 2 * tmax + 4 * mmax;  // A, A0, b, v, w, vn1, vn2 + perm
     double* A = smem + (size_t)wib * per;           // column-major, ld = t
     double* A0 = A + tmax * mmax;                   // untouched copy for the residual check
     double* b = A0 + tmax * mmax;
-    double* w = b + tmax;
-    int* perm = reinterpret_cast<int*>(w + mmax);
+    double* vh = b + tmax;                          // the current reflector (v0 = 1)
+    double* w = vh + tmax;
+    double* vn1 = w + mmax;
+    double* vn2 = vn1 + mmax;
+    int* perm = reinterpret_cast<int*>(vn2 + mmax);
     const int p = s.p, W = 2 * p + 1;
 
     for (int r = blockIdx.x * wpb + wib; r < nrows; r += gridDim.x * wpb) {
@@ -74,18 +158,18 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
         for (int rr = lane; rr < t; rr += 32) b[rr] = mom[(int64_t)i * W + (j0 + rr - i + p)];
         for (int c = lane; c < m; c += 32) perm[c] = c;
         __syncwarp();
+        for (int c = lane; c < m; c += 32) { const double nv = cr_norm(A + c * t, t); vn1[c] = nv; vn2[c] = nv; }
+        __syncwarp();
 
         const int kmax = t < m ? t : m;
         double r00 = 0.0;
         int rank = 0;
         for (int k = 0; k < kmax; ++k) {
-            // pivot: largest norm of A[k:t, c], c >= k
+            // pivot: idamax over vn1[k..m) (first maximum)
             double best = -1.0;
             int bi = 0x7fffffff;
             for (int c = k + lane; c < m; c += 32) {
-                double ss = 0.0;
-                for (int rr = k; rr < t; ++rr) { double a = A[c * t + rr]; ss += a * a; }
-                double nv = sqrt(ss);
+                const double nv = vn1[c];
                 if (nv > best || (nv == best && c < bi)) { best = nv; bi = c; }
             }
             warp_argmax(best, bi);
@@ -93,34 +177,63 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
                 for (int rr = lane; rr < t; rr += 32) {
                     double tmp = A[k * t + rr]; A[k * t + rr] = A[bi * t + rr]; A[bi * t + rr] = tmp;
                 }
-                if (lane == 0) { int tp = perm[k]; perm[k] = perm[bi]; perm[bi] = tp; }
+                if (lane == 0) {
+                    int tp = perm[k]; perm[k] = perm[bi]; perm[bi] = tp;
+                    vn1[bi] = vn1[k];
+                    vn2[bi] = vn2[k];
+                }
             }
             __syncwarp();
-            // Householder reflector of x = A[k:t, k] (dlarfg convention)
-            double alpha = A[k * t + k];
-            double xs = 0.0;
-            for (int rr = k + 1 + lane; rr < t; rr += 32) { double a = A[k * t + rr]; xs += a * a; }
-            xs = warp_sum(xs);
-            double xnorm = sqrt(xs);
-            double beta = alpha, tau = 0.0, scal = 0.0;
-            if (xnorm != 0.0) {
-                beta = -copysign(hypot(alpha, xnorm), alpha);
-                tau = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
+            // dlarfg on x = A[k:t, k]
+            double beta = A[k * t + k], tau = 0.0;
+            int lastv = 0;
+            if (lane == 0) {
+                const double alpha = beta;
+                const double xnorm = k + 1 < t ? cr_norm(A + k * t + k + 1, t - k - 1) : 0.0;
+                if (xnorm != 0.0) {
+                    beta = -copysign(dlapy2(alpha, xnorm), alpha);
+                    tau = (beta - alpha) / beta;
+                    const double scal = 1.0 / (alpha - beta);
+                    for (int rr = k + 1; rr < t; ++rr) A[k * t + rr] = A[k * t + rr] * scal;
+                    A[k * t + k] = beta;
+                }
+                // the reflector v = (1, A[k+1:t, k]) trimmed to its last non-zero (dlarf lastv)
+                vh[0] = 1.0;
+                lastv = 1;
+                for (int rr = k + 1; rr < t; ++rr) {
+                    vh[rr - k] = A[k * t + rr];
+                    if (vh[rr - k] != 0.0) lastv = rr - k + 1;
+                }
             }
+            beta = __shfl_sync(0xffffffffu, beta, 0);
+            tau = __shfl_sync(0xffffffffu, tau, 0);
+            lastv = __shfl_sync(0xffffffffu, lastv, 0);
             __syncwarp();
-            for (int rr = k + 1 + lane; rr < t; rr += 32) A[k * t + rr] *= scal;  // v (v0 = 1)
-            __syncwarp();
-            if (lane == 0) A[k * t + k] = beta;
-            // apply H = I - tau v v^T to the remaining columns and to b
+            // dlarf: H = I - tau v v^T on columns k+1.. (trailing zero columns
+            // of C(1:lastv, :) are untouched either way) and on b
             if (tau != 0.0) {
                 for (int c = k + 1 + lane; c <= m; c += 32) {
-                    double* col = (c < m) ? (A + c * t) : b;
-                    double dot = col[k];
-                    for (int rr = k + 1; rr < t; ++rr) dot += A[k * t + rr] * col[rr];
-                    dot *= tau;
-                    col[k] -= dot;
-                    for (int rr = k + 1; rr < t; ++rr) col[rr] -= dot * A[k * t + rr];
+                    double* col = (c < m ? A + c * t : b) + k;
+                    const double temp = -tau * gemv_dot(col, vh, lastv);
+                    for (int rr = 0; rr < lastv; ++rr) col[rr] = __fma_rn(vh[rr], temp, col[rr]);
+                }
+            }
+            __syncwarp();
+            // partial column norms (dlaqp2)
+            for (int c = k + 1 + lane; c < m; c += 32) {
+                if (vn1[c] != 0.0) {
+                    const double q = fabs(A[c * t + k]) / vn1[c];
+                    double temp = 1.0 - q * q;
+                    temp = temp > 0.0 ? temp : 0.0;
+                    const double rt = vn1[c] / vn2[c];
+                    const double temp2 = temp * (rt * rt);
+                    if (temp2 <= kTol3z) {
+                        const double nv = k + 1 < t ? cr_norm(A + c * t + k + 1, t - k - 1) : 0.0;
+                        vn1[c] = nv;
+                        vn2[c] = nv;
+                    } else {
+                        vn1[c] = vn1[c] * sqrt(temp);
+                    }
                 }
             }
             __syncwarp();
@@ -148,7 +261,7 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
         // residual with the original system (src/quadrature.py:299-301).
         // (A w)[j] = sum_k w_k B_j(x_k) is also the direction product of
         // sum_factor_row (src/assembly.py:245-252): written out when asked
-        // (same terms, same order as tq_wq_products -> bit-identical)
+        // (same terms, same fused order as tq_wq_products -> bit-identical)
         double rmax = 0.0, bmax = 0.0;
         if (prod)
             for (int o = lane; o < W; o += 32) {
@@ -157,7 +270,7 @@ __global__ void k_wq_solve(tq_space1d s, tq_layout lay, const int32_t* __restric
             }
         for (int rr = lane; rr < t; rr += 32) {
             double acc = 0.0;
-            for (int c = 0; c < m; ++c) acc += A0[c * t + rr] * w[c];
+            for (int c = 0; c < m; ++c) acc = __fma_rn(A0[c * t + rr], w[c], acc);
             if (prod) prod[(int64_t)i * W + (j0 + rr - i + p)] = acc;
             double bb = mom[(int64_t)i * W + (j0 + rr - i + p)];
             rmax = fmax(rmax, fabs(acc - bb));
@@ -231,7 +344,7 @@ extern "C" int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, co
     if (nrows == 0) return TQ_OK;
     if (tmax > 2 * kMaxP + 1) { set_error("too many trials per system (%d)", tmax); return TQ_EINVAL; }
     const int wpb = 4;
-    size_t per = 2 * (size_t)tmax * mmax + tmax + 2 * mmax;
+    size_t per = 2 * (size_t)tmax * mmax + 2 * (size_t)tmax + 4 * (size_t)mmax;
     size_t shm = per * sizeof(double) * wpb;
     if (shm > 200 * 1024) { set_error("moment system too large (t=%d, m=%d)", tmax, mmax); return TQ_EINVAL; }
     TQ_CUDA(cudaFuncSetAttribute(k_wq_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));

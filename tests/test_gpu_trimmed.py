@@ -2,11 +2,14 @@
 
 Integers (element/function classes, u_disc, active order, CSR pattern) are
 bit-exact; values rel-Frobenius and per-entry <= 1e-12 (sqrt(M_ii M_jj)
-scaled).  With c == 1 the GPU's own weights are used (any exact weights give
-the same matrix).  With c != 1 and for the naive ``wq`` strategy on trimmed
-spaces the matrix depends on the particular weights, so the
-reference's weight tables are imported (the oracle reproduces them bit for
-bit, tests/test_oracle_golden.py::test_oracle_weights_bit_exact).
+scaled).  The GPU's own weights are used throughout: its pivoted-QR fits
+choose LAPACK dgeqp3's pivots (wq.cu), so even where the matrix depends on
+the particular weights -- c != 1, and the naive ``wq`` strategy on trimmed
+spaces -- it matches the reference (p = 8 at 1e-10, see below).
+Those cases are also checked with the reference's weight tables imported
+(the oracle reproduces them bit for bit,
+tests/test_oracle_golden.py::test_oracle_weights_bit_exact), which isolates
+the row kernels at 1e-12.
 """
 
 import hashlib
@@ -101,19 +104,34 @@ def test_trimmed_matches_reference(tag):
     full = f"{G.strategies_in(d)[0]}_data" in d
     trimmed = d["cut_el"].size > 0
     for s in G.strategies_in(d):
-        rules = None
-        if s != "reference" and (coeff is not None or (s == "wq" and trimmed)):
-            rules = imported_rules(b2d, desc)
-        # (a) native host cut-cell rule: pattern exact, rel-Frobenius 1e-12
-        M = P.assemble_mass(b2d, cfg, coeff, strategy=s, rules=rules).data
+        weight_sensitive = s != "reference" and (coeff is not None or (s == "wq" and trimmed))
+        # (a) the product path as shipped: the GPU's OWN weights (k_wq_solve
+        #     pivots exactly as LAPACK dgeqp3, wq.cu) and the native cut-cell
+        #     rule -- pattern exact, values within 1e-12.  Weight-sensitive
+        #     matrices at p = 8 get 1e-10 on the sampled rows: the p = 8 moment
+        #     systems reach condition 7e8, which amplifies the last-bit
+        #     differences between OpenBLAS's kernel arithmetic and the GPU's
+        #     into ~1e-11 of a few weights (pivots identical; measured max
+        #     1.3e-11, scripts/probes/weights_gap.py).
+        tol = 1e-10 if (weight_sensitive and desc["p"] >= 8) else 1e-12
+        M = P.assemble_mass(b2d, cfg, coeff, strategy=s).data
         assert sha(M.indptr, M.indices) == str(d[f"{s}_hash"]), s
         if full:
             R = sp.csr_matrix((d[f"{s}_data"], d[f"{s}_indices"], d[f"{s}_indptr"]), shape=M.shape)
-            assert np.linalg.norm(M.data - R.data) <= 1e-12 * np.linalg.norm(R.data)
+            assert np.linalg.norm(M.data - R.data) <= tol * np.linalg.norm(R.data)
         else:
             got, ref = golden_rows(M, d, s)
-            assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+            assert np.max(np.abs(got - ref)) <= tol * np.max(np.abs(ref))
             assert abs(sp.linalg.norm(M) - float(d[f"{s}_fro"])) <= 1e-12 * float(d[f"{s}_fro"])
+        rules = imported_rules(b2d, desc) if weight_sensitive else None
+        if rules is not None:
+            # (a') kernels alone: the reference's weight tables imported, 1e-12
+            M = P.assemble_mass(b2d, cfg, coeff, strategy=s, rules=rules).data
+            if full:
+                assert np.linalg.norm(M.data - R.data) <= 1e-12 * np.linalg.norm(R.data)
+            else:
+                got, ref = golden_rows(M, d, s)
+                assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
         # (b) kernels alone: the reference's own cut-cell points injected,
         #     per-entry bar |dM_ij| <= 1e-12 sqrt(M_ii M_jj)
         if full and trimmed:
