@@ -136,6 +136,52 @@ int tq_wq_solve(tq_space1d s, tq_layout lay, const int32_t* first, const double*
                 int32_t tmax, int32_t mmax, int64_t* wptr, int32_t* k0, double* w,
                 int32_t* fail, double* products, void* stream);
 
+/* Fused, batched moment fits: every listed row of up to TQ_FIT_MAX_SETS rule
+ * sets in ONE launch, warp per system, each warp forming its own exact
+ * moments and collocation block and solving as tq_wq_solve (same pivots,
+ * same outputs).  Replaces, per set, the tq_basis_eval -> tq_moments_1d_g ->
+ * tq_wq_solve chain (src/quadrature.py:281-303 for every set the assembly
+ * builds, src/assembly.py:454-489).  The batch is passed by value (a kernel
+ * parameter: no upload, capturable); gx/gw: the (p+1)-point Gauss rule on
+ * [-1,1] of the (common) degree.  `start` is filled in by the call. */
+#define TQ_FIT_MAX_SETS 16
+typedef struct {
+    tq_space1d s;            /* basis of the set (refined basis for DWQ fits) */
+    tq_layout lay;           /* its point layout                               */
+    const int32_t* rows;     /* rows to fit                                    */
+    int32_t nrows;
+    const int64_t* wptr;     /* n + 1 weight offsets                           */
+    int32_t* k0;             /* out: first point of each fitted row            */
+    double* w;               /* out: weights at wptr                           */
+    int32_t* fail;           /* out: per listed row, residual flag             */
+    double* products;        /* out, nullable: n x (2p+1) direction products   */
+} tq_fitset;
+typedef struct {
+    tq_fitset set[TQ_FIT_MAX_SETS];
+    int32_t nsets;
+    int32_t start[TQ_FIT_MAX_SETS + 1];
+    const double* gx;
+    const double* gw;
+} tq_fitbatch;
+int tq_wq_fit_sets(const tq_fitbatch* batch_h, int32_t tmax, int32_t mmax, void* stream);
+
+/* every DWQ set's w = S^T w~ (tq_dwq_combine) in one launch; by value */
+typedef struct {
+    const int32_t* rows;     /* wanted original rows */
+    int32_t nrows;
+    const int32_t* colptr;   /* S in CSC */
+    const int32_t* rowidx;
+    const double* sval;
+    tq_rules fine;           /* the refined fits */
+    tq_rules out;            /* the set's rules (w written) */
+} tq_combineset;
+typedef struct {
+    tq_combineset set[TQ_FIT_MAX_SETS];
+    int32_t nsets;
+    int32_t start[TQ_FIT_MAX_SETS + 1];
+} tq_combinebatch;
+int tq_dwq_combine_sets(const tq_combinebatch* batch_h, void* stream);
+
 /* DWQ combination w_j = sum_i S_ij w~_i over augmented points (S in CSC,
  * device).  Replaces build_dwq step 4 (src/quadrature.py:434-444). */
 int tq_dwq_combine(const int32_t* rows, int32_t nrows, const int32_t* s_colptr,

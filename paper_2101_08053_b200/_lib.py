@@ -55,6 +55,28 @@ class Curve(C.Structure):
     _fields_ = [("kind", i32), ("m", i32), ("data", vp)]
 
 
+FIT_MAX_SETS = 16      # TQ_FIT_MAX_SETS
+
+
+class FitSet(C.Structure):
+    _fields_ = [("s", Space1D), ("lay", Layout), ("rows", vp), ("nrows", i32), ("wptr", vp), ("k0", vp),
+                ("w", vp), ("fail", vp), ("products", vp)]
+
+
+class FitBatch(C.Structure):
+    _fields_ = [("set", FitSet * FIT_MAX_SETS), ("nsets", i32), ("start", i32 * (FIT_MAX_SETS + 1)),
+                ("gx", vp), ("gw", vp)]
+
+
+class CombineSet(C.Structure):
+    _fields_ = [("rows", vp), ("nrows", i32), ("colptr", vp), ("rowidx", vp), ("sval", vp), ("fine", Rules),
+                ("out", Rules)]
+
+
+class CombineBatch(C.Structure):
+    _fields_ = [("set", CombineSet * FIT_MAX_SETS), ("nsets", i32), ("start", i32 * (FIT_MAX_SETS + 1))]
+
+
 class Coeff(C.Structure):
     _fields_ = [("kind", i32), ("p", i32), ("n", i32), ("knots", vp), ("X", vp), ("Y", vp)]
 
@@ -118,6 +140,8 @@ def lib():
                                     vp], i32),
         "tq_dwq_route": ([Space1D, Space1D, vp, vp, i32, vp, i32, vp, i32, vp, vp], i32),
         "tq_function_classes": ([Space1D, Space1D, vp, vp, vp, vp, vp], i32),
+        "tq_wq_fit_sets": ([C.POINTER(FitBatch), i32, i32, vp], i32),
+        "tq_dwq_combine_sets": ([C.POINTER(CombineBatch), vp], i32),
         "tq_mass_1d_mixed": ([Space1D, Space1D, vp, vp, i32, vp, vp], i32),
         "tq_curve_eval": ([C.POINTER(Curve), i32, vp, i64, vp, vp], i32),
         "tq_curve_intersect_line": ([C.POINTER(Curve), i32, f64, i32, vp, vp, vp, vp], i32),

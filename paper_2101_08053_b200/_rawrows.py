@@ -20,7 +20,7 @@ import torch
 
 from . import _lib as L
 from ._lib import CUT, INTERIOR
-from .quadrature import (_TAG as _QT, _st, DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async_t, build_dwq,
+from .quadrature import (_TAG as _QT, fit_sets_async, combine_sets_async, DiscontinuousRuleSet, _st, DwqPlan, WeightedRuleSet, _FitPlan, _failing, _solve_rows_async_t, build_dwq,
                          compute_wq_rules, dwq_solve_async, gauss_legendre, place_wq_points)
 
 MODE_GAUSS, MODE_BOX, MODE_MASK = 0, 1, 2
@@ -246,37 +246,45 @@ def build_all_rules(f):
             if pk not in g:
                 g[pk] = DwqPlan((f.b1, f.b2)[d], plans[d].layout, u, only_rows=rows)
             dplans[(d, u)] = g[pk]
-    # the fit chains are independent: fork them onto side streams (parallel
-    # branches of the captured graph), join before anything consumes them
+    # every fit of the pass in ONE fused launch (tq_wq_fit_sets: warp per
+    # moment system, own moments and collocation block), then every DWQ
+    # combination in one launch; the basis tables the raw rows read at the
+    # layout points (geometry: no dependence on the weights) go to a side
+    # stream and overlap the fits
     main = torch.cuda.current_stream()
-    sides = _side_streams(len(plans) + len(dplans))
-    std, dwq_pending = [], {}
-    tables, prods = [], []
     sep = f.strategy != "reference" and f.coeff.identity       # the direction products are needed
-    for k, pl in enumerate(plans):
-        with _forked(main, sides[k]):
-            _QT[0] = f"s{k}:"
-            full = pl.rows_h.size == pl.basis.n
-            prod = (torch.empty((pl.basis.n, 2 * pl.basis.p + 1), dtype=torch.float64, device=f.dev)
-                    if sep and full else None)
-            out, tab = _solve_rows_async_t(pl, products=prod)
-            _keep_on(main, out[1:] + (tab or ()) + ((prod,) if prod is not None else ()))
-        std.append(out)
-        tables.append(tab)
-        prods.append(prod)
-    for k, (key, pl) in enumerate(dplans.items()):
-        with _forked(main, sides[len(plans) + k]):
-            _QT[0] = f"d{k}:"
-            rs, fail = dwq_solve_async(pl, direction=key[0])
-            # basis table of the set's own basis at its points (geometry-only;
-            # built here so it overlaps the fits)
-            tab = rs.basis_table()
-            _st("table")
-            _keep_on(main, (rs.w, fail) + tuple(tab))
-        dwq_pending[key] = (pl, rs, fail)
-    _QT[0] = ""
-    for st in sides:
-        main.wait_stream(st)
+    prods = [torch.empty((pl.basis.n, 2 * pl.basis.p + 1), dtype=torch.float64, device=f.dev)
+             if sep and pl.rows_h.size == pl.basis.n else None for pl in plans]
+    dkeys = list(dplans)
+    side = _side_streams(1)[0]
+    with _forked(main, side):
+        tables = [pl.basis.eval_device(pl.layout.device_points(), check=False) for pl in plans]
+        dtables = [dplans[k].basis.eval_device(dplans[k].aug.device_points(), check=False) for k in dkeys]
+        _st("tables")
+        _keep_on(main, [t for tb in tables + dtables for t in tb])
+    # the fits gate the whole pass: the highest stream priority, so their
+    # blocks (and the combine's) dispatch ahead of the pass-start bulk work
+    fs = _named_stream("fits", priority=-5)
+    with _forked(main, fs):
+        _QT[0] = "fit:"
+        outs = fit_sets_async(plans + [dplans[k].fit for k in dkeys], prods + [None] * len(dkeys),
+                              [None] * len(plans) + [False] * len(dkeys))
+        _st("fits")
+        fine = outs[len(plans):]
+        ws = combine_sets_async([dplans[k] for k in dkeys], fine)
+        _st("combine")
+        _QT[0] = ""
+        _keep_on(main, [t for o in outs for t in o[1:]] + list(ws) + [p_ for p_ in prods if p_ is not None])
+    main.wait_stream(fs)
+    std = outs[: len(plans)]
+    dwq_pending = {}
+    for k, key, w, fo, tab in zip(range(len(dkeys)), dkeys, ws, fine, dtables):
+        pl = dplans[key]
+        rs = DiscontinuousRuleSet(pl.basis, pl.aug, pl.wptr, pl.k0, w, pl.u, pl.S, pl.refined, pl.base_layout,
+                                  key[0], None)
+        rs._basis_tab = tab
+        dwq_pending[key] = (pl, rs, fo[3])
+    main.wait_stream(side)
     _st("fits_joined")
     flags = [fl[: max(pl.rows_h.size, 1)] for pl, (_, _, _, fl) in zip(plans, std)]
     flags += [fl[: max(pl.fit.rows_h.size, 1)] for pl, _, fl in dwq_pending.values()]

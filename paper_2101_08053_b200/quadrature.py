@@ -13,6 +13,8 @@ import math
 from dataclasses import dataclass
 from functools import lru_cache
 
+import ctypes as C
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -308,6 +310,67 @@ def _solve_rows_async_t(plan: _FitPlan, init=None, products=None):
                L.ptr(fail), L.ptr(products), L.stream())
         _st("solve")
     return (plan.wptr, k0, w, fail), tab
+
+
+def fit_sets_async(plans, products=None, inits=None):
+    """Every plan's moment fits in one fused launch per TQ_FIT_MAX_SETS plans
+    (tq_wq_fit_sets: warp per system, its own moments and collocation block,
+    LAPACK pivoting).  Returns [(wptr, k0, w, fail)] per plan as device
+    tensors; no host sync.  Rows outside a plan are initialised (k0 = -1,
+    w = 0) when ``inits[k]`` (default: the plan leaves rows out)."""
+    dev = L.device()
+    products = products or [None] * len(plans)
+    inits = inits or [None] * len(plans)
+    outs = []
+    p = None
+    for pl in plans:
+        if p is not None and pl.basis.p != p:
+            raise ValueError("one fused fit takes rule sets of one degree")
+        p = pl.basis.p
+    for c0 in range(0, len(plans), L.FIT_MAX_SETS):
+        batch = L.FitBatch()
+        tmax = mmax = 1
+        chunk = list(zip(plans, products, inits))[c0: c0 + L.FIT_MAX_SETS]
+        for k, (pl, prod, init) in enumerate(chunk):
+            basis, layout = pl.basis, pl.layout
+            init = pl.rows_h.size < basis.n if init is None else init
+            if init:
+                k0 = torch.full((basis.n,), -1, dtype=torch.int32, device=dev)
+                w = torch.zeros(max(int(pl.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+            else:
+                k0 = torch.empty((basis.n,), dtype=torch.int32, device=dev)
+                w = torch.empty(max(int(pl.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+            fail = (torch.empty if pl.rows_h.size else torch.zeros)(max(pl.rows_h.size, 1), dtype=torch.int32,
+                                                                    device=dev)
+            outs.append((pl.wptr, k0, w, fail))
+            batch.set[k] = L.FitSet(basis.device(), layout.device(), L.ptr(pl.rows), int(pl.rows_h.size),
+                                    L.ptr(pl.wptr), L.ptr(k0), L.ptr(w), L.ptr(fail), L.ptr(prod))
+            tmax, mmax = max(tmax, pl.tmax), max(mmax, pl.mmax)
+        batch.nsets = len(chunk)
+        gx, gw = gauss_device(p + 1)
+        batch.gx, batch.gw = L.ptr(gx), L.ptr(gw)
+        L.call("tq_wq_fit_sets", C.byref(batch), tmax, mmax, L.stream())
+    return outs
+
+
+def combine_sets_async(dplans, fine_outs):
+    """w = S^T w~ of every DWQ plan, one launch per TQ_FIT_MAX_SETS plans
+    (tq_dwq_combine_sets); returns the weight tensors."""
+    dev = L.device()
+    ws = []
+    pairs = list(zip(dplans, fine_outs))
+    for c0 in range(0, len(pairs), L.FIT_MAX_SETS):
+        batch = L.CombineBatch()
+        chunk = pairs[c0: c0 + L.FIT_MAX_SETS]
+        for k, (pl, (fwptr, fk0, fw, _)) in enumerate(chunk):
+            w = torch.empty(max(int(pl.wptr_h[-1]), 1), dtype=torch.float64, device=dev)
+            ws.append(w)
+            batch.set[k] = L.CombineSet(L.ptr(pl.rows), int(pl.wanted.size), L.ptr(pl.cp), L.ptr(pl.ri),
+                                        L.ptr(pl.sv), L.Rules(L.ptr(fwptr), L.ptr(fk0), L.ptr(fw)),
+                                        L.Rules(L.ptr(pl.wptr), L.ptr(pl.k0), L.ptr(w)))
+        batch.nsets = len(chunk)
+        L.call("tq_dwq_combine_sets", C.byref(batch), L.stream())
+    return ws
 
 
 def _solve_rows_async(plan: _FitPlan, init=None):
