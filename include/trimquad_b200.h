@@ -112,6 +112,26 @@ int tq_debug_stamp(unsigned long long* stamps, int32_t slot, void* stream);
 int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* first,
                   double* vals, double* ders, int32_t* status, void* stream);
 
+/* several Cox-de Boor evaluations (one degree) in one launch; the batch is
+ * passed by value (kernel parameter, capturable).  Each task as
+ * tq_basis_eval without derivatives or domain status (points in the domain
+ * by construction).  `block_start` / `stage_bytes` are filled in by the call. */
+#define TQ_EVAL_MAX_TASKS 16
+typedef struct {
+    tq_space1d s;
+    const double* u;
+    int64_t n;
+    int32_t* first;
+    double* vals;
+} tq_evaltask;
+typedef struct {
+    tq_evaltask task[TQ_EVAL_MAX_TASKS];
+    int32_t ntasks;
+    int32_t block_start[TQ_EVAL_MAX_TASKS + 1];
+    int32_t stage_bytes;
+} tq_evalbatch;
+int tq_basis_eval_multi(const tq_evalbatch* batch_h, void* stream);
+
 /* exact banded 1-D mass matrix mom[i*(2p+1) + (j-i+p)] with (p+1)-point
  * Gauss per element.  Replaces mass_matrix_1d (src/quadrature.py:160-188). */
 int tq_moments_1d_g(tq_space1d s, const double* gx, const double* gw, int32_t ng,

@@ -77,6 +77,41 @@ class CombineBatch(C.Structure):
     _fields_ = [("set", CombineSet * FIT_MAX_SETS), ("nsets", i32), ("start", i32 * (FIT_MAX_SETS + 1))]
 
 
+EVAL_MAX_TASKS = 16    # TQ_EVAL_MAX_TASKS
+
+
+class EvalTask(C.Structure):
+    _fields_ = [("s", Space1D), ("u", vp), ("n", i64), ("first", vp), ("vals", vp)]
+
+
+class EvalBatch(C.Structure):
+    _fields_ = [("task", EvalTask * EVAL_MAX_TASKS), ("ntasks", i32), ("block_start", i32 * (EVAL_MAX_TASKS + 1)),
+                ("stage_bytes", i32)]
+
+
+def eval_many(jobs):
+    """[(basis, device points)] -> [(first, vals)]: one launch per degree
+    (and per EVAL_MAX_TASKS jobs) of tq_basis_eval_multi."""
+    outs = [None] * len(jobs)
+    by_p = {}
+    for k, (basis, u) in enumerate(jobs):
+        by_p.setdefault(basis.p, []).append(k)
+    for ks in by_p.values():
+        for c0 in range(0, len(ks), EVAL_MAX_TASKS):
+            chunk = ks[c0: c0 + EVAL_MAX_TASKS]
+            batch = EvalBatch()
+            for slot, k in enumerate(chunk):
+                basis, u = jobs[k]
+                n = u.numel()
+                first = torch.empty(n, dtype=torch.int32, device=u.device)
+                vals = torch.empty((n, basis.p + 1), dtype=torch.float64, device=u.device)
+                outs[k] = (first, vals)
+                batch.task[slot] = EvalTask(basis.device(), ptr(u), n, ptr(first), ptr(vals))
+            batch.ntasks = len(chunk)
+            call("tq_basis_eval_multi", C.byref(batch), stream())
+    return outs
+
+
 class Coeff(C.Structure):
     _fields_ = [("kind", i32), ("p", i32), ("n", i32), ("knots", vp), ("X", vp), ("Y", vp)]
 
@@ -142,6 +177,7 @@ def lib():
         "tq_function_classes": ([Space1D, Space1D, vp, vp, vp, vp, vp], i32),
         "tq_wq_fit_sets": ([C.POINTER(FitBatch), i32, i32, vp], i32),
         "tq_dwq_combine_sets": ([C.POINTER(CombineBatch), vp], i32),
+        "tq_basis_eval_multi": ([C.POINTER(EvalBatch), vp], i32),
         "tq_mass_1d_mixed": ([Space1D, Space1D, vp, vp, i32, vp, vp], i32),
         "tq_curve_eval": ([C.POINTER(Curve), i32, vp, i64, vp, vp], i32),
         "tq_curve_intersect_line": ([C.POINTER(Curve), i32, f64, i32, vp, vp, vp, vp], i32),

@@ -238,7 +238,12 @@ def build_all_rules(f):
     g = _geo(f.config)
     if "std_plans" not in g:
         g["std_plans"] = [_FitPlan(b, place_wq_points(b)) for b in (f.b1, f.b2)]
+        # identical directions (same knot vector, hence the same layout and
+        # the same moment systems): one set of fits serves both
+        g["std_same"] = (f.b1.p == f.b2.p and np.array_equal(f.b1.kv.knots, f.b2.kv.knots))
+    same = g["std_same"]
     plans = g["std_plans"]
+    fit_plans = plans[:1] if same else plans
     dplans = {}
     if f.strategy == "dwq":
         for (d, u), rows in dwq_keys(f).items():
@@ -254,12 +259,13 @@ def build_all_rules(f):
     main = torch.cuda.current_stream()
     sep = f.strategy != "reference" and f.coeff.identity       # the direction products are needed
     prods = [torch.empty((pl.basis.n, 2 * pl.basis.p + 1), dtype=torch.float64, device=f.dev)
-             if sep and pl.rows_h.size == pl.basis.n else None for pl in plans]
+             if sep and pl.rows_h.size == pl.basis.n else None for pl in fit_plans]
     dkeys = list(dplans)
     side = _side_streams(1)[0]
     with _forked(main, side):
-        tables = [pl.basis.eval_device(pl.layout.device_points(), check=False) for pl in plans]
-        dtables = [dplans[k].basis.eval_device(dplans[k].aug.device_points(), check=False) for k in dkeys]
+        tabs = L.eval_many([(pl.basis, pl.layout.device_points()) for pl in fit_plans]
+                           + [(dplans[k].basis, dplans[k].aug.device_points()) for k in dkeys])
+        tables, dtables = tabs[: len(fit_plans)], tabs[len(fit_plans):]
         _st("tables")
         _keep_on(main, [t for tb in tables + dtables for t in tb])
     # the fits gate the whole pass: the highest stream priority, so their
@@ -267,16 +273,18 @@ def build_all_rules(f):
     fs = _named_stream("fits", priority=-5)
     with _forked(main, fs):
         _QT[0] = "fit:"
-        outs = fit_sets_async(plans + [dplans[k].fit for k in dkeys], prods + [None] * len(dkeys),
-                              [None] * len(plans) + [False] * len(dkeys))
+        outs = fit_sets_async(fit_plans + [dplans[k].fit for k in dkeys], prods + [None] * len(dkeys),
+                              [None] * len(fit_plans) + [False] * len(dkeys))
         _st("fits")
-        fine = outs[len(plans):]
+        fine = outs[len(fit_plans):]
         ws = combine_sets_async([dplans[k] for k in dkeys], fine)
         _st("combine")
         _QT[0] = ""
         _keep_on(main, [t for o in outs for t in o[1:]] + list(ws) + [p_ for p_ in prods if p_ is not None])
     main.wait_stream(fs)
-    std = outs[: len(plans)]
+    std = outs[: len(fit_plans)]
+    if same:      # direction 2 reads direction 1's fits
+        std, tables, prods = std * 2, tables * 2, prods * 2
     dwq_pending = {}
     for k, key, w, fo, tab in zip(range(len(dkeys)), dkeys, ws, fine, dtables):
         pl = dplans[key]
@@ -412,12 +420,17 @@ def _elem_tables(f):
     per-element 1-D mass blocks and (c != 1) the coefficient on the Gauss
     grid; basis values evaluated per formation as in the reference's _Run."""
     eg, em = [], []
-    for b, (Xd, Wd) in zip((f.b1, f.b2), element_points(f)):
-        _, vals = b.eval_device(Xd, check=False)
+    pts = element_points(f)
+    same = f.b1.p == f.b2.p and np.array_equal(f.b1.kv.knots, f.b2.kv.knots)   # one table serves both
+    dirs = ((f.b1, pts[0]),) if same else tuple(zip((f.b1, f.b2), pts))
+    tabs = L.eval_many([(b, Xd) for b, (Xd, _) in dirs])
+    for b, (Xd, Wd), (_, vals) in zip([d[0] for d in dirs], [d[1] for d in dirs], tabs):
         eg.append((None, Wd, vals, Xd))
         m = torch.empty(b.num_elements * (b.p + 1) ** 2, dtype=torch.float64, device=f.dev)
         L.call("tq_elem_mass", L.ptr(vals), L.ptr(Wd), b.num_elements, b.p + 1, b.p, L.ptr(m), L.stream())
         em.append(m)
+    if same:
+        eg, em = eg * 2, em * 2
     cg = None if f.coeff.identity else f.coeff.grid_device(eg[0][3], eg[1][3])
     return eg, em, cg
 
@@ -452,8 +465,7 @@ def _cut_tables(f):
     dependence on the WQ fits)."""
     b1, b2 = f.b1, f.b2
     t = cut_point_tables(f)
-    f1, v1 = b1.eval_device(t["x"], check=False)
-    f2, v2 = b2.eval_device(t["y"], check=False)
+    (f1, v1), (f2, v2) = L.eval_many([(b1, t["x"]), (b2, t["y"])])
     cw = f.coeff.at_device(t["P"]) * t["W"] if not f.coeff.identity else t["W"]
     Q = (b1.p + 1) * (b2.p + 1)
     f.report.n_cutcell_points = t["npts"]

@@ -3,6 +3,8 @@
 //  tq_basis_eval  <- Basis1D.eval_nonzero_batch   src/splines.py:245-269
 //  tq_moments_1d  <- mass_matrix_1d              src/quadrature.py:160-188
 //  tq_mass_1d_mixed <- mass_matrix_1d(basis, trial_basis)  (same lines)
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace tq {
@@ -56,6 +58,36 @@ __global__ void k_basis_eval(tq_space1d s, const double* __restrict__ u, int64_t
         first[t] = span - P;
 #pragma unroll
         for (int k = 0; k <= P; ++k) vals[t * (P + 1) + k] = N[k];
+    }
+}
+
+// Several evaluations in one launch: the blocks are split among the tasks
+// by their block counts, each block stages its task's knots and runs the
+// k_basis_eval loop on its share of the task's points.
+template <int P>
+__global__ void k_basis_eval_multi(tq_evalbatch B) {
+    extern __shared__ double skn[];
+    int k = 0;
+    while ((int)blockIdx.x >= B.block_start[k + 1]) ++k;
+    const tq_evaltask& T = B.task[k];
+    const tq_space1d& s = T.s;
+    const double* kn = s.knots;
+    const bool staged = (size_t)s.nknots * sizeof(double) <= (size_t)B.stage_bytes;
+    if (staged) {
+        for (int q = threadIdx.x; q < s.nknots; q += blockDim.x) skn[q] = __ldg(s.knots + q);
+        __syncthreads();
+        kn = skn;
+    }
+    const int nb = B.block_start[k + 1] - B.block_start[k];
+    const int b = blockIdx.x - B.block_start[k];
+    for (int64_t t = b * (int64_t)blockDim.x + threadIdx.x; t < T.n; t += (int64_t)nb * blockDim.x) {
+        const double x = T.u[t];
+        const int span = find_span(kn, s.nknots, P, s.n, x);
+        double N[P + 1];
+        basis_funs<P>(kn, span, x, N);
+        T.first[t] = span - P;
+#pragma unroll
+        for (int q = 0; q <= P; ++q) T.vals[t * (P + 1) + q] = N[q];
     }
 }
 
@@ -173,6 +205,32 @@ extern "C" int tq_basis_eval(tq_space1d s, const double* u, int64_t n, int32_t* 
 #undef CASE
     }
     TQ_LAUNCH_CHECK("k_basis_eval");
+    return TQ_OK;
+}
+
+extern "C" int tq_basis_eval_multi(const tq_evalbatch* batch_h, void* stream) {
+    tq_evalbatch B = *batch_h;
+    if (B.ntasks <= 0) return TQ_OK;
+    if (B.ntasks > TQ_EVAL_MAX_TASKS) { set_error("tq_basis_eval_multi: %d tasks", B.ntasks); return TQ_EINVAL; }
+    const int p = B.task[0].s.p;
+    size_t stage = 0;
+    B.block_start[0] = 0;
+    for (int k = 0; k < B.ntasks; ++k) {
+        if (B.task[k].s.p != p) { set_error("tq_basis_eval_multi: tasks of one degree only"); return TQ_EINVAL; }
+        const int64_t nb = std::max<int64_t>(1, std::min<int64_t>((B.task[k].n + 255) / 256, 4 * 148));
+        B.block_start[k + 1] = B.block_start[k] + (int)nb;
+        stage = std::max(stage, (size_t)B.task[k].s.nknots * sizeof(double));
+    }
+    if (p < 0 || p > kMaxP) { set_error("degree %d unsupported", p); return TQ_EINVAL; }
+    if (stage > 32 * 1024) stage = 0;           // large knot vectors: read through L1
+    B.stage_bytes = (int32_t)stage;
+    const int grid = B.block_start[B.ntasks];
+    switch (p) {
+#define CASE(P) case P: k_basis_eval_multi<P><<<grid, 256, stage, S(stream)>>>(B); ::tq::note_launch(); break;
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    }
+    TQ_LAUNCH_CHECK("k_basis_eval_multi");
     return TQ_OK;
 }
 

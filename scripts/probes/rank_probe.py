@@ -12,7 +12,8 @@ flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for world in (1, 2, 4, 8):
     worst = 0.0
-    for rank in ((0, world - 1) if world > 1 else (0,)):
+    per = []
+    for rank in range(world):
         rb, re_ = (K * rank) // world, (K * (rank + 1)) // world
         gf = GraphFormation(b2d, cfg, None, "dwq", row_range=(rb, re_))
         ts = []
@@ -23,5 +24,6 @@ for world in (1, 2, 4, 8):
                 ts.append(e0.elapsed_time(e1))
         ts.sort()
         worst = max(worst, ts[len(ts) // 2])
+        per.append(round(ts[len(ts) // 2], 3))
         del gf
-    print(f"world {world}: per-rank step {worst:.3f} ms  (ideal {0.911 / world:.3f})", flush=True)
+    print(f"world {world}: per-rank step {worst:.3f} ms  ranks {per}", flush=True)
