@@ -310,6 +310,15 @@ int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* 
  * not-deep split that tq_fill_listed uses, so no deep array is formed. */
 int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, int32_t* counts, int32_t* work,
                       void* stream);
+/* count pass 1 from a cache: the arrays of an earlier tq_row_counts_geo on
+ * the same row plan (counts, rowfast, work lists, and `tiles0` = its tile
+ * buffer right after the pass) are reused; this call restores c.tiles from
+ * tiles0, recomputes the line positivity into `pos`, and redoes the pass on
+ * the device (into the same arrays) only when the positivity differs from
+ * `pos_cached` or an earlier redo left them dirty.  `flags`: 3 ints, the
+ * dirty word (flags[1]) zero-initialised once by the caller and kept. */
+int tq_row_counts_cached(tq_rowctx c, const int8_t* geo, int8_t* pos, const int8_t* pos_cached,
+                         int32_t* flags, int32_t* counts, int32_t* work, const int32_t* tiles0, void* stream);
 /* speculative count pass 1 (tq_row_counts_geo with every line's factors
  * assumed positive; needs no factor, so it can run before the fits) and its
  * check: tq_row_counts_verify computes the positivity (pos: n1+n2 bytes,

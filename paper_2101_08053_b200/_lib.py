@@ -150,6 +150,7 @@ def lib():
         "tq_row_counts_geo": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
         "tq_row_counts_spec": ([RowCtx, vp, vp, vp, vp], i32),
+        "tq_row_counts_cached": ([RowCtx, vp, vp, vp, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_verify": ([RowCtx, vp, vp, vp, vp, vp, vp], i32),
         "tq_scan_indptr": ([vp, i32, vp, C.POINTER(i64), vp], i32),
         "tq_scan_workspace_bytes": ([i32], i64),

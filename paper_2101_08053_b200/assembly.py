@@ -417,8 +417,19 @@ class Formation:
         spec = getattr(self, "_spec", None)
         if spec is not None and (spec["rows"] != (row_begin, row_end) or self.a1 is None):
             raise RuntimeError("speculative count pass launched for another row range")
+        # count pass 1 depends on the row plan's geometry and, through the
+        # factor positivity, on values only in a corner case: its arrays are
+        # cached per configuration like the reference's sparsity pattern
+        # (_pattern_for, src/assembly.py:186-195) and a captured pass checks
+        # the positivity against them on the device (tq_row_counts_cached)
+        from ._rawrows import _geo
+        ckey = ("counts1", row_begin, row_end, id(self.deep)) if self.a1 is not None else None
+        cached = _geo(self.config).get(ckey) if (ckey is not None and spec is None) else None
         if spec is not None:       # count pass 1 ran at pass start (prelaunch_counts)
             self.rowfast, counts, work, tiles = spec["rowfast"], spec["counts"], spec["work"], spec["tiles"]
+        elif cached is not None and self.capture is not None:
+            self.rowfast, counts, work = cached["rowfast"], cached["counts"], cached["work"]
+            tiles = torch.empty(L.tile_ints(nrows), dtype=torch.int32, device=self.dev)
         else:
             self.rowfast = torch.empty(max(nrows, 1), dtype=torch.int8, device=self.dev)   # written for every row
             counts = torch.empty(max(nrows, 1), dtype=torch.int32, device=self.dev)
@@ -437,10 +448,20 @@ class Formation:
                 pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
                 L.call("tq_row_counts_verify", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(spec["bad"]),
                        L.ptr(counts), L.ptr(work), L.stream())
+            elif cached is not None and self.capture is not None:
+                pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
+                L.call("tq_row_counts_cached", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(cached["pos"]),
+                       L.ptr(cached["flags"]), L.ptr(counts), L.ptr(work), L.ptr(cached["tiles0"]), L.stream())
             elif self.a1 is not None:
                 pos = torch.empty(self.b1.n + self.b2.n, dtype=torch.int8, device=self.dev)
                 L.call("tq_row_counts_geo", ctx, L.ptr(self.deep), L.ptr(pos), L.ptr(counts), L.ptr(work),
                        L.stream())
+                if ckey is not None and cached is None and self.capture is None:
+                    # snapshot right after pass 1 (pass 2 adds to the tile sums)
+                    _geo(self.config)[ckey] = dict(
+                        rowfast=self.rowfast.clone(), counts=counts.clone(), work=work.clone(),
+                        tiles0=tiles.clone(), pos=pos.clone(),
+                        flags=torch.zeros(3, dtype=torch.int32, device=self.dev))
             else:
                 L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_deep")

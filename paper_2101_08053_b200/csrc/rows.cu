@@ -662,6 +662,44 @@ __global__ void k_pos2(tq_rowctx c, int8_t* __restrict__ pos, int* __restrict__ 
     if (bad && !ok) atomicAdd(bad, 1);
 }
 
+// the cached count pass: the line positivity of this pass against the one
+// the cached pass was made with; flags[0] = changed, flags[1] = dirty (the
+// cache arrays hold a redo's results), flags[2] = redo guard
+__global__ void k_pos2_cmp(tq_rowctx c, int8_t* __restrict__ pos, const int8_t* __restrict__ pos_cached,
+                           int* __restrict__ flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = true;
+    if (t < c.n1) {
+        for (int j = c.ov_lo1[t]; j <= c.ov_hi1[t]; ++j)
+            ok = ok && c.a1[(int64_t)t * (2 * c.p1 + 1) + (j - t + c.p1)] > 0.0 &&
+                 c.a1[(int64_t)j * (2 * c.p1 + 1) + (t - j + c.p1)] > 0.0;
+    } else if (t < c.n1 + c.n2) {
+        const int i = t - c.n1;
+        for (int j = c.ov_lo2[i]; j <= c.ov_hi2[i]; ++j)
+            ok = ok && c.a2[(int64_t)i * (2 * c.p2 + 1) + (j - i + c.p2)] > 0.0 &&
+                 c.a2[(int64_t)j * (2 * c.p2 + 1) + (i - j + c.p2)] > 0.0;
+    }
+    if (t < c.n1 + c.n2) {
+        pos[t] = ok;
+        if ((int8_t)ok != pos_cached[t]) atomicOr(flags, 1);
+    }
+}
+
+__global__ void k_counts_cached_guard(int* __restrict__ flags, int32_t* __restrict__ work,
+                                      int32_t* __restrict__ ctl) {
+    const int redo = flags[0] | flags[1];
+    flags[2] = redo;
+    flags[1] = flags[0];        // after a redo the arrays hold this pass's results
+    if (redo) {
+        work[0] = 0;
+        work[1] = 0;
+        if (ctl) {
+            ctl[0] = 0;
+            ctl[1] = 0;
+        }
+    }
+}
+
 // before the redo of a speculative pass (only when some line is not
 // positive): the list counters and the first/last list-A words start over
 __global__ void k_counts_reset_if_bad(const int* __restrict__ bad, int32_t* __restrict__ work,
@@ -781,6 +819,24 @@ extern "C" int tq_row_counts_verify(tq_rowctx c, const int8_t* geo, int8_t* pos,
                                                                           work + 2 + nrows, work + 1, bad);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_verify");
+    return TQ_OK;
+}
+
+extern "C" int tq_row_counts_cached(tq_rowctx c, const int8_t* geo, int8_t* pos, const int8_t* pos_cached,
+                                    int32_t* flags, int32_t* counts, int32_t* work, const int32_t* tiles0,
+                                    void* stream) {
+    int nrows = c.row_end - c.row_begin;
+    if (nrows <= 0) return TQ_OK;
+    if (!c.a1 || !c.a2 || !c.tiles) { set_error("tq_row_counts_cached needs the separable factors and tiles"); return TQ_EINVAL; }
+    cudaStream_t st = S(stream);
+    TQ_CUDA(cudaMemcpyAsync(c.tiles, tiles0, sizeof(int32_t) * (size_t)TQ_TILE_INTS(nrows), cudaMemcpyDeviceToDevice, st));
+    TQ_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    k_pos2_cmp<<<grid_for(c.n1 + c.n2, 128), 128, 0, st>>>(c, pos, pos_cached, flags); ::tq::note_launch();
+    k_counts_cached_guard<<<1, 1, 0, st>>>(flags, work, c.tiles + TQ_TILE_CTL(nrows)); ::tq::note_launch();
+    k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, st>>>(c, geo, pos, counts, work + 2, work,
+                                                                   work + 2 + nrows, work + 1, flags + 2);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("tq_row_counts_cached");
     return TQ_OK;
 }
 
