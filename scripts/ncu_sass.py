@@ -5,7 +5,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kfilt = ["-k", sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 k = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
