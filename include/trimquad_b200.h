@@ -487,7 +487,11 @@ int tq_cutcell_device_pack(const tq_curve* curves_h, int32_t ncurves, const doub
 /* target f(x, y): kind 0 = values on the Gauss tensor grid (grid[r1*ld + r2]);
  * kind 1 = sum_k terms[7k] * phi(terms[7k+1], terms[7k+2] x + terms[7k+3])
  *                        * phi(terms[7k+4], terms[7k+5] y + terms[7k+6]),
- * phi kinds 0 = 1, 1 = sin, 2 = cos, 3 = exp (evaluated in-kernel) */
+ * phi kinds 0 = 1, 1 = sin, 2 = cos, 3 = exp (evaluated in-kernel);
+ * kind 2 = kind 1 with its factors tabulated per Gauss coordinate
+ * (tq_target_tables): grid[k*(ld + n2) + r1] = phi_k(x_r1), grid[k*(ld + n2)
+ * + ld + r2] = psi_k(y_r2), ld = nel1*g1n -- the same values, evaluated once
+ * per coordinate instead of once per tensor point */
 typedef struct {
     int32_t kind, nterms;
     const double* terms;
@@ -518,6 +522,19 @@ typedef struct {
 /* b over active rows [row_begin, row_end) (T: scratch (nel1*g1n) x n2). */
 int tq_rhs(tq_projctx c, double* T, const int32_t* cut_rows, int32_t ncut, double* b, void* stream);
 int tq_target_points(tq_target f, const double* P, const double* w, int64_t n, double* out, void* stream);
+/* the RHS for a kind-2 (tabulated separable) target with c == 1: per
+ * direction the element integrals Q_k[e][a] of each factor, their support
+ * sums A_k[i], then b_i = sum_k A1_k[i1] A2_k[i2] for all-interior supports
+ * and the interior-masked element double sum otherwise, plus the cut-cell
+ * points (replaces tq_rhs's two tensor stages for this case).
+ * `work`: tq_rhs_separable_work(c) doubles. */
+int tq_rhs_separable(tq_projctx c, const int8_t* func_class, double* work, const int32_t* cut_rows,
+                     int32_t ncut, double* b, void* stream);
+int64_t tq_rhs_separable_work(tq_projctx c);
+/* the kind-2 tables of a kind-1 target at the Gauss coordinates x1 (n1) and
+ * x2 (n2): out[k*(n1+n2) + i] (see tq_target) */
+int tq_target_tables(tq_target f, const double* x1, int64_t n1, const double* x2, int64_t n2, double* out,
+                     void* stream);
 /* (num, den) of the relative L2 error over interior elements [e_begin, e_end)
  * (row-major ids) and cut points [p_begin, p_end); C is the n1 x n2
  * coefficient grid (zeros off the active set). */

@@ -81,6 +81,9 @@ class TargetStruct(C.Structure):
 def _bind():
     L.optional("tq_rhs", [ProjCtx, L.vp, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_target_points", [TargetStruct, L.vp, L.vp, L.i64, L.vp, L.vp])
+    L.optional("tq_target_tables", [TargetStruct, L.vp, L.i64, L.vp, L.i64, L.vp, L.vp])
+    L.optional("tq_rhs_separable", [ProjCtx, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp])
+    L.optional("tq_rhs_separable_work", [ProjCtx], L.i64)
     L.optional("tq_l2_parts", [ProjCtx, L.vp, L.i64, L.i64, L.i64, L.i64, L.vp, L.vp, L.vp])
 
 
@@ -115,11 +118,21 @@ class _Tables:
 
 
 def _target_desc(target, tabs, keep):
-    """(kind, nterms, terms, grid, ld) for the kernels."""
+    """(kind, nterms, terms, grid, ld) for the kernels.  A separable target
+    is tabulated per Gauss coordinate on the device (kind 2,
+    tq_target_tables): the same factor values as the in-kernel evaluation,
+    once per coordinate instead of once per tensor point."""
     if isinstance(target, SeparableTarget):
         t = L.dev(target.terms.ravel(), torch.float64)
         keep.append(t)
-        return 1, target.terms.shape[0], L.ptr(t), L.vp(0), 0
+        nt = target.terms.shape[0]
+        x1, x2 = tabs.dirs[0][1], tabs.dirs[1][1]
+        n1, n2 = x1.numel(), x2.numel()
+        tab = torch.empty(max(nt * (n1 + n2), 1), dtype=torch.float64, device=x1.device)
+        keep.append(tab)
+        L.call("tq_target_tables", TargetStruct(1, nt, L.ptr(t), L.vp(0), 0), L.ptr(x1), n1, L.ptr(x2), n2,
+               L.ptr(tab), L.stream())
+        return 2, nt, L.ptr(t), L.ptr(tab), n1
     X1, X2 = tabs.dirs[0][0].ravel(), tabs.dirs[1][0].ravel()
     P = np.column_stack([np.repeat(X1, X2.size), np.tile(X2, X1.size)])
     g = L.dev(np.asarray(target(P), float), torch.float64)
@@ -193,9 +206,16 @@ def assemble_rhs_device(problem: ProjectionProblem, row_range=None):
         is_cut = config.func_class_dev.view(-1)[act.long()] == CUT
         cut_rows = (torch.nonzero(is_cut).view(-1).to(torch.int32) + rb).contiguous()
     b1, b2 = basis2d.dir
-    T = torch.empty((b1.num_elements * tabs.dirs[0][4], b2.n), dtype=torch.float64, device=L.device())
     b = torch.empty(max(re_ - rb, 1), dtype=torch.float64, device=L.device())
     ctx = _ctx(basis2d, config, tabs, tdesc, idx["active"], rb, re_, cgrid, cut, fcw)
+    if tdesc[0] == 2 and cgrid is None:
+        # separable target, c == 1: per-element 1-D integrals (tq_rhs_separable)
+        nw = L.lib().tq_rhs_separable_work(ctx)
+        work = torch.empty(max(int(nw), 1), dtype=torch.float64, device=L.device())
+        L.call("tq_rhs_separable", ctx, L.ptr(config.func_class_dev), L.ptr(work), L.ptr(cut_rows),
+               cut_rows.numel(), L.ptr(b), L.stream())
+        return b[: re_ - rb]
+    T = torch.empty((b1.num_elements * tabs.dirs[0][4], b2.n), dtype=torch.float64, device=L.device())
     L.call("tq_rhs", ctx, L.ptr(T), L.ptr(cut_rows), cut_rows.numel(), L.ptr(b), L.stream())
     return b[: re_ - rb]
 
