@@ -307,6 +307,91 @@ def torch_index(sel, device):
     return torch.from_numpy(sel.astype(np.int64)).to(device)
 
 
+def rhs_secondary(b2d, cfg, steps=20, cpu_nel=256, seed=0):
+    """The L2-projection legs of config 5 (src/projection.py:101-145, 221-260):
+    assemble_rhs of f = sin(2 pi x) cos(3 pi y) and l2_error of a seeded
+    coefficient vector, kernels only on resident inputs (ResidentProjection,
+    one CUDA graph of both, replayed with L2 flushed between steps), plus the
+    oracle port on a bounded sample (cpu_nel^2) for the CPU figure."""
+    import torch
+    from paper_2101_08053_b200 import cases as C, projection as PR
+    prob = PR.ProjectionProblem(C.f_config5, b2d, cfg, strategy="dwq")
+    rp = PR.ResidentProjection(prob)
+    x = torch.from_numpy(np.random.default_rng(5).standard_normal(rp.K)).to("cuda")
+    flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")
+    s_rhs = torch.cuda.Stream()
+    s_rhs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_rhs):       # warm the launch paths, then capture both legs
+        for _ in range(2):
+            rp.rhs(); rp.l2_parts(x)
+    torch.cuda.current_stream().wait_stream(s_rhs)
+    torch.cuda.synchronize()
+    graphs = {}
+    for name, fn in (("rhs", rp.rhs), ("l2", lambda: rp.l2_parts(x))):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        graphs[name] = g
+    torch.cuda.synchronize()
+    res = {}
+    for name, g in graphs.items():
+        ts = []
+        for _ in range(steps):
+            flush.fill_(1.0)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); g.replay(); b_.record(); torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b_))
+        res[name] = float(np.median(ts))
+    nd = rp.nd.cpu().numpy()
+    e = float(np.sqrt(nd[0] / nd[1]))
+    # algorithmic figures: RHS points = (p+2)^2 Gauss points per interior
+    # element + cut-cell points; L2: (p+3)^2 points, F_alg = 2 * per-element
+    # FMA of the sum-factorised u_h ((p+3)(p+1)^2 + (p+3)^2 (p+1)) + 3 per point
+    p = b2d.dir[0].p
+    n_int = int((cfg.element_class_dev == 0).sum().item())
+    ncut = rp.cut.n if rp.cut is not None else 0
+    rhs_pts = n_int * (p + 2) ** 2 + ncut
+    l2_pts = n_int * (p + 3) ** 2 + ncut
+    G, Q = p + 3, p + 1
+    F_l2 = 2.0 * n_int * (G * Q * Q + G * G * Q + 3 * G * G)
+    try:
+        pf = float(json.load(open(os.path.join(HERE, "profiles", "fp64_peaks.json")))["dfma_tflops"])
+    except Exception:
+        pf = 33.6
+    l2_tf = F_l2 / (res["l2"] / 1e3) / 1e12
+    out = {"workload": "config5 L2 projection legs: assemble_rhs(f = sin(2 pi x) cos(3 pi y)) and "
+                       "l2_error(seeded coefficients), 2048^2, p=4",
+           "rhs_ms": res["rhs"], "l2_error_ms": res["l2"], "l2_error_value": e,
+           "rhs_points_per_s": rhs_pts / (res["rhs"] / 1e3), "l2_points_per_s": l2_pts / (res["l2"] / 1e3),
+           "rhs_rows_per_s": rp.K / (res["rhs"] / 1e3),
+           "rhs_bound": "latency (five small kernels: separable target tabulated per Gauss coordinate, 1-D element "
+                        "integrals, interior rows as products of 1-D sums, cut rows masked + cut-cell points)",
+           "l2_roofline": {"bound": "fp64", "achieved": l2_tf, "peak": pf, "unit": "TFLOP/s", "frac": l2_tf / pf,
+                           "F_alg": F_l2, "peak_source": "profiles/fp64_peaks.json (DFMA loop)"},
+           "step": "CUDA graph of the kernels on resident inputs, L2 flushed between steps, median of "
+                   f"{steps}"}
+    try:                   # the reference algorithm (oracle port) on a bounded sample
+        from threadpoolctl import threadpool_limits
+        from oracle import configs as OC, project as OP
+        with threadpool_limits(limits=cpu_threads()):
+            oc = OC.config(5, seed=seed, nel=cpu_nel, p=p)
+            ocfg = OC.build_space(oc["curves"], cpu_nel, p)
+            ocfg.cut_cell_rule(p)
+            t0 = time.perf_counter()
+            rb = OP.assemble_rhs(oc["target"], ocfg)
+            t1 = time.perf_counter()
+            xs = np.random.default_rng(5).standard_normal(rb.size)
+            OP.l2_error(xs, oc["target"], ocfg)
+            t2 = time.perf_counter()
+        out["cpu_baseline"] = {"rhs_rows_per_s": rb.size / (t1 - t0), "l2_elements_per_s": cpu_nel ** 2 / (t2 - t1),
+                               "cores": cpu_threads(), "kind": "port",
+                               "sample": f"oracle/project.py assemble_rhs + l2_error on {cpu_nel}x{cpu_nel} elements "
+                                         f"of the config-5 recipe ({rb.size} rows), one run each"}
+    except Exception as exc:
+        out["cpu_baseline"] = {"failed": str(exc)}
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -509,6 +594,10 @@ def run_ours(args, rank, world, local_rank):
     secondary = None
     if world == 1 and not args.no_config4 and not args.profile_eager:
         secondary = {}
+        try:
+            secondary["rhs_l2_config5"] = rhs_secondary(b2d, cfg)
+        except Exception as exc:
+            secondary["rhs_l2_config5"] = {"failed": str(exc)}
         for p4 in (6, 8):
             try:
                 secondary[f"config4_p{p4}"] = config4_secondary(p4)

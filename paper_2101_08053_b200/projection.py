@@ -446,3 +446,72 @@ def run_convergence_study(case, strategies, degrees, meshes, target=None, parall
                 out.append(ConvergenceRecord(case.name, strategy, p, nel, 1.0 / nel, int(M.shape[0]), err, rate))
     return out
 
+
+
+class ResidentProjection:
+    """The RHS and L2-error kernels of one problem on device-resident inputs:
+    the Gauss tables, target tables, cut-cell points and launch contexts are
+    built once (``assemble_rhs_device`` / ``l2_error_parts_device`` rebuild
+    them per call); ``rhs()`` and ``l2_parts(C)`` then launch only the
+    kernels -- what a repeated solve loop or a benchmark replays."""
+
+    def __init__(self, problem: ProjectionProblem, row_range=None):
+        from . import _adapt
+        _bind()
+        problem = _adapt.problem(problem)
+        self.problem = problem
+        basis2d, config = problem.basis2d, problem.config
+        coeff = problem.field()
+        idx, _ = config.active_index()
+        self.K = K = idx["K"]
+        self.rb, self.re = (0, K) if row_range is None else row_range
+        self.keep = []
+        self.tabs_r = _Tables(basis2d, 2)
+        self.tdesc_r = _target_desc(problem.target, self.tabs_r, self.keep)
+        self.cgrid = None if coeff.identity else coeff.grid_device(self.tabs_r.dirs[0][1], self.tabs_r.dirs[1][1])
+        self.cut = cut = _CutPoints(config, basis2d) if config.has_cuts() else None
+        fcw = None
+        self.cut_rows = torch.empty(0, dtype=torch.int32, device=L.device())
+        if cut is not None:
+            fcw = _target_points(problem.target, cut.P, self.keep) * cut.W
+            if not coeff.identity:
+                fcw = fcw * coeff.at_device(cut.P)
+            act = idx["active"][self.rb:self.re]
+            is_cut = config.func_class_dev.view(-1)[act.long()] == CUT
+            self.cut_rows = (torch.nonzero(is_cut).view(-1).to(torch.int32) + self.rb).contiguous()
+        self.fcw = fcw
+        self.ctx_r = _ctx(basis2d, config, self.tabs_r, self.tdesc_r, idx["active"], self.rb, self.re, self.cgrid,
+                          cut, fcw)
+        self.sep = self.tdesc_r[0] == 2 and self.cgrid is None
+        b1, b2 = basis2d.dir
+        if self.sep:
+            nw = L.lib().tq_rhs_separable_work(self.ctx_r)
+            self.work = torch.empty(max(int(nw), 1), dtype=torch.float64, device=L.device())
+        else:
+            self.work = torch.empty((b1.num_elements * self.tabs_r.dirs[0][4], b2.n), dtype=torch.float64,
+                                    device=L.device())
+        self.b = torch.empty(max(self.re - self.rb, 1), dtype=torch.float64, device=L.device())
+        # error tables (p + 3 points)
+        self.tabs_e = _Tables(basis2d, 3)
+        self.tdesc_e = _target_desc(problem.target, self.tabs_e, self.keep)
+        self.fpts = _target_points(problem.target, cut.P, self.keep) if cut is not None else None
+        self.ctx_e = _ctx(basis2d, config, self.tabs_e, self.tdesc_e, idx["active"], 0, K, None, cut, None)
+        self.Cg = torch.zeros(b1.n * b2.n, dtype=torch.float64, device=L.device())
+        self.active_l = idx["active"][:K].long()
+        self.nd = torch.zeros(2, dtype=torch.float64, device=L.device())
+        self.ne = b1.num_elements * b2.num_elements
+
+    def rhs(self):
+        if self.sep:
+            L.call("tq_rhs_separable", self.ctx_r, L.ptr(self.problem.config.func_class_dev), L.ptr(self.work),
+                   L.ptr(self.cut_rows), self.cut_rows.numel(), L.ptr(self.b), L.stream())
+        else:
+            L.call("tq_rhs", self.ctx_r, L.ptr(self.work), L.ptr(self.cut_rows), self.cut_rows.numel(),
+                   L.ptr(self.b), L.stream())
+        return self.b[: self.re - self.rb]
+
+    def l2_parts(self, coeffs_dev):
+        self.Cg[self.active_l] = coeffs_dev
+        L.call("tq_l2_parts", self.ctx_e, L.ptr(self.Cg), 0, self.ne, 0, self.cut.n if self.cut else 0,
+               L.ptr(self.fpts), L.ptr(self.nd), L.stream())
+        return self.nd
