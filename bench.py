@@ -66,7 +66,8 @@ def config_dict(args, world):
                         f"c=1, {args.strategy}, seed {args.seed}",
             "nel": args.nel, "p": args.p, "strategy": args.strategy, "seed": args.seed,
             "parallelism": f"row-block x{world}", "l2": "flushed between steps (256 MiB write)",
-            "row_sharding": "contiguous active-row blocks, no collective during formation"}
+            "row_sharding": "contiguous active-row blocks balanced by window size (nnz proxy), no collective "
+                            "during formation"}
 
 
 def sample_config(args, world, nnz):
@@ -415,7 +416,8 @@ def run_ours(args, rank, world, local_rank):
     cfg.cut_cell_rule(args.p)
     idx, _ = cfg.active_index()
     K = idx["K"]
-    rb, re_ = (K * rank) // world, (K * (rank + 1)) // world
+    from paper_2101_08053_b200.distributed import row_block, window_counts
+    rb, re_ = row_block(K, world, rank, window_counts(cfg) if world > 1 else None)   # nnz-balanced blocks
     flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device=dev)
 
     # the timed step: one full formation pass captured as a CUDA graph

@@ -14,7 +14,8 @@ for world in (1, 2, 4, 8):
     worst = 0.0
     per = []
     for rank in range(world):
-        rb, re_ = (K * rank) // world, (K * (rank + 1)) // world
+        from paper_2101_08053_b200.distributed import row_block, window_counts
+        rb, re_ = row_block(K, world, rank, window_counts(cfg) if world > 1 else None)
         gf = GraphFormation(b2d, cfg, None, "dwq", row_range=(rb, re_))
         ts = []
         for k in range(13):

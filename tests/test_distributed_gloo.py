@@ -83,3 +83,52 @@ def test_gather_and_allreduce_world2_gloo():
     assert np.array_equal(dat, M.data)
     assert np.allclose(parts, [M.data.sum(), M.shape[0]], rtol=1e-15)
     assert np.array_equal(parts, other[1])
+
+
+def _halo_worker(rank, world, port, outq):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import scipy.sparse as sp
+        from paper_2101_08053_b200.distributed import BlockSystem, row_block
+        n, bw = 40, 3
+        A = sp.diags([np.full(n - abs(k), 1.0 + k) for k in range(-bw, bw + 1)], list(range(-bw, bw + 1)),
+                     format="csr")
+        rb, re_ = row_block(n, world, rank)
+        a, b = A.indptr[rb], A.indptr[re_]
+        S = BlockSystem(torch.from_numpy((A.indptr[rb:re_ + 1] - a).astype(np.int32)),
+                        torch.from_numpy(A.indices[a:b].astype(np.int32)), torch.from_numpy(A.data[a:b].copy()),
+                        rb, re_, n)
+        full = torch.zeros(n, dtype=torch.float64)
+        full[rb:re_] = torch.arange(rb, re_, dtype=torch.float64) + 100.0
+        S.exchange(full)
+        outq.put((rank, rb, re_, full.numpy(), S.sends, S.recvs, S.diag.numpy(),
+                  S.dot(torch.ones(re_ - rb, dtype=torch.float64), torch.ones(re_ - rb, dtype=torch.float64))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_halo_plan_and_exchange_world2_gloo():
+    """BlockSystem (the distributed CG's row block): each rank receives
+    exactly the off-block columns its rows read, from their owner; the block
+    diagonal; the all-reduced dot."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, a0, b0, f0, s0, v0, d0, dot0), (r1, a1, b1, f1, s1, v1, d1, dot1) = res
+    assert (a0, b1) == (0, 40) and b0 == a1
+    assert v0 == [(1, b0, b0 + 3)] and v1 == [(0, a1 - 3, a1)]       # halos of width = bandwidth
+    assert s0 == [(1, b0 - 3, b0)] and s1 == [(0, a1, a1 + 3)]
+    assert np.array_equal(f0[b0:b0 + 3], np.arange(b0, b0 + 3) + 100.0)
+    assert np.array_equal(f1[a1 - 3:a1], np.arange(a1 - 3, a1) + 100.0)
+    assert np.all(d0 == 1.0) and np.all(d1 == 1.0)
+    assert dot0 == dot1 == 40.0
