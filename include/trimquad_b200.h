@@ -268,6 +268,9 @@ typedef struct {
     const int32_t* counts;
     int32_t* tiles;              /* TQ_TILE_INTS(nrows) ints: the sums, then
                                     the bases (tq_tile_bases) */
+    int64_t raw_ld;              /* 0: raw blocks row-major (slot * W + o);
+                                    > 0: planes, entry o of slot s at
+                                    raw[o * raw_ld + s] (tq_planes_csr) */
 } tq_rowctx;
 
 /* tile-mode buffer layout (ints): the tile sums (padded to a multiple of 4
@@ -408,7 +411,13 @@ typedef struct {
     const int32_t* desc;             /* nraw x 8: fidx, mode, set1, set2, a1, b1, a2, b2 */
     int32_t nraw;
     int32_t nmax1, nmax2;            /* max points of one rule row per direction */
-    double* raw;                     /* nraw x (2p1+1)(2p2+1) */
+    double* raw;                     /* nraw x (2p1+1)(2p2+1), or planes (raw_ld) */
+    /* planes layout (raw_ld > 0): entry q of descriptor row r is stored at
+       raw[q * raw_ld + store[r]]; the storage index of a row is its active
+       index minus the block's first one, so the planes of consecutive rows
+       are contiguous (coalesced symmetrisation, tq_planes_csr) */
+    const int32_t* store;
+    int64_t raw_ld;
 } tq_rawctx;
 
 /* regular-support part of raw rows [r0, r1) (overwrites their blocks).
@@ -432,6 +441,32 @@ int tq_cut_blocks(tq_rawctx c, void* stream);
 int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int32_t ng, int32_t p, double* em,
                  void* stream);
 int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+
+/* ---- the all-raw path in the planes layout (c.raw_ld > 0) --------------- */
+
+/* interior rows of the c != 1 BOX plan (box = whole support, standard rules)
+ * by strips of up to 16 rows (i1, i20 + t): strips = nstrips x 18 ints
+ * (i1, i20, storage index of row t or -1); nu_max bounds the union of a
+ * strip's direction-2 point windows (shared-memory sizing); bw: scratch of
+ * tq_bw_table_doubles(c) doubles (rebuilt each call); a strip that
+ * breaks a bound sets *status |= 1 and writes zero blocks.  Replaces
+ * sum_factor_row over _interior_rows_batched (src/assembly.py:218-252,
+ * 409-449); writes the rows' planes. */
+int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips, int32_t nu_max, double* bw,
+                 int32_t* status, void* stream);
+/* scratch of tq_sf_strips: the weighted collocation tables of the standard
+ * rules (n_d x nmax_d x the padded window, both directions), in doubles;
+ * *status |= 2 when a rule row is longer than the context's nmax */
+int64_t tq_bw_table_doubles(tq_rawctx c);
+/* symmetrise / zero-drop / CSR of rows [row_begin, row_end) in one pass
+ * (_Run.finish, src/assembly.py:400-404) from the planes (c.raw, c.raw_ld;
+ * storage index = active row - raw_base): indptr nrows + 1, indices/data
+ * `cap` entries, state tq_planes_state_bytes(nrows) bytes of scratch, ctl 3
+ * ints ([1] nnz, [2] flags: 1 = nnz != expect (expect >= 0), 2 = nnz > cap).
+ * nnz_h (optional) reads nnz back, synchronising the stream. */
+int64_t tq_planes_state_bytes(int32_t nrows);
+int tq_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
+                  int64_t cap, void* state, int32_t* ctl, int64_t expect, int64_t* nnz_h, void* stream);
 
 /* coefficient c = det J of a B-spline geometry map on a tensor grid / at
  * points (the reference takes a host callable, src/assembly.py:54-85) */

@@ -120,7 +120,8 @@ class RowCtx(C.Structure):
     _fields_ = [("n1", i32), ("n2", i32), ("p1", i32), ("p2", i32),
                 ("ov_lo1", vp), ("ov_hi1", vp), ("ov_lo2", vp), ("ov_hi2", vp),
                 ("col_of", vp), ("active", vp), ("slot", vp), ("a1", vp), ("a2", vp), ("raw", vp),
-                ("deep", vp), ("rowfast", vp), ("row_begin", i32), ("row_end", i32), ("counts", vp), ("tiles", vp)]
+                ("deep", vp), ("rowfast", vp), ("row_begin", i32), ("row_end", i32), ("counts", vp), ("tiles", vp),
+                ("raw_ld", i64)]
 
 
 _lib = None

@@ -40,7 +40,8 @@ class RawCtx(C.Structure):
                 + [(k, L.vp) for k in ("grids", "cutidx", "cut_ptr", "cut_cw", "cfirst1", "cvals1", "cfirst2",
                                        "cvals2", "grp_ptr", "grp_key", "grp_pts", "grp_perm", "grp_blocks")]
                 + [("ngroups", L.i32), ("desc", L.vp)]
-                + [("nraw", L.i32), ("nmax1", L.i32), ("nmax2", L.i32), ("raw", L.vp)])
+                + [("nraw", L.i32), ("nmax1", L.i32), ("nmax2", L.i32), ("raw", L.vp), ("store", L.vp),
+                   ("raw_ld", L.i64)])
 
 
 def _bind():
@@ -53,6 +54,10 @@ def _bind():
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
+    L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_bw_table_doubles", [RawCtx], L.i64)
+    L.optional("tq_planes_csr", [L.RowCtx, L.i32, L.vp, L.vp, L.vp, L.i64, L.vp, L.vp, L.i64, L.vp, L.vp])
+    L.optional("tq_planes_state_bytes", [L.i32], L.i64)
 
 
 def _geo(config):
@@ -334,6 +339,99 @@ def needs_raw(f):
     return cut_rows_host(f).size > 0
 
 
+# the all-raw path (every active row raw: c != 1 or the `reference`
+# strategy) keeps its raw blocks in the planes layout and forms the CSR in
+# one pass (csrc/planes.cu); TQ_PLANES=0 selects the row-major blocks and the
+# two count passes (A/B and the parity tests)
+PLANES = os.environ.get("TQ_PLANES", "1") != "0"
+STRIP_ROWS = 16
+
+
+def planes(f):
+    """Does this formation use the planes layout?"""
+    return (PLANES and (f.strategy == "reference" or not f.coeff.identity) and f.b1.p == f.b2.p
+            and 1 <= f.b1.p <= 10)
+
+
+def planes_geo(f):
+    """Storage map of the planes layout for this formation's row plan
+    (geometry, cached): storage index of a row = its active index minus the
+    plan's first one (the plan holds every active row of its lines), the
+    per-function slot map with those indices, and the strips of the interior
+    (whole-support box) rows for tq_sf_strips."""
+    desc, nint = _plan(f)
+    g = _geo(f.config)
+    key = ("planes", id(desc))
+    if key not in g:
+        col_of = _col_of_host(f)
+        fid = desc[:, 0].astype(np.int64)
+        col = col_of[fid].astype(np.int64)
+        base = int(col.min()) if col.size else 0
+        store = col - base
+        if col.size and not (store.max() == col.size - 1 and np.unique(store).size == col.size):
+            raise RuntimeError("planes layout needs every active row of the plan's lines in the plan")
+        slot = torch.full((f.b1.n * f.b2.n,), -1, dtype=torch.int32, device=f.dev)
+        if fid.size:
+            slot[torch.as_tensor(fid, device=f.dev)] = torch.as_tensor(store.astype(np.int32), device=f.dev)
+        # strips: interior rows [0, nint) grouped by (i1, i2 // STRIP_ROWS)
+        n2 = f.b2.n
+        i1, i2 = fid[:nint] // n2, fid[:nint] % n2
+        full = ((desc[:nint, 1] == MODE_BOX) & (desc[:nint, 2] == 0) & (desc[:nint, 3] == 0)
+                & (desc[:nint, 4] == f.b1._el_first[i1]) & (desc[:nint, 5] == f.b1._el_last[i1])
+                & (desc[:nint, 6] == f.b2._el_first[i2]) & (desc[:nint, 7] == f.b2._el_last[i2]))
+        strips = np.empty((0, 2 + STRIP_ROWS), np.int32)
+        if nint and full.all():
+            skey = i1 * ((n2 + STRIP_ROWS - 1) // STRIP_ROWS) + i2 // STRIP_ROWS
+            uk, inv = np.unique(skey, return_inverse=True)
+            strips = np.full((uk.size, 2 + STRIP_ROWS), -1, np.int32)
+            strips[inv, 0] = i1
+            strips[inv, 1] = (i2 // STRIP_ROWS) * STRIP_ROWS
+            strips[inv, 2 + i2 % STRIP_ROWS] = store[:nint]
+        g[key] = dict(base=base, store=L.dev(store.astype(np.int32), torch.int32), slot=slot,
+                      strips_h=strips, strips=L.dev(strips if strips.size else np.zeros(1, np.int32), torch.int32),
+                      nstrips=int(strips.shape[0]), strip_ok=bool(nint == 0 or full.all()), ld=int(col.size))
+    return g[key]
+
+
+def strip_nu_max(f, pg, layout2):
+    """Bound of a strip's union of direction-2 point windows: the layout
+    points of the elements its rows' supports cover (a WQ rule row lies in
+    its support's points); cached per (plan, layout)."""
+    g = _geo(f.config)
+    key = ("nu_max", id(pg), id(layout2))
+    if key not in g:
+        st = pg["strips_h"]
+        if st.shape[0] == 0:
+            g[key] = 1
+        else:
+            rows = st[:, 2:] >= 0
+            t = np.arange(STRIP_ROWS)
+            lo = np.where(rows, t[None, :], STRIP_ROWS).min(axis=1)
+            hi = np.where(rows, t[None, :], -1).max(axis=1)
+            b2 = f.b2
+            off = layout2.offsets
+            a = off[b2._el_first[st[:, 1] + lo]]
+            b = off[b2._el_last[st[:, 1] + hi] + 1]
+            g[key] = max(int(np.max(b - a)), 1)
+        g[("nu_keep", id(pg), id(layout2))] = layout2       # the id stays valid
+    return g[key]
+
+
+def _col_of_host(f):
+    g = _geo(f.config)
+    if "col_of_h" not in g:
+        g["col_of_h"] = f.col_of.cpu().numpy()
+    return g["col_of_h"]
+
+
+def raw_buffer(f, ndesc):
+    """Raw blocks of the plan: row-major (ndesc x W) or planes (W x ld)."""
+    W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
+    if planes(f):
+        return torch.empty((W, max(ndesc, 1)), dtype=torch.float64, device=f.dev)
+    return torch.empty((max(ndesc, 1), W), dtype=torch.float64, device=f.dev)
+
+
 class _Setup:
     """Device tables shared by the raw-row kernels of one formation."""
 
@@ -400,7 +498,7 @@ class _Setup:
         d1, d2 = f.b1.device_arrays(), f.b2.device_arrays()
         cut = self.cut or {}
         P = L.ptr
-        return RawCtx(f.b1.n, f.b2.n, f.b1.p, f.b2.p, f.b1.num_elements, f.b2.num_elements,
+        ctx = RawCtx(f.b1.n, f.b2.n, f.b1.p, f.b2.p, f.b1.num_elements, f.b2.num_elements,
                       P(d1["el_first"]), P(d1["el_last"]), P(d2["el_first"]), P(d2["el_last"]),
                       P(d1["ov_lo"]), P(d1["ov_hi"]), P(d2["ov_lo"]), P(d2["ov_hi"]),
                       P(d1["espan"]), P(d2["espan"]), P(f.config.element_class_dev),
@@ -413,6 +511,10 @@ class _Setup:
                       P(cut.get("f2")), P(cut.get("v2")), P(cut.get("grp_ptr")), P(cut.get("grp_key")),
                       P(cut.get("grp_pts")), P(cut.get("grp_perm")), P(cut.get("blocks")), cut.get("ngroups", 0),
                       P(desc), nraw, self.nmax[0], self.nmax[1], P(raw))
+        if planes(f):
+            pg = planes_geo(f)
+            ctx.store, ctx.raw_ld = P(pg["store"]), pg["ld"]
+        return ctx
 
 
 def _elem_tables(f):
@@ -451,13 +553,17 @@ def _gauss_ctx(f, eg, em, cg, desc, raw, nraw):
     """Context of the element-Gauss part of the raw rows (no rule sets)."""
     d1, d2 = f.b1.device_arrays(), f.b2.device_arrays()
     P = L.ptr
-    return RawCtx(n1=f.b1.n, n2=f.b2.n, p1=f.b1.p, p2=f.b2.p, nel1=f.b1.num_elements, nel2=f.b2.num_elements,
+    ctx = RawCtx(n1=f.b1.n, n2=f.b2.n, p1=f.b1.p, p2=f.b2.p, nel1=f.b1.num_elements, nel2=f.b2.num_elements,
                   el_first1=P(d1["el_first"]), el_last1=P(d1["el_last"]), el_first2=P(d2["el_first"]),
                   el_last2=P(d2["el_last"]), ov_lo1=P(d1["ov_lo"]), ov_hi1=P(d1["ov_hi"]), ov_lo2=P(d2["ov_lo"]),
                   ov_hi2=P(d2["ov_hi"]), espan1=P(d1["espan"]), espan2=P(d2["espan"]),
                   elem_class=P(f.config.element_class_dev), ng1=f.b1.p + 1, ng2=f.b2.p + 1,
                   ew1=P(eg[0][1]), ev1=P(eg[0][2]), ew2=P(eg[1][1]), ev2=P(eg[1][2]), em1=P(em[0]), em2=P(em[1]),
                   cg=P(cg), desc=P(desc), nraw=nraw, nmax1=1, nmax2=1, raw=P(raw))
+    if planes(f):
+        pg = planes_geo(f)
+        ctx.store, ctx.raw_ld = P(pg["store"]), pg["ld"]
+    return ctx
 
 
 def _cut_tables(f):
@@ -543,8 +649,7 @@ def prelaunch_geometry(f):
         _st("preA:elem")
         desc_dev, ndesc = _desc_dev(f)
         f._desc_pre = desc_dev
-        W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
-        f._raw_pre = torch.empty((max(ndesc, 1), W), dtype=torch.float64, device=f.dev)
+        f._raw_pre = raw_buffer(f, ndesc)
         if ndesc:
             L.call("tq_raw_gauss", _gauss_ctx(f, eg, em, cg, desc_dev, f._raw_pre, ndesc), 0, ndesc, L.stream())
         _st("preA:gauss")
@@ -791,18 +896,32 @@ def run_phase(f, phase):
         f._desc, _ = _desc_dev(f)
         if getattr(f, "_raw_pre", None) is not None and f._desc is not f._desc_pre:
             raise RuntimeError("row plan changed between the pass-start launch and the raw phase")
-        W = (2 * f.b1.p + 1) * (2 * f.b2.p + 1)
         pre = getattr(f, "_raw_pre", None)
-        f.raw = pre if pre is not None else torch.empty((max(desc.shape[0], 1), W), dtype=torch.float64,
-                                                        device=f.dev)
+        f.raw = pre if pre is not None else raw_buffer(f, desc.shape[0])
         skey = ("slot", id(desc))
         if skey not in g:
-            slot = torch.full_like(f.slot, -1)
-            slot[f._desc[:, 0].long()] = torch.arange(desc.shape[0], dtype=torch.int32, device=f.dev)
+            if planes(f):
+                slot = planes_geo(f)["slot"]
+            else:
+                slot = torch.full_like(f.slot, -1)
+                slot[f._desc[:, 0].long()] = torch.arange(desc.shape[0], dtype=torch.int32, device=f.dev)
             g[skey] = (slot, f._desc[:, 0].contiguous())
         f.slot, f.raw_list = g[skey]
         f._ctx = f._setup.ctx(f._desc, f.raw, desc.shape[0])
-        if nint:
+        pg = planes_geo(f) if planes(f) else None
+        if nint and pg is not None and pg["strip_ok"] and f._setup.grids is not None:
+            # interior rows by strips (no element-Gauss part: disjoint from
+            # the pass-start launch, no wait)
+            ctx_int = RawCtx.from_buffer_copy(f._ctx)
+            ctx_int.nmax1, ctx_int.nmax2 = f._setup.nmax_std
+            f._ctx_int = ctx_int
+            nu = strip_nu_max(f, pg, f._setup.sets[1][0].layout)
+            f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
+            f._bw = torch.empty(max(int(L.lib().tq_bw_table_doubles(ctx_int)), 1), dtype=torch.float64,
+                                device=f.dev)
+            L.call("tq_sf_strips", ctx_int, L.ptr(pg["strips"]), pg["nstrips"], nu, L.ptr(f._bw),
+                   L.ptr(f._planes_status), L.stream())
+        elif nint:
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)
             # interior rows read the standard rules only: their launch sizes its

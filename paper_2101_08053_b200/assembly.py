@@ -397,7 +397,9 @@ class Formation:
         stream still computing the raw rows; the deep-row pass overlaps it."""
         row_end = self.K if row_end is None else row_end
         nrows = row_end - row_begin
-        from ._rawrows import join_cut_blocks
+        from ._rawrows import join_cut_blocks, planes
+        if self.raw is not None and planes(self):
+            return self._finish_planes(row_begin, row_end, join)
         if self.deep is None and self.a1 is not None:
             n1, n2 = self.basis2d.shape
             # geometric flags: cached per row plan (keyed by its raw-row list)
@@ -510,6 +512,43 @@ class Formation:
         for st in getattr(self, "_status_streams", []):       # status reductions rejoin
             torch.cuda.current_stream().wait_stream(st)
         _stamp("fill")
+        return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
+
+    def _finish_planes(self, row_begin, row_end, join):
+        """All-raw formation: symmetrise / zero-drop / CSR in one pass over
+        the planes (tq_planes_csr).  The output is sized by the window total
+        (an upper bound of nnz) so no count pass precedes it."""
+        from ._rawrows import join_cut_blocks, planes_geo
+        nrows = row_end - row_begin
+        pg = planes_geo(self)
+        join_cut_blocks(self)
+        if join is not None:
+            torch.cuda.current_stream().wait_stream(join)
+        _stamp("join")
+        W = (2 * self.b1.p + 1) * (2 * self.b2.p + 1)
+        cap = max(nrows * W, 1)
+        indptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.dev)
+        indices = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        data = torch.empty(cap, dtype=torch.float64, device=self.dev)
+        state = torch.empty((L.lib().tq_planes_state_bytes(nrows) + 7) // 8, dtype=torch.int64, device=self.dev)
+        ctl = torch.zeros(3, dtype=torch.int32, device=self.dev)
+        ctx = self.rowctx(row_begin, row_end)
+        ctx.raw_ld = pg["ld"]
+        expect = self.capture["nnz"] if self.capture else -1
+        nnz = L.i64(0)
+        with self.timer("fill"):
+            L.call("tq_planes_csr", ctx, pg["base"], L.ptr(indptr), L.ptr(indices), L.ptr(data), cap, L.ptr(state),
+                   L.ptr(ctl), expect, None if self.capture else L.C.byref(nnz), L.stream())
+        self._planes_ctl = ctl
+        self._count_bufs = (indptr, state)
+        self._nrows = nrows
+        for st in getattr(self, "_status_streams", []):       # status reductions rejoin
+            torch.cuda.current_stream().wait_stream(st)
+        st = getattr(self, "_planes_status", None)
+        if st is not None and self.capture is None and int(st.item()):
+            raise RuntimeError("strip workspace bound exceeded (tq_sf_strips)")
+        _stamp("fill")
+        nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
     def _alloc_out(self, nrows, nnz):
@@ -646,7 +685,14 @@ class GraphFormation:
         fail = getattr(self.f, "_fail_any", None)
         if fail is not None and bool(fail.item()):
             raise RuleConstructionError_("moment-fit residual above tolerance in a replayed pass")
-        if int(self.f._count_bufs[1][L.tile_ctl(self.f._nrows) + 4].item()):
+        ctl = getattr(self.f, "_planes_ctl", None)
+        if ctl is not None:
+            if int(ctl[2].item()):
+                raise RuntimeError("replayed pass formed a different nnz than the captured one")
+            st = getattr(self.f, "_planes_status", None)
+            if st is not None and int(st.item()):
+                raise RuntimeError("strip workspace bound exceeded (tq_sf_strips)")
+        elif int(self.f._count_bufs[1][L.tile_ctl(self.f._nrows) + 4].item()):
             raise RuntimeError("replayed pass formed a different nnz than the captured one")
 
 

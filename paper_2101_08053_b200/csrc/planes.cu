@@ -1,0 +1,479 @@
+// The all-raw formation path (c != 1, or the element-Gauss `reference`
+// strategy): every active row is a raw row, stored in the planes layout
+// raw[o * ld + s] -- window entry o = (j1 - i1 + p1)(2p2 + 1) + (j2 - i2 + p2)
+// of the row with storage index s = active index - raw_base.  The planes of
+// consecutive rows are contiguous, so both kernels here move whole 128-byte
+// lines per warp instruction.
+//
+//  tq_sf_strips  <- sum_factor_row (src/assembly.py:218-252) for the interior
+//                   rows of the c != 1 BOX plan (_interior_rows_batched,
+//                   src/assembly.py:409-449): rows of one direction-1 line
+//                   with consecutive i2 form a strip that shares the
+//                   direction-1 contraction of the coefficient grid.
+//  tq_planes_csr <- _Run.finish (src/assembly.py:400-404): 0.5 (M + M^T),
+//                   exact-zero drop and sorted columns, in ONE pass (tile
+//                   counts published with a decoupled look-back scan).
+#include <limits.h>
+
+#include "common.cuh"
+
+namespace tq {
+
+__device__ __forceinline__ double colloc_val(const tq_ruleset& s, int p, int k, int j) {
+    const int r = j - s.first[k];
+    return (r >= 0 && r <= p) ? s.vals[(int64_t)k * (p + 1) + r] : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Weighted collocation tables of the standard rules, once per pass:
+// BW_d[i][k][o] = colloc_d(k0_d(i) + k, i - p + o) w_d(i)[k] for k < the row's
+// length and j = i - p + o in the overlap range of i, else 0; i < n_d,
+// k < nmax_d, o < WP (the strips' padded window).  *status |= 2 when a rule
+// row is longer than nmax_d.
+// ---------------------------------------------------------------------------
+__global__ void k_bw_tables(tq_rawctx c, int WP, double* __restrict__ bw1, double* __restrict__ bw2,
+                            int* __restrict__ status) {
+    const int64_t t1 = (int64_t)c.n1 * c.nmax1 * WP, total = t1 + (int64_t)c.n2 * c.nmax2 * WP;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const bool d1 = q < t1;
+        const int64_t e = d1 ? q : q - t1;
+        const int nmax = d1 ? c.nmax1 : c.nmax2, p = d1 ? c.p1 : c.p2;
+        const tq_ruleset& R = d1 ? c.sets1[0] : c.sets2[0];
+        const int i = (int)(e / ((int64_t)nmax * WP)), rem = (int)(e - (int64_t)i * nmax * WP);
+        const int k = rem / WP, o = rem - k * WP, j = i - p + o;
+        const int k0 = R.rules.k0[i];
+        const int len = k0 >= 0 ? (int)(R.rules.wptr[i + 1] - R.rules.wptr[i]) : 0;
+        if (k == 0 && o == 0 && len > nmax) atomicOr(status, 2);
+        double v = 0.0;
+        if (k < len && o <= 2 * p && j >= (d1 ? c.ov_lo1 : c.ov_lo2)[i] && j <= (d1 ? c.ov_hi1 : c.ov_hi2)[i])
+            v = colloc_val(R, p, k0 + k, j) * R.rules.w[R.rules.wptr[i] + k];
+        (d1 ? bw1 : bw2)[e] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Strips.  One strip = up to TS rows (i1, i20 + t) of the c != 1 BOX plan
+// whose box is their whole support (standard rules in both directions).
+// With B_d = the BW tables above and the coefficient grid G on the WQ points:
+//   stage A (shared by the strip):  X[u][o1] = sum_k1 B1[k1][o1] G[k1][u0 + u]
+//            over the union u of the rows' direction-2 point windows;
+//   stage B (per row t):            M_t[o1][o2] = sum_kk X[k0_t - u0 + kk][o1] B2_t[kk][o2].
+// The same products as sum_factor_row with the direction-1 contraction done
+// first (one stage-A pass per strip instead of one direction-2 pass per row:
+// about half the multiply-adds of the row-by-row form).  A thread of stage B
+// owns a BA x BA register tile of one row's block (a 3 x 3 grid of tiles per
+// row); lanes run over the strip's rows, so every store is a run of 16
+// consecutive storage slots of one plane.
+// strips: nstrips x (2 + TS) ints: i1, i20, storage index of row t (or -1).
+// ---------------------------------------------------------------------------
+constexpr int kStripRows = 16;
+
+__host__ __device__ inline int strip_b2_stride(int p, int n2m) {
+    const int WP = 3 * ((2 * p + 3) / 3);
+    return (n2m * WP) | 1;
+}
+
+__host__ __device__ inline size_t strip_smem_doubles(int p, int n1m, int n2m, int nu_max, int ts) {
+    const int W = 2 * p + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1;
+    return (size_t)n1m * WP + (size_t)n1m * nu_max + (size_t)nu_max * WPI + (size_t)ts * strip_b2_stride(p, n2m);
+}
+
+template <int P, int TS>
+__global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t* __restrict__ strips, int nstrips,
+                                                      int nu_max, const double* __restrict__ bw1,
+                                                      const double* __restrict__ bw2, int* __restrict__ status) {
+    constexpr int W = 2 * P + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1, NT = TS * 9;
+    extern __shared__ double sm[];
+    const int n1m = c.nmax1, n2m = c.nmax2, SB = strip_b2_stride(P, n2m);
+    double* B1 = sm;                      // [n1m][WP]
+    double* GS = B1 + n1m * WP;           // [n1m][nu]
+    double* X = GS + n1m * nu_max;        // [nu][WPI]
+    double* B2 = X + nu_max * WPI;        // [TS][SB]
+    __shared__ int s_k0[TS], s_n2[TS], s_st[TS], s_hdr[4];
+    const int tid = threadIdx.x;
+    const tq_ruleset R1 = c.sets1[0], R2 = c.sets2[0];
+    const double* __restrict__ G = c.grids[0];
+    const int ldG = R2.lay.npts;
+    for (int s = blockIdx.x; s < nstrips; s += gridDim.x) {
+        const int32_t* st = strips + (int64_t)s * (2 + TS);
+        const int i1 = st[0], i20 = st[1];
+        if (tid < TS) {
+            const int sidx = st[2 + tid];
+            int k0 = -1, n2 = 0;
+            if (sidx >= 0) {
+                const int i2 = i20 + tid;
+                k0 = R2.rules.k0[i2];
+                n2 = k0 >= 0 ? (int)(R2.rules.wptr[i2 + 1] - R2.rules.wptr[i2]) : 0;
+            }
+            s_k0[tid] = k0;
+            s_n2[tid] = n2;
+            s_st[tid] = sidx;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int u0 = INT_MAX, u1 = INT_MIN, bad = 0;
+            for (int t = 0; t < TS; ++t)
+                if (s_n2[t] > 0) {
+                    u0 = min(u0, s_k0[t]);
+                    u1 = max(u1, s_k0[t] + s_n2[t]);
+                    bad |= s_n2[t] > n2m;
+                }
+            const int k01 = R1.rules.k0[i1];
+            int n1 = k01 >= 0 ? (int)(R1.rules.wptr[i1 + 1] - R1.rules.wptr[i1]) : 0;
+            int nu = u1 > u0 ? u1 - u0 : 0;
+            if (nu > nu_max || n1 > n1m || bad) {      // workspace bound broken: flagged, never silent
+                atomicOr(status, 1);
+                nu = 0;
+            }
+            if (nu == 0) n1 = 0;
+            s_hdr[0] = u0;
+            s_hdr[1] = nu;
+            s_hdr[2] = k01;
+            s_hdr[3] = n1;
+        }
+        __syncthreads();
+        const int u0 = s_hdr[0], nu = s_hdr[1], k01 = s_hdr[2], n1 = s_hdr[3];
+        if (n1 > 0) {
+            const double* b1src = bw1 + (int64_t)i1 * n1m * WP;
+            for (int q = tid; q < n1 * WP; q += NT) B1[q] = __ldg(b1src + q);
+            for (int q = tid; q < n1 * nu; q += NT) {
+                const int k = q / nu, u = q - k * nu;
+                GS[q] = __ldg(G + (int64_t)(k01 + k) * ldG + u0 + u);
+            }
+            const int nrow = min(TS, c.n2 - i20);
+            const double* b2src = bw2 + (int64_t)i20 * n2m * WP;
+            for (int q = tid; q < nrow * n2m * WP; q += NT) {
+                const int t = q / (n2m * WP), rem = q - t * (n2m * WP);
+                B2[t * SB + rem] = __ldg(b2src + q);
+            }
+        }
+        __syncthreads();
+        // stage A: lanes run over u (conflict-free column reads of GS; the B1
+        // reads broadcast)
+        for (int q = tid; q < 3 * nu; q += NT) {
+            const int ob = q / nu, u = q - ob * nu;
+            double acc[BA];
+#pragma unroll
+            for (int i = 0; i < BA; ++i) acc[i] = 0.0;
+            for (int k1 = 0; k1 < n1; ++k1) {
+                const double g = GS[k1 * nu + u];
+                const double* b = B1 + k1 * WP + ob * BA;
+#pragma unroll
+                for (int i = 0; i < BA; ++i) acc[i] = fma(b[i], g, acc[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < BA; ++i) X[u * WPI + ob * BA + i] = acc[i];
+        }
+        __syncthreads();
+        // stage B: thread (t = lane row, a, b) owns rows a*BA.., columns b*BA.. of row t
+        {
+            const int t = tid % TS, ab = tid / TS, a = ab / 3, b = ab - a * 3;
+            const int n2 = n1 > 0 ? s_n2[t] : 0, sidx = s_st[t];
+            double acc[BA][BA];
+#pragma unroll
+            for (int i = 0; i < BA; ++i)
+#pragma unroll
+                for (int j = 0; j < BA; ++j) acc[i][j] = 0.0;
+            const double* x = X + (n2 > 0 ? s_k0[t] - u0 : 0) * WPI + a * BA;
+            const double* y = B2 + t * SB + b * BA;
+            for (int kk = 0; kk < n2; ++kk) {
+                double xv[BA], yv[BA];
+#pragma unroll
+                for (int i = 0; i < BA; ++i) {
+                    xv[i] = x[kk * WPI + i];
+                    yv[i] = y[kk * WP + i];
+                }
+#pragma unroll
+                for (int i = 0; i < BA; ++i)
+#pragma unroll
+                    for (int j = 0; j < BA; ++j) acc[i][j] = fma(xv[i], yv[j], acc[i][j]);
+            }
+            if (sidx >= 0) {
+                double* dst = c.raw + sidx;
+#pragma unroll
+                for (int i = 0; i < BA; ++i)
+#pragma unroll
+                    for (int j = 0; j < BA; ++j) {
+                        const int o1 = a * BA + i, o2 = b * BA + j;
+                        if (o1 < W && o2 < W) dst[(int64_t)(o1 * W + o2) * c.raw_ld] = acc[i][j];
+                    }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Symmetrise / zero-drop / CSR in one pass over the planes.  A block takes
+// 16-row tiles in ticket order.  Phase 1: half-warp lane = row, half-warp h
+// of warp w = window lines o1 = 2w + h, 2w + h + 16, ..: M_ij + M_ji from two coalesced plane reads (the row's
+// own plane o and the partner's mirrored plane T-1-o), kept columns into a
+// [row][entry] shared stage.  Phase 2: per-row counts, the tile total
+// published and the tile's offset found by a decoupled look-back over the
+// earlier tiles' words (flag 1 = aggregate, 2 = inclusive prefix).  Phase 3:
+// warp per row, ballot-compacted contiguous stores of the kept entries.
+// ctl: [0] tile ticket, [1] nnz, [2] flags (1 = nnz differs from `expect`,
+// 2 = capacity exceeded; nothing past `cap` is written).
+// ---------------------------------------------------------------------------
+constexpr int kPlTile = 16, kPlThreads = 256;
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned v) {
+    return ((unsigned long long)flag << 32) | v;
+}
+
+__device__ __forceinline__ int pl_row_of(const tq_rowctx& c, int idx) { return idx / c.n2; }
+
+template <int P>
+__global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* __restrict__ indptr,
+                                                            int32_t* __restrict__ indices, double* __restrict__ data,
+                                                            int64_t cap, unsigned long long* __restrict__ state,
+                                                            int32_t* __restrict__ ctl, int64_t expect) {
+    constexpr int W = 2 * P + 1, T = W * W, NW = kPlThreads / 32;
+    extern __shared__ double sm[];
+    double* sv = sm;                                            // [kPlTile][T]
+    int* sc = reinterpret_cast<int*>(sv + kPlTile * T);        // [kPlTile][T]
+    __shared__ int s_tile, s_off[kPlTile], s_cnt[kPlTile];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int n = c.row_end - c.row_begin, nt = (n + kPlTile - 1) / kPlTile;
+    const double* __restrict__ raw = c.raw;
+    const int64_t ld = c.raw_ld;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ctl, 1);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= nt) break;
+        // ---- phase 1
+        {
+            const int tr = lane & (kPlTile - 1), half = lane / kPlTile;
+            const int r = c.row_begin + tile * kPlTile + tr;
+            const bool have = r < c.row_end;
+            int i1 = 0, i2 = 0, jl1 = 1, jh1 = 0, jl2 = 1, jh2 = 0;
+            if (have) {
+                const int idx = __ldg(c.active + r);
+                i1 = pl_row_of(c, idx);
+                i2 = idx - i1 * c.n2;
+                jl1 = __ldg(c.ov_lo1 + i1);
+                jh1 = __ldg(c.ov_hi1 + i1);
+                jl2 = __ldg(c.ov_lo2 + i2);
+                jh2 = __ldg(c.ov_hi2 + i2);
+            }
+            const int si = r - raw_base;
+            for (int o1 = 2 * warp + half; o1 < W; o1 += 2 * NW) {
+                const int j1 = i1 - P + o1;
+                const bool ok1 = have && j1 >= jl1 && j1 <= jh1;
+                const int* colrow = c.col_of + (int64_t)j1 * c.n2 + (i2 - P);
+                int col[W];
+#pragma unroll
+                for (int o2 = 0; o2 < W; ++o2) {
+                    const int j2 = i2 - P + o2;
+                    col[o2] = (ok1 && j2 >= jl2 && j2 <= jh2) ? __ldg(colrow + o2) : -1;
+                }
+                double vi[W];
+#pragma unroll
+                for (int o2 = 0; o2 < W; ++o2)
+                    vi[o2] = col[o2] >= 0 ? __ldg(raw + (int64_t)(o1 * W + o2) * ld + si) : 0.0;
+#pragma unroll
+                for (int o2 = 0; o2 < W; ++o2) {
+                    const int o = o1 * W + o2;
+                    int cl = col[o2];
+                    double v = 0.0;
+                    if (cl >= 0) {
+                        v = __dadd_rn(vi[o2], __ldg(raw + (int64_t)(T - 1 - o) * ld + (cl - raw_base)));
+                        if (v == 0.0) cl = -1;
+                    }
+                    sv[tr * T + o] = 0.5 * v;
+                    sc[tr * T + o] = cl;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- phase 2
+        for (int t = warp; t < kPlTile; t += NW) {
+            int cnt = 0;
+            for (int o = lane; o < T; o += 32) cnt += sc[t * T + o] >= 0;
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (lane == 0) s_cnt[t] = cnt;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int cnt = lane < kPlTile ? s_cnt[lane] : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int agg = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane == 0) st_release_u64(state + tile, lb_pack(tile == 0 ? 2u : 1u, (unsigned)agg));
+            int excl = 0;
+            if (tile > 0) {
+                for (int j = tile - 1;; j -= 32) {
+                    const int jj = j - lane;
+                    unsigned long long w = lb_pack(2u, 0u);
+                    if (jj >= 0) {
+                        do {
+                            w = ld_acquire_u64(state + jj);
+                        } while ((w >> 32) == 0);
+                    }
+                    const unsigned inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
+                    const int first = inc ? __ffs(inc) - 1 : 31;
+                    excl += __reduce_add_sync(0xffffffffu, lane <= first ? (int)(w & 0xffffffffu) : 0);
+                    if (inc) break;
+                }
+                if (lane == 0) st_release_u64(state + tile, lb_pack(2u, (unsigned)(excl + agg)));
+            }
+            if (lane < kPlTile) s_off[lane] = excl + incl - cnt;
+            if (tile == nt - 1 && lane == 0) {
+                const int total = excl + agg;
+                ctl[1] = total;
+                indptr[n] = total;
+                int fl = 0;
+                if (expect >= 0 && total != expect) fl |= 1;
+                if (total > cap) fl |= 2;
+                if (fl) atomicOr(ctl + 2, fl);
+            }
+        }
+        __syncthreads();
+        // ---- phase 3
+        for (int t = warp; t < kPlTile; t += NW) {
+            const int rr = c.row_begin + tile * kPlTile + t;
+            if (rr >= c.row_end) break;
+            int pos = s_off[t];
+            if (lane == 0) indptr[rr - c.row_begin] = pos;
+            for (int o0 = 0; o0 < T; o0 += 32) {
+                const int o = o0 + lane;
+                const int cl = o < T ? sc[t * T + o] : -1;
+                const unsigned m = __ballot_sync(0xffffffffu, cl >= 0);
+                if (cl >= 0) {
+                    const int at = pos + __popc(m & lt);
+                    if (at < cap) {
+                        indices[at] = cl;
+                        data[at] = sv[t * T + o];
+                    }
+                }
+                pos += __popc(m);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace tq
+
+using namespace tq;
+
+template <int P>
+static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t nstrips, int32_t nu_max,
+                            const double* bw1, const double* bw2, int32_t* status, cudaStream_t st) {
+    const size_t shm = sizeof(double) * strip_smem_doubles(P, c.nmax1, c.nmax2, nu_max, kStripRows);
+    if (shm > 220 * 1024) { set_error("strip workspace too large (%zu bytes)", shm); return TQ_EINVAL; }
+    auto kern = k_sf_strips<P, kStripRows>;
+    TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    int per_sm = 0;
+    TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStripRows * 9, shm));
+    const int grid = (int)std::min<int64_t>(nstrips, (int64_t)kSms * std::max(per_sm, 1));
+    kern<<<grid, kStripRows * 9, shm, st>>>(c, strips, nstrips, nu_max, bw1, bw2, status);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_sf_strips");
+    return TQ_OK;
+}
+
+extern "C" int64_t tq_bw_table_doubles(tq_rawctx c) {
+    const int WP = 3 * ((2 * c.p1 + 3) / 3);
+    return (int64_t)c.n1 * c.nmax1 * WP + (int64_t)c.n2 * c.nmax2 * WP;
+}
+
+// bw: tq_bw_table_doubles(c) doubles of scratch (both directions' tables).
+extern "C" int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips, int32_t nu_max, double* bw,
+                            int32_t* status, void* stream) {
+    if (nstrips <= 0) return TQ_OK;
+    if (!c.grids || !c.raw_ld || c.p1 != c.p2) { set_error("tq_sf_strips needs coefficient grids, planes and p1 == p2"); return TQ_EINVAL; }
+    if (c.p1 < 1 || c.p1 > kMaxP) { set_error("degree out of range"); return TQ_EINVAL; }
+    cudaStream_t st = S(stream);
+    const int WP = 3 * ((2 * c.p1 + 3) / 3);
+    double* bw1 = bw;
+    double* bw2 = bw + (int64_t)c.n1 * c.nmax1 * WP;
+    const int64_t nb = tq_bw_table_doubles(c);
+    k_bw_tables<<<grid_for(nb, 256), 256, 0, st>>>(c, WP, bw1, bw2, status);
+    ::tq::note_launch();
+    switch (c.p1) {
+#define CASE(Q) case Q: return sf_strips_launch<Q>(c, strips, nstrips, nu_max, bw1, bw2, status, st);
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    }
+    return TQ_EINVAL;
+}
+
+extern "C" int64_t tq_planes_state_bytes(int32_t nrows) {
+    return (int64_t)sizeof(unsigned long long) * ((nrows + kPlTile - 1) / kPlTile + 1);
+}
+
+template <int P>
+static int planes_csr_launch(const tq_rowctx& c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
+                             int64_t cap, void* state, int32_t* ctl, int64_t expect, cudaStream_t st) {
+    constexpr int T = (2 * P + 1) * (2 * P + 1);
+    const size_t shm = (size_t)kPlTile * T * (sizeof(double) + sizeof(int));
+    auto kern = k_planes_csr<P>;
+    static int per_sm_cache[kMaxP + 1][16] = {};
+    int dev = 0;
+    TQ_CUDA(cudaGetDevice(&dev));
+    int& per_sm = per_sm_cache[P][dev & 15];
+    if (!per_sm) {
+        TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPlThreads, shm));
+        if (per_sm < 1) { set_error("planes stage does not fit in shared memory"); return TQ_EINVAL; }
+    }
+    const int nrows = c.row_end - c.row_begin, nt = (nrows + kPlTile - 1) / kPlTile;
+    TQ_CUDA(cudaMemsetAsync(state, 0, (size_t)tq_planes_state_bytes(nrows), st));
+    TQ_CUDA(cudaMemsetAsync(ctl, 0, 3 * sizeof(int32_t), st));
+    const int grid = std::min(nt, kSms * per_sm);
+    kern<<<grid, kPlThreads, shm, st>>>(c, raw_base, indptr, indices, data, cap,
+                                        reinterpret_cast<unsigned long long*>(state), ctl, expect);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_planes_csr");
+    return TQ_OK;
+}
+
+// CSR rows [row_begin, row_end) of an all-raw formation from its planes
+// (c.raw, c.raw_ld; storage index = active row - raw_base).  indptr:
+// nrows + 1; indices/data: `cap` entries (>= nnz; the window total is
+// always enough); state: tq_planes_state_bytes(nrows) bytes of scratch;
+// ctl: 3 ints (ctl[1] = nnz, ctl[2] = flags, see k_planes_csr); expect: the
+// nnz a replayed pass must reproduce (-1: none).  nnz_h (optional) reads
+// ctl[1] back (synchronising the stream).
+extern "C" int tq_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
+                             int64_t cap, void* state, int32_t* ctl, int64_t expect, int64_t* nnz_h, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    cudaStream_t st = S(stream);
+    if (nrows <= 0) {
+        TQ_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int32_t), st));
+        if (nnz_h) *nnz_h = 0;
+        return TQ_OK;
+    }
+    if (!c.raw_ld || c.p1 != c.p2) { set_error("tq_planes_csr needs the planes layout and p1 == p2"); return TQ_EINVAL; }
+    int rc = TQ_EINVAL;
+    switch (c.p1) {
+#define CASE(Q) case Q: rc = planes_csr_launch<Q>(c, raw_base, indptr, indices, data, cap, state, ctl, expect, st); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+        default: set_error("degree out of range"); return TQ_EINVAL;
+    }
+    if (rc) return rc;
+    if (nnz_h) {
+        int32_t h[3];
+        TQ_CUDA(cudaMemcpyAsync(h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaStreamSynchronize(st));
+        if (h[2] & 2) { set_error("planes CSR: nnz %d exceeds the capacity %lld", h[1], (long long)cap); return TQ_EOVERFLOW; }
+        *nnz_h = h[1];
+    }
+    return TQ_OK;
+}

@@ -25,6 +25,19 @@ struct RowDesc {
     int fidx, mode, set1, set2, a1, b1, a2, b2;
 };
 
+// The raw block of descriptor row r: row-major (raw + r W1 W2, stride 1) or,
+// in the planes layout, entry q at raw[q * raw_ld + store[r]].
+struct RawRow {
+    double* p;
+    int64_t s;
+    __device__ __forceinline__ double& operator[](int q) const { return p[q * s]; }
+};
+
+__device__ __forceinline__ RawRow raw_row(const tq_rawctx& c, int r) {
+    if (c.raw_ld) return RawRow{c.raw + c.store[r], c.raw_ld};
+    return RawRow{c.raw + (int64_t)r * ((2 * c.p1 + 1) * (2 * c.p2 + 1)), 1};
+}
+
 __device__ inline double colloc_at(const tq_ruleset& s, int p, int k, int j) {
     int r = j - s.first[k];
     return (r >= 0 && r <= p) ? s.vals[(int64_t)k * (p + 1) + r] : 0.0;
@@ -115,7 +128,7 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
         if (PARTS == 2 && d.mode == TQ_ROW_GAUSS) continue;     // nothing to add
         if (PARTS == 2) {
-            const double* src = c.raw + (int64_t)r * T;
+            const RawRow src = raw_row(c, r);
             for (int q = lane; q < T; q += 32) blk[q] = src[q];
         } else {
             for (int q = lane; q < T; q += 32) blk[q] = 0.0;
@@ -305,7 +318,7 @@ __global__ void k_raw_regular(tq_rawctx c, int r0, int r1) {
                 __syncwarp();
             }
         }
-        double* dst = c.raw + (int64_t)r * T;
+        const RawRow dst = raw_row(c, r);
         for (int q = lane; q < T; q += 32) dst[q] = blk[q];
         __syncwarp();
     }
@@ -368,7 +381,7 @@ __global__ void __launch_bounds__(NT) k_raw_gauss_coef(tq_rawctx c, int r0, int 
     const int64_t ld = (int64_t)c.nel2 * ng2;
     for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
         const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
-        double* dst = c.raw + (int64_t)r * T;
+        const RawRow dst = raw_row(c, r);
         bool work = d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX;
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
         if (full_box_row(c, d, i1, i2)) continue;        // uniform: written by k_raw_sf_coef
@@ -496,7 +509,7 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
         const bool write = full_box_row(c, d, i1, i2);
         if (!(k01 >= 0 && k02 >= 0 && n1 > 0 && n2 > 0)) {       // uniform
             if (write)
-                for (int q = tid; q < T; q += NT) c.raw[(int64_t)r * T + q] = 0.0;
+                for (int q = tid; q < T; q += NT) raw_row(c, r)[q] = 0.0;
             continue;
         }
         const double* w1 = s1.rules.w + s1.rules.wptr[i1] + (lo1 - k01);
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(NT) k_raw_sf_coef(tq_rawctx c, int r0, int r1)
         __syncthreads();
         // stage 2: a thread owns one o2 and OB consecutive o1 (one inner
         // load feeds OB FMAs; the B1 reads broadcast)
-        double* dst = c.raw + (int64_t)r * T;
+        const RawRow dst = raw_row(c, r);
         {
             const int ng = (W1 + OB - 1) / OB;
             for (int q = tid; q < W2 * ng; q += NT) {
@@ -713,17 +726,26 @@ __global__ void __launch_bounds__(kCbThreads) k_cut_blocks_wide(tq_rawctx c) {
 }
 
 // Row gather of the element blocks into the raw rows (warp per row).
+// (planes layout: the row's contributions are summed in a warp-private
+// shared block first and added to its strided planes once)
 __global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
+    extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int W2 = 2 * c.p2 + 1, T = (2 * c.p1 + 1) * W2;
     const int q1 = c.p1 + 1, q2 = c.p2 + 1, Q = q1 * q2;
+    double* acc = sm + (threadIdx.x >> 5) * T;
     for (int r = r0 + blockIdx.x * wpb + (threadIdx.x >> 5); r < r1; r += gridDim.x * wpb) {
         RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
         const int ea1 = max(c.el_first1[i1] - 1, 0), eb1 = min(c.el_last1[i1] + 1, c.nel1 - 1);
         const int ea2 = max(c.el_first2[i2] - 1, 0), eb2 = min(c.el_last2[i2] + 1, c.nel2 - 1);
         const int w2 = eb2 - ea2 + 1, nh = (eb1 - ea1 + 1) * w2;
-        double* dst = c.raw + (int64_t)r * T;
+        const RawRow dst = c.raw_ld ? RawRow{acc, 1} : raw_row(c, r);
+        bool touched = false;
+        if (c.raw_ld) {
+            for (int q = lane; q < T; q += 32) acc[q] = 0.0;
+            __syncwarp();
+        }
         for (int h0 = 0; h0 < nh; h0 += 32) {
             int h = h0 + lane;
             int id = -1;
@@ -737,6 +759,7 @@ __global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
                     const int f1 = c.grp_key[2 * g], f2 = c.grp_key[2 * g + 1];
                     const int a1 = i1 - f1, a2 = i2 - f2;
                     if (a1 < 0 || a1 > c.p1 || a2 < 0 || a2 > c.p2) continue;
+                    touched = true;
                     const double* G = c.grp_blocks + ((int64_t)g * Q + (a1 * q2 + a2)) * Q;
                     for (int B = lane; B < Q; B += 32) {
                         int b1 = B / q2, b2 = B - (B / q2) * q2;
@@ -745,6 +768,12 @@ __global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
                 }
             }
         }
+        if (c.raw_ld && touched) {      // warp-uniform
+            __syncwarp();
+            const RawRow out = raw_row(c, r);
+            for (int q = lane; q < T; q += 32) out[q] += acc[q];
+        }
+        __syncwarp();
     }
 }
 
@@ -903,7 +932,7 @@ __global__ void __launch_bounds__(256) k_raw_gauss_sep(tq_rawctx c, int r0, int 
     for (int r = r0 + blockIdx.x * WPB + wib; r < r1; r += gridDim.x * WPB) {
         const RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
         const int i1 = d.fidx / c.n2, i2 = d.fidx - i1 * c.n2;
-        double* dst = c.raw + (int64_t)r * T;
+        const RawRow dst = raw_row(c, r);
         if (d.mode != TQ_ROW_GAUSS && d.mode != TQ_ROW_BOX) {
             for (int q = lane; q < T; q += 32) dst[q] = 0.0;
             continue;
@@ -1127,7 +1156,8 @@ extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
 extern "C" int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream) {
     if (r1 <= r0 || !c.cut_ptr || c.ngroups <= 0) return TQ_OK;
     int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 16);
-    k_raw_cutcells<<<grid, 256, 0, S(stream)>>>(c, r0, r1); ::tq::note_launch();
+    const size_t shm = c.raw_ld ? sizeof(double) * 8 * (2 * c.p1 + 1) * (2 * c.p2 + 1) : 0;
+    k_raw_cutcells<<<grid, 256, shm, S(stream)>>>(c, r0, r1); ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_raw_cutcells");
     return TQ_OK;
 }

@@ -94,6 +94,7 @@ __device__ __forceinline__ double raw_value(const tq_rowctx& c, int i1, int i2, 
     const int W1 = 2 * c.p1 + 1, W2 = 2 * c.p2 + 1;
     const int o1 = j1 - i1 + c.p1, o2 = j2 - i2 + c.p2;
     if (s_i < 0) return __dmul_rn(__ldg(c.a1 + (int64_t)i1 * W1 + o1), __ldg(c.a2 + (int64_t)i2 * W2 + o2));
+    if (c.raw_ld) return __ldg(c.raw + (int64_t)(o1 * W2 + o2) * c.raw_ld + s_i);
     return __ldg(c.raw + (int64_t)s_i * (W1 * W2) + o1 * W2 + o2);
 }
 
