@@ -54,7 +54,8 @@ def _bind():
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
-    L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
     L.optional("tq_bw_table_doubles", [RawCtx], L.i64)
     L.optional("tq_planes_csr", [L.RowCtx, L.i32, L.vp, L.vp, L.vp, L.i64, L.vp, L.vp, L.i64, L.vp, L.vp])
     L.optional("tq_planes_state_bytes", [L.i32], L.i64)
@@ -393,27 +394,39 @@ def planes_geo(f):
     return g[key]
 
 
-def strip_nu_max(f, pg, layout2):
-    """Bound of a strip's union of direction-2 point windows: the layout
-    points of the elements its rows' supports cover (a WQ rule row lies in
-    its support's points); cached per (plan, layout)."""
+def strip_classes(f, pg, layout1, layout2):
+    """The strips split into launches by shared-memory need: the regular
+    strips (rule rows no longer than the median support's points, the
+    interior of a uniform mesh) and the rest (boundary lines), each launch
+    with its own capacities (n1m, n2m) and union-window bound nu_max.  A WQ
+    rule row lies in its support's points, so the support point counts bound
+    the rows; the kernel flags any row that breaks them.  Cached per (plan,
+    layouts): [(strips_dev, nstrips, n1m, n2m, nu_max)]."""
     g = _geo(f.config)
-    key = ("nu_max", id(pg), id(layout2))
+    key = ("strip_classes", id(pg), id(layout1), id(layout2))
     if key not in g:
         st = pg["strips_h"]
-        if st.shape[0] == 0:
-            g[key] = 1
-        else:
+        out = []
+        if st.shape[0]:
+            b1, b2 = f.b1, f.b2
+            o1, o2 = layout1.offsets, layout2.offsets
+            cnt1 = o1[b1._el_last + 1] - o1[b1._el_first]
+            cnt2 = o2[b2._el_last + 1] - o2[b2._el_first]
             rows = st[:, 2:] >= 0
             t = np.arange(STRIP_ROWS)
+            i2 = np.minimum(st[:, 1:2] + t[None, :], b2.n - 1)
             lo = np.where(rows, t[None, :], STRIP_ROWS).min(axis=1)
             hi = np.where(rows, t[None, :], -1).max(axis=1)
-            b2 = f.b2
-            off = layout2.offsets
-            a = off[b2._el_first[st[:, 1] + lo]]
-            b = off[b2._el_last[st[:, 1] + hi] + 1]
-            g[key] = max(int(np.max(b - a)), 1)
-        g[("nu_keep", id(pg), id(layout2))] = layout2       # the id stays valid
+            c1 = cnt1[st[:, 0]]
+            c2 = np.where(rows, cnt2[i2], 0).max(axis=1)
+            nu = o2[b2._el_last[st[:, 1] + hi] + 1] - o2[b2._el_first[st[:, 1] + lo]]
+            reg = (c1 <= int(np.median(cnt1))) & (c2 <= int(np.median(cnt2)))
+            for sel in (reg, ~reg):
+                if sel.any():
+                    out.append((L.dev(np.ascontiguousarray(st[sel]), torch.int32), int(sel.sum()),
+                                int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1)))
+        g[key] = out
+        g[key + ("keep",)] = (layout1, layout2)       # the ids stay valid
     return g[key]
 
 
@@ -915,12 +928,14 @@ def run_phase(f, phase):
             ctx_int = RawCtx.from_buffer_copy(f._ctx)
             ctx_int.nmax1, ctx_int.nmax2 = f._setup.nmax_std
             f._ctx_int = ctx_int
-            nu = strip_nu_max(f, pg, f._setup.sets[1][0].layout)
             f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
             f._bw = torch.empty(max(int(L.lib().tq_bw_table_doubles(ctx_int)), 1), dtype=torch.float64,
                                 device=f.dev)
-            L.call("tq_sf_strips", ctx_int, L.ptr(pg["strips"]), pg["nstrips"], nu, L.ptr(f._bw),
-                   L.ptr(f._planes_status), L.stream())
+            L.call("tq_bw_tables", ctx_int, L.ptr(f._bw), L.ptr(f._planes_status), L.stream())
+            for strips, ns, n1m, n2m, nu in strip_classes(f, pg, f._setup.sets[0][0].layout,
+                                                          f._setup.sets[1][0].layout):
+                L.call("tq_sf_strips", ctx_int, L.ptr(strips), ns, n1m, n2m, nu, L.ptr(f._bw),
+                       L.ptr(f._planes_status), L.stream())
         elif nint:
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)

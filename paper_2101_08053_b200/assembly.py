@@ -86,7 +86,17 @@ class CoefficientField:
         if self._device is not None:
             return self._device.grid_device(x1_dev, x2_dev)
         g = self.grid(x1_dev.cpu().numpy(), x2_dev.cpu().numpy())
-        return L.dev(g, torch.float64)
+        out = _padded_grid(g.shape[0], g.shape[1], x1_dev.device)
+        out.copy_(torch.as_tensor(g, dtype=torch.float64))
+        return out
+
+
+def _padded_grid(n1, n2, device):
+    """(n1, n2) coefficient grid with two doubles of slack after its end: the
+    strips kernel reads rows with 16-byte bulk copies rounded up to an even
+    length (tq_sf_strips)."""
+    buf = torch.empty(n1 * n2 + 2, dtype=torch.float64, device=device)
+    return buf[: n1 * n2].view(n1, n2)
 
 
 class GeometryMap:
@@ -111,7 +121,7 @@ class GeometryMap:
         return self._dev[0]
 
     def grid_device(self, x1, x2):
-        out = torch.empty((x1.numel(), x2.numel()), dtype=torch.float64, device=x1.device)
+        out = _padded_grid(x1.numel(), x2.numel(), x1.device)
         L.call("tq_coeff_grid", self.device(), L.ptr(x1), x1.numel(), L.ptr(x2), x2.numel(), L.ptr(out), L.stream())
         return out
 

@@ -31,21 +31,27 @@ __device__ __forceinline__ double colloc_val(const tq_ruleset& s, int p, int k, 
 // k < nmax_d, o < WP (the strips' padded window).  *status |= 2 when a rule
 // row is longer than nmax_d.
 // ---------------------------------------------------------------------------
-__global__ void k_bw_tables(tq_rawctx c, int WP, double* __restrict__ bw1, double* __restrict__ bw2,
+__host__ __device__ inline int bw_wp(int p) { return 3 * ((2 * p + 3) / 3); }
+// doubles per table row (one test function): even, so rows start 16-byte aligned
+__host__ __device__ inline int bw_row(int p, int nmax) { return (nmax * bw_wp(p) + 1) & ~1; }
+
+__global__ void k_bw_tables(tq_rawctx c, double* __restrict__ bw1, double* __restrict__ bw2,
                             int* __restrict__ status) {
-    const int64_t t1 = (int64_t)c.n1 * c.nmax1 * WP, total = t1 + (int64_t)c.n2 * c.nmax2 * WP;
+    const int WP = bw_wp(c.p1), R1 = bw_row(c.p1, c.nmax1), R2 = bw_row(c.p2, c.nmax2);
+    const int64_t t1 = (int64_t)c.n1 * R1, total = t1 + (int64_t)c.n2 * R2;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const bool d1 = q < t1;
         const int64_t e = d1 ? q : q - t1;
-        const int nmax = d1 ? c.nmax1 : c.nmax2, p = d1 ? c.p1 : c.p2;
+        const int nmax = d1 ? c.nmax1 : c.nmax2, p = d1 ? c.p1 : c.p2, RS = d1 ? R1 : R2;
         const tq_ruleset& R = d1 ? c.sets1[0] : c.sets2[0];
-        const int i = (int)(e / ((int64_t)nmax * WP)), rem = (int)(e - (int64_t)i * nmax * WP);
+        const int i = (int)(e / RS), rem = (int)(e - (int64_t)i * RS);
         const int k = rem / WP, o = rem - k * WP, j = i - p + o;
         const int k0 = R.rules.k0[i];
         const int len = k0 >= 0 ? (int)(R.rules.wptr[i + 1] - R.rules.wptr[i]) : 0;
-        if (k == 0 && o == 0 && len > nmax) atomicOr(status, 2);
+        if (rem == 0 && len > nmax) atomicOr(status, 2);
         double v = 0.0;
-        if (k < len && o <= 2 * p && j >= (d1 ? c.ov_lo1 : c.ov_lo2)[i] && j <= (d1 ? c.ov_hi1 : c.ov_hi2)[i])
+        if (k < len && k < nmax && o <= 2 * p && j >= (d1 ? c.ov_lo1 : c.ov_lo2)[i] &&
+            j <= (d1 ? c.ov_hi1 : c.ov_hi2)[i])
             v = colloc_val(R, p, k0 + k, j) * R.rules.w[R.rules.wptr[i] + k];
         (d1 ? bw1 : bw2)[e] = v;
     }
@@ -68,32 +74,91 @@ __global__ void k_bw_tables(tq_rawctx c, int WP, double* __restrict__ bw1, doubl
 // ---------------------------------------------------------------------------
 constexpr int kStripRows = 16;
 
+// shared row stride of the B2 stage: an odd number of 16-byte units (the
+// rows' 16 lanes spread over the banks; rows stay 16-byte aligned)
 __host__ __device__ inline int strip_b2_stride(int p, int n2m) {
-    const int WP = 3 * ((2 * p + 3) / 3);
-    return (n2m * WP) | 1;
+    const int m = (n2m * bw_wp(p) + 1) / 2;
+    return 2 * (m | 1);
 }
+
+// row stride of the coefficient stage: even (16-byte aligned rows) with a
+// slot of slack for an odd first column
+__host__ __device__ inline int strip_gs_stride(int nu_max) { return (nu_max + 3) & ~1; }
+
+// shared stage offsets (doubles): B1 | GS | X | B2; the 16-byte copy
+// targets (B1, B2) start at even offsets
+struct StripSmem {
+    int gs, x, b2, total;
+    __host__ __device__ StripSmem(int p, int n1m, int n2m, int nu_max, int ts) {
+        const int WP = bw_wp(p), WPI = WP | 1;
+        gs = (n1m * WP + 1) & ~1;
+        x = gs + n1m * strip_gs_stride(nu_max);
+        b2 = (x + nu_max * WPI + 1) & ~1;
+        total = b2 + ts * strip_b2_stride(p, n2m);
+    }
+};
 
 __host__ __device__ inline size_t strip_smem_doubles(int p, int n1m, int n2m, int nu_max, int ts) {
-    const int W = 2 * p + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1;
-    return (size_t)n1m * WP + (size_t)n1m * nu_max + (size_t)nu_max * WPI + (size_t)ts * strip_b2_stride(p, n2m);
+    return (size_t)StripSmem(p, n1m, n2m, nu_max, ts).total;
 }
 
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one-dimensional TMA bulk copies into shared memory, completing on an mbarrier
+__device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+    unsigned done;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(sptr(b)), "r"(phase) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sptr(sdst)), "l"(gsrc), "r"(bytes), "r"(sptr(b)) : "memory");
+}
+
+// n1m, n2m: the rule-row capacity of the shared stage (the strips of one
+// launch have shorter rows than the tables' stride c.nmax1/2 when the
+// boundary strips go to a second launch)
 template <int P, int TS>
 __global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t* __restrict__ strips, int nstrips,
-                                                      int nu_max, const double* __restrict__ bw1,
+                                                      int n1m, int n2m, int nu_max, const double* __restrict__ bw1,
                                                       const double* __restrict__ bw2, int* __restrict__ status) {
     constexpr int W = 2 * P + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1, NT = TS * 9;
-    extern __shared__ double sm[];
-    const int n1m = c.nmax1, n2m = c.nmax2, SB = strip_b2_stride(P, n2m);
+    extern __shared__ __align__(128) double sm[];       // 16-byte aligned bulk-copy targets
+    const int SB = strip_b2_stride(P, n2m);
+    const StripSmem L(P, n1m, n2m, nu_max, TS);
     double* B1 = sm;                      // [n1m][WP]
-    double* GS = B1 + n1m * WP;           // [n1m][nu]
-    double* X = GS + n1m * nu_max;        // [nu][WPI]
-    double* B2 = X + nu_max * WPI;        // [TS][SB]
+    double* GS = sm + L.gs;               // [n1m][nu]
+    double* X = sm + L.x;                 // [nu][WPI]
+    double* B2 = sm + L.b2;               // [TS][SB]
     __shared__ int s_k0[TS], s_n2[TS], s_st[TS], s_hdr[4];
+    __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x;
     const tq_ruleset R1 = c.sets1[0], R2 = c.sets2[0];
     const double* __restrict__ G = c.grids[0];
-    const int ldG = R2.lay.npts;
+    const int ldG = R2.lay.npts, GL = strip_gs_stride(nu_max);
+    const bool bulk = (ldG & 1) == 0;      // coefficient rows 16-byte aligned: TMA bulk copies
+    unsigned phase = 0;
+    if (tid == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
     for (int s = blockIdx.x; s < nstrips; s += gridDim.x) {
         const int32_t* st = strips + (int64_t)s * (2 + TS);
         const int i1 = st[0], i20 = st[1];
@@ -133,18 +198,37 @@ __global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t
         }
         __syncthreads();
         const int u0 = s_hdr[0], nu = s_hdr[1], k01 = s_hdr[2], n1 = s_hdr[3];
+        const int sh = bulk ? (u0 & 1) : 0;      // GS column of u = 0
         if (n1 > 0) {
-            const double* b1src = bw1 + (int64_t)i1 * n1m * WP;
-            for (int q = tid; q < n1 * WP; q += NT) B1[q] = __ldg(b1src + q);
-            for (int q = tid; q < n1 * nu; q += NT) {
-                const int k = q / nu, u = q - k * nu;
-                GS[q] = __ldg(G + (int64_t)(k01 + k) * ldG + u0 + u);
-            }
-            const int nrow = min(TS, c.n2 - i20);
-            const double* b2src = bw2 + (int64_t)i20 * n2m * WP;
-            for (int q = tid; q < nrow * n2m * WP; q += NT) {
-                const int t = q / (n2m * WP), rem = q - t * (n2m * WP);
-                B2[t * SB + rem] = __ldg(b2src + q);
+            const int nrow = min(TS, c.n2 - i20), R2s = bw_row(P, c.nmax2);
+            const unsigned b1b = 8u * ((n1 * WP + 1) & ~1), b2b = 8u * ((n2m * WP + 1) & ~1);
+            if (bulk) {
+                // one thread arms the barrier and issues every copy of the strip
+                const int ua = u0 & ~1, gl = (sh + nu + 1) & ~1;
+                if (tid == 0) {
+                    fence_proxy_async_shared();       // the previous strip's reads precede these writes
+                    mbar_expect_tx(&s_bar, b1b + nrow * b2b + 8u * n1 * gl);
+                    bulk_g2s(B1, bw1 + (int64_t)i1 * bw_row(P, c.nmax1), b1b, &s_bar);
+                    for (int t = 0; t < nrow; ++t)
+                        bulk_g2s(B2 + t * SB, bw2 + (int64_t)(i20 + t) * R2s, b2b, &s_bar);
+                    for (int k = 0; k < n1; ++k)
+                        bulk_g2s(GS + k * GL, G + (int64_t)(k01 + k) * ldG + ua, 8u * gl, &s_bar);
+                }
+                mbar_wait(&s_bar, phase);
+                phase ^= 1;
+            } else {       // asynchronous copies, all in flight at once
+                const double* b1src = bw1 + (int64_t)i1 * bw_row(P, c.nmax1);
+                for (int q = tid; q < (n1 * WP + 1) / 2; q += NT) cp_async16(B1 + 2 * q, b1src + 2 * q);
+                for (int k = 0; k < n1; ++k) {
+                    const double* grow = G + (int64_t)(k01 + k) * ldG + u0;
+                    for (int u = tid; u < nu; u += NT) cp_async8(GS + k * GL + u, grow + u);
+                }
+                const int h2 = (n2m * WP + 1) / 2;
+                for (int t = 0; t < nrow; ++t) {
+                    const double* src = bw2 + (int64_t)(i20 + t) * R2s;
+                    for (int q = tid; q < h2; q += NT) cp_async16(B2 + t * SB + 2 * q, src + 2 * q);
+                }
+                cp_async_wait_all();
             }
         }
         __syncthreads();
@@ -156,7 +240,7 @@ __global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t
 #pragma unroll
             for (int i = 0; i < BA; ++i) acc[i] = 0.0;
             for (int k1 = 0; k1 < n1; ++k1) {
-                const double g = GS[k1 * nu + u];
+                const double g = GS[k1 * GL + sh + u];
                 const double* b = B1 + k1 * WP + ob * BA;
 #pragma unroll
                 for (int i = 0; i < BA; ++i) acc[i] = fma(b[i], g, acc[i]);
@@ -217,12 +301,15 @@ __global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t
 // ---------------------------------------------------------------------------
 constexpr int kPlTile = 16, kPlThreads = 256;
 
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// the look-back words carry flag and value in one 64-bit word, so relaxed
+// single-copy-atomic accesses suffice (no other data is published with them;
+// an acquire load would invalidate L1 on every spin)
+__device__ __forceinline__ void lb_store(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned v) {
@@ -267,29 +354,31 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
                 jh2 = __ldg(c.ov_hi2 + i2);
             }
             const int si = r - raw_base;
-            for (int o1 = 2 * warp + half; o1 < W; o1 += 2 * NW) {
-                const int j1 = i1 - P + o1;
-                const bool ok1 = have && j1 >= jl1 && j1 <= jh1;
-                const int* colrow = c.col_of + (int64_t)j1 * c.n2 + (i2 - P);
-                int col[W];
+            // entries o = hw, hw + 16, .. of the row (hw = the half-warp's
+            // index): every half-warp gets ceil(T / 16) entries
+            constexpr int NH = 2 * NW, PER = (T + NH - 1) / NH;
+            const int hw = 2 * warp + half;
+            int col[PER];
+            double vi[PER];
 #pragma unroll
-                for (int o2 = 0; o2 < W; ++o2) {
-                    const int j2 = i2 - P + o2;
-                    col[o2] = (ok1 && j2 >= jl2 && j2 <= jh2) ? __ldg(colrow + o2) : -1;
+            for (int k = 0; k < PER; ++k) {
+                const int o = hw + k * NH;
+                const int o1 = o / W, o2 = o - o1 * W;
+                const int j1 = i1 - P + o1, j2 = i2 - P + o2;
+                const bool ok = o < T && have && j1 >= jl1 && j1 <= jh1 && j2 >= jl2 && j2 <= jh2;
+                col[k] = ok ? __ldg(c.col_of + (int64_t)j1 * c.n2 + j2) : -1;
+                vi[k] = ok ? __ldg(raw + (int64_t)o * ld + si) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int o = hw + k * NH;
+                int cl = col[k];
+                double v = 0.0;
+                if (cl >= 0) {
+                    v = __dadd_rn(vi[k], __ldg(raw + (int64_t)(T - 1 - o) * ld + (cl - raw_base)));
+                    if (v == 0.0) cl = -1;
                 }
-                double vi[W];
-#pragma unroll
-                for (int o2 = 0; o2 < W; ++o2)
-                    vi[o2] = col[o2] >= 0 ? __ldg(raw + (int64_t)(o1 * W + o2) * ld + si) : 0.0;
-#pragma unroll
-                for (int o2 = 0; o2 < W; ++o2) {
-                    const int o = o1 * W + o2;
-                    int cl = col[o2];
-                    double v = 0.0;
-                    if (cl >= 0) {
-                        v = __dadd_rn(vi[o2], __ldg(raw + (int64_t)(T - 1 - o) * ld + (cl - raw_base)));
-                        if (v == 0.0) cl = -1;
-                    }
+                if (o < T) {
                     sv[tr * T + o] = 0.5 * v;
                     sc[tr * T + o] = cl;
                 }
@@ -313,7 +402,7 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
                 if (lane >= d) incl += y;
             }
             const int agg = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane == 0) st_release_u64(state + tile, lb_pack(tile == 0 ? 2u : 1u, (unsigned)agg));
+            if (lane == 0) lb_store(state + tile, lb_pack(tile == 0 ? 2u : 1u, (unsigned)agg));
             int excl = 0;
             if (tile > 0) {
                 for (int j = tile - 1;; j -= 32) {
@@ -321,7 +410,7 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
                     unsigned long long w = lb_pack(2u, 0u);
                     if (jj >= 0) {
                         do {
-                            w = ld_acquire_u64(state + jj);
+                            w = lb_load(state + jj);
                         } while ((w >> 32) == 0);
                     }
                     const unsigned inc = __ballot_sync(0xffffffffu, (w >> 32) == 2);
@@ -329,7 +418,7 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
                     excl += __reduce_add_sync(0xffffffffu, lane <= first ? (int)(w & 0xffffffffu) : 0);
                     if (inc) break;
                 }
-                if (lane == 0) st_release_u64(state + tile, lb_pack(2u, (unsigned)(excl + agg)));
+                if (lane == 0) lb_store(state + tile, lb_pack(2u, (unsigned)(excl + agg)));
             }
             if (lane < kPlTile) s_off[lane] = excl + incl - cnt;
             if (tile == nt - 1 && lane == 0) {
@@ -372,41 +461,46 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
 using namespace tq;
 
 template <int P>
-static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t nstrips, int32_t nu_max,
-                            const double* bw1, const double* bw2, int32_t* status, cudaStream_t st) {
-    const size_t shm = sizeof(double) * strip_smem_doubles(P, c.nmax1, c.nmax2, nu_max, kStripRows);
+static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
+                            int32_t nu_max, const double* bw1, const double* bw2, int32_t* status, cudaStream_t st) {
+    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, kStripRows);
     if (shm > 220 * 1024) { set_error("strip workspace too large (%zu bytes)", shm); return TQ_EINVAL; }
     auto kern = k_sf_strips<P, kStripRows>;
     TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int per_sm = 0;
     TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStripRows * 9, shm));
     const int grid = (int)std::min<int64_t>(nstrips, (int64_t)kSms * std::max(per_sm, 1));
-    kern<<<grid, kStripRows * 9, shm, st>>>(c, strips, nstrips, nu_max, bw1, bw2, status);
+    kern<<<grid, kStripRows * 9, shm, st>>>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_sf_strips");
     return TQ_OK;
 }
 
 extern "C" int64_t tq_bw_table_doubles(tq_rawctx c) {
-    const int WP = 3 * ((2 * c.p1 + 3) / 3);
-    return (int64_t)c.n1 * c.nmax1 * WP + (int64_t)c.n2 * c.nmax2 * WP;
+    return (int64_t)c.n1 * bw_row(c.p1, c.nmax1) + (int64_t)c.n2 * bw_row(c.p2, c.nmax2);
 }
 
-// bw: tq_bw_table_doubles(c) doubles of scratch (both directions' tables).
-extern "C" int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips, int32_t nu_max, double* bw,
-                            int32_t* status, void* stream) {
+// the weighted collocation tables of the standard rules (bw: tq_bw_table_doubles)
+extern "C" int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stream) {
+    if (!c.sets1 || !c.sets2 || c.p1 != c.p2) { set_error("tq_bw_tables needs rule sets and p1 == p2"); return TQ_EINVAL; }
+    const int64_t nb = tq_bw_table_doubles(c);
+    if (nb <= 0) return TQ_OK;
+    k_bw_tables<<<grid_for(nb, 256), 256, 0, S(stream)>>>(c, bw, bw + (int64_t)c.n1 * bw_row(c.p1, c.nmax1), status);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_bw_tables");
+    return TQ_OK;
+}
+
+extern "C" int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
+                            int32_t nu_max, const double* bw, int32_t* status, void* stream) {
     if (nstrips <= 0) return TQ_OK;
     if (!c.grids || !c.raw_ld || c.p1 != c.p2) { set_error("tq_sf_strips needs coefficient grids, planes and p1 == p2"); return TQ_EINVAL; }
     if (c.p1 < 1 || c.p1 > kMaxP) { set_error("degree out of range"); return TQ_EINVAL; }
-    cudaStream_t st = S(stream);
-    const int WP = 3 * ((2 * c.p1 + 3) / 3);
-    double* bw1 = bw;
-    double* bw2 = bw + (int64_t)c.n1 * c.nmax1 * WP;
-    const int64_t nb = tq_bw_table_doubles(c);
-    k_bw_tables<<<grid_for(nb, 256), 256, 0, st>>>(c, WP, bw1, bw2, status);
-    ::tq::note_launch();
+    if (n1m > c.nmax1 || n2m > c.nmax2) { set_error("strip capacity above the tables' stride"); return TQ_EINVAL; }
+    const double* bw1 = bw;
+    const double* bw2 = bw + (int64_t)c.n1 * bw_row(c.p1, c.nmax1);
     switch (c.p1) {
-#define CASE(Q) case Q: return sf_strips_launch<Q>(c, strips, nstrips, nu_max, bw1, bw2, status, st);
+#define CASE(Q) case Q: return sf_strips_launch<Q>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status, S(stream));
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     }
