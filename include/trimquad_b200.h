@@ -467,6 +467,19 @@ int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stream);
  * `cap` entries, state tq_planes_state_bytes(nrows) bytes of scratch, ctl 3
  * ints ([1] nnz, [2] flags: 1 = nnz != expect (expect >= 0), 2 = nnz > cap).
  * nnz_h (optional) reads nnz back, synchronising the stream. */
+/* cut rows of the c != 1 planes path, element-centric: element-Gauss blocks
+ * of the listed interior elements (gel: nslot x 2; cgp: c at their (p+1)^2
+ * Gauss points) and span-key group blocks of the cut elements, both in pair
+ * form (q(q+1)/2 x q(q+1)/2 per block: E[(a1,a2)][(b1,b2)] is symmetric in
+ * (a1,b1) and (a2,b2)); then per cut row the sum of the row slices it reads,
+ * written to its planes (gslot: element -> Gauss slot; status |= 4 when a
+ * needed element block is missing).  Replaces _Run.element_block and
+ * _Run.add_cut_blocks (src/assembly.py:310-332, 369-398). */
+int64_t tq_pair_block_doubles(int32_t p);
+int tq_gauss_pairs(tq_rawctx c, const int32_t* gel, int32_t nslot, const double* cgp, double* E, void* stream);
+int tq_cut_pairs(tq_rawctx c, double* E, void* stream);
+int tq_cut_rows_gather(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* gslot, const double* Eg,
+                       const double* Ec, int32_t* status, void* stream);
 int64_t tq_planes_state_bytes(int32_t nrows);
 int tq_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
                   int64_t cap, void* state, int32_t* ctl, int64_t expect, int64_t* nnz_h, void* stream);

@@ -56,6 +56,10 @@ def _bind():
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
     L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
+    L.optional("tq_gauss_pairs", [RawCtx, L.vp, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_cut_pairs", [RawCtx, L.vp, L.vp])
+    L.optional("tq_cut_rows_gather", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp])
+    L.optional("tq_pair_block_doubles", [L.i32], L.i64)
     L.optional("tq_bw_table_doubles", [RawCtx], L.i64)
     L.optional("tq_planes_csr", [L.RowCtx, L.i32, L.vp, L.vp, L.vp, L.i64, L.vp, L.vp, L.i64, L.vp, L.vp])
     L.optional("tq_planes_state_bytes", [L.i32], L.i64)
@@ -445,6 +449,77 @@ def raw_buffer(f, ndesc):
     return torch.empty((max(ndesc, 1), W), dtype=torch.float64, device=f.dev)
 
 
+def pairs_mode(f):
+    """c != 1 planes path whose cut rows are formed element-centric from
+    pair-form element blocks (csrc/cutrows.cu)."""
+    return planes(f) and not f.coeff.identity and f.strategy != "reference"
+
+
+def gauss_elements(f):
+    """Interior elements whose element-Gauss block a row of the plan reads
+    (GAUSS rows: every interior support element; BOX rows: those outside the
+    box) -- geometry of the plan, cached: element list (device, nslot x 2),
+    element -> slot map, and the point gather indices of their Gauss grids."""
+    desc, _ = _plan(f)
+    g = _geo(f.config)
+    key = ("gauss_el", id(desc))
+    if key not in g:
+        b1, b2 = f.b1, f.b2
+        nel1, nel2 = b1.num_elements, b2.num_elements
+        ec = f.config.element_class
+        mark = np.zeros((nel1, nel2), bool)
+        sel = desc[(desc[:, 1] == MODE_GAUSS) | (desc[:, 1] == MODE_BOX)]
+        if sel.shape[0]:
+            i1, i2 = sel[:, 0] // b2.n, sel[:, 0] % b2.n
+            o1, o2 = np.arange(b1.p + 1), np.arange(b2.p + 1)
+            e1 = b1._el_first[i1][:, None, None] + o1[None, :, None]
+            e2 = b2._el_first[i2][:, None, None] + o2[None, None, :]
+            e1, e2 = np.broadcast_arrays(e1, e2)
+            ok = (e1 <= b1._el_last[i1][:, None, None]) & (e2 <= b2._el_last[i2][:, None, None])
+            e1c, e2c = np.minimum(e1, nel1 - 1), np.minimum(e2, nel2 - 1)
+            ok &= ec[e1c, e2c] == INTERIOR
+            box = (sel[:, 1] == MODE_BOX) & (sel[:, 4] >= 0)
+            inbox = (box[:, None, None] & (e1 >= sel[:, 4, None, None]) & (e1 <= sel[:, 5, None, None])
+                     & (e2 >= sel[:, 6, None, None]) & (e2 <= sel[:, 7, None, None]))
+            ok &= ~inbox
+            mark[e1c[ok], e2c[ok]] = True
+        el = np.argwhere(mark).astype(np.int32)        # row-major element order
+        slot = np.full(nel1 * nel2, -1, np.int32)
+        slot[el[:, 0].astype(np.int64) * nel2 + el[:, 1]] = np.arange(el.shape[0], dtype=np.int32)
+        q1, q2 = b1.p + 1, b2.p + 1
+        gi = (el[:, 0].astype(np.int64)[:, None, None] * q1 + np.arange(q1)[None, :, None])
+        gj = (el[:, 1].astype(np.int64)[:, None, None] * q2 + np.arange(q2)[None, None, :])
+        gi, gj = np.broadcast_arrays(gi, gj)
+        g[key] = dict(n=int(el.shape[0]), gel=L.dev(el if el.size else np.zeros((1, 2), np.int32), torch.int32),
+                      gslot=L.dev(slot, torch.int32),
+                      idx1=L.dev(gi.reshape(-1) if el.size else np.zeros(1, np.int64), torch.int64),
+                      idx2=L.dev(gj.reshape(-1) if el.size else np.zeros(1, np.int64), torch.int64))
+    return g[key]
+
+
+def _gauss_pairs(f, eg, em):
+    """Element-Gauss blocks (pair form) of the plan's Gauss elements, with c
+    evaluated at just their Gauss points (current stream)."""
+    ge = gauss_elements(f)
+    npair = int(L.lib().tq_pair_block_doubles(f.b1.p))
+    E = torch.empty(max(ge["n"], 1) * npair, dtype=torch.float64, device=f.dev)
+    if ge["n"]:
+        P = torch.stack([eg[0][3][ge["idx1"]], eg[1][3][ge["idx2"]]], dim=1)
+        cgp = f.coeff.at_device(P)
+        ctx = _gauss_ctx(f, eg, em, None, _desc_dev(f)[0], torch.empty(1, dtype=torch.float64, device=f.dev), 0)
+        L.call("tq_gauss_pairs", ctx, L.ptr(ge["gel"]), ge["n"], L.ptr(cgp), L.ptr(E), L.stream())
+        f._keep_pairs = getattr(f, "_keep_pairs", []) + [P, cgp]
+    return E, ge["gslot"]
+
+
+def _cut_pairs(f, cut):
+    """Span-key group blocks (pair form) of the cut elements (current stream)."""
+    npair = int(L.lib().tq_pair_block_doubles(f.b1.p))
+    E = torch.empty(max(cut["ngroups"], 1) * npair, dtype=torch.float64, device=f.dev)
+    L.call("tq_cut_pairs", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.ptr(E), L.stream())
+    return E
+
+
 class _Setup:
     """Device tables shared by the raw-row kernels of one formation."""
 
@@ -458,7 +533,7 @@ class _Setup:
         # element Gauss tables, (p+1) points (src/assembly.py:198-211);
         # basis values evaluated per formation as in the reference's _Run
         pre = getattr(f, "_elem_pre", None)
-        self.eg, self.em, self.cg = pre if pre is not None else _elem_tables(f)
+        self.eg, self.em, self.cg = pre if pre is not None else _elem_tables(f, with_grid=not pairs_mode(f))
         # rule sets
         self.sets = ([], [])
         self.grids = None
@@ -497,6 +572,7 @@ class _Setup:
                         self.keep.append(g)
                         ptrs[a * len(self.sets[1]) + c] = g.data_ptr()
                 self.grids = L.dev(ptrs.view(np.int64), torch.int64)
+                _st("grids")
         else:
             self.sets_dev = [None, None]
             self.nmax = [1, 1]
@@ -530,7 +606,7 @@ class _Setup:
         return ctx
 
 
-def _elem_tables(f):
+def _elem_tables(f, with_grid=True):
     """Element Gauss tables ((p+1) points, src/assembly.py:198-211), the
     per-element 1-D mass blocks and (c != 1) the coefficient on the Gauss
     grid; basis values evaluated per formation as in the reference's _Run."""
@@ -546,7 +622,7 @@ def _elem_tables(f):
         em.append(m)
     if same:
         eg, em = eg * 2, em * 2
-    cg = None if f.coeff.identity else f.coeff.grid_device(eg[0][3], eg[1][3])
+    cg = None if (f.coeff.identity or not with_grid) else f.coeff.grid_device(eg[0][3], eg[1][3])
     return eg, em, cg
 
 
@@ -591,7 +667,8 @@ def _cut_tables(f):
     return dict(idx=t["idx"], ptr=t["ptr"], cw=cw.contiguous(), f1=f1, v1=v1, f2=f2, v2=v2,
                 npts=t["npts"], grp_ptr=t["grp_ptr"], grp_key=t["grp_key"], grp_pts=t["grp_pts"],
                 grp_perm=t["grp_perm"], ngroups=t["ngroups"],
-                blocks=torch.empty(max(t["ngroups"], 1) * Q * Q, dtype=torch.float64, device=f.dev))
+                blocks=torch.empty(1 if pairs_mode(f) else max(t["ngroups"], 1) * Q * Q, dtype=torch.float64,
+                                   device=f.dev))
 
 
 def _group_range(f, cut):
@@ -657,13 +734,16 @@ def prelaunch_geometry(f):
     # priority of the main chain: the Gauss part gates the cut-row chain (measured best)
     s = _named_stream("cut_blocks", priority=-2)
     main = torch.cuda.current_stream()
+    pm = pairs_mode(f)
     with _forked(main, s):
-        f._elem_pre = eg, em, cg = _elem_tables(f)
+        f._elem_pre = eg, em, cg = _elem_tables(f, with_grid=not pm)
         _st("preA:elem")
         desc_dev, ndesc = _desc_dev(f)
         f._desc_pre = desc_dev
         f._raw_pre = raw_buffer(f, ndesc)
-        if ndesc:
+        if pm:
+            f._gpairs = _gauss_pairs(f, eg, em)
+        elif ndesc:
             L.call("tq_raw_gauss", _gauss_ctx(f, eg, em, cg, desc_dev, f._raw_pre, ndesc), 0, ndesc, L.stream())
         _st("preA:gauss")
         f._elem_event = torch.cuda.Event()
@@ -675,7 +755,10 @@ def prelaunch_geometry(f):
         if f.config.has_cuts():
             cut = _cut_tables(f)
             _st("preB:tables")
-            L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.stream())
+            if pm:
+                f._cpairs = _cut_pairs(f, cut)
+            else:
+                L.call("tq_cut_blocks", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.stream())
         from .assembly import _stamp
         _stamp("cutpre:blocks")
     s.wait_stream(s2)         # one stream to join later
@@ -683,6 +766,8 @@ def prelaunch_geometry(f):
     tensors = [t for t in (cut or {}).values() if isinstance(t, torch.Tensor)]
     tensors += [t for e in eg for t in e if isinstance(t, torch.Tensor)] + list(em) + [f._raw_pre]
     tensors += [cg] if cg is not None else []
+    tensors += list(getattr(f, "_gpairs", ())) + ([f._cpairs] if getattr(f, "_cpairs", None) is not None else [])
+    tensors += getattr(f, "_keep_pairs", [])
     for st in (main, _side_streams(1)[0]):
         _keep_on(st, tensors)
     f._cut_pre = cut
@@ -936,6 +1021,7 @@ def run_phase(f, phase):
                                                           f._setup.sets[1][0].layout):
                 L.call("tq_sf_strips", ctx_int, L.ptr(strips), ns, n1m, n2m, nu, L.ptr(f._bw),
                        L.ptr(f._planes_status), L.stream())
+                _st(f"strips{n2m}")
         elif nint:
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)
@@ -945,6 +1031,25 @@ def run_phase(f, phase):
             ctx_int.nmax1, ctx_int.nmax2 = f._setup.nmax_std
             f._ctx_int = ctx_int
             L.call("tq_raw_sumfactor" if pre is not None else "tq_raw_regular", ctx_int, 0, nint, L.stream())
+    elif phase == "cut" and pairs_mode(f):
+        if f._ndesc > f._nint:
+            pre = getattr(f, "_raw_pre", None) is not None
+            if pre:
+                torch.cuda.current_stream().wait_event(f._elem_event)
+                join_cut_blocks(f)
+                Eg, gslot = f._gpairs
+                Ec = getattr(f, "_cpairs", None)
+            else:
+                Eg, gslot = _gauss_pairs(f, f._setup.eg, f._setup.em)
+                Ec = _cut_pairs(f, f._setup.cut) if f._setup.cut is not None else None
+                f._eager_pairs = (Eg, Ec)
+            if getattr(f, "_planes_status", None) is None:
+                f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
+            L.call("tq_cut_rows_gather", f._ctx, f._nint, f._ndesc, L.ptr(gslot), L.ptr(Eg), L.ptr(Ec),
+                   L.ptr(f._planes_status), L.stream())
+            L.call("tq_raw_sumfactor", f._ctx, f._nint, f._ndesc, L.stream())
+    elif phase == "cutcells" and pairs_mode(f):
+        pass          # in the cut phase (tq_cut_rows_gather)
     elif phase == "cut":
         if f._ndesc > f._nint:
             pre = getattr(f, "_raw_pre", None) is not None

@@ -556,7 +556,8 @@ class Formation:
             torch.cuda.current_stream().wait_stream(st)
         st = getattr(self, "_planes_status", None)
         if st is not None and self.capture is None and int(st.item()):
-            raise RuntimeError("strip workspace bound exceeded (tq_sf_strips)")
+            raise RuntimeError(f"planes path status {int(st.item())}: a strip workspace bound (1, 2) or an element "
+                               "block (4) missed")
         _stamp("fill")
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
@@ -701,7 +702,7 @@ class GraphFormation:
                 raise RuntimeError("replayed pass formed a different nnz than the captured one")
             st = getattr(self.f, "_planes_status", None)
             if st is not None and int(st.item()):
-                raise RuntimeError("strip workspace bound exceeded (tq_sf_strips)")
+                raise RuntimeError("planes path status word set in a replayed pass (tq_sf_strips / tq_cut_rows_gather)")
         elif int(self.f._count_bufs[1][L.tile_ctl(self.f._nrows) + 4].item()):
             raise RuntimeError("replayed pass formed a different nnz than the captured one")
 

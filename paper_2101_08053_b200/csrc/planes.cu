@@ -85,16 +85,17 @@ __host__ __device__ inline int strip_b2_stride(int p, int n2m) {
 // slot of slack for an odd first column
 __host__ __device__ inline int strip_gs_stride(int nu_max) { return (nu_max + 3) & ~1; }
 
-// shared stage offsets (doubles): B1 | GS | X | B2; the 16-byte copy
-// targets (B1, B2) start at even offsets
+// shared stage offsets (doubles): two buffers of B1 | GS | B2, then X; the
+// 16-byte copy targets start at even offsets
 struct StripSmem {
-    int gs, x, b2, total;
+    int gs, b2, buf, x, total;
     __host__ __device__ StripSmem(int p, int n1m, int n2m, int nu_max, int ts) {
         const int WP = bw_wp(p), WPI = WP | 1;
         gs = (n1m * WP + 1) & ~1;
-        x = gs + n1m * strip_gs_stride(nu_max);
-        b2 = (x + nu_max * WPI + 1) & ~1;
-        total = b2 + ts * strip_b2_stride(p, n2m);
+        b2 = gs + n1m * strip_gs_stride(nu_max);
+        buf = b2 + ts * strip_b2_stride(p, n2m);
+        x = 2 * buf;
+        total = x + nu_max * WPI;
     }
 };
 
@@ -134,132 +135,158 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
                  ::"r"(sptr(sdst)), "l"(gsrc), "r"(bytes), "r"(sptr(b)) : "memory");
 }
 
-// n1m, n2m: the rule-row capacity of the shared stage (the strips of one
+// mbarrier arrive (no transaction bytes)
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(b)) : "memory");
+}
+// named barrier of the consumer warps
+__device__ __forceinline__ void consumers_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+
+template <int TS>
+struct StripHdr {
+    int k0[TS], n2[TS], st[TS];
+    int i1, i20, u0, nu, k01, n1, sh, pad;
+};
+
+// Warp-specialised and double-buffered: warp CW (the producer) reads strip
+// s + 2G's header while the consumer warps 0..CW-1 compute strip s, and
+// stages it (TMA bulk copies of the B1 / B2 table rows and the coefficient
+// rows) into the free buffer; full[b] / empty[b] mbarriers hand the buffers
+// over.  n1m, n2m: the rule-row capacity of the stage (the strips of one
 // launch have shorter rows than the tables' stride c.nmax1/2 when the
-// boundary strips go to a second launch)
+// boundary strips go to a second launch).
 template <int P, int TS>
-__global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t* __restrict__ strips, int nstrips,
-                                                      int n1m, int n2m, int nu_max, const double* __restrict__ bw1,
-                                                      const double* __restrict__ bw2, int* __restrict__ status) {
-    constexpr int W = 2 * P + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1, NT = TS * 9;
+__global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
+    tq_rawctx c, const int32_t* __restrict__ strips, int nstrips, int n1m, int n2m, int nu_max,
+    const double* __restrict__ bw1, const double* __restrict__ bw2, int* __restrict__ status) {
+    constexpr int W = 2 * P + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1, NB = TS * 9;
+    constexpr int CW = (NB + 31) / 32, NC = 32 * CW;      // consumer warps / threads
     extern __shared__ __align__(128) double sm[];       // 16-byte aligned bulk-copy targets
-    const int SB = strip_b2_stride(P, n2m);
     const StripSmem L(P, n1m, n2m, nu_max, TS);
-    double* B1 = sm;                      // [n1m][WP]
-    double* GS = sm + L.gs;               // [n1m][nu]
+    const int SB = strip_b2_stride(P, n2m), GL = strip_gs_stride(nu_max);
     double* X = sm + L.x;                 // [nu][WPI]
-    double* B2 = sm + L.b2;               // [TS][SB]
-    __shared__ int s_k0[TS], s_n2[TS], s_st[TS], s_hdr[4];
-    __shared__ __align__(8) uint64_t s_bar;
-    const int tid = threadIdx.x;
+    __shared__ StripHdr<TS> H[2];
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const tq_ruleset R1 = c.sets1[0], R2 = c.sets2[0];
     const double* __restrict__ G = c.grids[0];
-    const int ldG = R2.lay.npts, GL = strip_gs_stride(nu_max);
-    const bool bulk = (ldG & 1) == 0;      // coefficient rows 16-byte aligned: TMA bulk copies
-    unsigned phase = 0;
-    if (tid == 0) mbar_init(&s_bar, 1);
+    const int ldG = R2.lay.npts;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], 1);
+        mbar_init(&empty[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
-    for (int s = blockIdx.x; s < nstrips; s += gridDim.x) {
-        const int32_t* st = strips + (int64_t)s * (2 + TS);
-        const int i1 = st[0], i20 = st[1];
-        if (tid < TS) {
-            const int sidx = st[2 + tid];
-            int k0 = -1, n2 = 0;
-            if (sidx >= 0) {
-                const int i2 = i20 + tid;
-                k0 = R2.rules.k0[i2];
-                n2 = k0 >= 0 ? (int)(R2.rules.wptr[i2 + 1] - R2.rules.wptr[i2]) : 0;
-            }
-            s_k0[tid] = k0;
-            s_n2[tid] = n2;
-            s_st[tid] = sidx;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int u0 = INT_MAX, u1 = INT_MIN, bad = 0;
-            for (int t = 0; t < TS; ++t)
-                if (s_n2[t] > 0) {
-                    u0 = min(u0, s_k0[t]);
-                    u1 = max(u1, s_k0[t] + s_n2[t]);
-                    bad |= s_n2[t] > n2m;
+    if (warp == CW) {
+        // ---------------- producer
+        const bool bulk = (ldG & 1) == 0;     // coefficient rows 16-byte aligned
+        for (int it = 0, s = blockIdx.x; s < nstrips; s += gridDim.x, ++it) {
+            const int b = it & 1;
+            if (it >= 2) mbar_wait(&empty[b], ((it >> 1) & 1) ^ 1);
+            StripHdr<TS>& h = H[b];
+            const int32_t* st = strips + (int64_t)s * (2 + TS);
+            const int i1 = st[0], i20 = st[1];
+            int k0 = -1, n2 = 0, sidx = -1;
+            if (lane < TS) {
+                sidx = st[2 + lane];
+                if (sidx >= 0) {
+                    const int i2 = i20 + lane;
+                    k0 = R2.rules.k0[i2];
+                    n2 = k0 >= 0 ? (int)(R2.rules.wptr[i2 + 1] - R2.rules.wptr[i2]) : 0;
                 }
+                h.k0[lane] = k0;
+                h.n2[lane] = n2;
+                h.st[lane] = sidx;
+            }
+            int lo = n2 > 0 ? k0 : INT_MAX, hi = n2 > 0 ? k0 + n2 : INT_MIN, bad = n2 > n2m;
+            lo = __reduce_min_sync(0xffffffffu, lo);
+            hi = __reduce_max_sync(0xffffffffu, hi);
+            bad = __reduce_or_sync(0xffffffffu, bad);
             const int k01 = R1.rules.k0[i1];
             int n1 = k01 >= 0 ? (int)(R1.rules.wptr[i1 + 1] - R1.rules.wptr[i1]) : 0;
-            int nu = u1 > u0 ? u1 - u0 : 0;
+            int nu = hi > lo ? hi - lo : 0;
             if (nu > nu_max || n1 > n1m || bad) {      // workspace bound broken: flagged, never silent
-                atomicOr(status, 1);
+                if (lane == 0) atomicOr(status, 1);
                 nu = 0;
             }
             if (nu == 0) n1 = 0;
-            s_hdr[0] = u0;
-            s_hdr[1] = nu;
-            s_hdr[2] = k01;
-            s_hdr[3] = n1;
-        }
-        __syncthreads();
-        const int u0 = s_hdr[0], nu = s_hdr[1], k01 = s_hdr[2], n1 = s_hdr[3];
-        const int sh = bulk ? (u0 & 1) : 0;      // GS column of u = 0
-        if (n1 > 0) {
-            const int nrow = min(TS, c.n2 - i20), R2s = bw_row(P, c.nmax2);
-            const unsigned b1b = 8u * ((n1 * WP + 1) & ~1), b2b = 8u * ((n2m * WP + 1) & ~1);
-            if (bulk) {
-                // one thread arms the barrier and issues every copy of the strip
-                const int ua = u0 & ~1, gl = (sh + nu + 1) & ~1;
-                if (tid == 0) {
-                    fence_proxy_async_shared();       // the previous strip's reads precede these writes
-                    mbar_expect_tx(&s_bar, b1b + nrow * b2b + 8u * n1 * gl);
-                    bulk_g2s(B1, bw1 + (int64_t)i1 * bw_row(P, c.nmax1), b1b, &s_bar);
-                    for (int t = 0; t < nrow; ++t)
-                        bulk_g2s(B2 + t * SB, bw2 + (int64_t)(i20 + t) * R2s, b2b, &s_bar);
-                    for (int k = 0; k < n1; ++k)
-                        bulk_g2s(GS + k * GL, G + (int64_t)(k01 + k) * ldG + ua, 8u * gl, &s_bar);
-                }
-                mbar_wait(&s_bar, phase);
-                phase ^= 1;
-            } else {       // asynchronous copies, all in flight at once
-                const double* b1src = bw1 + (int64_t)i1 * bw_row(P, c.nmax1);
-                for (int q = tid; q < (n1 * WP + 1) / 2; q += NT) cp_async16(B1 + 2 * q, b1src + 2 * q);
-                for (int k = 0; k < n1; ++k) {
-                    const double* grow = G + (int64_t)(k01 + k) * ldG + u0;
-                    for (int u = tid; u < nu; u += NT) cp_async8(GS + k * GL + u, grow + u);
-                }
-                const int h2 = (n2m * WP + 1) / 2;
-                for (int t = 0; t < nrow; ++t) {
-                    const double* src = bw2 + (int64_t)(i20 + t) * R2s;
-                    for (int q = tid; q < h2; q += NT) cp_async16(B2 + t * SB + 2 * q, src + 2 * q);
-                }
-                cp_async_wait_all();
+            const int sh = bulk ? (lo & 1) : 0;
+            double* B1 = sm + b * L.buf;
+            double* GS = B1 + L.gs;
+            double* B2 = B1 + L.b2;
+            if (n1 > 0 && !bulk) {        // odd grid stride: the coefficient rows through registers
+                for (int k = 0; k < n1; ++k)
+                    for (int u = lane; u < nu; u += 32) GS[k * GL + u] = __ldg(G + (int64_t)(k01 + k) * ldG + lo + u);
+                __threadfence_block();
             }
+            __syncwarp();
+            if (lane == 0) {
+                h.i1 = i1;
+                h.i20 = i20;
+                h.u0 = lo;
+                h.nu = nu;
+                h.k01 = k01;
+                h.n1 = n1;
+                h.sh = sh;
+                if (n1 > 0) {
+                    const int nrow = min(TS, c.n2 - i20), R2s = bw_row(P, c.nmax2);
+                    const unsigned b1b = 8u * ((n1 * WP + 1) & ~1), b2b = 8u * ((n2m * WP + 1) & ~1);
+                    const int ua = lo & ~1, gl = (sh + nu + 1) & ~1;
+                    fence_proxy_async_shared();       // the buffer's earlier reads precede these writes
+                    mbar_expect_tx(&full[b], b1b + nrow * b2b + (bulk ? 8u * n1 * gl : 0u));
+                    bulk_g2s(B1, bw1 + (int64_t)i1 * bw_row(P, c.nmax1), b1b, &full[b]);
+                    for (int t = 0; t < nrow; ++t)
+                        bulk_g2s(B2 + t * SB, bw2 + (int64_t)(i20 + t) * R2s, b2b, &full[b]);
+                    if (bulk)
+                        for (int k = 0; k < n1; ++k)
+                            bulk_g2s(GS + k * GL, G + (int64_t)(k01 + k) * ldG + ua, 8u * gl, &full[b]);
+                } else {
+                    mbar_arrive(&full[b]);
+                }
+            }
+            __syncwarp();
         }
-        __syncthreads();
+        return;
+    }
+    // ---------------- consumers
+    for (int it = 0, s = blockIdx.x; s < nstrips; s += gridDim.x, ++it) {
+        const int b = it & 1;
+        mbar_wait(&full[b], (it >> 1) & 1);
+        const StripHdr<TS>& h = H[b];
+        const double* B1 = sm + b * L.buf;
+        const double* GS = B1 + L.gs;
+        const double* B2 = B1 + L.b2;
+        const int u0 = h.u0, nu = h.nu, n1 = h.n1, sh = h.sh;
         // stage A: lanes run over u (conflict-free column reads of GS; the B1
         // reads broadcast)
-        for (int q = tid; q < 3 * nu; q += NT) {
+        for (int q = tid; q < 3 * nu; q += NC) {
             const int ob = q / nu, u = q - ob * nu;
             double acc[BA];
 #pragma unroll
             for (int i = 0; i < BA; ++i) acc[i] = 0.0;
             for (int k1 = 0; k1 < n1; ++k1) {
                 const double g = GS[k1 * GL + sh + u];
-                const double* b = B1 + k1 * WP + ob * BA;
+                const double* bb = B1 + k1 * WP + ob * BA;
 #pragma unroll
-                for (int i = 0; i < BA; ++i) acc[i] = fma(b[i], g, acc[i]);
+                for (int i = 0; i < BA; ++i) acc[i] = fma(bb[i], g, acc[i]);
             }
 #pragma unroll
             for (int i = 0; i < BA; ++i) X[u * WPI + ob * BA + i] = acc[i];
         }
-        __syncthreads();
+        consumers_sync(NC);
         // stage B: thread (t = lane row, a, b) owns rows a*BA.., columns b*BA.. of row t
-        {
-            const int t = tid % TS, ab = tid / TS, a = ab / 3, b = ab - a * 3;
-            const int n2 = n1 > 0 ? s_n2[t] : 0, sidx = s_st[t];
+        if (tid < NB) {
+            const int t = tid % TS, ab = tid / TS, a = ab / 3, bq = ab - a * 3;
+            const int n2 = n1 > 0 ? h.n2[t] : 0, sidx = h.st[t];
             double acc[BA][BA];
 #pragma unroll
             for (int i = 0; i < BA; ++i)
 #pragma unroll
                 for (int j = 0; j < BA; ++j) acc[i][j] = 0.0;
-            const double* x = X + (n2 > 0 ? s_k0[t] - u0 : 0) * WPI + a * BA;
-            const double* y = B2 + t * SB + b * BA;
+            const double* x = X + (n2 > 0 ? h.k0[t] - u0 : 0) * WPI + a * BA;
+            const double* y = B2 + t * SB + bq * BA;
             for (int kk = 0; kk < n2; ++kk) {
                 double xv[BA], yv[BA];
 #pragma unroll
@@ -278,12 +305,13 @@ __global__ void __launch_bounds__(TS * 9) k_sf_strips(tq_rawctx c, const int32_t
                 for (int i = 0; i < BA; ++i)
 #pragma unroll
                     for (int j = 0; j < BA; ++j) {
-                        const int o1 = a * BA + i, o2 = b * BA + j;
+                        const int o1 = a * BA + i, o2 = bq * BA + j;
                         if (o1 < W && o2 < W) dst[(int64_t)(o1 * W + o2) * c.raw_ld] = acc[i][j];
                     }
             }
         }
-        __syncthreads();
+        consumers_sync(NC);          // X and buffer b are free
+        if (tid == 0) mbar_arrive(&empty[b]);
     }
 }
 
@@ -319,7 +347,7 @@ __device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned v)
 __device__ __forceinline__ int pl_row_of(const tq_rowctx& c, int idx) { return idx / c.n2; }
 
 template <int P>
-__global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* __restrict__ indptr,
+__global__ void __launch_bounds__(kPlThreads, 4) k_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* __restrict__ indptr,
                                                             int32_t* __restrict__ indices, double* __restrict__ data,
                                                             int64_t cap, unsigned long long* __restrict__ state,
                                                             int32_t* __restrict__ ctl, int64_t expect) {
@@ -355,32 +383,41 @@ __global__ void __launch_bounds__(kPlThreads) k_planes_csr(tq_rowctx c, int32_t 
             }
             const int si = r - raw_base;
             // entries o = hw, hw + 16, .. of the row (hw = the half-warp's
-            // index): every half-warp gets ceil(T / 16) entries
-            constexpr int NH = 2 * NW, PER = (T + NH - 1) / NH;
+            // index): every half-warp gets ceil(T / 16) entries, loaded in
+            // chunks of CH (column loads, then the partners' values)
+            constexpr int NH = 2 * NW, PER = (T + NH - 1) / NH, CH = 8;
             const int hw = 2 * warp + half;
-            int col[PER];
-            double vi[PER];
+            // window-offset bounds of this row (j in the overlap range)
+            const int o1lo = jl1 - i1 + P, o1hi = jh1 - i1 + P, o2lo = jl2 - i2 + P, o2hi = jh2 - i2 + P;
+            const int* colbase = c.col_of + ((int64_t)(i1 - P) * c.n2 + (i2 - P));
+            const double* own = raw + si;
+            const double* part = raw + (int64_t)(T - 1) * ld - raw_base;
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                const int o = hw + k * NH;
-                const int o1 = o / W, o2 = o - o1 * W;
-                const int j1 = i1 - P + o1, j2 = i2 - P + o2;
-                const bool ok = o < T && have && j1 >= jl1 && j1 <= jh1 && j2 >= jl2 && j2 <= jh2;
-                col[k] = ok ? __ldg(c.col_of + (int64_t)j1 * c.n2 + j2) : -1;
-                vi[k] = ok ? __ldg(raw + (int64_t)o * ld + si) : 0.0;
-            }
+            for (int k0 = 0; k0 < PER; k0 += CH) {
+                int col[CH];
+                double vi[CH];
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                const int o = hw + k * NH;
-                int cl = col[k];
-                double v = 0.0;
-                if (cl >= 0) {
-                    v = __dadd_rn(vi[k], __ldg(raw + (int64_t)(T - 1 - o) * ld + (cl - raw_base)));
-                    if (v == 0.0) cl = -1;
+                for (int k = 0; k < CH; ++k) {
+                    const int o = hw + (k0 + k) * NH;
+                    const int o1 = o / W, o2 = o - o1 * W;
+                    const bool ok = k0 + k < PER && o < T && have && o1 >= o1lo && o1 <= o1hi && o2 >= o2lo &&
+                                    o2 <= o2hi;
+                    col[k] = ok ? __ldg(colbase + o1 * c.n2 + o2) : -1;
+                    vi[k] = ok ? __ldg(own + (int64_t)o * ld) : 0.0;
                 }
-                if (o < T) {
-                    sv[tr * T + o] = 0.5 * v;
-                    sc[tr * T + o] = cl;
+#pragma unroll
+                for (int k = 0; k < CH; ++k) {
+                    const int o = hw + (k0 + k) * NH;
+                    int cl = col[k];
+                    double v = 0.0;
+                    if (cl >= 0) {
+                        v = __dadd_rn(vi[k], __ldg(part - (int64_t)o * ld + cl));
+                        if (v == 0.0) cl = -1;
+                    }
+                    if (k0 + k < PER && o < T) {
+                        sv[tr * T + o] = 0.5 * v;
+                        sc[tr * T + o] = cl;
+                    }
                 }
             }
         }
@@ -466,11 +503,13 @@ static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t n
     const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, kStripRows);
     if (shm > 220 * 1024) { set_error("strip workspace too large (%zu bytes)", shm); return TQ_EINVAL; }
     auto kern = k_sf_strips<P, kStripRows>;
+    constexpr int NT = 32 * ((kStripRows * 9 + 31) / 32) + 32;
     TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int per_sm = 0;
-    TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStripRows * 9, shm));
-    const int grid = (int)std::min<int64_t>(nstrips, (int64_t)kSms * std::max(per_sm, 1));
-    kern<<<grid, kStripRows * 9, shm, st>>>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status);
+    TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, shm));
+    // at least two strips per block (the producer runs one strip ahead)
+    const int grid = (int)std::min<int64_t>((nstrips + 1) / 2, (int64_t)kSms * std::max(per_sm, 1));
+    kern<<<grid, NT, shm, st>>>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_sf_strips");
     return TQ_OK;
