@@ -472,14 +472,23 @@ int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stream);
  * Gauss points) and span-key group blocks of the cut elements, both in pair
  * form (q(q+1)/2 x q(q+1)/2 per block: E[(a1,a2)][(b1,b2)] is symmetric in
  * (a1,b1) and (a2,b2)); then per cut row the sum of the row slices it reads,
- * written to its planes (gslot: element -> Gauss slot; status |= 4 when a
- * needed element block is missing).  Replaces _Run.element_block and
+ * written to its planes (gslot: element -> Gauss slot; rg_ptr / rg: the
+ * rows' span-key groups, 3 ints each = group, key1, key2; status |= 4 when
+ * a needed element block is missing).  c of the Gauss blocks: det J computed in the kernel for a
+ * geometry map (X1/X2: element Gauss points), else cgp at their points.  Replaces _Run.element_block and
  * _Run.add_cut_blocks (src/assembly.py:310-332, 369-398). */
 int64_t tq_pair_block_doubles(int32_t p);
-int tq_gauss_pairs(tq_rawctx c, const int32_t* gel, int32_t nslot, const double* cgp, double* E, void* stream);
-int tq_cut_pairs(tq_rawctx c, double* E, void* stream);
+int tq_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* X1, const double* X2, const int32_t* gel,
+                   int32_t nslot, const double* cgp, double* E, void* stream);
+/* the group blocks by pieces of at most tq_cut_pair_piece() points (pieces:
+ * npieces x 2 int64 = group, first point; gpiece: ngroups + 1 offsets;
+ * Epart: npieces blocks of scratch), summed per group in piece order */
+int32_t tq_cut_pair_piece(void);
+int tq_cut_pairs(tq_rawctx c, const int64_t* pieces, int32_t npieces, const int32_t* gpiece, double* Epart,
+                 double* E, void* stream);
 int tq_cut_rows_gather(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* gslot, const double* Eg,
-                       const double* Ec, int32_t* status, void* stream);
+                       const double* Ec, const int32_t* rg_ptr, const int32_t* rg, int32_t* status,
+                       void* stream);
 int64_t tq_planes_state_bytes(int32_t nrows);
 int tq_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
                   int64_t cap, void* state, int32_t* ctl, int64_t expect, int64_t* nnz_h, void* stream);

@@ -56,9 +56,10 @@ def _bind():
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
     L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
-    L.optional("tq_gauss_pairs", [RawCtx, L.vp, L.i32, L.vp, L.vp, L.vp])
-    L.optional("tq_cut_pairs", [RawCtx, L.vp, L.vp])
-    L.optional("tq_cut_rows_gather", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp])
+    L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_cut_pairs", [RawCtx, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp])
+    L.optional("tq_cut_pair_piece", [], L.i32)
+    L.optional("tq_cut_rows_gather", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp])
     L.optional("tq_pair_block_doubles", [L.i32], L.i64)
     L.optional("tq_bw_table_doubles", [RawCtx], L.i64)
     L.optional("tq_planes_csr", [L.RowCtx, L.i32, L.vp, L.vp, L.vp, L.i64, L.vp, L.vp, L.i64, L.vp, L.vp])
@@ -452,7 +453,7 @@ def raw_buffer(f, ndesc):
 def pairs_mode(f):
     """c != 1 planes path whose cut rows are formed element-centric from
     pair-form element blocks (csrc/cutrows.cu)."""
-    return planes(f) and not f.coeff.identity and f.strategy != "reference"
+    return planes(f) and not f.coeff.identity and f.strategy != "reference" and f.b1.p <= 8
 
 
 def gauss_elements(f):
@@ -498,25 +499,105 @@ def gauss_elements(f):
 
 
 def _gauss_pairs(f, eg, em):
-    """Element-Gauss blocks (pair form) of the plan's Gauss elements, with c
-    evaluated at just their Gauss points (current stream)."""
+    """Element-Gauss blocks (pair form) of the plan's Gauss elements on the
+    current stream; c = det J computed in the kernel for a geometry map,
+    else evaluated at just their Gauss points."""
+    from .assembly import GeometryMap
     ge = gauss_elements(f)
     npair = int(L.lib().tq_pair_block_doubles(f.b1.p))
     E = torch.empty(max(ge["n"], 1) * npair, dtype=torch.float64, device=f.dev)
     if ge["n"]:
-        P = torch.stack([eg[0][3][ge["idx1"]], eg[1][3][ge["idx2"]]], dim=1)
-        cgp = f.coeff.at_device(P)
         ctx = _gauss_ctx(f, eg, em, None, _desc_dev(f)[0], torch.empty(1, dtype=torch.float64, device=f.dev), 0)
-        L.call("tq_gauss_pairs", ctx, L.ptr(ge["gel"]), ge["n"], L.ptr(cgp), L.ptr(E), L.stream())
-        f._keep_pairs = getattr(f, "_keep_pairs", []) + [P, cgp]
+        dev = getattr(f.coeff, "_device", None) or f.coeff
+        if isinstance(dev, GeometryMap):
+            geo, cgp = dev.device(), None
+        else:
+            P = torch.stack([eg[0][3][ge["idx1"]], eg[1][3][ge["idx2"]]], dim=1)
+            geo, cgp = L.Coeff(), f.coeff.at_device(P)
+            f._keep_pairs = getattr(f, "_keep_pairs", []) + [P, cgp]
+        L.call("tq_gauss_pairs", ctx, geo, L.ptr(eg[0][3]), L.ptr(eg[1][3]), L.ptr(ge["gel"]), ge["n"], L.ptr(cgp),
+               L.ptr(E), L.stream())
     return E, ge["gslot"]
+
+
+def _cut_pieces(f, cut):
+    """Pieces of the span-key groups for tq_cut_pairs (geometry, cached with
+    the cut-point tables): (pieces npieces x 2 int64, gpiece int32, npieces)."""
+    t = cut_point_tables(f)
+    if "pieces" not in t:
+        kp = int(L.lib().tq_cut_pair_piece())
+        gp = t["grp_pts"]
+        ng = t["ngroups"]
+        lens = gp[1:] - gp[:-1]
+        npc = (lens + kp - 1) // kp
+        gpiece = torch.zeros(ng + 1, dtype=torch.int64, device=f.dev)
+        gpiece[1:] = torch.cumsum(npc, 0)
+        npieces = int(gpiece[-1].item()) if ng else 0
+        grp = torch.repeat_interleave(torch.arange(ng, device=f.dev), npc)
+        within = torch.arange(npieces, device=f.dev) - gpiece[:-1][grp]
+        pieces = torch.stack([grp, gp[:-1][grp] + kp * within], dim=1).contiguous()
+        t["pieces"] = (pieces if npieces else torch.zeros((1, 2), dtype=torch.int64, device=f.dev),
+                       gpiece.to(torch.int32), npieces)
+    return t["pieces"]
+
+
+def cut_row_groups(f, r0, r1):
+    """Span-key groups each cut row [r0, r1) of the plan reads (cut elements
+    within one element of its support, groups in element / key order, key
+    within the row's reach) -- geometry, cached: (rg_ptr, rg) device int32."""
+    desc, _ = _plan(f)
+    t = cut_point_tables(f)
+    g = _geo(f.config)
+    key = ("row_groups", id(desc), id(t), r0, r1)
+    if key not in g:
+        b1, b2 = f.b1, f.b2
+        nel1, nel2 = b1.num_elements, b2.num_elements
+        if "host" not in t:
+            t["host"] = (t["idx"].cpu().numpy(), t["grp_ptr"].cpu().numpy().astype(np.int64),
+                         t["grp_key"].cpu().numpy())
+        cutidx, gptr, gkey = t["host"]
+        fid = desc[r0:r1, 0].astype(np.int64)
+        i1, i2 = fid // b2.n, fid % b2.n
+        ea1 = np.maximum(b1._el_first[i1] - 1, 0)
+        eb1 = np.minimum(b1._el_last[i1] + 1, nel1 - 1)
+        ea2 = np.maximum(b2._el_first[i2] - 1, 0)
+        eb2 = np.minimum(b2._el_last[i2] + 1, nel2 - 1)
+        w1 = int(np.max(eb1 - ea1 + 1)) if fid.size else 0
+        w2 = int(np.max(eb2 - ea2 + 1)) if fid.size else 0
+        e1 = ea1[:, None, None] + np.arange(w1)[None, :, None]
+        e2 = ea2[:, None, None] + np.arange(w2)[None, None, :]
+        e1, e2 = np.broadcast_arrays(e1, e2)
+        ok = (e1 <= eb1[:, None, None]) & (e2 <= eb2[:, None, None])
+        row = np.broadcast_to(np.arange(fid.size)[:, None, None], e1.shape)[ok]
+        cid = cutidx[np.minimum(e1, nel1 - 1)[ok].astype(np.int64) * nel2 + np.minimum(e2, nel2 - 1)[ok]]
+        row, cid = row[cid >= 0], cid[cid >= 0]
+        cnt = gptr[cid + 1] - gptr[cid]
+        rrow = np.repeat(row, cnt)
+        start = np.repeat(gptr[cid], cnt)
+        off = np.arange(rrow.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        grp = (start + off).astype(np.int64)
+        k1, k2 = gkey[grp, 0], gkey[grp, 1]
+        a1, a2 = i1[rrow] - k1, i2[rrow] - k2
+        keep = (a1 >= 0) & (a1 <= b1.p) & (a2 >= 0) & (a2 <= b2.p)
+        rrow, grp, k1, k2 = rrow[keep], grp[keep], k1[keep], k2[keep]
+        rg_ptr = np.zeros(fid.size + 1, np.int32)
+        rg_ptr[1:] = np.cumsum(np.bincount(rrow, minlength=fid.size))
+        rg = np.stack([grp, k1, k2], axis=1).astype(np.int32)
+        g[key] = (L.dev(rg_ptr, torch.int32), L.dev(rg if rg.size else np.zeros((1, 3), np.int32), torch.int32))
+        g[key + ("keep",)] = t
+    return g[key]
 
 
 def _cut_pairs(f, cut):
     """Span-key group blocks (pair form) of the cut elements (current stream)."""
     npair = int(L.lib().tq_pair_block_doubles(f.b1.p))
     E = torch.empty(max(cut["ngroups"], 1) * npair, dtype=torch.float64, device=f.dev)
-    L.call("tq_cut_pairs", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.ptr(E), L.stream())
+    pieces, gpiece, npieces = _cut_pieces(f, cut)
+    if cut["ngroups"]:
+        part = torch.empty(max(npieces, 1) * npair, dtype=torch.float64, device=f.dev)
+        L.call("tq_cut_pairs", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.ptr(pieces), npieces,
+               L.ptr(gpiece), L.ptr(part), L.ptr(E), L.stream())
+        f._keep_pairs = getattr(f, "_keep_pairs", []) + [part]
     return E
 
 
@@ -1045,8 +1126,10 @@ def run_phase(f, phase):
                 f._eager_pairs = (Eg, Ec)
             if getattr(f, "_planes_status", None) is None:
                 f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
+            rg_ptr, rg = (cut_row_groups(f, f._nint, f._ndesc) if Ec is not None
+                          else (None, None))
             L.call("tq_cut_rows_gather", f._ctx, f._nint, f._ndesc, L.ptr(gslot), L.ptr(Eg), L.ptr(Ec),
-                   L.ptr(f._planes_status), L.stream())
+                   L.ptr(rg_ptr), L.ptr(rg), L.ptr(f._planes_status), L.stream())
             L.call("tq_raw_sumfactor", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells" and pairs_mode(f):
         pass          # in the cut phase (tq_cut_rows_gather)

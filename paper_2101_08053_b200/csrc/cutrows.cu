@@ -15,6 +15,8 @@
 // and tq_cut_rows_gather sums, per cut row, the row slices of the blocks it
 // reads into a shared row block and writes the row's planes once (the WQ
 // sum-factorization part of BOX / MASK rows is added afterwards).
+#include <limits.h>
+
 #include "common.cuh"
 
 namespace tq {
@@ -42,61 +44,171 @@ __device__ __forceinline__ void pair_tables(int* pa, int* pb) {
 
 // ---------------------------------------------------------------------------
 // Element-Gauss blocks of the listed interior elements (q = ng = p + 1).
-// cgp: c at the elements' Gauss grids, [slot][g1][g2].
+// c at the element's Gauss grid: det J of the geometry map computed here
+// from per-line basis tables (geo.kind == TQ_COEFF_GEOMETRY; the element's
+// points are X1[e1 q + g] x X2[e2 q + g]), else read from cgp[slot][g1][g2].
+// E = PV1^T T is a (NP x q) (q x NP) product: a thread owns a 3 x 6 tile.
 // ---------------------------------------------------------------------------
+constexpr int kGpThreads = 128;
+
 template <int Q>
-__global__ void __launch_bounds__(128) k_gauss_pairs(tq_rawctx c, const int32_t* __restrict__ gel, int nslot,
-                                                     const double* __restrict__ cgp, double* __restrict__ E) {
-    constexpr int NP = Pairs<Q>::NP;
-    __shared__ double V1[Q][Q], V2[Q][Q], Wc[Q][Q + 1], PV1[Q][NP], PV2[Q][NP], T[Q][NP];
-    __shared__ int pa[NP], pb[NP];
+__global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* __restrict__ X1,
+                                                            const double* __restrict__ X2,
+                                                            const int32_t* __restrict__ gel, int nslot,
+                                                            const double* __restrict__ cgp, double* __restrict__ E) {
+    constexpr int NP = Pairs<Q>::NP, TA = 3, TB = 6, NA = 16 * TA, NB = 8 * TB;    // 48 x 48 >= NP x NP
+    static_assert(NA >= NP && NB >= NP, "pair tile");
+    constexpr int PG = kMaxP + 1;
+    __shared__ double V1[Q][Q], V2[Q][Q], Wc[Q][Q + 1], PV1[Q][NA], T[Q][NB];
+    __shared__ double Na[Q][PG], Da[Q][PG], Nb[Q][PG], Db[Q][PG];
+    __shared__ double XB[PG][Q], XDB[PG][Q], YB[PG][Q], YDB[PG][Q];
+    __shared__ int sa[Q], sb[Q], pa[NP], pb[NP];
     pair_tables<Q>(pa, pb);
+    const int tid = threadIdx.x;
+    const bool inline_c = geo.kind == TQ_COEFF_GEOMETRY;
     for (int slot = blockIdx.x; slot < nslot; slot += gridDim.x) {
         const int e1 = gel[2 * slot], e2 = gel[2 * slot + 1];
         __syncthreads();
-        for (int t = threadIdx.x; t < Q * Q; t += blockDim.x) {
+        for (int t = tid; t < Q * Q; t += blockDim.x) {
             const int g = t / Q, a = t - g * Q;
             V1[g][a] = c.ev1[((int64_t)e1 * Q + g) * Q + a];
             V2[g][a] = c.ev2[((int64_t)e2 * Q + g) * Q + a];
+        }
+        if (inline_c && tid < 2 * Q) {       // line tables of the geometry map
+            const bool d1 = tid < Q;
+            const int g = d1 ? tid : tid - Q;
+            const double u = d1 ? X1[(int64_t)e1 * Q + g] : X2[(int64_t)e2 * Q + g];
+            const int sp = find_span(geo.knots, geo.n + geo.p + 1, geo.p, geo.n, u);
+            double N[PG], D[PG];
+            basis_funs_ders_rt(geo.knots, geo.p, sp, u, N, D);
+            for (int k = 0; k <= geo.p; ++k) {
+                (d1 ? Na : Nb)[g][k] = N[k];
+                (d1 ? Da : Db)[g][k] = D[k];
+            }
+            (d1 ? sa : sb)[g] = sp;
+        }
+        __syncthreads();
+        // one geometry span per direction over the element (the usual case:
+        // the analysis mesh refines the geometry's): the control net is
+        // contracted along direction 2 first, as in k_coeff_grid_tiled
+        bool tensor = false;
+        if (inline_c) {
+            tensor = true;
+            for (int g = 1; g < Q; ++g) tensor = tensor && sa[g] == sa[0] && sb[g] == sb[0];
+        }
+        if (tensor) {
+            const int pg = geo.p;
+            for (int t = tid; t < (pg + 1) * Q; t += blockDim.x) {
+                const int a = t / Q, g2 = t - (t / Q) * Q;
+                const double* Xr = geo.X + (int64_t)(sa[0] - pg + a) * geo.n + (sb[0] - pg);
+                const double* Yr = geo.Y + (int64_t)(sa[0] - pg + a) * geo.n + (sb[0] - pg);
+                double xb = 0, xdb = 0, yb = 0, ydb = 0;
+                for (int b = 0; b <= pg; ++b) {
+                    const double Xc = __ldg(Xr + b), Yc = __ldg(Yr + b);
+                    xb += Nb[g2][b] * Xc;
+                    xdb += Db[g2][b] * Xc;
+                    yb += Nb[g2][b] * Yc;
+                    ydb += Db[g2][b] * Yc;
+                }
+                XB[a][g2] = xb;
+                XDB[a][g2] = xdb;
+                YB[a][g2] = yb;
+                YDB[a][g2] = ydb;
+            }
+            __syncthreads();
+        }
+        for (int t = tid; t < Q * Q; t += blockDim.x) {
+            const int g1 = t / Q, g2 = t - g1 * Q;
+            double cv;
+            if (tensor) {
+                double xu = 0, xv = 0, yu = 0, yv = 0;
+                for (int a = 0; a <= geo.p; ++a) {
+                    xu += Da[g1][a] * XB[a][g2];
+                    xv += Na[g1][a] * XDB[a][g2];
+                    yu += Da[g1][a] * YB[a][g2];
+                    yv += Na[g1][a] * YDB[a][g2];
+                }
+                cv = xu * yv - xv * yu;
+            } else if (inline_c) {      // detj (rawrows.cu): the same terms in the same order
+                double xu = 0, xv = 0, yu = 0, yv = 0;
+                for (int a = 0; a <= geo.p; ++a)
+                    for (int b = 0; b <= geo.p; ++b) {
+                        const int64_t idx = (int64_t)(sa[g1] - geo.p + a) * geo.n + (sb[g2] - geo.p + b);
+                        const double Xc = __ldg(geo.X + idx), Yc = __ldg(geo.Y + idx);
+                        xu += Da[g1][a] * Nb[g2][b] * Xc;
+                        xv += Na[g1][a] * Db[g2][b] * Xc;
+                        yu += Da[g1][a] * Nb[g2][b] * Yc;
+                        yv += Na[g1][a] * Db[g2][b] * Yc;
+                    }
+                cv = xu * yv - xv * yu;
+            } else {
+                cv = cgp[((int64_t)slot * Q + g1) * Q + g2];
+            }
             // the weights of gauss_entry: c (w1 w2)
-            Wc[g][a] = cgp[((int64_t)slot * Q + g) * Q + a] * (c.ew1[(int64_t)e1 * Q + g] * c.ew2[(int64_t)e2 * Q + a]);
+            Wc[g1][g2] = cv * (c.ew1[(int64_t)e1 * Q + g1] * c.ew2[(int64_t)e2 * Q + g2]);
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < Q * NP; t += blockDim.x) {
-            const int g = t / NP, s = t - g * NP;
-            PV1[g][s] = V1[g][pa[s]] * V1[g][pb[s]];
-            PV2[g][s] = V2[g][pa[s]] * V2[g][pb[s]];
+        for (int t = tid; t < Q * NA; t += blockDim.x) {
+            const int g = t / NA, s = t - g * NA;
+            PV1[g][s] = s < NP ? V1[g][pa[s]] * V1[g][pb[s]] : 0.0;
         }
-        __syncthreads();
-        for (int t = threadIdx.x; t < Q * NP; t += blockDim.x) {
-            const int g1 = t / NP, s2 = t - g1 * NP;
+        for (int t = tid; t < Q * NB; t += blockDim.x) {
+            const int g1 = t / NB, s2 = t - g1 * NB;
             double acc = 0.0;
+            if (s2 < NP) {
+                const int a2 = pa[s2], b2 = pb[s2];
 #pragma unroll
-            for (int g2 = 0; g2 < Q; ++g2) acc += PV2[g2][s2] * Wc[g1][g2];
+                for (int g2 = 0; g2 < Q; ++g2) acc += (V2[g2][a2] * V2[g2][b2]) * Wc[g1][g2];
+            }
             T[g1][s2] = acc;
         }
         __syncthreads();
-        double* out = E + (int64_t)slot * NP * NP;
-        for (int t = threadIdx.x; t < NP * NP; t += blockDim.x) {
-            const int s1 = t / NP, s2 = t - s1 * NP;
-            double acc = 0.0;
+        {
+            const int ta = tid / 8, tb = tid - (tid / 8) * 8;       // 16 x 8 threads
+            double acc[TA][TB];
 #pragma unroll
-            for (int g1 = 0; g1 < Q; ++g1) acc += PV1[g1][s1] * T[g1][s2];
-            out[t] = acc;
+            for (int i = 0; i < TA; ++i)
+#pragma unroll
+                for (int j = 0; j < TB; ++j) acc[i][j] = 0.0;
+#pragma unroll
+            for (int g1 = 0; g1 < Q; ++g1) {
+                double x[TA], y[TB];
+#pragma unroll
+                for (int i = 0; i < TA; ++i) x[i] = PV1[g1][ta * TA + i];
+#pragma unroll
+                for (int j = 0; j < TB; ++j) y[j] = T[g1][tb * TB + j];
+#pragma unroll
+                for (int i = 0; i < TA; ++i)
+#pragma unroll
+                    for (int j = 0; j < TB; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
+            }
+            double* out = E + (int64_t)slot * NP * NP;
+#pragma unroll
+            for (int i = 0; i < TA; ++i)
+#pragma unroll
+                for (int j = 0; j < TB; ++j) {
+                    const int s1 = ta * TA + i, s2 = tb * TB + j;
+                    if (s1 < NP && s2 < NP) out[s1 * NP + s2] = acc[i][j];
+                }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Span-key group blocks of the cut elements: one block of 128 threads per
-// group; points staged KC at a time (v1, v2, cw through the group
-// permutation), their pair products P1 / P2 formed in shared memory, then a
-// thread accumulates a TA x TB tile of E = P1^T P2.
+// Span-key group blocks of the cut elements, by pieces of at most kCpPiece
+// points (a group's pieces are summed in order by k_cut_pairs_reduce: the
+// largest groups no longer set the kernel's length).  One block of 128
+// threads per piece; points staged kCpChunk at a time (v1, v2, cw through the
+// group permutation), their pair products P1 / P2 formed in shared memory,
+// then a thread accumulates a TA x TB tile of P1^T P2.
+// pieces: npieces x 2 int64 (group, first point); piece end = min(first +
+// kCpPiece, the group's end).
 // ---------------------------------------------------------------------------
-constexpr int kCpThreads = 128, kCpChunk = 32;
+constexpr int kCpThreads = 128, kCpChunk = 32, kCpPiece = 128;
 
 template <int Q>
-__global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, double* __restrict__ E) {
+__global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,
+                                                          int npieces, double* __restrict__ Epart) {
     constexpr int NP = Pairs<Q>::NP, TA = (NP + 7) / 8, TB = (NP + 15) / 16, NA = 8 * TA, NB = 16 * TB;
     constexpr int ST = 2 * Q + 1;
     __shared__ double S[kCpChunk][ST];
@@ -104,8 +216,9 @@ __global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, double* _
     __shared__ int pa[NP], pb[NP];
     pair_tables<Q>(pa, pb);
     const int tid = threadIdx.x, ta = tid / 16, tb = tid - (tid / 16) * 16;
-    for (int g = blockIdx.x; g < c.ngroups; g += gridDim.x) {
-        const int64_t p0 = c.grp_pts[g], pe = c.grp_pts[g + 1];
+    for (int pc = blockIdx.x; pc < npieces; pc += gridDim.x) {
+        const int g = (int)pieces[2 * pc];
+        const int64_t p0 = pieces[2 * pc + 1], pe = min(p0 + kCpPiece, (int64_t)c.grp_pts[g + 1]);
         double acc[TA][TB];
 #pragma unroll
         for (int i = 0; i < TA; ++i)
@@ -114,14 +227,10 @@ __global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, double* _
         for (int64_t base = p0; base < pe; base += kCpChunk) {
             const int np = (int)(pe - base < kCpChunk ? pe - base : kCpChunk);
             __syncthreads();
-            for (int k = tid; k < np; k += kCpThreads) {
+            for (int t = tid; t < np * ST; t += kCpThreads) {
+                const int k = t / ST, o = t - k * ST;
                 const int64_t pt = c.grp_perm[base + k];
-#pragma unroll
-                for (int o = 0; o < Q; ++o) {
-                    S[k][o] = c.cvals1[pt * Q + o];
-                    S[k][Q + o] = c.cvals2[pt * Q + o];
-                }
-                S[k][2 * Q] = c.cut_cw[pt];
+                S[k][o] = o < Q ? c.cvals1[pt * Q + o] : (o < 2 * Q ? c.cvals2[pt * Q + (o - Q)] : c.cut_cw[pt]);
             }
             __syncthreads();
             for (int t = tid; t < kCpChunk * NA; t += kCpThreads) {
@@ -145,7 +254,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, double* _
                     for (int j = 0; j < TB; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
             }
         }
-        double* out = E + (int64_t)g * NP * NP;
+        double* out = Epart + (int64_t)pc * NP * NP;
 #pragma unroll
         for (int i = 0; i < TA; ++i)
 #pragma unroll
@@ -156,89 +265,129 @@ __global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, double* _
     }
 }
 
+// E[g] = sum of its pieces in order (gpiece: ngroups + 1 piece offsets)
+__global__ void k_cut_pairs_reduce(const int32_t* __restrict__ gpiece, int ngroups, int npp,
+                                   const double* __restrict__ Epart, double* __restrict__ E) {
+    const int64_t total = (int64_t)ngroups * npp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int g = (int)(t / npp), e = (int)(t - (int64_t)g * npp);
+        double acc = 0.0;
+        for (int pc = gpiece[g]; pc < gpiece[g + 1]; ++pc) acc += Epart[(int64_t)pc * npp + e];
+        E[t] = acc;
+    }
+}
+
 // ---------------------------------------------------------------------------
-// Per cut row (descriptor rows [r0, r1), warp per row): the Gauss part (GAUSS
-// and BOX rows: interior support elements outside the box) and the cut-cell
-// part (span-key groups of the cut elements within one element of the
-// support), summed in a warp-private shared row block in a fixed order,
-// then written to the row's planes.  gslot: element -> Gauss block slot.
+// Per cut row (descriptor rows [r0, r1)): a block per row, a thread per
+// window entry o = (o1, o2), j = (i1 - p + o1, i2 - p + o2).  The row's
+// support elements (slot of their Gauss block, -1 when excluded: not
+// interior, inside the box, or MASK rows) are staged with, per window line,
+// the range of support elements whose span covers j (the spans increase
+// along the support, so it is one range); the row's span-key groups come as
+// a list (rg_ptr / rg: group, key1, key2; geometry, built once per plan).
+// Every thread sums its entry's terms -- Gauss elements in (e1, e2) order,
+// then the groups in list order -- in registers, and writes the row's plane
+// entry.  gslot: element -> Gauss block slot.
 // ---------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(256) k_cut_rows_gather(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot,
-                                                         const double* __restrict__ Eg, const double* __restrict__ Ec,
-                                                         int* __restrict__ status) {
-    constexpr int Q = P + 1, W = 2 * P + 1, T = W * W, NP = Pairs<Q>::NP, QQ = Q * Q;
-    constexpr int WPB = 8;
-    __shared__ double acc_s[WPB][T];
-    __shared__ int pidx[Q][Q];
-    for (int t = threadIdx.x; t < QQ; t += blockDim.x) {
+__global__ void __launch_bounds__(32 * (((2 * P + 1) * (2 * P + 1) + 31) / 32))
+k_cut_rows_gather(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot, const double* __restrict__ Eg,
+                  const double* __restrict__ Ec, const int32_t* __restrict__ rg_ptr, const int32_t* __restrict__ rg,
+                  int* __restrict__ status) {
+    constexpr int Q = P + 1, W = 2 * P + 1, T = W * W, NP = Pairs<Q>::NP;
+    __shared__ int S[Q][Q], F1[Q], F2[Q], pidx[Q][Q], K1[W][2], K2[W][2];
+    const int tid = threadIdx.x;
+    for (int t = tid; t < Q * Q; t += blockDim.x) {
         const int a = t / Q, b = t - (t / Q) * Q;
         pidx[a][b] = a <= b ? Pairs<Q>::of(a, b) : Pairs<Q>::of(b, a);
     }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double* acc = acc_s[wib];
-    for (int r = r0 + blockIdx.x * WPB + wib; r < r1; r += gridDim.x * WPB) {
+    const int o1 = tid / W, o2 = tid - (tid / W) * W;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
         const RowDescC d = reinterpret_cast<const RowDescC*>(c.desc)[r];
         const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
-        for (int q = lane; q < T; q += 32) acc[q] = 0.0;
-        __syncwarp();
-        if (d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX) {
-            const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
-            for (int e1 = c.el_first1[i1]; e1 <= c.el_last1[i1]; ++e1) {
-                const int f1 = c.espan1[e1] - P, a1 = i1 - f1;
-                for (int e2 = c.el_first2[i2]; e2 <= c.el_last2[i2]; ++e2) {
-                    const int64_t e = (int64_t)e1 * c.nel2 + e2;
-                    if (c.elem_class[e] != TQ_INTERIOR) continue;
-                    if (box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2) continue;
-                    const int slot = gslot[e];
-                    if (slot < 0) {       // the element list missed an element: flagged, never silent
-                        if (lane == 0) atomicOr(status, 4);
-                        continue;
-                    }
-                    const int f2 = c.espan2[e2] - P, a2 = i2 - f2;
-                    const double* Es = Eg + (int64_t)slot * NP * NP;
-                    for (int B = lane; B < QQ; B += 32) {
-                        const int b1 = B / Q, b2 = B - (B / Q) * Q;
-                        acc[(f1 + b1 - i1 + P) * W + (f2 + b2 - i2 + P)] +=
-                            __ldg(Es + pidx[a1][b1] * NP + pidx[a2][b2]);
-                    }
-                    __syncwarp();
+        const int ef1 = c.el_first1[i1], ef2 = c.el_first2[i2];
+        const int ne1 = c.el_last1[i1] - ef1 + 1, ne2 = c.el_last2[i2] - ef2 + 1;
+        const bool gauss = d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX;
+        const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
+        __syncthreads();
+        for (int t = tid; t < Q * Q; t += blockDim.x) {
+            const int k1 = t / Q, k2 = t - (t / Q) * Q;
+            int sl = -1;
+            if (gauss && k1 < ne1 && k2 < ne2) {
+                const int e1 = ef1 + k1, e2 = ef2 + k2;
+                const int64_t e = (int64_t)e1 * c.nel2 + e2;
+                const bool inbox = box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2;
+                const int gs = gslot[e];
+                const bool inner = c.elem_class[e] == TQ_INTERIOR;
+                if (inner && !inbox) {
+                    sl = gs;
+                    if (sl < 0) atomicOr(status, 4);      // the element list missed it: flagged
                 }
             }
+            S[k1][k2] = sl;
+            if (k2 == 0) F1[k1] = k1 < ne1 ? c.espan1[ef1 + k1] - P : INT_MAX / 2;
+            if (k1 == 0) F2[k2] = k2 < ne2 ? c.espan2[ef2 + k2] - P : INT_MAX / 2;
         }
-        if (Ec && c.cut_ptr) {
-            const int ea1 = max(c.el_first1[i1] - 1, 0), eb1 = min(c.el_last1[i1] + 1, c.nel1 - 1);
-            const int ea2 = max(c.el_first2[i2] - 1, 0), eb2 = min(c.el_last2[i2] + 1, c.nel2 - 1);
-            const int w2 = eb2 - ea2 + 1, nh = (eb1 - ea1 + 1) * w2;
-            for (int h0 = 0; h0 < nh; h0 += 32) {
-                const int h = h0 + lane;
-                int id = -1;
-                if (h < nh) id = c.cutidx[(int64_t)(ea1 + h / w2) * c.nel2 + (ea2 + h % w2)];
-                unsigned m = __ballot_sync(0xffffffffu, id >= 0);
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int cid = __shfl_sync(0xffffffffu, id, src);
-                    for (int g = c.grp_ptr[cid]; g < c.grp_ptr[cid + 1]; ++g) {
-                        const int f1 = c.grp_key[2 * g], f2 = c.grp_key[2 * g + 1];
-                        const int a1 = i1 - f1, a2 = i2 - f2;
-                        if (a1 < 0 || a1 > P || a2 < 0 || a2 > P) continue;
-                        const double* Es = Ec + (int64_t)g * NP * NP;
-                        for (int B = lane; B < QQ; B += 32) {
-                            const int b1 = B / Q, b2 = B - (B / Q) * Q;
-                            acc[(f1 + b1 - i1 + P) * W + (f2 + b2 - i2 + P)] +=
-                                __ldg(Es + pidx[a1][b1] * NP + pidx[a2][b2]);
+        __syncthreads();
+        if (tid < 2 * W) {        // support elements whose span covers j: F(k) in [j - P, j]
+            const bool d1 = tid < W;
+            const int o = d1 ? tid : tid - W, j = (d1 ? i1 : i2) - P + o, ne = d1 ? ne1 : ne2;
+            const int* F = d1 ? F1 : F2;
+            int lo = 0, hi = -1;
+            for (int k = 0; k < ne; ++k)
+                if (F[k] >= j - P && F[k] <= j) {
+                    if (hi < lo) lo = k;
+                    hi = k;
+                }
+            (d1 ? K1 : K2)[o][0] = lo;
+            (d1 ? K1 : K2)[o][1] = hi;
+        }
+        __syncthreads();
+        if (tid < T) {
+            const int j1 = i1 - P + o1, j2 = i2 - P + o2;
+            const int lo1 = K1[o1][0], hi1 = K1[o1][1], lo2 = K2[o2][0], hi2 = K2[o2][1];
+            double acc = 0.0;
+            // a window line's terms are loaded together (Q predicated loads in
+            // flight), then added in order
+            for (int k1 = lo1; k1 <= hi1; ++k1) {
+                const int pr1 = pidx[i1 - F1[k1]][j1 - F1[k1]] * NP;
+                double v[Q];
+#pragma unroll
+                for (int k2 = 0; k2 < Q; ++k2) {
+                    const int sl = S[k1][k2];
+                    const bool ok = k2 >= lo2 && k2 <= hi2 && sl >= 0;
+                    v[k2] = ok ? __ldg(Eg + (int64_t)sl * (NP * NP) + pr1 + pidx[i2 - F2[k2]][j2 - F2[k2]]) : 0.0;
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < Q; ++k2)
+                    if (k2 >= lo2 && k2 <= hi2 && S[k1][k2] >= 0) acc += v[k2];
+            }
+            if (Ec) {
+                const int gb = rg_ptr[r - r0], ge = rg_ptr[r - r0 + 1];
+                constexpr int GU = 8;
+                for (int k0 = gb; k0 < ge; k0 += GU) {
+                    double v[GU];
+                    bool ok[GU];
+#pragma unroll
+                    for (int u = 0; u < GU; ++u) {
+                        const int k = k0 + u;
+                        ok[u] = false;
+                        v[u] = 0.0;
+                        if (k < ge) {
+                            const int g = __ldg(rg + 3 * k), f1 = __ldg(rg + 3 * k + 1), f2 = __ldg(rg + 3 * k + 2);
+                            const int b1 = j1 - f1, b2 = j2 - f2;
+                            ok[u] = b1 >= 0 && b1 <= P && b2 >= 0 && b2 <= P;
+                            if (ok[u])
+                                v[u] = __ldg(Ec + (int64_t)g * (NP * NP) + pidx[i1 - f1][b1] * NP + pidx[i2 - f2][b2]);
                         }
-                        __syncwarp();
                     }
+#pragma unroll
+                    for (int u = 0; u < GU; ++u)
+                        if (ok[u]) acc += v[u];
                 }
             }
+            c.raw[(int64_t)tid * c.raw_ld + c.store[r]] = acc;
         }
-        __syncwarp();
-        double* dst = c.raw + c.store[r];
-        for (int q = lane; q < T; q += 32) dst[(int64_t)q * c.raw_ld] = acc[q];
-        __syncwarp();
     }
 }
 
@@ -252,35 +401,47 @@ extern "C" int64_t tq_pair_block_doubles(int32_t p) {
 }
 
 // Element-Gauss blocks in pair form of the listed elements (gel: nslot x 2
-// element indices; cgp: c at their (p+1)^2 Gauss points, [slot][g1][g2];
-// E: nslot x tq_pair_block_doubles(p)).  Needs p1 == p2 and ng = p + 1.
-extern "C" int tq_gauss_pairs(tq_rawctx c, const int32_t* gel, int32_t nslot, const double* cgp, double* E,
-                              void* stream) {
+// element indices; E: nslot x tq_pair_block_doubles(p)).  c: det J computed
+// in the kernel when geo.kind == TQ_COEFF_GEOMETRY (X1 / X2: the element
+// Gauss points per direction, nel x (p+1)), else cgp = c at the elements'
+// (p+1)^2 Gauss points, [slot][g1][g2].  Needs p1 == p2 and ng = p + 1.
+extern "C" int tq_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* X1, const double* X2, const int32_t* gel,
+                              int32_t nslot, const double* cgp, double* E, void* stream) {
     if (nslot <= 0) return TQ_OK;
     if (c.p1 != c.p2 || c.ng1 != c.p1 + 1 || c.ng2 != c.p2 + 1) { set_error("tq_gauss_pairs needs p1 == p2 and p + 1 Gauss points"); return TQ_EINVAL; }
+    if (geo.kind == TQ_COEFF_GEOMETRY ? (geo.p > kMaxP || !X1 || !X2) : !cgp) { set_error("tq_gauss_pairs: no coefficient"); return TQ_EINVAL; }
     const int grid = std::min(nslot, kSms * 16);
     switch (c.p1 + 1) {
-#define CASE(Q) case Q: k_gauss_pairs<Q><<<grid, 128, 0, S(stream)>>>(c, gel, nslot, cgp, E); break;
-        CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11)
+#define CASE(Q) case Q: k_gauss_pairs<Q><<<grid, kGpThreads, 0, S(stream)>>>(c, geo, X1, X2, gel, nslot, cgp, E); break;
+        CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
-        default: set_error("degree out of range"); return TQ_EINVAL;
+        default: set_error("degree out of range for the pair blocks"); return TQ_EINVAL;
     }
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_gauss_pairs");
     return TQ_OK;
 }
 
-// Span-key group blocks in pair form (E: ngroups x tq_pair_block_doubles(p)).
-extern "C" int tq_cut_pairs(tq_rawctx c, double* E, void* stream) {
+extern "C" int32_t tq_cut_pair_piece(void) { return kCpPiece; }
+
+// Span-key group blocks in pair form (E: ngroups x tq_pair_block_doubles(p)),
+// by pieces of at most tq_cut_pair_piece() points: pieces npieces x 2 int64
+// (group, first point), gpiece ngroups + 1 piece offsets per group, Epart
+// npieces x tq_pair_block_doubles(p) scratch.
+extern "C" int tq_cut_pairs(tq_rawctx c, const int64_t* pieces, int32_t npieces, const int32_t* gpiece, double* Epart,
+                            double* E, void* stream) {
     if (c.ngroups <= 0) return TQ_OK;
     if (c.p1 != c.p2) { set_error("tq_cut_pairs needs p1 == p2"); return TQ_EINVAL; }
-    const int grid = std::min(c.ngroups, kSms * 16);
+    const int grid = std::min(npieces, kSms * 16);
     switch (c.p1 + 1) {
-#define CASE(Q) case Q: k_cut_pairs<Q><<<grid, kCpThreads, 0, S(stream)>>>(c, E); break;
+#define CASE(Q) case Q: k_cut_pairs<Q><<<grid, kCpThreads, 0, S(stream)>>>(c, pieces, npieces, Epart); break;
         CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11)
 #undef CASE
         default: set_error("degree out of range"); return TQ_EINVAL;
     }
+    ::tq::note_launch();
+    const int npp = (int)tq_pair_block_doubles(c.p1);
+    k_cut_pairs_reduce<<<grid_for((int64_t)c.ngroups * npp, 256), 256, 0, S(stream)>>>(gpiece, c.ngroups, npp, Epart, E);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_cut_pairs");
     return TQ_OK;
@@ -288,14 +449,18 @@ extern "C" int tq_cut_pairs(tq_rawctx c, double* E, void* stream) {
 
 // Rows [r0, r1) (the cut rows, planes layout): Gauss + cut-cell parts from
 // the pair blocks (Eg / gslot: tq_gauss_pairs, Ec: tq_cut_pairs or NULL),
-// written to the planes.  status |= 4 when a needed Gauss block is missing.
+// written to the planes (rg_ptr: r1 - r0 + 1 offsets into rg = the rows'
+// span-key groups, 3 ints each: group, key1, key2).  status |= 4 when a
+// needed Gauss block is missing.
 extern "C" int tq_cut_rows_gather(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* gslot, const double* Eg,
-                                  const double* Ec, int32_t* status, void* stream) {
+                                  const double* Ec, const int32_t* rg_ptr, const int32_t* rg, int32_t* status,
+                                  void* stream) {
     if (r1 <= r0) return TQ_OK;
     if (!c.raw_ld || !c.store || c.p1 != c.p2) { set_error("tq_cut_rows_gather needs the planes layout and p1 == p2"); return TQ_EINVAL; }
-    const int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 8);
+    const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 16);
     switch (c.p1) {
-#define CASE(Q) case Q: k_cut_rows_gather<Q><<<grid, 256, 0, S(stream)>>>(c, r0, r1, gslot, Eg, Ec, status); break;
+#define CASE(Q) case Q: k_cut_rows_gather<Q><<<grid, 32 * (((2 * Q + 1) * (2 * Q + 1) + 31) / 32), 0, S(stream)>>>( \
+            c, r0, r1, gslot, Eg, Ec, rg_ptr, rg, status); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
         default: set_error("degree out of range"); return TQ_EINVAL;
