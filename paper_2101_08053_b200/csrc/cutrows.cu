@@ -63,9 +63,18 @@ __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coef
     __shared__ double Na[Q][PG], Da[Q][PG], Nb[Q][PG], Db[Q][PG];
     __shared__ double XB[PG][Q], XDB[PG][Q], YB[PG][Q], YDB[PG][Q];
     __shared__ int sa[Q], sb[Q], pa[NP], pb[NP];
+    constexpr int KN = 128;                    // geometry knots kept in shared memory (when they fit)
+    __shared__ double kn_s[KN], XW[PG][PG], YW[PG][PG];
     pair_tables<Q>(pa, pb);
     const int tid = threadIdx.x;
     const bool inline_c = geo.kind == TQ_COEFF_GEOMETRY;
+    const int nk = geo.n + geo.p + 1;
+    const double* knots = geo.knots;
+    if (inline_c && nk <= KN) {
+        for (int t = tid; t < nk; t += blockDim.x) kn_s[t] = geo.knots[t];
+        knots = kn_s;
+    }
+    __syncthreads();
     for (int slot = blockIdx.x; slot < nslot; slot += gridDim.x) {
         const int e1 = gel[2 * slot], e2 = gel[2 * slot + 1];
         __syncthreads();
@@ -78,9 +87,9 @@ __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coef
             const bool d1 = tid < Q;
             const int g = d1 ? tid : tid - Q;
             const double u = d1 ? X1[(int64_t)e1 * Q + g] : X2[(int64_t)e2 * Q + g];
-            const int sp = find_span(geo.knots, geo.n + geo.p + 1, geo.p, geo.n, u);
+            const int sp = find_span(knots, nk, geo.p, geo.n, u);
             double N[PG], D[PG];
-            basis_funs_ders_rt(geo.knots, geo.p, sp, u, N, D);
+            basis_funs_ders_rt(knots, geo.p, sp, u, N, D);
             for (int k = 0; k <= geo.p; ++k) {
                 (d1 ? Na : Nb)[g][k] = N[k];
                 (d1 ? Da : Db)[g][k] = D[k];
@@ -98,13 +107,18 @@ __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coef
         }
         if (tensor) {
             const int pg = geo.p;
+            for (int t = tid; t < (pg + 1) * (pg + 1); t += blockDim.x) {      // the control window
+                const int a = t / (pg + 1), b = t - (t / (pg + 1)) * (pg + 1);
+                const int64_t idx = (int64_t)(sa[0] - pg + a) * geo.n + (sb[0] - pg + b);
+                XW[a][b] = __ldg(geo.X + idx);
+                YW[a][b] = __ldg(geo.Y + idx);
+            }
+            __syncthreads();
             for (int t = tid; t < (pg + 1) * Q; t += blockDim.x) {
                 const int a = t / Q, g2 = t - (t / Q) * Q;
-                const double* Xr = geo.X + (int64_t)(sa[0] - pg + a) * geo.n + (sb[0] - pg);
-                const double* Yr = geo.Y + (int64_t)(sa[0] - pg + a) * geo.n + (sb[0] - pg);
                 double xb = 0, xdb = 0, yb = 0, ydb = 0;
                 for (int b = 0; b <= pg; ++b) {
-                    const double Xc = __ldg(Xr + b), Yc = __ldg(Yr + b);
+                    const double Xc = XW[a][b], Yc = YW[a][b];
                     xb += Nb[g2][b] * Xc;
                     xdb += Db[g2][b] * Xc;
                     yb += Nb[g2][b] * Yc;
@@ -295,7 +309,7 @@ k_cut_rows_gather(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot
                   const double* __restrict__ Ec, const int32_t* __restrict__ rg_ptr, const int32_t* __restrict__ rg,
                   int* __restrict__ status) {
     constexpr int Q = P + 1, W = 2 * P + 1, T = W * W, NP = Pairs<Q>::NP;
-    __shared__ int S[Q][Q], F1[Q], F2[Q], pidx[Q][Q], K1[W][2], K2[W][2];
+    __shared__ int S[Q][Q], F1[Q], F2[Q], pidx[Q][Q], K1[W][2], OFF1[W][Q], OFF2[W][Q];
     const int tid = threadIdx.x;
     for (int t = tid; t < Q * Q; t += blockDim.x) {
         const int a = t / Q, b = t - (t / Q) * Q;
@@ -324,43 +338,55 @@ k_cut_rows_gather(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot
                     if (sl < 0) atomicOr(status, 4);      // the element list missed it: flagged
                 }
             }
-            S[k1][k2] = sl;
+            S[k1][k2] = sl < 0 ? -1 : sl * (NP * NP);      // block offset (or -1)
             if (k2 == 0) F1[k1] = k1 < ne1 ? c.espan1[ef1 + k1] - P : INT_MAX / 2;
             if (k1 == 0) F2[k2] = k2 < ne2 ? c.espan2[ef2 + k2] - P : INT_MAX / 2;
         }
         __syncthreads();
-        if (tid < 2 * W) {        // support elements whose span covers j: F(k) in [j - P, j]
-            const bool d1 = tid < W;
-            const int o = d1 ? tid : tid - W, j = (d1 ? i1 : i2) - P + o, ne = d1 ? ne1 : ne2;
-            const int* F = d1 ? F1 : F2;
+        // per window line o and support element k: the pair offset of
+        // (a, b) = (i - F(k), j - F(k)) when F(k) covers j (else -1), and the
+        // range of such k for direction 1
+        for (int t = tid; t < 2 * W * Q; t += blockDim.x) {
+            const bool d1 = t < W * Q;
+            const int u = d1 ? t : t - W * Q, o = u / Q, k = u - (u / Q) * Q;
+            const int i = d1 ? i1 : i2, j = i - P + o, F = (d1 ? F1 : F2)[k];
+            const bool ok = k < (d1 ? ne1 : ne2) && F >= j - P && F <= j;
+            (d1 ? OFF1 : OFF2)[o][k] = ok ? pidx[i - F][j - F] * (d1 ? NP : 1) : -1;
+        }
+        if (tid < W) {
             int lo = 0, hi = -1;
-            for (int k = 0; k < ne; ++k)
-                if (F[k] >= j - P && F[k] <= j) {
+            const int j = i1 - P + tid;
+            for (int k = 0; k < ne1; ++k)
+                if (F1[k] >= j - P && F1[k] <= j) {
                     if (hi < lo) lo = k;
                     hi = k;
                 }
-            (d1 ? K1 : K2)[o][0] = lo;
-            (d1 ? K1 : K2)[o][1] = hi;
+            K1[tid][0] = lo;
+            K1[tid][1] = hi;
         }
         __syncthreads();
         if (tid < T) {
             const int j1 = i1 - P + o1, j2 = i2 - P + o2;
-            const int lo1 = K1[o1][0], hi1 = K1[o1][1], lo2 = K2[o2][0], hi2 = K2[o2][1];
+            const int lo1 = K1[o1][0], hi1 = K1[o1][1];
+            int off2[Q];
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) off2[k2] = OFF2[o2][k2];
             double acc = 0.0;
             // a window line's terms are loaded together (Q predicated loads in
             // flight), then added in order
             for (int k1 = lo1; k1 <= hi1; ++k1) {
-                const int pr1 = pidx[i1 - F1[k1]][j1 - F1[k1]] * NP;
+                const int pr1 = OFF1[o1][k1];
                 double v[Q];
+                bool ok[Q];
 #pragma unroll
                 for (int k2 = 0; k2 < Q; ++k2) {
                     const int sl = S[k1][k2];
-                    const bool ok = k2 >= lo2 && k2 <= hi2 && sl >= 0;
-                    v[k2] = ok ? __ldg(Eg + (int64_t)sl * (NP * NP) + pr1 + pidx[i2 - F2[k2]][j2 - F2[k2]]) : 0.0;
+                    ok[k2] = sl >= 0 && off2[k2] >= 0;
+                    v[k2] = ok[k2] ? __ldg(Eg + (sl + pr1 + off2[k2])) : 0.0;
                 }
 #pragma unroll
                 for (int k2 = 0; k2 < Q; ++k2)
-                    if (k2 >= lo2 && k2 <= hi2 && S[k1][k2] >= 0) acc += v[k2];
+                    if (ok[k2]) acc += v[k2];
             }
             if (Ec) {
                 const int gb = rg_ptr[r - r0], ge = rg_ptr[r - r0 + 1];
