@@ -479,7 +479,11 @@ int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stream);
  * _Run.add_cut_blocks (src/assembly.py:310-332, 369-398). */
 int64_t tq_pair_block_doubles(int32_t p);
 int tq_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* X1, const double* X2, const int32_t* gel,
-                   int32_t nslot, const double* cgp, double* E, void* stream);
+                   int32_t nslot, const double* cgp, double* E, const int32_t* lsp1, const double* lnd1,
+                   const int32_t* lsp2, const double* lnd2, void* stream);
+/* geometry-map line tables (span; N[0..p], D[0..p]) at n points, read by
+ * tq_gauss_pairs for the element Gauss points (NULL tables: computed inline) */
+int tq_geo_lines(tq_coeff geo, const double* u, int32_t n, int32_t* span, double* nd, void* stream);
 /* the group blocks by pieces of at most tq_cut_pair_piece() points (pieces:
  * npieces x 2 int64 = group, first point; gpiece: ngroups + 1 offsets;
  * Epart: npieces blocks of scratch), summed per group in piece order */

@@ -56,7 +56,9 @@ def _bind():
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
     L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
-    L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp,
+                                  L.vp])
+    L.optional("tq_geo_lines", [L.Coeff, L.vp, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_cut_pairs", [RawCtx, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp])
     L.optional("tq_cut_pair_piece", [], L.i32)
     L.optional("tq_cut_rows_gather", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp])
@@ -509,14 +511,23 @@ def _gauss_pairs(f, eg, em):
     if ge["n"]:
         ctx = _gauss_ctx(f, eg, em, None, _desc_dev(f)[0], torch.empty(1, dtype=torch.float64, device=f.dev), 0)
         dev = getattr(f.coeff, "_device", None) or f.coeff
+        lines = [None] * 4
         if isinstance(dev, GeometryMap):
             geo, cgp = dev.device(), None
+            lines = []
+            for d in range(2):      # line tables of the element Gauss points (tiny; per pass)
+                X = eg[d][3]
+                sp = torch.empty(X.numel(), dtype=torch.int32, device=f.dev)
+                nd = torch.empty(X.numel() * 2 * (dev.p + 1), dtype=torch.float64, device=f.dev)
+                L.call("tq_geo_lines", geo, L.ptr(X), X.numel(), L.ptr(sp), L.ptr(nd), L.stream())
+                lines += [sp, nd]
+            f._keep_pairs = getattr(f, "_keep_pairs", []) + lines
         else:
             P = torch.stack([eg[0][3][ge["idx1"]], eg[1][3][ge["idx2"]]], dim=1)
             geo, cgp = L.Coeff(), f.coeff.at_device(P)
             f._keep_pairs = getattr(f, "_keep_pairs", []) + [P, cgp]
         L.call("tq_gauss_pairs", ctx, geo, L.ptr(eg[0][3]), L.ptr(eg[1][3]), L.ptr(ge["gel"]), ge["n"], L.ptr(cgp),
-               L.ptr(E), L.stream())
+               L.ptr(E), *[L.ptr(t) for t in lines], L.stream())
     return E, ge["gslot"]
 
 

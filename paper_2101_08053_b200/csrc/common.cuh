@@ -135,6 +135,32 @@ __host__ __device__ inline void basis_funs_ders_rt(const double* kn, int p, int 
     }
 }
 
+// compile-time-degree values + first derivatives (the runtime-degree
+// basis_funs_ders_rt above is miscompiled for sm_100a at -O3 in some inlining
+// contexts -- wrong derivatives, measured with CUDA 12.9 in k_geo_lines --
+// so new kernels dispatch on the degree and use this one)
+template <int P>
+__host__ __device__ inline void basis_funs_ders(const double* kn, int span, double u, double* N, double* D) {
+    basis_funs<P>(kn, span, u, N);
+    if (P == 0) { D[0] = 0.0; return; }
+    double Nl[P + 1];
+    basis_funs<(P > 0 ? P - 1 : 0)>(kn, span, u, Nl);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+        const int i = span - P + k;
+        double acc = 0.0;
+        if (k >= 1) {
+            const double den = kn[i + P] - kn[i];
+            if (den > 0.0) acc += (double)P / den * Nl[k - 1];
+        }
+        if (k <= P - 1) {
+            const double den = kn[i + P + 1] - kn[i + 1];
+            if (den > 0.0) acc -= (double)P / den * Nl[k];
+        }
+        D[k] = acc;
+    }
+}
+
 // tile mode: number of head tiles (those before the tile holding the first
 // list-A row; all tiles when list A is empty), from count pass 1's control word
 __device__ __forceinline__ int head_tiles(const tq_rowctx& c) {

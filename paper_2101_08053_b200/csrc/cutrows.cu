@@ -51,11 +51,33 @@ __device__ __forceinline__ void pair_tables(int* pa, int* pb) {
 // ---------------------------------------------------------------------------
 constexpr int kGpThreads = 128;
 
+// geometry-map line tables at points u: span, then N[0..p], D[0..p]
+template <int PG>
+__global__ void k_geo_lines(tq_coeff geo, const double* __restrict__ u, int n, int32_t* __restrict__ span,
+                            double* __restrict__ nd) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double x = u[t];
+    const int sp = find_span(geo.knots, geo.n + PG + 1, PG, geo.n, x);
+    double N[PG + 1], D[PG + 1];
+    basis_funs_ders<PG>(geo.knots, sp, x, N, D);
+    span[t] = sp;
+#pragma unroll
+    for (int k = 0; k <= PG; ++k) {
+        nd[(int64_t)t * 2 * (PG + 1) + k] = N[k];
+        nd[(int64_t)t * 2 * (PG + 1) + PG + 1 + k] = D[k];
+    }
+}
+
 template <int Q>
 __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* __restrict__ X1,
                                                             const double* __restrict__ X2,
                                                             const int32_t* __restrict__ gel, int nslot,
-                                                            const double* __restrict__ cgp, double* __restrict__ E) {
+                                                            const double* __restrict__ cgp, double* __restrict__ E,
+                                                            const int32_t* __restrict__ lsp1,
+                                                            const double* __restrict__ lnd1,
+                                                            const int32_t* __restrict__ lsp2,
+                                                            const double* __restrict__ lnd2) {
     constexpr int NP = Pairs<Q>::NP, TA = 3, TB = 6, NA = 16 * TA, NB = 8 * TB;    // 48 x 48 >= NP x NP
     static_assert(NA >= NP && NB >= NP, "pair tile");
     constexpr int PG = kMaxP + 1;
@@ -83,7 +105,18 @@ __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coef
             V1[g][a] = c.ev1[((int64_t)e1 * Q + g) * Q + a];
             V2[g][a] = c.ev2[((int64_t)e2 * Q + g) * Q + a];
         }
-        if (inline_c && tid < 2 * Q) {       // line tables of the geometry map
+        if (inline_c && lsp1) {              // precomputed line tables (tq_geo_lines)
+            const int pg1 = geo.p + 1;
+            for (int t = tid; t < 2 * Q * pg1; t += blockDim.x) {
+                const bool d1 = t < Q * pg1;
+                const int u = d1 ? t : t - Q * pg1, g = u / pg1, k = u - (u / pg1) * pg1;
+                const int64_t pt = (int64_t)(d1 ? e1 : e2) * Q + g;
+                const double* nd = (d1 ? lnd1 : lnd2) + pt * 2 * pg1;
+                (d1 ? Na : Nb)[g][k] = nd[k];
+                (d1 ? Da : Db)[g][k] = nd[pg1 + k];
+                if (k == 0) (d1 ? sa : sb)[g] = (d1 ? lsp1 : lsp2)[pt];
+            }
+        } else if (inline_c && tid < 2 * Q) {       // line tables of the geometry map
             const bool d1 = tid < Q;
             const int g = d1 ? tid : tid - Q;
             const double u = d1 ? X1[(int64_t)e1 * Q + g] : X2[(int64_t)e2 * Q + g];
@@ -431,14 +464,32 @@ extern "C" int64_t tq_pair_block_doubles(int32_t p) {
 // in the kernel when geo.kind == TQ_COEFF_GEOMETRY (X1 / X2: the element
 // Gauss points per direction, nel x (p+1)), else cgp = c at the elements'
 // (p+1)^2 Gauss points, [slot][g1][g2].  Needs p1 == p2 and ng = p + 1.
+// geometry line tables of the element Gauss points for tq_gauss_pairs
+// (n points u: span n int32, nd n x 2 (p_geo + 1) doubles)
+extern "C" int tq_geo_lines(tq_coeff geo, const double* u, int32_t n, int32_t* span, double* nd, void* stream) {
+    if (n <= 0) return TQ_OK;
+    if (geo.kind != TQ_COEFF_GEOMETRY || geo.p > kMaxP) { set_error("tq_geo_lines needs a geometry map"); return TQ_EINVAL; }
+    switch (geo.p) {
+#define CASE(Q) case Q: k_geo_lines<Q><<<(n + 127) / 128, 128, 0, S(stream)>>>(geo, u, n, span, nd); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+        default: set_error("geometry degree out of range"); return TQ_EINVAL;
+    }
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_geo_lines");
+    return TQ_OK;
+}
+
 extern "C" int tq_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* X1, const double* X2, const int32_t* gel,
-                              int32_t nslot, const double* cgp, double* E, void* stream) {
+                              int32_t nslot, const double* cgp, double* E, const int32_t* lsp1, const double* lnd1,
+                              const int32_t* lsp2, const double* lnd2, void* stream) {
     if (nslot <= 0) return TQ_OK;
     if (c.p1 != c.p2 || c.ng1 != c.p1 + 1 || c.ng2 != c.p2 + 1) { set_error("tq_gauss_pairs needs p1 == p2 and p + 1 Gauss points"); return TQ_EINVAL; }
     if (geo.kind == TQ_COEFF_GEOMETRY ? (geo.p > kMaxP || !X1 || !X2) : !cgp) { set_error("tq_gauss_pairs: no coefficient"); return TQ_EINVAL; }
     const int grid = std::min(nslot, kSms * 16);
     switch (c.p1 + 1) {
-#define CASE(Q) case Q: k_gauss_pairs<Q><<<grid, kGpThreads, 0, S(stream)>>>(c, geo, X1, X2, gel, nslot, cgp, E); break;
+#define CASE(Q) case Q: k_gauss_pairs<Q><<<grid, kGpThreads, 0, S(stream)>>>(c, geo, X1, X2, gel, nslot, cgp, E, \
+            lsp1, lnd1, lsp2, lnd2); break;
         CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
         default: set_error("degree out of range for the pair blocks"); return TQ_EINVAL;
