@@ -606,7 +606,9 @@ def _cut_pairs(f, cut):
     pieces, gpiece, npieces = _cut_pieces(f, cut)
     if cut["ngroups"]:
         part = torch.empty(max(npieces, 1) * npair, dtype=torch.float64, device=f.dev)
-        L.call("tq_cut_pairs", _cut_blocks_ctx(f, cut, _group_range(f, cut)), L.ptr(pieces), npieces,
+        # every group (the pieces index groups absolutely; a row block's
+        # rows read only some, the rest is small replicated work)
+        L.call("tq_cut_pairs", _cut_blocks_ctx(f, cut), L.ptr(pieces), npieces,
                L.ptr(gpiece), L.ptr(part), L.ptr(E), L.stream())
         f._keep_pairs = getattr(f, "_keep_pairs", []) + [part]
     return E
@@ -657,13 +659,21 @@ class _Setup:
                 self.nmax.append(max(ms))
                 self.nmax_std.append(ms[0])
             if not f.coeff.identity:
-                ptrs = np.zeros(len(self.sets[0]) * len(self.sets[1]), dtype=np.uint64)
-                for a, s1 in enumerate(self.sets[0]):
-                    for c, s2 in enumerate(self.sets[1]):
-                        g = f.coeff.grid_device(s1.layout.device_points(), s2.layout.device_points())
-                        self.keep.append(g)
-                        ptrs[a * len(self.sets[1]) + c] = g.data_ptr()
-                self.grids = L.dev(ptrs.view(np.int64), torch.int64)
+                pre = getattr(f, "_grids_pre", None)
+                lays = ([s.layout for s in self.sets[0]], [s.layout for s in self.sets[1]])
+                if pre is not None and all(len(a) == len(b) and all(x is y for x, y in zip(a, b))
+                                           for a, b in zip(pre[0], lays)):
+                    # computed at pass start on its own stream (prelaunch_grids)
+                    torch.cuda.current_stream().wait_event(pre[2])
+                    self.grids = pre[1]
+                else:
+                    ptrs = np.zeros(len(self.sets[0]) * len(self.sets[1]), dtype=np.uint64)
+                    for a, s1 in enumerate(self.sets[0]):
+                        for c, s2 in enumerate(self.sets[1]):
+                            g = f.coeff.grid_device(s1.layout.device_points(), s2.layout.device_points())
+                            self.keep.append(g)
+                            ptrs[a * len(self.sets[1]) + c] = g.data_ptr()
+                    self.grids = L.dev(ptrs.view(np.int64), torch.int64)
                 _st("grids")
         else:
             self.sets_dev = [None, None]
@@ -814,6 +824,51 @@ def _named_stream(name, priority=0):
     return _NAMED[key]
 
 
+def prelaunch_grids(f):
+    """Coefficient grids of every rule-set pair at pass start, on their own
+    stream (they depend on the point layouts -- geometry, cached by the eager
+    pass -- and the coefficient field, not on the weights)."""
+    if f.coeff.identity or f.strategy == "reference":
+        return
+    g = _geo(f.config)
+    if "std_plans" not in g:
+        return
+    lays = [[g["std_plans"][d].layout] for d in (0, 1)]
+    if f.strategy == "dwq":
+        for (d, u) in dwq_keys(f):
+            pk = ("dwq_plan", d, u)
+            if pk not in g:
+                return
+            lays[d].append(g[pk].aug)
+    s = _named_stream("grids", priority=-3)
+    main = torch.cuda.current_stream()
+    with _forked(main, s):
+        keep = []
+        ptrs = np.zeros(len(lays[0]) * len(lays[1]), dtype=np.uint64)
+        for a, l1 in enumerate(lays[0]):
+            for c, l2 in enumerate(lays[1]):
+                grid = f.coeff.grid_device(l1.device_points(), l2.device_points())
+                keep.append(grid)
+                ptrs[a * len(lays[1]) + c] = grid.data_ptr()
+        table = L.dev(ptrs.view(np.int64), torch.int64)
+        ev = torch.cuda.Event()
+        ev.record()
+    for st in (main, _side_streams(1)[0]):
+        _keep_on(st, keep + [table])
+    f._grids_pre = (lays, table, ev, keep)
+
+
+def _gather_ctx(f, eg, em, cut, desc_dev, raw, ndesc):
+    """Context of tq_cut_rows_gather before the rule sets exist."""
+    ctx = _gauss_ctx(f, eg, em, None, desc_dev, raw, ndesc)
+    if cut is not None:
+        cc = _cut_blocks_ctx(f, cut)
+        for k in ("cutidx", "cut_ptr", "cut_cw", "cfirst1", "cvals1", "cfirst2", "cvals2", "grp_ptr", "grp_key",
+                  "grp_pts", "grp_perm", "ngroups"):
+            setattr(ctx, k, getattr(cc, k))
+    return ctx
+
+
 def prelaunch_geometry(f):
     """Start the WQ-independent raw-row work of a captured pass on its own
     stream, overlapping the fits: element tables, the element-Gauss part of
@@ -854,6 +909,21 @@ def prelaunch_geometry(f):
         from .assembly import _stamp
         _stamp("cutpre:blocks")
     s.wait_stream(s2)         # one stream to join later
+    if pm:
+        # the cut rows' element parts need no weights: gathered on the
+        # pass-start stream as soon as both block sets exist
+        desc, nint = _plan(f)
+        if ndesc > nint:
+            f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)     # (main: before every user)
+            with _forked(main, s):
+                Eg, gslot = f._gpairs
+                Ec = getattr(f, "_cpairs", None)
+                rg_ptr, rg = cut_row_groups(f, nint, ndesc) if Ec is not None else (None, None)
+                L.call("tq_cut_rows_gather", _gather_ctx(f, eg, em, cut, desc_dev, f._raw_pre, ndesc), nint, ndesc,
+                       L.ptr(gslot), L.ptr(Eg), L.ptr(Ec), L.ptr(rg_ptr), L.ptr(rg), L.ptr(f._planes_status),
+                       L.stream())
+                _st("preA:gather")
+            f._gathered = True
     # tensors made here are consumed on the main and raw side streams
     tensors = [t for t in (cut or {}).values() if isinstance(t, torch.Tensor)]
     tensors += [t for e in eg for t in e if isinstance(t, torch.Tensor)] + list(em) + [f._raw_pre]
@@ -1105,7 +1175,8 @@ def run_phase(f, phase):
             ctx_int = RawCtx.from_buffer_copy(f._ctx)
             ctx_int.nmax1, ctx_int.nmax2 = f._setup.nmax_std
             f._ctx_int = ctx_int
-            f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
+            if getattr(f, "_planes_status", None) is None:
+                f._planes_status = torch.zeros(1, dtype=torch.int32, device=f.dev)
             f._bw = torch.empty(max(int(L.lib().tq_bw_table_doubles(ctx_int)), 1), dtype=torch.float64,
                                 device=f.dev)
             L.call("tq_bw_tables", ctx_int, L.ptr(f._bw), L.ptr(f._planes_status), L.stream())
@@ -1131,6 +1202,9 @@ def run_phase(f, phase):
                 join_cut_blocks(f)
                 Eg, gslot = f._gpairs
                 Ec = getattr(f, "_cpairs", None)
+                if getattr(f, "_gathered", False):       # gathered at pass start
+                    L.call("tq_raw_sumfactor", f._ctx, f._nint, f._ndesc, L.stream())
+                    return
             else:
                 Eg, gslot = _gauss_pairs(f, f._setup.eg, f._setup.em)
                 Ec = _cut_pairs(f, f._setup.cut) if f._setup.cut is not None else None

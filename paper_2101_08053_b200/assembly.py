@@ -603,8 +603,9 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     clk = _Clock(active=capture is None and timed)
     _stamp("start")
     if capture is not None:
-        from ._rawrows import prelaunch_counts, prelaunch_geometry
+        from ._rawrows import prelaunch_counts, prelaunch_geometry, prelaunch_grids
         prelaunch_counts(f)
+        prelaunch_grids(f)
         prelaunch_geometry(f)
     f.build_weights(rules)
     _stamp("weights")
