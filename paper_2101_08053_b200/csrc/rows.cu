@@ -686,6 +686,11 @@ __global__ void k_pos2_cmp(tq_rowctx c, int8_t* __restrict__ pos, const int8_t* 
     }
 }
 
+__global__ void k_copy_i32(int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = src[t];
+}
+
 __global__ void k_counts_cached_guard(int* __restrict__ flags, int32_t* __restrict__ work,
                                       int32_t* __restrict__ ctl) {
     const int redo = flags[0] | flags[1];
@@ -830,12 +835,17 @@ extern "C" int tq_row_counts_cached(tq_rowctx c, const int8_t* geo, int8_t* pos,
     if (nrows <= 0) return TQ_OK;
     if (!c.a1 || !c.a2 || !c.tiles) { set_error("tq_row_counts_cached needs the separable factors and tiles"); return TQ_EINVAL; }
     cudaStream_t st = S(stream);
-    TQ_CUDA(cudaMemcpyAsync(c.tiles, tiles0, sizeof(int32_t) * (size_t)TQ_TILE_INTS(nrows), cudaMemcpyDeviceToDevice, st));
+    // (a kernel copy: a device-to-device memcpy node in a captured graph
+    // goes to a copy engine and sits on the pass's critical path)
+    const int64_t nt = TQ_TILE_INTS(nrows);
+    k_copy_i32<<<grid_for(nt, 256), 256, 0, st>>>(c.tiles, tiles0, nt); ::tq::note_launch();
     TQ_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
     k_pos2_cmp<<<grid_for(c.n1 + c.n2, 128), 128, 0, st>>>(c, pos, pos_cached, flags); ::tq::note_launch();
     k_counts_cached_guard<<<1, 1, 0, st>>>(flags, work, c.tiles + TQ_TILE_CTL(nrows)); ::tq::note_launch();
-    k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, st>>>(c, geo, pos, counts, work + 2, work,
-                                                                   work + 2 + nrows, work + 1, flags + 2);
+    // guarded redo (a no-op unless the positivity changed): a capped grid
+    k_row_counts_deep<true><<<std::min(grid_for(nrows, 256), kSms * 8), 256, 0, st>>>(c, geo, pos, counts, work + 2,
+                                                                                      work, work + 2 + nrows,
+                                                                                      work + 1, flags + 2);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("tq_row_counts_cached");
     return TQ_OK;
