@@ -12,6 +12,7 @@ Every raw row also collects the cut-element points (``tq_raw_cutcells``).
 
 from __future__ import annotations
 
+import contextlib
 import os
 import ctypes as C
 
@@ -54,7 +55,7 @@ def _bind():
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
-    L.optional("tq_sf_strips", [RawCtx, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_sf_strips", [RawCtx, L.i32, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
     L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp,
                                   L.vp])
@@ -353,6 +354,10 @@ def needs_raw(f):
 # two count passes (A/B and the parity tests)
 PLANES = os.environ.get("TQ_PLANES", "1") != "0"
 STRIP_ROWS = 16
+# 8-row strips of their own for the long-rule functions at the ends of
+# direction 2 (smaller shared stage for the other strips); measured: more
+# total kernel time at config 4 p = 8 (fixed per-strip cost), off
+EDGE_STRIPS = os.environ.get("TQ_EDGE_STRIPS", "0") == "1"
 
 
 def planes(f):
@@ -381,57 +386,73 @@ def planes_geo(f):
         slot = torch.full((f.b1.n * f.b2.n,), -1, dtype=torch.int32, device=f.dev)
         if fid.size:
             slot[torch.as_tensor(fid, device=f.dev)] = torch.as_tensor(store.astype(np.int32), device=f.dev)
-        # strips: interior rows [0, nint) grouped by (i1, i2 // STRIP_ROWS)
+        # interior rows [0, nint) for the strips (grouped per layout in strip_classes)
         n2 = f.b2.n
         i1, i2 = fid[:nint] // n2, fid[:nint] % n2
         full = ((desc[:nint, 1] == MODE_BOX) & (desc[:nint, 2] == 0) & (desc[:nint, 3] == 0)
                 & (desc[:nint, 4] == f.b1._el_first[i1]) & (desc[:nint, 5] == f.b1._el_last[i1])
                 & (desc[:nint, 6] == f.b2._el_first[i2]) & (desc[:nint, 7] == f.b2._el_last[i2]))
-        strips = np.empty((0, 2 + STRIP_ROWS), np.int32)
-        if nint and full.all():
-            skey = i1 * ((n2 + STRIP_ROWS - 1) // STRIP_ROWS) + i2 // STRIP_ROWS
-            uk, inv = np.unique(skey, return_inverse=True)
-            strips = np.full((uk.size, 2 + STRIP_ROWS), -1, np.int32)
-            strips[inv, 0] = i1
-            strips[inv, 1] = (i2 // STRIP_ROWS) * STRIP_ROWS
-            strips[inv, 2 + i2 % STRIP_ROWS] = store[:nint]
+        interior = (i1, i2, store[:nint])
         g[key] = dict(base=base, store=L.dev(store.astype(np.int32), torch.int32), slot=slot,
-                      strips_h=strips, strips=L.dev(strips if strips.size else np.zeros(1, np.int32), torch.int32),
-                      nstrips=int(strips.shape[0]), strip_ok=bool(nint == 0 or full.all()), ld=int(col.size))
+                      interior=interior, strip_ok=bool(nint == 0 or full.all()), ld=int(col.size))
     return g[key]
 
 
 def strip_classes(f, pg, layout1, layout2):
-    """The strips split into launches by shared-memory need: the regular
-    strips (rule rows no longer than the median support's points, the
-    interior of a uniform mesh) and the rest (boundary lines), each launch
-    with its own capacities (n1m, n2m) and union-window bound nu_max.  A WQ
-    rule row lies in its support's points, so the support point counts bound
-    the rows; the kernel flags any row that breaks them.  Cached per (plan,
-    layouts): [(strips_dev, nstrips, n1m, n2m, nu_max)]."""
+    """The interior rows grouped into strips and the strips split into
+    launches by shared-memory need (cached per plan and layouts).  A WQ rule
+    row lies in its support's points, so the support point counts bound the
+    rows (the kernel flags any row that breaks them).  The functions at the
+    ends of direction 2 whose rules are longer than the median (the boundary
+    functions of an open knot vector) form 8-row strips of their own; the
+    rest form 16-row strips aligned after them.  Launches: 16-row strips on
+    regular lines, 16-row strips on long-rule lines, 8-row edge strips --
+    each [(rows per strip, strips_dev, nstrips, n1m, n2m, nu_max)]."""
     g = _geo(f.config)
     key = ("strip_classes", id(pg), id(layout1), id(layout2))
     if key not in g:
-        st = pg["strips_h"]
+        i1, i2, sto = pg["interior"]
         out = []
-        if st.shape[0]:
+        if i1.size:
             b1, b2 = f.b1, f.b2
             o1, o2 = layout1.offsets, layout2.offsets
             cnt1 = o1[b1._el_last + 1] - o1[b1._el_first]
             cnt2 = o2[b2._el_last + 1] - o2[b2._el_first]
-            rows = st[:, 2:] >= 0
-            t = np.arange(STRIP_ROWS)
-            i2 = np.minimum(st[:, 1:2] + t[None, :], b2.n - 1)
-            lo = np.where(rows, t[None, :], STRIP_ROWS).min(axis=1)
-            hi = np.where(rows, t[None, :], -1).max(axis=1)
-            c1 = cnt1[st[:, 0]]
-            c2 = np.where(rows, cnt2[i2], 0).max(axis=1)
-            nu = o2[b2._el_last[st[:, 1] + hi] + 1] - o2[b2._el_first[st[:, 1] + lo]]
-            reg = (c1 <= int(np.median(cnt1))) & (c2 <= int(np.median(cnt2)))
-            for sel in (reg, ~reg):
-                if sel.any():
-                    out.append((L.dev(np.ascontiguousarray(st[sel]), torch.int32), int(sel.sum()),
-                                int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1)))
+            med1, med2 = int(np.median(cnt1)), int(np.median(cnt2))
+            long2 = (cnt2 > med2) & EDGE_STRIPS
+            half = b2.n // 2
+            lo_l, hi_l = np.nonzero(long2[:half])[0], np.nonzero(long2[half:])[0]
+            e_lo = int(lo_l.max()) + 1 if lo_l.size else 0                 # edge: [0, e_lo)
+            mid_end = half + int(hi_l.min()) if hi_l.size else b2.n         # edge: [mid_end, n2)
+            edge = (i2 < e_lo) | (i2 >= mid_end)
+            # column chunk start of every interior row
+            start = np.where(i2 < e_lo, (i2 // 8) * 8,
+                             np.where(i2 >= mid_end, mid_end + ((i2 - mid_end) // 8) * 8,
+                                      e_lo + ((i2 - e_lo) // STRIP_ROWS) * STRIP_ROWS))
+            for ts, sel_rows in ((STRIP_ROWS, ~edge), (8, edge)):
+                if not sel_rows.any():
+                    continue
+                r1_, s_, t_, st_ = i1[sel_rows], start[sel_rows], i2[sel_rows] - start[sel_rows], sto[sel_rows]
+                skey = r1_.astype(np.int64) * (b2.n + 1) + s_
+                uk, inv = np.unique(skey, return_inverse=True)
+                strips = np.full((uk.size, 2 + ts), -1, np.int32)
+                strips[inv, 0] = r1_
+                strips[inv, 1] = s_
+                strips[inv, 2 + t_] = st_
+                rows = strips[:, 2:] >= 0
+                t = np.arange(ts)
+                ii2 = np.minimum(strips[:, 1:2] + t[None, :], b2.n - 1)
+                lo = np.where(rows, t[None, :], ts).min(axis=1)
+                hi = np.where(rows, t[None, :], -1).max(axis=1)
+                c1 = cnt1[strips[:, 0]]
+                c2 = np.where(rows, cnt2[ii2], 0).max(axis=1)
+                nu = o2[b2._el_last[strips[:, 1] + hi] + 1] - o2[b2._el_first[strips[:, 1] + lo]]
+                reg = (c1 <= med1) & (c2 <= med2)
+                groups = (reg, ~reg) if ts == STRIP_ROWS else (c1 <= med1, c1 > med1)
+                for sel in groups:
+                    if sel.any():
+                        out.append((ts, L.dev(np.ascontiguousarray(strips[sel]), torch.int32), int(sel.sum()),
+                                    int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1)))
         g[key] = out
         g[key + ("keep",)] = (layout1, layout2)       # the ids stay valid
     return g[key]
@@ -1180,11 +1201,21 @@ def run_phase(f, phase):
             f._bw = torch.empty(max(int(L.lib().tq_bw_table_doubles(ctx_int)), 1), dtype=torch.float64,
                                 device=f.dev)
             L.call("tq_bw_tables", ctx_int, L.ptr(f._bw), L.ptr(f._planes_status), L.stream())
-            for strips, ns, n1m, n2m, nu in strip_classes(f, pg, f._setup.sets[0][0].layout,
-                                                          f._setup.sets[1][0].layout):
-                L.call("tq_sf_strips", ctx_int, L.ptr(strips), ns, n1m, n2m, nu, L.ptr(f._bw),
-                       L.ptr(f._planes_status), L.stream())
-                _st(f"strips{n2m}")
+            # the launches write disjoint rows: the smaller ones run beside
+            # the main one on side streams (their tails overlap)
+            classes = strip_classes(f, pg, f._setup.sets[0][0].layout, f._setup.sets[1][0].layout)
+            main = torch.cuda.current_stream()
+            sides = []
+            for k, (ts, strips, ns, n1m, n2m, nu) in enumerate(classes):
+                st = main if k == 0 else _named_stream(f"strips{k}", priority=-2)
+                with (contextlib.nullcontext() if k == 0 else _forked(main, st)):
+                    L.call("tq_sf_strips", ctx_int, ts, L.ptr(strips), ns, n1m, n2m, nu, L.ptr(f._bw),
+                           L.ptr(f._planes_status), L.stream())
+                if k:
+                    sides.append(st)
+            for st in sides:
+                main.wait_stream(st)
+            _st("strips")
         elif nint:
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)

@@ -497,13 +497,13 @@ __global__ void __launch_bounds__(kPlThreads, 4) k_planes_csr(tq_rowctx c, int32
 
 using namespace tq;
 
-template <int P>
+template <int P, int TS>
 static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
                             int32_t nu_max, const double* bw1, const double* bw2, int32_t* status, cudaStream_t st) {
-    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, kStripRows);
+    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, TS);
     if (shm > 220 * 1024) { set_error("strip workspace too large (%zu bytes)", shm); return TQ_EINVAL; }
-    auto kern = k_sf_strips<P, kStripRows>;
-    constexpr int NT = 32 * ((kStripRows * 9 + 31) / 32) + 32;
+    auto kern = k_sf_strips<P, TS>;
+    constexpr int NT = 32 * ((TS * 9 + 31) / 32) + 32;
     TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     int per_sm = 0;
     TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, shm));
@@ -530,8 +530,9 @@ extern "C" int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stre
     return TQ_OK;
 }
 
-extern "C" int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
-                            int32_t nu_max, const double* bw, int32_t* status, void* stream) {
+extern "C" int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, int32_t nstrips, int32_t n1m,
+                            int32_t n2m, int32_t nu_max, const double* bw, int32_t* status, void* stream) {
+    if (rows != kStripRows && rows != 8) { set_error("strips of %d rows (16 or 8)", rows); return TQ_EINVAL; }
     if (nstrips <= 0) return TQ_OK;
     if (!c.grids || !c.raw_ld || c.p1 != c.p2) { set_error("tq_sf_strips needs coefficient grids, planes and p1 == p2"); return TQ_EINVAL; }
     if (c.p1 < 1 || c.p1 > kMaxP) { set_error("degree out of range"); return TQ_EINVAL; }
@@ -539,7 +540,10 @@ extern "C" int tq_sf_strips(tq_rawctx c, const int32_t* strips, int32_t nstrips,
     const double* bw1 = bw;
     const double* bw2 = bw + (int64_t)c.n1 * bw_row(c.p1, c.nmax1);
     switch (c.p1) {
-#define CASE(Q) case Q: return sf_strips_launch<Q>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status, S(stream));
+#define CASE(Q) case Q: return rows == 8 ? sf_strips_launch<Q, 8>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, \
+                                                                      status, S(stream)) \
+                                          : sf_strips_launch<Q, kStripRows>(c, strips, nstrips, n1m, n2m, nu_max, \
+                                                                            bw1, bw2, status, S(stream));
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     }
