@@ -21,6 +21,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -586,6 +587,12 @@ def run_ours(args, rank, world, local_rank):
     if args.e2e_steps > 0:
         knots = np.ascontiguousarray(P.make_uniform_knots(args.nel, args.p).knots)
         ctrl = np.ascontiguousarray(c5["curves"][0].ctrl)
+        # the ~185k objects alive after setup (torch/scipy modules, plans)
+        # move to the permanent generation: a full collection landing inside
+        # a step then scans only what that step made (~45 ms otherwise,
+        # scripts/probes/gc_census.py), the usual serving-process setting
+        gc.collect()
+        gc.freeze()
         e_ts, e_ph, h2d, d2h = [], [], 0, 0
         for k in range(args.e2e_steps + 1):
             barrier()
