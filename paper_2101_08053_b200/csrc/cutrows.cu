@@ -450,6 +450,131 @@ k_cut_rows_gather(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot
     }
 }
 
+// Element-major form of the same gather.  The row block is accumulated in
+// shared memory; element e with first functions (F1, F2) adds
+// E_e[pair(i1 - F1, b1)][pair(i2 - F2, b2)] to entry (F1 + b1 - i1 + P,
+// F2 + b2 - i2 + P).  Entry line o1 belongs to warp o1 mod NWG, so every
+// entry is updated by one warp only; within a warp the lanes cover (b1, b2)
+// pairs of one element at a time (distinct entries) and the elements are
+// walked in the entry-major kernel's order -- Gauss elements (k1, k2)
+// ascending, then the row's groups in list order -- with a warp barrier
+// between elements.  Every entry receives the same additions in the same
+// order as in k_cut_rows_gather (bit-identical), at one load per element and
+// lane instead of a predicated Q x Q sweep per entry.
+template <int P>
+struct GatherEm {
+    static constexpr int Q = P + 1, MB = 32 / Q, NWG = (Q + MB - 1) / MB;
+};
+
+template <int P>
+__global__ void __launch_bounds__(32 * GatherEm<P>::NWG)
+k_cut_rows_gather_em(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ gslot, const double* __restrict__ Eg,
+                     const double* __restrict__ Ec, const int32_t* __restrict__ rg_ptr, const int32_t* __restrict__ rg,
+                     int* __restrict__ status) {
+    constexpr int Q = P + 1, W = 2 * P + 1, T = W * W, NP = Pairs<Q>::NP, QQ = Q * Q, GB = 8;
+    constexpr int MB = GatherEm<P>::MB, NWG = GatherEm<P>::NWG, NT = 32 * NWG;
+    __shared__ double acc[T];
+    __shared__ int S[QQ], F1[Q], F2[Q], pidx[Q][Q];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int t = tid; t < QQ; t += NT) {
+        const int a = t / Q, b = t - (t / Q) * Q;
+        pidx[a][b] = a <= b ? Pairs<Q>::of(a, b) : Pairs<Q>::of(b, a);
+    }
+    const bool lact = lane < MB * Q;
+    const int b2 = lane % Q, m = lane / Q;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const RowDescC d = reinterpret_cast<const RowDescC*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const int ef1 = c.el_first1[i1], ef2 = c.el_first2[i2];
+        const int ne1 = c.el_last1[i1] - ef1 + 1, ne2 = c.el_last2[i2] - ef2 + 1;
+        const bool gauss = d.mode == TQ_ROW_GAUSS || d.mode == TQ_ROW_BOX;
+        const bool box = d.mode == TQ_ROW_BOX && d.a1 >= 0;
+        __syncthreads();          // the previous row's block is written out
+        for (int t = tid; t < T; t += NT) acc[t] = 0.0;
+        for (int t = tid; t < QQ; t += NT) {
+            const int k1 = t / Q, k2 = t - (t / Q) * Q;
+            int sl = -1;
+            if (gauss && k1 < ne1 && k2 < ne2) {
+                const int e1 = ef1 + k1, e2 = ef2 + k2;
+                const int64_t e = (int64_t)e1 * c.nel2 + e2;
+                const bool inbox = box && e1 >= d.a1 && e1 <= d.b1 && e2 >= d.a2 && e2 <= d.b2;
+                if (c.elem_class[e] == TQ_INTERIOR && !inbox) {
+                    sl = gslot[e];
+                    if (sl < 0) atomicOr(status, 4);      // the element list missed it: flagged
+                }
+            }
+            S[t] = sl;
+            if (k2 == 0) F1[k1] = k1 < ne1 ? c.espan1[ef1 + k1] - P : 0;
+            if (k1 == 0) F2[k2] = k2 < ne2 ? c.espan2[ef2 + k2] - P : 0;
+        }
+        __syncthreads();
+        // lane -> b1 of this warp's entry lines for an element starting at f1
+        auto lane_b1 = [&](int f1) {
+            const int base = f1 - i1 + P;                     // o1 of b1 = 0
+            const int start = ((warp - base) % NWG + NWG) % NWG;
+            return start + NWG * m;
+        };
+        // per-lane direction-2 parts of the support columns k2 (fixed over k1)
+        int A2[Q], O2[Q];
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2) {
+            const int f2 = F2[k2];
+            const bool ok2 = k2 < ne2;
+            A2[k2] = ok2 ? pidx[i2 - f2][b2] : 0;
+            O2[k2] = f2 + b2 - i2 + P;
+        }
+        // Gauss elements, (k1, k2) ascending: one support line k1 per batch
+        for (int k1 = 0; k1 < ne1; ++k1) {
+            const int f1 = F1[k1], b1 = lane_b1(f1);
+            const bool ok1 = lact && b1 < Q;
+            const int A1 = ok1 ? pidx[i1 - f1][b1] * NP : 0;
+            const int o1w = (f1 + b1 - i1 + P) * W;
+            double v[Q];
+            int sl[Q];
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) {
+                sl[k2] = S[k1 * Q + k2];
+                v[k2] = (ok1 && sl[k2] >= 0) ? __ldg(Eg + ((int64_t)sl[k2] * (NP * NP) + A1 + A2[k2])) : 0.0;
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) {
+                if (ok1 && sl[k2] >= 0) acc[o1w + O2[k2]] += v[k2];
+                __syncwarp();
+            }
+        }
+        // span-key groups of the row, list order
+        if (Ec) {
+            const int gb = rg_ptr[r - r0], ge = rg_ptr[r - r0 + 1];
+            for (int k0 = gb; k0 < ge; k0 += GB) {
+                double v[GB];
+                int at[GB];
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
+                    const int k = k0 + u;
+                    v[u] = 0.0;
+                    at[u] = -1;
+                    if (k < ge) {
+                        const int g = __ldg(rg + 3 * k), f1 = __ldg(rg + 3 * k + 1), f2 = __ldg(rg + 3 * k + 2);
+                        const int b1 = lane_b1(f1);
+                        if (lact && b1 < Q) {
+                            v[u] = __ldg(Ec + ((int64_t)g * (NP * NP) + pidx[i1 - f1][b1] * NP + pidx[i2 - f2][b2]));
+                            at[u] = (f1 + b1 - i1 + P) * W + (f2 + b2 - i2 + P);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
+                    if (at[u] >= 0) acc[at[u]] += v[u];
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        const int64_t st = c.store[r];
+        for (int t = tid; t < T; t += NT) c.raw[(int64_t)t * c.raw_ld + st] = acc[t];
+    }
+}
+
 }  // namespace tq
 
 using namespace tq;
@@ -534,9 +659,19 @@ extern "C" int tq_cut_rows_gather(tq_rawctx c, int32_t r0, int32_t r1, const int
                                   void* stream) {
     if (r1 <= r0) return TQ_OK;
     if (!c.raw_ld || !c.store || c.p1 != c.p2) { set_error("tq_cut_rows_gather needs the planes layout and p1 == p2"); return TQ_EINVAL; }
-    const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * 16);
+    // element-major (default; 127 -> 91 us at config 4 p = 8, bit-identical)
+    // or the entry-major kernel (TQ_GATHER_EM=0: A/B and the equality test)
+    static int em = -1;
+    if (em < 0) {
+        const char* e = getenv("TQ_GATHER_EM");
+        em = e ? atoi(e) : 1;
+    }
+    const int grid = (int)std::min<int64_t>(r1 - r0, (int64_t)kSms * (em ? 32 : 16));
     switch (c.p1) {
-#define CASE(Q) case Q: k_cut_rows_gather<Q><<<grid, 32 * (((2 * Q + 1) * (2 * Q + 1) + 31) / 32), 0, S(stream)>>>( \
+#define CASE(Q) case Q: \
+        if (em) k_cut_rows_gather_em<Q><<<grid, 32 * GatherEm<Q>::NWG, 0, S(stream)>>>(c, r0, r1, gslot, Eg, Ec, rg_ptr, \
+                                                                                      rg, status); \
+        else k_cut_rows_gather<Q><<<grid, 32 * (((2 * Q + 1) * (2 * Q + 1) + 31) / 32), 0, S(stream)>>>( \
             c, r0, r1, gslot, Eg, Ec, rg_ptr, rg, status); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE

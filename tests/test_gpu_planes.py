@@ -187,3 +187,38 @@ def test_coefficient_kernels_against_host_det_j(p):
     P = np.stack(np.meshgrid(u, v, indexing="ij"), axis=-1).reshape(-1, 2)
     pts = gm.at_host(P).reshape(7, 5)
     np.testing.assert_allclose(pts, ref, rtol=1e-12)
+
+
+_GATHER_SNIPPET = """
+import hashlib, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+from paper_2101_08053_b200 import cases as C, assembly as A
+for p, nel in ((4, 48), (6, 64), (8, 64)):
+    c4 = C.baseline_config(4, p=p, nel=nel)
+    b2d, cfg = C.build_space(None, nel, p, curves=c4["curves"])
+    for s in ("dwq", "hybrid"):
+        M = A.assemble_mass(b2d, cfg, c4["coeff"], strategy=s).data
+        h = hashlib.sha256()
+        for a in (M.indptr, M.indices, M.data):
+            h.update(np.ascontiguousarray(a).tobytes())
+        print(p, s, M.nnz, h.hexdigest())
+"""
+
+
+def test_cut_row_gather_element_major_bit_identical():
+    """k_cut_rows_gather_em (default) against the entry-major kernel
+    (TQ_GATHER_EM=0, read once per process): the same additions in the same
+    order per entry, so the CSR is bit-identical (p = 4, 6, 8; dwq and hybrid)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _GATHER_SNIPPET.format(root=root)
+    outs = []
+    for em in ("0", "1"):
+        env = dict(os.environ, TQ_GATHER_EM=em)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout)
+    assert outs[0] == outs[1] and len(outs[0].splitlines()) == 6
