@@ -314,16 +314,18 @@ def config4_secondary(p, nel=256, steps=20, seed=0):
                     f"{steps}"}
 
 
-def golden_check(args, world, csr):
+def golden_check(args, world, csr, rb=0, re_=None):
     """The timed CSR against the reference's own config-5 golden
     (tests/golden/config5.npz, written by make_golden.py --huge): nnz, the
-    pattern sha256 and the sampled rows (max bar 1e-12).  Runs after the
-    timed steps on the graph's output buffers; raises on any mismatch so a
-    bench number never stands for a wrong matrix.  -> summary dict or None
-    when no golden matches the workload."""
+    pattern sha256 and the sampled rows (max bar 1e-12); for a row block
+    (N > 1) the block's per-row nnz and the sampled rows that fall in it
+    (columns and values).  Runs after the timed steps on the graph's output
+    buffers; raises on any mismatch so a bench number never stands for a
+    wrong matrix.  -> summary dict or None when no golden matches the
+    workload."""
     import hashlib
     gpath = os.path.join(HERE, "tests", "golden", "config5.npz")
-    if (args.nel, args.p, args.seed, world) != (2048, 4, 0, 1) or args.strategy not in ("dwq", "hybrid") \
+    if (args.nel, args.p, args.seed) != (2048, 4, 0) or args.strategy not in ("dwq", "hybrid") \
             or not os.path.exists(gpath):
         return None
     g = np.load(gpath)
@@ -332,24 +334,40 @@ def golden_check(args, world, csr):
         return None
     ptr = csr.indptr.cpu().numpy()
     ind = csr.indices[:csr.nnz].cpu().numpy()
-    if csr.nnz != int(g[f"{s}_nnz"]):
-        raise SystemExit(f"bench: nnz {csr.nnz} != reference golden {int(g[f'{s}_nnz'])}")
-    h = hashlib.sha256()
-    for a in (ptr, ind):
-        h.update(str(a.dtype).encode())
-        h.update(np.ascontiguousarray(a).tobytes())
-    if h.hexdigest() != str(g[f"{s}_hash"]):
-        raise SystemExit("bench: CSR pattern sha256 differs from the reference golden")
     rows = g[f"{s}_rows"]
-    sel = np.concatenate([np.arange(ptr[r], ptr[r + 1]) for r in rows])
+    gptr = g[f"{s}_rowsptr"]
+    if world == 1:
+        if csr.nnz != int(g[f"{s}_nnz"]):
+            raise SystemExit(f"bench: nnz {csr.nnz} != reference golden {int(g[f'{s}_nnz'])}")
+        h = hashlib.sha256()
+        for a in (ptr, ind):
+            h.update(str(a.dtype).encode())
+            h.update(np.ascontiguousarray(a).tobytes())
+        if h.hexdigest() != str(g[f"{s}_hash"]):
+            raise SystemExit("bench: CSR pattern sha256 differs from the reference golden")
+        mine = np.arange(rows.size)
+    else:
+        re_ = int(ptr.size - 1 + rb) if re_ is None else re_
+        if not np.array_equal(np.diff(ptr), g[f"{s}_row_nnz"][rb:re_]):
+            raise SystemExit(f"bench: row block [{rb}, {re_}) per-row nnz differs from the reference golden")
+        mine = np.nonzero((rows >= rb) & (rows < re_))[0]
+    sel = np.concatenate([np.arange(ptr[r - rb], ptr[r - rb + 1]) for r in rows[mine]]) if mine.size else \
+        np.zeros(0, np.int64)
+    gsel = np.concatenate([np.arange(gptr[k], gptr[k + 1]) for k in mine]) if mine.size else np.zeros(0, np.int64)
+    if not np.array_equal(ind[sel], g[f"{s}_rowsidx"][gsel]):
+        raise SystemExit("bench: sampled rows' columns differ from the reference golden")
     got = csr.data[torch_index(sel, csr.data.device)].cpu().numpy()
-    ref = g[f"{s}_rowsdata"]
-    err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+    ref = g[f"{s}_rowsdata"][gsel]
+    err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))) if sel.size else 0.0
     if not err <= 1e-12:
         raise SystemExit(f"bench: sampled rows differ from the reference golden (max rel {err:.3g})")
-    return {"golden": "tests/golden/config5.npz (reference run at 2048^2)", "nnz": "equal",
-            "pattern_sha256": "equal", "rows_checked": int(rows.size), "entries_checked": int(sel.size),
-            "max_abs_err_over_max_abs": err}
+    out = {"golden": "tests/golden/config5.npz (reference run at 2048^2)", "rows_checked": int(mine.size),
+           "entries_checked": int(sel.size), "max_abs_err_over_max_abs": err}
+    if world == 1:
+        out.update({"nnz": "equal", "pattern_sha256": "equal"})
+    else:
+        out.update({"row_block": [int(rb), int(re_)], "row_nnz": "equal (this rank's block)"})
+    return out
 
 
 def torch_index(sel, device):
@@ -525,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
         barrier()
     nnz_local = gf.nnz
     clocks = sampler.stop()
-    parity = golden_check(args, world, gf.csr)
+    parity = golden_check(args, world, gf.csr, rb, re_)
     # kernels per step: the captured pass replays exactly the launches of one eager pass
     launches = gf.launches_per_pass * args.steps
     step_ms = [s.elapsed_time(e) for s, e in ev]
@@ -709,8 +727,17 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # TQ_BENCH_BACKEND=gloo (with ranks folded onto the visible GPUs) is
+        # the functional test of the N > 1 path on a one-GPU box
+        # (tests/test_gpu_bench_multirank.py); its timings are not bench values
+        backend = os.environ.get("TQ_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
