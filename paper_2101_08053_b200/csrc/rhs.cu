@@ -201,6 +201,10 @@ __global__ void k_l2_elements(tq_projctx c, const double* __restrict__ C, int64_
 // the terms of k_l2_elements (u_h, f, w exactly as there; the partial sums
 // in another order).
 constexpr int kL2Chunk = 64;
+// per-element staging stride (doubles): odd, so the 32 threads' rows fall on
+// distinct bank pairs (an even stride of 56 at P = 4 put every lane of a
+// half-warp on the same two banks: 16-way conflicts on every table read)
+__host__ __device__ constexpr int l2_stride(int P) { return ((P + 3) * (P + 1) + 3 * (P + 3)) | 1; }
 
 template <int P>
 __global__ void __launch_bounds__(kL2Chunk, 8) k_l2_elements_s(tq_projctx c, const double* __restrict__ C,
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kL2Chunk, 8) k_l2_elements_s(tq_projctx c, con
                                                                 double* __restrict__ parts) {
     extern __shared__ double sm[];
     __shared__ double red[2][kL2Chunk / 32];
-    constexpr int Q = P + 1, G = P + 3, ST = G * Q + 3 * G;     // per element: V2, y, w2, psi (one term)
+    constexpr int Q = P + 1, G = P + 3, ST = l2_stride(P);      // per element: V2, y, w2, psi (one term)
     constexpr int R1 = G * Q + 3 * G;                            // per element row: V1, x, w1, phi
     const bool sep = c.target.kind == 2 && c.target.nterms == 1;
     double* rows = sm + kL2Chunk * ST;                           // the chunk's (at most two) element rows
@@ -288,6 +292,120 @@ __global__ void __launch_bounds__(kL2Chunk, 8) k_l2_elements_s(tq_projctx c, con
                 const double w = r1[G * Q + G + g1] * w2;
                 num += w * (uh - f) * (uh - f);
                 den += w * f * f;
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, off);
+        den += __shfl_xor_sync(0xffffffffu, den, off);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { red[0][w] = num; red[1][w] = den; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, d = 0.0;
+        for (int k = 0; k < kL2Chunk / 32; ++k) { a += red[0][k]; d += red[1][k]; }
+        parts[2 * blockIdx.x] = a;
+        parts[2 * blockIdx.x + 1] = d;
+    }
+}
+
+// Tiled form of k_l2_elements_s: a block takes a tile of kL2Rows element rows
+// x kL2Chunk element columns, stages the columns' direction-2 tables ONCE for
+// the tile's rows (k_l2_elements_s re-staged them for every row: the staging
+// loads, not the sums, set its time) and the rows' direction-1 tables, and a
+// thread walks its column down the tile's rows.  Per element the terms and
+// their order are those of k_l2_elements_s; only the order of the partial
+// sums over elements changes.
+constexpr int kL2Rows = 16;
+
+template <int P>
+__global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const double* __restrict__ C,
+                                                         int64_t e_begin, int64_t e_end, double* __restrict__ parts) {
+    extern __shared__ double sm[];
+    __shared__ double red[2][kL2Chunk / 32];
+    constexpr int Q = P + 1, G = P + 3, ST = l2_stride(P);
+    constexpr int R1 = G * Q + 3 * G;                            // per element row: V1, x, w1, phi
+    const bool sep = c.target.kind == 2 && c.target.nterms == 1;
+    double* rows = sm + kL2Chunk * ST;                           // [kL2Rows][R1]
+    double num = 0.0, den = 0.0;
+    const int r_first = (int)(e_begin / c.nel2), r_last = (int)((e_end - 1) / c.nel2);
+    const int nrt = (r_last - r_first + kL2Rows) / kL2Rows, nct = (c.nel2 + kL2Chunk - 1) / kL2Chunk;
+    const int64_t ntiles = (int64_t)nrt * nct;
+    const double tk = sep ? c.target.terms[0] : 0.0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int rt = (int)(tile / nct), ct = (int)(tile - (int64_t)rt * nct);
+        const int e1a = r_first + rt * kL2Rows, e2a = ct * kL2Chunk;
+        const int nr = min(kL2Rows, r_last + 1 - e1a), ncol = min(kL2Chunk, c.nel2 - e2a);
+        __syncthreads();
+        for (int q = threadIdx.x; q < ncol * (G * Q); q += kL2Chunk) {
+            const int j = q / (G * Q), k = q - j * (G * Q);
+            sm[j * ST + k] = c.v2[(int64_t)(e2a + j) * G * Q + k];
+        }
+        for (int q = threadIdx.x; q < ncol * G; q += kL2Chunk) {
+            const int j = q / G, g = q - j * G;
+            const int64_t pc = (int64_t)(e2a + j) * G + g;
+            double* o = sm + j * ST + G * Q;
+            o[g] = c.x2[pc];
+            o[G + g] = c.w2[pc];
+            o[2 * G + g] = sep ? c.target.grid[c.target.ld + pc] : 0.0;
+        }
+        for (int q = threadIdx.x; q < nr * R1; q += kL2Chunk) {
+            const int rr = q / R1, k = q - rr * R1;
+            const int e1 = e1a + rr;
+            double v;
+            if (k < G * Q) v = c.v1[(int64_t)e1 * G * Q + k];
+            else if (k < G * Q + G) v = c.x1[(int64_t)e1 * G + (k - G * Q)];
+            else if (k < G * Q + 2 * G) v = c.w1[(int64_t)e1 * G + (k - G * Q - G)];
+            else v = sep ? c.target.grid[(int64_t)e1 * G + (k - G * Q - 2 * G)] : 0.0;
+            rows[rr * R1 + k] = v;
+        }
+        __syncthreads();
+        const int j = threadIdx.x;
+        if (j >= ncol) continue;
+        const int e2 = e2a + j;
+        const int f2 = c.espan2[e2] - P;
+        const double* s2 = sm + j * ST;
+        for (int rr = 0; rr < nr; ++rr) {
+            const int e1 = e1a + rr;
+            const int64_t t = (int64_t)e1 * c.nel2 + e2;
+            if (t < e_begin || t >= e_end || c.elem_class[t] != TQ_INTERIOR) continue;
+            const int f1 = c.espan1[e1] - P;
+            const double* r1 = rows + rr * R1;
+            double cb[Q][Q];
+#pragma unroll
+            for (int a1 = 0; a1 < Q; ++a1)
+#pragma unroll
+                for (int a2 = 0; a2 < Q; ++a2) cb[a1][a2] = C[(int64_t)(f1 + a1) * c.n2 + f2 + a2];
+#pragma unroll 1
+            for (int g2 = 0; g2 < G; ++g2) {
+                double S[Q];
+#pragma unroll
+                for (int a1 = 0; a1 < Q; ++a1) {
+                    double sa = 0.0;
+#pragma unroll
+                    for (int a2 = 0; a2 < Q; ++a2) sa += cb[a1][a2] * s2[g2 * Q + a2];
+                    S[a1] = sa;
+                }
+                const double y = s2[G * Q + g2], w2 = s2[G * Q + G + g2], psi = s2[G * Q + 2 * G + g2];
+                const int64_t pc = (int64_t)e2 * G + g2;
+#pragma unroll
+                for (int g1 = 0; g1 < G; ++g1) {
+                    double uh = 0.0;
+#pragma unroll
+                    for (int a1 = 0; a1 < Q; ++a1) uh += r1[g1 * Q + a1] * S[a1];
+                    double f;
+                    if (sep) {
+                        double acc = 0.0;
+                        acc += tk * r1[G * Q + 2 * G + g1] * psi;
+                        f = acc;
+                    } else {
+                        f = target_at(c, (int64_t)e1 * G + g1, pc, r1[G * Q + g1], y);
+                    }
+                    const double w = r1[G * Q + G + g1] * w2;
+                    num += w * (uh - f) * (uh - f);
+                    den += w * f * f;
+                }
             }
         }
     }
@@ -489,12 +607,18 @@ extern "C" int tq_l2_parts(tq_projctx c, const double* C, int64_t e_begin, int64
         const bool tq_t = c.p1 == c.p2 && c.g1n == c.p1 + 3 && c.g2n == c.p2 + 3 && c.p1 >= 1 && c.p1 <= 5 &&
                           c.nel2 >= kL2Chunk;
         if (tq_t) {
-            const int G = c.p1 + 3, Q = c.p1 + 1;
-            const size_t shm = sizeof(double) * (kL2Chunk + 2) * (G * Q + 3 * G);
+            static const bool tiled = !(getenv("TQ_L2_ROWS") && atoi(getenv("TQ_L2_ROWS")) == 1);   // A/B knob
+            const size_t shm = tiled ? sizeof(double) * (kL2Chunk * l2_stride(c.p1) + kL2Rows * l2_stride(c.p1))
+                                     : sizeof(double) * (kL2Chunk + 2) * l2_stride(c.p1);
             switch (c.p1) {
 #define CASE(P) case P: \
-                TQ_CUDA(cudaFuncSetAttribute(k_l2_elements_s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
-                k_l2_elements_s<P><<<nbe, kL2Chunk, shm, st>>>(c, C, e_begin, e_end, parts); break;
+                if (tiled) { \
+                    TQ_CUDA(cudaFuncSetAttribute(k_l2_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
+                    k_l2_tiles<P><<<nbe, kL2Chunk, shm, st>>>(c, C, e_begin, e_end, parts); \
+                } else { \
+                    TQ_CUDA(cudaFuncSetAttribute(k_l2_elements_s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
+                    k_l2_elements_s<P><<<nbe, kL2Chunk, shm, st>>>(c, C, e_begin, e_end, parts); \
+                } break;
                 CASE(1) CASE(2) CASE(3) CASE(4) CASE(5)
 #undef CASE
             }
