@@ -652,6 +652,7 @@ class _Setup:
         # rule sets
         self.sets = ([], [])
         self.grids = None
+        self.grids_all = None          # event: every rule-set pair's grid evaluated
         self.key_index = _key_index(f)
         if f.rules is not None:
             r1, r2, dwq = f.rules
@@ -684,9 +685,13 @@ class _Setup:
                 lays = ([s.layout for s in self.sets[0]], [s.layout for s in self.sets[1]])
                 if pre is not None and all(len(a) == len(b) and all(x is y for x, y in zip(a, b))
                                            for a, b in zip(pre[0], lays)):
-                    # computed at pass start on its own stream (prelaunch_grids)
-                    torch.cuda.current_stream().wait_event(pre[2])
+                    # computed at pass start on its own stream (prelaunch_grids):
+                    # the interior rows read the standard grid only; the
+                    # launches that read the DWQ sets' grids wait for all
+                    # (wait_all_grids)
+                    torch.cuda.current_stream().wait_event(pre[4])
                     self.grids = pre[1]
+                    self.grids_all = pre[2]
                 else:
                     ptrs = np.zeros(len(self.sets[0]) * len(self.sets[1]), dtype=np.uint64)
                     for a, s1 in enumerate(self.sets[0]):
@@ -704,6 +709,12 @@ class _Setup:
         # from the pass-start launch when the pass made one
         pre = getattr(f, "_cut_pre", None)
         self.cut = pre if pre is not None else (_cut_tables(f) if f.config.has_cuts() else None)
+
+    def wait_all_grids(self):
+        """Current stream waits until every rule-set pair's coefficient grid
+        exists (the pass-start grids signal the standard one first)."""
+        if self.grids_all is not None:
+            torch.cuda.current_stream().wait_event(self.grids_all)
 
     def ctx(self, desc, raw, nraw):
         f = self.f
@@ -863,20 +874,28 @@ def prelaunch_grids(f):
             lays[d].append(g[pk].aug)
     s = _named_stream("grids", priority=-3)
     main = torch.cuda.current_stream()
+    from .assembly import _padded_grid
     with _forked(main, s):
-        keep = []
-        ptrs = np.zeros(len(lays[0]) * len(lays[1]), dtype=np.uint64)
-        for a, l1 in enumerate(lays[0]):
-            for c, l2 in enumerate(lays[1]):
-                grid = f.coeff.grid_device(l1.device_points(), l2.device_points())
-                keep.append(grid)
-                ptrs[a * len(lays[1]) + c] = grid.data_ptr()
+        # every grid buffer first, so the pointer table is uploaded ahead of
+        # the evaluations; the standard x standard grid (the only one the
+        # interior strips read) is evaluated first and signalled on its own
+        pts = ([l.device_points() for l in lays[0]], [l.device_points() for l in lays[1]])
+        keep = [[_padded_grid(x1.numel(), x2.numel(), f.dev) for x2 in pts[1]] for x1 in pts[0]]
+        ptrs = np.array([g.data_ptr() for row in keep for g in row], dtype=np.uint64)
         table = L.dev(ptrs.view(np.int64), torch.int64)
+        ev_std = None
+        for a, x1 in enumerate(pts[0]):
+            for c, x2 in enumerate(pts[1]):
+                f.coeff.grid_device(x1, x2, out=keep[a][c])
+                if ev_std is None:
+                    ev_std = torch.cuda.Event()
+                    ev_std.record()
+        keep = [g for row in keep for g in row]
         ev = torch.cuda.Event()
         ev.record()
     for st in (main, _side_streams(1)[0]):
         _keep_on(st, keep + [table])
-    f._grids_pre = (lays, table, ev, keep)
+    f._grids_pre = (lays, table, ev, keep, ev_std)
 
 
 def _gather_ctx(f, eg, em, cut, desc_dev, raw, ndesc):
@@ -1238,6 +1257,7 @@ def run_phase(f, phase):
                 main.wait_stream(st)
             _st("strips")
         elif nint:
+            f._setup.wait_all_grids()
             if pre is not None:      # the sum-factor part adds onto the pass-start Gauss part
                 torch.cuda.current_stream().wait_event(f._elem_event)
             # interior rows read the standard rules only: their launch sizes its
@@ -1255,6 +1275,7 @@ def run_phase(f, phase):
                 Eg, gslot = f._gpairs
                 Ec = getattr(f, "_cpairs", None)
                 if getattr(f, "_gathered", False):       # gathered at pass start
+                    f._setup.wait_all_grids()
                     L.call("tq_raw_sumfactor", f._ctx, f._nint, f._ndesc, L.stream())
                     return
             else:
@@ -1267,6 +1288,7 @@ def run_phase(f, phase):
                           else (None, None))
             L.call("tq_cut_rows_gather", f._ctx, f._nint, f._ndesc, L.ptr(gslot), L.ptr(Eg), L.ptr(Ec),
                    L.ptr(rg_ptr), L.ptr(rg), L.ptr(f._planes_status), L.stream())
+            f._setup.wait_all_grids()
             L.call("tq_raw_sumfactor", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells" and pairs_mode(f):
         pass          # in the cut phase (tq_cut_rows_gather)
@@ -1275,6 +1297,7 @@ def run_phase(f, phase):
             pre = getattr(f, "_raw_pre", None) is not None
             if pre:
                 torch.cuda.current_stream().wait_event(f._elem_event)
+            f._setup.wait_all_grids()
             L.call("tq_raw_sumfactor" if pre else "tq_raw_regular", f._ctx, f._nint, f._ndesc, L.stream())
     elif phase == "cutcells":
         if f._setup.cut is not None:

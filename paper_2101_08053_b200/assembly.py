@@ -81,12 +81,13 @@ class CoefficientField:
             return self._device.at_device(P_dev)
         return L.dev(self.at(P_dev.cpu().numpy()), torch.float64)
 
-    def grid_device(self, x1_dev, x2_dev):
-        """c on the tensor grid x1 x x2 -> device (N1, N2)."""
+    def grid_device(self, x1_dev, x2_dev, out=None):
+        """c on the tensor grid x1 x x2 -> device (N1, N2) (into ``out``, a
+        ``_padded_grid``, when given)."""
         if self._device is not None:
-            return self._device.grid_device(x1_dev, x2_dev)
+            return self._device.grid_device(x1_dev, x2_dev, out)
         g = self.grid(x1_dev.cpu().numpy(), x2_dev.cpu().numpy())
-        out = _padded_grid(g.shape[0], g.shape[1], x1_dev.device)
+        out = _padded_grid(g.shape[0], g.shape[1], x1_dev.device) if out is None else out
         out.copy_(torch.as_tensor(g, dtype=torch.float64))
         return out
 
@@ -120,8 +121,8 @@ class GeometryMap:
             self._dev = (L.Coeff(1, self.p, self.n, L.ptr(k), L.ptr(X), L.ptr(Y)), (k, X, Y))
         return self._dev[0]
 
-    def grid_device(self, x1, x2):
-        out = _padded_grid(x1.numel(), x2.numel(), x1.device)
+    def grid_device(self, x1, x2, out=None):
+        out = _padded_grid(x1.numel(), x2.numel(), x1.device) if out is None else out
         L.call("tq_coeff_grid", self.device(), L.ptr(x1), x1.numel(), L.ptr(x2), x2.numel(), L.ptr(out), L.stream())
         return out
 
