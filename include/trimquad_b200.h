@@ -340,6 +340,11 @@ int tq_scan_indptr_ws(const int32_t* counts, int32_t nrows, int32_t* indptr, voi
  * of the tile sums -> tile bases (second half of c.tiles); indptr[nrows] = nnz.  nnz_h: as
  * tq_scan_indptr.  The fill kernels then write indptr[0 .. nrows). */
 int tq_scan_tiles(tq_rowctx c, int32_t* indptr, int64_t* nnz_h, void* stream);
+/* the nnz a captured (replayed) pass sized its output with: the following
+ * tq_scan_tiles compares its total against it; a mismatch sets the flag word
+ * TQ_TILE_CTL + 4 and the tile-mode fills (tq_fill_fast(_part),
+ * tq_fill_listed) then write nothing. */
+int tq_tiles_expect(tq_rowctx c, int64_t nnz, void* stream);
 int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices, double* data,
                  void* stream);
 /* tq_fill_rows split in two after tq_row_counts_deep/_rest: tq_fill_fast

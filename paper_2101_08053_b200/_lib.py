@@ -158,6 +158,7 @@ def lib():
         "tq_scan_indptr_ws": ([vp, i32, vp, vp, C.POINTER(i64), vp], i32),
         "tq_fill_rows": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_scan_tiles": ([RowCtx, vp, C.POINTER(i64), vp], i32),
+        "tq_tiles_expect": ([RowCtx, i64, vp], i32),
         "tq_scan_tiles_early": ([RowCtx, i64, i32, vp], i32),
         "tq_fill_fast_part": ([RowCtx, vp, vp, vp, i32, i32, vp], i32),
         "tq_fill_fast": ([RowCtx, vp, vp, vp, vp], i32),

@@ -509,6 +509,10 @@ class Formation:
         else:
             indptr, indices, data = out
         with self.timer("scan"):
+            if self.capture is not None and head is None:
+                # a replay must reproduce the captured nnz (its buffers' size):
+                # checked by the scan, the fill writes nothing otherwise
+                L.call("tq_tiles_expect", ctx, self.capture["nnz"], L.stream())
             L.call("tq_scan_tiles", ctx, L.ptr(indptr), None if self.capture else L.C.byref(nnz), L.stream())
         _stamp("scan")
         nnz = self.capture["nnz"] if self.capture else int(nnz.value)

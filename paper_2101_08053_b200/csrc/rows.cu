@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
     // Without tile mode: all tiles, static stride.
     const bool tm = c.tiles != nullptr;
     const int nr = c.row_end - c.row_begin, NT = (nr + kWarpRows - 1) / kWarpRows;
+    // the scan found another nnz than the captured pass sized the output
+    // with (tq_tiles_expect): write nothing
+    if (tm && part != 1 && c.tiles[TQ_TILE_CTL(nr) + 4]) return;
     const int32_t* tbase = tm ? (c.tiles + TQ_TILE_PAD(nr)) : nullptr;
     int tA = NT, tB = NT;
     if (tm && part) {
@@ -555,6 +558,7 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    if (c.tiles && c.tiles[TQ_TILE_CTL(c.row_end - c.row_begin) + 4]) return;     // see k_fill_tiles
     const int na = *irr_count, nrows = na + (irr_count_b ? *irr_count_b : 0);
     for (int u = warp; u < nrows; u += nw) {
         const int r = u < na ? irr_rows[u] : irr_rows_b[u - na];

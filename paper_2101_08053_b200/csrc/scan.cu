@@ -462,6 +462,25 @@ extern "C" int tq_active_index(const int8_t* func_class, int64_t nfun, int32_t* 
     return TQ_OK;
 }
 
+__global__ void k_tiles_expect(int32_t* __restrict__ ctl, int32_t nnz) {
+    ctl[5] = nnz;
+    ctl[6] = 1;
+}
+
+// The nnz a captured pass sized its output with: the next tq_scan_tiles
+// compares its total against it and sets TQ_TILE_CTL + 4 on a mismatch, and
+// the tile-mode fill kernels then write nothing (a replay whose counts moved
+// must not write past the captured buffers; GraphFormation.check raises).
+extern "C" int tq_tiles_expect(tq_rowctx c, int64_t nnz, void* stream) {
+    const int nrows = c.row_end - c.row_begin;
+    if (!c.tiles) { set_error("tq_tiles_expect needs the context's tiles"); return TQ_EINVAL; }
+    if (nnz < 0 || nnz > 0x7fffffffLL) { set_error("nnz %lld out of range", (long long)nnz); return TQ_EINVAL; }
+    if (nrows <= 0) return TQ_OK;
+    k_tiles_expect<<<1, 1, 0, S(stream)>>>(c.tiles + TQ_TILE_CTL(nrows), (int32_t)nnz); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_tiles_expect");
+    return TQ_OK;
+}
+
 extern "C" int tq_scan_tiles_early(tq_rowctx c, int64_t nnz, int32_t tail, void* stream) {
     const int nrows = c.row_end - c.row_begin;
     if (!c.tiles || !c.counts) { set_error("tq_scan_tiles_early needs the context's counts and tiles"); return TQ_EINVAL; }

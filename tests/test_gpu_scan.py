@@ -81,3 +81,50 @@ def test_scan_tiles_matches_cumsum(nrows):
 def test_scan_tiles_overflow_raises():
     with pytest.raises(OverflowError):
         scan_tiles(np.full(3, 2**30), 96)
+
+
+def test_tiles_expect_flags_a_changed_total():
+    """tq_tiles_expect + tq_scan_tiles: the total against the nnz a captured
+    pass sized its output with -> flag word TQ_TILE_CTL + 4 (the
+    replay guard must fire without the early scan)."""
+    from paper_2101_08053_b200 import _lib as L
+    nrows = 4096 * 3 + 7
+    sums = np.random.default_rng(2).integers(0, 32 * 81, size=(nrows + 31) // 32)
+    total = int(sums.sum())
+    for expect, flag in ((total, 0), (total + 1, 1), (total - 32, 1)):
+        tiles = torch.zeros((L.tile_ints(nrows),), dtype=torch.int32, device="cuda")
+        tiles[:len(sums)] = torch.from_numpy(sums.astype(np.int32)).cuda()
+        counts = torch.zeros(nrows, dtype=torch.int32, device="cuda")
+        indptr = torch.empty(nrows + 1, dtype=torch.int32, device="cuda")
+        ctx = L.RowCtx()
+        ctx.row_begin, ctx.row_end = 0, nrows
+        ctx.counts, ctx.tiles = L.ptr(counts), L.ptr(tiles)
+        L.call("tq_tiles_expect", ctx, expect, L.stream())
+        L.call("tq_scan_tiles", ctx, L.ptr(indptr), None, L.stream())
+        assert int(tiles[L.tile_ctl(nrows) + 4].item()) == flag
+
+
+def test_replayed_pass_with_another_nnz_writes_nothing_and_raises():
+    """A pass run in capture mode with a wrong expected nnz (what a replay
+    whose counts moved would see): the scan flags it, the fill kernels write
+    nothing into the (captured-size) buffers, and check() raises."""
+    from paper_2101_08053_b200 import assembly as A, cases as C, _lib as L
+    c5 = C.baseline_config(5, nel=64)
+    b2d, cfg = C.build_space(None, 64, 4, curves=c5["curves"])
+    f0, csr0 = A.form(b2d, cfg, None, "dwq")
+    nnz = csr0.nnz
+    A.form(b2d, cfg, None, "dwq", capture={"nnz": nnz})                 # right count: no flag
+    f1, csr1 = A.form(b2d, cfg, None, "dwq", capture={"nnz": nnz})
+    torch.cuda.synchronize()
+    assert int(f1._count_bufs[1][L.tile_ctl(f1._nrows) + 4].item()) == 0
+    assert np.array_equal(csr1.data.cpu().numpy(), csr0.data.cpu().numpy())
+    f2, csr2 = A.form(b2d, cfg, None, "dwq", capture={"nnz": nnz - 1})   # smaller buffers
+    torch.cuda.synchronize()
+    assert int(f2._count_bufs[1][L.tile_ctl(f2._nrows) + 4].item()) == 1
+
+    class _G:
+        pass
+    g = _G()
+    g.f = f2
+    with pytest.raises(RuntimeError):
+        A.GraphFormation.check(g)
