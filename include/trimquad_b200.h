@@ -271,6 +271,15 @@ typedef struct {
     int64_t raw_ld;              /* 0: raw blocks row-major (slot * W + o);
                                     > 0: planes, entry o of slot s at
                                     raw[o * raw_ld + s] (tq_planes_csr) */
+    /* optional (NULL: off): function classes (n1*n2) and the per-line factor
+       positivity of this pass (n1 + n2, k_pos2).  An interior separable row
+       whose two lines are positive has only positive partner sums M_ij + M_ji
+       (its own products are positive, and every partner's value is the
+       integral of B_i B_j over part of supp(i), which is visible): the value
+       count of tq_row_counts_rest counts it geometrically, and the fill
+       verifies it -- a dropped entry in such a row sets TQ_TILE_CTL + 8. */
+    const int8_t* fclass;
+    const int8_t* pos;
 } tq_rowctx;
 
 /* tile-mode buffer layout (ints): the tile sums (padded to a multiple of 4
@@ -283,7 +292,7 @@ typedef struct {
 #define TQ_TILE_PAD(nrows) ((TQ_TILE_NT(nrows) + 3) / 4 * 4)
 #define TQ_TILE_EARLY(nrows) (TQ_TILE_PAD(nrows) + TQ_TILE_NT(nrows) + 2)
 #define TQ_TILE_CTL(nrows) (TQ_TILE_EARLY(nrows) + TQ_TILE_NT(nrows))
-#define TQ_TILE_INTS(nrows) (TQ_TILE_CTL(nrows) + 8)
+#define TQ_TILE_INTS(nrows) (TQ_TILE_CTL(nrows) + 9)
 static inline int32_t* tq_tile_bases(int32_t* tiles, int32_t nrows) { return tiles + TQ_TILE_PAD(nrows); }
 
 /* deep-row flags: deep[i] = separable(i) && no raw row in window(i) &&

@@ -121,7 +121,7 @@ class RowCtx(C.Structure):
                 ("ov_lo1", vp), ("ov_hi1", vp), ("ov_lo2", vp), ("ov_hi2", vp),
                 ("col_of", vp), ("active", vp), ("slot", vp), ("a1", vp), ("a2", vp), ("raw", vp),
                 ("deep", vp), ("rowfast", vp), ("row_begin", i32), ("row_end", i32), ("counts", vp), ("tiles", vp),
-                ("raw_ld", i64)]
+                ("raw_ld", i64), ("fclass", vp), ("pos", vp)]
 
 
 _lib = None
@@ -258,8 +258,8 @@ def tile_ctl(nrows):
 
 def tile_ints(nrows):
     """TQ_TILE_INTS: ints of a tile-mode buffer (tq_rowctx.tiles): sums |
-    bases, total, overflow | early bases | eight control words."""
-    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 10
+    bases, total, overflow | early bases | nine control words."""
+    return tile_pad(nrows) + 2 * ((nrows + 31) // 32) + 11
 
 
 def ptr(t):

@@ -477,6 +477,11 @@ class Formation:
                         flags=torch.zeros(3, dtype=torch.int32, device=self.dev))
             else:
                 L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            if self.a1 is not None and GEOMETRIC_NEAR:
+                # interior separable rows on positive lines are counted
+                # geometrically by pass 2 and verified by the fill (rowctx.fclass)
+                ctx.fclass, ctx.pos = L.ptr(self.config.func_class_dev), L.ptr(pos)
+                self._near_pos = pos
             _stamp("counts_deep")
             head = None
             if self.capture is not None and HEAD_FILL:
@@ -527,6 +532,8 @@ class Formation:
         for st in getattr(self, "_status_streams", []):       # status reductions rejoin
             torch.cuda.current_stream().wait_stream(st)
         _stamp("fill")
+        if self.capture is None and ctx.fclass and int(tiles[L.tile_ctl(nrows) + 8].item()):
+            raise RuntimeError("a geometrically counted row dropped an entry (rowctx.fclass): pattern inconsistent")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
     def _finish_planes(self, row_begin, row_end, join):
@@ -579,6 +586,9 @@ STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
 # default since the single-stage fill: the early fill's memory traffic slows
 # the latency-bound count pass 2 by more than it saves, measured at config 5)
 HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "0"))
+# count pass 2 counts interior separable rows on positive factor lines
+# geometrically (their partner sums are positive; the fill verifies them)
+GEOMETRIC_NEAR = os.environ.get("TQ_GEOMETRIC_NEAR", "1") == "1"
 HEAD_BLOCKS_PER_SM = int(os.environ.get("TQ_HEAD_BPS", "3"))
 # ... and the tiles after the last list-A row too (their offsets from the
 # captured nnz): measured slower at config 5 (the early fill then delays the
@@ -709,8 +719,12 @@ class GraphFormation:
             st = getattr(self.f, "_planes_status", None)
             if st is not None and int(st.item()):
                 raise RuntimeError("planes path status word set in a replayed pass (tq_sf_strips / tq_cut_rows_gather)")
-        elif int(self.f._count_bufs[1][L.tile_ctl(self.f._nrows) + 4].item()):
-            raise RuntimeError("replayed pass formed a different nnz than the captured one")
+        else:
+            ctl = self.f._count_bufs[1][L.tile_ctl(self.f._nrows):].cpu()
+            if int(ctl[4]):
+                raise RuntimeError("replayed pass formed a different nnz than the captured one")
+            if int(ctl[8]):
+                raise RuntimeError("a geometrically counted row dropped an entry in a replayed pass")
 
 
 def assemble_mass(basis2d: TensorBasis2D, config: TrimConfiguration, coeff=None, strategy="reference",

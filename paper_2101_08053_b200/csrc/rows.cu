@@ -86,6 +86,13 @@ __device__ inline RowGeom row_geom(const tq_rowctx& c, int r) {
     return g;
 }
 
+// an interior separable row on positive factor lines: every window entry has
+// a positive partner sum (tq_rowctx.fclass / pos), counted geometrically
+__device__ __forceinline__ bool near_row(const tq_rowctx& c, const RowGeom& g) {
+    return c.fclass && c.pos && c.tiles && g.s_i < 0 && __ldg(c.fclass + ((int64_t)g.i1 * c.n2 + g.i2)) == TQ_INTERIOR &&
+           __ldg(c.pos + g.i1) && __ldg(c.pos + c.n1 + g.i2);
+}
+
 // unsymmetrised value of row (i1,i2) at column (j1,j2).  Every symmetrised
 // entry is formed as round(round(M_ij) + round(M_ji)) -- explicitly rounded
 // products and sum, never contracted into an FMA -- so M_ij and M_ji are
@@ -274,14 +281,21 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
             g[k] = row_geom(c, r[k]);
             small = small && g[k].t1 * g[k].t2 <= 96;
             cnt[k] = 0;
+            if (ok[k] && near_row(c, g[k])) {      // counted geometrically, no entry loads
+                cnt[k] = g[k].t1 * g[k].t2;
+                ok[k] = false;
+            }
         }
-        if (small) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < R; ++k) any = any || ok[k];
+        if (small && any) {
             int col[3 * R];
             double v[3 * R];
             entries_rows<R>(c, g, ok, lane, col, v);
 #pragma unroll
             for (int u = 0; u < 3 * R; ++u) cnt[u / 3] += __popc(__ballot_sync(0xffffffffu, col[u] >= 0));
-        } else {
+        } else if (!small) {
             for (int k = 0; k < R; ++k) {
                 if (!ok[k]) continue;
                 const int n = g[k].t1 * g[k].t2;
@@ -297,7 +311,7 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
         if (lane == 0) {
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-                if (!ok[k]) continue;
+                if (q0 + k >= n_rows) continue;
                 counts[r[k] - c.row_begin] = cnt[k];
                 if (c.tiles) atomicAdd(c.tiles + ((r[k] - c.row_begin) >> 5), cnt[k]);
             }
@@ -597,6 +611,7 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
                 }
             }
         } else {
+            const int pos0 = pos;
             for (int e0 = 0; e0 < n; e0 += 96) {
                 int col[3];
                 double v[3];
@@ -612,6 +627,9 @@ __global__ void __launch_bounds__(256) k_fill_irregular(tq_rowctx c, const int32
                     pos += __popc(m);
                 }
             }
+            // a geometrically counted row (near_row) must keep its whole window
+            if (lane == 0 && pos - pos0 != n && c.tiles && near_row(c, g))
+                atomicOr(c.tiles + TQ_TILE_CTL(c.row_end - c.row_begin) + 8, 1);
         }
     }
 }
@@ -632,6 +650,7 @@ __global__ void k_fill_rows(tq_rowctx c, int32_t* __restrict__ indptr, int32_t* 
             pos = indptr[r - c.row_begin];
         }
         int n = g.t1 * g.t2;
+        const int pos0 = pos;
         for (int e0 = 0; e0 < n; e0 += 32) {
             int e = e0 + lane;
             double v = 0.0;
@@ -644,6 +663,8 @@ __global__ void k_fill_rows(tq_rowctx c, int32_t* __restrict__ indptr, int32_t* 
             }
             pos += __popc(m);
         }
+        if (lane == 0 && pos - pos0 != n && c.tiles && near_row(c, g))      // see k_fill_irregular
+            atomicOr(c.tiles + TQ_TILE_CTL(c.row_end - c.row_begin) + 8, 1);
     }
 }
 
@@ -774,7 +795,7 @@ extern "C" int tq_wq_products(tq_space1d s, tq_layout lay, const int32_t* first,
 extern "C" int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream) {
     int nrows = c.row_end - c.row_begin;
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
-    if (c.tiles && nrows > 0) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
+    if (c.tiles && nrows > 0) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 9 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     k_row_counts_deep<false><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, nullptr, nullptr, counts, work + 2, work,
                                                                            work + 2 + nrows, work + 1); ::tq::note_launch();
@@ -791,7 +812,7 @@ extern "C" int tq_row_counts_geo(tq_rowctx c, const int8_t* geo, int8_t* pos, in
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
     if (!c.a1 || !c.a2) { set_error("tq_row_counts_geo needs the separable factors"); return TQ_EINVAL; }
-    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
+    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 9 * sizeof(int32_t), S(stream)));
     k_pos2<<<grid_for(c.n1 + c.n2, 128), 128, 0, S(stream)>>>(c, pos); ::tq::note_launch();
     k_row_counts_deep<true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, pos, counts, work + 2, work,
                                                                           work + 2 + nrows, work + 1); ::tq::note_launch();
@@ -808,7 +829,7 @@ extern "C" int tq_row_counts_spec(tq_rowctx c, const int8_t* geo, int32_t* count
     int nrows = c.row_end - c.row_begin;
     TQ_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(int32_t), S(stream)));
     if (nrows <= 0) return TQ_OK;
-    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 8 * sizeof(int32_t), S(stream)));
+    if (c.tiles) TQ_CUDA(cudaMemsetAsync(c.tiles + TQ_TILE_CTL(nrows), 0, 9 * sizeof(int32_t), S(stream)));
     k_row_counts_deep<true, true><<<grid_for(nrows, 256), 256, 0, S(stream)>>>(c, geo, nullptr, counts, work + 2,
                                                                                 work, work + 2 + nrows, work + 1);
     ::tq::note_launch();
@@ -885,16 +906,19 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
     auto launch = [&](auto kern, auto kirr, size_t per_warp) -> int {
         // launch configuration cached per kernel instance (host calls kept
         // off the per-pass path)
-        static int cached_wpb[kMaxP + 1] = {}, cached_per_sm[kMaxP + 1] = {};
-        int wpb = cached_wpb[P];
-        int per_sm = cached_per_sm[P];
+        // (per device: the shared-memory attribute is per-device state)
+        static int cached_wpb[kMaxP + 1][16] = {}, cached_per_sm[kMaxP + 1][16] = {};
+        int dev = 0;
+        TQ_CUDA(cudaGetDevice(&dev));
+        int wpb = cached_wpb[P][dev & 15];
+        int per_sm = cached_per_sm[P][dev & 15];
         if (!wpb) {
             wpb = 8;
             while (per_warp * wpb > 160 * 1024 && wpb > 1) wpb /= 2;
             TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * wpb)));
             TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, per_warp * wpb));
-            cached_wpb[P] = wpb;
-            cached_per_sm[P] = per_sm;
+            cached_wpb[P][dev & 15] = wpb;
+            cached_per_sm[P][dev & 15] = per_sm;
         }
         const size_t shm = per_warp * wpb;
         const int64_t full = (int64_t)kSms * std::max(per_sm, 1);
@@ -927,12 +951,16 @@ extern "C" int tq_fill_rows(tq_rowctx c, const int32_t* indptr, int32_t* indices
 template <int P>
 static int fill_fast_launch(const tq_rowctx& c, int32_t* indptr, int32_t* indices, double* data,
                             cudaStream_t st, int part = 0, int blocks_per_sm = 0) {
-    static int cached_wpb = 0, cached_per_sm = 0;
+    // cached per device (the shared-memory attribute is per-device state)
+    static int cached_wpb_d[16] = {}, cached_per_sm_d[16] = {};
+    int dev = 0;
+    TQ_CUDA(cudaGetDevice(&dev));
+    int& cached_wpb = cached_wpb_d[dev & 15];
+    int& cached_per_sm = cached_per_sm_d[dev & 15];
     const size_t per_warp = fill_slice_bytes<P>();
     if (!cached_wpb) {
         // warps per block maximising resident warps per SM (shared memory bound)
-        int dev = 0, smem_max = 0;
-        TQ_CUDA(cudaGetDevice(&dev));
+        int smem_max = 0;
         TQ_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         TQ_CUDA(cudaFuncSetAttribute(k_fill_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
         int best_w = 0;
