@@ -50,6 +50,15 @@ __device__ __forceinline__ void pair_tables(int* pa, int* pb) {
 // E = PV1^T T is a (NP x q) (q x NP) product: a thread owns a 3 x 6 tile.
 // ---------------------------------------------------------------------------
 constexpr int kGpThreads = 128;
+// element-Gauss and cut pair blocks: 8 resident blocks per SM (64
+// registers; 128 / 80 with no bound): config 4 p = 8 step 0.522 -> 0.506 ms
+// (the pair kernels overlap the fits and strips better)
+#ifndef TQ_GP_MINB
+#define TQ_GP_MINB 8
+#endif
+#ifndef TQ_CP_MINB
+#define TQ_CP_MINB 8
+#endif
 
 // geometry-map line tables at points u: span, then N[0..p], D[0..p]
 template <int PG>
@@ -70,7 +79,7 @@ __global__ void k_geo_lines(tq_coeff geo, const double* __restrict__ u, int n, i
 }
 
 template <int Q>
-__global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* __restrict__ X1,
+__global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawctx c, tq_coeff geo, const double* __restrict__ X1,
                                                             const double* __restrict__ X2,
                                                             const int32_t* __restrict__ gel, int nslot,
                                                             const double* __restrict__ cgp, double* __restrict__ E,
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(kGpThreads) k_gauss_pairs(tq_rawctx c, tq_coef
 constexpr int kCpThreads = 128, kCpChunk = 32, kCpPiece = 128;
 
 template <int Q>
-__global__ void __launch_bounds__(kCpThreads) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,
+__global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,
                                                           int npieces, double* __restrict__ Epart) {
     constexpr int NP = Pairs<Q>::NP, TA = (NP + 7) / 8, TB = (NP + 15) / 16, NA = 8 * TA, NB = 16 * TB;
     constexpr int ST = 2 * Q + 1;
