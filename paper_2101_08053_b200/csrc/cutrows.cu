@@ -264,7 +264,8 @@ constexpr int kCpThreads = 128, kCpChunk = 32, kCpPiece = 128;
 
 template <int Q>
 __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,
-                                                          int npieces, double* __restrict__ Epart) {
+                                                          int npieces, double* __restrict__ Epart,
+                                                          const int32_t* __restrict__ gpiece, double* __restrict__ E) {
     constexpr int NP = Pairs<Q>::NP, TA = (NP + 7) / 8, TB = (NP + 15) / 16, NA = 8 * TA, NB = 16 * TB;
     constexpr int ST = 2 * Q + 1;
     __shared__ double S[kCpChunk][ST];
@@ -310,7 +311,8 @@ __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx 
                     for (int j = 0; j < TB; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
             }
         }
-        double* out = Epart + (int64_t)pc * NP * NP;
+        // a group of one piece writes its block directly (the reduce skips it)
+        double* out = gpiece[g + 1] - gpiece[g] == 1 ? E + (int64_t)g * NP * NP : Epart + (int64_t)pc * NP * NP;
 #pragma unroll
         for (int i = 0; i < TA; ++i)
 #pragma unroll
@@ -321,12 +323,13 @@ __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx 
     }
 }
 
-// E[g] = sum of its pieces in order (gpiece: ngroups + 1 piece offsets)
+// E[g] = sum of its pieces in order (gpiece: ngroups + 1 piece offsets), groups of two or more pieces
 __global__ void k_cut_pairs_reduce(const int32_t* __restrict__ gpiece, int ngroups, int npp,
                                    const double* __restrict__ Epart, double* __restrict__ E) {
     const int64_t total = (int64_t)ngroups * npp;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int g = (int)(t / npp), e = (int)(t - (int64_t)g * npp);
+        if (gpiece[g + 1] - gpiece[g] == 1) continue;       // written by k_cut_pairs
         double acc = 0.0;
         for (int pc = gpiece[g]; pc < gpiece[g + 1]; ++pc) acc += Epart[(int64_t)pc * npp + e];
         E[t] = acc;
@@ -645,7 +648,7 @@ extern "C" int tq_cut_pairs(tq_rawctx c, const int64_t* pieces, int32_t npieces,
     if (c.p1 != c.p2) { set_error("tq_cut_pairs needs p1 == p2"); return TQ_EINVAL; }
     const int grid = std::min(npieces, kSms * 16);
     switch (c.p1 + 1) {
-#define CASE(Q) case Q: k_cut_pairs<Q><<<grid, kCpThreads, 0, S(stream)>>>(c, pieces, npieces, Epart); break;
+#define CASE(Q) case Q: k_cut_pairs<Q><<<grid, kCpThreads, 0, S(stream)>>>(c, pieces, npieces, Epart, gpiece, E); break;
         CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11)
 #undef CASE
         default: set_error("degree out of range"); return TQ_EINVAL;
