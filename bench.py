@@ -278,13 +278,13 @@ def config4_secondary(p, nel=256, steps=20, seed=0):
             # the launches of the shared-memory classes on concurrent streams
             # (they write disjoint rows), joined
             L.call("tq_bw_tables", f._ctx_int, L.ptr(f._bw), L.ptr(st), L.stream())
-            for k, (ts, sd, ns, n1m, n2m, nu) in enumerate(classes):
+            for k, (ts, sd, ns, n1m, n2m, nu, b2cap) in enumerate(classes):
                 stream = main if k == 0 else sides[k - 1]
                 if k:
                     stream.wait_stream(main)
                 with torch.cuda.stream(stream):
-                    L.call("tq_sf_strips", f._ctx_int, ts, L.ptr(sd), ns, n1m, n2m, nu, L.ptr(f._bw), L.ptr(st),
-                           L.stream())
+                    L.call("tq_sf_strips", f._ctx_int, ts, L.ptr(sd), ns, n1m, n2m, nu, b2cap, L.ptr(f._bw),
+                           L.ptr(st), L.stream())
             for sd_ in sides:
                 main.wait_stream(sd_)
         for _ in range(3):

@@ -462,13 +462,16 @@ int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
  * by strips of up to `rows` (16 or 8) rows (i1, i20 + t): strips = nstrips x
  * (2 + rows) ints (i1, i20, storage index of row t or -1); nu_max bounds the union of a
  * strip's direction-2 point windows and n1m / n2m its rule rows (shared-
- * memory sizing, <= the context's nmax); bw: the tables of tq_bw_tables; a
- * strip that
- * breaks a bound sets *status |= 1 and writes zero blocks.  Replaces
- * sum_factor_row over _interior_rows_batched (src/assembly.py:218-252,
- * 409-449); writes the rows' planes. */
+ * memory sizing, <= the context's nmax); b2cap > 0: the strip's direction-2
+ * table rows are staged packed, each row sized by its own rule length, in
+ * b2cap doubles (the largest sum over the strips of the launch of
+ * 2 * (((len * wp + 1) / 2) | 1), wp = 3 * ((2p + 3) / 3)); b2cap = 0: rows
+ * of n2m each; bw: the tables of tq_bw_tables; a strip that breaks a bound
+ * sets *status |= 1 and writes zero blocks.  Replaces sum_factor_row over
+ * _interior_rows_batched (src/assembly.py:218-252, 409-449); writes the
+ * rows' planes. */
 int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
-                 int32_t nu_max, const double* bw, int32_t* status, void* stream);
+                 int32_t nu_max, int32_t b2cap, const double* bw, int32_t* status, void* stream);
 /* the weighted collocation tables of the standard rules tq_sf_strips reads
  * (bw: n_d x nmax_d x the padded window, both directions; size in doubles
  * from tq_bw_table_doubles); *status |= 2 when a rule row is longer than

@@ -55,7 +55,7 @@ def _bind():
     L.optional("tq_dwq_route", [L.Space1D, L.Space1D, L.vp, L.vp, L.i32, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_grid", [L.Coeff, L.vp, L.i32, L.vp, L.i32, L.vp, L.vp])
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
-    L.optional("tq_sf_strips", [RawCtx, L.i32, L.vp, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_sf_strips", [RawCtx, L.i32, L.vp, L.i32, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
     L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp,
                                   L.vp])
@@ -407,7 +407,8 @@ def strip_classes(f, pg, layout1, layout2):
     functions of an open knot vector) form 8-row strips of their own; the
     rest form 16-row strips aligned after them.  Launches: 16-row strips on
     regular lines, 16-row strips on long-rule lines, 8-row edge strips --
-    each [(rows per strip, strips_dev, nstrips, n1m, n2m, nu_max)]."""
+    each [(rows per strip, strips_dev, nstrips, n1m, n2m, nu_max, b2cap)]
+    (b2cap: doubles of the packed B2 stage, tq_sf_strips)."""
     g = _geo(f.config)
     key = ("strip_classes", id(pg), id(layout1), id(layout2))
     if key not in g:
@@ -449,10 +450,20 @@ def strip_classes(f, pg, layout1, layout2):
                 nu = o2[b2._el_last[strips[:, 1] + hi] + 1] - o2[b2._el_first[strips[:, 1] + lo]]
                 reg = (c1 <= med1) & (c2 <= med2)
                 groups = (reg, ~reg) if ts == STRIP_ROWS else (c1 <= med1, c1 > med1)
-                for sel in groups:
+                # packed B2 stage: each row sized by its own rule-length bound
+                wp = 3 * ((2 * b1.p + 3) // 3)
+                lens = np.where(rows, cnt2[ii2], 0)
+                alloc = np.where(lens > 0, 2 * (((lens * wp + 1) // 2) | 1), 0).sum(axis=1)
+                for k, sel in enumerate(groups):
                     if sel.any():
+                        # the regular class keeps a fixed row stride (every row
+                        # an equal odd number of 16-byte units: conflict-free
+                        # stage-B reads); the long-rule class packs its rows
+                        # (two blocks per SM instead of one)
+                        packed = k > 0 and ts == STRIP_ROWS
                         out.append((ts, L.dev(np.ascontiguousarray(strips[sel]), torch.int32), int(sel.sum()),
-                                    int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1)))
+                                    int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1),
+                                    int(alloc[sel].max()) if packed else 0))
         g[key] = out
         g[key + ("keep",)] = (layout1, layout2)       # the ids stay valid
     return g[key]
@@ -1246,10 +1257,10 @@ def run_phase(f, phase):
             classes = strip_classes(f, pg, f._setup.sets[0][0].layout, f._setup.sets[1][0].layout)
             main = torch.cuda.current_stream()
             sides = []
-            for k, (ts, strips, ns, n1m, n2m, nu) in enumerate(classes):
+            for k, (ts, strips, ns, n1m, n2m, nu, b2cap) in enumerate(classes):
                 st = main if k == 0 else _named_stream(f"strips{k}", priority=-2)
                 with (contextlib.nullcontext() if k == 0 else _forked(main, st)):
-                    L.call("tq_sf_strips", ctx_int, ts, L.ptr(strips), ns, n1m, n2m, nu, L.ptr(f._bw),
+                    L.call("tq_sf_strips", ctx_int, ts, L.ptr(strips), ns, n1m, n2m, nu, b2cap, L.ptr(f._bw),
                            L.ptr(f._planes_status), L.stream())
                 if k:
                     sides.append(st)

@@ -85,22 +85,25 @@ __host__ __device__ inline int strip_b2_stride(int p, int n2m) {
 // slot of slack for an odd first column
 __host__ __device__ inline int strip_gs_stride(int nu_max) { return (nu_max + 3) & ~1; }
 
-// shared stage offsets (doubles): two buffers of B1 | GS | B2, then X; the
-// 16-byte copy targets start at even offsets
+// shared stage offsets (doubles): two buffers of B1 | GS (stage A's operands,
+// prefetched one strip ahead), ONE B2 stage (refilled while stage A of the
+// next strip runs), then X; the 16-byte copy targets start at even offsets
 struct StripSmem {
-    int gs, b2, buf, x, total;
-    __host__ __device__ StripSmem(int p, int n1m, int n2m, int nu_max, int ts) {
+    int gs, abuf, b2, x, total;
+    // b2cap > 0: the B2 stage holds the rows packed (each row its own odd
+    // number of 16-byte units, strip_b2_stride of its length), b2cap doubles
+    __host__ __device__ StripSmem(int p, int n1m, int n2m, int nu_max, int ts, int b2cap = 0) {
         const int WP = bw_wp(p), WPI = WP | 1;
         gs = (n1m * WP + 1) & ~1;
-        b2 = gs + n1m * strip_gs_stride(nu_max);
-        buf = b2 + ts * strip_b2_stride(p, n2m);
-        x = 2 * buf;
+        abuf = gs + n1m * strip_gs_stride(nu_max);
+        b2 = 2 * abuf;
+        x = b2 + (b2cap > 0 ? b2cap : ts * strip_b2_stride(p, n2m));
         total = x + nu_max * WPI;
     }
 };
 
-__host__ __device__ inline size_t strip_smem_doubles(int p, int n1m, int n2m, int nu_max, int ts) {
-    return (size_t)StripSmem(p, n1m, n2m, nu_max, ts).total;
+__host__ __device__ inline size_t strip_smem_doubles(int p, int n1m, int n2m, int nu_max, int ts, int b2cap = 0) {
+    return (size_t)StripSmem(p, n1m, n2m, nu_max, ts, b2cap).total;
 }
 
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
@@ -144,38 +147,45 @@ __device__ __forceinline__ void consumers_sync(int n) { asm volatile("bar.sync 1
 
 template <int TS>
 struct StripHdr {
-    int k0[TS], n2[TS], st[TS];
+    int k0[TS], n2[TS], st[TS], off2[TS];     // off2: B2 row offset in 16-byte units
     int i1, i20, u0, nu, k01, n1, sh, pad;
 };
 
-// Warp-specialised and double-buffered: warp CW (the producer) reads strip
-// s + 2G's header while the consumer warps 0..CW-1 compute strip s, and
-// stages it (TMA bulk copies of the B1 / B2 table rows and the coefficient
-// rows) into the free buffer; full[b] / empty[b] mbarriers hand the buffers
-// over.  n1m, n2m: the rule-row capacity of the stage (the strips of one
-// launch have shorter rows than the tables' stride c.nmax1/2 when the
-// boundary strips go to a second launch).
+// Warp-specialised: warp CW (the producer) reads strip s + G's header and
+// stages its stage-A operands (TMA bulk copies of the B1 table row and the
+// coefficient rows) into the free A buffer while the consumer warps
+// 0..CW-1 compute strip s; the B2 rows of a strip go to the single B2 stage
+// as soon as the consumers are done with the previous strip's stage B, so
+// they arrive while stage A of the strip runs (one B2 stage instead of two:
+// the long-rule classes fit two blocks per SM).  full_a[b] / empty_a[b]
+// hand the A buffers over, full_b / empty_b the B2 stage.  n1m, n2m: the
+// rule-row capacity of the stage (the strips of one launch have shorter
+// rows than the tables' stride c.nmax1/2 when the boundary strips go to a
+// second launch).
 template <int P, int TS>
 __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
-    tq_rawctx c, const int32_t* __restrict__ strips, int nstrips, int n1m, int n2m, int nu_max,
+    tq_rawctx c, const int32_t* __restrict__ strips, int nstrips, int n1m, int n2m, int nu_max, int b2cap,
     const double* __restrict__ bw1, const double* __restrict__ bw2, int* __restrict__ status) {
     constexpr int W = 2 * P + 1, BA = (W + 2) / 3, WP = 3 * BA, WPI = WP | 1, NB = TS * 9;
     constexpr int CW = (NB + 31) / 32, NC = 32 * CW;      // consumer warps / threads
     extern __shared__ __align__(128) double sm[];       // 16-byte aligned bulk-copy targets
-    const StripSmem L(P, n1m, n2m, nu_max, TS);
+    const StripSmem L(P, n1m, n2m, nu_max, TS, b2cap);
     const int SB = strip_b2_stride(P, n2m), GL = strip_gs_stride(nu_max);
     double* X = sm + L.x;                 // [nu][WPI]
+    double* B2 = sm + L.b2;               // [TS][SB]
     __shared__ StripHdr<TS> H[2];
-    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ __align__(8) uint64_t full_a[2], empty_a[2], full_b, empty_b;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const tq_ruleset R1 = c.sets1[0], R2 = c.sets2[0];
     const double* __restrict__ G = c.grids[0];
     const int ldG = R2.lay.npts;
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], 1);
-        mbar_init(&empty[1], 1);
+        mbar_init(&full_a[0], 1);
+        mbar_init(&full_a[1], 1);
+        mbar_init(&empty_a[0], 1);
+        mbar_init(&empty_a[1], 1);
+        mbar_init(&full_b, 1);
+        mbar_init(&empty_b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
         const bool bulk = (ldG & 1) == 0;     // coefficient rows 16-byte aligned
         for (int it = 0, s = blockIdx.x; s < nstrips; s += gridDim.x, ++it) {
             const int b = it & 1;
-            if (it >= 2) mbar_wait(&empty[b], ((it >> 1) & 1) ^ 1);
+            if (it >= 2) mbar_wait(&empty_a[b], ((it >> 1) & 1) ^ 1);
             StripHdr<TS>& h = H[b];
             const int32_t* st = strips + (int64_t)s * (2 + TS);
             const int i1 = st[0], i20 = st[1];
@@ -200,10 +210,20 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
                 h.n2[lane] = n2;
                 h.st[lane] = sidx;
             }
+            // B2 stage offsets: packed rows (b2cap > 0) or a fixed stride
+            const int alloc = lane < TS ? (b2cap > 0 ? (n2 > 0 ? strip_b2_stride(P, n2) : 0) : SB) : 0;
+            int incl = alloc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane < TS) h.off2[lane] = (incl - alloc) >> 1;     // allocations are even
             int lo = n2 > 0 ? k0 : INT_MAX, hi = n2 > 0 ? k0 + n2 : INT_MIN, bad = n2 > n2m;
             lo = __reduce_min_sync(0xffffffffu, lo);
             hi = __reduce_max_sync(0xffffffffu, hi);
             bad = __reduce_or_sync(0xffffffffu, bad);
+            if (b2cap > 0 && __shfl_sync(0xffffffffu, incl, 31) > b2cap) bad = 1;
             const int k01 = R1.rules.k0[i1];
             int n1 = k01 >= 0 ? (int)(R1.rules.wptr[i1 + 1] - R1.rules.wptr[i1]) : 0;
             int nu = hi > lo ? hi - lo : 0;
@@ -213,9 +233,8 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
             }
             if (nu == 0) n1 = 0;
             const int sh = bulk ? (lo & 1) : 0;
-            double* B1 = sm + b * L.buf;
+            double* B1 = sm + b * L.abuf;
             double* GS = B1 + L.gs;
-            double* B2 = B1 + L.b2;
             if (n1 > 0 && !bulk) {        // odd grid stride: the coefficient rows through registers
                 for (int k = 0; k < n1; ++k)
                     for (int u = lane; u < nu; u += 32) GS[k * GL + u] = __ldg(G + (int64_t)(k01 + k) * ldG + lo + u);
@@ -231,19 +250,34 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
                 h.n1 = n1;
                 h.sh = sh;
                 if (n1 > 0) {
-                    const int nrow = min(TS, c.n2 - i20), R2s = bw_row(P, c.nmax2);
-                    const unsigned b1b = 8u * ((n1 * WP + 1) & ~1), b2b = 8u * ((n2m * WP + 1) & ~1);
+                    const unsigned b1b = 8u * ((n1 * WP + 1) & ~1);
                     const int ua = lo & ~1, gl = (sh + nu + 1) & ~1;
                     fence_proxy_async_shared();       // the buffer's earlier reads precede these writes
-                    mbar_expect_tx(&full[b], b1b + nrow * b2b + (bulk ? 8u * n1 * gl : 0u));
-                    bulk_g2s(B1, bw1 + (int64_t)i1 * bw_row(P, c.nmax1), b1b, &full[b]);
-                    for (int t = 0; t < nrow; ++t)
-                        bulk_g2s(B2 + t * SB, bw2 + (int64_t)(i20 + t) * R2s, b2b, &full[b]);
+                    mbar_expect_tx(&full_a[b], b1b + (bulk ? 8u * n1 * gl : 0u));
+                    bulk_g2s(B1, bw1 + (int64_t)i1 * bw_row(P, c.nmax1), b1b, &full_a[b]);
                     if (bulk)
                         for (int k = 0; k < n1; ++k)
-                            bulk_g2s(GS + k * GL, G + (int64_t)(k01 + k) * ldG + ua, 8u * gl, &full[b]);
+                            bulk_g2s(GS + k * GL, G + (int64_t)(k01 + k) * ldG + ua, 8u * gl, &full_a[b]);
                 } else {
-                    mbar_arrive(&full[b]);
+                    mbar_arrive(&full_a[b]);
+                }
+                // the B2 rows once the previous strip's stage B is done
+                if (it >= 1) mbar_wait(&empty_b, (it - 1) & 1);
+                if (n1 > 0) {
+                    const int nrow = min(TS, c.n2 - i20), R2s = bw_row(P, c.nmax2);
+                    // the rows' own lengths (packed) or the class capacity
+                    unsigned tot = 0;
+                    for (int t = 0; t < nrow; ++t)
+                        tot += b2cap > 0 ? 8u * ((h.n2[t] * WP + 1) & ~1) : 8u * ((n2m * WP + 1) & ~1);
+                    fence_proxy_async_shared();
+                    mbar_expect_tx(&full_b, tot);
+                    for (int t = 0; t < nrow; ++t) {
+                        const unsigned bt = b2cap > 0 ? 8u * ((h.n2[t] * WP + 1) & ~1) : 8u * ((n2m * WP + 1) & ~1);
+                        if (bt) bulk_g2s(B2 + 2 * h.off2[t], bw2 + (int64_t)(i20 + t) * R2s, bt, &full_b);
+                    }
+                    if (!tot) mbar_arrive(&full_b);
+                } else {
+                    mbar_arrive(&full_b);
                 }
             }
             __syncwarp();
@@ -253,11 +287,10 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
     // ---------------- consumers
     for (int it = 0, s = blockIdx.x; s < nstrips; s += gridDim.x, ++it) {
         const int b = it & 1;
-        mbar_wait(&full[b], (it >> 1) & 1);
+        mbar_wait(&full_a[b], (it >> 1) & 1);
         const StripHdr<TS>& h = H[b];
-        const double* B1 = sm + b * L.buf;
+        const double* B1 = sm + b * L.abuf;
         const double* GS = B1 + L.gs;
-        const double* B2 = B1 + L.b2;
         const int u0 = h.u0, nu = h.nu, n1 = h.n1, sh = h.sh;
         // stage A: lanes run over u (conflict-free column reads of GS; the B1
         // reads broadcast)
@@ -276,6 +309,7 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
             for (int i = 0; i < BA; ++i) X[u * WPI + ob * BA + i] = acc[i];
         }
         consumers_sync(NC);
+        mbar_wait(&full_b, it & 1);
         // stage B: thread (t = lane row, a, b) owns rows a*BA.., columns b*BA.. of row t
         if (tid < NB) {
             const int t = tid % TS, ab = tid / TS, a = ab / 3, bq = ab - a * 3;
@@ -286,7 +320,7 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
 #pragma unroll
                 for (int j = 0; j < BA; ++j) acc[i][j] = 0.0;
             const double* x = X + (n2 > 0 ? h.k0[t] - u0 : 0) * WPI + a * BA;
-            const double* y = B2 + t * SB + bq * BA;
+            const double* y = B2 + 2 * h.off2[t] + bq * BA;      // 16-byte aligned: vector loads
             for (int kk = 0; kk < n2; ++kk) {
                 double xv[BA], yv[BA];
 #pragma unroll
@@ -310,8 +344,11 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
                     }
             }
         }
-        consumers_sync(NC);          // X and buffer b are free
-        if (tid == 0) mbar_arrive(&empty[b]);
+        consumers_sync(NC);          // X, the B2 stage and A buffer b are free
+        if (tid == 0) {
+            mbar_arrive(&empty_b);
+            mbar_arrive(&empty_a[b]);
+        }
     }
 }
 
@@ -499,8 +536,9 @@ using namespace tq;
 
 template <int P, int TS>
 static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
-                            int32_t nu_max, const double* bw1, const double* bw2, int32_t* status, cudaStream_t st) {
-    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, TS);
+                            int32_t nu_max, int32_t b2cap, const double* bw1, const double* bw2, int32_t* status,
+                            cudaStream_t st) {
+    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, TS, b2cap);
     if (shm > 220 * 1024) { set_error("strip workspace too large (%zu bytes)", shm); return TQ_EINVAL; }
     auto kern = k_sf_strips<P, TS>;
     constexpr int NT = 32 * ((TS * 9 + 31) / 32) + 32;
@@ -509,7 +547,7 @@ static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t n
     TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, shm));
     // at least two strips per block (the producer runs one strip ahead)
     const int grid = (int)std::min<int64_t>((nstrips + 1) / 2, (int64_t)kSms * std::max(per_sm, 1));
-    kern<<<grid, NT, shm, st>>>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, status);
+    kern<<<grid, NT, shm, st>>>(c, strips, nstrips, n1m, n2m, nu_max, b2cap, bw1, bw2, status);
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_sf_strips");
     return TQ_OK;
@@ -531,7 +569,8 @@ extern "C" int tq_bw_tables(tq_rawctx c, double* bw, int32_t* status, void* stre
 }
 
 extern "C" int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, int32_t nstrips, int32_t n1m,
-                            int32_t n2m, int32_t nu_max, const double* bw, int32_t* status, void* stream) {
+                            int32_t n2m, int32_t nu_max, int32_t b2cap, const double* bw, int32_t* status,
+                            void* stream) {
     if (rows != kStripRows && rows != 8) { set_error("strips of %d rows (16 or 8)", rows); return TQ_EINVAL; }
     if (nstrips <= 0) return TQ_OK;
     if (!c.grids || !c.raw_ld || c.p1 != c.p2) { set_error("tq_sf_strips needs coefficient grids, planes and p1 == p2"); return TQ_EINVAL; }
@@ -540,10 +579,10 @@ extern "C" int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, in
     const double* bw1 = bw;
     const double* bw2 = bw + (int64_t)c.n1 * bw_row(c.p1, c.nmax1);
     switch (c.p1) {
-#define CASE(Q) case Q: return rows == 8 ? sf_strips_launch<Q, 8>(c, strips, nstrips, n1m, n2m, nu_max, bw1, bw2, \
-                                                                      status, S(stream)) \
+#define CASE(Q) case Q: return rows == 8 ? sf_strips_launch<Q, 8>(c, strips, nstrips, n1m, n2m, nu_max, b2cap, bw1, \
+                                                                      bw2, status, S(stream)) \
                                           : sf_strips_launch<Q, kStripRows>(c, strips, nstrips, n1m, n2m, nu_max, \
-                                                                            bw1, bw2, status, S(stream));
+                                                                            b2cap, bw1, bw2, status, S(stream));
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     }
