@@ -262,12 +262,89 @@ __global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawct
 // ---------------------------------------------------------------------------
 constexpr int kCpThreads = 128, kCpChunk = 32, kCpPiece = 128;
 
+// FP64 tensor-core product of two fragments: C (8 x 8) += A (8 x 4) B (4 x 8)
+// with lane l holding A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) .. +1]
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+#ifndef TQ_CP_DMMA
+#define TQ_CP_DMMA 1
+#endif
+
+// pair-product operand stride: >= the padded width, = 4 (mod 16) doubles, so
+// a fragment load (4 rows x 8 columns) hits distinct banks per half-warp
+__host__ __device__ constexpr int cp_lda(int npad) { return npad + ((4 - npad % 16) + 16) % 16; }
+
 template <int Q>
 __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,
                                                           int npieces, double* __restrict__ Epart,
                                                           const int32_t* __restrict__ gpiece, double* __restrict__ E) {
-    constexpr int NP = Pairs<Q>::NP, TA = (NP + 7) / 8, TB = (NP + 15) / 16, NA = 8 * TA, NB = 16 * TB;
-    constexpr int ST = 2 * Q + 1;
+    constexpr int NP = Pairs<Q>::NP, ST = 2 * Q + 1;
+    if constexpr (TQ_CP_DMMA && Q <= 10) {      // (Q = 11: the padded operands exceed the static stage)
+    // E = P1^T P2 on the FP64 tensor cores (mma.sync m8n8k4): the NP x NP
+    // block in 8 x 8 tiles, a 2 x 2 grid of warps each owning TR x TR tiles;
+    // per 4 points a warp loads TR A and TR B fragments for TR^2 MMAs
+    constexpr int NT8 = (NP + 7) / 8, NPAD = 8 * NT8, LDA = cp_lda(NPAD), TR = (NT8 + 1) / 2;
+    __shared__ double S[kCpChunk][ST];
+    __shared__ __align__(16) double P1[kCpChunk][LDA], P2[kCpChunk][LDA];
+    __shared__ int pa[NP], pb[NP];
+    pair_tables<Q>(pa, pb);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp >> 1, wc = warp & 1, fr = lane >> 2, fk = lane & 3;
+    for (int pc = blockIdx.x; pc < npieces; pc += gridDim.x) {
+        const int g = (int)pieces[2 * pc];
+        const int64_t p0 = pieces[2 * pc + 1], pe = min(p0 + kCpPiece, (int64_t)c.grp_pts[g + 1]);
+        double acc[TR][TR][2];
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+            for (int j = 0; j < TR; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int64_t base = p0; base < pe; base += kCpChunk) {
+            const int np = (int)(pe - base < kCpChunk ? pe - base : kCpChunk);
+            __syncthreads();
+            for (int t = tid; t < np * ST; t += kCpThreads) {
+                const int k = t / ST, o = t - k * ST;
+                const int64_t pt = c.grp_perm[base + k];
+                S[k][o] = o < Q ? c.cvals1[pt * Q + o] : (o < 2 * Q ? c.cvals2[pt * Q + (o - Q)] : c.cut_cw[pt]);
+            }
+            __syncthreads();
+            for (int t = tid; t < kCpChunk * NPAD; t += kCpThreads) {
+                const int k = t / NPAD, s = t - k * NPAD;
+                const bool ok = k < np && s < NP;
+                P1[k][s] = ok ? (S[k][2 * Q] * S[k][pa[s]]) * S[k][pb[s]] : 0.0;
+                P2[k][s] = ok ? S[k][Q + pa[s]] * S[k][Q + pb[s]] : 0.0;
+            }
+            __syncthreads();
+            for (int k0 = 0; k0 < np; k0 += 4) {
+                double af[TR], bf[TR];
+#pragma unroll
+                for (int i = 0; i < TR; ++i) {
+                    const int tr = wr * TR + i, tc = wc * TR + i;
+                    af[i] = tr < NT8 ? P1[k0 + fk][tr * 8 + fr] : 0.0;
+                    bf[i] = tc < NT8 ? P2[k0 + fk][tc * 8 + fr] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < TR; ++i)
+#pragma unroll
+                    for (int j = 0; j < TR; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
+        }
+        // a group of one piece writes its block directly (the reduce skips it)
+        double* out = gpiece[g + 1] - gpiece[g] == 1 ? E + (int64_t)g * NP * NP : Epart + (int64_t)pc * NP * NP;
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+            for (int j = 0; j < TR; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int s1 = (wr * TR + i) * 8 + fr, s2 = (wc * TR + j) * 8 + 2 * fk + h;
+                    if (s1 < NP && s2 < NP) out[s1 * NP + s2] = acc[i][j][h];
+                }
+    }
+    } else {
+    constexpr int TA = (NP + 7) / 8, TB = (NP + 15) / 16, NA = 8 * TA, NB = 16 * TB;
     __shared__ double S[kCpChunk][ST];
     __shared__ double P1[kCpChunk][NA], P2[kCpChunk][NB];
     __shared__ int pa[NP], pb[NP];
@@ -311,7 +388,6 @@ __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx 
                     for (int j = 0; j < TB; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
             }
         }
-        // a group of one piece writes its block directly (the reduce skips it)
         double* out = gpiece[g + 1] - gpiece[g] == 1 ? E + (int64_t)g * NP * NP : Epart + (int64_t)pc * NP * NP;
 #pragma unroll
         for (int i = 0; i < TA; ++i)
@@ -320,6 +396,7 @@ __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx 
                 const int s1 = ta * TA + i, s2 = tb * TB + j;
                 if (s1 < NP && s2 < NP) out[s1 * NP + s2] = acc[i][j];
             }
+    }
     }
 }
 
