@@ -472,6 +472,10 @@ int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
  * rows' planes. */
 int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, int32_t nstrips, int32_t n1m, int32_t n2m,
                  int32_t nu_max, int32_t b2cap, const double* bw, int32_t* status, void* stream);
+/* resident tq_sf_strips blocks per SM for a launch of that shape (0: the
+ * stage does not fit; < 0: CUDA error) -- the host merges strip classes into
+ * one launch when that does not lower the occupancy */
+int32_t tq_sf_strips_occupancy(int32_t p, int32_t rows, int32_t n1m, int32_t n2m, int32_t nu_max, int32_t b2cap);
 /* the weighted collocation tables of the standard rules tq_sf_strips reads
  * (bw: n_d x nmax_d x the padded window, both directions; size in doubles
  * from tq_bw_table_doubles); *status |= 2 when a rule row is longer than

@@ -57,6 +57,7 @@ def _bind():
     L.optional("tq_coeff_points", [L.Coeff, L.vp, L.i64, L.vp, L.vp, L.vp])
     L.optional("tq_sf_strips", [RawCtx, L.i32, L.vp, L.i32, L.i32, L.i32, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_bw_tables", [RawCtx, L.vp, L.vp, L.vp])
+    L.optional("tq_sf_strips_occupancy", [L.i32] * 6)
     L.optional("tq_gauss_pairs", [RawCtx, L.Coeff, L.vp, L.vp, L.vp, L.i32, L.vp, L.vp, L.vp, L.vp, L.vp, L.vp,
                                   L.vp])
     L.optional("tq_geo_lines", [L.Coeff, L.vp, L.i32, L.vp, L.vp, L.vp])
@@ -358,6 +359,9 @@ STRIP_ROWS = 16
 # direction 2 (smaller shared stage for the other strips); measured: more
 # total kernel time at config 4 p = 8 (fixed per-strip cost), off
 EDGE_STRIPS = os.environ.get("TQ_EDGE_STRIPS", "0") == "1"
+# one strips launch (packed B2 rows) instead of one per shared-memory class:
+# by occupancy (default), TQ_MERGED_STRIPS=1 always, =0 never
+MERGED_STRIPS = os.environ.get("TQ_MERGED_STRIPS")
 
 
 def planes(f):
@@ -454,13 +458,22 @@ def strip_classes(f, pg, layout1, layout2):
                 wp = 3 * ((2 * b1.p + 3) // 3)
                 lens = np.where(rows, cnt2[ii2], 0)
                 alloc = np.where(lens > 0, 2 * (((lens * wp + 1) // 2) | 1), 0).sum(axis=1)
+                if ts == STRIP_ROWS and reg.any() and (~reg).any():
+                    # one launch (packed rows) when it keeps the regular
+                    # class's resident blocks per SM: no tail of a second
+                    # launch (config 4 p = 8: 0.496 -> 0.478 ms)
+                    occ = L.lib().tq_sf_strips_occupancy
+                    merged = occ(b1.p, ts, int(c1.max()), int(c2.max()), max(int(nu.max()), 1), int(alloc.max()))
+                    regular = occ(b1.p, ts, int(c1[reg].max()), int(c2[reg].max()), max(int(nu[reg].max()), 1), 0)
+                    if MERGED_STRIPS == "1" or (MERGED_STRIPS is None and merged >= regular > 0):
+                        groups = (np.ones_like(reg), )
                 for k, sel in enumerate(groups):
                     if sel.any():
                         # the regular class keeps a fixed row stride (every row
                         # an equal odd number of 16-byte units: conflict-free
                         # stage-B reads); the long-rule class packs its rows
                         # (two blocks per SM instead of one)
-                        packed = k > 0 and ts == STRIP_ROWS
+                        packed = (k > 0 or len(groups) == 1) and ts == STRIP_ROWS
                         out.append((ts, L.dev(np.ascontiguousarray(strips[sel]), torch.int32), int(sel.sum()),
                                     int(c1[sel].max()), int(c2[sel].max()), max(int(nu[sel].max()), 1),
                                     int(alloc[sel].max()) if packed else 0))

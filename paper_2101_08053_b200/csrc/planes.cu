@@ -553,6 +553,31 @@ static int sf_strips_launch(const tq_rawctx& c, const int32_t* strips, int32_t n
     return TQ_OK;
 }
 
+template <int P, int TS>
+static int sf_strips_occupancy(int32_t n1m, int32_t n2m, int32_t nu_max, int32_t b2cap) {
+    const size_t shm = sizeof(double) * strip_smem_doubles(P, n1m, n2m, nu_max, TS, b2cap);
+    if (shm > 220 * 1024) return 0;
+    auto kern = k_sf_strips<P, TS>;
+    constexpr int NT = 32 * ((TS * 9 + 31) / 32) + 32;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess) return -1;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, shm) != cudaSuccess) return -1;
+    return per_sm;
+}
+
+// resident tq_sf_strips blocks per SM of a launch class (the host groups
+// strips into launches by it); < 0 on a CUDA error
+extern "C" int32_t tq_sf_strips_occupancy(int32_t p, int32_t rows, int32_t n1m, int32_t n2m, int32_t nu_max,
+                                          int32_t b2cap) {
+    switch (p) {
+#define CASE(Q) case Q: return rows == 8 ? sf_strips_occupancy<Q, 8>(n1m, n2m, nu_max, b2cap) \
+                                          : sf_strips_occupancy<Q, kStripRows>(n1m, n2m, nu_max, b2cap);
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    }
+    return -1;
+}
+
 extern "C" int64_t tq_bw_table_doubles(tq_rawctx c) {
     return (int64_t)c.n1 * bw_row(c.p1, c.nmax1) + (int64_t)c.n2 * bw_row(c.p2, c.nmax2);
 }

@@ -10,7 +10,7 @@ f, _ = A.form(b2d, cfg, c4["coeff"], "dwq")
 pg = R.planes_geo(f)
 cl = R.strip_classes(f, pg, f._setup.sets[0][0].layout, f._setup.sets[1][0].layout)
 WP = 3 * ((2 * p + 3) // 3)
-for ts, sd, ns, n1m, n2m, nu in cl:
+for ts, sd, ns, n1m, n2m, nu, b2cap in cl:
     gs = (n1m * WP + 1) & ~1
     glen = (nu + 3) & ~1
     b2 = gs + n1m * glen
