@@ -96,6 +96,14 @@ int tq_version(void);
 /* keep freed cudaMallocAsync memory in the device's default pool (release
  * threshold = max) so scratch allocations of later calls re-map nothing */
 int tq_pool_keep(int32_t device);
+/* a captured graph (cudaGraph_t) instantiated with per-node priorities
+ * (use_node_priority != 0: each kernel node runs at the priority of the
+ * stream it was captured on), launched, destroyed; node priority census
+ * (hist[k] = kernel nodes of priority -k, k < 8) */
+int tq_graph_instantiate(void* graph, int32_t use_node_priority, void** exec);
+int tq_graph_launch(void* exec, void* stream);
+int tq_graph_exec_destroy(void* exec);
+int tq_graph_node_priorities(void* graph, int32_t* hist, int32_t* nkernels);
 const char* tq_last_error(void);
 int tq_device_sync(void* stream);
 /* kernels launched by the library since it was loaded (host counter) */

@@ -586,6 +586,12 @@ STAMPS = None     # timeline probe (an _lib.Stamps) -- development aid
 # default since the single-stage fill: the early fill's memory traffic slows
 # the latency-bound count pass 2 by more than it saves, measured at config 5)
 HEAD_FILL = int(os.environ.get("TQ_HEAD_FILL", "0"))
+# TQ_GRAPH_PRIO=1: replayed graphs honour the capture streams' priorities
+# (instantiated by the library with per-node priorities; the kernel nodes do
+# carry them, GraphFormation.node_priorities).  Default off: measured equal
+# at config 4 and 3-5 us slower at config 5 than torch's instantiation, which
+# runs every node at the launch stream's priority
+GRAPH_NODE_PRIORITY = os.environ.get("TQ_GRAPH_PRIO", "0") == "1"
 # count pass 2 counts interior separable rows on positive factor lines
 # geometrically (their partner sums are positive; the fill verifies them)
 GEOMETRIC_NEAR = os.environ.get("TQ_GEOMETRIC_NEAR", "1") == "1"
@@ -658,6 +664,19 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
 FILL_EVENTS = None
 
 
+def _graph_handle(graph):
+    """cudaGraph_t of a torch CUDAGraph(keep_graph=True) as an int."""
+    h = graph.raw_cuda_graph()
+    if isinstance(h, int):
+        return h
+    for conv in (int, lambda x: int(x.getPtr()), lambda x: x.value):
+        try:
+            return int(conv(h))
+        except Exception:
+            continue
+    raise RuntimeError(f"cannot read the cudaGraph_t handle from {type(h)}")
+
+
 class GraphFormation:
     """One formation pass captured as a CUDA graph and replayed.
 
@@ -687,7 +706,7 @@ class GraphFormation:
             form(*self.args, row_range=row_range, capture={"nnz": self.nnz})
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
+        self.graph = torch.cuda.CUDAGraph(keep_graph=True)
         lib = L.lib()
         lib.tq_launch_count.restype = L.C.c_longlong
         n0 = lib.tq_launch_count()
@@ -700,11 +719,39 @@ class GraphFormation:
         finally:
             FILL_EVENTS = None
         self.launches_per_pass = int(lib.tq_launch_count() - n0)
+        # instantiated by the library with per-node priorities: the capture
+        # streams' priorities (fit chain, pass-start chains, bulk work) hold
+        # in every replay (a default instantiation runs all nodes at the
+        # launch stream's priority)
+        self._exec = None
+        if GRAPH_NODE_PRIORITY:
+            ex = L.vp()
+            L.call("tq_graph_instantiate", L.vp(_graph_handle(self.graph)), 1, L.C.byref(ex))
+            self._exec = ex
+        else:
+            self.graph.instantiate()
         torch.cuda.synchronize()
 
+    def node_priorities(self):
+        """Kernel nodes of the captured graph by priority (hist[k]: -k)."""
+        hist, nk = (L.i32 * 8)(), L.i32(0)
+        L.call("tq_graph_node_priorities", L.vp(_graph_handle(self.graph)), hist, L.C.byref(nk))
+        return list(hist), int(nk.value)
+
     def run(self):
-        self.graph.replay()
+        if self._exec is not None:
+            L.call("tq_graph_launch", self._exec, L.stream())
+        else:
+            self.graph.replay()
         return self.csr
+
+    def __del__(self):
+        ex = getattr(self, "_exec", None)
+        if ex is not None and L is not None:
+            try:
+                L.lib().tq_graph_exec_destroy(ex)
+            except Exception:
+                pass
 
     def check(self):
         """Status of the last replay (host reads after the pass; the

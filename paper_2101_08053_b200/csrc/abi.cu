@@ -2,6 +2,7 @@
 #include <stdarg.h>
 
 #include <atomic>
+#include <vector>
 
 #include "common.cuh"
 
@@ -62,5 +63,57 @@ __global__ void k_stamp(unsigned long long* stamps, int slot) {
 extern "C" int tq_debug_stamp(unsigned long long* stamps, int32_t slot, void* stream) {
     k_stamp<<<1, 1, 0, tq::S(stream)>>>(stamps, slot);
     TQ_LAUNCH_CHECK("k_stamp");
+    return TQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Graph execution with per-node priorities.  A stream-captured kernel node
+// keeps the priority of the stream it was captured on; a graph instantiated
+// without cudaGraphInstantiateFlagUseNodePriority runs every node at the
+// priority of the stream it is launched into, which drops the pass's
+// schedule (fit chain and pass-start chains ahead of the bulk work).
+// ---------------------------------------------------------------------------
+extern "C" int tq_graph_instantiate(void* graph, int32_t use_node_priority, void** exec) {
+    if (!graph || !exec) { tq::set_error("tq_graph_instantiate: null graph"); return TQ_EINVAL; }
+    cudaGraphExec_t e = nullptr;
+    TQ_CUDA(cudaGraphInstantiateWithFlags(&e, static_cast<cudaGraph_t>(graph),
+                                          use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0));
+    *exec = e;
+    return TQ_OK;
+}
+
+extern "C" int tq_graph_launch(void* exec, void* stream) {
+    TQ_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), tq::S(stream)));
+    return TQ_OK;
+}
+
+extern "C" int tq_graph_exec_destroy(void* exec) {
+    if (exec) TQ_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
+    return TQ_OK;
+}
+
+// kernel nodes of a graph by their priority attribute: hist[0..7] counts
+// priorities 0, -1, .., -7 (clamped); returns the number of kernel nodes
+extern "C" int tq_graph_node_priorities(void* graph, int32_t* hist, int32_t* nkernels) {
+    size_t n = 0;
+    TQ_CUDA(cudaGraphGetNodes(static_cast<cudaGraph_t>(graph), nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    TQ_CUDA(cudaGraphGetNodes(static_cast<cudaGraph_t>(graph), nodes.data(), &n));
+    for (int k = 0; k < 8; ++k) hist[k] = 0;
+    int nk = 0;
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType t;
+        TQ_CUDA(cudaGraphNodeGetType(nodes[i], &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        ++nk;
+        cudaLaunchAttributeValue v;
+        if (cudaGraphKernelNodeGetAttribute(nodes[i], cudaLaunchAttributePriority, &v) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        const int pr = v.priority;
+        hist[pr > 0 ? 0 : (pr < -7 ? 7 : -pr)] += 1;
+    }
+    *nkernels = nk;
     return TQ_OK;
 }
