@@ -313,21 +313,30 @@ __global__ void __launch_bounds__(kL2Chunk, 8) k_l2_elements_s(tq_projctx c, con
 // Tiled form of k_l2_elements_s: a block takes a tile of kL2Rows element rows
 // x kL2Chunk element columns, stages the columns' direction-2 tables ONCE for
 // the tile's rows (k_l2_elements_s re-staged them for every row: the staging
-// loads, not the sums, set its time) and the rows' direction-1 tables, and a
-// thread walks its column down the tile's rows.  Per element the terms and
+// loads, not the sums, set its time), the rows' direction-1 tables and the
+// tile's coefficient window, and two threads walk each column down the
+// tile's rows (alternate rows; 224 registers, two blocks per SM: measured
+// best against 168 / 128-register bounds).  Per element the terms and
 // their order are those of k_l2_elements_s; only the order of the partial
 // sums over elements changes.
-constexpr int kL2Rows = 16;
+constexpr int kL2Rows = 16, kL2Threads = 2 * kL2Chunk;
+#ifndef TQ_L2_MINB
+#define TQ_L2_MINB 2
+#endif
 
 template <int P>
-__global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const double* __restrict__ C,
+__global__ void __launch_bounds__(kL2Threads, TQ_L2_MINB) k_l2_tiles(tq_projctx c, const double* __restrict__ C,
                                                          int64_t e_begin, int64_t e_end, double* __restrict__ parts) {
     extern __shared__ double sm[];
-    __shared__ double red[2][kL2Chunk / 32];
+    __shared__ double red[2][kL2Threads / 32];
     constexpr int Q = P + 1, G = P + 3, ST = l2_stride(P);
     constexpr int R1 = G * Q + 3 * G;                            // per element row: V1, x, w1, phi
     const bool sep = c.target.kind == 2 && c.target.nterms == 1;
     double* rows = sm + kL2Chunk * ST;                           // [kL2Rows][R1]
+    // the tile's coefficient window: rows f1(e1a) .. f1(last) + P, columns
+    // f2(e2a) .. f2(last) + P (staged when it fits; else read from C)
+    constexpr int CR = kL2Rows + P, CC = kL2Chunk + P, LDC = CC | 1;
+    double* cs = rows + kL2Rows * R1;                            // [CR][LDC]
     double num = 0.0, den = 0.0;
     const int r_first = (int)(e_begin / c.nel2), r_last = (int)((e_end - 1) / c.nel2);
     const int nrt = (r_last - r_first + kL2Rows) / kL2Rows, nct = (c.nel2 + kL2Chunk - 1) / kL2Chunk;
@@ -338,11 +347,11 @@ __global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const do
         const int e1a = r_first + rt * kL2Rows, e2a = ct * kL2Chunk;
         const int nr = min(kL2Rows, r_last + 1 - e1a), ncol = min(kL2Chunk, c.nel2 - e2a);
         __syncthreads();
-        for (int q = threadIdx.x; q < ncol * (G * Q); q += kL2Chunk) {
+        for (int q = threadIdx.x; q < ncol * (G * Q); q += kL2Threads) {
             const int j = q / (G * Q), k = q - j * (G * Q);
             sm[j * ST + k] = c.v2[(int64_t)(e2a + j) * G * Q + k];
         }
-        for (int q = threadIdx.x; q < ncol * G; q += kL2Chunk) {
+        for (int q = threadIdx.x; q < ncol * G; q += kL2Threads) {
             const int j = q / G, g = q - j * G;
             const int64_t pc = (int64_t)(e2a + j) * G + g;
             double* o = sm + j * ST + G * Q;
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const do
             o[G + g] = c.w2[pc];
             o[2 * G + g] = sep ? c.target.grid[c.target.ld + pc] : 0.0;
         }
-        for (int q = threadIdx.x; q < nr * R1; q += kL2Chunk) {
+        for (int q = threadIdx.x; q < nr * R1; q += kL2Threads) {
             const int rr = q / R1, k = q - rr * R1;
             const int e1 = e1a + rr;
             double v;
@@ -360,23 +369,40 @@ __global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const do
             else v = sep ? c.target.grid[(int64_t)e1 * G + (k - G * Q - 2 * G)] : 0.0;
             rows[rr * R1 + k] = v;
         }
+        const int r0 = c.espan1[e1a] - P, rn = c.espan1[e1a + nr - 1] + 1 - r0;
+        const int c0 = c.espan2[e2a] - P, cn = c.espan2[e2a + ncol - 1] + 1 - c0;
+        const bool staged = rn <= CR && cn <= CC;                   // (uniform across the block)
+        if (staged)
+            for (int q = threadIdx.x; q < rn * cn; q += kL2Threads) {
+                const int rr = q / cn, cc = q - rr * cn;
+                cs[rr * LDC + cc] = C[(int64_t)(r0 + rr) * c.n2 + c0 + cc];
+            }
         __syncthreads();
-        const int j = threadIdx.x;
+        // two threads per column, alternate rows
+        const int j = threadIdx.x % kL2Chunk, h = threadIdx.x / kL2Chunk;
         if (j >= ncol) continue;
         const int e2 = e2a + j;
         const int f2 = c.espan2[e2] - P;
         const double* s2 = sm + j * ST;
-        for (int rr = 0; rr < nr; ++rr) {
+        for (int rr = h; rr < nr; rr += kL2Threads / kL2Chunk) {
             const int e1 = e1a + rr;
             const int64_t t = (int64_t)e1 * c.nel2 + e2;
             if (t < e_begin || t >= e_end || c.elem_class[t] != TQ_INTERIOR) continue;
             const int f1 = c.espan1[e1] - P;
             const double* r1 = rows + rr * R1;
             double cb[Q][Q];
+            if (staged) {
+                const double* cw = cs + (f1 - r0) * LDC + (f2 - c0);
 #pragma unroll
-            for (int a1 = 0; a1 < Q; ++a1)
+                for (int a1 = 0; a1 < Q; ++a1)
 #pragma unroll
-                for (int a2 = 0; a2 < Q; ++a2) cb[a1][a2] = C[(int64_t)(f1 + a1) * c.n2 + f2 + a2];
+                    for (int a2 = 0; a2 < Q; ++a2) cb[a1][a2] = cw[a1 * LDC + a2];
+            } else {
+#pragma unroll
+                for (int a1 = 0; a1 < Q; ++a1)
+#pragma unroll
+                    for (int a2 = 0; a2 < Q; ++a2) cb[a1][a2] = C[(int64_t)(f1 + a1) * c.n2 + f2 + a2];
+            }
 #pragma unroll 1
             for (int g2 = 0; g2 < G; ++g2) {
                 double S[Q];
@@ -418,7 +444,7 @@ __global__ void __launch_bounds__(kL2Chunk, 6) k_l2_tiles(tq_projctx c, const do
     __syncthreads();
     if (threadIdx.x == 0) {
         double a = 0.0, d = 0.0;
-        for (int k = 0; k < kL2Chunk / 32; ++k) { a += red[0][k]; d += red[1][k]; }
+        for (int k = 0; k < kL2Threads / 32; ++k) { a += red[0][k]; d += red[1][k]; }
         parts[2 * blockIdx.x] = a;
         parts[2 * blockIdx.x + 1] = d;
     }
@@ -608,13 +634,14 @@ extern "C" int tq_l2_parts(tq_projctx c, const double* C, int64_t e_begin, int64
                           c.nel2 >= kL2Chunk;
         if (tq_t) {
             static const bool tiled = !(getenv("TQ_L2_ROWS") && atoi(getenv("TQ_L2_ROWS")) == 1);   // A/B knob
-            const size_t shm = tiled ? sizeof(double) * (kL2Chunk * l2_stride(c.p1) + kL2Rows * l2_stride(c.p1))
+            const size_t shm = tiled ? sizeof(double) * (kL2Chunk * l2_stride(c.p1) + kL2Rows * l2_stride(c.p1) +
+                                                         (kL2Rows + c.p1) * ((kL2Chunk + c.p1) | 1))
                                      : sizeof(double) * (kL2Chunk + 2) * l2_stride(c.p1);
             switch (c.p1) {
 #define CASE(P) case P: \
                 if (tiled) { \
                     TQ_CUDA(cudaFuncSetAttribute(k_l2_tiles<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
-                    k_l2_tiles<P><<<nbe, kL2Chunk, shm, st>>>(c, C, e_begin, e_end, parts); \
+                    k_l2_tiles<P><<<nbe, kL2Threads, shm, st>>>(c, C, e_begin, e_end, parts); \
                 } else { \
                     TQ_CUDA(cudaFuncSetAttribute(k_l2_elements_s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
                     k_l2_elements_s<P><<<nbe, kL2Chunk, shm, st>>>(c, C, e_begin, e_end, parts); \
