@@ -10,6 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -234,11 +236,14 @@ class Stamps:
 
 
 _POOLS_KEPT = set()
+_HAVE_CUDA = []
 
 
 def device():
-    if not torch.cuda.is_available():
-        raise RuntimeError("trimquad_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    if not _HAVE_CUDA:        # (torch.cuda.is_available queries NVML: once per process)
+        if not torch.cuda.is_available():
+            raise RuntimeError("trimquad_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+        _HAVE_CUDA.append(True)
     d = torch.cuda.current_device()
     if d not in _POOLS_KEPT:      # once per device: freed scratch stays in the stream-ordered pool
         _POOLS_KEPT.add(d)
@@ -271,24 +276,79 @@ def ptr(t):
 
 
 _pinned_keep = []
+_NP_DTYPE = {torch.float64: np.float64, torch.float32: np.float32, torch.int64: np.int64,
+             torch.int32: np.int32, torch.int8: np.int8, torch.uint8: np.uint8, torch.int16: np.int16}
 _PAGEABLE_UPLOADS = os.environ.get("TQ_PAGEABLE_UPLOADS", "0") == "1"     # A/B knob
 
 
+class _StagingRing:
+    """Pinned host ring for small uploads: the array is written into the
+    next free slot and copied from there (no per-upload pinned allocation).
+    A slot is reused only after the copy that read it has run: an event per
+    use, and a new lap of the ring waits for every copy of the previous one."""
+
+    SIZE = 8 << 20
+
+    def __init__(self):
+        import collections
+        self.buf = torch.empty(self.SIZE, dtype=torch.uint8, pin_memory=True)
+        self.host = self.buf.numpy()
+        self.head = 0
+        self.pending = collections.deque()       # events of this lap's copies
+
+    def stage(self, a):
+        n = (a.nbytes + 255) & ~255
+        if n > self.SIZE // 4:
+            return None
+        if self.head + n > self.SIZE:
+            # a new lap: every copy of the previous one must have run (rare:
+            # 8 MB of small uploads per lap); within a lap slots never overlap
+            while self.pending:
+                self.pending.popleft().synchronize()
+            self.head = 0
+        while self.pending and self.pending[0].query():
+            self.pending.popleft()
+        lo = self.head
+        self.host[lo: lo + a.nbytes] = a.reshape(-1).view(np.uint8)
+        self.head = lo + n
+        return self.buf[lo: lo + a.nbytes]
+
+    def done(self, view):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.pending.append(ev)
+
+
+_RINGS = {}
+
+
 def dev(x, dtype):
-    """Upload a host array (numpy) as a contiguous device tensor: staged in
-    pinned memory and copied asynchronously on the current stream (no host
-    sync; torch's caching host allocator keeps the staging block until the
-    copy has run).  Under CUDA stream capture the pinned source is kept alive
-    for good (every replay reads it again)."""
-    import numpy as np
-    a = np.array(x, copy=True) if not np.asarray(x).flags.writeable else np.ascontiguousarray(x)
-    src = torch.from_numpy(np.ascontiguousarray(a))
-    if src.numel() == 0:
-        return torch.empty(src.shape, dtype=dtype, device=device())
-    if _PAGEABLE_UPLOADS and not torch.cuda.is_current_stream_capturing():
-        return src.to(device=device(), dtype=dtype, non_blocking=False).contiguous()
+    """Upload a host array (numpy) as a contiguous device tensor, copied
+    asynchronously on the current stream (no host sync).  Small arrays go
+    through a pinned staging ring (_StagingRing); larger ones are staged in
+    pinned memory from torch's caching host allocator, which keeps the block
+    until the copy has run.  Under CUDA stream capture the pinned source is
+    kept alive for good (every replay reads it again)."""
+    a = np.ascontiguousarray(x, dtype=_NP_DTYPE.get(dtype))
+    if a.size == 0:
+        return torch.empty(a.shape, dtype=dtype, device=device())
+    capturing = torch.cuda.is_current_stream_capturing()
+    if _PAGEABLE_UPLOADS and not capturing:
+        return torch.from_numpy(a.copy()).to(device=device(), dtype=dtype, non_blocking=False).contiguous()
+    if not capturing and dtype in _NP_DTYPE:
+        d = device()
+        ring = _RINGS.get(d.index)
+        if ring is None:
+            ring = _RINGS[d.index] = _StagingRing()
+        view = ring.stage(a)
+        if view is not None:
+            out = torch.empty(a.shape, dtype=dtype, device=d)
+            out.view(-1).view(torch.uint8).copy_(view, non_blocking=True)
+            ring.done(view)
+            return out
+    src = torch.from_numpy(a.copy() if not a.flags.writeable else a)
     src = src.pin_memory()
-    if torch.cuda.is_current_stream_capturing():
+    if capturing:
         _pinned_keep.append(src)
     out = src.to(device=device(), non_blocking=True)
     return out if out.dtype == dtype else out.to(dtype)

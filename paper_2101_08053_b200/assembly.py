@@ -532,7 +532,7 @@ class Formation:
         for st in getattr(self, "_status_streams", []):       # status reductions rejoin
             torch.cuda.current_stream().wait_stream(st)
         _stamp("fill")
-        if self.capture is None and ctx.fclass and int(tiles[L.tile_ctl(nrows) + 8].item()):
+        if self.capture is None and nrows > 0 and ctx.fclass and int(tiles[L.tile_ctl(nrows) + 8].item()):
             raise RuntimeError("a geometrically counted row dropped an entry (rowctx.fclass): pattern inconsistent")
         return DeviceCSR(indptr, indices[:nnz], data[:nnz], row_begin, row_end, nnz)
 
@@ -766,7 +766,7 @@ class GraphFormation:
             st = getattr(self.f, "_planes_status", None)
             if st is not None and int(st.item()):
                 raise RuntimeError("planes path status word set in a replayed pass (tq_sf_strips / tq_cut_rows_gather)")
-        else:
+        elif self.f._nrows > 0:
             ctl = self.f._count_bufs[1][L.tile_ctl(self.f._nrows):].cpu()
             if int(ctl[4]):
                 raise RuntimeError("replayed pass formed a different nnz than the captured one")
