@@ -222,7 +222,12 @@ extern "C" int tq_basis_eval_multi(const tq_evalbatch* batch_h, void* stream) {
         stage = std::max(stage, (size_t)B.task[k].s.nknots * sizeof(double));
     }
     if (p < 0 || p > kMaxP) { set_error("degree %d unsupported", p); return TQ_EINVAL; }
-    if (stage > 32 * 1024) stage = 0;           // large knot vectors: read through L1
+    // a block evaluates ~256 points (one per thread): staging the knots pays
+    // only while they are few; large knot vectors are read through L1 (the
+    // staging of 2053 knots per block dominated the launch at config 5)
+    static const size_t stage_max = getenv("TQ_BASIS_STAGE_MAX") ? (size_t)atol(getenv("TQ_BASIS_STAGE_MAX"))
+                                                                  : 512 * sizeof(double);
+    if (stage > stage_max) stage = 0;
     B.stage_bytes = (int32_t)stage;
     const int grid = B.block_start[B.ntasks];
     switch (p) {
