@@ -1,3 +1,2 @@
-for v in 32768 4096; do TQ_BASIS_STAGE_MAX=$v ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -k regex:"k_basis_eval_multi" python scripts/step_launches.py 2048 eager 2>&1 | grep -E "duration"; done
-for v in 32768 4096 32768 4096; do TQ_BASIS_STAGE_MAX=$v timeout 600 python bench.py --no-config4 --e2e-steps 0 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v c5', d['ms_per_step'])"; done
-for v in 32768 4096; do TQ_BASIS_STAGE_MAX=$v timeout 300 python scripts/config4_probe.py 8 256 2>&1 | tail -1 | cut -c60-110; done
+for v in "" ef "" ef; do lib=paper_2101_08053_b200/libtq_b200${v:+_$v}.so
+ TQ_LIB=$PWD/$lib timeout 600 python bench.py --no-config4 --e2e-steps 0 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v c5', d['ms_per_step'], d['kernels_ms_per_step'], d['roofline']['frac'])"; done
