@@ -463,6 +463,15 @@ int tq_cut_blocks(tq_rawctx c, void* stream);
 int tq_elem_mass(const double* ev, const double* ew, int32_t nel, int32_t ng, int32_t p, double* em,
                  void* stream);
 int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+/* per-row span-key group lists of raw rows [r0, r1) (geometry of the plan):
+ * off == NULL: out = the counts (r1 - r0 ints); else out = the triplets
+ * (group, key1, key2) at 3 * off[r - r0] (off: exclusive prefix of the
+ * counts) -- in tq_raw_cutcells's order */
+int tq_row_groups(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* off, int32_t* out, void* stream);
+/* tq_raw_cutcells over those lists (rg_ptr: r1 - r0 + 1 offsets); the same
+ * additions in the same order */
+int tq_raw_cutcells_list(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* rg_ptr, const int32_t* rg,
+                         void* stream);
 
 /* ---- the all-raw path in the planes layout (c.raw_ld > 0) --------------- */
 

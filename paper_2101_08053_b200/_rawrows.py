@@ -48,6 +48,8 @@ class RawCtx(C.Structure):
 def _bind():
     L.optional("tq_raw_regular", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_raw_cutcells", [RawCtx, L.i32, L.i32, L.vp])
+    L.optional("tq_row_groups", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp])
+    L.optional("tq_raw_cutcells_list", [RawCtx, L.i32, L.i32, L.vp, L.vp, L.vp])
     L.optional("tq_cut_blocks", [RawCtx, L.vp])
     L.optional("tq_raw_gauss", [RawCtx, L.i32, L.i32, L.vp])
     L.optional("tq_raw_sumfactor", [RawCtx, L.i32, L.i32, L.vp])
@@ -595,6 +597,34 @@ def _cut_pieces(f, cut):
         t["pieces"] = (pieces if npieces else torch.zeros((1, 2), dtype=torch.int64, device=f.dev),
                        gpiece.to(torch.int32), npieces)
     return t["pieces"]
+
+
+# the cut-cell rows gathered over per-row group lists (geometry, built once
+# per plan on the device) instead of scanning each row's element window
+CUTCELL_LISTS = os.environ.get("TQ_CUTCELL_LISTS", "1") == "1"
+
+
+def raw_row_groups(f):
+    """Span-key groups of every raw row of the plan, in tq_raw_cutcells's
+    order (tq_row_groups: counts, prefix, triplets) -- geometry, cached per
+    plan and cut-point tables: (rg_ptr int32 ndesc + 1, rg int32 3 x total)."""
+    desc, _ = _plan(f)
+    t = cut_point_tables(f)
+    g = _geo(f.config)
+    key = ("raw_row_groups", id(desc), id(t))
+    if key not in g:
+        n = int(f._ndesc)
+        counts = torch.empty(max(n, 1), dtype=torch.int32, device=f.dev)
+        L.call("tq_row_groups", f._ctx, 0, n, None, L.ptr(counts), L.stream())
+        rg_ptr = torch.zeros(n + 1, dtype=torch.int32, device=f.dev)
+        if n:
+            rg_ptr[1:] = torch.cumsum(counts[:n], 0)
+        total = int(rg_ptr[-1].item())          # once per plan (the eager pass)
+        rg = torch.empty(max(3 * total, 3), dtype=torch.int32, device=f.dev)
+        L.call("tq_row_groups", f._ctx, 0, n, L.ptr(rg_ptr), L.ptr(rg), L.stream())
+        g[key] = (rg_ptr, rg)
+        g[key + ("keep",)] = (desc, t)
+    return g[key]
 
 
 def cut_row_groups(f, r0, r1):
@@ -1329,4 +1359,8 @@ def run_phase(f, phase):
                 L.call("tq_cut_blocks", _cut_blocks_ctx(f, f._setup.cut, _group_range(f, f._setup.cut)),
                        L.stream())
             join_cut_blocks(f)
-            L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())
+            if CUTCELL_LISTS:
+                rg_ptr, rg = raw_row_groups(f)
+                L.call("tq_raw_cutcells_list", f._ctx, 0, f._ndesc, L.ptr(rg_ptr), L.ptr(rg), L.stream())
+            else:
+                L.call("tq_raw_cutcells", f._ctx, 0, f._ndesc, L.stream())

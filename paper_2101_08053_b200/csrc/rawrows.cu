@@ -777,6 +777,111 @@ __global__ void k_raw_cutcells(tq_rawctx c, int r0, int r1) {
     }
 }
 
+// Per raw row, the span-key groups k_raw_cutcells adds (cut elements of the
+// row's support window in window order, their groups in order, key within
+// the row's reach): geometry of the plan, built once per configuration
+// (COUNT: the counts; else the (group, key1, key2) triplets at off[r - r0]).
+template <bool COUNT>
+__global__ void k_row_groups(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ off, int32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = r0 + warp; r < r1; r += nw) {
+        RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const int ea1 = max(c.el_first1[i1] - 1, 0), eb1 = min(c.el_last1[i1] + 1, c.nel1 - 1);
+        const int ea2 = max(c.el_first2[i2] - 1, 0), eb2 = min(c.el_last2[i2] + 1, c.nel2 - 1);
+        const int w2 = eb2 - ea2 + 1, nh = (eb1 - ea1 + 1) * w2;
+        int n = 0;
+        int32_t* o = COUNT ? nullptr : out + 3 * (int64_t)off[r - r0];
+        for (int h0 = 0; h0 < nh; h0 += 32) {
+            const int h = h0 + lane;
+            const int id = h < nh ? c.cutidx[(int64_t)(ea1 + h / w2) * c.nel2 + (ea2 + h % w2)] : -1;
+            unsigned m = __ballot_sync(0xffffffffu, id >= 0);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const int cid = __shfl_sync(0xffffffffu, id, src);
+                const int gb = c.grp_ptr[cid], ge = c.grp_ptr[cid + 1];
+                for (int g0 = gb; g0 < ge; g0 += 32) {       // lanes over the element's groups
+                    const int g = g0 + lane;
+                    bool ok = false;
+                    int f1 = 0, f2 = 0;
+                    if (g < ge) {
+                        f1 = c.grp_key[2 * g];
+                        f2 = c.grp_key[2 * g + 1];
+                        const int a1 = i1 - f1, a2 = i2 - f2;
+                        ok = a1 >= 0 && a1 <= c.p1 && a2 >= 0 && a2 <= c.p2;
+                    }
+                    const unsigned vm = __ballot_sync(0xffffffffu, ok);
+                    if (!COUNT && ok) {
+                        const int at = n + __popc(vm & ((1u << lane) - 1u));
+                        o[3 * at] = g;
+                        o[3 * at + 1] = f1;
+                        o[3 * at + 2] = f2;
+                    }
+                    n += __popc(vm);
+                }
+            }
+        }
+        if (COUNT && lane == 0) out[r - r0] = n;
+    }
+}
+
+// k_raw_cutcells over the per-row group lists (k_row_groups): the group
+// row slices of a batch of kCcBatch groups are loaded together, then added
+// in list order into a shared copy of the row (row-major raw rows: loaded
+// first, so the result is bit-identical to k_raw_cutcells; planes: summed
+// from zero and added, as there).  A few dependent load rounds per row
+// instead of the element-window scan and two global round trips per group.
+constexpr int kCcBatch = 8;
+
+__global__ void k_raw_cutcells_list(tq_rawctx c, int r0, int r1, const int32_t* __restrict__ rg_ptr,
+                                    const int32_t* __restrict__ rg) {
+    extern __shared__ double sm[];
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+    const int W2 = 2 * c.p2 + 1, T = (2 * c.p1 + 1) * W2;
+    const int q2 = c.p2 + 1, Q = (c.p1 + 1) * q2;
+    double* acc = sm + wib * T;
+    const int lb1 = lane / q2, lb2 = lane - (lane / q2) * q2;
+    for (int r = r0 + blockIdx.x * wpb + wib; r < r1; r += gridDim.x * wpb) {
+        const int gb = __ldg(rg_ptr + (r - r0)), ge = __ldg(rg_ptr + (r - r0) + 1);
+        if (ge == gb) continue;
+        RowDesc d = reinterpret_cast<const RowDesc*>(c.desc)[r];
+        const int i1 = d.fidx / c.n2, i2 = d.fidx - (d.fidx / c.n2) * c.n2;
+        const RawRow out = raw_row(c, r);
+        for (int q = lane; q < T; q += 32) acc[q] = c.raw_ld ? 0.0 : out[q];
+        __syncwarp();
+        for (int k0 = gb; k0 < ge; k0 += kCcBatch) {
+            double v[kCcBatch];
+            int at[kCcBatch];
+#pragma unroll
+            for (int u = 0; u < kCcBatch; ++u) {
+                const int k = k0 + u;
+                at[u] = -1;
+                v[u] = 0.0;
+                if (k < ge && lane < Q) {
+                    const int g = __ldg(rg + 3 * k), f1 = __ldg(rg + 3 * k + 1), f2 = __ldg(rg + 3 * k + 2);
+                    const int a1 = i1 - f1, a2 = i2 - f2;
+                    v[u] = __ldg(c.grp_blocks + ((int64_t)g * Q + (a1 * q2 + a2)) * Q + lane);
+                    at[u] = (f1 + lb1 - i1 + c.p1) * W2 + (f2 + lb2 - i2 + c.p2);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kCcBatch; ++u) {
+                if (at[u] >= 0) acc[at[u]] += v[u];
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        if (c.raw_ld) {
+            for (int q = lane; q < T; q += 32) out[q] += acc[q];
+        } else {
+            for (int q = lane; q < T; q += 32) out[q] = acc[q];
+        }
+        __syncwarp();
+    }
+}
+
 __device__ inline double detj(const tq_coeff& g, double u, double v) {
     double N1[kMaxP + 1], D1[kMaxP + 1], N2[kMaxP + 1], D2[kMaxP + 1];
     const int nk = g.n + g.p + 1;
@@ -1150,6 +1255,36 @@ extern "C" int tq_cut_blocks(tq_rawctx c, void* stream) {
     }
     ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_cut_blocks");
+    return TQ_OK;
+}
+
+extern "C" int tq_raw_cutcells(tq_rawctx c, int32_t r0, int32_t r1, void* stream);
+
+// per-row group lists of rows [r0, r1) (geometry): counts (r1 - r0 ints),
+// then, with off = their exclusive prefix (r1 - r0 ints), the triplets
+// (3 * total ints: group, key1, key2)
+extern "C" int tq_row_groups(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* off, int32_t* out, void* stream) {
+    if (r1 <= r0) return TQ_OK;
+    if (!c.cut_ptr || c.ngroups <= 0) { set_error("tq_row_groups needs the cut-element tables"); return TQ_EINVAL; }
+    const int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 16);
+    if (off) k_row_groups<false><<<grid, 256, 0, S(stream)>>>(c, r0, r1, off, out);
+    else k_row_groups<true><<<grid, 256, 0, S(stream)>>>(c, r0, r1, nullptr, out);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_groups");
+    return TQ_OK;
+}
+
+// tq_raw_cutcells with the rows' group lists of tq_row_groups (rg_ptr:
+// r1 - r0 + 1 offsets, rg: triplets)
+extern "C" int tq_raw_cutcells_list(tq_rawctx c, int32_t r0, int32_t r1, const int32_t* rg_ptr, const int32_t* rg,
+                                    void* stream) {
+    if (r1 <= r0 || !c.cut_ptr || c.ngroups <= 0) return TQ_OK;
+    if ((c.p1 + 1) * (c.p2 + 1) > 32) return tq_raw_cutcells(c, r0, r1, stream);     // a lane per slice entry
+    const int grid = (int)std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)kSms * 16);
+    const size_t shm = sizeof(double) * 8 * (2 * c.p1 + 1) * (2 * c.p2 + 1);
+    k_raw_cutcells_list<<<grid, 256, shm, S(stream)>>>(c, r0, r1, rg_ptr, rg);
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_raw_cutcells_list");
     return TQ_OK;
 }
 

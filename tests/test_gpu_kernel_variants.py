@@ -159,3 +159,39 @@ def test_wide_cut_blocks_bit_identical(tmp_path, kind, nel, p, strategy):
         out[mode] = [z[k] for k in ("arr_0", "arr_1", "arr_2")]
     for a, b in zip(out["wide"], out["warp"]):
         assert np.array_equal(a, b)
+
+
+_CUTCELL_SNIPPET = """
+import hashlib, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+from paper_2101_08053_b200 import cases as C, assembly as A
+for nel in (96, 256):
+    c5 = C.baseline_config(5, nel=nel)
+    b2d, cfg = C.build_space(None, nel, 4, curves=c5["curves"])
+    for s in ("dwq", "hybrid", "wq"):
+        M = A.assemble_mass(b2d, cfg, None, strategy=s).data
+        h = hashlib.sha256()
+        for a in (M.indptr, M.indices, M.data):
+            h.update(np.ascontiguousarray(a).tobytes())
+        print(nel, s, M.nnz, h.hexdigest())
+"""
+
+
+def test_cutcell_rows_over_group_lists_bit_identical():
+    """k_raw_cutcells_list (default: per-row group lists built once per plan)
+    against the element-window scan of k_raw_cutcells (TQ_CUTCELL_LISTS=0,
+    read once per process): the same additions in the same order, so the
+    CSR is bit-identical (config-5 recipe, three strategies)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, TQ_CUTCELL_LISTS=v)
+        r = subprocess.run([sys.executable, "-c", _CUTCELL_SNIPPET.format(root=root)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout)
+    assert outs[0] == outs[1] and len(outs[0].splitlines()) == 6
