@@ -324,6 +324,13 @@ int tq_row_counts(tq_rowctx c, int32_t* counts, void* stream);
  * at work + 2, list B (deep rows with a partial window) at work + 2 + nrows */
 int tq_row_counts_deep(tq_rowctx c, int32_t* counts, int32_t* work, void* stream);
 int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream);
+/* count pass 2 split: the listed rows' geometry records (one 32-byte record
+ * per list-A row, rec: (row_end - row_begin) * tq_list_record_bytes()),
+ * then the value-based counts from them (the same counts as
+ * tq_row_counts_rest) */
+int64_t tq_list_record_bytes(void);
+int tq_list_geometry(tq_rowctx c, const int32_t* work, void* rec, void* stream);
+int tq_row_counts_rest_rec(tq_rowctx c, int32_t* counts, const int32_t* work, const void* rec, void* stream);
 /* tq_row_counts_deep from the geometric flags of tq_deep_geometry and the
  * per-line factor positivity (computed here into `pos`, n1 + n2 bytes of
  * caller scratch); c.deep is not read.  The lists then carry the deep /

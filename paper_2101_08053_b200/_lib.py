@@ -156,6 +156,9 @@ def lib():
         "tq_row_counts_deep": ([RowCtx, vp, vp, vp], i32),
         "tq_row_counts_geo": ([RowCtx, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_rest": ([RowCtx, vp, vp, vp], i32),
+        "tq_list_record_bytes": ([], i64),
+        "tq_list_geometry": ([RowCtx, vp, vp, vp], i32),
+        "tq_row_counts_rest_rec": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_row_counts_spec": ([RowCtx, vp, vp, vp, vp], i32),
         "tq_row_counts_cached": ([RowCtx, vp, vp, vp, vp, vp, vp, vp, vp], i32),
         "tq_row_counts_verify": ([RowCtx, vp, vp, vp, vp, vp, vp], i32),

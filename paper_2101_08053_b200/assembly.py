@@ -477,11 +477,18 @@ class Formation:
                         flags=torch.zeros(3, dtype=torch.int32, device=self.dev))
             else:
                 L.call("tq_row_counts_deep", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            rec = None
             if self.a1 is not None and GEOMETRIC_NEAR:
                 # interior separable rows on positive lines are counted
                 # geometrically by pass 2 and verified by the fill (rowctx.fclass)
                 ctx.fclass, ctx.pos = L.ptr(self.config.func_class_dev), L.ptr(pos)
                 self._near_pos = pos
+                # the listed rows' geometry records, before the join (pass 2
+                # starts from them: one load per row)
+                rec = torch.empty(max(nrows, 1) * int(L.lib().tq_list_record_bytes()), dtype=torch.uint8,
+                                  device=self.dev)
+                L.call("tq_list_geometry", ctx, L.ptr(work), L.ptr(rec), L.stream())
+                self._list_rec = rec
             _stamp("counts_deep")
             head = None
             if self.capture is not None and HEAD_FILL:
@@ -506,7 +513,10 @@ class Formation:
             if join is not None:
                 torch.cuda.current_stream().wait_stream(join)
             _stamp("join")
-            L.call("tq_row_counts_rest", ctx, L.ptr(counts), L.ptr(work), L.stream())
+            if rec is not None:
+                L.call("tq_row_counts_rest_rec", ctx, L.ptr(counts), L.ptr(work), L.ptr(rec), L.stream())
+            else:
+                L.call("tq_row_counts_rest", ctx, L.ptr(counts), L.ptr(work), L.stream())
             _stamp("counts_rest")
         nnz = L.i64(0)
         if head is None:

@@ -263,8 +263,36 @@ __device__ __forceinline__ void entries_rows(const tq_rowctx& c, const RowGeom* 
 // (p > 4) go one at a time.
 constexpr int kRowsPass2 = 2;
 
+// Row geometry of the listed rows, one coalesced 32-byte record each
+// (k_list_geometry, launched right after count pass 1, off the critical
+// path): count pass 2 then starts from one load per row instead of the
+// list -> active -> slot / overlap chain.  near: near_row(), counted
+// geometrically.
+struct alignas(16) ListRec {
+    int r, i1, i2, s_i, j1lo, j2lo, t1, t2n;      // t2n = t2 | near << 16
+};
+
+__global__ void k_list_geometry(tq_rowctx c, const int* __restrict__ list, const int* __restrict__ nlist,
+                                ListRec* __restrict__ rec) {
+    const int n = *nlist;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const int r = list[u];
+        const RowGeom g = row_geom(c, r);
+        ListRec x;
+        x.r = r;
+        x.i1 = g.i1;
+        x.i2 = g.i2;
+        x.s_i = g.s_i;
+        x.j1lo = g.j1lo;
+        x.j2lo = g.j2lo;
+        x.t1 = g.t1;
+        x.t2n = g.t2 | (near_row(c, g) ? 1 << 16 : 0);
+        rec[u] = x;
+    }
+}
+
 __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, const int* __restrict__ list,
-                                  const int* __restrict__ nlist) {
+                                  const int* __restrict__ nlist, const ListRec* __restrict__ recs = nullptr) {
     constexpr int R = kRowsPass2;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -277,11 +305,26 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             ok[k] = q0 + k < n_rows;
-            r[k] = ok[k] ? list[q0 + k] : list[q0];
-            g[k] = row_geom(c, r[k]);
+            bool near;
+            if (recs) {           // the row's geometry in one record
+                const ListRec x = recs[ok[k] ? q0 + k : q0];
+                r[k] = x.r;
+                g[k].i1 = x.i1;
+                g[k].i2 = x.i2;
+                g[k].s_i = x.s_i;
+                g[k].j1lo = x.j1lo;
+                g[k].j2lo = x.j2lo;
+                g[k].t1 = x.t1;
+                g[k].t2 = x.t2n & 0xffff;
+                near = (x.t2n >> 16) != 0;
+            } else {
+                r[k] = ok[k] ? list[q0 + k] : list[q0];
+                g[k] = row_geom(c, r[k]);
+                near = near_row(c, g[k]);
+            }
             small = small && g[k].t1 * g[k].t2 <= 96;
             cnt[k] = 0;
-            if (ok[k] && near_row(c, g[k])) {      // counted geometrically, no entry loads
+            if (ok[k] && near) {      // counted geometrically, no entry loads
                 cnt[k] = g[k].t1 * g[k].t2;
                 ok[k] = false;
             }
@@ -879,6 +922,29 @@ extern "C" int tq_row_counts_cached(tq_rowctx c, const int8_t* geo, int8_t* pos,
 extern "C" int tq_row_counts_rest(tq_rowctx c, int32_t* counts, const int32_t* work, void* stream) {
     if (c.row_end <= c.row_begin) return TQ_OK;
     k_row_counts_list<<<kSms * 16, 256, 0, S(stream)>>>(c, counts, work + 2, work); ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_row_counts_list");
+    return TQ_OK;
+}
+
+extern "C" int64_t tq_list_record_bytes(void) { return (int64_t)sizeof(ListRec); }
+
+// the geometry records of list A (work: the count passes' lists; rec:
+// (row_end - row_begin) * tq_list_record_bytes() bytes)
+extern "C" int tq_list_geometry(tq_rowctx c, const int32_t* work, void* rec, void* stream) {
+    if (c.row_end <= c.row_begin) return TQ_OK;
+    k_list_geometry<<<kSms * 8, 256, 0, S(stream)>>>(c, work + 2, work, static_cast<ListRec*>(rec));
+    ::tq::note_launch();
+    TQ_LAUNCH_CHECK("k_list_geometry");
+    return TQ_OK;
+}
+
+// tq_row_counts_rest from the records of tq_list_geometry
+extern "C" int tq_row_counts_rest_rec(tq_rowctx c, int32_t* counts, const int32_t* work, const void* rec,
+                                      void* stream) {
+    if (c.row_end <= c.row_begin) return TQ_OK;
+    k_row_counts_list<<<kSms * 16, 256, 0, S(stream)>>>(c, counts, work + 2, work,
+                                                        static_cast<const ListRec*>(rec));
+    ::tq::note_launch();
     TQ_LAUNCH_CHECK("k_row_counts_list");
     return TQ_OK;
 }
