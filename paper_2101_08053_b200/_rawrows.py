@@ -619,8 +619,10 @@ def raw_row_groups(f):
         rg_ptr = torch.zeros(n + 1, dtype=torch.int32, device=f.dev)
         if n:
             rg_ptr[1:] = torch.cumsum(counts[:n], 0)
-        total = int(rg_ptr[-1].item())          # once per plan (the eager pass)
-        rg = torch.empty(max(3 * total, 3), dtype=torch.int32, device=f.dev)
+        # a (row, group) pair appears once and a group reaches the (p1+1)(p2+1)
+        # functions of its key: that bounds the total without a host read
+        cap = int(t["ngroups"]) * (f.b1.p + 1) * (f.b2.p + 1)
+        rg = torch.empty(max(3 * cap, 3), dtype=torch.int32, device=f.dev)
         L.call("tq_row_groups", f._ctx, 0, n, L.ptr(rg_ptr), L.ptr(rg), L.stream())
         g[key] = (rg_ptr, rg)
         g[key + ("keep",)] = (desc, t)
