@@ -381,6 +381,10 @@ __global__ void k_row_counts_list(tq_rowctx c, int32_t* __restrict__ counts, con
 //    trimming curve; row-parallel processing keeps them off the critical path).
 // ---------------------------------------------------------------------------
 constexpr int kWarpRows = 32;
+#ifndef TQ_FILL_SPLIT_TAIL
+#define TQ_FILL_SPLIT_TAIL 1
+#endif
+constexpr bool kFillSplitTail = TQ_FILL_SPLIT_TAIL != 0;   // the last wave of tiles in 16-row halves
 #ifndef TQ_FILL_STAGES
 #define TQ_FILL_STAGES 1     // one staging buffer per warp: more resident warps beat double buffering (measured)
 #endif
@@ -519,8 +523,16 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
     }
     const int ntp = part == 1 ? tA + (NT - tB) : part == 2 ? tB - tA : NT;   // tiles in this part
     int* ctr = tm ? c.tiles + TQ_TILE_CTL(nr) + (part == 1 ? 3 : 2) : nullptr;
-    auto tile_row = [&](int t) -> int {       // part-local tile -> first row (row_end: done)
-        if (t >= ntp) return c.row_end;
+    // work units: the part's tiles, the last `ks` of them split into two
+    // 16-row halves (dynamic claims only: the final wave of 26-us tiles
+    // would otherwise leave most warps idle at the end of the fill)
+    const int ks = ctr ? min(ntp, kFillSplitTail ? nwarps : 0) : 0;
+    const int nunits = ntp + ks;
+    auto unit_tile = [&](int u) -> int { return u < ntp - ks ? u : ntp - ks + ((u - (ntp - ks)) >> 1); };
+    auto unit_half = [&](int u) -> int { return u < ntp - ks ? -1 : ((u - (ntp - ks)) & 1); };
+    auto tile_row = [&](int u) -> int {       // unit -> first row of its tile (row_end: done)
+        if (u >= nunits) return c.row_end;
+        const int t = unit_tile(u);
         const int tile = part == 1 ? (t < tA ? t : tB + (t - tA)) : part == 2 ? tA + t : t;
         return c.row_begin + kWarpRows * tile;
     };
@@ -540,7 +552,10 @@ __global__ void __launch_bounds__(256) k_fill_tiles(tq_rowctx c, int32_t* __rest
     }
     if (tm && R0 < rhi) n_tb = __ldg(tbase + ((R0 - c.row_begin) >> 5));
     for (int R1; R0 < rhi; R0 = R1) {
-        const bool valid = R0 + lane < rhi;
+        // a half-tile unit processes its 16 lanes' rows (the offsets still
+        // come from the whole tile's counts)
+        const int half = unit_half(tcur);
+        const bool valid = R0 + lane < rhi && (half < 0 || (lane >> 4) == half);
         int my_pos = n_pos;
         const int my_idx = n_idx, my_fast = valid ? n_fast : 0;
         if (tm) {
