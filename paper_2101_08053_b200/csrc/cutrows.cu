@@ -42,6 +42,21 @@ __device__ __forceinline__ void pair_tables(int* pa, int* pb) {
         }
 }
 
+// FP64 tensor-core product of two fragments: C (8 x 8) += A (8 x 4) B (4 x 8)
+// with lane l holding A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) .. +1]
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+#ifndef TQ_CP_DMMA
+#define TQ_CP_DMMA 1
+#endif
+
+// pair-product operand stride: >= the padded width, = 4 (mod 16) doubles, so
+// a fragment load (4 rows x 8 columns) hits distinct banks per half-warp
+__host__ __device__ constexpr int cp_lda(int npad) { return npad + ((4 - npad % 16) + 16) % 16; }
+
 // ---------------------------------------------------------------------------
 // Element-Gauss blocks of the listed interior elements (q = ng = p + 1).
 // c at the element's Gauss grid: det J of the geometry map computed here
@@ -87,10 +102,15 @@ __global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawct
                                                             const double* __restrict__ lnd1,
                                                             const int32_t* __restrict__ lsp2,
                                                             const double* __restrict__ lnd2) {
-    constexpr int NP = Pairs<Q>::NP, TA = 3, TB = 6, NA = 16 * TA, NB = 8 * TB;    // 48 x 48 >= NP x NP
-    static_assert(NA >= NP && NB >= NP, "pair tile");
+    // E = PV1^T T on the FP64 tensor cores (mma.sync m8n8k4): NP x NP in
+    // 8 x 8 tiles (2 x 2 warps, TR x TR tiles each), K = Q Gauss points
+    // padded to a multiple of 4 with zero rows
+    constexpr int NP = Pairs<Q>::NP, NT8 = (NP + 7) / 8, NPAD = 8 * NT8, LDA = cp_lda(NPAD), TR = (NT8 + 1) / 2;
+    constexpr int KP = (Q + 3) & ~3;
+    constexpr int NA = NPAD, NB = NPAD;
     constexpr int PG = kMaxP + 1;
-    __shared__ double V1[Q][Q], V2[Q][Q], Wc[Q][Q + 1], PV1[Q][NA], T[Q][NB];
+    __shared__ double V1[Q][Q], V2[Q][Q], Wc[Q][Q + 1];
+    __shared__ __align__(16) double PV1[KP][LDA], T[KP][LDA];
     __shared__ double Na[Q][PG], Da[Q][PG], Nb[Q][PG], Db[Q][PG];
     __shared__ double XB[PG][Q], XDB[PG][Q], YB[PG][Q], YDB[PG][Q];
     __shared__ int sa[Q], sb[Q], pa[NP], pb[NP];
@@ -98,6 +118,10 @@ __global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawct
     __shared__ double kn_s[KN], XW[PG][PG], YW[PG][PG];
     pair_tables<Q>(pa, pb);
     const int tid = threadIdx.x;
+    for (int t = tid; t < (KP - Q) * LDA; t += blockDim.x) {      // the K padding rows stay zero
+        PV1[Q + t / LDA][t % LDA] = 0.0;
+        T[Q + t / LDA][t % LDA] = 0.0;
+    }
     const bool inline_c = geo.kind == TQ_COEFF_GEOMETRY;
     const int nk = geo.n + geo.p + 1;
     const double* knots = geo.knots;
@@ -220,32 +244,36 @@ __global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawct
         }
         __syncthreads();
         {
-            const int ta = tid / 8, tb = tid - (tid / 8) * 8;       // 16 x 8 threads
-            double acc[TA][TB];
+            const int lane = tid & 31, warp = tid >> 5, wr = warp >> 1, wc = warp & 1, fr = lane >> 2, fk = lane & 3;
+            double acc[TR][TR][2];
 #pragma unroll
-            for (int i = 0; i < TA; ++i)
+            for (int i = 0; i < TR; ++i)
 #pragma unroll
-                for (int j = 0; j < TB; ++j) acc[i][j] = 0.0;
+                for (int j = 0; j < TR; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
-            for (int g1 = 0; g1 < Q; ++g1) {
-                double x[TA], y[TB];
+            for (int k0 = 0; k0 < KP; k0 += 4) {
+                double af[TR], bf[TR];
 #pragma unroll
-                for (int i = 0; i < TA; ++i) x[i] = PV1[g1][ta * TA + i];
+                for (int i = 0; i < TR; ++i) {
+                    const int tr = wr * TR + i, tc = wc * TR + i;
+                    af[i] = tr < NT8 ? PV1[k0 + fk][tr * 8 + fr] : 0.0;
+                    bf[i] = tc < NT8 ? T[k0 + fk][tc * 8 + fr] : 0.0;
+                }
 #pragma unroll
-                for (int j = 0; j < TB; ++j) y[j] = T[g1][tb * TB + j];
+                for (int i = 0; i < TR; ++i)
 #pragma unroll
-                for (int i = 0; i < TA; ++i)
-#pragma unroll
-                    for (int j = 0; j < TB; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
+                    for (int j = 0; j < TR; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
             double* out = E + (int64_t)slot * NP * NP;
 #pragma unroll
-            for (int i = 0; i < TA; ++i)
+            for (int i = 0; i < TR; ++i)
 #pragma unroll
-                for (int j = 0; j < TB; ++j) {
-                    const int s1 = ta * TA + i, s2 = tb * TB + j;
-                    if (s1 < NP && s2 < NP) out[s1 * NP + s2] = acc[i][j];
-                }
+                for (int j = 0; j < TR; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int s1 = (wr * TR + i) * 8 + fr, s2 = (wc * TR + j) * 8 + 2 * fk + h;
+                        if (s1 < NP && s2 < NP) out[s1 * NP + s2] = acc[i][j][h];
+                    }
         }
     }
 }
@@ -261,21 +289,6 @@ __global__ void __launch_bounds__(kGpThreads, TQ_GP_MINB) k_gauss_pairs(tq_rawct
 // kCpPiece, the group's end).
 // ---------------------------------------------------------------------------
 constexpr int kCpThreads = 128, kCpChunk = 32, kCpPiece = 128;
-
-// FP64 tensor-core product of two fragments: C (8 x 8) += A (8 x 4) B (4 x 8)
-// with lane l holding A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) .. +1]
-__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
-}
-
-#ifndef TQ_CP_DMMA
-#define TQ_CP_DMMA 1
-#endif
-
-// pair-product operand stride: >= the padded width, = 4 (mod 16) doubles, so
-// a fragment load (4 rows x 8 columns) hits distinct banks per half-warp
-__host__ __device__ constexpr int cp_lda(int npad) { return npad + ((4 - npad % 16) + 16) % 16; }
 
 template <int Q>
 __global__ void __launch_bounds__(kCpThreads, TQ_CP_MINB) k_cut_pairs(tq_rawctx c, const int64_t* __restrict__ pieces,

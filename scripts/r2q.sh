@@ -1,4 +1,4 @@
-timeout 300 python scripts/probes/c5_hash.py 256
-for v in ns "" ns ""; do lib=paper_2101_08053_b200/libtq_b200${v:+_$v}.so
- TQ_LIB=$PWD/$lib timeout 600 python bench.py --no-config4 --e2e-steps 0 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v c5', d['ms_per_step'], d['kernels_ms_per_step']['fill'], d['parity']['pattern_sha256'])"; done
-for v in ns ""; do lib=paper_2101_08053_b200/libtq_b200${v:+_$v}.so; echo "== $v"; TQ_LIB=$PWD/$lib timeout 600 python scripts/probes/rank_probe.py 2>&1 | tail -4; done
+for p in 8 6 4; do timeout 300 python scripts/probes/c4_hash.py $p 64; done
+for i in 1 2; do timeout 300 python scripts/config4_probe.py 8 256 2>&1 | tail -1 | cut -c60-110; timeout 300 python scripts/config4_probe.py 6 256 2>&1 | tail -1 | cut -c60-110; done
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -k regex:"k_gauss_pairs" python scripts/config4_probe.py 8 256 prof 2>&1 | grep -E "duration"
+timeout 900 python -m pytest tests/test_gpu_planes.py tests/test_gpu_trimmed.py -q -x 2>&1 | tail -2
