@@ -104,6 +104,8 @@ int tq_graph_instantiate(void* graph, int32_t use_node_priority, void** exec);
 int tq_graph_launch(void* exec, void* stream);
 int tq_graph_exec_destroy(void* exec);
 int tq_graph_node_priorities(void* graph, int32_t* hist, int32_t* nkernels);
+/* graph nodes by cudaGraphNodeType (counts[0..11]) */
+int tq_graph_node_types(void* graph, int32_t* counts);
 const char* tq_last_error(void);
 int tq_device_sync(void* stream);
 /* kernels launched by the library since it was loaded (host counter) */

@@ -144,6 +144,7 @@ def lib():
         "tq_graph_launch": ([vp, vp], i32),
         "tq_graph_exec_destroy": ([vp], i32),
         "tq_graph_node_priorities": ([vp, C.POINTER(i32), C.POINTER(i32)], i32),
+        "tq_graph_node_types": ([vp, C.POINTER(i32)], i32),
         "tq_last_error": ([], C.c_char_p),
         "tq_device_sync": ([vp], i32),
         "tq_debug_stamp": ([vp, i32, vp], i32),

@@ -748,6 +748,15 @@ class GraphFormation:
         L.call("tq_graph_node_priorities", L.vp(_graph_handle(self.graph)), hist, L.C.byref(nk))
         return list(hist), int(nk.value)
 
+    def node_types(self):
+        """Graph nodes by type: kernel, memcpy, memset, host, graph, empty,
+        event wait, event record, ... (cudaGraphNodeType order)."""
+        counts = (L.i32 * 12)()
+        L.call("tq_graph_node_types", L.vp(_graph_handle(self.graph)), counts)
+        names = ["kernel", "memcpy", "memset", "host", "graph", "empty", "wait_event", "event_record",
+                 "ext_sem_signal", "ext_sem_wait", "mem_alloc", "mem_free"]
+        return {n: int(c) for n, c in zip(names, counts) if c}
+
     def run(self):
         if self._exec is not None:
             L.call("tq_graph_launch", self._exec, L.stream())

@@ -117,3 +117,18 @@ extern "C" int tq_graph_node_priorities(void* graph, int32_t* hist, int32_t* nke
     *nkernels = nk;
     return TQ_OK;
 }
+
+// graph node census by type (cudaGraphNodeType values 0..11 -> counts[0..11])
+extern "C" int tq_graph_node_types(void* graph, int32_t* counts) {
+    size_t n = 0;
+    TQ_CUDA(cudaGraphGetNodes(static_cast<cudaGraph_t>(graph), nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    TQ_CUDA(cudaGraphGetNodes(static_cast<cudaGraph_t>(graph), nodes.data(), &n));
+    for (int k = 0; k < 12; ++k) counts[k] = 0;
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType t;
+        TQ_CUDA(cudaGraphNodeGetType(nodes[i], &t));
+        if ((int)t >= 0 && (int)t < 12) counts[(int)t] += 1;
+    }
+    return TQ_OK;
+}

@@ -10,3 +10,8 @@ c4 = C.baseline_config(4, p=6, nel=64)
 b2d, cfg = C.build_space(None, 64, 6, curves=c4["curves"])
 gf = A.GraphFormation(b2d, cfg, c4["coeff"], "dwq")
 print("config4 p6 64^2", gf.node_priorities())
+print("config4 node types", gf.node_types())
+c5 = C.baseline_config(5, nel=2048)
+b2d, cfg = C.build_space(None, 2048, 4, curves=c5["curves"])
+gf = A.GraphFormation(b2d, cfg, None, "dwq")
+print("config5 2048^2 node types", gf.node_types(), gf.node_priorities())
