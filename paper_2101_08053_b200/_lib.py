@@ -317,6 +317,21 @@ class _StagingRing:
         self.head = lo + n
         return self.buf[lo: lo + a.nbytes]
 
+    def reserve(self, n):
+        """Offset of n free bytes (256-aligned) in the ring, or None."""
+        n = (n + 255) & ~255
+        if n > self.SIZE // 4:
+            return None
+        if self.head + n > self.SIZE:
+            while self.pending:
+                self.pending.popleft().synchronize()
+            self.head = 0
+        while self.pending and self.pending[0].query():
+            self.pending.popleft()
+        lo = self.head
+        self.head = lo + n
+        return lo
+
     def done(self, view):
         ev = torch.cuda.Event()
         ev.record()
@@ -356,6 +371,47 @@ def dev(x, dtype):
         _pinned_keep.append(src)
     out = src.to(device=device(), non_blocking=True)
     return out if out.dtype == dtype else out.to(dtype)
+
+
+_DEV_MANY = os.environ.get("TQ_DEV_MANY", "1") == "1"      # A/B knob
+
+
+def dev_many(items):
+    """Upload several small host arrays with ONE copy: ``items`` is a list of
+    (array, torch dtype); returns the device tensors (views of one device
+    block, each 256-byte aligned) in order.  Same stream semantics as
+    ``dev``; falls back to one upload per array under stream capture or when
+    the batch does not fit a ring slot."""
+    arrs = [np.ascontiguousarray(x, dtype=_NP_DTYPE.get(dt)) for x, dt in items]
+    offs, total = [], 0
+    for a in arrs:
+        offs.append(total)
+        total += (a.nbytes + 255) & ~255
+    ok = (_DEV_MANY and total > 0 and not _PAGEABLE_UPLOADS and all(dt in _NP_DTYPE for _, dt in items)
+          and not torch.cuda.is_current_stream_capturing())
+    lo = None
+    if ok:
+        d = device()
+        ring = _RINGS.get(d.index)
+        if ring is None:
+            ring = _RINGS[d.index] = _StagingRing()
+        lo = ring.reserve(total)
+    if lo is None:
+        return [dev(a, dt) for a, (_, dt) in zip(arrs, items)]
+    host = ring.host
+    for a, o in zip(arrs, offs):
+        if a.nbytes:
+            host[lo + o: lo + o + a.nbytes] = a.reshape(-1).view(np.uint8)
+    block = torch.empty(total, dtype=torch.uint8, device=d)
+    block.copy_(ring.buf[lo: lo + total], non_blocking=True)
+    ring.done(None)
+    out = []
+    for a, o, (_, dt) in zip(arrs, offs, items):
+        if a.size == 0:
+            out.append(torch.empty(a.shape, dtype=dt, device=d))
+        else:
+            out.append(block[o: o + a.nbytes].view(dt).view(a.shape))
+    return out
 
 
 def dev_bytes(buf):

@@ -102,8 +102,7 @@ class PointLayout:
 
     def device(self):
         if self._dev is None:
-            pts = L.dev(self.points, torch.float64)
-            off = L.dev(self.offsets, torch.int32)
+            pts, off = L.dev_many([(self.points, torch.float64), (self.offsets, torch.int32)])
             self._dev = (L.Layout(L.ptr(pts), L.ptr(off), self.num_points, self.num_elements), pts, off)
         return self._dev[0]
 
@@ -277,8 +276,7 @@ class _FitPlan:
         t = basis._ov_hi - basis._ov_lo + 1
         self.tmax = int(t[self.rows_h].max()) if self.rows_h.size else 1
         self.mmax = int(lens[self.rows_h].max()) if self.rows_h.size else 1
-        self.wptr = L.dev(self.wptr_h, torch.int64)
-        self.rows = L.dev(self.rows_h, torch.int32)
+        self.wptr, self.rows = L.dev_many([(self.wptr_h, torch.int64), (self.rows_h, torch.int32)])
 
 
 def _solve_rows_async_t(plan: _FitPlan, init=None, products=None):
@@ -500,11 +498,9 @@ class DwqPlan:
         lens = np.where(sel, lens, 0)
         self.wptr_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
         k0_h = np.where(sel, aug.offsets[basis._el_first], -1).astype(np.int32)
-        self.wptr, self.k0 = L.dev(self.wptr_h, torch.int64), L.dev(k0_h, torch.int32)
-        self.cp = L.dev(self.Sc.indptr.astype(np.int32), torch.int32)
-        self.ri = L.dev(self.Sc.indices.astype(np.int32), torch.int32)
-        self.sv = L.dev(self.Sc.data, torch.float64)
-        self.rows = L.dev(self.wanted.astype(np.int32), torch.int32)
+        self.wptr, self.k0, self.cp, self.ri, self.sv, self.rows = L.dev_many([
+            (self.wptr_h, torch.int64), (k0_h, torch.int32), (self.Sc.indptr, torch.int32),
+            (self.Sc.indices, torch.int32), (self.Sc.data, torch.float64), (self.wanted, torch.int32)])
 
     def bump(self, failing):
         """Enrichment retry of the refined fit (src/quadrature.py:420-432)."""

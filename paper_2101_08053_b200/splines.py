@@ -154,15 +154,11 @@ class Basis1D:
     def device(self):
         """tq_space1d view with device arrays (cached)."""
         if self._dev is None:
-            keep = {
-                "knots": L.dev(self.kv.knots, torch.float64),
-                "bp": L.dev(self.breakpoints, torch.float64),
-                "espan": L.dev(self.kv.element_spans, torch.int32),
-                "el_first": L.dev(self._el_first, torch.int32),
-                "el_last": L.dev(self._el_last, torch.int32),
-                "ov_lo": L.dev(self._ov_lo, torch.int32),
-                "ov_hi": L.dev(self._ov_hi, torch.int32),
-            }
+            names = ("knots", "bp", "espan", "el_first", "el_last", "ov_lo", "ov_hi")
+            f64, i32 = torch.float64, torch.int32
+            keep = dict(zip(names, L.dev_many([      # one upload for the seven tables
+                (self.kv.knots, f64), (self.breakpoints, f64), (self.kv.element_spans, i32),
+                (self._el_first, i32), (self._el_last, i32), (self._ov_lo, i32), (self._ov_hi, i32)])))
             st = L.Space1D(*(L.ptr(keep[k]) for k in ("knots", "bp", "espan", "el_first", "el_last",
                                                      "ov_lo", "ov_hi")),
                            self.kv.knots.size, self.p, self.n, self.num_elements)
