@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(32 * ((TS * 9 + 31) / 32) + 32) k_sf_strips(
 // ctl: [0] tile ticket, [1] nnz, [2] flags (1 = nnz differs from `expect`,
 // 2 = capacity exceeded; nothing past `cap` is written).
 // ---------------------------------------------------------------------------
-constexpr int kPlTile = 16, kPlThreads = 256;
+constexpr int kPlThreadsPerRow = 16;      // block = 16 threads per tile row (256 at 16 rows, 128 at 8)
 
 // the look-back words carry flag and value in one 64-bit word, so relaxed
 // single-copy-atomic accesses suffice (no other data is published with them;
@@ -383,12 +383,12 @@ __device__ __forceinline__ unsigned long long lb_pack(unsigned flag, unsigned v)
 
 __device__ __forceinline__ int pl_row_of(const tq_rowctx& c, int idx) { return idx / c.n2; }
 
-template <int P>
-__global__ void __launch_bounds__(kPlThreads, 4) k_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* __restrict__ indptr,
+template <int P, int kPlTile>
+__global__ void __launch_bounds__(kPlThreadsPerRow * kPlTile, 64 / kPlTile) k_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* __restrict__ indptr,
                                                             int32_t* __restrict__ indices, double* __restrict__ data,
                                                             int64_t cap, unsigned long long* __restrict__ state,
                                                             int32_t* __restrict__ ctl, int64_t expect) {
-    constexpr int W = 2 * P + 1, T = W * W, NW = kPlThreads / 32;
+    constexpr int W = 2 * P + 1, T = W * W, kPlThreads = kPlThreadsPerRow * kPlTile, NW = kPlThreads / 32;
     extern __shared__ double sm[];
     double* sv = sm;                                            // [kPlTile][T]
     int* sc = reinterpret_cast<int*>(sv + kPlTile * T);        // [kPlTile][T]
@@ -422,8 +422,9 @@ __global__ void __launch_bounds__(kPlThreads, 4) k_planes_csr(tq_rowctx c, int32
             // entries o = hw, hw + 16, .. of the row (hw = the half-warp's
             // index): every half-warp gets ceil(T / 16) entries, loaded in
             // chunks of CH (column loads, then the partners' values)
-            constexpr int NH = 2 * NW, PER = (T + NH - 1) / NH, CH = 8;
-            const int hw = 2 * warp + half;
+            constexpr int SUB = 32 / kPlTile, NH = SUB * NW, PER = (T + NH - 1) / NH;
+            constexpr int NCH = (PER + 7) / 8, CH = (PER + NCH - 1) / NCH;
+            const int hw = SUB * warp + half;
             // window-offset bounds of this row (j in the overlap range)
             const int o1lo = jl1 - i1 + P, o1hi = jh1 - i1 + P, o2lo = jl2 - i2 + P, o2hi = jh2 - i2 + P;
             const int* colbase = c.col_of + ((int64_t)(i1 - P) * c.n2 + (i2 - P));
@@ -615,15 +616,16 @@ extern "C" int tq_sf_strips(tq_rawctx c, int32_t rows, const int32_t* strips, in
 }
 
 extern "C" int64_t tq_planes_state_bytes(int32_t nrows) {
-    return (int64_t)sizeof(unsigned long long) * ((nrows + kPlTile - 1) / kPlTile + 1);
+    return (int64_t)sizeof(unsigned long long) * ((nrows + 7) / 8 + 1);      // the smallest tile (8 rows)
 }
 
-template <int P>
+template <int P, int kPlTile>
 static int planes_csr_launch(const tq_rowctx& c, int32_t raw_base, int32_t* indptr, int32_t* indices, double* data,
                              int64_t cap, void* state, int32_t* ctl, int64_t expect, cudaStream_t st) {
     constexpr int T = (2 * P + 1) * (2 * P + 1);
     const size_t shm = (size_t)kPlTile * T * (sizeof(double) + sizeof(int));
-    auto kern = k_planes_csr<P>;
+    constexpr int kPlThreads = kPlThreadsPerRow * kPlTile;
+    auto kern = k_planes_csr<P, kPlTile>;
     static int per_sm_cache[kMaxP + 1][16] = {};
     int dev = 0;
     TQ_CUDA(cudaGetDevice(&dev));
@@ -662,8 +664,11 @@ extern "C" int tq_planes_csr(tq_rowctx c, int32_t raw_base, int32_t* indptr, int
     }
     if (!c.raw_ld || c.p1 != c.p2) { set_error("tq_planes_csr needs the planes layout and p1 == p2"); return TQ_EINVAL; }
     int rc = TQ_EINVAL;
+    // rows per tile: 16 (default) or 8 (TQ_PL_TILE=8: half the stage, twice the resident blocks)
+    static const bool tile8 = [] { const char* e = getenv("TQ_PL_TILE"); return e && atoi(e) == 8; }();
     switch (c.p1) {
-#define CASE(Q) case Q: rc = planes_csr_launch<Q>(c, raw_base, indptr, indices, data, cap, state, ctl, expect, st); break;
+#define CASE(Q) case Q: rc = tile8 ? planes_csr_launch<Q, 8>(c, raw_base, indptr, indices, data, cap, state, ctl, expect, st) \
+                           : planes_csr_launch<Q, 16>(c, raw_base, indptr, indices, data, cap, state, ctl, expect, st); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
         default: set_error("degree out of range"); return TQ_EINVAL;
