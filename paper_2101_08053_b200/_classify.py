@@ -152,6 +152,81 @@ _CUT_ERRORS = {1: "cannot decompose cell at maximum split depth 4", 2: "folded s
 SLOT_CELLS = 4
 
 
+class _DeviceRulePending:
+    """A device cut-cell decomposition in flight (start_cut_cell_rule_device):
+    the slots kernel is queued and its summary is on its way to pinned host
+    memory; ``result()`` waits for that copy and packs the rule."""
+
+    def __init__(self, config, q, slot_cells=None):
+        if q < 1:
+            raise ValueError("Lagrange degree q must be >= 1")
+        b1, b2 = config.basis2d.dir
+        ec = config.element_class_dev.reshape(b1.num_elements, b2.num_elements)
+        el = torch.nonzero(ec == 1).to(torch.int32).contiguous()
+        ncut = el.shape[0]
+        dev = el.device
+        arr, keep = curve_array(config.curves)
+        tabs = cell_tables(q)
+        bp1, bp2 = b1.device_arrays()["bp"], b2.device_arrays()["bp"]
+        cap = (SLOT_CELLS if slot_cells is None else slot_cells) * (q + 1) ** 2
+        ptr = torch.zeros(ncut + 1, dtype=torch.int64, device=dev)
+        ncells = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
+        status = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
+        sP = torch.empty(max(ncut, 1) * cap * 2, dtype=torch.float64, device=dev)
+        sW = torch.empty(max(ncut, 1) * cap, dtype=torch.float64, device=dev)
+        common = (arr, len(config.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q, tabs.ctypes.data_as(L.vp), cap)
+        L.call("tq_cutcell_device_slots", *common, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(ncells), L.ptr(status),
+               L.stream())
+        self.summary = self.event = None
+        if ncut:
+            cnt = ptr[1:]
+            summary = torch.stack([status[:ncut].max().to(torch.int64), cnt.max(), cnt.sum()])
+            self.summary = torch.empty(3, dtype=torch.int64, pin_memory=True)
+            self.summary.copy_(summary, non_blocking=True)
+            self.event = torch.cuda.Event()
+            self.event.record()
+        self.el_host = torch.empty(el.shape, dtype=torch.int32, pin_memory=True)
+        self.el_host.copy_(el, non_blocking=True)
+        self.el_event = torch.cuda.Event()
+        self.el_event.record()
+        self.s = dict(q=q, el=el, ncut=ncut, common=common, keep=(keep, tabs, bp1, bp2), cap=cap, ptr=ptr,
+                      ncells=ncells, status=status, sP=sP, sW=sW)
+
+    def result(self):
+        s = self.s
+        q, el, ncut, cap, ptr, status = s["q"], s["el"], s["ncut"], s["cap"], s["ptr"], s["status"]
+        over = 0
+        if ncut:
+            self.event.synchronize()
+            summary = self.summary.tolist()
+            if summary[0]:
+                bad = torch.nonzero(status[:ncut]).flatten()
+                z = int(bad[0])
+                e1, e2 = (int(v) for v in el[z].tolist())
+                raise TrimmingConfigurationError(f"element ({e1}, {e2}): {_CUT_ERRORS.get(int(status[z]), 'error')}")
+            over = int(summary[1] > cap)
+            ptr[1:] = torch.cumsum(ptr[1:], 0)
+            npts = int(summary[2])
+        else:
+            npts = 0
+        dev = el.device
+        P = torch.empty((max(npts, 1), 2), dtype=torch.float64, device=dev)
+        W = torch.empty(max(npts, 1), dtype=torch.float64, device=dev)
+        L.call("tq_cutcell_device_pack", *s["common"], L.ptr(s["sP"]), L.ptr(s["sW"]), L.ptr(ptr), L.ptr(P), L.ptr(W),
+               over, L.stream())
+        self.el_event.synchronize()
+        elements = self.el_host.numpy().astype(np.int64).reshape(-1, 2)
+        return CutCellRule(q, elements, None, None, None, None,
+                           dev=dict(P=P[:npts], W=W[:npts], ptr=ptr, el=el, ncells=s["ncells"][:ncut], npts=npts))
+
+
+def start_cut_cell_rule_device(config, q, slot_cells=None):
+    """Queue the device decomposition and return at once; ``.result()``
+    joins (called by TrimConfiguration.cut_cell_rule).  The kernel and its
+    read-back then overlap the host's plan building of the formation."""
+    return _DeviceRulePending(config, q, slot_cells)
+
+
 def cut_cell_rule_device(config, q, slot_cells=None):
     """Cut-element quadrature decomposed on the GPU (one thread per cut
     element; same decomposition as the host C++): one decomposition into
@@ -159,46 +234,7 @@ def cut_cell_rule_device(config, q, slot_cells=None):
     status and point count, then the slots are packed to their offsets
     (tq_cutcell_device_pack; overflowing elements are decomposed again).
     The rule's device arrays are kept on it (``rule.dev``)."""
-    if q < 1:
-        raise ValueError("Lagrange degree q must be >= 1")
-    b1, b2 = config.basis2d.dir
-    ec = config.element_class_dev.reshape(b1.num_elements, b2.num_elements)
-    el = torch.nonzero(ec == 1).to(torch.int32).contiguous()
-    ncut = el.shape[0]
-    dev = el.device
-    arr, keep = curve_array(config.curves)
-    tabs = cell_tables(q)
-    bp1, bp2 = b1.device_arrays()["bp"], b2.device_arrays()["bp"]
-    cap = (SLOT_CELLS if slot_cells is None else slot_cells) * (q + 1) ** 2
-    ptr = torch.zeros(ncut + 1, dtype=torch.int64, device=dev)
-    ncells = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
-    status = torch.zeros(max(ncut, 1), dtype=torch.int32, device=dev)
-    sP = torch.empty(max(ncut, 1) * cap * 2, dtype=torch.float64, device=dev)
-    sW = torch.empty(max(ncut, 1) * cap, dtype=torch.float64, device=dev)
-    common = (arr, len(config.curves), L.ptr(bp1), L.ptr(bp2), L.ptr(el), ncut, q, tabs.ctypes.data_as(L.vp), cap)
-    L.call("tq_cutcell_device_slots", *common, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(ncells), L.ptr(status),
-           L.stream())
-    over = 0
-    if ncut:
-        cnt = ptr[1:]
-        summary = torch.stack([status[:ncut].max().to(torch.int64), cnt.max(), cnt.sum()]).cpu().tolist()
-        if summary[0]:
-            bad = torch.nonzero(status[:ncut]).flatten()
-            z = int(bad[0])
-            e1, e2 = (int(v) for v in el[z].tolist())
-            raise TrimmingConfigurationError(f"element ({e1}, {e2}): {_CUT_ERRORS.get(int(status[z]), 'error')}")
-        over = int(summary[1] > cap)
-        ptr[1:] = torch.cumsum(cnt, 0)
-        npts = int(summary[2])
-    else:
-        npts = 0
-    P = torch.empty((max(npts, 1), 2), dtype=torch.float64, device=dev)
-    W = torch.empty(max(npts, 1), dtype=torch.float64, device=dev)
-    L.call("tq_cutcell_device_pack", *common, L.ptr(sP), L.ptr(sW), L.ptr(ptr), L.ptr(P), L.ptr(W), over,
-           L.stream())
-    elements = el.long().cpu().numpy().reshape(-1, 2)
-    return CutCellRule(q, elements, None, None, None, None,
-                       dev=dict(P=P[:npts], W=W[:npts], ptr=ptr, el=el, ncells=ncells[:ncut], npts=npts))
+    return _DeviceRulePending(config, q, slot_cells).result()
 
 
 def cut_cell_rule(config, q, host_only=False):

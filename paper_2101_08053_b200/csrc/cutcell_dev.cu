@@ -506,8 +506,9 @@ using namespace tq;
 namespace {
 
 // one upload of curve tables, curve structs and cell tables; runs `launch`
-// with them, frees the upload and synchronises the stream (the host
-// staging buffer must outlive the copy)
+// with them and frees the upload in stream order.  No stream sync: the
+// staging buffer is pageable, and cudaMemcpyAsync from pageable memory
+// returns once the source has been staged, so `host` may die on return
 template <class F>
 int with_uploaded(const tq_curve* curves_h, int32_t ncurves, int32_t q, const double* tabs_h, cudaStream_t st,
                   F&& launch) {
@@ -538,7 +539,6 @@ int with_uploaded(const tq_curve* curves_h, int32_t ncurves, int32_t q, const do
     launch(dcv, T);
     TQ_LAUNCH_CHECK("k_cutcells");
     TQ_CUDA(cudaFreeAsync(dev, st));
-    TQ_CUDA(cudaStreamSynchronize(st));
     return TQ_OK;
 }
 

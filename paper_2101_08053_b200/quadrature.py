@@ -15,6 +15,8 @@ from functools import lru_cache
 
 import ctypes as C
 
+import bisect
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -434,11 +436,17 @@ def _augment_nested(layout: PointLayout, extra) -> PointLayout:
     prev = 0
     for e in touched:
         pieces.append(pts[off[prev]: off[e]])
-        g = np.sort(pts[off[e]: off[e + 1]])
+        # a handful of points per element: plain floats (the same IEEE
+        # arithmetic as _split_largest_gap, first largest gap, sorted insert)
+        g = sorted(pts[off[e]: off[e + 1]].tolist())
+        a, b = float(bp[e]), float(bp[e + 1])
         for _ in range(int(extra[e])):
-            g = np.sort(np.append(g, _split_largest_gap(g, bp[e], bp[e + 1])))
-        pieces.append(g)
-        counts[e] = g.size
+            fence = [a, *g, b]
+            gaps = [fence[k + 1] - fence[k] for k in range(len(fence) - 1)]
+            k = gaps.index(max(gaps))
+            bisect.insort(g, 0.5 * (fence[k] + fence[k + 1]))
+        pieces.append(np.asarray(g, dtype=float))
+        counts[e] = len(g)
         prev = e + 1
     pieces.append(pts[off[prev]:])
     new_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)

@@ -358,40 +358,35 @@ def _repeated_insertion(kn, p, u, r):
     n = kn.size - p - 1
     if r <= 0:
         return kn.copy(), sp.identity(n, format="csr")
-    l0 = int(np.clip(np.searchsorted(kn, u, side="right") - 1, p, n - 1))
+    at = int(np.searchsorted(kn, u, side="right"))       # every copy of u goes in here
+    l0 = min(max(at - 1, p), n - 1)
     lo = max(l0 - p, 0)
     w = l0 - lo + 1
     B = np.eye(w)                        # rows = coefficients lo .., cols = source lo .. l0
-    for _ in range(r):
+    zrow = np.zeros((1, w))
+    for s in range(r):
         nc = kn.size - p - 1
-        l = int(np.clip(np.searchsorted(kn, u, side="right") - 1, p, nc - 1))
+        l = min(max(at + s - 1, p), nc - 1)
         nb = B.shape[0]
-        new = np.zeros((nb + 1, w))
-        for k in range(nb + 1):
-            g = lo + k                   # global coefficient index after the insertion
-            if g <= l - p:
-                new[k] = B[k]
-            elif g >= l + 1:
-                new[k] = B[k - 1]
-            else:
-                a = (u - kn[g]) / (kn[g + p] - kn[g])
-                new[k] = a * B[k] + (1.0 - a) * B[k - 1]
+        g = lo + np.arange(nb + 1)       # global coefficient index after the insertion
+        mid = (g > l - p) & (g < l + 1)
+        gm = g[mid]
+        a = np.where(g <= l - p, 1.0, 0.0)
+        a[mid] = (u - kn[gm]) / (kn[gm + p] - kn[gm])
+        # rows above the span copy B[k] (a = 1), rows below copy B[k - 1]
+        # (a = 0): 1 * x + 0 * y is exact, so this is the scalar recurrence
+        new = a[:, None] * np.concatenate([B, zrow]) + (1.0 - a)[:, None] * np.concatenate([zrow, B])
         B = new
-        kn = np.insert(kn, int(np.searchsorted(kn, u, side="right")), u)
+        kn = np.concatenate([kn[: at + s], [u], kn[at + s:]])
     nb = B.shape[0]
-    rows = [np.arange(lo)]
-    cols = [np.arange(lo)]
-    vals = [np.ones(lo)]
-    bi, bj = np.nonzero(B)
-    rows.append(lo + bi)
-    cols.append(lo + bj)
-    vals.append(B[bi, bj])
+    bi, bj = np.nonzero(B)               # row-major: sorted by row, then column
     tail = np.arange(lo + nb, n + r)
-    rows.append(tail)
-    cols.append(tail - r)
-    vals.append(np.ones(tail.size))
-    S = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n + r, n))
-    S.sort_indices()
+    counts = np.concatenate([np.ones(lo, np.int64), np.bincount(bi, minlength=nb), np.ones(tail.size, np.int64)])
+    indptr = np.concatenate([[0], np.cumsum(counts)])
+    indices = np.concatenate([np.arange(lo), lo + bj, tail - r])
+    vals = np.concatenate([np.ones(lo), B[bi, bj], np.ones(tail.size)])
+    S = sp.csr_matrix((vals, indices.astype(np.int32), indptr.astype(np.int32)), shape=(n + r, n))
+    S.has_sorted_indices = True
     return kn, S
 
 

@@ -193,7 +193,13 @@ class TrimConfiguration:
         if getattr(self, "_cut_rule_source", None) is not None:
             return
         if self.element_class_dev is not None and self.element_class_dev.is_cuda:
-            return          # decomposed on the device on first use (tq_cutcell_device)
+            # decomposed on the device: queued now (outside stream capture),
+            # joined on first use, so the kernel and the read-back of its
+            # summary overlap the caller's host work
+            if not torch.cuda.is_current_stream_capturing():
+                from . import _classify
+                self._cut_pending[q] = _classify.start_cut_cell_rule_device(self, q)
+            return
         from . import _classify
         self._cut_pending[q] = _classify.submit(_classify.cut_cell_rule, self, q, True)
 
