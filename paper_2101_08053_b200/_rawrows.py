@@ -16,6 +16,8 @@ import contextlib
 import os
 import ctypes as C
 
+import weakref
+
 import numpy as np
 import torch
 
@@ -700,7 +702,9 @@ class _Setup:
         b1, b2 = f.b1, f.b2
         cfg = f.config
         dev = f.dev
-        self.f = f
+        # (a proxy: the formation owns this object, and a strong reference
+        # back would leave the pass's device tables to the cyclic collector)
+        self.f = weakref.proxy(f)
         # element Gauss tables, (p+1) points (src/assembly.py:198-211);
         # basis values evaluated per formation as in the reference's _Run
         pre = getattr(f, "_elem_pre", None)
