@@ -629,8 +629,17 @@ def form(basis2d, config, coeff=None, strategy="reference", rules=None, row_rang
     f = Formation(basis2d, config, coeff, strategy, timer, capture)
     f.row_range = row_range        # a row block forms only the raw rows its rows read
     rep = f.report
-    if config.has_cuts():     # shared geometry (src/assembly.py:505-508): built on a worker
-        config.cut_cell_rule_async(max(basis2d.degrees))   # thread while the fits run
+    if config.has_cuts():     # shared geometry (src/assembly.py:505-508)
+        if capture is None:
+            # the cut-row list and the DWQ routing read two small results
+            # back: before the cut-cell kernel is queued, not behind it
+            from ._rawrows import cut_rows_host, dwq_keys
+            cut_rows_host(f)
+            if strategy == "dwq":
+                dwq_keys(f)
+        # queued now (device) or built on a worker thread (host), joined on
+        # first use: it runs while the host builds the plans and the fits run
+        config.cut_cell_rule_async(max(basis2d.degrees))
     clk = _Clock(active=capture is None and timed)
     _stamp("start")
     if capture is not None:
