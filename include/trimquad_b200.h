@@ -574,7 +574,9 @@ void tq_cutcell_free(void* handle);
  * caller turns ptr into offsets (inclusive scan of ptr[1..]) and calls again
  * with pts (2 per point) and w to write.  bp1/bp2 breakpoints, cut_el
  * (ncut x 2 int32, row-major element order) and the outputs are device
- * arrays; curves and tabs (as for tq_cutcell_build) are host arrays. */
+ * arrays; curves and tabs (as for tq_cutcell_build) are host arrays (staged
+ * before the call returns).  The three device entry points are asynchronous
+ * on `stream`: the outputs are valid in stream order, not on return. */
 int tq_cutcell_device(const tq_curve* curves_h, int32_t ncurves, const double* bp1, const double* bp2,
                       const int32_t* cut_el, int32_t ncut, int32_t q, const double* tabs_h, int64_t* ptr,
                       double* pts, double* w, int32_t* ncells, int32_t* status, void* stream);
